@@ -91,6 +91,7 @@ typedef struct orc_ctx {
     uint64_t *twist[ORC_MAXMOD];   /* psi^t, t < N */
     uint64_t *itwist[ORC_MAXMOD];  /* psi^-t, t < N */
     long double *cosl_tab;      /* cos(pi e / N), e < 2N  (encode/decode, A7) */
+    __float128 *cosq_tab;       /* same in binary128, built on first near-tie (A7) */
     int nthreads;
 } orc_ctx;
 
@@ -128,6 +129,7 @@ void orc_destroy(orc_ctx *c) {
     if (!c) return;
     for (int i = 0; i <= c->L; i++) { free(c->twist[i]); free(c->itwist[i]); }
     free(c->cosl_tab);
+    free(c->cosq_tab);
     free(c);
 }
 
@@ -460,29 +462,39 @@ static __float128 enc_value_q(const orc_ctx *c, const double *z, uint64_t n, dou
     __float128 acc = 0;
     for (uint64_t j = 0; j < n; j++) {
         uint64_t e = (uint64_t)(((u128)pow5[j] * t) % twoN);
-        acc += 2 * (__float128)z[j] * cosq(M_PIq * (__float128)e / (__float128)c->N);
+        acc += 2 * (__float128)z[j] * c->cosq_tab[e];
     }
     return acc * (__float128)scale / (__float128)c->N;
 }
 
 /*
  * Exact-rounded encoding coefficients (A7): m_t = round-half-away(v_t).  Long-double direct
- * sum; coefficients whose fractional part is within 2^-20 of 1/2 are recomputed in
- * __float128.  Returns 0, or -1 if some |m_t| >= 2^62.
+ * sum (absolute error << 2^-12 for |v| < 2^62); coefficients whose fractional part is within
+ * 2^-12 of 1/2 are recomputed by direct summation in __float128 (error ~2^-60).
+ * Returns 0, or -1 if some |m_t| >= 2^62.
  */
+#define ORC_TIE_WINDOW 0x1p-12L
+static void ensure_cosq(orc_ctx *c) {
+    if (c->cosq_tab) return;
+    uint64_t twoN = 2 * c->N;
+    __float128 *tab = (__float128 *)malloc(sizeof(__float128) * twoN);
+    for (uint64_t e = 0; e < twoN; e++) tab[e] = cosq(M_PIq * (__float128)e / (__float128)c->N);
+    c->cosq_tab = tab;
+}
 int orc_encode_coeffs(const orc_ctx *c, const double *z, uint64_t n, double scale, int64_t *m) {
     uint64_t N = c->N, twoN = 2 * N;
     uint64_t *pow5 = (uint64_t *)malloc((n ? n : 1) * 8);
     uint64_t p = 1;
     for (uint64_t j = 0; j < n; j++) { pow5[j] = p; p = (p * 5) % twoN; }
     int bad = 0;
+    ensure_cosq(c);
 #pragma omp parallel for num_threads(c->nthreads) reduction(| : bad)
     for (uint64_t t = 0; t < N; t++) {
         long double v = enc_value_ld(c, z, n, scale, t, pow5);
         long double av = fabsl(v);
         long double fr = av - floorl(av);
         long double r;
-        if (fabsl(fr - 0.5L) < 0x1p-20L) {
+        if (fabsl(fr - 0.5L) < ORC_TIE_WINDOW) {
             __float128 vq = enc_value_q(c, z, n, scale, t, pow5);
             __float128 aq = fabsq(vq);
             __float128 rq = floorq(aq + 0.5Q);
