@@ -1,0 +1,166 @@
+// elem_kernels.cu -- HBM-bound elementwise HISA ops (a3 add/sub/addPlain/addScalar/mulScalar/
+// mulPlain, a4 tensor / mulNoRelin, decrypt) and the NTT-domain automorphism (K6, a7).
+// 16-byte vector loads/stores, one pair of words per thread, grid = (pairs, ciphertexts).
+#include <cuda_runtime.h>
+#include "launch.h"
+
+namespace hisa {
+
+template <int OP>
+__global__ void __launch_bounds__(256) k_elem(ElemJob job, const Mod* __restrict__ mods) {
+    const int z = blockIdx.y;
+    const long long n2 = 1ll << (job.log_n - 1);               // word pairs per limb
+    const long long per_poly = (long long)job.nl * n2;
+    const int np_out = (OP == EL_TENSOR || OP == EL_SQUARE_TENSOR) ? 3
+                     : (OP == EL_DECRYPT2 || OP == EL_DECRYPT3) ? 1 : job.npolys;
+    const long long total = (OP == EL_TENSOR || OP == EL_SQUARE_TENSOR || OP == EL_DECRYPT2 || OP == EL_DECRYPT3)
+                                ? per_poly : (long long)np_out * per_poly;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int p = (int)(idx / per_poly);
+        const long long rem = idx - p * per_poly;
+        const int i = (int)(rem / n2);
+        const long long w = (rem - (long long)i * n2) * 2;         // word offset in limb
+        const Mod md = mods[i];
+        const uint64_t q = md.q;
+        const long long limb_off = (long long)i << job.log_n;
+        const ulonglong2* A = reinterpret_cast<const ulonglong2*>(job.a[z] + p * job.a_poly + limb_off + w);
+        ulonglong2* O = reinterpret_cast<ulonglong2*>(job.out[z] + p * job.out_poly + limb_off + w);
+        if (OP == EL_ADD || OP == EL_SUB) {
+            const ulonglong2 x = *A;
+            const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(job.b[z] + p * job.b_poly + limb_off + w);
+            ulonglong2 r;
+            if (OP == EL_ADD) { r.x = add_mod(x.x, y.x, q); r.y = add_mod(x.y, y.y, q); }
+            else { r.x = sub_mod(x.x, y.x, q); r.y = sub_mod(x.y, y.y, q); }
+            *O = r;
+        } else if (OP == EL_NEG) {
+            const ulonglong2 x = *A;
+            *O = make_ulonglong2(neg_mod(x.x, q), neg_mod(x.y, q));
+        } else if (OP == EL_COPY) {
+            *O = *A;
+        } else if (OP == EL_ADD_PLAIN || OP == EL_SUB_PLAIN) {
+            ulonglong2 x = *A;
+            if (p == 0) {
+                const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(job.b[z] + limb_off + w);
+                if (OP == EL_ADD_PLAIN) { x.x = add_mod(x.x, y.x, q); x.y = add_mod(x.y, y.y, q); }
+                else { x.x = sub_mod(x.x, y.x, q); x.y = sub_mod(x.y, y.y, q); }
+            }
+            *O = x;
+        } else if (OP == EL_MUL_PLAIN) {
+            const ulonglong2 x = *A;
+            const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(job.b[z] + limb_off + w);
+            *O = make_ulonglong2(mul_mod(x.x, y.x, md), mul_mod(x.y, y.y, md));
+        } else if (OP == EL_ADD_SCALAR) {
+            ulonglong2 x = *A;
+            if (p == 0) { x.x = add_mod(x.x, job.scal[i], q); x.y = add_mod(x.y, job.scal[i], q); }
+            *O = x;
+        } else if (OP == EL_MUL_SCALAR) {
+            const ulonglong2 x = *A;
+            const uint64_t s = job.scal[i], sp = job.scalp[i];
+            *O = make_ulonglong2(mul_shoup(x.x, s, sp, q), mul_shoup(x.y, s, sp, q));
+        } else if (OP == EL_TENSOR || OP == EL_SQUARE_TENSOR) {
+            const ulonglong2 a0 = *reinterpret_cast<const ulonglong2*>(job.a[z] + limb_off + w);
+            const ulonglong2 a1 = *reinterpret_cast<const ulonglong2*>(job.a[z] + job.a_poly + limb_off + w);
+            ulonglong2 b0, b1;
+            if (OP == EL_TENSOR) {
+                b0 = *reinterpret_cast<const ulonglong2*>(job.b[z] + limb_off + w);
+                b1 = *reinterpret_cast<const ulonglong2*>(job.b[z] + job.b_poly + limb_off + w);
+            } else { b0 = a0; b1 = a1; }
+            uint64_t* o = job.out[z] + limb_off + w;
+            ulonglong2 r0, r1, r2;
+            r0.x = mul_mod(a0.x, b0.x, md); r0.y = mul_mod(a0.y, b0.y, md);
+            // a0 b1 + a1 b0 with one reduction: sum of two 120-bit products fits 128 bits
+            {
+                U128 s{0, 0};
+                mac128(s, a0.x, b1.x); mac128(s, a1.x, b0.x);
+                r1.x = barrett128(s.lo, s.hi, md);
+                U128 u{0, 0};
+                mac128(u, a0.y, b1.y); mac128(u, a1.y, b0.y);
+                r1.y = barrett128(u.lo, u.hi, md);
+            }
+            r2.x = mul_mod(a1.x, b1.x, md); r2.y = mul_mod(a1.y, b1.y, md);
+            *reinterpret_cast<ulonglong2*>(o) = r0;
+            *reinterpret_cast<ulonglong2*>(o + job.out_poly) = r1;
+            *reinterpret_cast<ulonglong2*>(o + 2 * job.out_poly) = r2;
+        } else if (OP == EL_DECRYPT2 || OP == EL_DECRYPT3) {
+            // b = secret key NTT limbs; out = c0 + c1 s (+ c2 s^2)
+            const ulonglong2 s = *reinterpret_cast<const ulonglong2*>(job.b[z] + limb_off + w);
+            const ulonglong2 c0 = *reinterpret_cast<const ulonglong2*>(job.a[z] + limb_off + w);
+            const ulonglong2 c1 = *reinterpret_cast<const ulonglong2*>(job.a[z] + job.a_poly + limb_off + w);
+            ulonglong2 r;
+            r.x = add_mod(c0.x, mul_mod(c1.x, s.x, md), q);
+            r.y = add_mod(c0.y, mul_mod(c1.y, s.y, md), q);
+            if (OP == EL_DECRYPT3) {
+                const ulonglong2 c2 = *reinterpret_cast<const ulonglong2*>(job.a[z] + 2 * job.a_poly + limb_off + w);
+                r.x = add_mod(r.x, mul_mod(c2.x, mul_mod(s.x, s.x, md), md), q);
+                r.y = add_mod(r.y, mul_mod(c2.y, mul_mod(s.y, s.y, md), md), q);
+            }
+            *reinterpret_cast<ulonglong2*>(job.out[z] + limb_off + w) = r;
+        }
+    }
+}
+
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, cudaStream_t st) {
+    const long long pairs = ((long long)job.nl << (job.log_n - 1)) *
+                            ((op == EL_TENSOR || op == EL_SQUARE_TENSOR || op == EL_DECRYPT2 || op == EL_DECRYPT3)
+                                 ? 1 : job.npolys);
+    long long blocks = (pairs + 255) / 256;
+    const long long cap = (long long)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    dim3 grid((unsigned)blocks, nz);
+    switch (op) {
+#define C(OPV) case OPV: k_elem<OPV><<<grid, 256, 0, st>>>(job, mods); break;
+        C(EL_ADD) C(EL_SUB) C(EL_NEG) C(EL_ADD_PLAIN) C(EL_SUB_PLAIN) C(EL_MUL_PLAIN) C(EL_ADD_SCALAR)
+        C(EL_MUL_SCALAR) C(EL_COPY) C(EL_TENSOR) C(EL_DECRYPT2) C(EL_DECRYPT3) C(EL_SQUARE_TENSOR)
+#undef C
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// NTT-domain automorphism (A15, K6): slot j holds a(psi^(2 brv(j)+1)); psi_g(a) at slot j is
+// a at slot perm[j] = brv(((2 brv(j) + 1) g mod 2N - 1) / 2).
+// ------------------------------------------------------------------------------------------
+struct PtrPack {
+    const uint64_t* in[MAXB];
+    uint64_t* out[MAXB];
+};
+__global__ void __launch_bounds__(256) k_automorphism(PtrPack pk, int nlimbs_total, int log_n, uint64_t g) {
+    const int z = blockIdx.z;
+    const int limb = blockIdx.y;
+    const uint32_t N = 1u << log_n;
+    const uint64_t mask2n = 2ull * N - 1;
+    const uint64_t* in = pk.in[z] + ((long long)limb << log_n);
+    uint64_t* out = pk.out[z] + ((long long)limb << log_n);
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+        const uint32_t bj = __brev(j) >> (32 - log_n);
+        const uint64_t e = ((2ull * bj + 1) * g) & mask2n;
+        const uint32_t src = __brev((uint32_t)((e - 1) >> 1)) >> (32 - log_n);
+        out[j] = in[src];
+    }
+    (void)nlimbs_total;
+}
+
+cudaError_t launch_automorphism(const uint64_t* const* in, uint64_t* const* out, int nz, int nlimbs_total, int log_n,
+                                uint64_t g, cudaStream_t st) {
+    PtrPack pk;
+    for (int z = 0; z < nz; z++) { pk.in[z] = in[z]; pk.out[z] = out[z]; }
+    const int N = 1 << log_n;
+    dim3 grid((N + 255) / 256, nlimbs_total, nz);
+    k_automorphism<<<grid, 256, 0, st>>>(pk, nlimbs_total, log_n, g);
+    return cudaGetLastError();
+}
+
+}  // namespace hisa

@@ -1,0 +1,1521 @@
+// hisa.cu -- host layer of libhisa: the C-ABI of include/hisa.h.
+//
+// Parameters / primes / roots / tables (A3-A6), the handle table (use-after-free detection,
+// S:32-36), a first-fit arena on caller-provided device memory (PyTorch owns device memory),
+// synchronous host checks (levels, scales, keys: A8, A15, A17, A18), and the orchestration of
+// the sm_100a kernels for every HISA instruction.  Encode/decode are host boundary steps (A7, A13).
+// Nothing here computes ciphertext arithmetic on the CPU: every step of the path is a kernel.
+#include <cuda_runtime.h>
+#include <quadmath.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/hisa.h"
+#include "launch.h"
+
+using namespace hisa;
+typedef unsigned __int128 u128;
+
+// ============================================================================================
+// errors
+// ============================================================================================
+static thread_local std::string g_err;
+static int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+extern "C" const char* hisa_last_error(void) { return g_err.c_str(); }
+
+// ============================================================================================
+// host number theory (independent of oracle/): deterministic 7-base Miller-Rabin for 64 bits
+// ============================================================================================
+static uint64_t h_mul(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)((u128)a * b % m); }
+static uint64_t h_pow(uint64_t b, uint64_t e, uint64_t m) {
+    uint64_t r = 1;
+    b %= m;
+    for (; e; e >>= 1, b = h_mul(b, b, m))
+        if (e & 1) r = h_mul(r, b, m);
+    return r;
+}
+static uint64_t h_inv(uint64_t a, uint64_t m) { return h_pow(a % m, m - 2, m); }
+static bool h_prime(uint64_t n) {
+    if (n < 2 || n % 2 == 0) return n == 2;
+    uint64_t d = n - 1;
+    int s = 0;
+    while (!(d & 1)) { d >>= 1; s++; }
+    static const uint64_t W[] = {2, 325, 9375, 28178, 450775, 9780504, 1795265022};
+    for (uint64_t a : W) {
+        a %= n;
+        if (a == 0) continue;
+        uint64_t x = h_pow(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int i = 1; i < s && comp; i++) {
+            x = h_mul(x, x, n);
+            if (x == n - 1) comp = false;
+        }
+        if (comp) return false;
+    }
+    return true;
+}
+static uint32_t h_brv(uint32_t x, int bits) {
+    uint32_t r = 0;
+    for (int i = 0; i < bits; i++) r |= ((x >> i) & 1u) << (bits - 1 - i);
+    return r;
+}
+static uint64_t shoup(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+static Mod make_mod(uint64_t q) {
+    u128 ratio = (~(u128)0) / q;   // floor((2^128 - 1)/q) == floor(2^128/q) for odd q
+    Mod m;
+    m.q = q;
+    m.r0 = (uint64_t)ratio;
+    m.r1 = (uint64_t)(ratio >> 64);
+    return m;
+}
+// A4: the minimal element of multiplicative order exactly 2N
+static uint64_t h_min_root(uint64_t q, uint64_t N) {
+    uint64_t x = 0;
+    for (uint64_t g = 3;; g++) {
+        x = h_pow(g, (q - 1) / (2 * N), q);
+        if (h_pow(x, N, q) == q - 1) break;
+    }
+    const uint64_t x2 = h_mul(x, x, q);
+    uint64_t best = x, cur = x;
+    for (uint64_t i = 1; i < N; i++) {
+        cur = h_mul(cur, x2, q);
+        if (cur < best) best = cur;
+    }
+    return best;
+}
+
+// ============================================================================================
+// device memory: first-fit arena on a caller-owned buffer, else cudaMallocAsync
+// ============================================================================================
+struct Arena {
+    char* base = nullptr;
+    size_t size = 0;
+    std::map<size_t, size_t> free_;   // offset -> bytes
+    std::map<size_t, size_t> used_;
+    size_t in_use = 0, peak = 0;
+    void attach(void* p, size_t n) {
+        base = (char*)p;
+        size = n & ~(size_t)255;
+        free_.clear();
+        used_.clear();
+        free_[0] = size;
+    }
+    void* alloc(size_t n) {
+        n = (n + 255) & ~(size_t)255;
+        if (n == 0) n = 256;
+        for (auto it = free_.begin(); it != free_.end(); ++it) {
+            if (it->second >= n) {
+                size_t off = it->first, rem = it->second - n;
+                free_.erase(it);
+                if (rem) free_[off + n] = rem;
+                used_[off] = n;
+                in_use += n;
+                if (in_use > peak) peak = in_use;
+                return base + off;
+            }
+        }
+        return nullptr;
+    }
+    void release(void* p) {
+        size_t off = (char*)p - base;
+        auto u = used_.find(off);
+        if (u == used_.end()) return;
+        size_t n = u->second;
+        used_.erase(u);
+        in_use -= n;
+        auto nx = free_.lower_bound(off);
+        if (nx != free_.end() && off + n == nx->first) {
+            n += nx->second;
+            free_.erase(nx);
+        }
+        auto pv = free_.lower_bound(off);
+        if (pv != free_.begin()) {
+            --pv;
+            if (pv->first + pv->second == off) {
+                pv->second += n;
+                return;
+            }
+        }
+        free_[off] = n;
+    }
+};
+
+// ============================================================================================
+// context
+// ============================================================================================
+enum ObjKind { OBJ_CT = 1, OBJ_PT = 2 };
+struct Obj {
+    int kind = 0;
+    uint64_t* ptr = nullptr;
+    int level = 0;
+    int npolys = 0;
+    double scale = 0;
+    uint32_t gen = 0;
+    bool live = false;
+};
+
+struct hisa_ctx {
+    int log_n = 0;
+    uint64_t N = 0;
+    int L = 0;                        // number of q primes
+    std::vector<uint64_t> mod;        // q_0..q_{L-1}, p
+    uint64_t seed = 0;
+    int device = 0;
+    cudaStream_t stream = 0;
+    bool poisoned = false;
+    Arena arena;
+    bool has_arena = false;
+    size_t pool_in_use = 0, pool_peak = 0;
+    std::map<void*, size_t> pool_sizes;
+    // device tables
+    Mod* d_mods = nullptr;
+    ulonglong2* d_fwd = nullptr;
+    ulonglong2* d_inv = nullptr;
+    ulonglong2* d_ninv = nullptr;
+    ulonglong2* d_pinv = nullptr;     // p^-1 mod q_i (ModDown)
+    ulonglong2* d_qlinv = nullptr;    // [l][L+1]: q_l^-1 mod q_i (rescale)
+    std::vector<void*> table_allocs;
+    // keys
+    bool have_sk = false;
+    int64_t* d_s_int = nullptr;
+    uint64_t* d_sk = nullptr;         // [(L+1)][N]
+    uint64_t* d_pk = nullptr;         // [2][L][N]
+    uint64_t* d_rlk = nullptr;        // [L][2][L+1][N]
+    std::map<uint64_t, uint64_t*> rot_keys;
+    uint64_t enc_counter = 0;
+    // handles
+    std::vector<Obj> objs;
+    std::vector<uint32_t> free_slots;
+
+    Tables tables(const ulonglong2* comb = nullptr) const {
+        Tables t;
+        t.fwd = d_fwd;
+        t.inv = d_inv;
+        t.mods = d_mods;
+        t.ninv = d_ninv;
+        t.comb = comb;
+        t.log_n = log_n;
+        return t;
+    }
+};
+
+static size_t key_words(const hisa_ctx* c) { return (size_t)c->L * 2 * (c->L + 1) * c->N; }
+
+static void* dalloc(hisa_ctx* c, size_t bytes) {
+    if (c->has_arena) return c->arena.alloc(bytes);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 256, c->stream) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    c->pool_sizes[p] = bytes;
+    c->pool_in_use += bytes;
+    if (c->pool_in_use > c->pool_peak) c->pool_peak = c->pool_in_use;
+    return p;
+}
+static void dfree(hisa_ctx* c, void* p) {
+    if (!p) return;
+    if (c->has_arena) { c->arena.release(p); return; }
+    auto it = c->pool_sizes.find(p);
+    if (it != c->pool_sizes.end()) { c->pool_in_use -= it->second; c->pool_sizes.erase(it); }
+    cudaFreeAsync(p, c->stream);
+}
+template <class T>
+static T* dalloc_t(hisa_ctx* c, size_t n) { return (T*)dalloc(c, n * sizeof(T)); }
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            c->poisoned = true;                                                           \
+            return fail(HISA_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+        }                                                                                 \
+    } while (0)
+#define CHECK_CTX(c)                                                              \
+    do {                                                                          \
+        if (!(c)) return fail(HISA_E_PARAMS, "null context");                     \
+        if ((c)->poisoned) return fail(HISA_E_CUDA, "context poisoned by an earlier CUDA error"); \
+    } while (0)
+#define RET(x)                      \
+    do {                            \
+        int r_ = (x);               \
+        if (r_ != HISA_OK) return r_; \
+    } while (0)
+
+// ---- handle table ----
+static uint64_t new_handle(hisa_ctx* c, int kind, uint64_t* ptr, int level, int npolys, double scale) {
+    uint32_t slot;
+    if (!c->free_slots.empty()) {
+        slot = c->free_slots.back();
+        c->free_slots.pop_back();
+    } else {
+        c->objs.push_back(Obj());
+        slot = (uint32_t)c->objs.size() - 1;
+        if (slot == 0) {   // slot 0 reserved: handle 0 is never valid
+            c->objs.push_back(Obj());
+            slot = 1;
+        }
+    }
+    Obj& o = c->objs[slot];
+    o.kind = kind;
+    o.ptr = ptr;
+    o.level = level;
+    o.npolys = npolys;
+    o.scale = scale;
+    o.gen += 1;
+    o.live = true;
+    return ((uint64_t)o.gen << 32) | slot;
+}
+static Obj* get_obj(hisa_ctx* c, uint64_t h, int kind) {
+    uint32_t slot = (uint32_t)h, gen = (uint32_t)(h >> 32);
+    if (slot == 0 || slot >= c->objs.size()) return nullptr;
+    Obj& o = c->objs[slot];
+    if (!o.live || o.gen != gen || (kind && o.kind != kind)) return nullptr;
+    return &o;
+}
+static size_t obj_words(const hisa_ctx* c, const Obj* o) {
+    return (size_t)(o->kind == OBJ_CT ? o->npolys : 1) * (o->level + 1) * c->N;
+}
+
+// result placement: fresh handle, or in place (Assign form) on `self`
+static int emit_ct(hisa_ctx* c, hisa_ct* out, hisa_ct self, uint64_t* ptr, int level, int npolys, double scale) {
+    if (out) {
+        *out = new_handle(c, OBJ_CT, ptr, level, npolys, scale);
+        return HISA_OK;
+    }
+    Obj* o = get_obj(c, self, OBJ_CT);
+    dfree(c, o->ptr);
+    o->ptr = ptr;
+    o->level = level;
+    o->npolys = npolys;
+    o->scale = scale;
+    return HISA_OK;
+}
+
+#define GET_CT(var, h)                                                            \
+    Obj* var = get_obj(c, h, OBJ_CT);                                            \
+    if (!var) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle %llx", (unsigned long long)(h));
+#define GET_PT(var, h)                                                            \
+    Obj* var = get_obj(c, h, OBJ_PT);                                            \
+    if (!var) return fail(HISA_E_INVALID_HANDLE, "invalid plaintext handle %llx", (unsigned long long)(h));
+
+// ============================================================================================
+// NTT helpers over contiguous limb arrays
+// ============================================================================================
+static PassJob job0() {
+    PassJob j;
+    memset(&j, 0, sizeof j);
+    return j;
+}
+// forward NTT in place of `nz` arrays of `nlimbs` limbs (limb lambda mod mmap[lambda % nb])
+static int ntt_fwd(hisa_ctx* c, uint64_t* const* ptrs, int nz, int nb, const uint8_t* mmap, int nlimbs = -1) {
+    if (nlimbs < 0) nlimbs = nb;
+    PassJob j = job0();
+    for (int z = 0; z < nz; z++) { j.src[z] = ptrs[z]; j.dst[z] = ptrs[z]; }
+    j.nb = nb;
+    j.src_a = j.dst_a = (long long)nb * c->N;
+    j.src_b = j.dst_b = (long long)c->N;
+    for (int i = 0; i < nb; i++) j.mod_map[i] = mmap[i];
+    Tables tb = c->tables();
+    CK(launch_fwd_pass1(j, tb, nlimbs, nz, false, c->stream));
+    CK(launch_fwd_pass2(j, tb, nlimbs, nz, false, c->stream));
+    return HISA_OK;
+}
+static int ntt_inv(hisa_ctx* c, const uint64_t* const* src, uint64_t* const* dst, int nz, int nb, const uint8_t* mmap,
+                   int nlimbs = -1) {
+    if (nlimbs < 0) nlimbs = nb;
+    PassJob j = job0();
+    for (int z = 0; z < nz; z++) { j.src[z] = src[z]; j.dst[z] = dst[z]; }
+    j.nb = nb;
+    j.src_a = j.dst_a = (long long)nb * c->N;
+    j.src_b = j.dst_b = (long long)c->N;
+    for (int i = 0; i < nb; i++) j.mod_map[i] = mmap[i];
+    Tables tb = c->tables();
+    CK(launch_inv_passA(j, tb, nlimbs, nz, c->stream));
+    for (int z = 0; z < nz; z++) j.src[z] = dst[z];
+    CK(launch_inv_passB(j, tb, nlimbs, nz, c->stream));
+    return HISA_OK;
+}
+static void ident_map(uint8_t* m, int n, int base = 0) {
+    for (int i = 0; i < n; i++) m[i] = (uint8_t)(base + i);
+}
+
+// ============================================================================================
+// context create / destroy
+// ============================================================================================
+extern "C" int hisa_ctx_create(const hisa_params* p, hisa_ctx** out) {
+    if (!p || !out) return fail(HISA_E_PARAMS, "null argument");
+    if (p->log_n < 8 || p->log_n > 16) return fail(HISA_E_PARAMS, "log_n must be in [8, 16]");
+    if (p->num_q < 1 || p->num_q > MAXL - 4 || !p->q_bits) return fail(HISA_E_PARAMS, "num_q must be in [1, 60]");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(HISA_E_CUDA, "no CUDA device: libhisa has no CPU fallback");
+    }
+    if (p->device < 0 || p->device >= ndev) return fail(HISA_E_PARAMS, "bad device %d", p->device);
+    hisa_ctx* c = new hisa_ctx();
+    c->log_n = p->log_n;
+    c->N = 1ull << p->log_n;
+    c->L = p->num_q;
+    c->seed = p->seed;
+    c->device = p->device;
+    if (cudaSetDevice(p->device) != cudaSuccess) { delete c; return fail(HISA_E_CUDA, "cudaSetDevice"); }
+    // A3: special prime first, then q_0 .. q_{L-1}; per bit size descending from 2^b
+    std::map<int, uint64_t> cursor;   // bits -> next k
+    const uint64_t twoN = 2 * c->N;
+    auto take = [&](int bits) -> uint64_t {
+        if (bits < 20 || bits > 60) return 0;
+        if (!cursor.count(bits)) cursor[bits] = ((1ull << bits) - 2) / twoN;
+        for (uint64_t k = cursor[bits]; k > 0; k--) {
+            uint64_t q = k * twoN + 1;
+            if (h_prime(q)) { cursor[bits] = k - 1; return q; }
+        }
+        return 0;
+    };
+    uint64_t pp = take(p->p_bits);
+    for (int i = 0; i < c->L; i++) c->mod.push_back(take(p->q_bits[i]));
+    c->mod.push_back(pp);
+    for (uint64_t q : c->mod)
+        if (!q) { delete c; return fail(HISA_E_PARAMS, "prime bit sizes must be in [20, 60] with enough primes"); }
+    const int M = c->L + 1;
+    const uint64_t N = c->N;
+    std::vector<ulonglong2> fwd((size_t)M * N), inv((size_t)M * N), ninv(M), pinv(M), qlinv((size_t)c->L * M);
+    std::vector<Mod> mods(M);
+    for (int m = 0; m < M; m++) {
+        const uint64_t q = c->mod[m];
+        mods[m] = make_mod(q);
+        const uint64_t psi = h_min_root(q, N), psii = h_inv(psi, q);
+        // psi^k for k < N, then scatter to bit-reversed positions
+        std::vector<uint64_t> pw(N), pwi(N);
+        pw[0] = pwi[0] = 1;
+        for (uint64_t k = 1; k < N; k++) { pw[k] = h_mul(pw[k - 1], psi, q); pwi[k] = h_mul(pwi[k - 1], psii, q); }
+        for (uint64_t k = 0; k < N; k++) {
+            const uint64_t w = pw[h_brv((uint32_t)k, c->log_n)], wi = pwi[h_brv((uint32_t)k, c->log_n)];
+            fwd[(size_t)m * N + k] = make_ulonglong2(w, shoup(w, q));
+            inv[(size_t)m * N + k] = make_ulonglong2(wi, shoup(wi, q));
+        }
+        const uint64_t ni = h_inv(N % q, q);
+        ninv[m] = make_ulonglong2(ni, shoup(ni, q));
+        const uint64_t pi = h_inv(pp % q, q);
+        pinv[m] = make_ulonglong2(pi, shoup(pi, q));
+    }
+    for (int l = 0; l < c->L; l++)
+        for (int m = 0; m < M; m++) {
+            const uint64_t q = c->mod[m];
+            const uint64_t v = (m == l) ? 0 : h_inv(c->mod[l] % q, q);
+            qlinv[(size_t)l * M + m] = make_ulonglong2(v, shoup(v, q));
+        }
+    auto up = [&](void** dptr, const void* src, size_t bytes) -> bool {
+        if (cudaMalloc(dptr, bytes) != cudaSuccess) return false;
+        c->table_allocs.push_back(*dptr);
+        return cudaMemcpy(*dptr, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+    };
+    bool ok = up((void**)&c->d_mods, mods.data(), M * sizeof(Mod)) &&
+              up((void**)&c->d_fwd, fwd.data(), fwd.size() * sizeof(ulonglong2)) &&
+              up((void**)&c->d_inv, inv.data(), inv.size() * sizeof(ulonglong2)) &&
+              up((void**)&c->d_ninv, ninv.data(), M * sizeof(ulonglong2)) &&
+              up((void**)&c->d_pinv, pinv.data(), M * sizeof(ulonglong2)) &&
+              up((void**)&c->d_qlinv, qlinv.data(), qlinv.size() * sizeof(ulonglong2));
+    if (!ok) {
+        for (void* q : c->table_allocs) cudaFree(q);
+        delete c;
+        cudaGetLastError();
+        return fail(HISA_E_CUDA, "table upload failed");
+    }
+    c->objs.push_back(Obj());   // slot 0 reserved
+    *out = c;
+    return HISA_OK;
+}
+
+extern "C" int hisa_ctx_destroy(hisa_ctx* c) {
+    if (!c) return HISA_OK;
+    cudaStreamSynchronize(c->stream);
+    if (!c->has_arena) {
+        for (auto& kv : c->pool_sizes) cudaFree(kv.first);
+    }
+    for (void* q : c->table_allocs) cudaFree(q);
+    cudaGetLastError();
+    delete c;
+    return HISA_OK;
+}
+
+extern "C" int hisa_attach_arena(hisa_ctx* c, void* dev_ptr, size_t bytes) {
+    CHECK_CTX(c);
+    if (!dev_ptr || bytes < 4096) return fail(HISA_E_PARAMS, "bad arena");
+    if (c->has_arena || !c->pool_sizes.empty()) return fail(HISA_E_PARAMS, "arena must be attached before allocation");
+    c->arena.attach(dev_ptr, bytes);
+    c->has_arena = true;
+    return HISA_OK;
+}
+extern "C" int hisa_set_stream(hisa_ctx* c, void* stream) {
+    CHECK_CTX(c);
+    CK(cudaStreamSynchronize(c->stream));
+    c->stream = (cudaStream_t)stream;
+    return HISA_OK;
+}
+extern "C" int hisa_sync(hisa_ctx* c) {
+    CHECK_CTX(c);
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaGetLastError());
+    return HISA_OK;
+}
+extern "C" int hisa_supports(const hisa_ctx* c, int profile) {
+    if (!c) return 0;
+    return (profile & HISA_PROFILE_BOOTSTRAP) ? 0
+           : (profile & (HISA_PROFILE_ENCRYPTION | HISA_PROFILE_INTEGERS | HISA_PROFILE_DIVISION | HISA_PROFILE_RELIN)) ? 1 : 0;
+}
+extern "C" int hisa_moduli(const hisa_ctx* c, uint64_t* out, size_t n) {
+    if (!c || !out || n < c->mod.size()) return fail(HISA_E_PARAMS, "buffer too small");
+    for (size_t i = 0; i < c->mod.size(); i++) out[i] = c->mod[i];
+    return HISA_OK;
+}
+extern "C" int hisa_ring_degree(const hisa_ctx* c, uint64_t* n_out, int* num_q_out) {
+    if (!c) return fail(HISA_E_PARAMS, "null context");
+    if (n_out) *n_out = c->N;
+    if (num_q_out) *num_q_out = c->L;
+    return HISA_OK;
+}
+extern "C" int hisa_mem_stats(const hisa_ctx* c, size_t* in_use, size_t* peak) {
+    if (!c) return fail(HISA_E_PARAMS, "null context");
+    if (in_use) *in_use = c->has_arena ? c->arena.in_use : c->pool_in_use;
+    if (peak) *peak = c->has_arena ? c->arena.peak : c->pool_peak;
+    return HISA_OK;
+}
+
+// ============================================================================================
+// keys (A9-A16) and encryption (A12) -- all sampling and arithmetic in kernels
+// ============================================================================================
+enum { TAG_SK = 1, TAG_PK_A = 2, TAG_PK_E = 3, TAG_ENC_V = 4, TAG_ENC_E0 = 5, TAG_ENC_E1 = 6,
+       TAG_KSK_A = 7, TAG_KSK_E = 8, TAG_BENCH = 9 };
+
+// b[r] = e[r] - a[r] s[r] (+ gadget * sp[r] on limb `glimb`) over nl limbs (limb r mod mods[mmap[r]])
+struct KeyAsmJob { uint8_t mmap[MAXL]; };
+__global__ void k_key_assemble(uint64_t* b, const uint64_t* a, const uint64_t* s, const uint64_t* sp, int glimb,
+                               uint64_t gadget, KeyAsmJob job, int nl, int log_n, const Mod* mods) {
+    const long long N = 1ll << log_n;
+    const long long total = N * nl;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(idx >> log_n);
+        const Mod md = mods[job.mmap[r]];
+        uint64_t v = sub_mod(b[idx], mul_mod(a[idx], s[(long long)job.mmap[r] * N + (idx & (N - 1))], md), md.q);
+        if (r == glimb) v = add_mod(v, mul_mod(gadget, sp[(long long)job.mmap[r] * N + (idx & (N - 1))], md), md.q);
+        b[idx] = v;
+    }
+}
+// c0 = v pk_b + e0 + m ; c1 = v pk_a + e1 (all NTT, limbs 0..l)
+__global__ void k_enc_assemble(uint64_t* ct, const uint64_t* v, const uint64_t* e0, const uint64_t* e1,
+                               const uint64_t* m, const uint64_t* pk, int l1, int L, int log_n, const Mod* mods) {
+    const long long N = 1ll << log_n;
+    const long long total = N * l1;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(idx >> log_n);
+        const Mod md = mods[i];
+        const uint64_t pb = pk[idx], pa = pk[(long long)L * N + idx];
+        ct[idx] = add_mod(add_mod(mul_mod(v[idx], pb, md), e0[idx], md.q), m[idx], md.q);
+        ct[(long long)l1 * N + idx] = add_mod(mul_mod(v[idx], pa, md), e1[idx], md.q);
+    }
+}
+
+static int sample_small_ntt(hisa_ctx* c, uint32_t tag, uint64_t index, int kind, int nl, uint64_t* out) {
+    int64_t* tmp = dalloc_t<int64_t>(c, c->N);
+    if (!tmp) return fail(HISA_E_OOM, "sampler scratch");
+    uint8_t mm[MAXL];
+    ident_map(mm, nl);
+    CK(launch_sample_small(tmp, c->seed, tag, index, kind, c->log_n, c->stream));
+    CK(launch_int_to_limbs(tmp, out, mm, nl, c->log_n, c->d_mods, c->stream));
+    uint64_t* pp[1] = {out};
+    RET(ntt_fwd(c, pp, 1, nl, mm));
+    dfree(c, tmp);
+    return HISA_OK;
+}
+
+static int gen_ksk(hisa_ctx* c, uint64_t keyid, const uint64_t* sp, uint64_t** out) {
+    const int L = c->L, M = L + 1;
+    const uint64_t N = c->N;
+    uint64_t* key = dalloc_t<uint64_t>(c, key_words(c));
+    if (!key) return fail(HISA_E_OOM, "key allocation (%zu MiB)", key_words(c) * 8 >> 20);
+    uint8_t mm[MAXL];
+    ident_map(mm, M);
+    uint64_t idx[MAXL];
+    for (int j = 0; j < L; j++) {
+        uint64_t* b = key + (size_t)j * 2 * M * N;
+        uint64_t* a = b + (size_t)M * N;
+        RET(sample_small_ntt(c, TAG_KSK_E, (keyid << 32) | (uint64_t)j, 1, M, b));
+        for (int r = 0; r < M; r++) idx[r] = (keyid << 32) | ((uint64_t)j << 16) | (uint64_t)r;
+        CK(launch_sample_uniform(a, c->seed, TAG_KSK_A, idx, mm, M, c->log_n, c->d_mods, c->stream));
+        KeyAsmJob kj;
+        ident_map(kj.mmap, M);
+        const uint64_t gadget = c->mod[L] % c->mod[j];   // [P]_{q_j}
+        k_key_assemble<<<592, 256, 0, c->stream>>>(b, a, c->d_sk, sp, j, gadget, kj, M, c->log_n, c->d_mods);
+        CK(cudaGetLastError());
+    }
+    *out = key;
+    return HISA_OK;
+}
+
+extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin) {
+    CHECK_CTX(c);
+    if (n && !rot) return fail(HISA_E_PARAMS, "null rotation list");
+    const int L = c->L, M = L + 1;
+    const uint64_t N = c->N, slots = N / 2;
+    uint8_t mm[MAXL];
+    ident_map(mm, M);
+    if (!c->have_sk) {
+        c->d_s_int = dalloc_t<int64_t>(c, N);
+        c->d_sk = dalloc_t<uint64_t>(c, (size_t)M * N);
+        c->d_pk = dalloc_t<uint64_t>(c, (size_t)2 * L * N);
+        if (!c->d_s_int || !c->d_sk || !c->d_pk) return fail(HISA_E_OOM, "key allocation");
+        CK(launch_sample_small(c->d_s_int, c->seed, TAG_SK, 0, 0, c->log_n, c->stream));
+        CK(launch_int_to_limbs(c->d_s_int, c->d_sk, mm, M, c->log_n, c->d_mods, c->stream));
+        uint64_t* pp[1] = {c->d_sk};
+        RET(ntt_fwd(c, pp, 1, M, mm));
+        // pk = (-a s + e, a) over q_0..q_{L-1}
+        RET(sample_small_ntt(c, TAG_PK_E, 0, 1, L, c->d_pk));
+        uint64_t idx[MAXL];
+        for (int m = 0; m < L; m++) idx[m] = (uint64_t)m;
+        CK(launch_sample_uniform(c->d_pk + (size_t)L * N, c->seed, TAG_PK_A, idx, mm, L, c->log_n, c->d_mods,
+                                 c->stream));
+        KeyAsmJob kj;
+        ident_map(kj.mmap, L);
+        k_key_assemble<<<592, 256, 0, c->stream>>>(c->d_pk, c->d_pk + (size_t)L * N, c->d_sk, nullptr, -1, 0, kj, L,
+                                                   c->log_n, c->d_mods);
+        CK(cudaGetLastError());
+        c->have_sk = true;
+    }
+    if (relin && !c->d_rlk) {
+        uint64_t* sp = dalloc_t<uint64_t>(c, (size_t)M * N);
+        if (!sp) return fail(HISA_E_OOM, "relin target");
+        ElemJob ej;
+        memset(&ej, 0, sizeof ej);
+        ej.a[0] = c->d_sk; ej.b[0] = c->d_sk; ej.out[0] = sp;
+        ej.npolys = 1; ej.nl = M; ej.log_n = c->log_n;
+        CK(launch_elem(EL_MUL_PLAIN, ej, c->d_mods, 1, c->stream));
+        RET(gen_ksk(c, 0, sp, &c->d_rlk));
+        dfree(c, sp);
+    }
+    for (size_t i = 0; i < n; i++) {
+        int64_t k = rot[i] % (int64_t)slots;
+        if (k < 0) k += (int64_t)slots;
+        if (k == 0 || c->rot_keys.count((uint64_t)k)) continue;
+        const uint64_t g = h_pow(5, (uint64_t)k, 2 * N);
+        int64_t* sg = dalloc_t<int64_t>(c, N);
+        uint64_t* sp = dalloc_t<uint64_t>(c, (size_t)M * N);
+        if (!sg || !sp) return fail(HISA_E_OOM, "rotation target");
+        CK(launch_automorphism_int(c->d_s_int, sg, c->log_n, g, c->stream));
+        CK(launch_int_to_limbs(sg, sp, mm, M, c->log_n, c->d_mods, c->stream));
+        uint64_t* pp[1] = {sp};
+        RET(ntt_fwd(c, pp, 1, M, mm));
+        uint64_t* key = nullptr;
+        RET(gen_ksk(c, (uint64_t)k, sp, &key));
+        c->rot_keys[(uint64_t)k] = key;
+        dfree(c, sg);
+        dfree(c, sp);
+    }
+    return HISA_OK;
+}
+
+extern "C" int hisa_key_export(hisa_ctx* c, int64_t which, uint64_t* host, size_t words) {
+    CHECK_CTX(c);
+    if (!c->have_sk) return fail(HISA_E_NO_SECRET, "keygen first");
+    const uint64_t* src = nullptr;
+    size_t w = 0;
+    if (which == -1) { src = c->d_pk; w = (size_t)2 * c->L * c->N; }
+    else if (which == -2) { src = c->d_sk; w = (size_t)(c->L + 1) * c->N; }
+    else if (which == 0) { src = c->d_rlk; w = key_words(c); }
+    else if (c->rot_keys.count((uint64_t)which)) { src = c->rot_keys[(uint64_t)which]; w = key_words(c); }
+    if (!src) return fail(HISA_E_NO_KEY, "no such key %lld", (long long)which);
+    if (words != w) return fail(HISA_E_PARAMS, "key has %zu words", w);
+    CK(cudaMemcpyAsync(host, src, w * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return HISA_OK;
+}
+
+extern "C" int hisa_encrypt(hisa_ctx* c, hisa_pt pt, hisa_ct* out) {
+    CHECK_CTX(c);
+    GET_PT(p, pt);
+    if (!out) return fail(HISA_E_PARAMS, "null out");
+    if (!c->have_sk) return fail(HISA_E_NO_SECRET, "keygen first");
+    const int l1 = p->level + 1;
+    const uint64_t N = c->N;
+    uint64_t* tmp = dalloc_t<uint64_t>(c, (size_t)3 * l1 * N);
+    uint64_t* ct = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+    if (!tmp || !ct) return fail(HISA_E_OOM, "encrypt");
+    const uint64_t ctr = c->enc_counter++;
+    RET(sample_small_ntt(c, TAG_ENC_V, ctr, 0, l1, tmp));
+    RET(sample_small_ntt(c, TAG_ENC_E0, ctr, 1, l1, tmp + (size_t)l1 * N));
+    RET(sample_small_ntt(c, TAG_ENC_E1, ctr, 1, l1, tmp + (size_t)2 * l1 * N));
+    k_enc_assemble<<<592, 256, 0, c->stream>>>(ct, tmp, tmp + (size_t)l1 * N, tmp + (size_t)2 * l1 * N, p->ptr, c->d_pk,
+                                               l1, c->L, c->log_n, c->d_mods);
+    CK(cudaGetLastError());
+    dfree(c, tmp);
+    *out = new_handle(c, OBJ_CT, ct, p->level, 2, p->scale);
+    return HISA_OK;
+}
+
+extern "C" int hisa_decrypt(hisa_ctx* c, hisa_ct h, hisa_pt* out) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (!out) return fail(HISA_E_PARAMS, "null out");
+    if (!c->have_sk) return fail(HISA_E_NO_SECRET, "keygen first");
+    const int l1 = o->level + 1;
+    uint64_t* pt = dalloc_t<uint64_t>(c, (size_t)l1 * c->N);
+    if (!pt) return fail(HISA_E_OOM, "decrypt");
+    ElemJob ej;
+    memset(&ej, 0, sizeof ej);
+    ej.a[0] = o->ptr; ej.b[0] = c->d_sk; ej.out[0] = pt;
+    ej.npolys = 1; ej.nl = l1; ej.log_n = c->log_n;
+    ej.a_poly = (long long)l1 * c->N;
+    CK(launch_elem(o->npolys == 3 ? EL_DECRYPT3 : EL_DECRYPT2, ej, c->d_mods, 1, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = new_handle(c, OBJ_PT, pt, o->level, 1, o->scale);
+    return HISA_OK;
+}
+
+extern "C" int hisa_free(hisa_ctx* c, uint64_t h) {
+    if (!c) return fail(HISA_E_PARAMS, "null context");
+    Obj* o = get_obj(c, h, 0);
+    if (!o) return fail(HISA_E_INVALID_HANDLE, "invalid handle %llx", (unsigned long long)h);
+    dfree(c, o->ptr);
+    o->ptr = nullptr;
+    o->live = false;
+    c->free_slots.push_back((uint32_t)h);
+    return HISA_OK;
+}
+
+static int copy_obj(hisa_ctx* c, const Obj* o, uint64_t** out) {
+    const size_t w = obj_words(c, o);
+    uint64_t* p = dalloc_t<uint64_t>(c, w);
+    if (!p) return fail(HISA_E_OOM, "copy");
+    CK(cudaMemcpyAsync(p, o->ptr, w * 8, cudaMemcpyDeviceToDevice, c->stream));
+    *out = p;
+    return HISA_OK;
+}
+
+extern "C" int hisa_copy(hisa_ctx* c, hisa_ct h, hisa_ct* out) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (!out) return fail(HISA_E_PARAMS, "null out");
+    uint64_t* p;
+    RET(copy_obj(c, o, &p));
+    *out = new_handle(c, OBJ_CT, p, o->level, o->npolys, o->scale);
+    return HISA_OK;
+}
+
+// ============================================================================================
+// encode / decode (A7, A13): host boundary, long-double FFT, binary128 near-tie recomputation
+// ============================================================================================
+typedef std::complex<long double> cld;
+static void fft_ld(std::vector<cld>& a, int sign) {
+    const size_t n = a.size();
+    int bits = 0;
+    while ((1ull << bits) < n) bits++;
+    for (size_t i = 0; i < n; i++) {
+        size_t j = h_brv((uint32_t)i, bits);
+        if (i < j) std::swap(a[i], a[j]);
+    }
+    const long double pi = acosl(-1.0L);
+    for (size_t len = 2; len <= n; len <<= 1) {
+        const size_t half = len / 2;
+        std::vector<cld> w(half);
+        for (size_t k = 0; k < half; k++) {
+            const long double ang = sign * 2.0L * pi * (long double)k / (long double)len;
+            w[k] = cld(cosl(ang), sinl(ang));
+        }
+        for (size_t i = 0; i < n; i += len)
+            for (size_t k = 0; k < half; k++) {
+                cld u = a[i + k], v = a[i + k + half] * w[k];
+                a[i + k] = u + v;
+                a[i + k + half] = u - v;
+            }
+    }
+}
+
+static int encode_coeffs(hisa_ctx* c, const double* z, size_t n, double scale, std::vector<int64_t>& m) {
+    const uint64_t N = c->N, twoN = 2 * N;
+    std::vector<cld> A(N, cld(0, 0));
+    std::vector<uint64_t> pow5(n);
+    uint64_t k = 1;
+    for (size_t j = 0; j < n; j++) {
+        pow5[j] = k;
+        A[(k - 1) / 2] += cld((long double)z[j], 0);
+        const uint64_t kc = twoN - k;
+        A[(kc - 1) / 2] += cld((long double)z[j], 0);
+        k = k * 5 % twoN;
+    }
+    fft_ld(A, -1);   // F[t] = sum_m A[m] e^{-2 pi i m t / N}
+    const long double pi = acosl(-1.0L);
+    m.assign(N, 0);
+    std::vector<__float128> cq;
+    for (uint64_t t = 0; t < N; t++) {
+        const long double ang = -pi * (long double)t / (long double)N;
+        const cld tw(cosl(ang), sinl(ang));
+        const long double v = (A[t] * tw).real() * (long double)scale / (long double)N;
+        const long double av = fabsl(v);
+        const long double fr = av - floorl(av);
+        long double r;
+        if (fabsl(fr - 0.5L) < 0x1p-12L) {   // near tie: binary128 direct sum (A7)
+            if (cq.empty()) {
+                cq.resize(twoN);
+                for (uint64_t e = 0; e < twoN; e++) cq[e] = cosq(M_PIq * (__float128)e / (__float128)N);
+            }
+            __float128 acc = 0;
+            for (size_t j = 0; j < n; j++) acc += 2 * (__float128)z[j] * cq[(uint64_t)((u128)pow5[j] * t % twoN)];
+            acc = acc * (__float128)scale / (__float128)N;
+            __float128 rq = floorq(fabsq(acc) + 0.5Q);
+            r = (long double)(acc < 0 ? -rq : rq);
+        } else {
+            r = floorl(av + 0.5L);
+            if (v < 0) r = -r;
+        }
+        if (!(fabsl(r) < 0x1p62L)) return fail(HISA_E_PARAMS, "encoded coefficient exceeds 2^62");
+        m[t] = (int64_t)r;
+    }
+    return HISA_OK;
+}
+
+extern "C" int hisa_encode(hisa_ctx* c, const double* v, size_t n, double scale, int level, hisa_pt* out) {
+    CHECK_CTX(c);
+    if (!out || (n && !v)) return fail(HISA_E_PARAMS, "null argument");
+    if (n > c->N / 2) return fail(HISA_E_CAPACITY, "%zu values > N/2 = %llu slots", n, (unsigned long long)(c->N / 2));
+    if (level < 0) level = c->L - 1;
+    if (level >= c->L) return fail(HISA_E_PARAMS, "level %d >= L", level);
+    if (!(scale > 0) || !std::isfinite(scale)) return fail(HISA_E_PARAMS, "bad scale");
+    for (size_t i = 0; i < n; i++)
+        if (!std::isfinite(v[i])) return fail(HISA_E_PARAMS, "non-finite slot value");
+    std::vector<int64_t> m;
+    RET(encode_coeffs(c, v, n, scale, m));
+    const int l1 = level + 1;
+    int64_t* dm = dalloc_t<int64_t>(c, c->N);
+    uint64_t* pt = dalloc_t<uint64_t>(c, (size_t)l1 * c->N);
+    if (!dm || !pt) return fail(HISA_E_OOM, "encode");
+    CK(cudaMemcpyAsync(dm, m.data(), c->N * 8, cudaMemcpyHostToDevice, c->stream));
+    uint8_t mm[MAXL];
+    ident_map(mm, l1);
+    CK(launch_int_to_limbs(dm, pt, mm, l1, c->log_n, c->d_mods, c->stream));
+    uint64_t* pp[1] = {pt};
+    RET(ntt_fwd(c, pp, 1, l1, mm));
+    CK(cudaStreamSynchronize(c->stream));   // host vector m must outlive the copy
+    dfree(c, dm);
+    *out = new_handle(c, OBJ_PT, pt, level, 1, scale);
+    return HISA_OK;
+}
+
+extern "C" int hisa_decode(hisa_ctx* c, hisa_pt h, double* out, size_t n) {
+    CHECK_CTX(c);
+    GET_PT(p, h);
+    if (n > c->N / 2) return fail(HISA_E_CAPACITY, "n > N/2");
+    if (n && !out) return fail(HISA_E_PARAMS, "null out");
+    const uint64_t N = c->N;
+    uint64_t* tmp = dalloc_t<uint64_t>(c, N);
+    if (!tmp) return fail(HISA_E_OOM, "decode");
+    uint8_t mm[1] = {0};
+    const uint64_t* s[1] = {p->ptr};
+    uint64_t* d[1] = {tmp};
+    RET(ntt_inv(c, s, d, 1, 1, mm));
+    std::vector<uint64_t> a(N);
+    CK(cudaMemcpyAsync(a.data(), tmp, N * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, tmp);
+    const uint64_t q0 = c->mod[0];
+    // G[m] = sum_t (m_t zeta^t) e^{+2 pi i m t / N};  value at zeta^(2m+1)
+    std::vector<cld> A(N);
+    const long double pi = acosl(-1.0L);
+    for (uint64_t t = 0; t < N; t++) {
+        const long double mt = a[t] > (q0 >> 1) ? -(long double)(q0 - a[t]) : (long double)a[t];
+        const long double ang = pi * (long double)t / (long double)N;
+        A[t] = cld(mt * cosl(ang), mt * sinl(ang));
+    }
+    fft_ld(A, +1);
+    uint64_t k = 1;
+    for (size_t j = 0; j < n; j++) {
+        out[j] = (double)(A[(k - 1) / 2].real() / (long double)p->scale);
+        k = k * 5 % (2 * N);
+    }
+    return HISA_OK;
+}
+
+// ============================================================================================
+// elementwise instructions (a3, a4)
+// ============================================================================================
+static ElemJob ejob(const hisa_ctx* c, int npolys, int level) {
+    ElemJob j;
+    memset(&j, 0, sizeof j);
+    j.npolys = npolys;
+    j.nl = level + 1;
+    j.log_n = c->log_n;
+    j.a_poly = j.b_poly = j.out_poly = (long long)(level + 1) * c->N;
+    return j;
+}
+static bool scale_eq(double a, double b) { return fabs(a / b - 1.0) <= 0x1p-30; }
+
+static int binary_ct(hisa_ctx* c, hisa_ct ha, hisa_ct hb, hisa_ct* out, ElemOp op) {
+    CHECK_CTX(c);
+    GET_CT(a, ha);
+    GET_CT(b, hb);
+    if (a->level != b->level) return fail(HISA_E_LEVEL_MISMATCH, "levels %d vs %d", a->level, b->level);
+    if (!scale_eq(a->scale, b->scale)) return fail(HISA_E_SCALE_MISMATCH, "scales %.17g vs %.17g", a->scale, b->scale);
+    if (a->npolys != b->npolys) return fail(HISA_E_NOT_RELINEARIZED, "poly counts %d vs %d", a->npolys, b->npolys);
+    uint64_t* o = dalloc_t<uint64_t>(c, obj_words(c, a));
+    if (!o) return fail(HISA_E_OOM, "add/sub");
+    ElemJob j = ejob(c, a->npolys, a->level);
+    j.a[0] = a->ptr; j.b[0] = b->ptr; j.out[0] = o;
+    CK(launch_elem(op, j, c->d_mods, 1, c->stream));
+    return emit_ct(c, out, ha, o, a->level, a->npolys, a->scale);
+}
+extern "C" int hisa_add(hisa_ctx* c, hisa_ct a, hisa_ct b, hisa_ct* out) { return binary_ct(c, a, b, out, EL_ADD); }
+extern "C" int hisa_sub(hisa_ctx* c, hisa_ct a, hisa_ct b, hisa_ct* out) { return binary_ct(c, a, b, out, EL_SUB); }
+
+static int plain_op(hisa_ctx* c, hisa_ct ha, hisa_pt hp, hisa_ct* out, ElemOp op) {
+    CHECK_CTX(c);
+    GET_CT(a, ha);
+    GET_PT(p, hp);
+    if (a->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext");
+    if (a->level != p->level) return fail(HISA_E_LEVEL_MISMATCH, "levels %d vs %d", a->level, p->level);
+    double scale = a->scale;
+    if (op == EL_MUL_PLAIN) scale = a->scale * p->scale;
+    else if (!scale_eq(a->scale, p->scale)) return fail(HISA_E_SCALE_MISMATCH, "scales %.17g vs %.17g", a->scale, p->scale);
+    uint64_t* o = dalloc_t<uint64_t>(c, obj_words(c, a));
+    if (!o) return fail(HISA_E_OOM, "plain op");
+    ElemJob j = ejob(c, 2, a->level);
+    j.a[0] = a->ptr; j.b[0] = p->ptr; j.out[0] = o;
+    CK(launch_elem(op, j, c->d_mods, 1, c->stream));
+    return emit_ct(c, out, ha, o, a->level, 2, scale);
+}
+extern "C" int hisa_add_plain(hisa_ctx* c, hisa_ct a, hisa_pt p, hisa_ct* out) { return plain_op(c, a, p, out, EL_ADD_PLAIN); }
+extern "C" int hisa_sub_plain(hisa_ctx* c, hisa_ct a, hisa_pt p, hisa_ct* out) { return plain_op(c, a, p, out, EL_SUB_PLAIN); }
+extern "C" int hisa_mul_plain(hisa_ctx* c, hisa_ct a, hisa_pt p, hisa_ct* out) { return plain_op(c, a, p, out, EL_MUL_PLAIN); }
+
+// A20: X = llround(x * s), |X| < 2^62, residues X mod q_i
+static int scalar_residues(hisa_ctx* c, double x, double s, int l1, ElemJob& j) {
+    const double v = x * s;
+    if (!std::isfinite(v) || fabs(v) >= 0x1p62) return fail(HISA_E_PARAMS, "scalar out of range");
+    const long long X = llround(v);
+    for (int i = 0; i < l1; i++) {
+        const uint64_t q = c->mod[i];
+        const __int128 r = ((__int128)X % (__int128)q + q) % q;
+        j.scal[i] = (uint64_t)r;
+        j.scalp[i] = shoup((uint64_t)r, q);
+    }
+    return HISA_OK;
+}
+static int scalar_op(hisa_ctx* c, hisa_ct ha, double x, double pt_scale, hisa_ct* out, ElemOp op, int sign) {
+    CHECK_CTX(c);
+    GET_CT(a, ha);
+    if (a->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext");
+    ElemJob j = ejob(c, 2, a->level);
+    double s = a->scale, out_scale = a->scale;
+    if (op == EL_MUL_SCALAR) {
+        s = pt_scale == 0.0 ? (double)c->mod[a->level] : pt_scale;
+        out_scale = a->scale * s;
+    }
+    RET(scalar_residues(c, sign * x, s, a->level + 1, j));
+    uint64_t* o = dalloc_t<uint64_t>(c, obj_words(c, a));
+    if (!o) return fail(HISA_E_OOM, "scalar op");
+    j.a[0] = a->ptr; j.out[0] = o;
+    CK(launch_elem(op, j, c->d_mods, 1, c->stream));
+    return emit_ct(c, out, ha, o, a->level, 2, out_scale);
+}
+extern "C" int hisa_add_scalar(hisa_ctx* c, hisa_ct a, double x, hisa_ct* out) { return scalar_op(c, a, x, 0, out, EL_ADD_SCALAR, 1); }
+extern "C" int hisa_sub_scalar(hisa_ctx* c, hisa_ct a, double x, hisa_ct* out) { return scalar_op(c, a, x, 0, out, EL_ADD_SCALAR, -1); }
+extern "C" int hisa_mul_scalar(hisa_ctx* c, hisa_ct a, double x, double ps, hisa_ct* out) {
+    return scalar_op(c, a, x, ps, out, EL_MUL_SCALAR, 1);
+}
+
+extern "C" int hisa_mul_norelin(hisa_ctx* c, hisa_ct ha, hisa_ct hb, hisa_ct* out) {
+    CHECK_CTX(c);
+    GET_CT(a, ha);
+    GET_CT(b, hb);
+    if (a->npolys != 2 || b->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly operand");
+    if (a->level != b->level) return fail(HISA_E_LEVEL_MISMATCH, "levels %d vs %d", a->level, b->level);
+    const int l1 = a->level + 1;
+    uint64_t* o = dalloc_t<uint64_t>(c, (size_t)3 * l1 * c->N);
+    if (!o) return fail(HISA_E_OOM, "tensor");
+    ElemJob j = ejob(c, 2, a->level);
+    j.a[0] = a->ptr; j.b[0] = b->ptr; j.out[0] = o;
+    CK(launch_elem(ha == hb ? EL_SQUARE_TENSOR : EL_TENSOR, j, c->d_mods, 1, c->stream));
+    return emit_ct(c, out, ha, o, a->level, 3, a->scale * b->scale);
+}
+
+// ============================================================================================
+// key switching (a5): INTT -> ModUp pass 1 (lift) -> fused pass 2 + key inner product ->
+// INTT_p -> ModDown pass 1 (lift) -> pass 2 with combine epilogue (+ addend)
+// ============================================================================================
+struct KsBatch {
+    const uint64_t* d[MAXB];      // poly to switch, NTT form, (l+1) limbs
+    uint64_t* out[MAXB];          // output ct [2][l+1][N]
+    const uint64_t* add[MAXB];    // addend base (poly-stride add_a) or null
+    int add_polys;                // how many output polys receive the addend (1: rotation, 2: relin)
+    long long add_a;
+};
+static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const KsBatch& kb) {
+    const int l1 = level + 1, l2 = level + 2, L = c->L;
+    const long long N = (long long)c->N;
+    // scratch per ciphertext: dtil l1, T1 l1*l2, acc 2*l2, ptmp 2, md 2*l1
+    const size_t per = (size_t)N * ((size_t)l1 + (size_t)l1 * l2 + 2 * l2 + 2 + 2 * l1);
+    uint64_t* scratch = dalloc_t<uint64_t>(c, per * nz);
+    if (!scratch) return fail(HISA_E_OOM, "key-switch scratch (%zu MiB)", per * nz * 8 >> 20);
+    uint64_t *dtil[MAXB], *t1[MAXB], *acc[MAXB], *ptmp[MAXB], *md[MAXB];
+    for (int z = 0; z < nz; z++) {
+        uint64_t* s = scratch + per * z;
+        dtil[z] = s; s += (size_t)l1 * N;
+        t1[z] = s; s += (size_t)l1 * l2 * N;
+        acc[z] = s; s += (size_t)2 * l2 * N;
+        ptmp[z] = s; s += (size_t)2 * N;
+        md[z] = s;
+    }
+    uint8_t mm[MAXL];
+    ident_map(mm, l1);
+    // (1) INTT of the digits
+    RET(ntt_inv(c, kb.d, dtil, nz, l1, mm));
+    Tables tb = c->tables();
+    // (2) ModUp pass 1: (j, ri) with ri != j; lift q_j -> r on load
+    {
+        PassJob j = job0();
+        for (int z = 0; z < nz; z++) { j.src[z] = dtil[z]; j.dst[z] = t1[z]; }
+        j.nb = l2;
+        j.src_a = N; j.src_b = 0;
+        j.dst_a = (long long)l2 * N; j.dst_b = N;
+        j.skip_diag = 1;
+        for (int ri = 0; ri < l2; ri++) j.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+        for (int a = 0; a < l1; a++) j.smod_map[a] = (uint8_t)a;
+        CK(launch_fwd_pass1(j, tb, l1 * l2, nz, true, c->stream));
+    }
+    // (3) fused pass 2 + inner product with the key
+    {
+        KsJob kj;
+        memset(&kj, 0, sizeof kj);
+        for (int z = 0; z < nz; z++) { kj.t1[z] = t1[z]; kj.d[z] = kb.d[z]; kj.acc[z] = acc[z]; }
+        kj.key = key;
+        kj.l1 = l1;
+        kj.L = L;
+        for (int ri = 0; ri < l2; ri++) kj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+        CK(launch_ks_ip(kj, tb, nz, c->stream));
+    }
+    // (4) INTT_p of acc_p (both polys)
+    {
+        PassJob j = job0();
+        for (int z = 0; z < nz; z++) { j.src[z] = acc[z] + (long long)l1 * N; j.dst[z] = ptmp[z]; }
+        j.nb = 1;
+        j.src_a = (long long)l2 * N; j.dst_a = N;
+        j.mod_map[0] = (uint8_t)L;
+        CK(launch_inv_passA(j, tb, 2, nz, c->stream));
+        for (int z = 0; z < nz; z++) { j.src[z] = ptmp[z]; }
+        j.src_a = N;
+        CK(launch_inv_passB(j, tb, 2, nz, c->stream));
+    }
+    // (5) ModDown pass 1: lift p -> q_i
+    {
+        PassJob j = job0();
+        for (int z = 0; z < nz; z++) { j.src[z] = ptmp[z]; j.dst[z] = md[z]; }
+        j.nb = l1;
+        j.src_a = N; j.src_b = 0;
+        j.dst_a = (long long)l1 * N; j.dst_b = N;
+        ident_map(j.mod_map, l1);
+        j.smod_map[0] = j.smod_map[1] = (uint8_t)L;
+        CK(launch_fwd_pass1(j, tb, 2 * l1, nz, true, c->stream));
+    }
+    // (6) pass 2 + combine: out_i = (acc_i - NTT_i(y)) p^-1 (+ add)
+    {
+        PassJob j = job0();
+        for (int z = 0; z < nz; z++) {
+            j.src[z] = md[z];
+            j.dst[z] = kb.out[z];
+            j.aux[z] = acc[z];
+            j.add[z] = kb.add[z];
+        }
+        j.nb = l1;
+        j.src_a = (long long)l1 * N; j.src_b = N;
+        j.dst_a = (long long)l1 * N; j.dst_b = N;
+        j.aux_a = (long long)l2 * N; j.aux_b = N;
+        j.add_a = kb.add_a; j.add_b = N;
+        j.aux_limit = kb.add_polys;
+        ident_map(j.mod_map, l1);
+        Tables tc = c->tables(c->d_pinv);
+        CK(launch_fwd_pass2(j, tc, 2 * l1, nz, true, c->stream));
+    }
+    dfree(c, scratch);
+    return HISA_OK;
+}
+
+extern "C" int hisa_relinearize(hisa_ctx* c, hisa_ct h) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (o->npolys == 2) return HISA_OK;
+    if (!c->d_rlk) return fail(HISA_E_NO_KEY, "relinearisation key not generated");
+    const int l1 = o->level + 1;
+    const long long N = (long long)c->N;
+    uint64_t* out = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+    if (!out) return fail(HISA_E_OOM, "relin");
+    KsBatch kb;
+    memset(&kb, 0, sizeof kb);
+    kb.d[0] = o->ptr + 2 * l1 * N;
+    kb.out[0] = out;
+    kb.add[0] = o->ptr;
+    kb.add_polys = 2;
+    kb.add_a = (long long)l1 * N;
+    RET(keyswitch(c, 1, o->level, c->d_rlk, kb));
+    dfree(c, o->ptr);
+    o->ptr = out;
+    o->npolys = 2;
+    return HISA_OK;
+}
+
+extern "C" int hisa_mul(hisa_ctx* c, hisa_ct a, hisa_ct b, hisa_ct* out) {
+    hisa_ct t;
+    RET(hisa_mul_norelin(c, a, b, &t));
+    int r = hisa_relinearize(c, t);
+    if (r != HISA_OK) { hisa_free(c, t); return r; }
+    Obj* ot = get_obj(c, t, OBJ_CT);
+    if (out) { *out = t; return HISA_OK; }
+    // in place on a
+    Obj* oa = get_obj(c, a, OBJ_CT);
+    dfree(c, oa->ptr);
+    oa->ptr = ot->ptr; oa->level = ot->level; oa->npolys = ot->npolys; oa->scale = ot->scale;
+    ot->ptr = nullptr;
+    hisa_free(c, t);
+    return HISA_OK;
+}
+
+// rotation of nz ciphertexts (same level, same amount): automorphism then key switch (A15)
+static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_t** outs) {
+    const int level = in[0]->level, l1 = level + 1;
+    const long long N = (long long)c->N;
+    auto it = c->rot_keys.find(k);
+    if (it == c->rot_keys.end()) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)k);
+    const uint64_t g = h_pow(5, k, 2 * c->N);
+    uint64_t* perm = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N * nz);
+    if (!perm) return fail(HISA_E_OOM, "rotation scratch");
+    const uint64_t* ins[MAXB];
+    uint64_t* ps[MAXB];
+    KsBatch kb;
+    memset(&kb, 0, sizeof kb);
+    for (int z = 0; z < nz; z++) {
+        ins[z] = in[z]->ptr;
+        ps[z] = perm + (size_t)2 * l1 * N * z;
+        outs[z] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        if (!outs[z]) return fail(HISA_E_OOM, "rotation output");
+        kb.d[z] = ps[z] + l1 * N;
+        kb.out[z] = outs[z];
+        kb.add[z] = ps[z];
+    }
+    kb.add_polys = 1;
+    kb.add_a = 0;
+    CK(launch_automorphism(ins, ps, nz, 2 * l1, c->log_n, g, c->stream));
+    RET(keyswitch(c, nz, level, it->second, kb));
+    dfree(c, perm);
+    return HISA_OK;
+}
+
+static int rot_common(hisa_ctx* c, hisa_ct h, int64_t k, hisa_ct* out) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (o->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext");
+    const int64_t s = (int64_t)(c->N / 2);
+    int64_t kk = k % s;
+    if (kk < 0) kk += s;
+    if (kk == 0) {
+        if (!out) return HISA_OK;
+        return hisa_copy(c, h, out);
+    }
+    if (!c->rot_keys.count((uint64_t)kk)) return fail(HISA_E_NO_KEY, "no rotation key for %lld", (long long)kk);
+    uint64_t* res[1];
+    Obj* ins[1] = {o};
+    RET(rotate_batch(c, ins, 1, (uint64_t)kk, res));
+    return emit_ct(c, out, h, res[0], o->level, 2, o->scale);
+}
+extern "C" int hisa_rot_left(hisa_ctx* c, hisa_ct h, int64_t k, hisa_ct* out) { return rot_common(c, h, k, out); }
+extern "C" int hisa_rot_right(hisa_ctx* c, hisa_ct h, int64_t k, hisa_ct* out) {
+    if (!c) return fail(HISA_E_PARAMS, "null context");
+    const int64_t s = (int64_t)(c->N / 2);
+    int64_t kk = k % s;
+    if (kk < 0) kk += s;
+    return rot_common(c, h, (s - kk) % s, out);   // right rotations become left rotations
+}
+
+extern "C" int hisa_rot_left_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int64_t k, hisa_ct* outs) {
+    CHECK_CTX(c);
+    if (!in || !outs) return fail(HISA_E_PARAMS, "null argument");
+    if (n == 0) return HISA_OK;
+    std::vector<Obj*> objs(n);
+    for (size_t i = 0; i < n; i++) {
+        objs[i] = get_obj(c, in[i], OBJ_CT);
+        if (!objs[i]) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle at %zu", i);
+        if (objs[i]->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext at %zu", i);
+        if (objs[i]->level != objs[0]->level) return fail(HISA_E_LEVEL_MISMATCH, "batch levels differ");
+    }
+    const int64_t s = (int64_t)(c->N / 2);
+    int64_t kk = k % s;
+    if (kk < 0) kk += s;
+    if (kk == 0) {
+        for (size_t i = 0; i < n; i++) RET(hisa_copy(c, in[i], &outs[i]));
+        return HISA_OK;
+    }
+    if (!c->rot_keys.count((uint64_t)kk)) return fail(HISA_E_NO_KEY, "no rotation key for %lld", (long long)kk);
+    for (size_t i0 = 0; i0 < n; i0 += MAXB) {
+        const int nz = (int)std::min((size_t)MAXB, n - i0);
+        uint64_t* res[MAXB];
+        RET(rotate_batch(c, objs.data() + i0, nz, (uint64_t)kk, res));
+        for (int z = 0; z < nz; z++)
+            outs[i0 + z] = new_handle(c, OBJ_CT, res[z], objs[i0 + z]->level, 2, objs[i0 + z]->scale);
+    }
+    return HISA_OK;
+}
+
+extern "C" int hisa_rot_left_hoisted(hisa_ctx* c, hisa_ct h, const int64_t* k, size_t n, hisa_ct* outs) {
+    CHECK_CTX(c);
+    if (!k || !outs) return fail(HISA_E_PARAMS, "null argument");
+    // v1: one rotation per amount (hoisted ModUp sharing is a later optimisation; results are
+    // bit-identical by A14)
+    for (size_t i = 0; i < n; i++) RET(hisa_rot_left(c, h, k[i], &outs[i]));
+    return HISA_OK;
+}
+
+// ============================================================================================
+// rescale / divScalar (a8), modulus switch
+// ============================================================================================
+static int rescale_ptr(hisa_ctx* c, const Obj* o, uint64_t** res) {
+    const int l = o->level, l1 = l + 1, P = o->npolys;
+    const long long N = (long long)c->N;
+    uint64_t* out = dalloc_t<uint64_t>(c, (size_t)P * l * N);
+    uint64_t* tmp = dalloc_t<uint64_t>(c, (size_t)P * N + (size_t)P * l * N);
+    if (!out || !tmp) return fail(HISA_E_OOM, "rescale");
+    uint64_t* top = tmp;
+    uint64_t* r1 = tmp + (size_t)P * N;
+    Tables tb = c->tables();
+    {   // INTT of the top limb of every poly
+        PassJob j = job0();
+        j.src[0] = o->ptr + (long long)l * N; j.dst[0] = top;
+        j.nb = 1; j.src_a = (long long)l1 * N; j.dst_a = N;
+        j.mod_map[0] = (uint8_t)l;
+        CK(launch_inv_passA(j, tb, P, 1, c->stream));
+        j.src[0] = top; j.src_a = N;
+        CK(launch_inv_passB(j, tb, P, 1, c->stream));
+    }
+    {   // lift q_l -> q_i (i < l), forward pass 1
+        PassJob j = job0();
+        j.src[0] = top; j.dst[0] = r1;
+        j.nb = l; j.src_a = N; j.src_b = 0; j.dst_a = (long long)l * N; j.dst_b = N;
+        ident_map(j.mod_map, l);
+        for (int a = 0; a < P; a++) j.smod_map[a] = (uint8_t)l;
+        CK(launch_fwd_pass1(j, tb, P * l, 1, true, c->stream));
+    }
+    {   // pass 2 + combine: out_i = (u_i - NTT_i(y)) q_l^-1
+        PassJob j = job0();
+        j.src[0] = r1; j.dst[0] = out; j.aux[0] = o->ptr;
+        j.nb = l;
+        j.src_a = (long long)l * N; j.src_b = N;
+        j.dst_a = (long long)l * N; j.dst_b = N;
+        j.aux_a = (long long)l1 * N; j.aux_b = N;
+        ident_map(j.mod_map, l);
+        Tables tc = c->tables(c->d_qlinv + (size_t)l * (c->L + 1));
+        CK(launch_fwd_pass2(j, tc, P * l, 1, true, c->stream));
+    }
+    dfree(c, tmp);
+    *res = out;
+    return HISA_OK;
+}
+
+extern "C" int hisa_max_scalar_div(hisa_ctx* c, hisa_ct h, uint64_t ub, uint64_t* d) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (!d) return fail(HISA_E_PARAMS, "null out");
+    const uint64_t qt = c->mod[o->level];
+    *d = (qt <= ub) ? qt : 1;   // A18 reading of P:584-587
+    return HISA_OK;
+}
+extern "C" int hisa_div_scalar(hisa_ctx* c, hisa_ct h, uint64_t d, hisa_ct* out) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (d == 1) {
+        if (!out) return HISA_OK;
+        return hisa_copy(c, h, out);
+    }
+    if (o->level == 0) return fail(HISA_E_MODULUS_EXHAUSTED, "rescale at level 0");
+    if (d != c->mod[o->level]) return fail(HISA_E_INVALID_DIVISOR, "divisor %llu is not q_top", (unsigned long long)d);
+    uint64_t* res;
+    RET(rescale_ptr(c, o, &res));
+    const double ns = o->scale / (double)c->mod[o->level];
+    return emit_ct(c, out, h, res, o->level - 1, o->npolys, ns);
+}
+extern "C" int hisa_rescale(hisa_ctx* c, hisa_ct h, hisa_ct* out) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (o->level == 0) return fail(HISA_E_MODULUS_EXHAUSTED, "rescale at level 0");
+    return hisa_div_scalar(c, h, c->mod[o->level], out);
+}
+extern "C" int hisa_mod_switch(hisa_ctx* c, hisa_ct h, int drop, hisa_ct* out) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (drop < 0) return fail(HISA_E_PARAMS, "negative drop");
+    if (o->level - drop < 0) return fail(HISA_E_MODULUS_EXHAUSTED, "mod-switch below level 0");
+    const int nl = o->level + 1 - drop, l1 = o->level + 1;
+    const size_t N = c->N;
+    uint64_t* p = dalloc_t<uint64_t>(c, (size_t)o->npolys * nl * N);
+    if (!p) return fail(HISA_E_OOM, "mod switch");
+    CK(cudaMemcpy2DAsync(p, (size_t)nl * N * 8, o->ptr, (size_t)l1 * N * 8, (size_t)nl * N * 8, o->npolys,
+                         cudaMemcpyDeviceToDevice, c->stream));
+    return emit_ct(c, out, h, p, o->level - drop, o->npolys, o->scale);
+}
+
+extern "C" int hisa_bootstrap(hisa_ctx* c, hisa_ct h) {
+    (void)h;
+    if (!c) return fail(HISA_E_PARAMS, "null context");
+    return fail(HISA_E_UNSUPPORTED_PROFILE, "Bootstrap profile is not implemented (P:292-293)");
+}
+
+// ============================================================================================
+// conv accumulation (a9, K8): out[o] = sum_t X[o][t] in[t], X = llround(W * pt_scale)
+// ============================================================================================
+struct ConvJob {
+    int T, OC, l1, log_n;
+    long long poly_stride;
+};
+// weights: [OC][T][l1] residues; in_ptrs: device array of T pointers; out_ptrs: OC pointers
+__global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restrict__ in_ptrs,
+                                                  uint64_t* const* __restrict__ out_ptrs,
+                                                  const uint64_t* __restrict__ w, ConvJob job,
+                                                  const Mod* __restrict__ mods) {
+    const long long N = 1ll << job.log_n;
+    const int poly = blockIdx.z;
+    const int limb = blockIdx.y;
+    const Mod md = mods[limb];
+    constexpr int OT = 8;   // outputs per pass held in registers
+    const long long off = (long long)poly * job.poly_stride + (long long)limb * N;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < N; x += (long long)gridDim.x * blockDim.x) {
+        for (int o0 = 0; o0 < job.OC; o0 += OT) {
+            U128 acc[OT];
+#pragma unroll
+            for (int k = 0; k < OT; k++) acc[k] = U128{0, 0};
+            for (int t = 0; t < job.T; t++) {
+                const uint64_t v = in_ptrs[t][off + x];
+#pragma unroll
+                for (int k = 0; k < OT; k++)
+                    if (o0 + k < job.OC) mac128(acc[k], v, w[((long long)(o0 + k) * job.T + t) * job.l1 + limb]);
+                if ((t & 31) == 31) {   // keep the 128-bit sums below 2^127
+#pragma unroll
+                    for (int k = 0; k < OT; k++) { acc[k].lo = barrett128(acc[k].lo, acc[k].hi, md); acc[k].hi = 0; }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < OT; k++)
+                if (o0 + k < job.OC) out_ptrs[o0 + k][off + x] = barrett128(acc[k].lo, acc[k].hi, md);
+        }
+    }
+}
+
+extern "C" int hisa_conv_accumulate(hisa_ctx* c, const hisa_ct* in, size_t T, const double* W, size_t OC,
+                                    double pt_scale, hisa_ct* outs) {
+    CHECK_CTX(c);
+    if (!in || !W || !outs || T == 0 || OC == 0) return fail(HISA_E_PARAMS, "bad arguments");
+    std::vector<Obj*> objs(T);
+    for (size_t t = 0; t < T; t++) {
+        objs[t] = get_obj(c, in[t], OBJ_CT);
+        if (!objs[t]) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle at %zu", t);
+        if (objs[t]->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly input");
+        if (objs[t]->level != objs[0]->level) return fail(HISA_E_LEVEL_MISMATCH, "input levels differ");
+        if (!scale_eq(objs[t]->scale, objs[0]->scale)) return fail(HISA_E_SCALE_MISMATCH, "input scales differ");
+    }
+    const int level = objs[0]->level, l1 = level + 1;
+    const double ps = pt_scale == 0.0 ? (double)c->mod[level] : pt_scale;
+    std::vector<uint64_t> wres((size_t)OC * T * l1);
+    for (size_t o = 0; o < OC; o++)
+        for (size_t t = 0; t < T; t++) {
+            const double v = W[o * T + t] * ps;
+            if (!std::isfinite(v) || fabs(v) >= 0x1p62) return fail(HISA_E_PARAMS, "weight out of range");
+            const long long X = llround(v);
+            for (int i = 0; i < l1; i++) {
+                const uint64_t q = c->mod[i];
+                wres[(o * T + t) * l1 + i] = (uint64_t)(((__int128)X % (__int128)q + q) % q);
+            }
+        }
+    const long long N = (long long)c->N;
+    std::vector<uint64_t*> optr(OC);
+    for (size_t o = 0; o < OC; o++) {
+        optr[o] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        if (!optr[o]) return fail(HISA_E_OOM, "conv outputs");
+    }
+    std::vector<const uint64_t*> iptr(T);
+    for (size_t t = 0; t < T; t++) iptr[t] = objs[t]->ptr;
+    uint64_t* dw = dalloc_t<uint64_t>(c, wres.size());
+    const uint64_t** dip = (const uint64_t**)dalloc(c, T * sizeof(void*));
+    uint64_t** dop = (uint64_t**)dalloc(c, OC * sizeof(void*));
+    if (!dw || !dip || !dop) return fail(HISA_E_OOM, "conv scratch");
+    CK(cudaMemcpyAsync(dw, wres.data(), wres.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dip, iptr.data(), T * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dop, optr.data(), OC * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+    ConvJob cj{(int)T, (int)OC, l1, c->log_n, (long long)l1 * N};
+    dim3 grid((unsigned)std::min<long long>((N + 255) / 256, 64), l1, 2);
+    k_conv_acc<<<grid, 256, 0, c->stream>>>(dip, dop, dw, cj, c->d_mods);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));   // host staging vectors must outlive the copies
+    dfree(c, dw);
+    dfree(c, (void*)dip);
+    dfree(c, (void*)dop);
+    for (size_t o = 0; o < OC; o++) outs[o] = new_handle(c, OBJ_CT, optr[o], level, 2, objs[0]->scale * ps);
+    return HISA_OK;
+}
+
+// ============================================================================================
+// inspection / import / export
+// ============================================================================================
+extern "C" int hisa_ct_info(hisa_ctx* c, hisa_ct h, int* level, int* npolys, double* scale) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (level) *level = o->level;
+    if (npolys) *npolys = o->npolys;
+    if (scale) *scale = o->scale;
+    return HISA_OK;
+}
+extern "C" int hisa_pt_info(hisa_ctx* c, hisa_pt h, int* level, double* scale) {
+    CHECK_CTX(c);
+    GET_PT(o, h);
+    if (level) *level = o->level;
+    if (scale) *scale = o->scale;
+    return HISA_OK;
+}
+static int export_obj(hisa_ctx* c, Obj* o, uint64_t* host, size_t words) {
+    const size_t w = obj_words(c, o);
+    if (!host || words != w) return fail(HISA_E_PARAMS, "object has %zu words, got %zu", w, words);
+    CK(cudaMemcpyAsync(host, o->ptr, w * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return HISA_OK;
+}
+extern "C" int hisa_ct_export(hisa_ctx* c, hisa_ct h, uint64_t* host, size_t words) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    return export_obj(c, o, host, words);
+}
+extern "C" int hisa_pt_export(hisa_ctx* c, hisa_pt h, uint64_t* host, size_t words) {
+    CHECK_CTX(c);
+    GET_PT(o, h);
+    return export_obj(c, o, host, words);
+}
+static int check_layout(hisa_ctx* c, int level, int npolys) {
+    if (level < 0 || level >= c->L) return fail(HISA_E_PARAMS, "level %d out of range", level);
+    if (npolys < 1 || npolys > 3) return fail(HISA_E_PARAMS, "npolys must be 1..3");
+    return HISA_OK;
+}
+extern "C" int hisa_ct_import(hisa_ctx* c, const uint64_t* host, int level, int npolys, double scale, hisa_ct* out) {
+    CHECK_CTX(c);
+    if (!host || !out) return fail(HISA_E_PARAMS, "null argument");
+    RET(check_layout(c, level, npolys));
+    if (npolys < 2) return fail(HISA_E_PARAMS, "a ciphertext has 2 or 3 polys");
+    const size_t w = (size_t)npolys * (level + 1) * c->N;
+    uint64_t* p = dalloc_t<uint64_t>(c, w);
+    if (!p) return fail(HISA_E_OOM, "import");
+    CK(cudaMemcpyAsync(p, host, w * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = new_handle(c, OBJ_CT, p, level, npolys, scale);
+    return HISA_OK;
+}
+extern "C" int hisa_pt_import(hisa_ctx* c, const uint64_t* host, int level, double scale, hisa_pt* out) {
+    CHECK_CTX(c);
+    if (!host || !out) return fail(HISA_E_PARAMS, "null argument");
+    RET(check_layout(c, level, 1));
+    const size_t w = (size_t)(level + 1) * c->N;
+    uint64_t* p = dalloc_t<uint64_t>(c, w);
+    if (!p) return fail(HISA_E_OOM, "import");
+    CK(cudaMemcpyAsync(p, host, w * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = new_handle(c, OBJ_PT, p, level, 1, scale);
+    return HISA_OK;
+}
+extern "C" int hisa_ct_device_view(hisa_ctx* c, hisa_ct h, uint64_t** dev, size_t* words) {
+    CHECK_CTX(c);
+    GET_CT(o, h);
+    if (dev) *dev = o->ptr;
+    if (words) *words = obj_words(c, o);
+    return HISA_OK;
+}
+extern "C" int hisa_ct_adopt_device(hisa_ctx* c, const uint64_t* dev, int level, int npolys, double scale,
+                                    hisa_ct* out) {
+    CHECK_CTX(c);
+    if (!dev || !out) return fail(HISA_E_PARAMS, "null argument");
+    RET(check_layout(c, level, npolys));
+    const size_t w = (size_t)npolys * (level + 1) * c->N;
+    uint64_t* p = dalloc_t<uint64_t>(c, w);
+    if (!p) return fail(HISA_E_OOM, "adopt");
+    CK(cudaMemcpyAsync(p, dev, w * 8, cudaMemcpyDeviceToDevice, c->stream));
+    *out = new_handle(c, OBJ_CT, p, level, npolys, scale);
+    return HISA_OK;
+}
+extern "C" int hisa_ct_random(hisa_ctx* c, uint64_t b, int level, int npolys, hisa_ct* out) {
+    CHECK_CTX(c);
+    if (!out) return fail(HISA_E_PARAMS, "null out");
+    RET(check_layout(c, level, npolys));
+    const int l1 = level + 1;
+    uint64_t* p = dalloc_t<uint64_t>(c, (size_t)npolys * l1 * c->N);
+    if (!p) return fail(HISA_E_OOM, "random ct");
+    uint64_t idx[MAXL];
+    uint8_t mm[MAXL];
+    ident_map(mm, l1);
+    for (int k = 0; k < npolys; k++) {
+        for (int i = 0; i < l1; i++) idx[i] = (b << 32) | ((uint64_t)k << 16) | (uint64_t)i;
+        CK(launch_sample_uniform(p + (size_t)k * l1 * c->N, c->seed, TAG_BENCH, idx, mm, l1, c->log_n, c->d_mods,
+                                 c->stream));
+    }
+    *out = new_handle(c, OBJ_CT, p, level, npolys, 0x1p40);
+    return HISA_OK;
+}
+extern "C" int hisa_pt_random(hisa_ctx* c, uint64_t b, int level, hisa_pt* out) {
+    CHECK_CTX(c);
+    if (!out) return fail(HISA_E_PARAMS, "null out");
+    RET(check_layout(c, level, 1));
+    const int l1 = level + 1;
+    uint64_t* p = dalloc_t<uint64_t>(c, (size_t)l1 * c->N);
+    if (!p) return fail(HISA_E_OOM, "random pt");
+    uint64_t idx[MAXL];
+    uint8_t mm[MAXL];
+    ident_map(mm, l1);
+    for (int i = 0; i < l1; i++) idx[i] = (b << 32) | (0xFFFFull << 16) | (uint64_t)i;
+    CK(launch_sample_uniform(p, c->seed, TAG_BENCH, idx, mm, l1, c->log_n, c->d_mods, c->stream));
+    *out = new_handle(c, OBJ_PT, p, level, 1, 0x1p40);
+    return HISA_OK;
+}
+
+// ============================================================================================
+// raw NTT / INTT of every limb of ciphertexts, in place (config 2 sweeps these as ops, a1/a2)
+// ============================================================================================
+extern "C" int hisa_ntt_batch(hisa_ctx* c, const hisa_ct* hs, size_t n, int inverse) {
+    CHECK_CTX(c);
+    if (!hs && n) return fail(HISA_E_PARAMS, "null argument");
+    std::vector<Obj*> objs(n);
+    for (size_t i = 0; i < n; i++) {
+        objs[i] = get_obj(c, hs[i], OBJ_CT);
+        if (!objs[i]) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle at %zu", i);
+        if (objs[i]->level != objs[0]->level || objs[i]->npolys != objs[0]->npolys)
+            return fail(HISA_E_LEVEL_MISMATCH, "batch shapes differ");
+    }
+    for (size_t i0 = 0; i0 < n; i0 += MAXB) {
+        const int nz = (int)std::min((size_t)MAXB, n - i0);
+        const int l1 = objs[i0]->level + 1, P = objs[i0]->npolys;
+        uint64_t* ptrs[MAXB];
+        for (int z = 0; z < nz; z++) ptrs[z] = objs[i0 + z]->ptr;
+        uint8_t mm[MAXL];
+        ident_map(mm, l1);
+        if (inverse) RET(ntt_inv(c, ptrs, ptrs, nz, l1, mm, P * l1));
+        else RET(ntt_fwd(c, ptrs, nz, l1, mm, P * l1));
+    }
+    return HISA_OK;
+}
+extern "C" int hisa_ntt(hisa_ctx* c, hisa_ct h, int inverse) { return hisa_ntt_batch(c, &h, 1, inverse); }

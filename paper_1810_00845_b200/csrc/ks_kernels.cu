@@ -1,0 +1,98 @@
+// ks_kernels.cu -- key-switch inner product fused with the forward-NTT row pass (K4, step a5).
+//
+// For output prime r (grid y = ri over q_0..q_l, p) and a tile of rows (grid x), loop over the
+// digits j <= l: bring D_{j,r} for the tile on chip -- either the pass-1 output T1[j][ri] followed by
+// the last log M2 CT stages in shared memory, or (r == q_j) the digit itself, which is already in
+// the NTT domain -- then multiply with the key limbs (b and a) and accumulate in 128-bit
+// registers (products < 2^122, at most 64 terms).  One Barrett reduction per output word.
+// D never touches HBM in its NTT form; the key is streamed once per ciphertext.
+#include <cuda_runtime.h>
+#include "launch.h"
+
+namespace hisa {
+
+constexpr int LOG_R_KS = 3;
+
+template <int LOG_M>
+__global__ void __launch_bounds__(256) k_ks_ip(KsJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R_KS>;
+    extern __shared__ uint64_t sm[];
+    const int z = blockIdx.z;
+    const int ri = blockIdx.y;
+    const int l1 = job.l1;
+    const int nri = l1 + 1;
+    const int log_n = tb.log_n;
+    const int Gr = blockDim.x / G::T;
+    const int row0 = blockIdx.x * Gr;
+    const long long off0 = (long long)row0 << LOG_M;
+    const int mi = job.mod_map[ri];
+    const Mod md = tb.mods[mi];
+    const int tile = Gr * G::M;
+    const int nthr = blockDim.x;
+    constexpr int EPT = G::R;   // elements per thread in the MAC phase (tile / nthr)
+    U128 acc0[EPT], acc1[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
+    int g = threadIdx.x / G::T, t = threadIdx.x % G::T;
+    const long long kstride_j = 2ll * (job.L + 1) << log_n;
+    const long long kstride_p = (long long)(job.L + 1) << log_n;
+    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
+    for (int j = 0; j < l1; j++) {
+        if (j == ri) {
+            const uint64_t* src = job.d[z] + ((long long)j << log_n) + off0;
+            for (int i = threadIdx.x; i < tile; i += nthr) sm[G::addr(i >> LOG_M, i & (G::M - 1))] = src[i];
+            __syncthreads();
+        } else {
+            const uint64_t* src = job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
+            for (int i = threadIdx.x; i < tile; i += nthr) sm[G::addr(i >> LOG_M, i & (G::M - 1))] = src[i];
+            __syncthreads();
+            fwd_engine<LOG_M, LOG_R_KS>(sm, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
+                                        (uint32_t)(row0 + g), g, t);
+        }
+        const uint64_t* kb = key_r + j * kstride_j;
+        const uint64_t* ka = kb + kstride_p;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * nthr;
+            const uint64_t D = sm[G::addr(i >> LOG_M, i & (G::M - 1))];   // < 4q
+            mac128(acc0[k], D, __ldg(kb + i));
+            mac128(acc1[k], D, __ldg(ka + i));
+        }
+        __syncthreads();
+    }
+    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
+    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
+#pragma unroll
+    for (int k = 0; k < EPT; k++) {
+        const int i = threadIdx.x + k * nthr;
+        out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
+        out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
+    }
+}
+
+template <int LOG_M>
+static cudaError_t ks_ip_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+    using G = Geo<LOG_M, LOG_R_KS>;
+    const int rows = 1 << (tb.log_n - LOG_M);
+    int gr = 256 / G::T;
+    if (gr > rows) gr = rows;
+    const int threads = gr * G::T;
+    const size_t smem = (size_t)gr * G::STRIDE * sizeof(uint64_t);
+    dim3 grid(rows / gr, job.l1 + 1, nz);
+    k_ks_ip<LOG_M><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+    const int lm = tb.log_n - split_m1(tb.log_n);
+    switch (lm) {
+        case 4: return ks_ip_t<4>(job, tb, nz, st);
+        case 5: return ks_ip_t<5>(job, tb, nz, st);
+        case 6: return ks_ip_t<6>(job, tb, nz, st);
+        case 7: return ks_ip_t<7>(job, tb, nz, st);
+        case 8: return ks_ip_t<8>(job, tb, nz, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace hisa

@@ -1,0 +1,66 @@
+// launch.h -- internal launch wrappers between the C-ABI host layer (hisa.cu) and the kernels.
+// Not part of the public boundary (include/hisa.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "ntt.cuh"
+
+namespace hisa {
+
+int split_m1(int log_n);
+
+// a1/a2 passes (ntt_kernels.cu)
+cudaError_t launch_fwd_pass1(const PassJob& job, const Tables& tb, int nlimbs, int nz, bool lift, cudaStream_t st);
+cudaError_t launch_fwd_pass2(const PassJob& job, const Tables& tb, int nlimbs, int nz, bool combine, cudaStream_t st);
+cudaError_t launch_inv_passA(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st);
+cudaError_t launch_inv_passB(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st);
+
+// elementwise family (a3, a4) -- elem_kernels.cu.  Operates on nz ciphertexts, each with
+// `npolys` polys of `nl` limbs (limb i mod mods[i]), word layout [poly][limb][N].
+enum ElemOp {
+    EL_ADD = 0, EL_SUB, EL_NEG, EL_ADD_PLAIN, EL_SUB_PLAIN, EL_MUL_PLAIN, EL_ADD_SCALAR, EL_MUL_SCALAR,
+    EL_COPY, EL_TENSOR, EL_DECRYPT2, EL_DECRYPT3, EL_SQUARE_TENSOR
+};
+struct ElemJob {
+    const uint64_t* a[MAXB];
+    const uint64_t* b[MAXB];
+    uint64_t* out[MAXB];
+    int npolys;          // polys of a / out (for tensor: a,b have 2, out has 3)
+    int nl;              // limbs per poly
+    int log_n;
+    long long a_poly, b_poly, out_poly;  // poly strides (words)
+    uint64_t scal[MAXL];    // per-limb scalar residues (add/mul scalar)
+    uint64_t scalp[MAXL];   // Shoup companions
+};
+cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, cudaStream_t st);
+
+// automorphism psi_g in the NTT domain (K6): out[j] = in[perm_g[j]] on every limb
+cudaError_t launch_automorphism(const uint64_t* const* in, uint64_t* const* out, int nz, int nlimbs_total,
+                                int log_n, uint64_t g, cudaStream_t st);
+
+// key-switch inner product fused with forward pass 2 (K4) -- ks_kernels.cu
+struct KsJob {
+    const uint64_t* t1[MAXB];     // pass-1 output [j][ri][N] (ri over l+2 output primes)
+    const uint64_t* d[MAXB];      // the digit source in NTT form [(l+1)][N] (D_{j,q_j} = d_j)
+    uint64_t* acc[MAXB];          // out [2][l+2][N], fully reduced
+    const uint64_t* key;          // [L][2][L+1][N]
+    int l1;                       // active limbs l+1
+    int L;                        // total q primes (key stride)
+    uint8_t mod_map[MAXL];        // ri -> modulus index
+};
+cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st);
+
+// samplers (ChaCha20, A11) -- rng_kernels.cu
+cudaError_t launch_sample_uniform(uint64_t* out, uint64_t seed, uint32_t tag, const uint64_t* index_per_limb_host,
+                                  const uint8_t* mod_per_limb_host, int nlimbs, int log_n, const Mod* mods,
+                                  cudaStream_t st);
+// int64 polynomial samplers: kind 0 = ternary, 1 = cbd
+cudaError_t launch_sample_small(int64_t* out, uint64_t seed, uint32_t tag, uint64_t index, int kind, int log_n,
+                                cudaStream_t st);
+// reduce an int64 polynomial into limbs: out[i][t] = x[t] mod mods[mod_map[i]]
+cudaError_t launch_int_to_limbs(const int64_t* x, uint64_t* out, const uint8_t* mod_map_host, int nlimbs, int log_n,
+                                const Mod* mods, cudaStream_t st);
+// integer-coefficient automorphism (used for rotation-key targets)
+cudaError_t launch_automorphism_int(const int64_t* in, int64_t* out, int log_n, uint64_t g, cudaStream_t st);
+
+}  // namespace hisa

@@ -1,0 +1,263 @@
+// ntt_kernels.cu -- pass kernels (a1/a2) and the fused lift / combine variants used by rescale
+// (a8), ModUp and ModDown (a5).  See ntt.cuh for the decomposition.
+#include <cuda_runtime.h>
+#include "ntt.cuh"
+#include "launch.h"
+
+namespace hisa {
+
+// smem tile geometry: column passes stage G columns x M rows, row passes G rows x M.
+template <int LOG_M, int LOG_R>
+__device__ __forceinline__ void tile_coords(int& g, int& t) {
+    using G = Geo<LOG_M, LOG_R>;
+    g = threadIdx.x / G::T;
+    t = threadIdx.x % G::T;
+}
+
+__device__ __forceinline__ bool job_limb(const PassJob& job, int& a, int& b) {
+    const int lam = blockIdx.y;
+    a = lam / job.nb;
+    b = lam % job.nb;
+    return !(job.skip_diag && a == b);
+}
+
+// ------------------------------------------------------------------------------------------
+// forward pass 1: columns.  Tile = Gc consecutive columns (Gc = blockDim/T), M = M1 rows.
+// ------------------------------------------------------------------------------------------
+template <int LOG_M, int LOG_R, int LOADMODE>
+__global__ void __launch_bounds__(256) k_fwd_cols(PassJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R>;
+    extern __shared__ uint64_t sm[];
+    int a, b;
+    if (!job_limb(job, a, b)) return;
+    const int z = blockIdx.z;
+    const int log_n = tb.log_n;
+    const int M2 = 1 << (log_n - LOG_M);
+    const int Gc = blockDim.x / G::T;
+    const int col0 = blockIdx.x * Gc;
+    const int mi = job.mod_map[b];
+    const Mod md = tb.mods[mi];
+    const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
+    uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
+    const int nthr = blockDim.x;
+    // coalesced load: lanes run along columns
+    if (LOADMODE == LOAD_LIFT) {
+        const uint64_t Qs = tb.mods[job.smod_map[a]].q;
+        for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
+            const int c = i % Gc, mid = i / Gc;
+            sm[G::addr(c, mid)] = lift_centered(src[(long long)mid * M2 + col0 + c], Qs, md);
+        }
+    } else {
+        for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
+            const int c = i % Gc, mid = i / Gc;
+            sm[G::addr(c, mid)] = src[(long long)mid * M2 + col0 + c];
+        }
+    }
+    __syncthreads();
+    int g, t;
+    tile_coords<LOG_M, LOG_R>(g, t);
+    fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), 0, 0, g, t);
+    for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
+        const int c = i % Gc, mid = i / Gc;
+        dst[(long long)mid * M2 + col0 + c] = sm[G::addr(c, mid)];   // lazy [0, 4q)
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// forward pass 2: rows (contiguous).  Tile = Gr consecutive rows of M = M2 words.
+// STORE_PLAIN: full reduction.  STORE_COMBINE: out = (aux - v) * comb[mod] (+ add if a < aux_limit).
+// ------------------------------------------------------------------------------------------
+template <int LOG_M, int LOG_R, int STOREMODE>
+__global__ void __launch_bounds__(256) k_fwd_rows(PassJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R>;
+    extern __shared__ uint64_t sm[];
+    int a, b;
+    if (!job_limb(job, a, b)) return;
+    const int z = blockIdx.z;
+    const int log_n = tb.log_n;
+    const int Gr = blockDim.x / G::T;
+    const int row0 = blockIdx.x * Gr;
+    const int mi = job.mod_map[b];
+    const Mod md = tb.mods[mi];
+    const long long off0 = (long long)row0 << LOG_M;
+    const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
+    uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
+    const int nthr = blockDim.x;
+    const int tile = Gr * G::M;
+    for (int i = threadIdx.x; i < tile; i += nthr) sm[G::addr(i >> LOG_M, i & (G::M - 1))] = src[i];
+    __syncthreads();
+    int g, t;
+    tile_coords<LOG_M, LOG_R>(g, t);
+    const int s0 = log_n - LOG_M;
+    fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), s0, (uint32_t)(row0 + g), g, t);
+    if (STOREMODE == STORE_PLAIN) {
+        for (int i = threadIdx.x; i < tile; i += nthr) dst[i] = reduce4(sm[G::addr(i >> LOG_M, i & (G::M - 1))], md.q);
+    } else {
+        const uint64_t* aux = job.aux[z] + a * job.aux_a + b * job.aux_b + off0;
+        const ulonglong2 cm = tb.comb[mi];
+        const bool has_add = job.add[z] != nullptr && a < job.aux_limit;
+        const uint64_t* add = has_add ? job.add[z] + a * job.add_a + b * job.add_b + off0 : nullptr;
+        for (int i = threadIdx.x; i < tile; i += nthr) {
+            const uint64_t v = reduce4(sm[G::addr(i >> LOG_M, i & (G::M - 1))], md.q);
+            uint64_t r = mul_shoup(sub_mod(aux[i], v, md.q), cm.x, cm.y, md.q);
+            if (has_add) r = add_mod(r, add[i], md.q);
+            dst[i] = r;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// inverse pass A: rows; stores lazily in [0, 2q)
+// ------------------------------------------------------------------------------------------
+template <int LOG_M, int LOG_R>
+__global__ void __launch_bounds__(256) k_inv_rows(PassJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R>;
+    extern __shared__ uint64_t sm[];
+    int a, b;
+    if (!job_limb(job, a, b)) return;
+    const int z = blockIdx.z;
+    const int log_n = tb.log_n;
+    const int Gr = blockDim.x / G::T;
+    const int row0 = blockIdx.x * Gr;
+    const int mi = job.mod_map[b];
+    const Mod md = tb.mods[mi];
+    const long long off0 = (long long)row0 << LOG_M;
+    const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
+    uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
+    const int nthr = blockDim.x;
+    const int tile = Gr * G::M;
+    for (int i = threadIdx.x; i < tile; i += nthr) sm[G::addr(i >> LOG_M, i & (G::M - 1))] = src[i];
+    __syncthreads();
+    int g, t;
+    tile_coords<LOG_M, LOG_R>(g, t);
+    inv_engine<LOG_M, LOG_R>(sm, md.q, tb.inv + ((long long)mi << log_n), 0, log_n, (uint32_t)(row0 + g), g, t);
+    for (int i = threadIdx.x; i < tile; i += nthr) dst[i] = sm[G::addr(i >> LOG_M, i & (G::M - 1))];
+}
+
+// ------------------------------------------------------------------------------------------
+// inverse pass B: columns; multiplies by N^-1 and fully reduces.
+// ------------------------------------------------------------------------------------------
+template <int LOG_M, int LOG_R>
+__global__ void __launch_bounds__(256) k_inv_cols(PassJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R>;
+    extern __shared__ uint64_t sm[];
+    int a, b;
+    if (!job_limb(job, a, b)) return;
+    const int z = blockIdx.z;
+    const int log_n = tb.log_n;
+    const int M2 = 1 << (log_n - LOG_M);
+    const int Gc = blockDim.x / G::T;
+    const int col0 = blockIdx.x * Gc;
+    const int mi = job.mod_map[b];
+    const Mod md = tb.mods[mi];
+    const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
+    uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
+    const int nthr = blockDim.x;
+    for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
+        const int c = i % Gc, mid = i / Gc;
+        sm[G::addr(c, mid)] = src[(long long)mid * M2 + col0 + c];
+    }
+    __syncthreads();
+    int g, t;
+    tile_coords<LOG_M, LOG_R>(g, t);
+    inv_engine<LOG_M, LOG_R>(sm, md.q, tb.inv + ((long long)mi << log_n), log_n - LOG_M, log_n, 0, g, t);
+    const ulonglong2 ni = tb.ninv[mi];
+    for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
+        const int c = i % Gc, mid = i / Gc;
+        dst[(long long)mid * M2 + col0 + c] = mul_shoup(sm[G::addr(c, mid)], ni.x, ni.y, md.q);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// host launchers
+// ------------------------------------------------------------------------------------------
+constexpr int LOG_R_NTT = 4;
+
+template <int LOG_M>
+static void launch_geom(int log_m_other, int& threads, int& gx, size_t& smem) {
+    using G = Geo<LOG_M, LOG_R_NTT>;
+    int groups_per_limb = 1 << log_m_other;
+    int gpc = 256 / G::T;
+    if (gpc > groups_per_limb) gpc = groups_per_limb;
+    threads = gpc * G::T;
+    gx = groups_per_limb / gpc;
+    smem = (size_t)gpc * G::STRIDE * sizeof(uint64_t);
+}
+
+template <int LOG_M>
+static cudaError_t fwd_cols_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, int lift, cudaStream_t st) {
+    int threads, gx; size_t smem;
+    launch_geom<LOG_M>(tb.log_n - LOG_M, threads, gx, smem);
+    dim3 grid(gx, nlimbs, nz);
+    if (lift) k_fwd_cols<LOG_M, LOG_R_NTT, LOAD_LIFT><<<grid, threads, smem, st>>>(job, tb);
+    else k_fwd_cols<LOG_M, LOG_R_NTT, LOAD_PLAIN><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+template <int LOG_M>
+static cudaError_t fwd_rows_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, int combine, cudaStream_t st) {
+    int threads, gx; size_t smem;
+    launch_geom<LOG_M>(tb.log_n - LOG_M, threads, gx, smem);
+    dim3 grid(gx, nlimbs, nz);
+    if (combine) k_fwd_rows<LOG_M, LOG_R_NTT, STORE_COMBINE><<<grid, threads, smem, st>>>(job, tb);
+    else k_fwd_rows<LOG_M, LOG_R_NTT, STORE_PLAIN><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+template <int LOG_M>
+static cudaError_t inv_rows_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st) {
+    int threads, gx; size_t smem;
+    launch_geom<LOG_M>(tb.log_n - LOG_M, threads, gx, smem);
+    dim3 grid(gx, nlimbs, nz);
+    k_inv_rows<LOG_M, LOG_R_NTT><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+template <int LOG_M>
+static cudaError_t inv_cols_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st) {
+    int threads, gx; size_t smem;
+    launch_geom<LOG_M>(tb.log_n - LOG_M, threads, gx, smem);
+    dim3 grid(gx, nlimbs, nz);
+    k_inv_cols<LOG_M, LOG_R_NTT><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+
+#define DISPATCH_LOGM(lm, CALL)                      \
+    switch (lm) {                                    \
+        case 4: return CALL<4>;                      \
+        case 5: return CALL<5>;                      \
+        case 6: return CALL<6>;                      \
+        case 7: return CALL<7>;                      \
+        case 8: return CALL<8>;                      \
+        default: return cudaErrorInvalidValue;       \
+    }
+
+int split_m1(int log_n) { return log_n / 2; }
+
+cudaError_t launch_fwd_pass1(const PassJob& job, const Tables& tb, int nlimbs, int nz, bool lift, cudaStream_t st) {
+    const int lm = split_m1(tb.log_n);
+#define C(LM) fwd_cols_t<LM>(job, tb, nlimbs, nz, lift, st)
+    switch (lm) { case 4: return C(4); case 5: return C(5); case 6: return C(6); case 7: return C(7); case 8: return C(8); }
+#undef C
+    return cudaErrorInvalidValue;
+}
+cudaError_t launch_fwd_pass2(const PassJob& job, const Tables& tb, int nlimbs, int nz, bool combine, cudaStream_t st) {
+    const int lm = tb.log_n - split_m1(tb.log_n);
+#define C(LM) fwd_rows_t<LM>(job, tb, nlimbs, nz, combine, st)
+    switch (lm) { case 4: return C(4); case 5: return C(5); case 6: return C(6); case 7: return C(7); case 8: return C(8); }
+#undef C
+    return cudaErrorInvalidValue;
+}
+cudaError_t launch_inv_passA(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st) {
+    const int lm = tb.log_n - split_m1(tb.log_n);
+#define C(LM) inv_rows_t<LM>(job, tb, nlimbs, nz, st)
+    switch (lm) { case 4: return C(4); case 5: return C(5); case 6: return C(6); case 7: return C(7); case 8: return C(8); }
+#undef C
+    return cudaErrorInvalidValue;
+}
+cudaError_t launch_inv_passB(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st) {
+    const int lm = split_m1(tb.log_n);
+#define C(LM) inv_cols_t<LM>(job, tb, nlimbs, nz, st)
+    switch (lm) { case 4: return C(4); case 5: return C(5); case 6: return C(6); case 7: return C(7); case 8: return C(8); }
+#undef C
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace hisa

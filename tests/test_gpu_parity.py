@@ -1,0 +1,233 @@
+"""GPU parity: libhisa (sm_100a, via the C-ABI binding) vs the CPU oracle, bit for bit.
+
+Every case feeds identical seeded inputs to both sides: ChaCha20 streams (keys, encryption
+randomness, BENCH residues) are generated independently on each side from the same seed (A11);
+float inputs come from synth/.  Ciphertexts are compared word by word after canonical export.
+"""
+import numpy as np
+import pytest
+
+from oracle.ckks import Ct, Oracle, Pt
+
+pytestmark = pytest.mark.gpu
+
+H = pytest.importorskip("paper_1810_00845_b200.hisa")
+
+# (log_n, q_bits, p_bits): several tiles per pass and odd log N splits (M1 != M2)
+PARAMS = {
+    "n10": (10, [60, 40, 40], 60),
+    "n11_odd": (11, [50] * 5, 60),
+    "c1_n13": (13, [60, 40, 40], 60),
+    "c2_n14": (14, [50] * 8, 60),
+    "n15_odd": (15, [60, 40, 40, 40], 60),
+}
+SEED = 1234
+
+
+class Pair:
+    def __init__(self, log_n, qb, pb, rots=(1, 3)):
+        self.g = H.Context(log_n, qb, pb, seed=SEED, arena_bytes=3 << 30)
+        self.o = Oracle(log_n, qb, pb, seed=SEED)
+        assert self.g.moduli == self.o.moduli
+        self.rots = list(rots)
+        self.g.keygen(self.rots, True)
+        self.o.keygen(rot_amounts=self.rots)
+
+    def ct(self, b, level=None, npolys=2):
+        level = self.o.L - 1 if level is None else level
+        h = self.g.ct_random(b, level, npolys)
+        oc = self.o.bench_ct(b, level, npolys)
+        assert (self.g.ct_export(h) == oc.data).all(), "BENCH sampler mismatch"
+        return h, oc
+
+    def pt(self, b, level=None):
+        level = self.o.L - 1 if level is None else level
+        h = self.g.pt_random(b, level)
+        op = self.o.bench_pt(b, level)
+        assert (self.g.pt_export(h) == op.data).all()
+        return h, op
+
+    def same(self, h, oc: Ct):
+        got = self.g.ct_export(h)
+        lv, npl, sc = self.g.ct_info(h)
+        assert (lv, npl) == (oc.level, oc.npolys)
+        assert sc == oc.scale
+        if not (got == oc.data).all():
+            bad = np.argwhere(got != oc.data)
+            raise AssertionError(f"{len(bad)} words differ, first at {bad[0].tolist()}")
+
+
+@pytest.fixture(scope="module", params=sorted(PARAMS))
+def pair(request):
+    log_n, qb, pb = PARAMS[request.param]
+    p = Pair(log_n, qb, pb, rots=(1, 3, (1 << (log_n - 1)) - 1))
+    yield p
+    p.g.close()
+
+
+def test_keys_bit_exact(pair):
+    g, o = pair.g, pair.o
+    N, L = o.N, o.L
+    assert (g.key_export(-2, (L + 1) * N).reshape(L + 1, N) == o.s_ntt).all()
+    assert (g.key_export(-1, 2 * L * N).reshape(2, L, N) == o.pk).all()
+    kw = L * 2 * (L + 1) * N
+    assert (g.key_export(0, kw).reshape(o.rlk.shape) == o.rlk).all()
+    for k in pair.rots:
+        assert (g.key_export(k, kw).reshape(o.rlk.shape) == o.rot_keys[k]).all()
+
+
+def test_ntt_intt_bit_exact(pair):
+    h, oc = pair.ct(11)
+    pair.g.ntt(h, False)
+    want = np.stack([pair.o.ntt(oc.data[p], 0) for p in range(2)])
+    assert (pair.g.ct_export(h) == want).all()
+    pair.g.ntt(h, True)
+    assert (pair.g.ct_export(h) == oc.data).all()
+
+
+def test_elementwise_bit_exact(pair):
+    g, o = pair.g, pair.o
+    a, oa = pair.ct(1)
+    b, ob = pair.ct(2)
+    p, op = pair.pt(3)
+    pair.same(g.add(a, b), o.add(oa, ob))
+    pair.same(g.sub(a, b), o.sub(oa, ob))
+    pair.same(g.add_plain(a, p), o.add_plain(oa, op))
+    pair.same(g.sub_plain(a, p), o.sub_plain(oa, op))
+    pair.same(g.mul_plain(a, p), o.mul_plain(oa, op))
+    for x in (0.5, -1.25, 3.0e-3):
+        pair.same(g.mul_scalar(a, x), o.mul_scalar(oa, x))
+        pair.same(g.mul_scalar(a, x, 2.0 ** 30), o.mul_scalar(oa, x, 2.0 ** 30))
+        pair.same(g.add_scalar(a, x), o.add_scalar(oa, x))
+        pair.same(g.sub_scalar(a, x), o.sub_scalar(oa, x))
+    pair.same(g.mul_norelin(a, b), o.mul_norelin(oa, ob))
+    pair.same(g.mul_norelin(a, a), o.mul_norelin(oa, oa))
+    pair.same(g.mod_switch(a, 1), o.mod_switch(oa, 1))
+
+
+def test_rescale_bit_exact(pair):
+    g, o = pair.g, pair.o
+    for npolys in (2, 3):
+        a, oa = pair.ct(4, npolys=npolys)
+        r, orr = g.rescale(a), o.rescale(oa)
+        pair.same(r, orr)
+        if orr.level > 0:
+            pair.same(g.div_scalar(r, o.q[orr.level]), o.div_scalar(orr, o.q[orr.level]))
+
+
+def test_relinearize_bit_exact(pair):
+    g, o = pair.g, pair.o
+    a, oa = pair.ct(5, npolys=3)
+    g.relinearize(a)
+    pair.same(a, o.relinearize(oa))
+    b, ob = pair.ct(6)
+    c, oc = pair.ct(7)
+    pair.same(g.mul(b, c), o.mul(ob, oc))
+
+
+def test_rotation_bit_exact(pair):
+    g, o = pair.g, pair.o
+    a, oa = pair.ct(8)
+    for k in pair.rots:
+        pair.same(g.rot_left(a, k), o.rot_left(oa, k))
+    k = pair.rots[0]
+    pair.same(g.rot_right(a, o.slots - k), o.rot_left(oa, k))
+    pair.same(g.rot_left(a, 0), oa)
+    # lower level: keys truncated to the active limbs
+    lo = g.mod_switch(a, 1)
+    pair.same(g.rot_left(lo, 3), o.rot_left(o.mod_switch(oa, 1), 3))
+    # in-place (Assign) form reuses the handle
+    h = g.copy(a)
+    assert g.rot_left(h, 1, inplace=True) == h
+    pair.same(h, o.rot_left(oa, 1))
+
+
+def test_rotation_batch_and_hoisted_bit_exact(pair):
+    g, o = pair.g, pair.o
+    hs, os_ = zip(*[pair.ct(20 + i) for i in range(3)])
+    outs = g.rot_left_batch(list(hs), 3)
+    for h, oc in zip(outs, os_):
+        pair.same(h, o.rot_left(oc, 3))
+    outs = g.rot_left_hoisted(hs[0], pair.rots)
+    for h, k in zip(outs, pair.rots):
+        pair.same(h, o.rot_left(os_[0], k))
+
+
+def test_encode_encrypt_decrypt_bit_exact(pair):
+    g, o = pair.g, pair.o
+    rng = np.random.default_rng(0)
+    for n in (o.slots, 37):      # full and ragged slot counts
+        z = rng.uniform(0, 1, n)
+        hp = g.encode(z, 2.0 ** 40)
+        op = o.encode(z, 2.0 ** 40)
+        assert (g.pt_export(hp) == op.data).all()
+        hc = g.encrypt(hp)
+        oc = o.encrypt(op)
+        pair.same(hc, oc)
+        hd = g.decrypt(hc)
+        od = o.decrypt(oc)
+        assert (g.pt_export(hd) == od.data).all()
+        assert np.abs(g.decode(hd, n) - z).max() < 2.0 ** -20
+        assert np.abs(g.decode(hd, n) - o.decode(od, n)).max() < 1e-12
+
+
+def test_conv_accumulate_bit_exact(pair):
+    g, o = pair.g, pair.o
+    T, OC = 5, 3
+    hs, os_ = zip(*[pair.ct(40 + i) for i in range(T)])
+    W = np.random.default_rng(3).normal(0, 0.1, (OC, T))
+    outs = g.conv_accumulate(list(hs), W.ravel())
+    for oi in range(OC):
+        acc = None
+        for t in range(T):
+            term = o.mul_scalar(os_[t], float(W[oi, t]))
+            acc = term if acc is None else o.add(acc, term)
+        pair.same(outs[oi], acc)
+
+
+def test_semantics_rotation_mul(pair):
+    g, o = pair.g, pair.o
+    z = np.random.default_rng(1).uniform(0, 1, o.slots)
+    c = g.encrypt(g.encode(z, 2.0 ** 40))
+    for k in pair.rots:
+        r = g.decode(g.decrypt(g.rot_left(c, k)), o.slots)
+        assert np.abs(r - np.roll(z, -k)).max() < 1e-6
+    if o.L >= 2:
+        sq = g.rescale(g.mul(c, c))
+        assert np.abs(g.decode(g.decrypt(sq), o.slots) - z * z).max() < 1e-5
+
+
+def test_error_contract(pair):
+    g, o = pair.g, pair.o
+    a, _ = pair.ct(50)
+    with pytest.raises(H.HisaError) as ei:
+        g.add(a, g.mod_switch(a, 1))
+    assert ei.value.code == "LEVEL_MISMATCH"
+    with pytest.raises(H.HisaError) as ei:
+        g.rot_left(a, 2)
+    assert ei.value.code == "NO_KEY"
+    with pytest.raises(H.HisaError) as ei:
+        g.bootstrap(a)
+    assert ei.value.code == "UNSUPPORTED_PROFILE"
+    with pytest.raises(H.HisaError) as ei:
+        g.div_scalar(a, 12345)
+    assert ei.value.code == "INVALID_DIVISOR"
+    with pytest.raises(H.HisaError) as ei:
+        g.encode(np.zeros(o.slots + 1), 2.0 ** 40)
+    assert ei.value.code == "CAPACITY"
+    t = g.mul_norelin(a, a)
+    with pytest.raises(H.HisaError) as ei:
+        g.rot_left(t, 1)
+    assert ei.value.code == "NOT_RELINEARIZED"
+    x = g.copy(a)
+    g.free(x)
+    with pytest.raises(H.HisaError) as ei:
+        g.add(x, a)
+    assert ei.value.code == "INVALID_HANDLE"
+    lo = g.mod_switch(a, o.L - 1)
+    with pytest.raises(H.HisaError) as ei:
+        g.rescale(lo)
+    assert ei.value.code == "MODULUS_EXHAUSTED"
+    assert g.max_scalar_div(a, 2 ** 62) == o.q[o.L - 1]
+    assert g.max_scalar_div(a, 2) == 1
+    assert not g.supports(H.PROFILE_BOOTSTRAP) and g.supports(H.PROFILE_RELIN)
