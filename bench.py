@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""bench.py -- key-switch rotations/s at N=2^16 (BASELINE.json metric, config 2 top point).
+
+Workload: RNS-CKKS N = 2^16, L = 24 limbs of 50-bit primes + one
+60-bit special prime, dnum = L; B ciphertexts per GPU at the top level with uniform residues
+(ChaCha20 tag BENCH, resident in HBM before timing), one rotation amount k (A30).  One step =
+hisa_rot_left_batch over the B ciphertexts: automorphism + the full key switch (INTT, ModUp,
+key inner product, ModDown) for every ciphertext.  Multi-GPU: each rank rotates its own batch
+(independent ciphertexts, no data-path collective) -> "scaling": "weak".
+
+--impl reference times the CPU oracle (oracle/) on this box's host cores on the same metric:
+each step is one rotation of one ciphertext at the same parameters (a bounded sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "key-switch rotations/s at N=2^16"
+UNIT = "rot/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hisa", choices=["hisa", "reference"])
+    ap.add_argument("--batch", type=int, default=8, help="ciphertexts per GPU per step")
+    ap.add_argument("--log-n", type=int, default=16)
+    ap.add_argument("--limbs", type=int, default=24)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(a):
+    return {"workload": f"config2 HISA rotate sweep top point: N=2^{a.log_n}, L={a.limbs} x 50-bit q_i + 60-bit p, "
+                        f"dnum=L, uniform-residue ciphertexts at the top level",
+            "log_n": a.log_n, "limbs": a.limbs, "q_bits": 50, "p_bits": 60, "dnum": a.limbs}
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = []
+        reasons = set()
+        smax = None
+        for p in self.samples:
+            try:
+                sm.append(float(p[0]))
+                smax = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ work model
+def kernel_units(name: str, log_n: int, l1: int, B: int) -> float:
+    """Algorithmic 64-bit modular multiplies per step for one kernel class:
+    an NTT pass over one limb = (N/2) * log2(M) butterflies (one Shoup modmul each); the key
+    inner product adds 2 multiply-accumulates per (digit, output prime, word)."""
+    N = 1 << log_n
+    m1 = log_n // 2
+    m2 = log_n - m1
+    hb = N // 2
+    per_ct = {
+        "ntt_inv_rows": l1 * hb * m2,
+        "ntt_inv_cols": l1 * hb * m1,
+        "ks_modup_cols": l1 * l1 * hb * m1,                       # (j, r != q_j) pairs, first log M1 stages
+        "ks_ip_rows": l1 * l1 * hb * m2 + 2 * l1 * (l1 + 1) * N,  # last log M2 stages + key MACs
+        "ks_intt_p_rows": 2 * hb * m2,
+        "ks_intt_p_cols": 2 * hb * m1,
+        "ks_moddown_cols": 2 * l1 * hb * m1,
+        "ks_moddown_rows": 2 * l1 * hb * m2,
+    }
+    return float(per_ct.get(name, 0)) * B
+
+
+def rotation_alg_bytes(log_n: int, l1: int, B: int) -> float:
+    """read ct 2(l+1) + key 2 beta (l+2) (once per same-key batch) + write 2(l+1) limbs."""
+    limb = 8 * (1 << log_n)
+    return (B * 4 * l1 + 2 * l1 * (l1 + 1)) * limb
+
+
+# ------------------------------------------------------------------------------ reference arm (oracle)
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.ckks import Oracle
+    cores = os.cpu_count() or 1
+    o = Oracle(a.log_n, [50] * a.limbs, 60, seed=a.seed, nthreads=cores)
+    import synth
+    k = synth.rot_amount(a.seed, a.log_n, a.limbs)
+    o.keygen(rot_amounts=[k], relin=False)
+    ct = o.bench_ct(0, a.limbs - 1)
+    for _ in range(a.warmup):
+        o.rot_left(ct, k)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        o.rot_left(ct, k)
+    dt = time.perf_counter() - t0
+    v = a.steps / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": dt * 1e3 / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": {**workload(a), "batch_per_gpu": 1,
+                                                                                  "k": k},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": "1 top-level rotation of 1 ciphertext per step (oracle/ckks_oracle.c, "
+                                       "OpenMP over limbs)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(a, k):
+    from oracle.ckks import Oracle
+    cores = os.cpu_count() or 1
+    o = Oracle(a.log_n, [50] * a.limbs, 60, seed=a.seed, nthreads=cores)
+    o.keygen(rot_amounts=[k], relin=False)
+    ct = o.bench_ct(0, a.limbs - 1)
+    t0 = time.perf_counter()
+    o.rot_left(ct, k)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"1 top-level rotation of 1 ciphertext (N=2^{a.log_n}, L={a.limbs}), "
+                      f"keygen excluded, {dt:.1f} s"}
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import synth
+    from paper_1810_00845_b200 import hisa as H
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    B, L, log_n = a.batch, a.limbs, a.log_n
+    N = 1 << log_n
+    k = synth.rot_amount(a.seed, log_n, L)
+    ctx = H.Context(log_n, [50] * L, 60, seed=a.seed, device=local)
+    ctx.keygen([k], False)
+    cts = [ctx.ct_random(rank * B + b, L - 1) for b in range(B)]
+    ctx.sync()
+    stream = torch.cuda.current_stream(local)
+
+    def step():
+        outs = ctx.rot_left_batch(cts, k)
+        for h in outs:
+            ctx.free(h)
+
+    for _ in range(a.warmup):
+        step()
+    ctx.sync()
+    ctx.profile(True)
+    clocks = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(a.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ck = clocks.stop()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ms_max = ms
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = world * B * a.steps / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (integer-ALU bound)
+    peak_bfly = ctx.microbench_butterfly(2000)
+    dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 0))
+    dom_name, (dom_ms, dom_n) = dom
+    units = kernel_units(dom_name, log_n, L, B) * a.steps
+    achieved = units / (dom_ms / 1e3) if dom_ms > 0 else 0.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"{dom_name}@{log_n}/{L}/B{B}")
+        except (ValueError, OSError):
+            traffic = None
+    hbm_peak = 6549.8
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        hbm_peak = json.load(open(mp)).get("hbm_gbs", hbm_peak)
+    alg_bytes_step = rotation_alg_bytes(log_n, L, B)
+    hbm_gbs = alg_bytes_step * a.steps / (ms / 1e3) / 1e9
+    total_ms = sum(v[0] for v in prof.values()) or 1.0
+    roofline = {"bound": "alu", "kernel": dom_name, "achieved": achieved / 1e9, "peak": peak_bfly / 1e9,
+                "unit": "Gmodmul/s", "frac": achieved / peak_bfly if peak_bfly else None, "traffic": traffic,
+                "peak_source": "measured: hisa_microbench_butterfly (register-resident Harvey butterflies, all SMs)",
+                "launch_ms_avg": dom_ms / max(dom_n, 1), "share_of_step": dom_ms / total_ms,
+                "rotation_hbm": {"alg_bytes_per_step": alg_bytes_step, "achieved_gbs": hbm_gbs,
+                                 "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
+                                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
+    kernels = {n: {"ms": v[0], "launches": v[1], "share": v[0] / total_ms,
+                   "gmodmul_s": kernel_units(n, log_n, L, B) * a.steps / (v[0] / 1e3) / 1e9 if v[0] else None}
+               for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
+
+    # end-to-end through the C-ABI with pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        words = 2 * L * N
+        host_in = [torch.empty(words, dtype=torch.int64, pin_memory=True).numpy().view("uint64") for _ in range(B)]
+        for b in range(B):
+            host_in[b][:] = ctx.ct_export(cts[b]).ravel()
+        host_out = [torch.empty(words, dtype=torch.int64, pin_memory=True).numpy().view("uint64") for _ in range(B)]
+        from paper_1810_00845_b200.hisa import _chk, _ptr, _u64p, load
+        lib = load()
+
+        def e2e_step():
+            ins = [ctx.ct_import(host_in[b], L - 1, 2, 2.0 ** 40) for b in range(B)]
+            outs = ctx.rot_left_batch(ins, k)
+            for b, h in enumerate(outs):
+                _chk(lib.hisa_ct_export(ctx.ctx, h, _ptr(host_out[b], _u64p), words))
+                ctx.free(h)
+            for h in ins:
+                ctx.free(h)
+
+        e2e_step()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        n_e2e = max(1, a.steps // 2)
+        for _ in range(n_e2e):
+            e2e_step()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([dt], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": world * B * n_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": B * words * 8,
+               "d2h_bytes_per_step": B * words * 8, "steps": n_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(a, k)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms_max / a.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": {**workload(a), "batch_per_gpu": B, "global_batch": B * world, "k": k,
+                           "parallelism": f"dp{world} (independent ciphertexts)",
+                           "l2": "inputs larger than L2 (600 MiB key + B x 24 MiB ciphertexts per step)"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": ck, "kernels": kernels}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

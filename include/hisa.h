@@ -203,6 +203,19 @@ int hisa_ct_random(hisa_ctx* ctx, uint64_t b, int level, int npolys, hisa_ct* ou
 /* uniform plaintext residues, stream index (b << 32 | 0xFFFF << 16 | limb) */
 int hisa_pt_random(hisa_ctx* ctx, uint64_t b, int level, hisa_pt* out);
 
+/* ---- diagnostics (not HISA instructions) -------------------------------------------------- */
+/* enable != 0: record a CUDA event pair around every kernel launch on the context stream from now
+ * on (and reset the launch counter); 0: stop.  Synchronises. */
+int hisa_profile(hisa_ctx* ctx, int enable);
+/* aggregate recorded launches per kernel class: names ('\n'-separated) / total ms / launch count;
+ * synchronises and clears the records */
+int hisa_profile_read(hisa_ctx* ctx, char* names, size_t names_len, double* ms, uint64_t* counts,
+                      size_t max_entries, size_t* n_entries);
+/* kernels launched since the last hisa_profile call */
+int hisa_launch_count(hisa_ctx* ctx, uint64_t* n);
+/* register-resident 64-bit Harvey butterflies on every SM (mod q_0): butterflies per second */
+int hisa_microbench_butterfly(hisa_ctx* ctx, int iters, double* bfly_per_s);
+
 const char* hisa_last_error(void);
 
 #ifdef __cplusplus

@@ -201,6 +201,12 @@ struct hisa_ctx {
     uint64_t* d_rlk = nullptr;        // [L][2][L+1][N]
     std::map<uint64_t, uint64_t*> rot_keys;
     uint64_t enc_counter = 0;
+    // profiling: CUDA events around every launch on the context stream (hisa_profile)
+    bool prof_on = false;
+    struct ProfRec { const char* name; cudaEvent_t a, b; };
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    uint64_t launches = 0;
     // handles
     std::vector<Obj> objs;
     std::vector<uint32_t> free_slots;
@@ -258,6 +264,40 @@ static T* dalloc_t(hisa_ctx* c, size_t n) { return (T*)dalloc(c, n * sizeof(T));
     do {                            \
         int r_ = (x);               \
         if (r_ != HISA_OK) return r_; \
+    } while (0)
+
+// ---- launch accounting / profiling ----
+static cudaEvent_t take_event(hisa_ctx* c) {
+    if (!c->ev_pool.empty()) { cudaEvent_t e = c->ev_pool.back(); c->ev_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+struct ProfScope {
+    hisa_ctx* c;
+    hisa_ctx::ProfRec r;
+    bool on;
+    ProfScope(hisa_ctx* c_, const char* name) : c(c_), on(c_->prof_on) {
+        c->launches++;
+        if (on) {
+            r.name = name;
+            r.a = take_event(c);
+            r.b = take_event(c);
+            cudaEventRecord(r.a, c->stream);
+        }
+    }
+    ~ProfScope() {
+        if (on) {
+            cudaEventRecord(r.b, c->stream);
+            c->prof.push_back(r);
+        }
+    }
+};
+// launch `call` (returning cudaError_t) accounted under `name`
+#define KL(name, call)                 \
+    do {                               \
+        ProfScope ps_(c, name);        \
+        CK(call);                      \
     } while (0)
 
 // ---- handle table ----
@@ -335,8 +375,8 @@ static int ntt_fwd(hisa_ctx* c, uint64_t* const* ptrs, int nz, int nb, const uin
     j.src_b = j.dst_b = (long long)c->N;
     for (int i = 0; i < nb; i++) j.mod_map[i] = mmap[i];
     Tables tb = c->tables();
-    CK(launch_fwd_pass1(j, tb, nlimbs, nz, false, c->stream));
-    CK(launch_fwd_pass2(j, tb, nlimbs, nz, false, c->stream));
+    KL("ntt_fwd_cols", launch_fwd_pass1(j, tb, nlimbs, nz, false, c->stream));
+    KL("ntt_fwd_rows", launch_fwd_pass2(j, tb, nlimbs, nz, false, c->stream));
     return HISA_OK;
 }
 static int ntt_inv(hisa_ctx* c, const uint64_t* const* src, uint64_t* const* dst, int nz, int nb, const uint8_t* mmap,
@@ -349,9 +389,9 @@ static int ntt_inv(hisa_ctx* c, const uint64_t* const* src, uint64_t* const* dst
     j.src_b = j.dst_b = (long long)c->N;
     for (int i = 0; i < nb; i++) j.mod_map[i] = mmap[i];
     Tables tb = c->tables();
-    CK(launch_inv_passA(j, tb, nlimbs, nz, c->stream));
+    KL("ntt_inv_rows", launch_inv_passA(j, tb, nlimbs, nz, c->stream));
     for (int z = 0; z < nz; z++) j.src[z] = dst[z];
-    CK(launch_inv_passB(j, tb, nlimbs, nz, c->stream));
+    KL("ntt_inv_cols", launch_inv_passB(j, tb, nlimbs, nz, c->stream));
     return HISA_OK;
 }
 static void ident_map(uint8_t* m, int n, int base = 0) {
@@ -541,8 +581,8 @@ static int sample_small_ntt(hisa_ctx* c, uint32_t tag, uint64_t index, int kind,
     if (!tmp) return fail(HISA_E_OOM, "sampler scratch");
     uint8_t mm[MAXL];
     ident_map(mm, nl);
-    CK(launch_sample_small(tmp, c->seed, tag, index, kind, c->log_n, c->stream));
-    CK(launch_int_to_limbs(tmp, out, mm, nl, c->log_n, c->d_mods, c->stream));
+    KL("rng_small", launch_sample_small(tmp, c->seed, tag, index, kind, c->log_n, c->stream));
+    KL("int_to_limbs", launch_int_to_limbs(tmp, out, mm, nl, c->log_n, c->d_mods, c->stream));
     uint64_t* pp[1] = {out};
     RET(ntt_fwd(c, pp, 1, nl, mm));
     dfree(c, tmp);
@@ -609,7 +649,7 @@ extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin)
         memset(&ej, 0, sizeof ej);
         ej.a[0] = c->d_sk; ej.b[0] = c->d_sk; ej.out[0] = sp;
         ej.npolys = 1; ej.nl = M; ej.log_n = c->log_n;
-        CK(launch_elem(EL_MUL_PLAIN, ej, c->d_mods, 1, c->stream));
+        KL("elementwise", launch_elem(EL_MUL_PLAIN, ej, c->d_mods, 1, c->stream));
         RET(gen_ksk(c, 0, sp, &c->d_rlk));
         dfree(c, sp);
     }
@@ -685,7 +725,7 @@ extern "C" int hisa_decrypt(hisa_ctx* c, hisa_ct h, hisa_pt* out) {
     ej.a[0] = o->ptr; ej.b[0] = c->d_sk; ej.out[0] = pt;
     ej.npolys = 1; ej.nl = l1; ej.log_n = c->log_n;
     ej.a_poly = (long long)l1 * c->N;
-    CK(launch_elem(o->npolys == 3 ? EL_DECRYPT3 : EL_DECRYPT2, ej, c->d_mods, 1, c->stream));
+    KL("elementwise", launch_elem(o->npolys == 3 ? EL_DECRYPT3 : EL_DECRYPT2, ej, c->d_mods, 1, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     *out = new_handle(c, OBJ_PT, pt, o->level, 1, o->scale);
     return HISA_OK;
@@ -879,7 +919,7 @@ static int binary_ct(hisa_ctx* c, hisa_ct ha, hisa_ct hb, hisa_ct* out, ElemOp o
     if (!o) return fail(HISA_E_OOM, "add/sub");
     ElemJob j = ejob(c, a->npolys, a->level);
     j.a[0] = a->ptr; j.b[0] = b->ptr; j.out[0] = o;
-    CK(launch_elem(op, j, c->d_mods, 1, c->stream));
+    KL("elementwise", launch_elem(op, j, c->d_mods, 1, c->stream));
     return emit_ct(c, out, ha, o, a->level, a->npolys, a->scale);
 }
 extern "C" int hisa_add(hisa_ctx* c, hisa_ct a, hisa_ct b, hisa_ct* out) { return binary_ct(c, a, b, out, EL_ADD); }
@@ -898,7 +938,7 @@ static int plain_op(hisa_ctx* c, hisa_ct ha, hisa_pt hp, hisa_ct* out, ElemOp op
     if (!o) return fail(HISA_E_OOM, "plain op");
     ElemJob j = ejob(c, 2, a->level);
     j.a[0] = a->ptr; j.b[0] = p->ptr; j.out[0] = o;
-    CK(launch_elem(op, j, c->d_mods, 1, c->stream));
+    KL("elementwise", launch_elem(op, j, c->d_mods, 1, c->stream));
     return emit_ct(c, out, ha, o, a->level, 2, scale);
 }
 extern "C" int hisa_add_plain(hisa_ctx* c, hisa_ct a, hisa_pt p, hisa_ct* out) { return plain_op(c, a, p, out, EL_ADD_PLAIN); }
@@ -932,7 +972,7 @@ static int scalar_op(hisa_ctx* c, hisa_ct ha, double x, double pt_scale, hisa_ct
     uint64_t* o = dalloc_t<uint64_t>(c, obj_words(c, a));
     if (!o) return fail(HISA_E_OOM, "scalar op");
     j.a[0] = a->ptr; j.out[0] = o;
-    CK(launch_elem(op, j, c->d_mods, 1, c->stream));
+    KL("elementwise", launch_elem(op, j, c->d_mods, 1, c->stream));
     return emit_ct(c, out, ha, o, a->level, 2, out_scale);
 }
 extern "C" int hisa_add_scalar(hisa_ctx* c, hisa_ct a, double x, hisa_ct* out) { return scalar_op(c, a, x, 0, out, EL_ADD_SCALAR, 1); }
@@ -952,7 +992,7 @@ extern "C" int hisa_mul_norelin(hisa_ctx* c, hisa_ct ha, hisa_ct hb, hisa_ct* ou
     if (!o) return fail(HISA_E_OOM, "tensor");
     ElemJob j = ejob(c, 2, a->level);
     j.a[0] = a->ptr; j.b[0] = b->ptr; j.out[0] = o;
-    CK(launch_elem(ha == hb ? EL_SQUARE_TENSOR : EL_TENSOR, j, c->d_mods, 1, c->stream));
+    KL("elementwise", launch_elem(ha == hb ? EL_SQUARE_TENSOR : EL_TENSOR, j, c->d_mods, 1, c->stream));
     return emit_ct(c, out, ha, o, a->level, 3, a->scale * b->scale);
 }
 
@@ -998,7 +1038,7 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         j.skip_diag = 1;
         for (int ri = 0; ri < l2; ri++) j.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
         for (int a = 0; a < l1; a++) j.smod_map[a] = (uint8_t)a;
-        CK(launch_fwd_pass1(j, tb, l1 * l2, nz, true, c->stream));
+        KL("ks_modup_cols", launch_fwd_pass1(j, tb, l1 * l2, nz, true, c->stream));
     }
     // (3) fused pass 2 + inner product with the key
     {
@@ -1009,7 +1049,7 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         kj.l1 = l1;
         kj.L = L;
         for (int ri = 0; ri < l2; ri++) kj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
-        CK(launch_ks_ip(kj, tb, nz, c->stream));
+        KL("ks_ip_rows", launch_ks_ip(kj, tb, nz, c->stream));
     }
     // (4) INTT_p of acc_p (both polys)
     {
@@ -1018,10 +1058,10 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         j.nb = 1;
         j.src_a = (long long)l2 * N; j.dst_a = N;
         j.mod_map[0] = (uint8_t)L;
-        CK(launch_inv_passA(j, tb, 2, nz, c->stream));
+        KL("ks_intt_p_rows", launch_inv_passA(j, tb, 2, nz, c->stream));
         for (int z = 0; z < nz; z++) { j.src[z] = ptmp[z]; }
         j.src_a = N;
-        CK(launch_inv_passB(j, tb, 2, nz, c->stream));
+        KL("ks_intt_p_cols", launch_inv_passB(j, tb, 2, nz, c->stream));
     }
     // (5) ModDown pass 1: lift p -> q_i
     {
@@ -1032,7 +1072,7 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         j.dst_a = (long long)l1 * N; j.dst_b = N;
         ident_map(j.mod_map, l1);
         j.smod_map[0] = j.smod_map[1] = (uint8_t)L;
-        CK(launch_fwd_pass1(j, tb, 2 * l1, nz, true, c->stream));
+        KL("ks_moddown_cols", launch_fwd_pass1(j, tb, 2 * l1, nz, true, c->stream));
     }
     // (6) pass 2 + combine: out_i = (acc_i - NTT_i(y)) p^-1 (+ add)
     {
@@ -1051,7 +1091,7 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         j.aux_limit = kb.add_polys;
         ident_map(j.mod_map, l1);
         Tables tc = c->tables(c->d_pinv);
-        CK(launch_fwd_pass2(j, tc, 2 * l1, nz, true, c->stream));
+        KL("ks_moddown_rows", launch_fwd_pass2(j, tc, 2 * l1, nz, true, c->stream));
     }
     dfree(c, scratch);
     return HISA_OK;
@@ -1120,7 +1160,7 @@ static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_
     }
     kb.add_polys = 1;
     kb.add_a = 0;
-    CK(launch_automorphism(ins, ps, nz, 2 * l1, c->log_n, g, c->stream));
+    KL("automorphism", launch_automorphism(ins, ps, nz, 2 * l1, c->log_n, g, c->stream));
     RET(keyswitch(c, nz, level, it->second, kb));
     dfree(c, perm);
     return HISA_OK;
@@ -1207,9 +1247,9 @@ static int rescale_ptr(hisa_ctx* c, const Obj* o, uint64_t** res) {
         j.src[0] = o->ptr + (long long)l * N; j.dst[0] = top;
         j.nb = 1; j.src_a = (long long)l1 * N; j.dst_a = N;
         j.mod_map[0] = (uint8_t)l;
-        CK(launch_inv_passA(j, tb, P, 1, c->stream));
+        KL("rescale_intt_rows", launch_inv_passA(j, tb, P, 1, c->stream));
         j.src[0] = top; j.src_a = N;
-        CK(launch_inv_passB(j, tb, P, 1, c->stream));
+        KL("rescale_intt_cols", launch_inv_passB(j, tb, P, 1, c->stream));
     }
     {   // lift q_l -> q_i (i < l), forward pass 1
         PassJob j = job0();
@@ -1217,7 +1257,7 @@ static int rescale_ptr(hisa_ctx* c, const Obj* o, uint64_t** res) {
         j.nb = l; j.src_a = N; j.src_b = 0; j.dst_a = (long long)l * N; j.dst_b = N;
         ident_map(j.mod_map, l);
         for (int a = 0; a < P; a++) j.smod_map[a] = (uint8_t)l;
-        CK(launch_fwd_pass1(j, tb, P * l, 1, true, c->stream));
+        KL("rescale_lift_cols", launch_fwd_pass1(j, tb, P * l, 1, true, c->stream));
     }
     {   // pass 2 + combine: out_i = (u_i - NTT_i(y)) q_l^-1
         PassJob j = job0();
@@ -1228,7 +1268,7 @@ static int rescale_ptr(hisa_ctx* c, const Obj* o, uint64_t** res) {
         j.aux_a = (long long)l1 * N; j.aux_b = N;
         ident_map(j.mod_map, l);
         Tables tc = c->tables(c->d_qlinv + (size_t)l * (c->L + 1));
-        CK(launch_fwd_pass2(j, tc, P * l, 1, true, c->stream));
+        KL("rescale_combine_rows", launch_fwd_pass2(j, tc, P * l, 1, true, c->stream));
     }
     dfree(c, tmp);
     *res = out;
@@ -1365,8 +1405,11 @@ extern "C" int hisa_conv_accumulate(hisa_ctx* c, const hisa_ct* in, size_t T, co
     CK(cudaMemcpyAsync(dop, optr.data(), OC * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
     ConvJob cj{(int)T, (int)OC, l1, c->log_n, (long long)l1 * N};
     dim3 grid((unsigned)std::min<long long>((N + 255) / 256, 64), l1, 2);
-    k_conv_acc<<<grid, 256, 0, c->stream>>>(dip, dop, dw, cj, c->d_mods);
-    CK(cudaGetLastError());
+    {
+        ProfScope ps_(c, "conv_acc");
+        k_conv_acc<<<grid, 256, 0, c->stream>>>(dip, dop, dw, cj, c->d_mods);
+        CK(cudaGetLastError());
+    }
     CK(cudaStreamSynchronize(c->stream));   // host staging vectors must outlive the copies
     dfree(c, dw);
     dfree(c, (void*)dip);
@@ -1519,3 +1562,106 @@ extern "C" int hisa_ntt_batch(hisa_ctx* c, const hisa_ct* hs, size_t n, int inve
     return HISA_OK;
 }
 extern "C" int hisa_ntt(hisa_ctx* c, hisa_ct h, int inverse) { return hisa_ntt_batch(c, &h, 1, inverse); }
+
+// ============================================================================================
+// profiling / accounting / microbenchmark (diagnostics; not HISA instructions)
+// ============================================================================================
+extern "C" int hisa_profile(hisa_ctx* c, int enable) {
+    CHECK_CTX(c);
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto& r : c->prof) { c->ev_pool.push_back(r.a); c->ev_pool.push_back(r.b); }
+    c->prof.clear();
+    c->prof_on = enable != 0;
+    c->launches = 0;
+    return HISA_OK;
+}
+extern "C" int hisa_launch_count(hisa_ctx* c, uint64_t* n) {
+    CHECK_CTX(c);
+    if (!n) return fail(HISA_E_PARAMS, "null out");
+    *n = c->launches;
+    return HISA_OK;
+}
+extern "C" int hisa_profile_read(hisa_ctx* c, char* names, size_t names_len, double* ms, uint64_t* counts,
+                                 size_t max_entries, size_t* n_entries) {
+    CHECK_CTX(c);
+    CK(cudaStreamSynchronize(c->stream));
+    std::map<std::string, std::pair<double, uint64_t>> agg;
+    for (auto& r : c->prof) {
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, r.a, r.b));
+        auto& e = agg[r.name];
+        e.first += t;
+        e.second += 1;
+        c->ev_pool.push_back(r.a);
+        c->ev_pool.push_back(r.b);
+    }
+    c->prof.clear();
+    std::string all;
+    size_t i = 0;
+    for (auto& kv : agg) {
+        if (i >= max_entries) break;
+        if (ms) ms[i] = kv.second.first;
+        if (counts) counts[i] = kv.second.second;
+        all += kv.first;
+        all += "\n";
+        i++;
+    }
+    if (names) {
+        if (all.size() + 1 > names_len) return fail(HISA_E_PARAMS, "names buffer too small");
+        memcpy(names, all.c_str(), all.size() + 1);
+    }
+    if (n_entries) *n_entries = i;
+    return HISA_OK;
+}
+
+// register-resident Harvey CT butterflies (radix-16 pattern, twiddle in registers): the
+// integer-pipe ceiling for the NTT-bearing kernels
+__global__ void __launch_bounds__(256) k_mb_butterfly(uint64_t* out, uint64_t q, uint64_t w, uint64_t wp, int iters) {
+    uint64_t r[16];
+    const uint64_t q2 = 2 * q;
+#pragma unroll
+    for (int e = 0; e < 16; e++) r[e] = (threadIdx.x * 16 + e + blockIdx.x) % q;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int st = 0; st < 4; st++) {
+            const int dist = 8 >> st;
+#pragma unroll
+            for (int e = 0; e < 16; e++) {
+                if (e & dist) continue;
+                uint64_t X = r[e];
+                X = X >= q2 ? X - q2 : X;
+                const uint64_t T = mul_shoup_lazy(r[e + dist], w, wp, q);
+                r[e] = X + T;
+                r[e + dist] = X - T + q2;
+            }
+        }
+    }
+    uint64_t x = 0;
+#pragma unroll
+    for (int e = 0; e < 16; e++) x ^= r[e];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x;
+}
+extern "C" int hisa_microbench_butterfly(hisa_ctx* c, int iters, double* bfly_per_s) {
+    CHECK_CTX(c);
+    if (!bfly_per_s || iters <= 0) return fail(HISA_E_PARAMS, "bad arguments");
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * 8, threads = 256;
+    uint64_t* out = dalloc_t<uint64_t>(c, (size_t)blocks * threads);
+    if (!out) return fail(HISA_E_OOM, "microbench");
+    const uint64_t q = c->mod[0], w = 3 % q;
+    cudaEvent_t a = take_event(c), b = take_event(c);
+    k_mb_butterfly<<<blocks, threads, 0, c->stream>>>(out, q, w, shoup(w, q), 4);   // warm-up
+    CK(cudaEventRecord(a, c->stream));
+    k_mb_butterfly<<<blocks, threads, 0, c->stream>>>(out, q, w, shoup(w, q), iters);
+    CK(cudaEventRecord(b, c->stream));
+    CK(cudaEventSynchronize(b));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, a, b));
+    c->ev_pool.push_back(a);
+    c->ev_pool.push_back(b);
+    dfree(c, out);
+    *bfly_per_s = (double)blocks * threads * iters * 32.0 / (t * 1e-3);
+    return HISA_OK;
+}

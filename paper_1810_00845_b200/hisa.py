@@ -97,6 +97,10 @@ _SIGS = {
     "hisa_ct_adopt_device": [_vp, _vp, _ci, _ci, _cd, _u64p],
     "hisa_ct_random": [_vp, _cu64, _ci, _ci, _u64p],
     "hisa_pt_random": [_vp, _cu64, _ci, _u64p],
+    "hisa_profile": [_vp, _ci],
+    "hisa_profile_read": [_vp, ctypes.c_char_p, _csz, _dp, _u64p, _csz, ctypes.POINTER(_csz)],
+    "hisa_launch_count": [_vp, _u64p],
+    "hisa_microbench_butterfly": [_vp, _ci, _dp],
     "hisa_last_error": [],
 }
 
@@ -396,6 +400,31 @@ def hisa_ct_random(ctx, b: int, level: int, npolys: int = 2) -> int:
 
 def hisa_pt_random(ctx, b: int, level: int) -> int:
     return _h1(load().hisa_pt_random, ctx, b, level)
+
+
+def hisa_profile(ctx, enable: bool = True):
+    _chk(load().hisa_profile(ctx, int(enable)))
+
+
+def hisa_profile_read(ctx) -> dict[str, tuple[float, int]]:
+    """{kernel class: (total ms, launches)} recorded since hisa_profile(ctx, True)."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    ms = np.zeros(256, dtype=np.float64)
+    cnt = np.zeros(256, dtype=np.uint64)
+    n = _csz()
+    _chk(load().hisa_profile_read(ctx, buf, len(buf), _ptr(ms, _dp), _ptr(cnt, _u64p), 256, ctypes.byref(n)))
+    names = buf.value.decode().split("\n")[: n.value]
+    return {nm: (float(ms[i]), int(cnt[i])) for i, nm in enumerate(names)}
+
+
+def hisa_launch_count(ctx) -> int:
+    return _h1(load().hisa_launch_count, ctx)
+
+
+def hisa_microbench_butterfly(ctx, iters: int = 2000) -> float:
+    out = _cd()
+    _chk(load().hisa_microbench_butterfly(ctx, iters, ctypes.byref(out)))
+    return out.value
 
 
 def hisa_last_error() -> str:
