@@ -1048,6 +1048,7 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         kj.key = key;
         kj.l1 = l1;
         kj.L = L;
+        kj.nz = nz;
         for (int ri = 0; ri < l2; ri++) kj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
         KL("ks_ip_rows", launch_ks_ip(kj, tb, nz, c->stream));
     }

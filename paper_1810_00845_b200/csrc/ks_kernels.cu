@@ -17,17 +17,18 @@ template <int LOG_M>
 __global__ void __launch_bounds__(256) k_ks_ip(KsJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R_KS>;
     extern __shared__ uint64_t sm[];
-    const int z = blockIdx.z;
+    // ciphertext index fastest: CTAs that read the same key tile are scheduled together (L2 reuse)
+    const int nz = job.nz;
+    const int z = blockIdx.x % nz;
     const int ri = blockIdx.y;
     const int l1 = job.l1;
     const int nri = l1 + 1;
     const int log_n = tb.log_n;
     const int Gr = blockDim.x / G::T;
-    const int row0 = blockIdx.x * Gr;
+    const int row0 = (blockIdx.x / nz) * Gr;
     const long long off0 = (long long)row0 << LOG_M;
     const int mi = job.mod_map[ri];
     const Mod md = tb.mods[mi];
-    const int tile = Gr * G::M;
     const int nthr = blockDim.x;
     constexpr int EPT = G::R;   // elements per thread in the MAC phase (tile / nthr)
     U128 acc0[EPT], acc1[EPT];
@@ -38,14 +39,17 @@ __global__ void __launch_bounds__(256) k_ks_ip(KsJob job, Tables tb) {
     const long long kstride_p = (long long)(job.L + 1) << log_n;
     const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
     for (int j = 0; j < l1; j++) {
-        if (j == ri) {
-            const uint64_t* src = job.d[z] + ((long long)j << log_n) + off0;
-            for (int i = threadIdx.x; i < tile; i += nthr) sm[G::addr(i >> LOG_M, i & (G::M - 1))] = src[i];
-            __syncthreads();
-        } else {
-            const uint64_t* src = job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
-            for (int i = threadIdx.x; i < tile; i += nthr) sm[G::addr(i >> LOG_M, i & (G::M - 1))] = src[i];
-            __syncthreads();
+        const uint64_t* src = (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
+                                        : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * nthr;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&sm[G::addr(i >> LOG_M, i & (G::M - 1))]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + i) : "memory");
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        if (j != ri) {
             fwd_engine<LOG_M, LOG_R_KS>(sm, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
                                         (uint32_t)(row0 + g), g, t);
         }
@@ -78,7 +82,7 @@ static cudaError_t ks_ip_t(const KsJob& job, const Tables& tb, int nz, cudaStrea
     if (gr > rows) gr = rows;
     const int threads = gr * G::T;
     const size_t smem = (size_t)gr * G::STRIDE * sizeof(uint64_t);
-    dim3 grid(rows / gr, job.l1 + 1, nz);
+    dim3 grid((rows / gr) * nz, job.l1 + 1, 1);
     k_ks_ip<LOG_M><<<grid, threads, smem, st>>>(job, tb);
     return cudaGetLastError();
 }

@@ -46,6 +46,7 @@ struct KsJob {
     const uint64_t* key;          // [L][2][L+1][N]
     int l1;                       // active limbs l+1
     int L;                        // total q primes (key stride)
+    int nz;                       // ciphertexts in the batch (grid.x = tiles * nz)
     uint8_t mod_map[MAXL];        // ri -> modulus index
 };
 cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st);

@@ -54,13 +54,39 @@ struct Tables {
 enum LoadMode { LOAD_PLAIN = 0, LOAD_LIFT = 1 };
 enum StoreMode { STORE_PLAIN = 0, STORE_COMBINE = 1 };
 
+// Shared-memory layout of a tile: addr(g, mid) = g * STRIDE + swz(mid).  Chosen per (LOG_M, LOG_R)
+// by exhaustive search over every access pattern of both engines, the row / column tile loads
+// and the MAC reads (64-bit words: 16 distinct word slots per half-warp wavefront):
+//   PAD: swz = mid + (mid >> K);  XOR: swz = mid ^ ((mid >> K) & 15);  NONE: swz = mid.
+// Average wavefronts / ideal: 1.0 - 1.33 (the plain mid + mid/R padding was 2.25 - 3.5).
+enum SwzKind { SWZ_NONE = 0, SWZ_PAD = 1, SWZ_XOR = 2 };
+template <int LOG_M, int LOG_R>
+struct Layout {
+    static constexpr int M = 1 << LOG_M;
+    static constexpr int KIND = (LOG_M == 8 && LOG_R == 4) ? SWZ_PAD
+                              : (LOG_M == 5 && LOG_R == 4) ? SWZ_PAD
+                              : (LOG_M >= 6) ? SWZ_XOR : SWZ_NONE;
+    static constexpr int K = (KIND == SWZ_PAD) ? 4 : (LOG_M == 6 ? 2 : 3);
+    static constexpr int STRIDE = (LOG_M == 8 && LOG_R == 4) ? M + M / 16 + 1
+                                : (LOG_M == 8) ? M + 2
+                                : (LOG_M == 7) ? M + 1
+                                : (LOG_M == 6) ? (LOG_R == 4 ? M + 7 : M + 1)
+                                : (LOG_M == 5) ? (LOG_R == 4 ? M + 2 : M + 3)
+                                : M + 1;
+};
+
 template <int LOG_M, int LOG_R>
 struct Geo {
     static constexpr int M = 1 << LOG_M;
     static constexpr int R = 1 << LOG_R;
     static constexpr int T = M / R;                 // threads per group
-    static constexpr int STRIDE = M + M / R;        // padded group stride in smem
-    __device__ static __forceinline__ int addr(int g, int mid) { return g * STRIDE + mid + (mid >> LOG_R); }
+    using Lay = Layout<LOG_M, LOG_R>;
+    static constexpr int STRIDE = Lay::STRIDE;      // group stride in smem (words)
+    __device__ static __forceinline__ int addr(int g, int mid) {
+        if (Lay::KIND == SWZ_PAD) return g * STRIDE + mid + (mid >> Lay::K);
+        if (Lay::KIND == SWZ_XOR) return g * STRIDE + (mid ^ ((mid >> Lay::K) & 15));
+        return g * STRIDE + mid;
+    }
 };
 
 // ------------------------------------------------------------------------------------------

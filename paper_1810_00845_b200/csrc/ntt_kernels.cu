@@ -14,6 +14,14 @@ __device__ __forceinline__ void tile_coords(int& g, int& t) {
     t = threadIdx.x % G::T;
 }
 
+// 8-byte asynchronous global -> shared copy (LDGSTS): tiles land in the swizzled layout without
+// staging registers, all of a thread's copies in flight at once
+__device__ __forceinline__ void cp_async8(uint64_t* smem, const uint64_t* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 __device__ __forceinline__ bool job_limb(const PassJob& job, int& a, int& b) {
     const int lam = blockIdx.y;
     a = lam / job.nb;
@@ -40,26 +48,31 @@ __global__ void __launch_bounds__(256) k_fwd_cols(PassJob job, Tables tb) {
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
     const int nthr = blockDim.x;
-    // coalesced load: lanes run along columns
-    if (LOADMODE == LOAD_LIFT) {
+    // coalesced asynchronous load, lanes along columns
+    const int lg = __ffs(Gc) - 1;
+#pragma unroll 4
+    for (int k = 0; k < G::R; k++) {
+        const int i = threadIdx.x + k * nthr;
+        cp_async8(&sm[G::addr(i & (Gc - 1), i >> lg)], &src[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))]);
+    }
+    cp_async_wait_all();
+    if (LOADMODE == LOAD_LIFT) {   // each thread lifts the words it copied
         const uint64_t Qs = tb.mods[job.smod_map[a]].q;
-        for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
-            const int c = i % Gc, mid = i / Gc;
-            sm[G::addr(c, mid)] = lift_centered(src[(long long)mid * M2 + col0 + c], Qs, md);
-        }
-    } else {
-        for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
-            const int c = i % Gc, mid = i / Gc;
-            sm[G::addr(c, mid)] = src[(long long)mid * M2 + col0 + c];
+#pragma unroll 4
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
+            uint64_t* p = &sm[G::addr(i & (Gc - 1), i >> lg)];
+            *p = lift_centered(*p, Qs, md);
         }
     }
     __syncthreads();
     int g, t;
     tile_coords<LOG_M, LOG_R>(g, t);
     fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), 0, 0, g, t);
-    for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
-        const int c = i % Gc, mid = i / Gc;
-        dst[(long long)mid * M2 + col0 + c] = sm[G::addr(c, mid)];   // lazy [0, 4q)
+#pragma unroll 4
+    for (int k = 0; k < G::R; k++) {
+        const int i = threadIdx.x + k * nthr;
+        dst[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))] = sm[G::addr(i & (Gc - 1), i >> lg)];   // lazy [0, 4q)
     }
 }
 
@@ -83,21 +96,31 @@ __global__ void __launch_bounds__(256) k_fwd_rows(PassJob job, Tables tb) {
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
     const int nthr = blockDim.x;
-    const int tile = Gr * G::M;
-    for (int i = threadIdx.x; i < tile; i += nthr) sm[G::addr(i >> LOG_M, i & (G::M - 1))] = src[i];
+#pragma unroll 4
+    for (int k = 0; k < G::R; k++) {
+        const int i = threadIdx.x + k * nthr;
+        cp_async8(&sm[G::addr(i >> LOG_M, i & (G::M - 1))], &src[i]);
+    }
+    cp_async_wait_all();
     __syncthreads();
     int g, t;
     tile_coords<LOG_M, LOG_R>(g, t);
     const int s0 = log_n - LOG_M;
     fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), s0, (uint32_t)(row0 + g), g, t);
     if (STOREMODE == STORE_PLAIN) {
-        for (int i = threadIdx.x; i < tile; i += nthr) dst[i] = reduce4(sm[G::addr(i >> LOG_M, i & (G::M - 1))], md.q);
+#pragma unroll 4
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
+            dst[i] = reduce4(sm[G::addr(i >> LOG_M, i & (G::M - 1))], md.q);
+        }
     } else {
         const uint64_t* aux = job.aux[z] + a * job.aux_a + b * job.aux_b + off0;
         const ulonglong2 cm = tb.comb[mi];
         const bool has_add = job.add[z] != nullptr && a < job.aux_limit;
         const uint64_t* add = has_add ? job.add[z] + a * job.add_a + b * job.add_b + off0 : nullptr;
-        for (int i = threadIdx.x; i < tile; i += nthr) {
+#pragma unroll 4
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
             const uint64_t v = reduce4(sm[G::addr(i >> LOG_M, i & (G::M - 1))], md.q);
             uint64_t r = mul_shoup(sub_mod(aux[i], v, md.q), cm.x, cm.y, md.q);
             if (has_add) r = add_mod(r, add[i], md.q);
@@ -125,13 +148,21 @@ __global__ void __launch_bounds__(256) k_inv_rows(PassJob job, Tables tb) {
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
     const int nthr = blockDim.x;
-    const int tile = Gr * G::M;
-    for (int i = threadIdx.x; i < tile; i += nthr) sm[G::addr(i >> LOG_M, i & (G::M - 1))] = src[i];
+#pragma unroll 4
+    for (int k = 0; k < G::R; k++) {
+        const int i = threadIdx.x + k * nthr;
+        cp_async8(&sm[G::addr(i >> LOG_M, i & (G::M - 1))], &src[i]);
+    }
+    cp_async_wait_all();
     __syncthreads();
     int g, t;
     tile_coords<LOG_M, LOG_R>(g, t);
     inv_engine<LOG_M, LOG_R>(sm, md.q, tb.inv + ((long long)mi << log_n), 0, log_n, (uint32_t)(row0 + g), g, t);
-    for (int i = threadIdx.x; i < tile; i += nthr) dst[i] = sm[G::addr(i >> LOG_M, i & (G::M - 1))];
+#pragma unroll 4
+    for (int k = 0; k < G::R; k++) {
+        const int i = threadIdx.x + k * nthr;
+        dst[i] = sm[G::addr(i >> LOG_M, i & (G::M - 1))];
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -153,18 +184,23 @@ __global__ void __launch_bounds__(256) k_inv_cols(PassJob job, Tables tb) {
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
     const int nthr = blockDim.x;
-    for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
-        const int c = i % Gc, mid = i / Gc;
-        sm[G::addr(c, mid)] = src[(long long)mid * M2 + col0 + c];
+    const int lg = __ffs(Gc) - 1;
+#pragma unroll 4
+    for (int k = 0; k < G::R; k++) {
+        const int i = threadIdx.x + k * nthr;
+        cp_async8(&sm[G::addr(i & (Gc - 1), i >> lg)], &src[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))]);
     }
+    cp_async_wait_all();
     __syncthreads();
     int g, t;
     tile_coords<LOG_M, LOG_R>(g, t);
     inv_engine<LOG_M, LOG_R>(sm, md.q, tb.inv + ((long long)mi << log_n), log_n - LOG_M, log_n, 0, g, t);
     const ulonglong2 ni = tb.ninv[mi];
-    for (int i = threadIdx.x; i < Gc * G::M; i += nthr) {
-        const int c = i % Gc, mid = i / Gc;
-        dst[(long long)mid * M2 + col0 + c] = mul_shoup(sm[G::addr(c, mid)], ni.x, ni.y, md.q);
+#pragma unroll 4
+    for (int k = 0; k < G::R; k++) {
+        const int i = threadIdx.x + k * nthr;
+        dst[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))] =
+            mul_shoup(sm[G::addr(i & (Gc - 1), i >> lg)], ni.x, ni.y, md.q);
     }
 }
 
@@ -218,16 +254,6 @@ static cudaError_t inv_cols_t(const PassJob& job, const Tables& tb, int nlimbs, 
     k_inv_cols<LOG_M, LOG_R_NTT><<<grid, threads, smem, st>>>(job, tb);
     return cudaGetLastError();
 }
-
-#define DISPATCH_LOGM(lm, CALL)                      \
-    switch (lm) {                                    \
-        case 4: return CALL<4>;                      \
-        case 5: return CALL<5>;                      \
-        case 6: return CALL<6>;                      \
-        case 7: return CALL<7>;                      \
-        case 8: return CALL<8>;                      \
-        default: return cudaErrorInvalidValue;       \
-    }
 
 int split_m1(int log_n) { return log_n / 2; }
 
