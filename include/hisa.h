@@ -171,7 +171,11 @@ int hisa_bootstrap(hisa_ctx* ctx, hisa_ct ct);   /* always HISA_E_UNSUPPORTED_PR
 /* ---- hot-path extensions ----------------------------------------------------------------- */
 /* drop `drop` top limbs without division (A19), scale unchanged */
 int hisa_mod_switch(hisa_ctx* ctx, hisa_ct ct, int drop, hisa_ct* out);
-/* n rotations of one ciphertext sharing one ModUp (hoisting); outs[n] */
+/* n rotations of one ciphertext sharing one ModUp (hoisting: "the rotations of the input
+ * ciphertexts ... can be code motioned out"); outs[n] (fresh handles, k = 0 copies).
+ * Results are bit-identical to n separate hisa_rot_left calls (A14: the automorphism commutes
+ * with the exact centred ModUp / ModDown).  Device scratch: (l+1)(l+2) limbs for the shared
+ * ModUp output plus ~(6l+8) limbs per amount in flight (chunks of 8 amounts). */
 int hisa_rot_left_hoisted(hisa_ctx* ctx, hisa_ct ct, const int64_t* k, size_t n, hisa_ct* outs);
 /* the same rotation amount on n ciphertexts of one level, batched launches; outs[n] */
 int hisa_rot_left_batch(hisa_ctx* ctx, const hisa_ct* in, size_t n, int64_t k, hisa_ct* outs);
@@ -180,6 +184,11 @@ int hisa_rot_left_batch(hisa_ctx* ctx, const hisa_ct* in, size_t n, int64_t k, h
  * one scale; no rescale (caller divScalars once per output) */
 int hisa_conv_accumulate(hisa_ctx* ctx, const hisa_ct* in, size_t T, const double* W, size_t OC, double pt_scale,
                          hisa_ct* outs);
+/* the same accumulation written into caller-owned device memory dev_out = uint64 [OC][2][l+1][N]
+ * (contiguous; e.g. a torch tensor that a multi-GPU layer then reduce-scatters); every
+ * word fully reduced in [0, q_i).  The partial sums carry scale in_scale * pt_scale. */
+int hisa_conv_accumulate_dev(hisa_ctx* ctx, const hisa_ct* in, size_t T, const double* W, size_t OC,
+                             double pt_scale, uint64_t* dev_out);
 
 /* forward (inverse = 0) or inverse NTT of every limb of the ciphertext(s), in place: the words
  * are reinterpreted (coefficient <-> NTT domain, A5); limb i uses q_i.  Steps a1/a2 as ops. */
@@ -197,6 +206,11 @@ int hisa_pt_import(hisa_ctx* ctx, const uint64_t* host, int level, double scale,
 int hisa_ct_device_view(hisa_ctx* ctx, hisa_ct ct, uint64_t** dev, size_t* words);
 /* new ciphertext copied (device to device) from `dev` (words = npolys (level+1) N) */
 int hisa_ct_adopt_device(hisa_ctx* ctx, const uint64_t* dev, int level, int npolys, double scale, hisa_ct* out);
+/* a15 exchange fix-up: `dev` holds the int64 element-wise SUM over <= 8 ranks of fully reduced
+ * ciphertext residue arrays [npolys][level+1][N] (an NCCL reduce-scatter / all-reduce output;
+ * every sum < 8 q_i < 2^63, exact).  Creates a ciphertext with each word reduced back into
+ * [0, q_i) by a device kernel.  `dev` is caller-owned and not retained. */
+int hisa_ct_adopt_sum(hisa_ctx* ctx, const int64_t* dev, int level, int npolys, double scale, hisa_ct* out);
 /* benchmark input (config 2): uniform residues from ChaCha20 tag BENCH, stream index
  * (b << 32 | poly << 16 | limb); not a valid encryption */
 int hisa_ct_random(hisa_ctx* ctx, uint64_t b, int level, int npolys, hisa_ct* out);

@@ -451,6 +451,7 @@ static long double enc_value_ld(const orc_ctx *c, const double *z, uint64_t n, d
     uint64_t twoN = 2 * c->N;
     long double acc = 0.0L;
     for (uint64_t j = 0; j < n; j++) {
+        if (z[j] == 0.0) continue;   /* a zero slot adds an exact 0 (sparse weight plaintexts) */
         uint64_t e = (uint64_t)(((u128)pow5[j] * t) % twoN);
         acc += 2.0L * (long double)z[j] * c->cosl_tab[e];
     }
@@ -461,6 +462,7 @@ static __float128 enc_value_q(const orc_ctx *c, const double *z, uint64_t n, dou
     uint64_t twoN = 2 * c->N;
     __float128 acc = 0;
     for (uint64_t j = 0; j < n; j++) {
+        if (z[j] == 0.0) continue;
         uint64_t e = (uint64_t)(((u128)pow5[j] * t) % twoN);
         acc += 2 * (__float128)z[j] * c->cosq_tab[e];
     }

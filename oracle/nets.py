@@ -1,0 +1,257 @@
+"""Encrypted HW-tiled CNN evaluation on the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Written from the paper, independently of ``paper_1810_00845_b200/driver.py``: it follows
+Alg. 1 literally -- for every output channel, for every input channel and filter
+tap: rotLeft, mulScalar, add; then one divScalar -- with only the code motion the paper
+itself names ("the rotations of the input ciphertexts are invariant to the output batch and
+channel, so they can be code motioned out"): each (input channel, tap) rotation is
+computed once (a plain, un-hoisted rotLeft) and reused across output channels.
+
+Lowering readings, in the order they apply:
+  layout   CipherTensor metadata: C ciphertexts, valid H x W at slot
+           origin + y*hS + x*wS; `clean` = every other slot is zero.
+  input    the client packs the image zero-padded by the first conv's padding p (A24):
+           hS = W + 2p, wS = 1, origin = p*hS + p, encoded at Delta = 2^40 at the top level.
+  folding  (compile time) the 1/4 of every avgpool is folded into the next linear layer's
+           weights (A26); an "act" right after a linear layer is rewritten
+           a2 x^2 + a1 x + a0 = sign(a2) x'^2 + (a0 - a1^2/(4 a2)), x' = sqrt|a2| x + sqrt|a2| a1/(2 a2):
+           weights * sqrt|a2|, bias beta = sqrt|a2| a1 / (2 a2) added after the linear layer's
+           rescale, constant gamma = a0 - a1^2/(4 a2) added after the square's rescale (A25).
+  conv     (Alg. 1) if p > 0 and the input is not clean: mask = mulPlain(x, 1 on the valid
+           slots, 0 elsewhere, at scale q_top) + rescale.  Rotation amount of tap
+           (i, j): origin + (i - p) hS + (j - p) wS (mod N/2).  mulScalar at pt_scale = q_top
+           (A8), accumulate from the first term (A21), rescale once per output (A22),
+           then add_scalar(beta).  Output layout: strides * s, origin 0, not clean (A23).
+  act      rescale(mul(x, x)) (tensor + relinearize) then add_scalar(gamma).
+  square   rescale(mul(x, x)).
+  avgpool  x + rot(x, wS) + rot(x, hS) + rot(x, hS + wS); strides * 2 (A26).
+  fc (hw input)    acc_j = sum_c mulPlain(x_c, P_jc), P_jc holding W'[j, (c, y, x)] at the valid
+                   slots and 0 elsewhere (encoded at scale q_top, at x's level); rescale; then
+                   rotate-and-sum acc += rot(acc, 2^t) for t < ceil(log2(span)), slot 0 holds
+                   the dot product (A27, R = 1); add_scalar(beta).  Output layout "slot0".
+  fc (slot0 input) out_k = sum_j mulScalar(x_j, W'[k, j]) (pt_scale q_top); rescale; add beta.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .ckks import Ct, Oracle
+
+
+class Layout:
+    def __init__(self, kind, C, H, W, hS=0, wS=0, origin=0, clean=False):
+        self.kind, self.C, self.H, self.W = kind, C, H, W
+        self.hS, self.wS, self.origin, self.clean = hS, wS, origin, clean
+
+    def valid_slots(self):
+        return [self.origin + y * self.hS + x * self.wS for y in range(self.H) for x in range(self.W)]
+
+
+def fold(net: dict, weights, act_coeffs):
+    """Compile-time rewrite (A25, A26): per linear layer (W', beta); per act gamma."""
+    a0, a1, a2 = act_coeffs
+    assert a2 > 0, "the folded form needs a2 > 0 (sign(a2) = +1)"
+    r = math.sqrt(a2)
+    beta = r * a1 / (2 * a2)
+    gamma = a0 - a1 * a1 / (4 * a2)
+    layers = net["layers"]
+    folded, wi, pools = [], 0, 0
+    for i, layer in enumerate(layers):
+        if layer[0] == "avgpool":
+            pools += 1
+        if layer[0] in ("conv", "fc"):
+            w = np.array(weights[wi], dtype=np.float64) * (0.25 ** pools)
+            pools = 0
+            b = 0.0
+            if i + 1 < len(layers) and layers[i + 1][0] == "act":
+                w = w * r
+                b = beta
+            folded.append((w, b))
+            wi += 1
+    return folded, gamma
+
+
+class OracleNet:
+    """The network on the oracle: keys for exactly the rotation amounts the lowering uses
+    (the compiler's rotation-key selection)."""
+
+    def __init__(self, net: dict, weights, act_coeffs, seed: int = 0, nthreads=None):
+        self.net = net
+        self.o = Oracle(net["log_n"], net["q_bits"], net["p_bits"], seed=seed, nthreads=nthreads)
+        self.folded, self.gamma = fold(net, weights, act_coeffs)
+        self.amounts = sorted(self._rotation_amounts())
+        self.o.keygen(rot_amounts=self.amounts, relin=True)
+
+    # ---- layout walk (same walk as forward, metadata only) -------------------------------
+    def _input_layout(self):
+        c, h, w = self.net["input"]
+        first = self.net["layers"][0]
+        p = first[4] if first[0] == "conv" else 0
+        hs = w + 2 * p
+        return Layout("hw", c, h, w, hS=hs, wS=1, origin=p * hs + p, clean=True)
+
+    def _rotation_amounts(self):
+        s = self.o.slots
+        lay = self._input_layout()
+        amts = set()
+        for layer in self.net["layers"]:
+            kind = layer[0]
+            if kind == "conv":
+                _, oc, k, st, p = layer
+                for i in range(k):
+                    for j in range(k):
+                        amts.add((lay.origin + (i - p) * lay.hS + (j - p) * lay.wS) % s)
+                lay = Layout("hw", oc, (lay.H + 2 * p - k) // st + 1, (lay.W + 2 * p - k) // st + 1,
+                             lay.hS * st, lay.wS * st, 0, False)
+            elif kind == "avgpool":
+                amts.update({lay.wS % s, lay.hS % s, (lay.hS + lay.wS) % s})
+                lay = Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
+            elif kind == "fc" and lay.kind == "hw":
+                span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+                amts.update(1 << t for t in range(math.ceil(math.log2(span))))
+                lay = Layout("slot0", layer[1], 1, 1)
+            elif kind == "fc":
+                lay = Layout("slot0", layer[1], 1, 1)
+        amts.discard(0)
+        return amts
+
+    # ---- client ---------------------------------------------------------------------------
+    def encrypt_image(self, image: np.ndarray):
+        lay = self._input_layout()
+        cts = []
+        for c in range(lay.C):
+            v = np.zeros(self.o.slots)
+            for y in range(lay.H):
+                for x in range(lay.W):
+                    v[lay.origin + y * lay.hS + x * lay.wS] = image[c, y, x]
+            cts.append(self.o.encrypt(self.o.encode(v, self.net["scale"])))
+        return cts, lay
+
+    def decrypt_output(self, cts, lay) -> np.ndarray:
+        vals = [self.o.decode(self.o.decrypt(ct)) for ct in cts]
+        if lay.kind == "slot0":
+            return np.array([v[0] for v in vals])
+        sl = lay.valid_slots()
+        return np.array([[v[i] for i in sl] for v in vals]).reshape(lay.C, lay.H, lay.W)
+
+    # ---- server ---------------------------------------------------------------------------
+    def _mask(self, cts, lay):
+        o = self.o
+        m = np.zeros(o.slots)
+        m[lay.valid_slots()] = 1.0
+        out = []
+        for ct in cts:
+            pt = o.encode(m, float(o.q[ct.level]), ct.level)
+            out.append(o.rescale(o.mul_plain(ct, pt)))
+        lay = Layout(lay.kind, lay.C, lay.H, lay.W, lay.hS, lay.wS, lay.origin, True)
+        return out, lay
+
+    def conv(self, cts, lay, layer, w, beta):
+        """Alg. 1 with the rotations code-motioned out of the oc loop."""
+        o = self.o
+        _, oc_n, k, st, p = layer
+        if p > 0 and not lay.clean:
+            cts, lay = self._mask(cts, lay)
+        rotated = {}
+        for ic in range(lay.C):
+            for i in range(k):
+                for j in range(k):
+                    rotated[ic, i, j] = o.rot_left(cts[ic], lay.origin + (i - p) * lay.hS + (j - p) * lay.wS)
+        outs = []
+        for oc in range(oc_n):
+            acc = None                                   # zeroCipher (A21)
+            for ic in range(lay.C):
+                for i in range(k):
+                    for j in range(k):
+                        temp = o.mul_scalar(rotated[ic, i, j], float(w[oc, ic, i, j]))
+                        acc = temp if acc is None else o.add(acc, temp)
+            acc = o.div_scalar(acc, o.max_scalar_div(acc, 1 << 62))
+            if beta:
+                acc = o.add_scalar(acc, beta)
+            outs.append(acc)
+        nl = Layout("hw", oc_n, (lay.H + 2 * p - k) // st + 1, (lay.W + 2 * p - k) // st + 1,
+                    lay.hS * st, lay.wS * st, 0, False)
+        return outs, nl
+
+    def act(self, cts, lay, square_only=False):
+        o = self.o
+        out = []
+        for ct in cts:
+            y = o.rescale(o.mul(ct, ct))
+            if not square_only and self.gamma:
+                y = o.add_scalar(y, self.gamma)
+            out.append(y)
+        return out, Layout(lay.kind, lay.C, lay.H, lay.W, lay.hS, lay.wS, lay.origin, False)
+
+    def avgpool(self, cts, lay):
+        o = self.o
+        out = []
+        for ct in cts:
+            y = o.add(ct, o.rot_left(ct, lay.wS))
+            y = o.add(y, o.rot_left(ct, lay.hS))
+            y = o.add(y, o.rot_left(ct, lay.hS + lay.wS))
+            out.append(y)
+        return out, Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
+
+    def fc(self, cts, lay, layer, w, beta):
+        o = self.o
+        n_out = layer[1]
+        outs = []
+        if lay.kind == "hw":
+            sl = lay.valid_slots()
+            span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+            steps = math.ceil(math.log2(span))
+            hw = lay.H * lay.W
+            for jo in range(n_out):
+                acc = None
+                for c in range(lay.C):
+                    v = np.zeros(o.slots)
+                    v[sl] = w[jo, c * hw:(c + 1) * hw]
+                    pt = o.encode(v, float(o.q[cts[c].level]), cts[c].level)
+                    term = o.mul_plain(cts[c], pt)
+                    acc = term if acc is None else o.add(acc, term)
+                acc = o.rescale(acc)
+                for t in range(steps):
+                    acc = o.add(acc, o.rot_left(acc, 1 << t))
+                if beta:
+                    acc = o.add_scalar(acc, beta)
+                outs.append(acc)
+        else:
+            for ko in range(n_out):
+                acc = None
+                for jn, ct in enumerate(cts):
+                    term = o.mul_scalar(ct, float(w[ko, jn]))
+                    acc = term if acc is None else o.add(acc, term)
+                acc = o.rescale(acc)
+                if beta:
+                    acc = o.add_scalar(acc, beta)
+                outs.append(acc)
+        return outs, Layout("slot0", n_out, 1, 1)
+
+    def forward(self, cts, lay, trace=None):
+        """Server-side evaluation; `trace` (a list) receives (layer index, ciphertexts) after
+        every layer for per-layer parity checks."""
+        wi = 0
+        for li, layer in enumerate(self.net["layers"]):
+            kind = layer[0]
+            if kind == "conv":
+                w, b = self.folded[wi]
+                wi += 1
+                cts, lay = self.conv(cts, lay, layer, w, b)
+            elif kind == "fc":
+                w, b = self.folded[wi]
+                wi += 1
+                cts, lay = self.fc(cts, lay, layer, w, b)
+            elif kind == "act":
+                cts, lay = self.act(cts, lay)
+            elif kind == "square":
+                cts, lay = self.act(cts, lay, square_only=True)
+            elif kind == "avgpool":
+                cts, lay = self.avgpool(cts, lay)
+            else:
+                raise ValueError(kind)
+            if trace is not None:
+                trace.append((li, list(cts)))
+        return cts, lay

@@ -136,12 +136,14 @@ cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, 
 struct PtrPack {
     const uint64_t* in[MAXB];
     uint64_t* out[MAXB];
+    uint64_t g[MAXB];
 };
-__global__ void __launch_bounds__(256) k_automorphism(PtrPack pk, int nlimbs_total, int log_n, uint64_t g) {
+__global__ void __launch_bounds__(256) k_automorphism(PtrPack pk, int log_n) {
     const int z = blockIdx.z;
     const int limb = blockIdx.y;
     const uint32_t N = 1u << log_n;
     const uint64_t mask2n = 2ull * N - 1;
+    const uint64_t g = pk.g[z];
     const uint64_t* in = pk.in[z] + ((long long)limb << log_n);
     uint64_t* out = pk.out[z] + ((long long)limb << log_n);
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
@@ -150,16 +152,41 @@ __global__ void __launch_bounds__(256) k_automorphism(PtrPack pk, int nlimbs_tot
         const uint32_t src = __brev((uint32_t)((e - 1) >> 1)) >> (32 - log_n);
         out[j] = in[src];
     }
-    (void)nlimbs_total;
 }
 
 cudaError_t launch_automorphism(const uint64_t* const* in, uint64_t* const* out, int nz, int nlimbs_total, int log_n,
-                                uint64_t g, cudaStream_t st) {
+                                const uint64_t* gs, cudaStream_t st) {
     PtrPack pk;
-    for (int z = 0; z < nz; z++) { pk.in[z] = in[z]; pk.out[z] = out[z]; }
+    for (int z = 0; z < nz; z++) { pk.in[z] = in[z]; pk.out[z] = out[z]; pk.g[z] = gs[z]; }
     const int N = 1 << log_n;
-    dim3 grid((N + 255) / 256, nlimbs_total, nz);
-    k_automorphism<<<grid, 256, 0, st>>>(pk, nlimbs_total, log_n, g);
+    for (int l0 = 0; l0 < nlimbs_total; l0 += 65535) {   // grid.y limit (keys have 2 L (L+1) limbs)
+        const int nl = nlimbs_total - l0 < 65535 ? nlimbs_total - l0 : 65535;
+        PtrPack pz = pk;
+        for (int z = 0; z < nz; z++) { pz.in[z] += ((long long)l0 << log_n); pz.out[z] += ((long long)l0 << log_n); }
+        dim3 grid((N + 255) / 256, nl, nz);
+        k_automorphism<<<grid, 256, 0, st>>>(pz, log_n);
+    }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// a15 exchange fix-up: the int64 SUM of <= 8 reduced residue arrays (< 2^63) back to [0, q_i)
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_reduce_sum(const int64_t* __restrict__ in, uint64_t* __restrict__ out,
+                                                    long long total, int l1, int log_n, const Mod* __restrict__ mods) {
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)((idx >> log_n) % l1);
+        out[idx] = barrett64((uint64_t)in[idx], mods[i]);
+    }
+}
+
+cudaError_t launch_reduce_sum(const int64_t* in, uint64_t* out, int npolys, int l1, int log_n, const Mod* mods,
+                              cudaStream_t st) {
+    const long long total = ((long long)npolys * l1) << log_n;
+    long long blocks = (total + 255) / 256;
+    if (blocks > (long long)sm_count() * 8) blocks = (long long)sm_count() * 8;
+    k_reduce_sum<<<(unsigned)blocks, 256, 0, st>>>(in, out, total, l1, log_n, mods);
     return cudaGetLastError();
 }
 

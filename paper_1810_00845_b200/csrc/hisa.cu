@@ -667,7 +667,15 @@ extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin)
         RET(ntt_fwd(c, pp, 1, M, mm));
         uint64_t* key = nullptr;
         RET(gen_ksk(c, (uint64_t)k, sp, &key));
-        c->rot_keys[(uint64_t)k] = key;
+        // store key' = psi_g^-1(key) (see "Rotation" below); psi_g^-1 = psi_{5^(N/2 - k)}
+        uint64_t* kp = dalloc_t<uint64_t>(c, key_words(c));
+        if (!kp) return fail(HISA_E_OOM, "key allocation (%zu MiB)", key_words(c) * 8 >> 20);
+        const uint64_t ginv = h_pow(5, slots - (uint64_t)k, 2 * N);
+        const uint64_t* kin[1] = {key};
+        uint64_t* kout[1] = {kp};
+        KL("automorphism", launch_automorphism(kin, kout, 1, 2 * L * M, c->log_n, &ginv, c->stream));
+        dfree(c, key);
+        c->rot_keys[(uint64_t)k] = kp;
         dfree(c, sg);
         dfree(c, sp);
     }
@@ -685,8 +693,19 @@ extern "C" int hisa_key_export(hisa_ctx* c, int64_t which, uint64_t* host, size_
     else if (c->rot_keys.count((uint64_t)which)) { src = c->rot_keys[(uint64_t)which]; w = key_words(c); }
     if (!src) return fail(HISA_E_NO_KEY, "no such key %lld", (long long)which);
     if (words != w) return fail(HISA_E_PARAMS, "key has %zu words", w);
+    uint64_t* canon = nullptr;
+    if (which > 0) {   // rotation keys are stored pre-permuted: export the canonical key (A37)
+        canon = dalloc_t<uint64_t>(c, w);
+        if (!canon) return fail(HISA_E_OOM, "key export");
+        const uint64_t g = h_pow(5, (uint64_t)which, 2 * c->N);
+        const uint64_t* kin[1] = {src};
+        uint64_t* kout[1] = {canon};
+        KL("automorphism", launch_automorphism(kin, kout, 1, 2 * c->L * (c->L + 1), c->log_n, &g, c->stream));
+        src = canon;
+    }
     CK(cudaMemcpyAsync(host, src, w * 8, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (canon) dfree(c, canon);
     return HISA_OK;
 }
 
@@ -1007,52 +1026,34 @@ struct KsBatch {
     int add_polys;                // how many output polys receive the addend (1: rotation, 2: relin)
     long long add_a;
 };
-static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const KsBatch& kb) {
+// (1) INTT of the digits, (2) ModUp pass 1: lift q_j -> r (r != q_j) on load + first log M1
+// forward stages; T1[z] = [j][ri][N] (ri over q_0..q_l, p; diagonal blocks untouched)
+static int ks_modup_pass1(hisa_ctx* c, int nz, int level, const uint64_t* const* d, uint64_t* const* dtil,
+                          uint64_t* const* t1) {
     const int l1 = level + 1, l2 = level + 2, L = c->L;
     const long long N = (long long)c->N;
-    // scratch per ciphertext: dtil l1, T1 l1*l2, acc 2*l2, ptmp 2, md 2*l1
-    const size_t per = (size_t)N * ((size_t)l1 + (size_t)l1 * l2 + 2 * l2 + 2 + 2 * l1);
-    uint64_t* scratch = dalloc_t<uint64_t>(c, per * nz);
-    if (!scratch) return fail(HISA_E_OOM, "key-switch scratch (%zu MiB)", per * nz * 8 >> 20);
-    uint64_t *dtil[MAXB], *t1[MAXB], *acc[MAXB], *ptmp[MAXB], *md[MAXB];
-    for (int z = 0; z < nz; z++) {
-        uint64_t* s = scratch + per * z;
-        dtil[z] = s; s += (size_t)l1 * N;
-        t1[z] = s; s += (size_t)l1 * l2 * N;
-        acc[z] = s; s += (size_t)2 * l2 * N;
-        ptmp[z] = s; s += (size_t)2 * N;
-        md[z] = s;
-    }
     uint8_t mm[MAXL];
     ident_map(mm, l1);
-    // (1) INTT of the digits
-    RET(ntt_inv(c, kb.d, dtil, nz, l1, mm));
+    RET(ntt_inv(c, d, dtil, nz, l1, mm));
+    PassJob j = job0();
+    for (int z = 0; z < nz; z++) { j.src[z] = dtil[z]; j.dst[z] = t1[z]; }
+    j.nb = l2;
+    j.src_a = N; j.src_b = 0;
+    j.dst_a = (long long)l2 * N; j.dst_b = N;
+    j.skip_diag = 1;
+    for (int ri = 0; ri < l2; ri++) j.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+    for (int a = 0; a < l1; a++) j.smod_map[a] = (uint8_t)a;
     Tables tb = c->tables();
-    // (2) ModUp pass 1: (j, ri) with ri != j; lift q_j -> r on load
-    {
-        PassJob j = job0();
-        for (int z = 0; z < nz; z++) { j.src[z] = dtil[z]; j.dst[z] = t1[z]; }
-        j.nb = l2;
-        j.src_a = N; j.src_b = 0;
-        j.dst_a = (long long)l2 * N; j.dst_b = N;
-        j.skip_diag = 1;
-        for (int ri = 0; ri < l2; ri++) j.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
-        for (int a = 0; a < l1; a++) j.smod_map[a] = (uint8_t)a;
-        KL("ks_modup_cols", launch_fwd_pass1(j, tb, l1 * l2, nz, true, c->stream));
-    }
-    // (3) fused pass 2 + inner product with the key
-    {
-        KsJob kj;
-        memset(&kj, 0, sizeof kj);
-        for (int z = 0; z < nz; z++) { kj.t1[z] = t1[z]; kj.d[z] = kb.d[z]; kj.acc[z] = acc[z]; }
-        kj.key = key;
-        kj.l1 = l1;
-        kj.L = L;
-        kj.nz = nz;
-        for (int ri = 0; ri < l2; ri++) kj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
-        KL("ks_ip_rows", launch_ks_ip(kj, tb, nz, c->stream));
-    }
-    // (4) INTT_p of acc_p (both polys)
+    KL("ks_modup_cols", launch_fwd_pass1(j, tb, l1 * l2, nz, true, c->stream));
+    return HISA_OK;
+}
+// (4) INTT_p of acc_p, (5) lift p -> q_i + first stages, (6) last stages with the combine
+// epilogue out_i = (acc_i - NTT_i(y)) p^-1 (+ addend).  ptmp[z]: 2 limbs, md[z]: 2 l1 limbs.
+static int ks_moddown(hisa_ctx* c, int nz, int level, uint64_t* const* acc, uint64_t* const* ptmp,
+                      uint64_t* const* md, const KsBatch& kb) {
+    const int l1 = level + 1, l2 = level + 2, L = c->L;
+    const long long N = (long long)c->N;
+    Tables tb = c->tables();
     {
         PassJob j = job0();
         for (int z = 0; z < nz; z++) { j.src[z] = acc[z] + (long long)l1 * N; j.dst[z] = ptmp[z]; }
@@ -1064,7 +1065,6 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         j.src_a = N;
         KL("ks_intt_p_cols", launch_inv_passB(j, tb, 2, nz, c->stream));
     }
-    // (5) ModDown pass 1: lift p -> q_i
     {
         PassJob j = job0();
         for (int z = 0; z < nz; z++) { j.src[z] = ptmp[z]; j.dst[z] = md[z]; }
@@ -1075,7 +1075,6 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         j.smod_map[0] = j.smod_map[1] = (uint8_t)L;
         KL("ks_moddown_cols", launch_fwd_pass1(j, tb, 2 * l1, nz, true, c->stream));
     }
-    // (6) pass 2 + combine: out_i = (acc_i - NTT_i(y)) p^-1 (+ add)
     {
         PassJob j = job0();
         for (int z = 0; z < nz; z++) {
@@ -1094,6 +1093,41 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         Tables tc = c->tables(c->d_pinv);
         KL("ks_moddown_rows", launch_fwd_pass2(j, tc, 2 * l1, nz, true, c->stream));
     }
+    return HISA_OK;
+}
+
+// key switch of nz digits under ONE key: ModUp pass 1 -> fused pass 2 + key inner product (K4,
+// D never stored in NTT form) -> ModDown
+static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const KsBatch& kb) {
+    const int l1 = level + 1, l2 = level + 2, L = c->L;
+    const long long N = (long long)c->N;
+    // scratch per ciphertext: dtil l1, T1 l1*l2, acc 2*l2, ptmp 2, md 2*l1
+    const size_t per = (size_t)N * ((size_t)l1 + (size_t)l1 * l2 + 2 * l2 + 2 + 2 * l1);
+    uint64_t* scratch = dalloc_t<uint64_t>(c, per * nz);
+    if (!scratch) return fail(HISA_E_OOM, "key-switch scratch (%zu MiB)", per * nz * 8 >> 20);
+    uint64_t *dtil[MAXB], *t1[MAXB], *acc[MAXB], *ptmp[MAXB], *md[MAXB];
+    for (int z = 0; z < nz; z++) {
+        uint64_t* s = scratch + per * z;
+        dtil[z] = s; s += (size_t)l1 * N;
+        t1[z] = s; s += (size_t)l1 * l2 * N;
+        acc[z] = s; s += (size_t)2 * l2 * N;
+        ptmp[z] = s; s += (size_t)2 * N;
+        md[z] = s;
+    }
+    RET(ks_modup_pass1(c, nz, level, kb.d, dtil, t1));
+    {
+        KsJob kj;
+        memset(&kj, 0, sizeof kj);
+        for (int z = 0; z < nz; z++) { kj.t1[z] = t1[z]; kj.d[z] = kb.d[z]; kj.acc[z] = acc[z]; }
+        kj.key = key;
+        kj.l1 = l1;
+        kj.L = L;
+        kj.nz = nz;
+        for (int ri = 0; ri < l2; ri++) kj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+        Tables tb = c->tables();
+        KL("ks_ip_rows", launch_ks_ip(kj, tb, nz, c->stream));
+    }
+    RET(ks_moddown(c, nz, level, acc, ptmp, md, kb));
     dfree(c, scratch);
     return HISA_OK;
 }
@@ -1137,33 +1171,116 @@ extern "C" int hisa_mul(hisa_ctx* c, hisa_ct a, hisa_ct b, hisa_ct* out) {
     return HISA_OK;
 }
 
-// rotation of nz ciphertexts (same level, same amount): automorphism then key switch (A15)
+// Rotation (A15) with pre-permuted keys.  Stored rotation keys are key'_k = psi_g^-1(key_k)
+// (permuted once at keygen; hisa_key_export returns the canonical key).  Because psi_g is a ring
+// automorphism that commutes with the centred lifts of ModUp / ModDown (a signed coefficient
+// permutation), KS_k(psi_g(c1)) = psi_g(KS'_k(c1)), so
+//     rotLeft(c, k) = psi_g( (c0 + KS'_k(c1)_0, KS'_k(c1)_1) )
+// -- bit-identical to "automorphism, then key switch" (A14, A37), with the ModUp of c1 shared
+// by every amount (hoisting) and the permutation applied once to the output.
+static int normalize_rot(const hisa_ctx* c, int64_t k, uint64_t* out) {
+    const int64_t s = (int64_t)(c->N / 2);
+    int64_t kk = k % s;
+    if (kk < 0) kk += s;
+    *out = (uint64_t)kk;
+    return HISA_OK;
+}
+static uint64_t galois(const hisa_ctx* c, uint64_t k) { return h_pow(5, k, 2 * c->N); }
+
+// rotation of nz ciphertexts (same level, same amount, own key switch each): batched K4 path
 static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_t** outs) {
     const int level = in[0]->level, l1 = level + 1;
     const long long N = (long long)c->N;
     auto it = c->rot_keys.find(k);
     if (it == c->rot_keys.end()) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)k);
-    const uint64_t g = h_pow(5, k, 2 * c->N);
-    uint64_t* perm = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N * nz);
-    if (!perm) return fail(HISA_E_OOM, "rotation scratch");
-    const uint64_t* ins[MAXB];
-    uint64_t* ps[MAXB];
+    uint64_t* pre = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N * nz);
+    if (!pre) return fail(HISA_E_OOM, "rotation scratch");
+    const uint64_t* pres[MAXB];
+    uint64_t gs[MAXB];
     KsBatch kb;
     memset(&kb, 0, sizeof kb);
     for (int z = 0; z < nz; z++) {
-        ins[z] = in[z]->ptr;
-        ps[z] = perm + (size_t)2 * l1 * N * z;
         outs[z] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
         if (!outs[z]) return fail(HISA_E_OOM, "rotation output");
-        kb.d[z] = ps[z] + l1 * N;
-        kb.out[z] = outs[z];
-        kb.add[z] = ps[z];
+        kb.d[z] = in[z]->ptr + l1 * N;
+        kb.out[z] = pre + (size_t)2 * l1 * N * z;
+        kb.add[z] = in[z]->ptr;
+        pres[z] = kb.out[z];
+        gs[z] = galois(c, k);
     }
     kb.add_polys = 1;
     kb.add_a = 0;
-    KL("automorphism", launch_automorphism(ins, ps, nz, 2 * l1, c->log_n, g, c->stream));
     RET(keyswitch(c, nz, level, it->second, kb));
-    dfree(c, perm);
+    KL("automorphism", launch_automorphism(pres, outs, nz, 2 * l1, c->log_n, gs, c->stream));
+    dfree(c, pre);
+    return HISA_OK;
+}
+
+// hoisted rotations of ONE ciphertext by n distinct non-zero amounts (K7): one ModUp (INTT +
+// lift + both forward passes, D materialised), then per chunk of MAXR amounts one streaming
+// inner product over the chunk's keys, a batched ModDown and a batched permutation
+static int rotate_hoisted(hisa_ctx* c, const Obj* o, const uint64_t* ks, int n, uint64_t** outs) {
+    const int level = o->level, l1 = level + 1, l2 = level + 2, L = c->L;
+    const long long N = (long long)c->N;
+    const int RC = std::min(n, MAXR);
+    const size_t per_amt = (size_t)N * (2 * l2 + 2 + 2 * l1 + 2 * l1);   // acc, ptmp, md, pre
+    const size_t base = (size_t)N * ((size_t)l1 + (size_t)l1 * l2);      // dtil, D
+    uint64_t* scratch = dalloc_t<uint64_t>(c, base + per_amt * RC);
+    if (!scratch) return fail(HISA_E_OOM, "hoisted rotation scratch (%zu MiB)", (base + per_amt * RC) * 8 >> 20);
+    for (int r = 0; r < n; r++) {
+        outs[r] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        if (!outs[r]) return fail(HISA_E_OOM, "rotation output");
+    }
+    uint64_t* dtil = scratch;
+    uint64_t* D = scratch + (size_t)l1 * N;
+    const uint64_t* d1[1] = {o->ptr + l1 * N};
+    uint64_t* dt[1] = {dtil};
+    uint64_t* Dp[1] = {D};
+    RET(ks_modup_pass1(c, 1, level, d1, dt, Dp));
+    {   // ModUp pass 2 in place: D_{j,r} for r != q_j, fully reduced
+        PassJob j = job0();
+        j.src[0] = D; j.dst[0] = D;
+        j.nb = l2;
+        j.src_a = j.dst_a = (long long)l2 * N;
+        j.src_b = j.dst_b = N;
+        j.skip_diag = 1;
+        for (int ri = 0; ri < l2; ri++) j.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+        Tables tb = c->tables();
+        KL("ks_modup_rows", launch_fwd_pass2(j, tb, l1 * l2, 1, false, c->stream));
+    }
+    for (int r0 = 0; r0 < n; r0 += MAXR) {
+        const int R = std::min(MAXR, n - r0);
+        uint64_t *acc[MAXB], *ptmp[MAXB], *md[MAXB];
+        const uint64_t* pres[MAXB];
+        uint64_t gs[MAXB];
+        KsBatch kb;
+        memset(&kb, 0, sizeof kb);
+        KsHoistJob hj;
+        memset(&hj, 0, sizeof hj);
+        for (int r = 0; r < R; r++) {
+            uint64_t* s = scratch + base + per_amt * r;
+            acc[r] = s; s += (size_t)2 * l2 * N;
+            ptmp[r] = s; s += (size_t)2 * N;
+            md[r] = s; s += (size_t)2 * l1 * N;
+            pres[r] = s;
+            kb.out[r] = s;
+            kb.add[r] = o->ptr;
+            gs[r] = galois(c, ks[r0 + r]);
+            hj.key[r] = c->rot_keys[ks[r0 + r]];
+            hj.acc[r] = acc[r];
+        }
+        kb.add_polys = 1;
+        kb.add_a = 0;
+        hj.D = D;
+        hj.diag = d1[0];
+        hj.l1 = l1;
+        hj.L = L;
+        for (int ri = 0; ri < l2; ri++) hj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+        KL("ks_ip_hoisted", launch_ks_ip_hoisted(hj, R, c->d_mods, c->log_n, c->stream));
+        RET(ks_moddown(c, R, level, acc, ptmp, md, kb));
+        KL("automorphism", launch_automorphism(pres, outs + r0, R, 2 * l1, c->log_n, gs, c->stream));
+    }
+    dfree(c, scratch);
     return HISA_OK;
 }
 
@@ -1171,17 +1288,16 @@ static int rot_common(hisa_ctx* c, hisa_ct h, int64_t k, hisa_ct* out) {
     CHECK_CTX(c);
     GET_CT(o, h);
     if (o->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext");
-    const int64_t s = (int64_t)(c->N / 2);
-    int64_t kk = k % s;
-    if (kk < 0) kk += s;
+    uint64_t kk;
+    normalize_rot(c, k, &kk);
     if (kk == 0) {
         if (!out) return HISA_OK;
         return hisa_copy(c, h, out);
     }
-    if (!c->rot_keys.count((uint64_t)kk)) return fail(HISA_E_NO_KEY, "no rotation key for %lld", (long long)kk);
+    if (!c->rot_keys.count(kk)) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk);
     uint64_t* res[1];
     Obj* ins[1] = {o};
-    RET(rotate_batch(c, ins, 1, (uint64_t)kk, res));
+    RET(rotate_batch(c, ins, 1, kk, res));
     return emit_ct(c, out, h, res[0], o->level, 2, o->scale);
 }
 extern "C" int hisa_rot_left(hisa_ctx* c, hisa_ct h, int64_t k, hisa_ct* out) { return rot_common(c, h, k, out); }
@@ -1204,18 +1320,17 @@ extern "C" int hisa_rot_left_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int
         if (objs[i]->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext at %zu", i);
         if (objs[i]->level != objs[0]->level) return fail(HISA_E_LEVEL_MISMATCH, "batch levels differ");
     }
-    const int64_t s = (int64_t)(c->N / 2);
-    int64_t kk = k % s;
-    if (kk < 0) kk += s;
+    uint64_t kk;
+    normalize_rot(c, k, &kk);
     if (kk == 0) {
         for (size_t i = 0; i < n; i++) RET(hisa_copy(c, in[i], &outs[i]));
         return HISA_OK;
     }
-    if (!c->rot_keys.count((uint64_t)kk)) return fail(HISA_E_NO_KEY, "no rotation key for %lld", (long long)kk);
+    if (!c->rot_keys.count(kk)) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk);
     for (size_t i0 = 0; i0 < n; i0 += MAXB) {
         const int nz = (int)std::min((size_t)MAXB, n - i0);
         uint64_t* res[MAXB];
-        RET(rotate_batch(c, objs.data() + i0, nz, (uint64_t)kk, res));
+        RET(rotate_batch(c, objs.data() + i0, nz, kk, res));
         for (int z = 0; z < nz; z++)
             outs[i0 + z] = new_handle(c, OBJ_CT, res[z], objs[i0 + z]->level, 2, objs[i0 + z]->scale);
     }
@@ -1224,10 +1339,32 @@ extern "C" int hisa_rot_left_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int
 
 extern "C" int hisa_rot_left_hoisted(hisa_ctx* c, hisa_ct h, const int64_t* k, size_t n, hisa_ct* outs) {
     CHECK_CTX(c);
-    if (!k || !outs) return fail(HISA_E_PARAMS, "null argument");
-    // v1: one rotation per amount (hoisted ModUp sharing is a later optimisation; results are
-    // bit-identical by A14)
-    for (size_t i = 0; i < n; i++) RET(hisa_rot_left(c, h, k[i], &outs[i]));
+    if ((!k || !outs) && n) return fail(HISA_E_PARAMS, "null argument");
+    GET_CT(o, h);
+    if (o->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext");
+    std::vector<uint64_t> kk(n);
+    for (size_t i = 0; i < n; i++) {
+        normalize_rot(c, k[i], &kk[i]);
+        if (kk[i] && !c->rot_keys.count(kk[i]))
+            return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk[i]);
+    }
+    // non-zero amounts share one ModUp (hoisted path); a single one uses the fused K4 path
+    // (no D materialisation)
+    std::vector<size_t> nz_idx;
+    std::vector<uint64_t> amounts;
+    for (size_t i = 0; i < n; i++) {
+        if (kk[i] == 0) RET(hisa_copy(c, h, &outs[i]));
+        else { nz_idx.push_back(i); amounts.push_back(kk[i]); }
+    }
+    if (nz_idx.empty()) return HISA_OK;
+    std::vector<uint64_t*> res(nz_idx.size());
+    if (nz_idx.size() == 1) {
+        Obj* ins[1] = {o};
+        RET(rotate_batch(c, ins, 1, amounts[0], res.data()));
+    } else {
+        RET(rotate_hoisted(c, o, amounts.data(), (int)amounts.size(), res.data()));
+    }
+    for (size_t r = 0; r < nz_idx.size(); r++) outs[nz_idx[r]] = new_handle(c, OBJ_CT, res[r], o->level, 2, o->scale);
     return HISA_OK;
 }
 
@@ -1364,10 +1501,10 @@ __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restr
     }
 }
 
-extern "C" int hisa_conv_accumulate(hisa_ctx* c, const hisa_ct* in, size_t T, const double* W, size_t OC,
-                                    double pt_scale, hisa_ct* outs) {
+static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const double* W, size_t OC, double pt_scale,
+                           hisa_ct* outs, uint64_t* dev_out) {
     CHECK_CTX(c);
-    if (!in || !W || !outs || T == 0 || OC == 0) return fail(HISA_E_PARAMS, "bad arguments");
+    if (!in || !W || (!outs && !dev_out) || T == 0 || OC == 0) return fail(HISA_E_PARAMS, "bad arguments");
     std::vector<Obj*> objs(T);
     for (size_t t = 0; t < T; t++) {
         objs[t] = get_obj(c, in[t], OBJ_CT);
@@ -1392,7 +1529,7 @@ extern "C" int hisa_conv_accumulate(hisa_ctx* c, const hisa_ct* in, size_t T, co
     const long long N = (long long)c->N;
     std::vector<uint64_t*> optr(OC);
     for (size_t o = 0; o < OC; o++) {
-        optr[o] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        optr[o] = dev_out ? dev_out + (size_t)o * 2 * l1 * N : dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
         if (!optr[o]) return fail(HISA_E_OOM, "conv outputs");
     }
     std::vector<const uint64_t*> iptr(T);
@@ -1415,8 +1552,19 @@ extern "C" int hisa_conv_accumulate(hisa_ctx* c, const hisa_ct* in, size_t T, co
     dfree(c, dw);
     dfree(c, (void*)dip);
     dfree(c, (void*)dop);
-    for (size_t o = 0; o < OC; o++) outs[o] = new_handle(c, OBJ_CT, optr[o], level, 2, objs[0]->scale * ps);
+    if (outs)
+        for (size_t o = 0; o < OC; o++) outs[o] = new_handle(c, OBJ_CT, optr[o], level, 2, objs[0]->scale * ps);
     return HISA_OK;
+}
+extern "C" int hisa_conv_accumulate(hisa_ctx* c, const hisa_ct* in, size_t T, const double* W, size_t OC,
+                                    double pt_scale, hisa_ct* outs) {
+    if (!outs) return fail(HISA_E_PARAMS, "null outs");
+    return conv_acc_common(c, in, T, W, OC, pt_scale, outs, nullptr);
+}
+extern "C" int hisa_conv_accumulate_dev(hisa_ctx* c, const hisa_ct* in, size_t T, const double* W, size_t OC,
+                                        double pt_scale, uint64_t* dev_out) {
+    if (!dev_out) return fail(HISA_E_PARAMS, "null dev_out");
+    return conv_acc_common(c, in, T, W, OC, pt_scale, nullptr, dev_out);
 }
 
 // ============================================================================================
@@ -1500,6 +1648,17 @@ extern "C" int hisa_ct_adopt_device(hisa_ctx* c, const uint64_t* dev, int level,
     uint64_t* p = dalloc_t<uint64_t>(c, w);
     if (!p) return fail(HISA_E_OOM, "adopt");
     CK(cudaMemcpyAsync(p, dev, w * 8, cudaMemcpyDeviceToDevice, c->stream));
+    *out = new_handle(c, OBJ_CT, p, level, npolys, scale);
+    return HISA_OK;
+}
+extern "C" int hisa_ct_adopt_sum(hisa_ctx* c, const int64_t* dev, int level, int npolys, double scale, hisa_ct* out) {
+    CHECK_CTX(c);
+    if (!dev || !out) return fail(HISA_E_PARAMS, "null argument");
+    RET(check_layout(c, level, npolys));
+    const size_t w = (size_t)npolys * (level + 1) * c->N;
+    uint64_t* p = dalloc_t<uint64_t>(c, w);
+    if (!p) return fail(HISA_E_OOM, "adopt");
+    KL("reduce_sum", launch_reduce_sum(dev, p, npolys, level + 1, c->log_n, c->d_mods, c->stream));
     *out = new_handle(c, OBJ_CT, p, level, npolys, scale);
     return HISA_OK;
 }

@@ -99,4 +99,63 @@ cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_
     return cudaErrorInvalidValue;
 }
 
+// ------------------------------------------------------------------------------------------
+// K7 hoisted inner product: R rotation amounts share one materialised ModUp output D (hoisting,
+// P:717 "rotations ... code motioned out").  Each thread owns two words of one output prime ri,
+// streams D[j][ri] once and the R keys' (b, a) limbs, and keeps 2R 128-bit accumulators per word.
+// Pure HBM stream: (1 + 2R) 16-byte loads per digit per thread, no shared memory.
+// ------------------------------------------------------------------------------------------
+template <int R>
+__global__ void __launch_bounds__(256) k_ks_ip_hoisted(KsHoistJob job, const Mod* __restrict__ mods, int log_n) {
+    const int ri = blockIdx.y;
+    const int l1 = job.l1, l2 = l1 + 1;
+    const long long N = 1ll << log_n;
+    const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+    if (x >= N) return;
+    const int mi = job.mod_map[ri];
+    const Mod md = mods[mi];
+    U128 acc[R][2][2];
+#pragma unroll
+    for (int k = 0; k < R; k++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) { acc[k][h][0] = U128{0, 0}; acc[k][h][1] = U128{0, 0}; }
+    const long long kstride_j = 2ll * (job.L + 1) * N;
+    const long long kstride_p = (long long)(job.L + 1) * N;
+    const long long koff = (long long)mi * N + x;
+    for (int j = 0; j < l1; j++) {
+        const uint64_t* src = (j == ri) ? job.diag + (long long)j * N + x : job.D + ((long long)j * l2 + ri) * N + x;
+        const ulonglong2 d = __ldcs(reinterpret_cast<const ulonglong2*>(src));
+#pragma unroll
+        for (int k = 0; k < R; k++) {
+            const uint64_t* kb = job.key[k] + j * kstride_j + koff;
+            const ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2*>(kb));
+            const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(kb + kstride_p));
+            mac128(acc[k][0][0], d.x, b.x);
+            mac128(acc[k][0][1], d.y, b.y);
+            mac128(acc[k][1][0], d.x, a.x);
+            mac128(acc[k][1][1], d.y, a.y);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < R; k++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            uint64_t* o = job.acc[k] + ((long long)h * l2 + ri) * N + x;
+            *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(barrett128(acc[k][h][0].lo, acc[k][h][0].hi, md),
+                                                                barrett128(acc[k][h][1].lo, acc[k][h][1].hi, md));
+        }
+}
+
+cudaError_t launch_ks_ip_hoisted(const KsHoistJob& job, int R, const Mod* mods, int log_n, cudaStream_t st) {
+    const long long N = 1ll << log_n;
+    dim3 grid((unsigned)((N / 2 + 255) / 256), job.l1 + 1, 1);
+    switch (R) {
+#define C(RR) case RR: k_ks_ip_hoisted<RR><<<grid, 256, 0, st>>>(job, mods, log_n); break;
+        C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8)
+#undef C
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace hisa

@@ -34,9 +34,28 @@ struct ElemJob {
 };
 cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, cudaStream_t st);
 
-// automorphism psi_g in the NTT domain (K6): out[j] = in[perm_g[j]] on every limb
+// automorphism psi_g in the NTT domain (K6): out[j] = in[perm_g[j]] on every limb; gs[z] is the
+// Galois element of batch entry z (one per ciphertext: hoisted rotations permute by different g)
 cudaError_t launch_automorphism(const uint64_t* const* in, uint64_t* const* out, int nz, int nlimbs_total,
-                                int log_n, uint64_t g, cudaStream_t st);
+                                int log_n, const uint64_t* gs, cudaStream_t st);
+
+// hoisted key-switch inner product (K7): for R rotation amounts sharing one ModUp output D,
+// acc_k[b|a][ri] = sum_j D[j][ri] (.) key_k[j][b|a][ri] -- an HBM stream of the R keys
+constexpr int MAXR = 8;
+struct KsHoistJob {
+    const uint64_t* D;            // [j][ri][N], ri over l+2 output primes (diagonal entries unused)
+    const uint64_t* diag;         // the digit source in NTT form [(l+1)][N] (D_{j,q_j} = d_j)
+    const uint64_t* key[MAXR];    // [L][2][L+1][N] per amount (pre-permuted, see hisa.cu)
+    uint64_t* acc[MAXR];          // out [2][l+2][N], fully reduced
+    int l1;
+    int L;
+    uint8_t mod_map[MAXL];
+};
+cudaError_t launch_ks_ip_hoisted(const KsHoistJob& job, int R, const Mod* mods, int log_n, cudaStream_t st);
+
+// int64 sum of <= 8 fully reduced residue arrays (the NCCL reduce-scatter output, a15) -> residues
+cudaError_t launch_reduce_sum(const int64_t* in, uint64_t* out, int npolys, int l1, int log_n, const Mod* mods,
+                              cudaStream_t st);
 
 // key-switch inner product fused with forward pass 2 (K4) -- ks_kernels.cu
 struct KsJob {

@@ -1,0 +1,442 @@
+"""HW-tiled encrypted CNN driver on libhisa.
+
+The CHET runtime's homomorphic tensor kernels lowered onto the HISA calls of
+``hisa.py`` -- argument marshalling and layout bookkeeping only; every ciphertext word is
+produced by the sm_100a kernels behind the C-ABI.
+
+  * CipherTensor metadata: C ciphertexts (HW-tiling), valid H x W at slot
+    origin + y*hS + x*wS, `clean` = zeros outside the valid slots.
+  * conv2d = Alg. 1: the IC*K^2 rotations are hoisted out of the output-channel
+    loop AND share one ModUp per input channel (hisa_rot_left_hoisted, K7); the
+    mulScalar + add accumulation over all (ic, tap) for all OC outputs is ONE fused kernel
+    (hisa_conv_accumulate, K8); one divScalar per output.
+  * activation a0 + a1 x + a2 x^2 (A25) folded to sign(a2) x'^2 + const: one level.
+  * 2x2 average pool: three hoisted rotations + adds, 1/4 folded forward (A26).
+  * FC / matmul (A27, R = 1): mulPlain per input channel, rescale, rotate-and-sum
+    with every output neuron's rotation batched under one key (hisa_rot_left_batch).
+  * multi-GPU: input channels of every conv / FC are partitioned across ranks;
+    each rank accumulates partial sums for ALL outputs (hisa_conv_accumulate_dev into a torch
+    int64 buffer), one NCCL reduce-scatter (int64 SUM, exact: partials < 2^60, <= 8 ranks)
+    hands every rank its own output channels, hisa_ct_adopt_sum reduces them mod q_i, and the
+    owner rescales / activates -- its outputs are exactly its input shard of the next layer.
+
+The lowering is written down in DESIGN.md section 5 and implemented independently (without
+shared code) by oracle/nets.py; ciphertexts are compared bit for bit by tests/test_driver.py.
+
+A symbolic backend (`Symbolic`) executes the same driver on metadata only -- the paper's
+symbolic analysers: it yields the level plan, the distinct rotation amounts for
+key generation and the operation counts, and never touches ciphertext data.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+
+# ------------------------------------------------------------------------------ layouts
+@dataclass(frozen=True)
+class Layout:
+    """CipherTensor metadata.  kind "hw": channel c's valid H x W plane at slots
+    origin + y*hS + x*wS; kind "slot0": one value per ciphertext, in slot 0."""
+    kind: str
+    C: int
+    H: int = 1
+    W: int = 1
+    hS: int = 0
+    wS: int = 0
+    origin: int = 0
+    clean: bool = False
+
+    def slots_of_valid(self) -> np.ndarray:
+        y, x = np.meshgrid(np.arange(self.H), np.arange(self.W), indexing="ij")
+        return (self.origin + y * self.hS + x * self.wS).ravel()
+
+
+def act_fold(coeffs):
+    """A25: a2 x^2 + a1 x + a0 = x'^2 + gamma with x' = r x + beta (a2 > 0)."""
+    a0, a1, a2 = coeffs
+    if not a2 > 0:
+        raise ValueError("folded activation needs a2 > 0")
+    r = math.sqrt(a2)
+    return r, r * a1 / (2 * a2), a0 - a1 * a1 / (4 * a2)
+
+
+def compile_weights(net: dict, weights, act_coeffs):
+    """Compile-time weight rewriting: avg-pool 1/4 factors pushed into the next linear layer
+    (A26) and the activation scale / bias folded into the preceding one (A25).
+    Returns ([(W', beta)] per linear layer, gamma)."""
+    r, beta, gamma = act_fold(act_coeffs)
+    layers = net["layers"]
+    out, pending, it = [], 1.0, iter(weights)
+    for i, layer in enumerate(layers):
+        if layer[0] == "avgpool":
+            pending *= 0.25
+        elif layer[0] in ("conv", "fc"):
+            nxt_act = i + 1 < len(layers) and layers[i + 1][0] == "act"
+            w = np.asarray(next(it), dtype=np.float64) * pending * (r if nxt_act else 1.0)
+            out.append((w, beta if nxt_act else 0.0))
+            pending = 1.0
+    return out, gamma
+
+
+def input_layout(net: dict) -> Layout:
+    """The client's packing (A24): zero padding of the first conv materialised."""
+    c, h, w = net["input"]
+    first = net["layers"][0]
+    p = first[4] if first[0] == "conv" else 0
+    hs = w + 2 * p
+    return Layout("hw", c, h, w, hs, 1, p * hs + p, True)
+
+
+# ------------------------------------------------------------------------------ symbolic backend
+class Symbolic:
+    """Metadata-only HISA backend (the paper's symbolic analysers)."""
+
+    def __init__(self, log_n: int, moduli):
+        self.slots = (1 << log_n) // 2
+        self.q = list(moduli)
+        self.cts = {}
+        self.next = 1
+        self.rotations = set()
+        self.counts = {}
+
+    def _new(self, level, scale):
+        h = self.next
+        self.next += 1
+        self.cts[h] = (level, scale)
+        return h
+
+    def _count(self, op, n=1):
+        self.counts[op] = self.counts.get(op, 0) + n
+
+    def ct_info(self, h):
+        lv, sc = self.cts[h]
+        return lv, 2, sc
+
+    def free(self, h):
+        self.cts.pop(h, None)
+
+    def fresh(self, level, scale):
+        return self._new(level, scale)
+
+    def rot_left_hoisted(self, h, ks):
+        lv, sc = self.cts[h]
+        out = []
+        for k in ks:
+            kk = k % self.slots
+            if kk:
+                self.rotations.add(kk)
+                self._count("rot_hoisted")
+            out.append(self._new(lv, sc))
+        return out
+
+    def rot_left_batch(self, hs, k):
+        kk = k % self.slots
+        if kk:
+            self.rotations.add(kk)
+            self._count("rot", len(hs))
+        return [self._new(*self.cts[h]) for h in hs]
+
+    def conv_accumulate(self, hs, W, pt_scale=0.0):
+        lv, sc = self.cts[hs[0]]
+        n_out = len(W) // len(hs)
+        self._count("scalar_mac_ct", len(W))
+        return [self._new(lv, sc * float(self.q[lv])) for _ in range(n_out)]
+
+    def rescale(self, h):
+        lv, sc = self.cts[h]
+        if lv == 0:
+            raise RuntimeError("level budget exhausted (MODULUS_EXHAUSTED)")
+        self._count("rescale")
+        return self._new(lv - 1, sc / float(self.q[lv]))
+
+    def mul(self, a, b):
+        lv, sa = self.cts[a]
+        self._count("mul_relin")
+        return self._new(lv, sa * self.cts[b][1])
+
+    def add(self, a, b):
+        self._count("add")
+        return self._new(*self.cts[a])
+
+    def add_scalar(self, a, x):
+        return self._new(*self.cts[a])
+
+    def encode(self, v, scale, level):
+        self._count("encode")
+        return ("pt", level, scale)
+
+    def mul_plain(self, a, p):
+        lv, sc = self.cts[a]
+        self._count("mul_plain")
+        return self._new(lv, sc * p[2])
+
+
+# ------------------------------------------------------------------------------ the network
+class EncryptedNet:
+    """One network on one backend (a hisa.Context, or Symbolic for planning).
+
+    `group` (torch.distributed process group, optional) shards every linear layer's input
+    channels across ranks; None = single GPU."""
+
+    def __init__(self, backend, net: dict, weights, act_coeffs, group=None):
+        self.b = backend
+        self.net = net
+        self.folded, self.gamma = compile_weights(net, weights, act_coeffs)
+        self.slots = backend.slots
+        self.q = list(backend.q)
+        self._pts = {}
+        self.group = group
+        if group is not None:
+            import torch.distributed as dist
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+
+    # ---- planning (symbolic execution) ------------------------------------------------------
+    @staticmethod
+    def plan(net: dict, weights, act_coeffs, moduli):
+        """Level plan, distinct rotation amounts (keygen input), op counts."""
+        sym = Symbolic(net["log_n"], moduli)
+        en = EncryptedNet(sym, net, weights, act_coeffs)
+        lay = input_layout(net)
+        top = len(moduli) - 2
+        cts = [sym.fresh(top, net["scale"]) for _ in range(lay.C)]
+        outs, out_lay = en.forward(cts, lay)
+        final = sym.cts[outs[0]][0]
+        return {"rotations": sorted(sym.rotations), "final_level": final, "levels_used": top - final,
+                "counts": dict(sym.counts), "out_layout": out_lay}
+
+    # ---- sharding ---------------------------------------------------------------
+    def owned(self, n: int) -> range:
+        """Contiguous block of channel indices owned by this rank (rank r gets block r)."""
+        per = -(-n // self.world)
+        return range(min(n, self.rank * per), min(n, (self.rank + 1) * per))
+
+    # ---- client ---------------------------------------------------------------------------
+    def encrypt_image(self, image):
+        """Encode + encrypt the packed image (client side), one ciphertext per channel."""
+        lay = input_layout(self.net)
+        cts = []
+        for c in range(lay.C):
+            v = np.zeros(self.slots)
+            v[lay.slots_of_valid()] = np.asarray(image[c], dtype=np.float64).ravel()
+            pt = self.b.encode(v, self.net["scale"], -1)
+            cts.append(self.b.encrypt(pt))
+            self.b.free(pt)
+        return cts, lay
+
+    def decrypt_output(self, cts, lay) -> np.ndarray:
+        vals = []
+        for ct in cts:
+            pt = self.b.decrypt(ct)
+            vals.append(self.b.decode(pt, self.slots))
+            self.b.free(pt)
+        if lay.kind == "slot0":
+            return np.array([v[0] for v in vals])
+        idx = lay.slots_of_valid()
+        return np.stack([v[idx] for v in vals]).reshape(lay.C, lay.H, lay.W)
+
+    # ---- helpers --------------------------------------------------------------------------
+    def _plaintext(self, key, values_fn, level):
+        """Weight / mask plaintexts at scale q_top (A8), encoded once per model (cached)."""
+        pt = self._pts.get((key, level))
+        if pt is None:
+            pt = self.b.encode(values_fn(), float(self.q[level]), level)
+            self._pts[(key, level)] = pt
+        return pt
+
+    def _free_all(self, hs, keep=()):
+        keep = set(keep)
+        for h in hs:
+            if h not in keep:
+                self.b.free(h)
+
+    def _level(self, h):
+        return self.b.ct_info(h)[0]
+
+    # ---- layers ---------------------------------------------------------------------------
+    def mask(self, cts, lay, li):
+        """Zero the invalid slots before a padded conv: mulPlain by the 0/1 mask,
+        rescale.  One level."""
+        idx = lay.slots_of_valid()
+
+        def vals():
+            v = np.zeros(self.slots)
+            v[idx] = 1.0
+            return v
+        out = []
+        for ct in cts:
+            pt = self._plaintext(("mask", li), vals, self._level(ct))
+            m = self.b.mul_plain(ct, pt)
+            out.append(self.b.rescale(m))
+            self.b.free(m)
+        return out, replace(lay, clean=True)
+
+    def conv(self, cts, lay, layer, w, beta, li):
+        """Alg. 1: hoisted rotations per input channel + fused accumulation."""
+        _, oc_n, k, st, p = layer
+        own_in = self.owned(lay.C)
+        if p > 0 and not lay.clean:
+            cts, lay = self.mask(cts, lay, li)
+            masked = True
+        else:
+            masked = False
+        amounts = [(lay.origin + (i - p) * lay.hS + (j - p) * lay.wS) % self.slots
+                   for i in range(k) for j in range(k)]
+        rotated, wcols = [], []
+        for ci, ct in zip(own_in, cts):
+            rs = self.b.rot_left_hoisted(ct, amounts)
+            rotated += rs
+            wcols.append(w[:, ci].reshape(oc_n, k * k))
+        wmat = np.concatenate(wcols, axis=1) if wcols else np.zeros((oc_n, 0))
+        outs = self._accumulate(rotated, wmat, oc_n)
+        self._free_all(rotated)
+        if masked:
+            self._free_all(cts)
+        res = []
+        for h in outs:
+            r = self.b.rescale(h)
+            self.b.free(h)
+            if beta:
+                r2 = self.b.add_scalar(r, beta)
+                self.b.free(r)
+                r = r2
+            res.append(r)
+        nl = Layout("hw", oc_n, (lay.H + 2 * p - k) // st + 1, (lay.W + 2 * p - k) // st + 1,
+                    lay.hS * st, lay.wS * st, 0, False)
+        return res, nl
+
+    def _accumulate(self, rotated, wmat, n_out):
+        """sum_t W[o, t] rotated[t] for o < n_out (pre-rescale).  Single GPU: one fused kernel.
+        Multi-GPU: partial sums over this rank's inputs for ALL outputs, NCCL reduce-scatter,
+        mod-q fix-up; returns the outputs this rank owns (owned(n_out))."""
+        if self.world == 1:
+            return self.b.conv_accumulate(rotated, wmat.ravel())
+        from . import parallel
+        return parallel.reduce_scatter_partials(self, rotated, wmat, n_out)
+
+    def act(self, cts, lay, square_only=False):
+        """(A25) x'^2 + gamma: tensor + relinearize + rescale (+ addScalar): one level."""
+        out = []
+        for ct in cts:
+            sq = self.b.mul(ct, ct)
+            r = self.b.rescale(sq)
+            self.b.free(sq)
+            if not square_only and self.gamma:
+                r2 = self.b.add_scalar(r, self.gamma)
+                self.b.free(r)
+                r = r2
+            out.append(r)
+        return out, replace(lay, clean=False)
+
+    def avgpool(self, cts, lay):
+        """2x2 average pool (A26): x + rot(wS) + rot(hS) + rot(hS + wS), hoisted."""
+        out = []
+        for ct in cts:
+            r = self.b.rot_left_hoisted(ct, [lay.wS, lay.hS, lay.hS + lay.wS])
+            s1 = self.b.add(ct, r[0])
+            s2 = self.b.add(r[1], r[2])
+            out.append(self.b.add(s1, s2))
+            self._free_all(r + [s1, s2])
+        return out, Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
+
+    def fc(self, cts, lay, layer, w, beta, li):
+        """Matmul (A27, R = 1)."""
+        n_out = layer[1]
+        if lay.kind == "slot0":          # next FC reads slot 0: scalar MACs, fused
+            own = self.owned(lay.C)
+            outs = self._accumulate(list(cts), w[:, own.start:own.stop], n_out)
+            res = [self.b.rescale(h) for h in outs]
+            self._free_all(outs)
+            return self._bias(res, beta), Layout("slot0", n_out)
+        idx = lay.slots_of_valid()
+        hw = lay.H * lay.W
+        own_in = self.owned(lay.C)
+        span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+        steps = math.ceil(math.log2(span))
+        lv = self._level(cts[0]) if cts else None
+        sums = []
+        for jo in range(n_out):
+            acc = None
+            for ci, ct in zip(own_in, cts):
+                def vals(jo=jo, ci=ci):
+                    v = np.zeros(self.slots)
+                    v[idx] = w[jo, ci * hw:(ci + 1) * hw]
+                    return v
+                pt = self._plaintext(("fc", li, jo, ci), vals, lv)
+                term = self.b.mul_plain(ct, pt)
+                if acc is None:
+                    acc = term
+                else:
+                    nxt = self.b.add(acc, term)
+                    self._free_all([acc, term])
+                    acc = nxt
+            sums.append(acc)
+        if self.world > 1:
+            from . import parallel
+            sums = parallel.reduce_scatter_cts(self, sums, n_out)
+        res = [self.b.rescale(h) for h in sums]
+        self._free_all(sums)
+        for t in range(steps):          # rotate-and-sum, every neuron under one key per step
+            rs = self.b.rot_left_batch(res, 1 << t)
+            nxt = [self.b.add(a, r) for a, r in zip(res, rs)]
+            self._free_all(res + rs)
+            res = nxt
+        return self._bias(res, beta), Layout("slot0", n_out)
+
+    def _bias(self, cts, beta):
+        if not beta:
+            return cts
+        out = [self.b.add_scalar(h, beta) for h in cts]
+        self._free_all(cts)
+        return out
+
+    # ---- forward ----------------------------------------------------------------------------
+    def forward(self, cts, lay, trace=None):
+        """Server-side evaluation of the whole network.  With a process group, `cts` are this
+        rank's owned input channels and the result is this rank's owned output channels.
+        `trace(layer_index, cts, layout)` (optional) is called after every layer, before the
+        layer's inputs are freed (per-layer parity checks)."""
+        wi = 0
+        cur = list(cts)
+        for li, layer in enumerate(self.net["layers"]):
+            kind = layer[0]
+            if kind in ("conv", "fc"):
+                w, beta = self.folded[wi]
+                wi += 1
+                fn = self.conv if kind == "conv" else self.fc
+                nxt, lay = fn(cur, lay, layer, w, beta, li)
+            elif kind == "act":
+                nxt, lay = self.act(cur, lay)
+            elif kind == "square":
+                nxt, lay = self.act(cur, lay, square_only=True)
+            elif kind == "avgpool":
+                nxt, lay = self.avgpool(cur, lay)
+            else:
+                raise ValueError(kind)
+            self._free_all(cur, keep=cts)
+            cur = nxt
+            if trace is not None:
+                trace(li, cur, lay)
+        return cur, lay
+
+    def forward_gathered(self, cts, lay):
+        """forward() followed, under a process group, by the final all-gather: every rank ends
+        with all output ciphertexts (rank 0 decrypts)."""
+        out, lay = self.forward(cts, lay)
+        if self.world > 1:
+            from . import parallel
+            allc = parallel.gather_outputs(self, out, lay.C)
+            self._free_all(out)
+            out = allc
+        return out, lay
+
+    def shard_input(self, cts):
+        """This rank's owned input channels of a full list (the rest are freed)."""
+        own = self.owned(len(cts))
+        mine = [cts[i] for i in own]
+        self._free_all([h for i, h in enumerate(cts) if i not in own])
+        return mine

@@ -85,6 +85,8 @@ _SIGS = {
     "hisa_rot_left_hoisted": [_vp, _cu64, _i64p, _csz, _u64p],
     "hisa_rot_left_batch": [_vp, _u64p, _csz, _ci64, _u64p],
     "hisa_conv_accumulate": [_vp, _u64p, _csz, _dp, _csz, _cd, _u64p],
+    "hisa_conv_accumulate_dev": [_vp, _u64p, _csz, _dp, _csz, _cd, _vp],
+    "hisa_ct_adopt_sum": [_vp, _vp, _ci, _ci, _cd, _u64p],
     "hisa_ntt": [_vp, _cu64, _ci],
     "hisa_ntt_batch": [_vp, _u64p, _csz, _ci],
     "hisa_ct_info": [_vp, _cu64, ctypes.POINTER(_ci), ctypes.POINTER(_ci), ctypes.POINTER(_cd)],
@@ -335,6 +337,19 @@ def hisa_conv_accumulate(ctx, cts, W, pt_scale: float = 0.0) -> list[int]:
     _chk(load().hisa_conv_accumulate(ctx, _ptr(ins, _u64p), ins.size, _ptr(w, _dp), oc, float(pt_scale),
                                      _ptr(outs, _u64p)))
     return [int(x) for x in outs]
+
+
+def hisa_conv_accumulate_dev(ctx, cts, W, dev_out: int, pt_scale: float = 0.0):
+    """Accumulation into caller device memory (uint64 [OC][2][l+1][N] at address dev_out)."""
+    ins = _u64(list(cts))
+    w = np.ascontiguousarray(W, dtype=np.float64)
+    oc = w.size // max(ins.size, 1)
+    _chk(load().hisa_conv_accumulate_dev(ctx, _ptr(ins, _u64p), ins.size, _ptr(w, _dp), oc, float(pt_scale),
+                                         _vp(dev_out)))
+
+
+def hisa_ct_adopt_sum(ctx, dev_ptr: int, level: int, npolys: int, scale: float) -> int:
+    return _h1(load().hisa_ct_adopt_sum, ctx, _vp(dev_ptr), level, npolys, float(scale))
 
 
 def hisa_ntt(ctx, ct: int, inverse: bool = False):

@@ -1,0 +1,71 @@
+"""Synthetic CNN workloads of BASELINE.json configs 1, 3, 4, 5 (shapes, seeds, sigmas only).
+
+This module is workload DATA shared by the oracle side and the CUDA side: layer shapes as the
+configs state them, the seeded float64 weights / images (A34) and the fixed activation
+coefficients (A25).  It holds no encrypted-evaluation logic: the HW-tiled lowering (layouts,
+rotation amounts, folding, masks, level plan) is implemented independently by
+``paper_1810_00845_b200/driver.py`` and ``oracle/nets.py``.
+
+Layer tuples (PyTorch semantics for the float64 definition):
+    ("conv", oc, k, stride, pad)   cross-correlation, zero padding `pad`
+    ("act",)                       a0 + a1 x + a2 x^2 with ACT_COEFFS (A25)
+    ("square",)                    x^2 (config 1)
+    ("avgpool",)                   2x2, stride 2
+    ("fc", out)                    W @ flatten(x) (flatten order c, y, x)
+    ("gap",)                       global average pool (config 5)
+Convs and FCs have no bias (A34).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import image as _image, weights as _weights
+
+# A25: (a0, a1, a2) -- SPEC's example activation values a = 0.25 (x^2), b = 0.5 (x)
+ACT_COEFFS = (0.0, 0.5, 0.25)
+
+NETS = {
+    # config 1: tiny encrypted conv (BASELINE.json configs[0])
+    "tiny": dict(log_n=13, q_bits=[60, 40, 40], p_bits=60, scale=2.0 ** 40, input=(1, 8, 8),
+                 layers=[("conv", 2, 3, 1, 0), ("square",)], sigma=[0.1]),
+    # config 3: LeNet-5-small-shaped (A31: pad 1 -> 30x30, 5x5 stride 2 -> 13x13x5 = 845)
+    "lenet_small": dict(log_n=14, q_bits=[60] + [40] * 6, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
+                        layers=[("conv", 5, 5, 2, 1), ("act",), ("fc", 100), ("act",), ("fc", 10)],
+                        sigma=[0.1, 0.1, 0.1]),
+    # config 4: LeNet-5-large-shaped (A32: SAME 5x5 convs, 28 -> 14 -> 7, 7*7*64 = 3136)
+    "lenet_large": dict(log_n=15, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
+                        layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2), ("act",),
+                                ("avgpool",), ("fc", 512), ("act",), ("fc", 10)],
+                        sigma=[0.05, 0.05, 0.05, 0.05]),
+}
+
+
+def linear_shapes(name: str):
+    """Weight shapes of the net's conv / fc layers in order (OC, IC, K, K) / (OUT, IN)."""
+    net = NETS[name]
+    c, h, w = net["input"]
+    shapes = []
+    for layer in net["layers"]:
+        if layer[0] == "conv":
+            _, oc, k, s, p = layer
+            shapes.append((oc, c, k, k))
+            c, h, w = oc, (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+        elif layer[0] == "avgpool":
+            h, w = h // 2, w // 2
+        elif layer[0] == "fc":
+            shapes.append((layer[1], c * h * w))
+            c, h, w = layer[1], 1, 1
+        elif layer[0] == "gap":
+            h, w = 1, 1
+    return shapes
+
+
+def net_weights(name: str, seed: int = 1000):
+    """A34: N(0, sigma_i) float64 weights, layer i drawn from PCG64(seed + i)."""
+    net = NETS[name]
+    return [_weights(seed + i, shp, net["sigma"][i]) for i, shp in enumerate(linear_shapes(name))]
+
+
+def net_image(name: str, seed: int = 0) -> np.ndarray:
+    """A34: uniform[0, 1] (C, H, W) image from PCG64(seed) (stand-in for MNIST / CIFAR-10)."""
+    return _image(seed, NETS[name]["input"])

@@ -1,0 +1,208 @@
+"""Host-side driver logic (no GPU): the symbolic planner (the paper's analysers),
+the compile-time folding (A25, A26), the oracle's lowering pinned to the float64 definition on
+small networks that exercise every branch, and the multi-rank path over gloo (world size 2)."""
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from synth import nets as SN
+
+
+def _moduli(net):
+    from oracle.ckks import Oracle
+    return Oracle(net["log_n"], net["q_bits"], net["p_bits"]).moduli
+
+
+# every lowering branch: padded first conv, act, avgpool, SAME conv on a pooled (unclean)
+# input -> mask, FC from the HW layout (mulPlain + rotate-and-sum), FC from slot 0
+MINI = dict(log_n=11, q_bits=[60] + [40] * 8, p_bits=60, scale=2.0 ** 40, input=(2, 8, 8),
+            layers=[("conv", 2, 3, 1, 1), ("act",), ("avgpool",), ("conv", 2, 3, 1, 1), ("act",),
+                    ("fc", 3), ("act",), ("fc", 2)], sigma=[0.3, 0.3, 0.3, 0.3])
+
+
+def _mini_weights():
+    shapes = [(2, 2, 3, 3), (2, 2, 3, 3), (3, 2 * 4 * 4), (2, 3)]
+    return [SN._weights(77 + i, s, 0.3) for i, s in enumerate(shapes)]
+
+
+def test_plan_tiny_rotation_set_and_levels():
+    from paper_1810_00845_b200.driver import EncryptedNet
+    net = SN.NETS["tiny"]
+    pl = EncryptedNet.plan(net, SN.net_weights("tiny"), SN.ACT_COEFFS, _moduli(net))
+    # 3x3 taps on an 8-wide channel: fh*8 + fw
+    assert pl["rotations"] == [1, 2, 8, 9, 10, 16, 17, 18]
+    assert pl["levels_used"] == 2 and pl["final_level"] == 0        # A28: 2 of 2
+    assert pl["counts"]["rot_hoisted"] == 8                          # IC * (K^2 - 1)
+
+
+def test_plan_spec_example_rotation_set():
+    """a 3x3 filter on a 5x5 channel with hS = 5 needs left rotations
+    {1, 2, 5, 6, 7, 10, 11, 12}; rotations counted IC * (K^2 - 1), independent of OC."""
+    from paper_1810_00845_b200.driver import EncryptedNet
+    for oc in (1, 4):
+        net = dict(log_n=10, q_bits=[60, 40], p_bits=60, scale=2.0 ** 40, input=(3, 5, 5),
+                   layers=[("conv", oc, 3, 1, 0)], sigma=[0.1])
+        w = [SN._weights(1, (oc, 3, 3, 3), 0.1)]
+        pl = EncryptedNet.plan(net, w, SN.ACT_COEFFS, _moduli(net))
+        assert pl["rotations"] == [1, 2, 5, 6, 7, 10, 11, 12]
+        assert pl["counts"]["rot_hoisted"] == 3 * 8
+        assert pl["counts"]["scalar_mac_ct"] == oc * 3 * 9
+
+
+def test_plan_lenet_small_levels():
+    from paper_1810_00845_b200.driver import EncryptedNet
+    net = SN.NETS["lenet_small"]
+    pl = EncryptedNet.plan(net, SN.net_weights("lenet_small"), SN.ACT_COEFFS, _moduli(net))
+    assert pl["levels_used"] == 5                                    # A28: 5 of 6
+    assert pl["counts"]["rot_hoisted"] == 24
+    # FC1 rotate-and-sum: 100 neurons x ceil(log2(12*60 + 12*2 + 1)) = 10 steps
+    assert pl["counts"]["rot"] == 100 * 10
+
+
+def test_fold_identity():
+    """A25: a2 x^2 + a1 x + a0 == (r x + beta)^2 + gamma (the folded form, one level)."""
+    from paper_1810_00845_b200.driver import act_fold
+    x = np.linspace(-3, 3, 101)
+    for coeffs in (SN.ACT_COEFFS, (0.1, -0.7, 2.0), (1.0, 0.0, 0.5)):
+        r, beta, gamma = act_fold(coeffs)
+        a0, a1, a2 = coeffs
+        assert np.allclose((r * x + beta) ** 2 + gamma, a0 + a1 * x + a2 * x * x, atol=1e-12)
+
+
+def test_compile_weights_pool_and_act_factors():
+    from paper_1810_00845_b200.driver import compile_weights
+    w = _mini_weights()
+    folded, gamma = compile_weights(MINI, w, SN.ACT_COEFFS)
+    r = math.sqrt(SN.ACT_COEFFS[2])
+    assert np.allclose(folded[0][0], w[0] * r) and folded[0][1] == pytest.approx(0.5)   # act after
+    assert np.allclose(folded[1][0], w[1] * 0.25 * r)                                    # pool before
+    assert np.allclose(folded[3][0], w[3]) and folded[3][1] == 0.0                       # last layer
+    assert gamma == pytest.approx(-0.25)
+
+
+def test_oracle_net_tiny_matches_float64():
+    from oracle import plain
+    from oracle.nets import OracleNet
+    net = SN.NETS["tiny"]
+    W = SN.net_weights("tiny")
+    img = SN.net_image("tiny", 3)
+    on = OracleNet(net, W, SN.ACT_COEFFS)
+    cts, lay = on.encrypt_image(img)
+    out, ol = on.forward(cts, lay)
+    got = on.decrypt_output(out, ol)
+    ref = plain.forward(net, img, W, SN.ACT_COEFFS)
+    assert got.shape == (2, 6, 6)
+    assert np.abs(got - ref).max() <= 1e-3
+    assert out[0].level == 0
+
+
+def test_oracle_net_every_branch_matches_float64():
+    """Pins the oracle's lowering (mask, SAME padding through wrap-around, pools, both FC
+    forms, folded activations) to the float64 definition of the network."""
+    from oracle import plain
+    from oracle.nets import OracleNet
+    W = _mini_weights()
+    img = SN._image(5, MINI["input"])
+    on = OracleNet(MINI, W, SN.ACT_COEFFS)
+    cts, lay = on.encrypt_image(img)
+    out, ol = on.forward(cts, lay)
+    got = on.decrypt_output(out, ol)
+    ref = plain.forward(MINI, img, W, SN.ACT_COEFFS)
+    assert got.shape == ref.shape == (2,)
+    assert np.abs(got - ref).max() <= 1e-3, (got, ref)
+
+
+def test_plan_matches_oracle_rotation_selection():
+    """The product planner and the oracle's own walk select the same key set (independent
+    implementations of the same lowering)."""
+    from oracle.nets import OracleNet
+    from paper_1810_00845_b200.driver import EncryptedNet
+    W = _mini_weights()
+    on = OracleNet(MINI, W, SN.ACT_COEFFS)
+    pl = EncryptedNet.plan(MINI, W, SN.ACT_COEFFS, on.o.moduli)
+    assert pl["rotations"] == on.amounts
+    assert pl["levels_used"] == 8
+
+
+# ------------------------------------------------------------------------------ gloo, world 2
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch
+        from paper_1810_00845_b200 import parallel
+        from paper_1810_00845_b200.driver import EncryptedNet, Symbolic, input_layout
+        res = {}
+        # (1) the numeric exchange: int64 SUM reduce-scatter of reduced residues
+        qm = (1 << 60) - 93
+        rng = np.random.default_rng(100 + rank)
+        per = 3
+        parts = torch.from_numpy(rng.integers(0, qm, size=(world * per, 5), dtype=np.int64))
+        res["parts"] = parts.numpy().copy()
+        res["block"] = parallel.exchange(parts, per, None).numpy()
+        # (2) the sharded driver on the symbolic backend (metadata + real collectives)
+        net = SN.NETS["lenet_small"]
+        from oracle.ckks import Oracle
+        mod = Oracle(net["log_n"], net["q_bits"], net["p_bits"]).moduli
+        sym = Symbolic(net["log_n"], mod)
+        en = EncryptedNet(sym, net, SN.net_weights("lenet_small"), SN.ACT_COEFFS, group=dist.group.WORLD)
+        lay = input_layout(net)
+        cts = en.shard_input([sym.fresh(len(mod) - 2, net["scale"]) for _ in range(lay.C)])
+        out, ol = en.forward_gathered(cts, lay)
+        res["n_out"] = len(out)
+        res["final_level"] = sym.cts[out[0]][0]
+        res["counts"] = sym.counts
+        res["rotations"] = sorted(sym.rotations)
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_multirank_gloo_world2():
+    import torch.multiprocessing as mp
+    from oracle.ckks import Oracle
+    from paper_1810_00845_b200.driver import EncryptedNet
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # exchange: rank r's block = rows [3r, 3r+3) summed over ranks (< 2^63, exact)
+    total = got[0]["parts"] + got[1]["parts"]
+    for r in range(world):
+        assert (got[r]["block"] == total[3 * r:3 * r + 3]).all()
+        assert ((got[r]["block"] % ((1 << 60) - 93)) >= 0).all()
+    # sharded symbolic run: same final level, all 10 outputs gathered on every rank, the
+    # (ic, tap) work partitioned (scalar MACs sum to the single-GPU count), keys needed only
+    # where the rank holds channels
+    net = SN.NETS["lenet_small"]
+    single = EncryptedNet.plan(net, SN.net_weights("lenet_small"), SN.ACT_COEFFS,
+                               Oracle(net["log_n"], net["q_bits"], net["p_bits"]).moduli)
+    for r in range(world):
+        assert got[r]["n_out"] == 10
+        assert got[r]["final_level"] == single["final_level"]
+        assert set(got[r]["rotations"]) <= set(single["rotations"])
+    macs = sum(got[r]["counts"].get("scalar_mac_ct", 0) for r in range(world))
+    assert macs == single["counts"]["scalar_mac_ct"]
+    hoisted = sum(got[r]["counts"].get("rot_hoisted", 0) for r in range(world))
+    assert hoisted == single["counts"]["rot_hoisted"]
+    mulp = sum(got[r]["counts"].get("mul_plain", 0) for r in range(world))
+    assert mulp == single["counts"]["mul_plain"]

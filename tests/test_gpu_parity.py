@@ -234,3 +234,69 @@ def test_error_contract(pair):
     assert g.max_scalar_div(a, 2 ** 62) == o.q[o.L - 1]
     assert g.max_scalar_div(a, 2) == 1
     assert not g.supports(H.PROFILE_BOOTSTRAP) and g.supports(H.PROFILE_RELIN)
+
+
+def test_hoisted_many_amounts_and_levels(pair):
+    """K7 chunking (> 8 amounts), zero amounts (copies), and a lower level (truncated keys)."""
+    g, o = pair.g, pair.o
+    s = o.slots
+    extra = [5, 7, 9, 11, 13, 17, 19, 23, 29, 31]
+    g.keygen(extra, False)
+    for k in extra:
+        o.add_rot_key(k)
+    a, oa = pair.ct(60)
+    ks = [0] + extra + [1, s + 3]           # s + 3 normalises to 3
+    outs = g.rot_left_hoisted(a, ks)
+    for h, k in zip(outs, ks):
+        pair.same(h, o.rot_left(oa, k))
+    if o.L >= 2:
+        lo, olo = g.mod_switch(a, 1), o.mod_switch(oa, 1)
+        for h, k in zip(g.rot_left_hoisted(lo, extra[:3]), extra[:3]):
+            pair.same(h, o.rot_left(olo, k))
+
+
+def test_exchange_fixups(pair):
+    """a15 device steps: conv accumulation into caller memory + adoption of int64 sums."""
+    import torch
+    g, o = pair.g, pair.o
+    T, OC = 3, 2
+    hs, os_ = zip(*[pair.ct(70 + i) for i in range(T)])
+    W = np.random.default_rng(5).normal(0, 0.1, (OC, T))
+    l1 = o.L
+    buf = torch.zeros((OC, 2, l1, o.N), dtype=torch.int64, device="cuda")
+    g.conv_accumulate_dev(list(hs), W.ravel(), buf.data_ptr())
+    ref = [o.add(o.add(o.mul_scalar(os_[0], W[i, 0]), o.mul_scalar(os_[1], W[i, 1])), o.mul_scalar(os_[2], W[i, 2]))
+           for i in range(OC)]
+    for i in range(OC):
+        assert (buf[i].cpu().numpy().view(np.uint64) == ref[i].data).all()
+    # int64 sum of up to 8 reduced residue arrays -> residues (exact, < 2^63)
+    s8 = buf[0] * 8
+    h = g.ct_adopt_sum(s8.data_ptr(), o.L - 1, 2, ref[0].scale)
+    want = ref[0].data
+    for _ in range(7):
+        want = o.add(Ct(want, ref[0].level, ref[0].scale), ref[0]).data
+    assert (g.ct_export(h) == want).all()
+
+
+@pytest.mark.slow
+def test_full_size_bench_config_rotation():
+    """BASELINE.json config 2 top point at full size (N = 2^16, L = 24, dnum = L), in the launch
+    configuration bench.py times (batched K4 path, B = 8 ciphertexts, one key), sampled: two of
+    the eight outputs are compared word for word with the oracle; plus one hoisted pair."""
+    import synth
+    log_n, L = 16, 24
+    k = synth.rot_amount(0, log_n, L)
+    g = H.Context(log_n, [50] * L, 60, seed=0)
+    o = Oracle(log_n, [50] * L, 60, seed=0)
+    assert g.moduli == o.moduli
+    g.keygen([k, 1], False)
+    o.keygen(rot_amounts=[k, 1], relin=False)
+    cts = [g.ct_random(b, L - 1) for b in range(8)]
+    outs = g.rot_left_batch(cts, k)
+    for b in (0, 7):
+        oc = o.bench_ct(b, L - 1)
+        assert (g.ct_export(outs[b]) == o.rot_left(oc, k).data).all(), f"ct {b}"
+    oc0 = o.bench_ct(0, L - 1)
+    hz = g.rot_left_hoisted(cts[0], [k, 1])
+    assert (g.ct_export(hz[1]) == o.rot_left(oc0, 1).data).all()
+    g.close()
