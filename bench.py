@@ -24,7 +24,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "key-switch rotations/s at N=2^16"
+METRIC = "key-switch rotations/s at N=2^16"   # + "inference": encrypted CNN latency (s), configs 1 / 3
 UNIT = "rot/s"
 
 
@@ -40,6 +40,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-hoisted", action="store_true")
+    ap.add_argument("--no-inference", action="store_true")
+    ap.add_argument("--hoist-r", type=int, default=8, help="rotation amounts per hoisted ModUp")
+    ap.add_argument("--nets", default="tiny,lenet_small", help="encrypted-inference configs to time")
     return ap.parse_args()
 
 
@@ -131,6 +135,135 @@ def rotation_alg_bytes(log_n: int, l1: int, B: int) -> float:
     """read ct 2(l+1) + key 2 beta (l+2) (once per same-key batch) + write 2(l+1) limbs."""
     limb = 8 * (1 << log_n)
     return (B * 4 * l1 + 2 * l1 * (l1 + 1)) * limb
+
+
+def hoisted_ip_alg_bytes(log_n: int, l1: int, R: int) -> float:
+    """K7 inner product, one launch: D read once (l1 (l1+1) limbs), R keys (2 l1 (l1+1) limbs
+    each) streamed, R accumulators (2 (l1+1) limbs) written."""
+    limb = 8 * (1 << log_n)
+    return (l1 * (l1 + 1) + R * (2 * l1 * (l1 + 1) + 2 * (l1 + 1))) * limb
+
+
+def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream):
+    """Hoisted rotations (the conv pattern): each ciphertext rotated by R amounts
+    sharing one ModUp.  Returns the sub-object of the JSON line."""
+    import torch
+    R = len(amounts)
+
+    def step():
+        for h in cts:
+            for o in ctx.rot_left_hoisted(h, amounts):
+                ctx.free(o)
+    for _ in range(warmup):
+        step()
+    ctx.sync()
+    ctx.profile(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ip_ms, ip_n = prof.get("ks_ip_hoisted", (0.0, 0))
+    total = sum(v[0] for v in prof.values()) or 1.0
+    per_launch = ip_ms / max(ip_n, 1)
+    alg = hoisted_ip_alg_bytes(log_n, L, R)
+    hbm_peak = _hbm_peak()
+    rot = len(cts) * R * steps
+    return {"value": rot / (ms / 1e3), "unit": "rot/s", "amounts_per_modup": R, "ciphertexts": len(cts),
+            "ms_per_step": ms / steps,
+            "roofline": {"bound": "hbm", "kernel": "ks_ip_hoisted", "achieved": alg / (per_launch / 1e3) / 1e9,
+                         "peak": hbm_peak, "unit": "GB/s", "frac": alg / (per_launch / 1e3) / 1e9 / hbm_peak,
+                         "alg_bytes_per_launch": alg, "launch_ms_avg": per_launch, "share_of_step": ip_ms / total,
+                         "traffic": _ncu_traffic("ks_ip_hoisted", log_n, L, R),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "kernels": {n: {"ms": v[0], "launches": v[1], "share": v[0] / total}
+                        for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}}
+
+
+def measure_inference(name, device, reps=3):
+    """Encrypted CNN inference latency (BASELINE.json metric, configs 1 / 3): server-side
+    forward from encrypted input resident on the GPU to encrypted output, CUDA events + wall
+    clock; client encode/encrypt and decrypt/decode timed separately.  (Accuracy against the
+    float64 network is asserted by tests/test_driver.py, not here.)"""
+    import numpy as np
+    import torch
+    from synth import nets as SN
+    from paper_1810_00845_b200 import hisa as H
+    from paper_1810_00845_b200.driver import EncryptedNet
+    net = SN.NETS[name]
+    W = SN.net_weights(name)
+    img = SN.net_image(name, 0)
+    ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=device, arena_bytes=16 << 30)
+    t0 = time.perf_counter()
+    plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli)
+    ctx.keygen(plan["rotations"], True)
+    ctx.sync()
+    t_keys = time.perf_counter() - t0
+    en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS)
+    stream = torch.cuda.current_stream(device)
+    # warm-up pass: encodes (caches) the weight plaintexts once per model
+    t0 = time.perf_counter()
+    cts, lay = en.encrypt_image(img)
+    out, ol = en.forward(cts, lay)
+    ctx.sync()
+    t_first = time.perf_counter() - t0
+    for h in out + cts:
+        ctx.free(h)
+    lat, walls = [], []
+    for r in range(reps):
+        t0 = time.perf_counter()
+        cts, lay = en.encrypt_image(img)
+        ctx.sync()
+        t_enc = time.perf_counter() - t0
+        ctx.profile(True)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        ev0.record(stream)
+        out, ol = en.forward(cts, lay)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        walls.append(time.perf_counter() - w0)
+        lat.append(ev0.elapsed_time(ev1) / 1e3)
+        launches = ctx.launch_count()
+        prof = ctx.profile_read()
+        ctx.profile(False)
+        t0 = time.perf_counter()
+        got = en.decrypt_output(out, ol)
+        t_dec = time.perf_counter() - t0
+        for h in out + cts:
+            ctx.free(h)
+    total = sum(v[0] for v in prof.values()) or 1.0
+    top = sorted(prof.items(), key=lambda kv: -kv[1][0])[:6]
+    ctx.close()
+    return {"config": name, "latency_s": float(np.median(lat)), "wall_s": float(np.median(walls)), "unit": "s",
+            "reps": reps, "log_n": net["log_n"], "limbs": len(net["q_bits"]), "gpu_launches": launches,
+            "client_encrypt_s": t_enc, "client_decrypt_s": t_dec, "keygen_s": t_keys,
+            "first_pass_incl_weight_encoding_s": t_first, "levels_used": plan["levels_used"],
+            "rotation_keys": len(plan["rotations"]), "output_head": [float(x) for x in np.ravel(got)[:3]],
+            "kernel_share": {n: round(v[0] / total, 4) for n, v in top}}
+
+
+def _hbm_peak():
+    hbm_peak = 6549.8
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        hbm_peak = json.load(open(mp)).get("hbm_gbs", hbm_peak)
+    return hbm_peak
+
+
+def _ncu_traffic(kernel, log_n, L, B):
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            return json.load(open(tf)).get(f"{kernel}@{log_n}/{L}/B{B}")
+        except (ValueError, OSError):
+            return None
+    return None
 
 
 # ------------------------------------------------------------------------------ reference arm (oracle)
@@ -244,17 +377,8 @@ def main():
     dom_name, (dom_ms, dom_n) = dom
     units = kernel_units(dom_name, log_n, L, B) * a.steps
     achieved = units / (dom_ms / 1e3) if dom_ms > 0 else 0.0
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get(f"{dom_name}@{log_n}/{L}/B{B}")
-        except (ValueError, OSError):
-            traffic = None
-    hbm_peak = 6549.8
-    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(mp):
-        hbm_peak = json.load(open(mp)).get("hbm_gbs", hbm_peak)
+    traffic = _ncu_traffic(dom_name, log_n, L, B)
+    hbm_peak = _hbm_peak()
     alg_bytes_step = rotation_alg_bytes(log_n, L, B)
     hbm_gbs = alg_bytes_step * a.steps / (ms / 1e3) / 1e9
     total_ms = sum(v[0] for v in prof.values()) or 1.0
@@ -306,6 +430,18 @@ def main():
         e2e = {"value": world * B * n_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": B * words * 8,
                "d2h_bytes_per_step": B * words * 8, "steps": n_e2e}
 
+    hoisted = None
+    if not a.no_hoisted:
+        import synth as _s
+        rng = _s.rng(a.seed, 11, log_n, L)
+        amounts = sorted({int(x) for x in rng.integers(1, N // 2, size=a.hoist_r)})
+        ctx.keygen(amounts, False)
+        hoisted = measure_hoisted(ctx, cts[:2], amounts, max(2, a.steps // 2), a.warmup, log_n, L, stream)
+        if dist:
+            t = torch.tensor([hoisted["ms_per_step"]], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            hoisted["value"] = world * len(cts[:2]) * len(amounts) / (float(t.item()) / 1e3)
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = cpu_baseline(a, k)
@@ -318,9 +454,12 @@ def main():
                            "parallelism": f"dp{world} (independent ciphertexts)",
                            "l2": "inputs larger than L2 (600 MiB key + B x 24 MiB ciphertexts per step)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": ck, "kernels": kernels}
-        print(json.dumps(line), flush=True)
+                "clocks": ck, "kernels": kernels, "hoisted": hoisted}
     ctx.close()
+    if rank == 0:
+        if not a.no_inference and world == 1:
+            line["inference"] = [measure_inference(nm, local) for nm in a.nets.split(",") if nm]
+        print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
 

@@ -30,6 +30,14 @@ Lowering readings, in the order t
                    rotate-and-sum acc += rot(acc, 2^t) for t < ceil(log2(span)), slot 0 holds
                    the dot product (A27, R = 1); add_scalar(beta).  Output layout "slot0".
   fc (slot0 input) out_k = sum_j mulScalar(x_j, W'[k, j]) (pt_scale q_top); rescale; add beta.
+  fc, R > 1 replicas ("replicas ... in log number of rotations", A27): mask if not
+                   clean; block Bk = 2^ceil(log2(span)); replicate y += rotRight(y, Bk 2^t) for
+                   t < log2 R (copy r at slot offset r Bk); group g (R neurons g R + r):
+                   acc_g = sum_c mulPlain(y_c, P_gc) with W'[g R + r, (c, y, x)] at slot r Bk +
+                   valid slot; rescale; acc += rot(acc, 2^t) for t < log2 Bk; add beta.
+                   Output layout "rep": neuron g R + r at slot r Bk of ciphertext g.
+  fc (rep input)   out_k = sum_g mulPlain(z_g, Q_kg), Q_kg[r Bk] = W'[k, g R + r]; rescale;
+                   acc += rot(acc, Bk 2^t) for t < log2 R; add beta.  Output "slot0".
 """
 from __future__ import annotations
 
@@ -41,9 +49,10 @@ from .ckks import Ct, Oracle
 
 
 class Layout:
-    def __init__(self, kind, C, H, W, hS=0, wS=0, origin=0, clean=False):
+    def __init__(self, kind, C, H, W, hS=0, wS=0, origin=0, clean=False, R=1, Bk=0, count=0):
         self.kind, self.C, self.H, self.W = kind, C, H, W
         self.hS, self.wS, self.origin, self.clean = hS, wS, origin, clean
+        self.R, self.Bk, self.count = R, Bk, count
 
     def valid_slots(self):
         return [self.origin + y * self.hS + x * self.wS for y in range(self.H) for x in range(self.W)]
@@ -108,6 +117,16 @@ class OracleNet:
             elif kind == "avgpool":
                 amts.update({lay.wS % s, lay.hS % s, (lay.hS + lay.wS) % s})
                 lay = Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
+            elif kind == "fc" and lay.kind == "hw" and len(layer) > 2 and layer[2] > 1:
+                R = layer[2]
+                span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+                bk = 2 ** math.ceil(math.log2(span))
+                amts.update((s - bk * 2 ** t) % s for t in range(int(math.log2(R))))
+                amts.update(2 ** t for t in range(int(math.log2(bk))))
+                lay = Layout("rep", -(-layer[1] // R), 1, 1, R=R, Bk=bk, count=layer[1])
+            elif kind == "fc" and lay.kind == "rep":
+                amts.update(lay.Bk * 2 ** t for t in range(int(math.log2(lay.R))))
+                lay = Layout("slot0", layer[1], 1, 1)
             elif kind == "fc" and lay.kind == "hw":
                 span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
                 amts.update(1 << t for t in range(math.ceil(math.log2(span))))
@@ -133,6 +152,9 @@ class OracleNet:
         vals = [self.o.decode(self.o.decrypt(ct)) for ct in cts]
         if lay.kind == "slot0":
             return np.array([v[0] for v in vals])
+        if lay.kind == "rep":
+            flat = [v[r * lay.Bk] for v in vals for r in range(lay.R)]
+            return np.array(flat[:lay.count])
         sl = lay.valid_slots()
         return np.array([[v[i] for i in sl] for v in vals]).reshape(lay.C, lay.H, lay.W)
 
@@ -183,7 +205,8 @@ class OracleNet:
             if not square_only and self.gamma:
                 y = o.add_scalar(y, self.gamma)
             out.append(y)
-        return out, Layout(lay.kind, lay.C, lay.H, lay.W, lay.hS, lay.wS, lay.origin, False)
+        return out, Layout(lay.kind, lay.C, lay.H, lay.W, lay.hS, lay.wS, lay.origin, False, lay.R, lay.Bk,
+                           lay.count)
 
     def avgpool(self, cts, lay):
         o = self.o
@@ -195,10 +218,66 @@ class OracleNet:
             out.append(y)
         return out, Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
 
+    def fc_replicas(self, cts, lay, layer, w, beta):
+        o = self.o
+        n_out, R = layer[1], layer[2]
+        if not lay.clean:
+            cts, lay = self._mask(cts, lay)
+        span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+        bk = 2 ** math.ceil(math.log2(span))
+        assert R * bk <= o.slots
+        ys = []
+        for ct in cts:
+            y = ct
+            for t in range(int(math.log2(R))):
+                y = o.add(y, o.rot_right(y, bk * 2 ** t))
+            ys.append(y)
+        sl = lay.valid_slots()
+        hw = lay.H * lay.W
+        groups = -(-n_out // R)
+        outs = []
+        for g in range(groups):
+            acc = None
+            for c in range(lay.C):
+                v = np.zeros(o.slots)
+                for r in range(R):
+                    if g * R + r < n_out:
+                        for i, slot in enumerate(sl):
+                            v[r * bk + slot] = w[g * R + r, c * hw + i]
+                pt = o.encode(v, float(o.q[ys[c].level]), ys[c].level)
+                term = o.mul_plain(ys[c], pt)
+                acc = term if acc is None else o.add(acc, term)
+            acc = o.rescale(acc)
+            for t in range(int(math.log2(bk))):
+                acc = o.add(acc, o.rot_left(acc, 2 ** t))
+            if beta:
+                acc = o.add_scalar(acc, beta)
+            outs.append(acc)
+        return outs, Layout("rep", groups, 1, 1, R=R, Bk=bk, count=n_out)
+
     def fc(self, cts, lay, layer, w, beta):
         o = self.o
         n_out = layer[1]
         outs = []
+        if lay.kind == "hw" and len(layer) > 2 and layer[2] > 1:
+            return self.fc_replicas(cts, lay, layer, w, beta)
+        if lay.kind == "rep":
+            for k in range(n_out):
+                acc = None
+                for g, ct in enumerate(cts):
+                    v = np.zeros(o.slots)
+                    for r in range(lay.R):
+                        if g * lay.R + r < lay.count:
+                            v[r * lay.Bk] = w[k, g * lay.R + r]
+                    term = o.mul_plain(ct, o.encode(v, float(o.q[ct.level]), ct.level))
+                    acc = term if acc is None else o.add(acc, term)
+                acc = o.rescale(acc)
+                for t in range(int(math.log2(lay.R))):
+                    acc = o.add(acc, o.rot_left(acc, lay.Bk * 2 ** t))
+                if beta:
+                    acc = o.add_scalar(acc, beta)
+                outs.append(acc)
+            return outs, Layout("slot0", n_out, 1, 1)
         if lay.kind == "hw":
             sl = lay.valid_slots()
             span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
@@ -230,11 +309,14 @@ class OracleNet:
                 outs.append(acc)
         return outs, Layout("slot0", n_out, 1, 1)
 
-    def forward(self, cts, lay, trace=None):
+    def forward(self, cts, lay, trace=None, stop_after=None):
         """Server-side evaluation; `trace` (a list) receives (layer index, ciphertexts) after
-        every layer for per-layer parity checks."""
+        every layer for per-layer parity checks; `stop_after` = last layer index to evaluate
+        (sampled parity of networks too large for the oracle end to end)."""
         wi = 0
         for li, layer in enumerate(self.net["layers"]):
+            if stop_after is not None and li > stop_after:
+                break
             kind = layer[0]
             if kind == "conv":
                 w, b = self.folded[wi]

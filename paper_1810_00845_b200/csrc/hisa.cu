@@ -201,6 +201,10 @@ struct hisa_ctx {
     uint64_t* d_rlk = nullptr;        // [L][2][L+1][N]
     std::map<uint64_t, uint64_t*> rot_keys;
     uint64_t enc_counter = 0;
+    // encode/decode long-double tables (built on first use): cis(2 pi k / N), k < N/2, and
+    // cis(pi t / N), t < N
+    std::vector<std::complex<long double>> enc_root, enc_twist;
+    std::vector<__float128> enc_cosq;   // binary128 cos(pi e / N), e < 2N (near-tie recomputation, A7)
     // profiling: CUDA events around every launch on the context stream (hisa_profile)
     bool prof_on = false;
     struct ProfRec { const char* name; cudaEvent_t a, b; };
@@ -784,7 +788,23 @@ extern "C" int hisa_copy(hisa_ctx* c, hisa_ct h, hisa_ct* out) {
 // encode / decode (A7, A13): host boundary, long-double FFT, binary128 near-tie recomputation
 // ============================================================================================
 typedef std::complex<long double> cld;
-static void fft_ld(std::vector<cld>& a, int sign) {
+static void enc_tables(hisa_ctx* c) {
+    if (!c->enc_root.empty()) return;
+    const uint64_t N = c->N;
+    const long double pi = acosl(-1.0L);
+    c->enc_root.resize(N / 2);
+    for (uint64_t k = 0; k < N / 2; k++) {
+        const long double ang = 2.0L * pi * (long double)k / (long double)N;
+        c->enc_root[k] = cld(cosl(ang), sinl(ang));
+    }
+    c->enc_twist.resize(N);
+    for (uint64_t t = 0; t < N; t++) {
+        const long double ang = pi * (long double)t / (long double)N;
+        c->enc_twist[t] = cld(cosl(ang), sinl(ang));
+    }
+}
+// radix-2 DIT FFT in long double: a[t] <- sum_m a[m] e^{sign 2 pi i m t / n}, n = a.size() = N
+static void fft_ld(const hisa_ctx* c, std::vector<cld>& a, int sign) {
     const size_t n = a.size();
     int bits = 0;
     while ((1ull << bits) < n) bits++;
@@ -792,17 +812,13 @@ static void fft_ld(std::vector<cld>& a, int sign) {
         size_t j = h_brv((uint32_t)i, bits);
         if (i < j) std::swap(a[i], a[j]);
     }
-    const long double pi = acosl(-1.0L);
     for (size_t len = 2; len <= n; len <<= 1) {
-        const size_t half = len / 2;
-        std::vector<cld> w(half);
-        for (size_t k = 0; k < half; k++) {
-            const long double ang = sign * 2.0L * pi * (long double)k / (long double)len;
-            w[k] = cld(cosl(ang), sinl(ang));
-        }
+        const size_t half = len / 2, step = n / len;
         for (size_t i = 0; i < n; i += len)
             for (size_t k = 0; k < half; k++) {
-                cld u = a[i + k], v = a[i + k + half] * w[k];
+                const cld r = c->enc_root[k * step];
+                const cld w = sign < 0 ? std::conj(r) : r;
+                cld u = a[i + k], v = a[i + k + half] * w;
                 a[i + k] = u + v;
                 a[i + k + half] = u - v;
             }
@@ -821,13 +837,12 @@ static int encode_coeffs(hisa_ctx* c, const double* z, size_t n, double scale, s
         A[(kc - 1) / 2] += cld((long double)z[j], 0);
         k = k * 5 % twoN;
     }
-    fft_ld(A, -1);   // F[t] = sum_m A[m] e^{-2 pi i m t / N}
-    const long double pi = acosl(-1.0L);
+    enc_tables(c);
+    fft_ld(c, A, -1);   // F[t] = sum_m A[m] e^{-2 pi i m t / N}
     m.assign(N, 0);
-    std::vector<__float128> cq;
+    std::vector<__float128>& cq = c->enc_cosq;
     for (uint64_t t = 0; t < N; t++) {
-        const long double ang = -pi * (long double)t / (long double)N;
-        const cld tw(cosl(ang), sinl(ang));
+        const cld tw = std::conj(c->enc_twist[t]);
         const long double v = (A[t] * tw).real() * (long double)scale / (long double)N;
         const long double av = fabsl(v);
         const long double fr = av - floorl(av);
@@ -838,7 +853,8 @@ static int encode_coeffs(hisa_ctx* c, const double* z, size_t n, double scale, s
                 for (uint64_t e = 0; e < twoN; e++) cq[e] = cosq(M_PIq * (__float128)e / (__float128)N);
             }
             __float128 acc = 0;
-            for (size_t j = 0; j < n; j++) acc += 2 * (__float128)z[j] * cq[(uint64_t)((u128)pow5[j] * t % twoN)];
+            for (size_t j = 0; j < n; j++)
+                if (z[j] != 0.0) acc += 2 * (__float128)z[j] * cq[(uint64_t)((u128)pow5[j] * t % twoN)];
             acc = acc * (__float128)scale / (__float128)N;
             __float128 rq = floorq(fabsq(acc) + 0.5Q);
             r = (long double)(acc < 0 ? -rq : rq);
@@ -898,13 +914,12 @@ extern "C" int hisa_decode(hisa_ctx* c, hisa_pt h, double* out, size_t n) {
     const uint64_t q0 = c->mod[0];
     // G[m] = sum_t (m_t zeta^t) e^{+2 pi i m t / N};  value at zeta^(2m+1)
     std::vector<cld> A(N);
-    const long double pi = acosl(-1.0L);
+    enc_tables(c);
     for (uint64_t t = 0; t < N; t++) {
         const long double mt = a[t] > (q0 >> 1) ? -(long double)(q0 - a[t]) : (long double)a[t];
-        const long double ang = pi * (long double)t / (long double)N;
-        A[t] = cld(mt * cosl(ang), mt * sinl(ang));
+        A[t] = mt * c->enc_twist[t];
     }
-    fft_ld(A, +1);
+    fft_ld(c, A, +1);
     uint64_t k = 1;
     for (size_t j = 0; j < n; j++) {
         out[j] = (double)(A[(k - 1) / 2].real() / (long double)p->scale);

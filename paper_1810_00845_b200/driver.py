@@ -48,10 +48,14 @@ class Layout:
     wS: int = 0
     origin: int = 0
     clean: bool = False
+    count: int = 0       # kind "rep": number of valid values (R per ciphertext at slots r * hS)
 
     def slots_of_valid(self) -> np.ndarray:
         y, x = np.meshgrid(np.arange(self.H), np.arange(self.W), indexing="ij")
         return (self.origin + y * self.hS + x * self.wS).ravel()
+
+    def span(self) -> int:
+        return self.origin + (self.H - 1) * self.hS + (self.W - 1) * self.wS + 1
 
 
 def act_fold(coeffs):
@@ -236,6 +240,8 @@ class EncryptedNet:
             self.b.free(pt)
         if lay.kind == "slot0":
             return np.array([v[0] for v in vals])
+        if lay.kind == "rep":
+            return np.concatenate([v[np.arange(lay.H) * lay.hS] for v in vals])[:lay.count]
         idx = lay.slots_of_valid()
         return np.stack([v[idx] for v in vals]).reshape(lay.C, lay.H, lay.W)
 
@@ -343,30 +349,26 @@ class EncryptedNet:
             self._free_all(r + [s1, s2])
         return out, Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
 
-    def fc(self, cts, lay, layer, w, beta, li):
-        """Matmul (P:728-729, A27, R = 1)."""
-        n_out = layer[1]
-        if lay.kind == "slot0":          # next FC reads slot 0: scalar MACs, fused
-            own = self.owned(lay.C)
-            outs = self._accumulate(list(cts), w[:, own.start:own.stop], n_out)
-            res = [self.b.rescale(h) for h in outs]
-            self._free_all(outs)
-            return self._bias(res, beta), Layout("slot0", n_out)
-        idx = lay.slots_of_valid()
-        hw = lay.H * lay.W
-        own_in = self.owned(lay.C)
-        span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
-        steps = math.ceil(math.log2(span))
+    def _rotate_sum(self, res, amounts):
+        """acc += rot(acc, a) for a in amounts, every ciphertext under one key per step."""
+        for a in amounts:
+            rs = self.b.rot_left_batch(res, a)
+            nxt = [self.b.add(x, r) for x, r in zip(res, rs)]
+            self._free_all(res + rs)
+            res = nxt
+        return res
+
+    def _mulplain_sums(self, cts, n_in, n_rows, key, li, vals_fn):
+        """acc_j = sum_c mulPlain(cts[c], P_{j,c}) for j < n_rows over this rank's channels of
+        the n_in inputs (None where the rank owns none); P built by vals_fn(j, global c).
+        Multi-GPU: reduce-scattered, so the result is this rank's owned rows."""
+        own_in = self.owned(n_in)
         lv = self._level(cts[0]) if cts else None
         sums = []
-        for jo in range(n_out):
+        for jo in range(n_rows):
             acc = None
             for ci, ct in zip(own_in, cts):
-                def vals(jo=jo, ci=ci):
-                    v = np.zeros(self.slots)
-                    v[idx] = w[jo, ci * hw:(ci + 1) * hw]
-                    return v
-                pt = self._plaintext(("fc", li, jo, ci), vals, lv)
+                pt = self._plaintext((key, li, jo, ci), lambda jo=jo, ci=ci: vals_fn(jo, ci), lv)
                 term = self.b.mul_plain(ct, pt)
                 if acc is None:
                     acc = term
@@ -377,14 +379,94 @@ class EncryptedNet:
             sums.append(acc)
         if self.world > 1:
             from . import parallel
-            sums = parallel.reduce_scatter_cts(self, sums, n_out)
+            return parallel.reduce_scatter_cts(self, sums, n_rows)
+        return sums
+
+    def fc_replicated(self, cts, lay, layer, w, beta, li):
+        """FC with R replicas per ciphertext ("replicas ... added in log number of
+        rotations", A27): mask, replicate R times at block stride Bk (log2 R rotations), one
+        mulPlain per (group of R neurons, input channel), rescale, rotate-and-sum inside each
+        block; neuron g R + r ends in slot r Bk of ciphertext g."""
+        n_out, R = layer[1], layer[2]
+        if not lay.clean:
+            cts, lay = self.mask(cts, lay, li)
+            masked = True
+        else:
+            masked = False
+        Bk = 1 << math.ceil(math.log2(lay.span()))
+        if R * Bk > self.slots or R & (R - 1):
+            raise ValueError(f"replicas R={R} x block {Bk} exceed {self.slots} slots")
+        reps, temp = list(cts), masked
+        for t in range(int(math.log2(R))):           # copies at r * Bk (right rotations, P:759)
+            rs = self.b.rot_left_batch(reps, self.slots - (Bk << t))
+            nxt = [self.b.add(x, r) for x, r in zip(reps, rs)]
+            self._free_all(rs + (reps if temp else []))
+            reps, temp = nxt, True
+        idx = lay.slots_of_valid()
+        hw = lay.H * lay.W
+        n_groups = -(-n_out // R)
+
+        def vals(g, c):
+            v = np.zeros(self.slots)
+            for r in range(R):
+                j = g * R + r
+                if j < n_out:
+                    v[r * Bk + idx] = w[j, c * hw:(c + 1) * hw]
+            return v
+        sums = self._mulplain_sums(reps, lay.C, n_groups, "fcrep", li, vals)
+        if temp:
+            self._free_all(reps)
         res = [self.b.rescale(h) for h in sums]
         self._free_all(sums)
-        for t in range(steps):          # rotate-and-sum, every neuron under one key per step
-            rs = self.b.rot_left_batch(res, 1 << t)
-            nxt = [self.b.add(a, r) for a, r in zip(res, rs)]
-            self._free_all(res + rs)
-            res = nxt
+        res = self._rotate_sum(res, [1 << t for t in range(int(math.log2(Bk)))])
+        return self._bias(res, beta), Layout("rep", n_groups, H=R, hS=Bk, count=n_out)
+
+    def fc_from_rep(self, cts, lay, layer, w, beta, li):
+        """FC whose input holds R values per ciphertext at slots r * Bk: one mulPlain per
+        (output, input ciphertext) with the weights at those slots, rescale, rotate-and-sum
+        across the R blocks (log2 R rotations) into slot 0."""
+        n_out = layer[1]
+        R, Bk = lay.H, lay.hS
+
+        def vals(k, g):
+            v = np.zeros(self.slots)
+            for r in range(R):
+                j = g * R + r
+                if j < lay.count:
+                    v[r * Bk] = w[k, j]
+            return v
+        sums = self._mulplain_sums(cts, lay.C, n_out, "fcfromrep", li, vals)
+        res = [self.b.rescale(h) for h in sums]
+        self._free_all(sums)
+        res = self._rotate_sum(res, [Bk << t for t in range(int(math.log2(R)))])
+        return self._bias(res, beta), Layout("slot0", n_out)
+
+    def fc(self, cts, lay, layer, w, beta, li):
+        """Matmul (A27): R = 1 (below), replicas (fc_replicated), or an input in
+        replica layout (fc_from_rep)."""
+        if lay.kind == "rep":
+            return self.fc_from_rep(cts, lay, layer, w, beta, li)
+        if lay.kind == "hw" and len(layer) > 2 and layer[2] > 1:
+            return self.fc_replicated(cts, lay, layer, w, beta, li)
+        n_out = layer[1]
+        if lay.kind == "slot0":          # next FC reads slot 0: scalar MACs, fused
+            own = self.owned(lay.C)
+            outs = self._accumulate(list(cts), w[:, own.start:own.stop], n_out)
+            res = [self.b.rescale(h) for h in outs]
+            self._free_all(outs)
+            return self._bias(res, beta), Layout("slot0", n_out)
+        idx = lay.slots_of_valid()
+        hw = lay.H * lay.W
+        steps = math.ceil(math.log2(lay.span()))
+
+        def vals(jo, ci):
+            v = np.zeros(self.slots)
+            v[idx] = w[jo, ci * hw:(ci + 1) * hw]
+            return v
+        sums = self._mulplain_sums(cts, lay.C, n_out, "fc", li, vals)
+        res = [self.b.rescale(h) for h in sums]
+        self._free_all(sums)
+        res = self._rotate_sum(res, [1 << t for t in range(steps)])   # slot 0 <- dot product
         return self._bias(res, beta), Layout("slot0", n_out)
 
     def _bias(self, cts, beta):

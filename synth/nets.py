@@ -11,7 +11,8 @@ Layer tuples (PyTorch semantics for the float64 definition):
     ("act",)                       a0 + a1 x + a2 x^2 with ACT_COEFFS (A25)
     ("square",)                    x^2 (config 1)
     ("avgpool",)                   2x2, stride 2
-    ("fc", out)                    W @ flatten(x) (flatten order c, y, x)
+    ("fc", out[, R])               W @ flatten(x) (flatten order c, y, x); R = replicas per
+                                   ciphertext in the encrypted lowering (A27), not semantics
     ("gap",)                       global average pool (config 5)
 Convs and FCs have no bias (A34).
 """
@@ -35,7 +36,7 @@ NETS = {
     # config 4: LeNet-5-large-shaped (A32: SAME 5x5 convs, 28 -> 14 -> 7, 7*7*64 = 3136)
     "lenet_large": dict(log_n=15, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
                         layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2), ("act",),
-                                ("avgpool",), ("fc", 512), ("act",), ("fc", 10)],
+                                ("avgpool",), ("fc", 512, 16), ("act",), ("fc", 10)],
                         sigma=[0.05, 0.05, 0.05, 0.05]),
 }
 

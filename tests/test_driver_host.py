@@ -23,6 +23,18 @@ MINI = dict(log_n=11, q_bits=[60] + [40] * 8, p_bits=60, scale=2.0 ** 40, input=
                     ("fc", 3), ("act",), ("fc", 2)], sigma=[0.3, 0.3, 0.3, 0.3])
 
 
+# replica FC (A27): pooled 3x3 plane (span 37 -> block 64), R = 4 neurons per ciphertext, then
+# an FC reading the replica layout
+MINI_REP = dict(log_n=11, q_bits=[60] + [40] * 6, p_bits=60, scale=2.0 ** 40, input=(2, 6, 6),
+                layers=[("conv", 2, 3, 1, 1), ("act",), ("avgpool",), ("fc", 6, 4), ("act",), ("fc", 3)],
+                sigma=[0.3, 0.3, 0.3])
+
+
+def _mini_rep_weights():
+    shapes = [(2, 2, 3, 3), (6, 2 * 3 * 3), (3, 6)]
+    return [SN._weights(91 + i, s, 0.3) for i, s in enumerate(shapes)]
+
+
 def _mini_weights():
     shapes = [(2, 2, 3, 3), (2, 2, 3, 3), (3, 2 * 4 * 4), (2, 3)]
     return [SN._weights(77 + i, s, 0.3) for i, s in enumerate(shapes)]
@@ -113,6 +125,38 @@ def test_oracle_net_every_branch_matches_float64():
     ref = plain.forward(MINI, img, W, SN.ACT_COEFFS)
     assert got.shape == ref.shape == (2,)
     assert np.abs(got - ref).max() <= 1e-3, (got, ref)
+
+
+def test_oracle_net_replica_fc_matches_float64():
+    """Pins the oracle's replica FC lowering (mask, log R replication, block rotate-and-sum,
+    FC from the replica layout) to the float64 network."""
+    from oracle import plain
+    from oracle.nets import OracleNet
+    from paper_1810_00845_b200.driver import EncryptedNet
+    W = _mini_rep_weights()
+    img = SN._image(6, MINI_REP["input"])
+    on = OracleNet(MINI_REP, W, SN.ACT_COEFFS)
+    cts, lay = on.encrypt_image(img)
+    out, ol = on.forward(cts, lay)
+    got = on.decrypt_output(out, ol)
+    ref = plain.forward(MINI_REP, img, W, SN.ACT_COEFFS)
+    assert got.shape == ref.shape == (3,)
+    assert np.abs(got - ref).max() <= 1e-3, (got, ref)
+    pl = EncryptedNet.plan(MINI_REP, W, SN.ACT_COEFFS, on.o.moduli)
+    assert pl["rotations"] == on.amounts
+    assert pl["levels_used"] == 6
+
+
+def test_plan_lenet_large_replicas():
+    """Config 4 with FC1 at R = 16 (A27): 2048 weight plaintexts instead of 32768, 9 of 13
+    levels (SURVEY A.4 plans 8-11)."""
+    from paper_1810_00845_b200.driver import EncryptedNet
+    net = SN.NETS["lenet_large"]
+    pl = EncryptedNet.plan(net, SN.net_weights("lenet_large"), SN.ACT_COEFFS, _moduli(net))
+    assert pl["levels_used"] == 9
+    assert pl["counts"]["rot_hoisted"] == 24 + 32 * 3 + 32 * 24 + 64 * 3
+    fc_pts = pl["counts"]["encode"] - 2          # minus the two mask plaintexts
+    assert fc_pts == 32 * 64 + 10 * 32
 
 
 def test_plan_matches_oracle_rotation_selection():
