@@ -7,15 +7,17 @@
 // registers (products < 2^122, at most 64 terms).  One Barrett reduction per output word.
 // D never touches HBM in its NTT form; the key is streamed once per ciphertext.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include "launch.h"
 
 namespace hisa {
 
-constexpr int LOG_R_KS = 3;
-
-template <int LOG_M>
-__global__ void __launch_bounds__(256) k_ks_ip(KsJob job, Tables tb) {
-    using G = Geo<LOG_M, LOG_R_KS>;
+// Variant knobs (tuned on B200, see profiles/): LOG_R = radix of the on-chip engine phases,
+// GR = rows (groups) per CTA, MINB = __launch_bounds__ min blocks.  Threads = GR * M / R,
+// elements per thread in the MAC phase = R (2R 128-bit accumulators per thread).
+template <int LOG_M, int LOG_R, int GR, int MINB>
+__global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip(KsJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
     // ciphertext index fastest: CTAs that read the same key tile are scheduled together (L2 reuse)
     const int nz = job.nz;
@@ -24,17 +26,16 @@ __global__ void __launch_bounds__(256) k_ks_ip(KsJob job, Tables tb) {
     const int l1 = job.l1;
     const int nri = l1 + 1;
     const int log_n = tb.log_n;
-    const int Gr = blockDim.x / G::T;
-    const int row0 = (blockIdx.x / nz) * Gr;
+    const int row0 = (blockIdx.x / nz) * GR;
     const long long off0 = (long long)row0 << LOG_M;
     const int mi = job.mod_map[ri];
     const Mod md = tb.mods[mi];
-    const int nthr = blockDim.x;
-    constexpr int EPT = G::R;   // elements per thread in the MAC phase (tile / nthr)
+    constexpr int NTHR = GR * G::T;
+    constexpr int EPT = G::R;   // elements per thread in the MAC phase (tile / threads)
     U128 acc0[EPT], acc1[EPT];
 #pragma unroll
     for (int k = 0; k < EPT; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
-    int g = threadIdx.x / G::T, t = threadIdx.x % G::T;
+    const int g = threadIdx.x / G::T, t = threadIdx.x % G::T;
     const long long kstride_j = 2ll * (job.L + 1) << log_n;
     const long long kstride_p = (long long)(job.L + 1) << log_n;
     const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
@@ -43,21 +44,21 @@ __global__ void __launch_bounds__(256) k_ks_ip(KsJob job, Tables tb) {
                                         : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
 #pragma unroll
         for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * nthr;
+            const int i = threadIdx.x + k * NTHR;
             const unsigned sa = (unsigned)__cvta_generic_to_shared(&sm[G::addr(i >> LOG_M, i & (G::M - 1))]);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + i) : "memory");
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
         if (j != ri) {
-            fwd_engine<LOG_M, LOG_R_KS>(sm, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
-                                        (uint32_t)(row0 + g), g, t);
+            fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
+                                     (uint32_t)(row0 + g), g, t);
         }
         const uint64_t* kb = key_r + j * kstride_j;
         const uint64_t* ka = kb + kstride_p;
 #pragma unroll
         for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * nthr;
+            const int i = threadIdx.x + k * NTHR;
             const uint64_t D = sm[G::addr(i >> LOG_M, i & (G::M - 1))];   // < 4q
             mac128(acc0[k], D, __ldg(kb + i));
             mac128(acc1[k], D, __ldg(ka + i));
@@ -68,33 +69,65 @@ __global__ void __launch_bounds__(256) k_ks_ip(KsJob job, Tables tb) {
     uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
 #pragma unroll
     for (int k = 0; k < EPT; k++) {
-        const int i = threadIdx.x + k * nthr;
+        const int i = threadIdx.x + k * NTHR;
         out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
         out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
     }
 }
 
-template <int LOG_M>
+template <int LOG_M, int LOG_R, int GR, int MINB>
 static cudaError_t ks_ip_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
-    using G = Geo<LOG_M, LOG_R_KS>;
+    using G = Geo<LOG_M, LOG_R>;
     const int rows = 1 << (tb.log_n - LOG_M);
-    int gr = 256 / G::T;
-    if (gr > rows) gr = rows;
-    const int threads = gr * G::T;
-    const size_t smem = (size_t)gr * G::STRIDE * sizeof(uint64_t);
-    dim3 grid((rows / gr) * nz, job.l1 + 1, 1);
-    k_ks_ip<LOG_M><<<grid, threads, smem, st>>>(job, tb);
+    if (rows < GR) return cudaErrorInvalidValue;
+    constexpr int threads = GR * G::T;
+    const size_t smem = (size_t)GR * G::STRIDE * sizeof(uint64_t);
+    dim3 grid((rows / GR) * nz, job.l1 + 1, 1);
+    k_ks_ip<LOG_M, LOG_R, GR, MINB><<<grid, threads, smem, st>>>(job, tb);
     return cudaGetLastError();
+}
+
+static int ks_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("HISA_KS_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+template <int LOG_M>
+static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+    const int rows = 1 << (tb.log_n - LOG_M);
+    switch (ks_variant()) {
+        case 1: if (rows >= 4) return ks_ip_t<LOG_M, 2, 4, 1>(job, tb, nz, st); break;
+        case 2: if (rows >= 8) return ks_ip_t<LOG_M, 2, 8, 1>(job, tb, nz, st); break;
+        case 3: if (rows >= 8) return ks_ip_t<LOG_M, 3, 8, 2>(job, tb, nz, st); break;
+        case 4: if (rows >= 4) return ks_ip_t<LOG_M, 3, 4, 1>(job, tb, nz, st); break;
+        case 5: if (rows >= 4) return ks_ip_t<LOG_M, 2, 4, 3>(job, tb, nz, st); break;
+        case 6: if (rows >= 4) return ks_ip_t<LOG_M, 2, 4, 2>(job, tb, nz, st); break;
+        case 7: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 4>(job, tb, nz, st); break;
+        case 8: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 5>(job, tb, nz, st); break;
+        case 9: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 6>(job, tb, nz, st); break;
+        case 10: if (rows >= 1) return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st); break;
+        case 11: if (rows >= 2) return ks_ip_t<LOG_M, 3, 2, 4>(job, tb, nz, st); break;
+        case 12: if (rows >= 4) return ks_ip_t<LOG_M, 2, 4, 4>(job, tb, nz, st); break;
+        case 13: if (rows >= 1) return ks_ip_t<LOG_M, 2, 1, 12>(job, tb, nz, st); break;
+        default: break;
+    }
+    // default = variant 10 (measured best on B200 at N = 2^16, L = 24: radix-4 phases, one row
+    // per CTA of 64 threads, >= 8 CTAs / SM; profiles/r1_ks_variants.txt)
+    return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
 }
 
 cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     const int lm = tb.log_n - split_m1(tb.log_n);
     switch (lm) {
-        case 4: return ks_ip_t<4>(job, tb, nz, st);
-        case 5: return ks_ip_t<5>(job, tb, nz, st);
-        case 6: return ks_ip_t<6>(job, tb, nz, st);
-        case 7: return ks_ip_t<7>(job, tb, nz, st);
-        case 8: return ks_ip_t<8>(job, tb, nz, st);
+        case 4: return ks_ip_m<4>(job, tb, nz, st);
+        case 5: return ks_ip_m<5>(job, tb, nz, st);
+        case 6: return ks_ip_m<6>(job, tb, nz, st);
+        case 7: return ks_ip_m<7>(job, tb, nz, st);
+        case 8: return ks_ip_m<8>(job, tb, nz, st);
     }
     return cudaErrorInvalidValue;
 }

@@ -1,6 +1,7 @@
 // ntt_kernels.cu -- pass kernels (a1/a2) and the fused lift / combine variants used by rescale
 // (a8), ModUp and ModDown (a5).  See ntt.cuh for the decomposition.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include "ntt.cuh"
 #include "launch.h"
 
@@ -32,8 +33,8 @@ __device__ __forceinline__ bool job_limb(const PassJob& job, int& a, int& b) {
 // ------------------------------------------------------------------------------------------
 // forward pass 1: columns.  Tile = Gc consecutive columns (Gc = blockDim/T), M = M1 rows.
 // ------------------------------------------------------------------------------------------
-template <int LOG_M, int LOG_R, int LOADMODE>
-__global__ void __launch_bounds__(256) k_fwd_cols(PassJob job, Tables tb) {
+template <int LOG_M, int LOG_R, int LOADMODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
     int a, b;
@@ -80,8 +81,8 @@ __global__ void __launch_bounds__(256) k_fwd_cols(PassJob job, Tables tb) {
 // forward pass 2: rows (contiguous).  Tile = Gr consecutive rows of M = M2 words.
 // STORE_PLAIN: full reduction.  STORE_COMBINE: out = (aux - v) * comb[mod] (+ add if a < aux_limit).
 // ------------------------------------------------------------------------------------------
-template <int LOG_M, int LOG_R, int STOREMODE>
-__global__ void __launch_bounds__(256) k_fwd_rows(PassJob job, Tables tb) {
+template <int LOG_M, int LOG_R, int STOREMODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
     int a, b;
@@ -132,8 +133,8 @@ __global__ void __launch_bounds__(256) k_fwd_rows(PassJob job, Tables tb) {
 // ------------------------------------------------------------------------------------------
 // inverse pass A: rows; stores lazily in [0, 2q)
 // ------------------------------------------------------------------------------------------
-template <int LOG_M, int LOG_R>
-__global__ void __launch_bounds__(256) k_inv_rows(PassJob job, Tables tb) {
+template <int LOG_M, int LOG_R, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
     int a, b;
@@ -168,8 +169,8 @@ __global__ void __launch_bounds__(256) k_inv_rows(PassJob job, Tables tb) {
 // ------------------------------------------------------------------------------------------
 // inverse pass B: columns; multiplies by N^-1 and fully reduces.
 // ------------------------------------------------------------------------------------------
-template <int LOG_M, int LOG_R>
-__global__ void __launch_bounds__(256) k_inv_cols(PassJob job, Tables tb) {
+template <int LOG_M, int LOG_R, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_inv_cols(PassJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
     int a, b;
@@ -205,13 +206,21 @@ __global__ void __launch_bounds__(256) k_inv_cols(PassJob job, Tables tb) {
 }
 
 // ------------------------------------------------------------------------------------------
-// host launchers
+// host launchers.  Variant (HISA_NTT_VARIANT, tuned on B200): radix of the engine phases
+// (LOG_R) and the __launch_bounds__ minimum blocks per SM.
 // ------------------------------------------------------------------------------------------
-constexpr int LOG_R_NTT = 4;
+static int ntt_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("HISA_NTT_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
 
-template <int LOG_M>
+template <int LOG_M, int LOG_R>
 static void launch_geom(int log_m_other, int& threads, int& gx, size_t& smem) {
-    using G = Geo<LOG_M, LOG_R_NTT>;
+    using G = Geo<LOG_M, LOG_R>;
     int groups_per_limb = 1 << log_m_other;
     int gpc = 256 / G::T;
     if (gpc > groups_per_limb) gpc = groups_per_limb;
@@ -220,40 +229,65 @@ static void launch_geom(int log_m_other, int& threads, int& gx, size_t& smem) {
     smem = (size_t)gpc * G::STRIDE * sizeof(uint64_t);
 }
 
-template <int LOG_M>
+template <int LOG_M, int LOG_R, int MINB>
+static cudaError_t fwd_cols_v(const PassJob& job, const Tables& tb, int nlimbs, int nz, int lift, cudaStream_t st) {
+    int threads, gx; size_t smem;
+    launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
+    dim3 grid(gx, nlimbs, nz);
+    if (lift) k_fwd_cols<LOG_M, LOG_R, LOAD_LIFT, MINB><<<grid, threads, smem, st>>>(job, tb);
+    else k_fwd_cols<LOG_M, LOG_R, LOAD_PLAIN, MINB><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+template <int LOG_M, int LOG_R, int MINB>
+static cudaError_t fwd_rows_v(const PassJob& job, const Tables& tb, int nlimbs, int nz, int combine, cudaStream_t st) {
+    int threads, gx; size_t smem;
+    launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
+    dim3 grid(gx, nlimbs, nz);
+    if (combine) k_fwd_rows<LOG_M, LOG_R, STORE_COMBINE, MINB><<<grid, threads, smem, st>>>(job, tb);
+    else k_fwd_rows<LOG_M, LOG_R, STORE_PLAIN, MINB><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+template <int LOG_M, int LOG_R, int MINB>
+static cudaError_t inv_rows_v(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st) {
+    int threads, gx; size_t smem;
+    launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
+    dim3 grid(gx, nlimbs, nz);
+    k_inv_rows<LOG_M, LOG_R, MINB><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+template <int LOG_M, int LOG_R, int MINB>
+static cudaError_t inv_cols_v(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st) {
+    int threads, gx; size_t smem;
+    launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
+    dim3 grid(gx, nlimbs, nz);
+    k_inv_cols<LOG_M, LOG_R, MINB><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+#define NTT_DISPATCH(FN, ...)                                                   \
+    switch (ntt_variant()) {                                                    \
+        case 1: return FN<LM, 4, 1>(__VA_ARGS__);                               \
+        case 2: return FN<LM, 3, 1>(__VA_ARGS__);                               \
+        case 3: return FN<LM, 3, 4>(__VA_ARGS__);                               \
+        case 4: return FN<LM, 4, 3>(__VA_ARGS__);                               \
+        default: return FN<LM, 4, 4>(__VA_ARGS__);  /* measured best: radix-16, 4 CTAs/SM */ \
+    }
+template <int LM>
 static cudaError_t fwd_cols_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, int lift, cudaStream_t st) {
-    int threads, gx; size_t smem;
-    launch_geom<LOG_M>(tb.log_n - LOG_M, threads, gx, smem);
-    dim3 grid(gx, nlimbs, nz);
-    if (lift) k_fwd_cols<LOG_M, LOG_R_NTT, LOAD_LIFT><<<grid, threads, smem, st>>>(job, tb);
-    else k_fwd_cols<LOG_M, LOG_R_NTT, LOAD_PLAIN><<<grid, threads, smem, st>>>(job, tb);
-    return cudaGetLastError();
+    NTT_DISPATCH(fwd_cols_v, job, tb, nlimbs, nz, lift, st)
 }
-template <int LOG_M>
+template <int LM>
 static cudaError_t fwd_rows_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, int combine, cudaStream_t st) {
-    int threads, gx; size_t smem;
-    launch_geom<LOG_M>(tb.log_n - LOG_M, threads, gx, smem);
-    dim3 grid(gx, nlimbs, nz);
-    if (combine) k_fwd_rows<LOG_M, LOG_R_NTT, STORE_COMBINE><<<grid, threads, smem, st>>>(job, tb);
-    else k_fwd_rows<LOG_M, LOG_R_NTT, STORE_PLAIN><<<grid, threads, smem, st>>>(job, tb);
-    return cudaGetLastError();
+    NTT_DISPATCH(fwd_rows_v, job, tb, nlimbs, nz, combine, st)
 }
-template <int LOG_M>
+template <int LM>
 static cudaError_t inv_rows_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st) {
-    int threads, gx; size_t smem;
-    launch_geom<LOG_M>(tb.log_n - LOG_M, threads, gx, smem);
-    dim3 grid(gx, nlimbs, nz);
-    k_inv_rows<LOG_M, LOG_R_NTT><<<grid, threads, smem, st>>>(job, tb);
-    return cudaGetLastError();
+    NTT_DISPATCH(inv_rows_v, job, tb, nlimbs, nz, st)
 }
-template <int LOG_M>
+template <int LM>
 static cudaError_t inv_cols_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, cudaStream_t st) {
-    int threads, gx; size_t smem;
-    launch_geom<LOG_M>(tb.log_n - LOG_M, threads, gx, smem);
-    dim3 grid(gx, nlimbs, nz);
-    k_inv_cols<LOG_M, LOG_R_NTT><<<grid, threads, smem, st>>>(job, tb);
-    return cudaGetLastError();
+    NTT_DISPATCH(inv_cols_v, job, tb, nlimbs, nz, st)
 }
+#undef NTT_DISPATCH
 
 int split_m1(int log_n) { return log_n / 2; }
 
