@@ -192,6 +192,11 @@ struct hisa_ctx {
     ulonglong2* d_ninv = nullptr;
     ulonglong2* d_pinv = nullptr;     // p^-1 mod q_i (ModDown)
     ulonglong2* d_qlinv = nullptr;    // [l][L+1]: q_l^-1 mod q_i (rescale)
+    double* d_fwd_d = nullptr;        // FP64-engine twiddles (moduli < 2^50, ntt_f64.cuh)
+    double* d_inv_d = nullptr;
+    double2* d_modd = nullptr;
+    double* d_ninv_d = nullptr;
+    double f64_max_q = 0x1p50;        // FP64 engine for q < 2^50 (HISA_F64=0 disables; diagnostics)
     std::vector<void*> table_allocs;
     // keys
     bool have_sk = false;
@@ -222,6 +227,11 @@ struct hisa_ctx {
         t.mods = d_mods;
         t.ninv = d_ninv;
         t.comb = comb;
+        t.fwd_d = d_fwd_d;
+        t.inv_d = d_inv_d;
+        t.modd = d_modd;
+        t.ninv_d = d_ninv_d;
+        t.f64_max_q = f64_max_q;
         t.log_n = log_n;
         return t;
     }
@@ -442,6 +452,8 @@ extern "C" int hisa_ctx_create(const hisa_params* p, hisa_ctx** out) {
     const int M = c->L + 1;
     const uint64_t N = c->N;
     std::vector<ulonglong2> fwd((size_t)M * N), inv((size_t)M * N), ninv(M), pinv(M), qlinv((size_t)c->L * M);
+    std::vector<double> fwd_d((size_t)M * N), inv_d((size_t)M * N), ninv_d(M);
+    std::vector<double2> modd(M);
     std::vector<Mod> mods(M);
     for (int m = 0; m < M; m++) {
         const uint64_t q = c->mod[m];
@@ -455,9 +467,13 @@ extern "C" int hisa_ctx_create(const hisa_params* p, hisa_ctx** out) {
             const uint64_t w = pw[h_brv((uint32_t)k, c->log_n)], wi = pwi[h_brv((uint32_t)k, c->log_n)];
             fwd[(size_t)m * N + k] = make_ulonglong2(w, shoup(w, q));
             inv[(size_t)m * N + k] = make_ulonglong2(wi, shoup(wi, q));
+            fwd_d[(size_t)m * N + k] = (double)w;    // exact: w < q < 2^50 where used
+            inv_d[(size_t)m * N + k] = (double)wi;
         }
         const uint64_t ni = h_inv(N % q, q);
         ninv[m] = make_ulonglong2(ni, shoup(ni, q));
+        ninv_d[m] = (double)ni;
+        modd[m] = make_double2((double)q, 1.0 / (double)q);
         const uint64_t pi = h_inv(pp % q, q);
         pinv[m] = make_ulonglong2(pi, shoup(pi, q));
     }
@@ -477,7 +493,11 @@ extern "C" int hisa_ctx_create(const hisa_params* p, hisa_ctx** out) {
               up((void**)&c->d_inv, inv.data(), inv.size() * sizeof(ulonglong2)) &&
               up((void**)&c->d_ninv, ninv.data(), M * sizeof(ulonglong2)) &&
               up((void**)&c->d_pinv, pinv.data(), M * sizeof(ulonglong2)) &&
-              up((void**)&c->d_qlinv, qlinv.data(), qlinv.size() * sizeof(ulonglong2));
+              up((void**)&c->d_qlinv, qlinv.data(), qlinv.size() * sizeof(ulonglong2)) &&
+              up((void**)&c->d_fwd_d, fwd_d.data(), fwd_d.size() * sizeof(double)) &&
+              up((void**)&c->d_inv_d, inv_d.data(), inv_d.size() * sizeof(double)) &&
+              up((void**)&c->d_ninv_d, ninv_d.data(), M * sizeof(double)) &&
+              up((void**)&c->d_modd, modd.data(), M * sizeof(double2));
     if (!ok) {
         for (void* q : c->table_allocs) cudaFree(q);
         delete c;
@@ -485,6 +505,7 @@ extern "C" int hisa_ctx_create(const hisa_params* p, hisa_ctx** out) {
         return fail(HISA_E_CUDA, "table upload failed");
     }
     c->objs.push_back(Obj());   // slot 0 reserved
+    if (const char* e = getenv("HISA_F64")) c->f64_max_q = atoi(e) ? 0x1p50 : 0.0;
     *out = c;
     return HISA_OK;
 }

@@ -8,6 +8,7 @@
 // D never touches HBM in its NTT form; the key is streamed once per ciphertext.
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include "ntt_f64.cuh"
 #include "launch.h"
 
 namespace hisa {
@@ -30,6 +31,8 @@ __global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_i
     const long long off0 = (long long)row0 << LOG_M;
     const int mi = job.mod_map[ri];
     const Mod md = tb.mods[mi];
+    const bool fp = (double)md.q < tb.f64_max_q;
+    const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
     constexpr int NTHR = GR * G::T;
     constexpr int EPT = G::R;   // elements per thread in the MAC phase (tile / threads)
     U128 acc0[EPT], acc1[EPT];
@@ -50,16 +53,23 @@ __global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_i
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
+        const bool conv = fp && j != ri;   // FP64-engine output: centred-lazy doubles
         if (j != ri) {
-            fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
-                                     (uint32_t)(row0 + g), g, t);
+            if (fp)
+                fwd_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y,
+                                             tb.fwd_d + ((long long)mi << log_n), log_n - LOG_M,
+                                             (uint32_t)(row0 + g), g, t);
+            else
+                fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
+                                         (uint32_t)(row0 + g), g, t);
         }
         const uint64_t* kb = key_r + j * kstride_j;
         const uint64_t* ka = kb + kstride_p;
 #pragma unroll
         for (int k = 0; k < EPT; k++) {
             const int i = threadIdx.x + k * NTHR;
-            const uint64_t D = sm[G::addr(i >> LOG_M, i & (G::M - 1))];   // < 4q
+            uint64_t D = sm[G::addr(i >> LOG_M, i & (G::M - 1))];   // int: < 4q
+            if (conv) D = d_canon(__longlong_as_double((long long)D), qd.x, qd.y);
             mac128(acc0[k], D, __ldg(kb + i));
             mac128(acc1[k], D, __ldg(ka + i));
         }
@@ -99,20 +109,9 @@ static int ks_variant() {
 template <int LOG_M>
 static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     const int rows = 1 << (tb.log_n - LOG_M);
-    switch (ks_variant()) {
-        case 1: if (rows >= 4) return ks_ip_t<LOG_M, 2, 4, 1>(job, tb, nz, st); break;
-        case 2: if (rows >= 8) return ks_ip_t<LOG_M, 2, 8, 1>(job, tb, nz, st); break;
-        case 3: if (rows >= 8) return ks_ip_t<LOG_M, 3, 8, 2>(job, tb, nz, st); break;
-        case 4: if (rows >= 4) return ks_ip_t<LOG_M, 3, 4, 1>(job, tb, nz, st); break;
-        case 5: if (rows >= 4) return ks_ip_t<LOG_M, 2, 4, 3>(job, tb, nz, st); break;
-        case 6: if (rows >= 4) return ks_ip_t<LOG_M, 2, 4, 2>(job, tb, nz, st); break;
+    switch (ks_variant()) {   // alternatives kept for re-measurement (profiles/r1_ks_variants.txt)
         case 7: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 4>(job, tb, nz, st); break;
-        case 8: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 5>(job, tb, nz, st); break;
-        case 9: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 6>(job, tb, nz, st); break;
-        case 10: if (rows >= 1) return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st); break;
-        case 11: if (rows >= 2) return ks_ip_t<LOG_M, 3, 2, 4>(job, tb, nz, st); break;
-        case 12: if (rows >= 4) return ks_ip_t<LOG_M, 2, 4, 4>(job, tb, nz, st); break;
-        case 13: if (rows >= 1) return ks_ip_t<LOG_M, 2, 1, 12>(job, tb, nz, st); break;
+        case 8: if (rows >= 8) return ks_ip_t<LOG_M, 3, 8, 1>(job, tb, nz, st); break;
         default: break;
     }
     // default = variant 10 (measured best on B200 at N = 2^16, L = 24: radix-4 phases, one row

@@ -48,6 +48,11 @@ struct Tables {
     const Mod* mods;            // [mod]
     const ulonglong2* ninv;     // [mod] (N^-1, shoup)
     const ulonglong2* comb;     // [mod] combine multiplier (p^-1 or q_l^-1 mod q_i), Shoup
+    const double* fwd_d;        // [mod][N] W as doubles (FP64 engine, q < 2^50; ntt_f64.cuh)
+    const double* inv_d;        // [mod][N]
+    const double2* modd;        // [mod] (q, fl(1/q))
+    const double* ninv_d;       // [mod] N^-1 mod q as double
+    double f64_max_q;           // moduli below this run the FP64 engine (0 disables it)
     int log_n;
 };
 

@@ -1,0 +1,157 @@
+// ntt_f64.cuh -- exact modular NTT butterflies on the FP64 pipe, for limbs with q < 2^50.
+//
+// Why: on B200 the 64-bit integer Shoup butterfly is IMAD-pipe bound (~20 IMAD per butterfly,
+// measured 856 G butterflies/s on all SMs), while an exact FP64 butterfly needs ~11 FP64 ops
+// (measured 1310 G/s even with conditional corrections; tools/mb_fp64.cu).  Every config-2 limb
+// (50-bit q_i) and every 40-bit limb of configs 1, 3-5 qualifies; 60-bit moduli (the special prime,
+// q_0 of configs 1, 3-5) keep the integer engine of ntt.cuh.  Results are the same residues: every
+// FP64 step below is exact integer arithmetic (values are integers of magnitude < 2^53).
+//
+// Representation: a residue class v mod q is held as a double (an integer) of magnitude <= B q,
+// signed ("centred lazy").  Primitives (q < 2^50, qinv = fl(1/q)):
+//   red(v)          = v - rint(v qinv) q                    exact (one FMA); |red(v)| <= (0.5 + B 2^-52) q
+//   mulred(a, w)    = a w - rint(fl(a w) qinv) q, computed exactly as
+//                     h = fl(a w); l = fma(a, w, -h) (= a w - h exactly); t = fma(-qt, q, h) + l
+//                     the FMA result h - qt q is an integer of magnitude < 2^53 (exact), l is an
+//                     integer, |l| <= ulp(h)/2; |t| <= (0.5 + 0.375 |a|/q) q for 0 <= w < q
+//                     (three roundings in the quotient estimate: relative error <= 1.5 2^-52).
+// Forward CT butterfly (X, Y) -> (X' + t, X' - t), X' = red(X), t = mulred(Y, W):
+//   B_out = 0.5 + 0.5 + 0.375 B_in  -> fixed point B = 1.6 (inputs start at B = 1).
+// Inverse GS butterfly (X, Y) -> (red(X + Y), mulred(X - Y, W)):
+//   B_out = max(0.5, 0.5 + 0.75 B_in) -> fixed point B = 2 (|X - Y| <= 4q < 2^52).
+// Loads convert [0, q) uint64 -> double exactly (bit trick, x < 2^52); stores reduce fully:
+//   r = red(v); r += q if r < 0 -> [0, q), then back to uint64.
+#pragma once
+#include <cstdint>
+#include "ntt.cuh"
+
+namespace hisa {
+
+constexpr uint64_t F64_MAX_Q = 1ull << 50;
+
+__device__ __forceinline__ double u2d(uint64_t x) {   // exact for x < 2^52
+    return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), 4503599627370496.0);
+}
+__device__ __forceinline__ uint64_t d2u(double y) {   // y an integer in [0, 2^52)
+    return (uint64_t)__double_as_longlong(__dadd_rn(y, 4503599627370496.0)) & 0xFFFFFFFFFFFFFull;
+}
+__device__ __forceinline__ double redd(double v, double q, double qinv) {
+    return __fma_rn(-rint(__dmul_rn(v, qinv)), q, v);
+}
+__device__ __forceinline__ double mulred(double a, double w, double q, double qinv) {
+    const double h = __dmul_rn(a, w);
+    const double l = __fma_rn(a, w, -h);
+    const double qt = rint(__dmul_rn(h, qinv));
+    return __dadd_rn(__fma_rn(-qt, q, h), l);
+}
+// any centred-lazy value -> canonical residue in [0, q) as uint64
+__device__ __forceinline__ uint64_t d_canon(double v, double q, double qinv) {
+    double r = redd(v, q, qinv);
+    r = r < 0.0 ? __dadd_rn(r, q) : r;
+    r = r >= q ? __dsub_rn(r, q) : r;
+    return d2u(r);
+}
+
+// forward CT stages [s0, s0 + LOG_M) on doubles in smem; mirrors fwd_engine (ntt.cuh) with
+// the FP64 butterfly; tw = doubles W = psi^brv(k) mod q
+template <int LOG_M, int LOG_R>
+__device__ __forceinline__ void fwd_engine_f64(double* sm, double q, double qinv, const double* __restrict__ tw,
+                                               int s0, uint32_t high, int g, int t) {
+    using G = Geo<LOG_M, LOG_R>;
+#pragma unroll
+    for (int u0 = 0; u0 < LOG_M; u0 += LOG_R) {
+        const int w = (LOG_M - u0) < LOG_R ? (LOG_M - u0) : LOG_R;
+        const int lo_bit = LOG_M - u0 - w;
+        const int per = G::R >> w;
+#pragma unroll
+        for (int x = 0; x < G::R; x++) {
+            if (x >= per) break;
+            const int o = t * per + x;
+            const int olow = o & ((1 << lo_bit) - 1);
+            const int ohigh = o >> lo_bit;
+            double reg[G::R];
+            int base = (ohigh << (lo_bit + w)) | olow;
+#pragma unroll
+            for (int e = 0; e < G::R; e++)
+                if (e < (1 << w)) reg[e] = sm[G::addr(g, base | (e << lo_bit))];
+#pragma unroll
+            for (int uu = 0; uu < LOG_R; uu++) {
+                if (uu >= w) break;
+                const int u = u0 + uu;
+                const int dist = 1 << (w - 1 - uu);
+                const uint32_t tbase = (1u << (s0 + u)) + (high << u) + ((uint32_t)ohigh << uu);
+#pragma unroll
+                for (int k = 0; k < (1 << LOG_R); k++) {
+                    if (k >= (1 << uu)) break;
+                    const double W = __ldg(&tw[tbase + k]);
+#pragma unroll
+                    for (int e0 = 0; e0 < G::R; e0++) {
+                        if (e0 >= dist) break;
+                        const int e = k * 2 * dist + e0;
+                        const double X = redd(reg[e], q, qinv);
+                        const double T = mulred(reg[e + dist], W, q, qinv);
+                        reg[e] = __dadd_rn(X, T);
+                        reg[e + dist] = __dsub_rn(X, T);
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < G::R; e++)
+                if (e < (1 << w)) sm[G::addr(g, base | (e << lo_bit))] = reg[e];
+        }
+        __syncthreads();
+    }
+}
+
+// inverse GS stages, mirrors inv_engine (ntt.cuh)
+template <int LOG_M, int LOG_R>
+__device__ __forceinline__ void inv_engine_f64(double* sm, double q, double qinv, const double* __restrict__ tw,
+                                               int v0, int log_n, uint32_t high, int g, int t) {
+    using G = Geo<LOG_M, LOG_R>;
+#pragma unroll
+    for (int b0 = 0; b0 < LOG_M; b0 += LOG_R) {
+        const int w = (LOG_M - b0) < LOG_R ? (LOG_M - b0) : LOG_R;
+        const int lo_bit = b0;
+        const int per = G::R >> w;
+#pragma unroll
+        for (int x = 0; x < G::R; x++) {
+            if (x >= per) break;
+            const int o = t * per + x;
+            const int olow = o & ((1 << lo_bit) - 1);
+            const int ohigh = o >> lo_bit;
+            double reg[G::R];
+            const int base = (ohigh << (lo_bit + w)) | olow;
+#pragma unroll
+            for (int e = 0; e < G::R; e++)
+                if (e < (1 << w)) reg[e] = sm[G::addr(g, base | (e << lo_bit))];
+#pragma unroll
+            for (int uu = 0; uu < LOG_R; uu++) {
+                if (uu >= w) break;
+                const int bit = lo_bit + uu;
+                const int v = v0 + bit;
+                const int dist = 1 << uu;
+                const uint32_t tbase = (1u << (log_n - v - 1)) + (high << (LOG_M - bit - 1)) +
+                                       ((uint32_t)ohigh << (w - uu - 1));
+#pragma unroll
+                for (int k = 0; k < (1 << LOG_R); k++) {
+                    if (k >= (1 << (w - uu - 1))) break;
+                    const double W = __ldg(&tw[tbase + k]);
+#pragma unroll
+                    for (int e0 = 0; e0 < G::R; e0++) {
+                        if (e0 >= dist) break;
+                        const int e = k * 2 * dist + e0;
+                        const double X = reg[e], Y = reg[e + dist];
+                        reg[e] = redd(__dadd_rn(X, Y), q, qinv);
+                        reg[e + dist] = mulred(__dsub_rn(X, Y), W, q, qinv);
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < G::R; e++)
+                if (e < (1 << w)) sm[G::addr(g, base | (e << lo_bit))] = reg[e];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace hisa

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cstdlib>
 #include "ntt.cuh"
+#include "ntt_f64.cuh"
 #include "launch.h"
 
 namespace hisa {
@@ -31,7 +32,15 @@ __device__ __forceinline__ bool job_limb(const PassJob& job, int& a, int& b) {
 }
 
 // ------------------------------------------------------------------------------------------
+// FP64 engine selection: limbs with q < 2^50 run the exact FP64 butterflies (ntt_f64.cuh); the
+// pass-1 -> pass-2 (and pass-A -> pass-B) intermediate of such a limb is stored as centred-lazy
+// doubles (|v| <= 2q), a format only the next pass of the same modulus reads.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool use_f64(uint64_t q, const Tables& tb) { return (double)q < tb.f64_max_q; }
+
+// ------------------------------------------------------------------------------------------
 // forward pass 1: columns.  Tile = Gc consecutive columns (Gc = blockDim/T), M = M1 rows.
+// Input canonical (or lifted) residues; output lazy (int: [0, 4q); FP64: centred doubles).
 // ------------------------------------------------------------------------------------------
 template <int LOG_M, int LOG_R, int LOADMODE, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) {
@@ -46,6 +55,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
     const int col0 = blockIdx.x * Gc;
     const int mi = job.mod_map[b];
     const Mod md = tb.mods[mi];
+    const bool fp = use_f64(md.q, tb);
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
     const int nthr = blockDim.x;
@@ -57,29 +67,39 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
         cp_async8(&sm[G::addr(i & (Gc - 1), i >> lg)], &src[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))]);
     }
     cp_async_wait_all();
-    if (LOADMODE == LOAD_LIFT) {   // each thread lifts the words it copied
-        const uint64_t Qs = tb.mods[job.smod_map[a]].q;
+    if (LOADMODE == LOAD_LIFT || fp) {   // each thread converts the words it copied
+        const uint64_t Qs = LOADMODE == LOAD_LIFT ? tb.mods[job.smod_map[a]].q : 0;
 #pragma unroll 4
         for (int k = 0; k < G::R; k++) {
             const int i = threadIdx.x + k * nthr;
             uint64_t* p = &sm[G::addr(i & (Gc - 1), i >> lg)];
-            *p = lift_centered(*p, Qs, md);
+            uint64_t v = *p;
+            if (LOADMODE == LOAD_LIFT) v = lift_centered(v, Qs, md);
+            if (fp) *reinterpret_cast<double*>(p) = u2d(v);
+            else *p = v;
         }
     }
     __syncthreads();
     int g, t;
     tile_coords<LOG_M, LOG_R>(g, t);
-    fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), 0, 0, g, t);
+    if (fp) {
+        const double2 qd = tb.modd[mi];
+        fwd_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y, tb.fwd_d + ((long long)mi << log_n),
+                                     0, 0, g, t);
+    } else {
+        fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), 0, 0, g, t);
+    }
 #pragma unroll 4
     for (int k = 0; k < G::R; k++) {
         const int i = threadIdx.x + k * nthr;
-        dst[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))] = sm[G::addr(i & (Gc - 1), i >> lg)];   // lazy [0, 4q)
+        dst[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))] = sm[G::addr(i & (Gc - 1), i >> lg)];   // lazy
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// forward pass 2: rows (contiguous).  Tile = Gr consecutive rows of M = M2 words.
-// STORE_PLAIN: full reduction.  STORE_COMBINE: out = (aux - v) * comb[mod] (+ add if a < aux_limit).
+// forward pass 2: rows (contiguous).  Tile = Gr consecutive rows of M = M2 words.  Input = the
+// lazy pass-1 output.  STORE_PLAIN: full reduction.  STORE_COMBINE: out = (aux - v) * comb[mod]
+// (+ add if a < aux_limit).
 // ------------------------------------------------------------------------------------------
 template <int LOG_M, int LOG_R, int STOREMODE, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) {
@@ -93,6 +113,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) 
     const int row0 = blockIdx.x * Gr;
     const int mi = job.mod_map[b];
     const Mod md = tb.mods[mi];
+    const bool fp = use_f64(md.q, tb);
     const long long off0 = (long long)row0 << LOG_M;
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
@@ -107,12 +128,23 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) 
     int g, t;
     tile_coords<LOG_M, LOG_R>(g, t);
     const int s0 = log_n - LOG_M;
-    fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), s0, (uint32_t)(row0 + g), g, t);
+    double2 qd = make_double2(0, 0);
+    if (fp) {
+        qd = tb.modd[mi];
+        fwd_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y, tb.fwd_d + ((long long)mi << log_n),
+                                     s0, (uint32_t)(row0 + g), g, t);
+    } else {
+        fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), s0, (uint32_t)(row0 + g), g, t);
+    }
+    auto canon = [&](int idx) -> uint64_t {
+        const uint64_t w = sm[idx];
+        return fp ? d_canon(__longlong_as_double((long long)w), qd.x, qd.y) : reduce4(w, md.q);
+    };
     if (STOREMODE == STORE_PLAIN) {
 #pragma unroll 4
         for (int k = 0; k < G::R; k++) {
             const int i = threadIdx.x + k * nthr;
-            dst[i] = reduce4(sm[G::addr(i >> LOG_M, i & (G::M - 1))], md.q);
+            dst[i] = canon(G::addr(i >> LOG_M, i & (G::M - 1)));
         }
     } else {
         const uint64_t* aux = job.aux[z] + a * job.aux_a + b * job.aux_b + off0;
@@ -122,7 +154,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) 
 #pragma unroll 4
         for (int k = 0; k < G::R; k++) {
             const int i = threadIdx.x + k * nthr;
-            const uint64_t v = reduce4(sm[G::addr(i >> LOG_M, i & (G::M - 1))], md.q);
+            const uint64_t v = canon(G::addr(i >> LOG_M, i & (G::M - 1)));
             uint64_t r = mul_shoup(sub_mod(aux[i], v, md.q), cm.x, cm.y, md.q);
             if (has_add) r = add_mod(r, add[i], md.q);
             dst[i] = r;
@@ -131,7 +163,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) 
 }
 
 // ------------------------------------------------------------------------------------------
-// inverse pass A: rows; stores lazily in [0, 2q)
+// inverse pass A: rows; input canonical; stores lazily (int: [0, 2q); FP64: centred doubles)
 // ------------------------------------------------------------------------------------------
 template <int LOG_M, int LOG_R, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) {
@@ -145,6 +177,7 @@ __global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) 
     const int row0 = blockIdx.x * Gr;
     const int mi = job.mod_map[b];
     const Mod md = tb.mods[mi];
+    const bool fp = use_f64(md.q, tb);
     const long long off0 = (long long)row0 << LOG_M;
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
@@ -155,10 +188,23 @@ __global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) 
         cp_async8(&sm[G::addr(i >> LOG_M, i & (G::M - 1))], &src[i]);
     }
     cp_async_wait_all();
+    if (fp) {
+#pragma unroll 4
+        for (int k = 0; k < G::R; k++) {
+            uint64_t* p = &sm[G::addr((threadIdx.x + k * nthr) >> LOG_M, (threadIdx.x + k * nthr) & (G::M - 1))];
+            *reinterpret_cast<double*>(p) = u2d(*p);
+        }
+    }
     __syncthreads();
     int g, t;
     tile_coords<LOG_M, LOG_R>(g, t);
-    inv_engine<LOG_M, LOG_R>(sm, md.q, tb.inv + ((long long)mi << log_n), 0, log_n, (uint32_t)(row0 + g), g, t);
+    if (fp) {
+        const double2 qd = tb.modd[mi];
+        inv_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y, tb.inv_d + ((long long)mi << log_n),
+                                     0, log_n, (uint32_t)(row0 + g), g, t);
+    } else {
+        inv_engine<LOG_M, LOG_R>(sm, md.q, tb.inv + ((long long)mi << log_n), 0, log_n, (uint32_t)(row0 + g), g, t);
+    }
 #pragma unroll 4
     for (int k = 0; k < G::R; k++) {
         const int i = threadIdx.x + k * nthr;
@@ -182,6 +228,7 @@ __global__ void __launch_bounds__(256, MINB) k_inv_cols(PassJob job, Tables tb) 
     const int col0 = blockIdx.x * Gc;
     const int mi = job.mod_map[b];
     const Mod md = tb.mods[mi];
+    const bool fp = use_f64(md.q, tb);
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
     const int nthr = blockDim.x;
@@ -195,13 +242,26 @@ __global__ void __launch_bounds__(256, MINB) k_inv_cols(PassJob job, Tables tb) 
     __syncthreads();
     int g, t;
     tile_coords<LOG_M, LOG_R>(g, t);
-    inv_engine<LOG_M, LOG_R>(sm, md.q, tb.inv + ((long long)mi << log_n), log_n - LOG_M, log_n, 0, g, t);
-    const ulonglong2 ni = tb.ninv[mi];
+    if (fp) {
+        const double2 qd = tb.modd[mi];
+        inv_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y, tb.inv_d + ((long long)mi << log_n),
+                                     log_n - LOG_M, log_n, 0, g, t);
+        const double ni = tb.ninv_d[mi];
 #pragma unroll 4
-    for (int k = 0; k < G::R; k++) {
-        const int i = threadIdx.x + k * nthr;
-        dst[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))] =
-            mul_shoup(sm[G::addr(i & (Gc - 1), i >> lg)], ni.x, ni.y, md.q);
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
+            const double v = reinterpret_cast<const double*>(sm)[G::addr(i & (Gc - 1), i >> lg)];
+            dst[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))] = d_canon(mulred(v, ni, qd.x, qd.y), qd.x, qd.y);
+        }
+    } else {
+        inv_engine<LOG_M, LOG_R>(sm, md.q, tb.inv + ((long long)mi << log_n), log_n - LOG_M, log_n, 0, g, t);
+        const ulonglong2 ni = tb.ninv[mi];
+#pragma unroll 4
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
+            dst[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))] =
+                mul_shoup(sm[G::addr(i & (Gc - 1), i >> lg)], ni.x, ni.y, md.q);
+        }
     }
 }
 
@@ -266,9 +326,6 @@ static cudaError_t inv_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
 #define NTT_DISPATCH(FN, ...)                                                   \
     switch (ntt_variant()) {                                                    \
         case 1: return FN<LM, 4, 1>(__VA_ARGS__);                               \
-        case 2: return FN<LM, 3, 1>(__VA_ARGS__);                               \
-        case 3: return FN<LM, 3, 4>(__VA_ARGS__);                               \
-        case 4: return FN<LM, 4, 3>(__VA_ARGS__);                               \
         default: return FN<LM, 4, 4>(__VA_ARGS__);  /* measured best: radix-16, 4 CTAs/SM */ \
     }
 template <int LM>
