@@ -38,6 +38,11 @@ Lowering readings, in the order t
                    Output layout "rep": neuron g R + r at slot r Bk of ciphertext g.
   fc (rep input)   out_k = sum_g mulPlain(z_g, Q_kg), Q_kg[r Bk] = W'[k, g R + r]; rescale;
                    acc += rot(acc, Bk 2^t) for t < log2 R; add beta.  Output "slot0".
+  fire     (config 5, A33) squeeze = conv 1x1 + act; mask (the 3x3 expand's SAME padding needs
+           zeros); e1 = conv 1x1 + act and e3 = conv 3x3 SAME + act on the masked
+           squeeze output; output channels = e1 then e3 (concatenation is metadata).
+  gap      global average pool: acc += rot(acc, wS 2^t) (t < log2 W), then hS 2^t (t < log2 H);
+           slot 0 holds the sum; 1/(H W) folded into the preceding linear layer (A26).
 """
 from __future__ import annotations
 
@@ -59,7 +64,7 @@ class Layout:
 
 
 def fold(net: dict, weights, act_coeffs):
-    """Compile-time rewrite (A25, A26): per linear layer (W', beta); per act gamma."""
+    """Compile-time rewrite (A25, A26): per weight tensor (W', beta); per act gamma."""
     a0, a1, a2 = act_coeffs
     assert a2 > 0, "the folded form needs a2 > 0 (sign(a2) = +1)"
     r = math.sqrt(a2)
@@ -67,18 +72,34 @@ def fold(net: dict, weights, act_coeffs):
     gamma = a0 - a1 * a1 / (4 * a2)
     layers = net["layers"]
     folded, wi, pools = [], 0, 0
+    _c, h, w_ = net["input"]
     for i, layer in enumerate(layers):
+        nxt = layers[i + 1][0] if i + 1 < len(layers) else None
         if layer[0] == "avgpool":
             pools += 1
+            h, w_ = h // 2, w_ // 2
+        if layer[0] == "conv":
+            _, _oc, k, st, p = layer
+            h, w_ = (h + 2 * p - k) // st + 1, (w_ + 2 * p - k) // st + 1
         if layer[0] in ("conv", "fc"):
-            w = np.array(weights[wi], dtype=np.float64) * (0.25 ** pools)
+            if layer[0] == "fc":
+                h, w_ = 1, 1
+            wt = np.array(weights[wi], dtype=np.float64) * (0.25 ** pools)
             pools = 0
             b = 0.0
-            if i + 1 < len(layers) and layers[i + 1][0] == "act":
-                w = w * r
+            if nxt == "act":
+                wt = wt * r
                 b = beta
-            folded.append((w, b))
+            if nxt == "gap":
+                wt = wt / (h * w_)
+            folded.append((wt, b))
             wi += 1
+        if layer[0] == "fire":
+            folded.append((np.array(weights[wi], dtype=np.float64) * (0.25 ** pools) * r, beta))
+            folded.append((np.array(weights[wi + 1], dtype=np.float64) * r, beta))
+            folded.append((np.array(weights[wi + 2], dtype=np.float64) * r, beta))
+            pools = 0
+            wi += 3
     return folded, gamma
 
 
@@ -117,6 +138,16 @@ class OracleNet:
             elif kind == "avgpool":
                 amts.update({lay.wS % s, lay.hS % s, (lay.hS + lay.wS) % s})
                 lay = Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
+            elif kind == "fire":
+                for i in range(3):
+                    for j in range(3):
+                        amts.add((lay.origin + (i - 1) * lay.hS + (j - 1) * lay.wS) % s)
+                amts.add(lay.origin % s)
+                lay = Layout("hw", layer[2] + layer[3], lay.H, lay.W, lay.hS, lay.wS, lay.origin, False)
+            elif kind == "gap":
+                amts.update(lay.wS * 2 ** t for t in range(int(math.log2(lay.W))))
+                amts.update(lay.hS * 2 ** t for t in range(int(math.log2(lay.H))))
+                lay = Layout("slot0", lay.C, 1, 1)
             elif kind == "fc" and lay.kind == "hw" and len(layer) > 2 and layer[2] > 1:
                 R = layer[2]
                 span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
@@ -309,6 +340,30 @@ class OracleNet:
                 outs.append(acc)
         return outs, Layout("slot0", n_out, 1, 1)
 
+    def fire(self, cts, lay, layer, f3):
+        _, sq, e1, e3 = layer
+        (wsq, bsq), (we1, b1), (we3, b3) = f3
+        s, ls = self.conv(cts, lay, ("conv", sq, 1, 1, 0), wsq, bsq)
+        s, ls = self.act(s, ls)
+        s, ls = self._mask(s, ls)
+        x1, l1 = self.conv(s, ls, ("conv", e1, 1, 1, 0), we1, b1)
+        x3, _l3 = self.conv(s, ls, ("conv", e3, 3, 1, 1), we3, b3)
+        x1, l1 = self.act(x1, l1)
+        x3, _l3 = self.act(x3, _l3)
+        return x1 + x3, Layout("hw", e1 + e3, l1.H, l1.W, l1.hS, l1.wS, l1.origin, False)
+
+    def gap(self, cts, lay):
+        o = self.o
+        out = []
+        for ct in cts:
+            acc = ct
+            for t in range(int(math.log2(lay.W))):
+                acc = o.add(acc, o.rot_left(acc, lay.wS * 2 ** t))
+            for t in range(int(math.log2(lay.H))):
+                acc = o.add(acc, o.rot_left(acc, lay.hS * 2 ** t))
+            out.append(acc)
+        return out, Layout("slot0", lay.C, 1, 1)
+
     def forward(self, cts, lay, trace=None, stop_after=None):
         """Server-side evaluation; `trace` (a list) receives (layer index, ciphertexts) after
         every layer for per-layer parity checks; `stop_after` = last layer index to evaluate
@@ -332,6 +387,11 @@ class OracleNet:
                 cts, lay = self.act(cts, lay, square_only=True)
             elif kind == "avgpool":
                 cts, lay = self.avgpool(cts, lay)
+            elif kind == "fire":
+                cts, lay = self.fire(cts, lay, layer, self.folded[wi:wi + 3])
+                wi += 3
+            elif kind == "gap":
+                cts, lay = self.gap(cts, lay)
             else:
                 raise ValueError(kind)
             if trace is not None:

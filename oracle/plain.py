@@ -9,6 +9,7 @@ folded (A25 folding is an encrypted-side rewrite, checked against this unfolded 
     square  x^2                         (config 1)
     avgpool mean over 2x2 windows, stride 2 (max-pool replaced by average pool)
     fc      W @ flatten(x), flatten order (c, y, x)
+    fire    SqueezeNet module: s = act(conv1x1(x)); concat(act(conv1x1(s)), act(conv3x3 SAME(s)))
     gap     mean over H x W
 """
 from __future__ import annotations
@@ -63,6 +64,13 @@ def forward(net: dict, image: np.ndarray, weights, act_coeffs) -> np.ndarray:
         elif kind == "fc":
             x = weights[wi] @ x.reshape(-1)
             wi += 1
+        elif kind == "fire":
+            _, _sq, _e1, _e3 = layer
+            sq = act(conv2d(x, weights[wi], 1, 0), act_coeffs)
+            e1 = act(conv2d(sq, weights[wi + 1], 1, 0), act_coeffs)
+            e3 = act(conv2d(sq, weights[wi + 2], 1, 1), act_coeffs)
+            x = np.concatenate([e1, e3], axis=0)
+            wi += 3
         elif kind == "gap":
             x = x.mean(axis=(1, 2))
         else:

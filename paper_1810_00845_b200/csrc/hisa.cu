@@ -1503,36 +1503,71 @@ extern "C" int hisa_bootstrap(hisa_ctx* c, hisa_ct h) {
 struct ConvJob {
     int T, OC, l1, log_n;
     long long poly_stride;
+    int red_every;          // partial Barrett every this many terms (128-bit headroom: 2^127 / q^2)
 };
-// weights: [OC][T][l1] residues; in_ptrs: device array of T pointers; out_ptrs: OC pointers
+// K8: out[o][x] = sum_t W[limb][o][t] in[t][x] mod q_limb -- a modular GEMM (OC x T) x (T x N)
+// per limb and poly.  CTA = 256 threads x 2 words (16-byte loads); OT outputs per pass held in
+// 128-bit register accumulators; the T input pointers and a TT-wide weight tile live in shared
+// memory (no dependent global loads in the t loop); inputs are re-read from L2 once per OT
+// outputs.  weights: [limb][OC][T] residues; in_ptrs: device array of T pointers; out_ptrs: OC.
+constexpr int CONV_OT = 8, CONV_TT = 256;
 __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restrict__ in_ptrs,
                                                   uint64_t* const* __restrict__ out_ptrs,
                                                   const uint64_t* __restrict__ w, ConvJob job,
                                                   const Mod* __restrict__ mods) {
+    extern __shared__ uint64_t csm[];
+    const uint64_t** ptrs = reinterpret_cast<const uint64_t**>(csm);          // [T]
+    uint64_t* wsm = csm + job.T;                                               // [OT][TT]
     const long long N = 1ll << job.log_n;
     const int poly = blockIdx.z;
     const int limb = blockIdx.y;
     const Mod md = mods[limb];
-    constexpr int OT = 8;   // outputs per pass held in registers
     const long long off = (long long)poly * job.poly_stride + (long long)limb * N;
-    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < N; x += (long long)gridDim.x * blockDim.x) {
-        for (int o0 = 0; o0 < job.OC; o0 += OT) {
-            U128 acc[OT];
+    const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+    for (int t = threadIdx.x; t < job.T; t += blockDim.x) ptrs[t] = in_ptrs[t] + off;
+    const uint64_t* wl = w + (long long)limb * job.OC * job.T;
+    for (int o0 = 0; o0 < job.OC; o0 += CONV_OT) {
+        U128 acc[CONV_OT][2];
 #pragma unroll
-            for (int k = 0; k < OT; k++) acc[k] = U128{0, 0};
-            for (int t = 0; t < job.T; t++) {
-                const uint64_t v = in_ptrs[t][off + x];
+        for (int k = 0; k < CONV_OT; k++) { acc[k][0] = U128{0, 0}; acc[k][1] = U128{0, 0}; }
+        int since = 0;   // terms since the last partial reduction (carried across weight tiles)
+        for (int t0 = 0; t0 < job.T; t0 += CONV_TT) {
+            const int tn = min(CONV_TT, job.T - t0);
+            __syncthreads();
+            for (int i = threadIdx.x; i < CONV_OT * CONV_TT; i += blockDim.x) {
+                const int k = i / CONV_TT, tt = i % CONV_TT;
+                wsm[i] = (o0 + k < job.OC && tt < tn) ? wl[(long long)(o0 + k) * job.T + t0 + tt] : 0;
+            }
+            __syncthreads();
+            if (x < N) {
+                for (int tt = 0; tt < tn; tt++) {
+                    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(ptrs[t0 + tt] + x));
 #pragma unroll
-                for (int k = 0; k < OT; k++)
-                    if (o0 + k < job.OC) mac128(acc[k], v, w[((long long)(o0 + k) * job.T + t) * job.l1 + limb]);
-                if ((t & 31) == 31) {   // keep the 128-bit sums below 2^127
+                    for (int k = 0; k < CONV_OT; k++) {
+                        const uint64_t wk = wsm[k * CONV_TT + tt];
+                        mac128(acc[k][0], v.x, wk);
+                        mac128(acc[k][1], v.y, wk);
+                    }
+                    if (++since == job.red_every) {   // keep the 128-bit sums bounded
+                        since = 0;
 #pragma unroll
-                    for (int k = 0; k < OT; k++) { acc[k].lo = barrett128(acc[k].lo, acc[k].hi, md); acc[k].hi = 0; }
+                        for (int k = 0; k < CONV_OT; k++)
+#pragma unroll
+                            for (int h = 0; h < 2; h++) {
+                                acc[k][h].lo = barrett128(acc[k][h].lo, acc[k][h].hi, md);
+                                acc[k][h].hi = 0;
+                            }
+                    }
                 }
             }
+        }
+        if (x < N) {
 #pragma unroll
-            for (int k = 0; k < OT; k++)
-                if (o0 + k < job.OC) out_ptrs[o0 + k][off + x] = barrett128(acc[k].lo, acc[k].hi, md);
+            for (int k = 0; k < CONV_OT; k++)
+                if (o0 + k < job.OC)
+                    *reinterpret_cast<ulonglong2*>(out_ptrs[o0 + k] + off + x) =
+                        make_ulonglong2(barrett128(acc[k][0].lo, acc[k][0].hi, md),
+                                        barrett128(acc[k][1].lo, acc[k][1].hi, md));
         }
     }
 }
@@ -1551,7 +1586,7 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
     }
     const int level = objs[0]->level, l1 = level + 1;
     const double ps = pt_scale == 0.0 ? (double)c->mod[level] : pt_scale;
-    std::vector<uint64_t> wres((size_t)OC * T * l1);
+    std::vector<uint64_t> wres((size_t)OC * T * l1);   // [limb][OC][T]
     for (size_t o = 0; o < OC; o++)
         for (size_t t = 0; t < T; t++) {
             const double v = W[o * T + t] * ps;
@@ -1559,7 +1594,7 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
             const long long X = llround(v);
             for (int i = 0; i < l1; i++) {
                 const uint64_t q = c->mod[i];
-                wres[(o * T + t) * l1 + i] = (uint64_t)(((__int128)X % (__int128)q + q) % q);
+                wres[((size_t)i * OC + o) * T + t] = (uint64_t)(((__int128)X % (__int128)q + q) % q);
             }
         }
     const long long N = (long long)c->N;
@@ -1577,11 +1612,17 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
     CK(cudaMemcpyAsync(dw, wres.data(), wres.size() * 8, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dip, iptr.data(), T * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dop, optr.data(), OC * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
-    ConvJob cj{(int)T, (int)OC, l1, c->log_n, (long long)l1 * N};
-    dim3 grid((unsigned)std::min<long long>((N + 255) / 256, 64), l1, 2);
+    uint64_t qmax = 0;
+    for (int i = 0; i < l1; i++) qmax = std::max(qmax, c->mod[i]);
+    const double terms = std::ldexp(1.0, 127) / ((double)qmax * (double)qmax);   // 128-bit headroom
+    ConvJob cj{(int)T, (int)OC, l1, c->log_n, (long long)l1 * N, (int)std::min(1024.0, std::floor(terms) - 1)};
+    dim3 grid((unsigned)((N / 2 + 255) / 256), l1, 2);
+    const size_t smem = (size_t)T * sizeof(void*) + (size_t)CONV_OT * CONV_TT * 8;
+    if (smem > 200 * 1024) return fail(HISA_E_PARAMS, "conv accumulation: T = %zu inputs too many", T);
     {
         ProfScope ps_(c, "conv_acc");
-        k_conv_acc<<<grid, 256, 0, c->stream>>>(dip, dop, dw, cj, c->d_mods);
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_conv_acc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_conv_acc<<<grid, 256, smem, c->stream>>>(dip, dop, dw, cj, c->d_mods);
         CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(c->stream));   // host staging vectors must outlive the copies

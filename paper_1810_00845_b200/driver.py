@@ -69,19 +69,36 @@ def act_fold(coeffs):
 
 def compile_weights(net: dict, weights, act_coeffs):
     """Compile-time weight rewriting: avg-pool 1/4 factors pushed into the next linear layer
-    (A26) and the activation scale / bias folded into the preceding one (A25).
-    Returns ([(W', beta)] per linear layer, gamma)."""
+    (A26), the global-average-pool 1/(H W) into the linear layer before it (A26), and the
+    activation scale / bias folded into the preceding linear layer (A25; a fire module's three
+    convs are each followed by an activation).
+    Returns ([(W', beta)] per weight tensor, in order, gamma)."""
     r, beta, gamma = act_fold(act_coeffs)
     layers = net["layers"]
     out, pending, it = [], 1.0, iter(weights)
+    c, h, w = net["input"]
     for i, layer in enumerate(layers):
-        if layer[0] == "avgpool":
+        kind = layer[0]
+        if kind == "avgpool":
             pending *= 0.25
-        elif layer[0] in ("conv", "fc"):
-            nxt_act = i + 1 < len(layers) and layers[i + 1][0] == "act"
-            w = np.asarray(next(it), dtype=np.float64) * pending * (r if nxt_act else 1.0)
-            out.append((w, beta if nxt_act else 0.0))
+            h, w = h // 2, w // 2
+        elif kind in ("conv", "fc"):
+            nxt = layers[i + 1][0] if i + 1 < len(layers) else None
+            if kind == "conv":
+                _, oc, k, st, p = layer
+                h, w = (h + 2 * p - k) // st + 1, (w + 2 * p - k) // st + 1
+                c = oc
+            else:
+                c, h, w = layer[1], 1, 1
+            f = pending * (r if nxt == "act" else 1.0) * (1.0 / (h * w) if nxt == "gap" else 1.0)
+            out.append((np.asarray(next(it), dtype=np.float64) * f, beta if nxt == "act" else 0.0))
             pending = 1.0
+        elif kind == "fire":
+            out.append((np.asarray(next(it), dtype=np.float64) * pending * r, beta))   # squeeze
+            out.append((np.asarray(next(it), dtype=np.float64) * r, beta))             # expand 1x1
+            out.append((np.asarray(next(it), dtype=np.float64) * r, beta))             # expand 3x3
+            pending = 1.0
+            c = layer[2] + layer[3]
     return out, gamma
 
 
@@ -166,6 +183,9 @@ class Symbolic:
         return self._new(*self.cts[a])
 
     def add_scalar(self, a, x):
+        return self._new(*self.cts[a])
+
+    def copy(self, a):
         return self._new(*self.cts[a])
 
     def encode(self, v, scale, level):
@@ -292,14 +312,19 @@ class EncryptedNet:
             masked = False
         amounts = [(lay.origin + (i - p) * lay.hS + (j - p) * lay.wS) % self.slots
                    for i in range(k) for j in range(k)]
-        rotated, wcols = [], []
+        nz = [a for a in amounts if a]
+        rotated, wcols, temps = [], [], []
         for ci, ct in zip(own_in, cts):
-            rs = self.b.rot_left_hoisted(ct, amounts)
-            rotated += rs
+            rs = iter(self.b.rot_left_hoisted(ct, nz) if nz else [])
+            for a in amounts:                     # tap with amount 0 = the input itself
+                h = next(rs) if a else ct
+                rotated.append(h)
+                if a:
+                    temps.append(h)
             wcols.append(w[:, ci].reshape(oc_n, k * k))
         wmat = np.concatenate(wcols, axis=1) if wcols else np.zeros((oc_n, 0))
         outs = self._accumulate(rotated, wmat, oc_n)
-        self._free_all(rotated)
+        self._free_all(temps)
         if masked:
             self._free_all(cts)
         res = []
@@ -349,13 +374,47 @@ class EncryptedNet:
             self._free_all(r + [s1, s2])
         return out, Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
 
-    def _rotate_sum(self, res, amounts):
-        """acc += rot(acc, a) for a in amounts, every ciphertext under one key per step."""
+    def fire(self, cts, lay, layer, folded3, li):
+        """SqueezeNet fire module (config 5, A33): squeeze 1x1 conv + act, mask (the 3x3 expand
+        needs zeros around the valid plane), then ONE expand conv whose OC = e1 + e3
+        outputs are the 1x1 expand (its weights at the centre tap of a 3x3 kernel, amount 0 = no
+        rotation) and the 3x3 SAME expand -- the concatenation is the channel order -- + act."""
+        _, sq, e1, e3 = layer
+        (wsq, bsq), (we1, b1), (we3, b3) = folded3
+        s, lay_s = self.conv(cts, lay, ("conv", sq, 1, 1, 0), wsq, bsq, (li, "sq"))
+        s2, lay_s = self.act(s, lay_s)
+        self._free_all(s)
+        m, lay_m = self.mask(s2, lay_s, (li, "mask"))
+        self._free_all(s2)
+        wexp = np.zeros((e1 + e3, sq, 3, 3))
+        wexp[:e1, :, 1, 1] = we1[:, :, 0, 0]
+        wexp[e1:] = we3
+        assert b1 == b3
+        e, lay_e = self.conv(m, lay_m, ("conv", e1 + e3, 3, 1, 1), wexp, b1, (li, "exp"))
+        self._free_all(m)
+        out, lay_o = self.act(e, lay_e)
+        self._free_all(e)
+        return out, lay_o
+
+    def gap(self, cts, lay):
+        """Global average pool (A26): rotate-and-sum over the valid H x W grid (powers of two)
+        into slot 0; the 1/(H W) is folded into the preceding linear layer."""
+        if lay.H & (lay.H - 1) or lay.W & (lay.W - 1):
+            raise ValueError("global average pool needs power-of-two H, W")
+        amts = [lay.wS << t for t in range(int(math.log2(lay.W)))] + \
+               [lay.hS << t for t in range(int(math.log2(lay.H)))]
+        res = self._rotate_sum(list(cts), amts, consume=False) if amts else [self.b.copy(h) for h in cts]
+        return res, Layout("slot0", lay.C)
+
+    def _rotate_sum(self, res, amounts, consume=True):
+        """acc += rot(acc, a) for a in amounts, every ciphertext under one key per step.  The
+        input handles are freed unless consume=False (or amounts is empty)."""
+        first = True
         for a in amounts:
             rs = self.b.rot_left_batch(res, a)
             nxt = [self.b.add(x, r) for x, r in zip(res, rs)]
-            self._free_all(res + rs)
-            res = nxt
+            self._free_all(rs + (res if consume or not first else []))
+            res, first = nxt, False
         return res
 
     def _mulplain_sums(self, cts, n_in, n_rows, key, li, vals_fn):
@@ -497,6 +556,11 @@ class EncryptedNet:
                 nxt, lay = self.act(cur, lay, square_only=True)
             elif kind == "avgpool":
                 nxt, lay = self.avgpool(cur, lay)
+            elif kind == "fire":
+                nxt, lay = self.fire(cur, lay, layer, self.folded[wi:wi + 3], li)
+                wi += 3
+            elif kind == "gap":
+                nxt, lay = self.gap(cur, lay)
             else:
                 raise ValueError(kind)
             self._free_all(cur, keep=cts)

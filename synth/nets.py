@@ -13,6 +13,8 @@ Layer tuples (PyTorch semantics for the float64 definition):
     ("avgpool",)                   2x2, stride 2
     ("fc", out[, R])               W @ flatten(x) (flatten order c, y, x); R = replicas per
                                    ciphertext in the encrypted lowering (A27), not semantics
+    ("fire", sq, e1, e3)           SqueezeNet fire module (config 5): s = act(conv1x1(x));
+                                   out = concat(act(conv1x1(s)) [e1 ch], act(conv3x3 SAME(s)) [e3 ch])
     ("gap",)                       global average pool (config 5)
 Convs and FCs have no bias (A34).
 """
@@ -38,6 +40,13 @@ NETS = {
                         layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2), ("act",),
                                 ("avgpool",), ("fc", 512, 16), ("act",), ("fc", 10)],
                         sigma=[0.05, 0.05, 0.05, 0.05]),
+    # config 5: SqueezeNet-CIFAR-shaped (A33: conv1 + 4 fire modules + 1x1 conv + global avg pool;
+    # 1 + 4*2 + 1 = 10 conv layers, 9 activations), N = 2^16, 24 limbs
+    "squeezenet": dict(log_n=16, q_bits=[60] + [40] * 23, p_bits=60, scale=2.0 ** 40, input=(3, 32, 32),
+                       layers=[("conv", 64, 3, 1, 1), ("act",), ("avgpool",), ("fire", 16, 32, 32),
+                               ("fire", 16, 32, 32), ("avgpool",), ("fire", 32, 64, 64), ("fire", 32, 64, 64),
+                               ("conv", 10, 1, 1, 0), ("gap",)],
+                       sigma=[0.05] * 14),
 }
 
 
@@ -56,6 +65,10 @@ def linear_shapes(name: str):
         elif layer[0] == "fc":
             shapes.append((layer[1], c * h * w))
             c, h, w = layer[1], 1, 1
+        elif layer[0] == "fire":
+            _, sq, e1, e3 = layer
+            shapes += [(sq, c, 1, 1), (e1, sq, 1, 1), (e3, sq, 3, 3)]
+            c = e1 + e3
         elif layer[0] == "gap":
             h, w = 1, 1
     return shapes

@@ -35,6 +35,25 @@ def _mini_rep_weights():
     return [SN._weights(91 + i, s, 0.3) for i, s in enumerate(shapes)]
 
 
+# SqueezeNet-shaped (config 5 layer kinds): padded 3x3 conv, pools, two fire modules (squeeze,
+# mask, fused 1x1 || 3x3 SAME expand), final 1x1 conv, global average pool
+MINI_SQ = dict(log_n=11, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(3, 8, 8),
+               layers=[("conv", 4, 3, 1, 1), ("act",), ("avgpool",), ("fire", 2, 2, 2), ("avgpool",),
+                       ("fire", 2, 3, 1), ("conv", 3, 1, 1, 0), ("gap",)], sigma=[0.5] * 8)
+
+
+def _mini_sq_weights():
+    from synth import nets as _n
+    saved = _n.NETS.get("_mini_sq")
+    _n.NETS["_mini_sq"] = MINI_SQ
+    try:
+        shapes = _n.linear_shapes("_mini_sq")
+    finally:
+        if saved is None:
+            del _n.NETS["_mini_sq"]
+    return [SN._weights(31 + i, s, 0.5) for i, s in enumerate(shapes)]
+
+
 def _mini_weights():
     shapes = [(2, 2, 3, 3), (2, 2, 3, 3), (3, 2 * 4 * 4), (2, 3)]
     return [SN._weights(77 + i, s, 0.3) for i, s in enumerate(shapes)]
@@ -157,6 +176,35 @@ def test_plan_lenet_large_replicas():
     assert pl["counts"]["rot_hoisted"] == 24 + 32 * 3 + 32 * 24 + 64 * 3
     fc_pts = pl["counts"]["encode"] - 2          # minus the two mask plaintexts
     assert fc_pts == 32 * 64 + 10 * 32
+
+
+def test_oracle_net_squeezenet_kinds_match_float64():
+    """Pins the oracle's fire-module and global-average-pool lowering to the float64 net."""
+    from oracle import plain
+    from oracle.nets import OracleNet
+    from paper_1810_00845_b200.driver import EncryptedNet
+    W = _mini_sq_weights()
+    img = SN._image(8, MINI_SQ["input"])
+    on = OracleNet(MINI_SQ, W, SN.ACT_COEFFS)
+    cts, lay = on.encrypt_image(img)
+    out, ol = on.forward(cts, lay)
+    got = on.decrypt_output(out, ol)
+    ref = plain.forward(MINI_SQ, img, W, SN.ACT_COEFFS)
+    assert got.shape == ref.shape == (3,)
+    assert np.abs(got - ref).max() <= 1e-3, (got, ref)
+    pl = EncryptedNet.plan(MINI_SQ, W, SN.ACT_COEFFS, on.o.moduli)
+    assert pl["rotations"] == on.amounts
+    assert pl["levels_used"] == 13 and pl["final_level"] == 0
+
+
+def test_plan_squeezenet_levels():
+    """Config 5 (A33): 1 + 4 x 5 + 1 + 1 = 23 of 23 levels with masked fire expands (A24)."""
+    from paper_1810_00845_b200.driver import EncryptedNet
+    net = SN.NETS["squeezenet"]
+    pl = EncryptedNet.plan(net, SN.net_weights("squeezenet"), SN.ACT_COEFFS, _moduli(net))
+    assert pl["levels_used"] == 23 and pl["final_level"] == 0
+    # hoisted rotations: conv1 3 x 8, fire expands 16,16,32,32 input channels x 8, pools 64 x 3 x 2
+    assert pl["counts"]["rot_hoisted"] == 3 * 8 + (16 + 16 + 32 + 32) * 8 + 64 * 3 * 2
 
 
 def test_plan_matches_oracle_rotation_selection():

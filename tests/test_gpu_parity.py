@@ -300,3 +300,58 @@ def test_full_size_bench_config_rotation():
     hz = g.rot_left_hoisted(cts[0], [k, 1])
     assert (g.ct_export(hz[1]) == o.rot_left(oc0, 1).data).all()
     g.close()
+
+
+@pytest.mark.parametrize("fill", ["max", "half", "alt", "zero_one"])
+def test_extreme_residues_ntt_and_keyswitch(pair, fill):
+    """Adversarial residues for the lazy-reduction bounds of both engines (the FP64 engine runs
+    every modulus < 2^50, ntt_f64.cuh; the 60-bit moduli run the integer one): every word q-1,
+    (q-1)/2, alternating q-1 / 0, or 0 / 1.  NTT, INTT, rotation (ModUp + ModDown) and rescale
+    must equal the oracle bit for bit."""
+    g, o = pair.g, pair.o
+    L, N = o.L, o.N
+    data = np.zeros((2, L, N), dtype=np.uint64)
+    for i in range(L):
+        q = o.q[i]
+        if fill == "max":
+            data[:, i, :] = q - 1
+        elif fill == "half":
+            data[:, i, :] = (q - 1) // 2
+        elif fill == "alt":
+            data[:, i, 0::2] = q - 1
+        else:
+            data[:, i, 1::2] = 1
+    h = g.ct_import(data, L - 1, 2, 2.0 ** 40)
+    oc = Ct(data.copy(), L - 1, 2.0 ** 40)
+    pair.same(g.rot_left(h, pair.rots[0]), o.rot_left(oc, pair.rots[0]))
+    if L >= 2:
+        pair.same(g.rescale(h), o.rescale(oc))
+    g.ntt(h, False)
+    want = np.stack([o.ntt(data[p], 0) for p in range(2)])
+    assert (g.ct_export(h) == want).all()
+    g.ntt(h, True)
+    assert (g.ct_export(h) == data).all()
+
+
+def test_conv_accumulate_large_t_worst_case(pair):
+    """K8 across weight tiles (T > 256) and past the 128-bit headroom of 60-bit moduli (partial
+    reductions every 2^127 / q^2 terms): inputs all q - 1 and weights with residue q - 1
+    (X = -1), plus random weights; OC not a multiple of the 8-output register tile."""
+    g, o = pair.g, pair.o
+    L, N = o.L, o.N
+    T, OC = 300, 11
+    data = np.zeros((2, L, N), dtype=np.uint64)
+    for i in range(L):
+        data[:, i, :] = o.q[i] - 1
+    h = g.ct_import(data, L - 1, 2, 2.0 ** 40)
+    oc = Ct(data.copy(), L - 1, 2.0 ** 40)
+    ps = float(o.q[L - 1])
+    W = np.full((OC, T), -1.0 / ps)
+    W[5:] = np.random.default_rng(9).normal(0, 0.3, (OC - 5, T))
+    outs = g.conv_accumulate([h] * T, W.ravel())
+    for oi in (0, 4, 5, OC - 1):
+        acc = None
+        for t in range(T):
+            term = o.mul_scalar(oc, float(W[oi, t]))
+            acc = term if acc is None else o.add(acc, term)
+        pair.same(outs[oi], acc)
