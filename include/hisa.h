@@ -179,6 +179,15 @@ int hisa_mod_switch(hisa_ctx* ctx, hisa_ct ct, int drop, hisa_ct* out);
 int hisa_rot_left_hoisted(hisa_ctx* ctx, hisa_ct ct, const int64_t* k, size_t n, hisa_ct* outs);
 /* the same rotation amount on n ciphertexts of one level, batched launches; outs[n] */
 int hisa_rot_left_batch(hisa_ctx* ctx, const hisa_ct* in, size_t n, int64_t k, hisa_ct* outs);
+/* rotate-and-sum step ("reduction ... in log rotations"; A27): outs[i] = in[i] +
+ * rotLeft(in[i], k) for n ciphertexts of one level, batched under one key, the addition fused into
+ * the final permutation kernel.  Bit-identical to hisa_add(in, hisa_rot_left(in, k)). */
+int hisa_rot_add_batch(hisa_ctx* ctx, const hisa_ct* in, size_t n, int64_t k, hisa_ct* outs);
+/* matmul accumulation: outs[j] = sum_c in[c] * pts[j*C + c] (mulPlain + add) for j < J,
+ * one HBM-streaming kernel; all inputs one level / scale, all plaintexts that level and one scale.
+ * Bit-identical to the mulPlain / add chain. */
+int hisa_mul_plain_accumulate(hisa_ctx* ctx, const hisa_ct* in, size_t C, const hisa_pt* pts, size_t J,
+                              hisa_ct* outs);
 /* out[o] = sum_t W[o*T + t] * in[t] with X = llround(W * pt_scale) (pt_scale 0 => q_top):
  * the mulScalar + add accumulation of Alg. 1 for OC outputs; all inputs one level,
  * one scale; no rescale (caller divScalars once per output) */
@@ -229,6 +238,8 @@ int hisa_profile_read(hisa_ctx* ctx, char* names, size_t names_len, double* ms, 
 int hisa_launch_count(hisa_ctx* ctx, uint64_t* n);
 /* register-resident 64-bit Harvey butterflies on every SM (mod q_0): butterflies per second */
 int hisa_microbench_butterfly(hisa_ctx* ctx, int iters, double* bfly_per_s);
+/* the same with the exact FP64-pipe butterfly used for moduli < 2^50 (ntt_f64.cuh) */
+int hisa_microbench_butterfly_f64(hisa_ctx* ctx, int iters, double* bfly_per_s);
 
 const char* hisa_last_error(void);
 

@@ -136,7 +136,10 @@ cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, 
 struct PtrPack {
     const uint64_t* in[MAXB];
     uint64_t* out[MAXB];
+    const uint64_t* add[MAXB];   // optional addend (rotate-and-sum): out = add + psi_g(in)
     uint64_t g[MAXB];
+    const Mod* mods;
+    int nl;                      // limbs per poly (modulus of limb index i = mods[i % nl])
 };
 __global__ void __launch_bounds__(256) k_automorphism(PtrPack pk, int log_n) {
     const int z = blockIdx.z;
@@ -146,18 +149,46 @@ __global__ void __launch_bounds__(256) k_automorphism(PtrPack pk, int log_n) {
     const uint64_t g = pk.g[z];
     const uint64_t* in = pk.in[z] + ((long long)limb << log_n);
     uint64_t* out = pk.out[z] + ((long long)limb << log_n);
+    const uint64_t* add = pk.add[z] ? pk.add[z] + ((long long)limb << log_n) : nullptr;
+    const uint64_t q = add ? pk.mods[limb % pk.nl].q : 0;
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
         const uint32_t bj = __brev(j) >> (32 - log_n);
         const uint64_t e = ((2ull * bj + 1) * g) & mask2n;
         const uint32_t src = __brev((uint32_t)((e - 1) >> 1)) >> (32 - log_n);
-        out[j] = in[src];
+        out[j] = add ? add_mod(in[src], add[j], q) : in[src];
     }
+}
+
+cudaError_t launch_automorphism_add(const uint64_t* const* in, uint64_t* const* out, const uint64_t* const* add,
+                                    int nz, int nlimbs_total, int nl, int log_n, const uint64_t* gs, const Mod* mods,
+                                    cudaStream_t st) {
+    PtrPack pk;
+    for (int z = 0; z < nz; z++) {
+        pk.in[z] = in[z]; pk.out[z] = out[z]; pk.g[z] = gs[z]; pk.add[z] = add ? add[z] : nullptr;
+    }
+    pk.mods = mods;
+    pk.nl = nl;
+    const int N = 1 << log_n;
+    for (int l0 = 0; l0 < nlimbs_total; l0 += 65535) {
+        const int nlc = nlimbs_total - l0 < 65535 ? nlimbs_total - l0 : 65535;
+        PtrPack pz = pk;
+        for (int z = 0; z < nz; z++) {
+            pz.in[z] += ((long long)l0 << log_n);
+            pz.out[z] += ((long long)l0 << log_n);
+            if (pz.add[z]) pz.add[z] += ((long long)l0 << log_n);
+        }
+        dim3 grid((N + 255) / 256, nlc, nz);
+        k_automorphism<<<grid, 256, 0, st>>>(pz, log_n);
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_automorphism(const uint64_t* const* in, uint64_t* const* out, int nz, int nlimbs_total, int log_n,
                                 const uint64_t* gs, cudaStream_t st) {
     PtrPack pk;
-    for (int z = 0; z < nz; z++) { pk.in[z] = in[z]; pk.out[z] = out[z]; pk.g[z] = gs[z]; }
+    for (int z = 0; z < nz; z++) { pk.in[z] = in[z]; pk.out[z] = out[z]; pk.g[z] = gs[z]; pk.add[z] = nullptr; }
+    pk.mods = nullptr;
+    pk.nl = 1;
     const int N = 1 << log_n;
     for (int l0 = 0; l0 < nlimbs_total; l0 += 65535) {   // grid.y limit (keys have 2 L (L+1) limbs)
         const int nl = nlimbs_total - l0 < 65535 ? nlimbs_total - l0 : 65535;
@@ -187,6 +218,82 @@ cudaError_t launch_reduce_sum(const int64_t* in, uint64_t* out, int npolys, int 
     long long blocks = (total + 255) / 256;
     if (blocks > (long long)sm_count() * 8) blocks = (long long)sm_count() * 8;
     k_reduce_sum<<<(unsigned)blocks, 256, 0, st>>>(in, out, total, l1, log_n, mods);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// mulPlain accumulation (FC / matmul): out_j = sum_c in_c (.) pt_{j,c} for j < J, both
+// ciphertext polys.  HBM stream of the J*C plaintext limbs; OT outputs per pass in 128-bit
+// register accumulators (products < 2^120, partial Barrett every red_every terms).
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_mulplain_acc(const uint64_t* const* __restrict__ in_ptrs,
+                                                      const uint64_t* const* __restrict__ pt_ptrs,
+                                                      uint64_t* const* __restrict__ out_ptrs, MpaJob job,
+                                                      const Mod* __restrict__ mods) {
+    constexpr int OT = 4;
+    extern __shared__ uint64_t msm[];
+    const uint64_t** ins = reinterpret_cast<const uint64_t**>(msm);   // [C]
+    const long long N = 1ll << job.log_n;
+    const int limb = blockIdx.y;
+    const Mod md = mods[limb];
+    const long long loff = (long long)limb * N;
+    const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+    for (int c = threadIdx.x; c < job.C; c += blockDim.x) ins[c] = in_ptrs[c] + loff;
+    __syncthreads();
+    if (x >= N) return;
+    const long long pstride = (long long)job.l1 * N;   // poly stride of a ciphertext
+    for (int j0 = 0; j0 < job.J; j0 += OT) {
+        U128 acc[OT][2][2];
+#pragma unroll
+        for (int k = 0; k < OT; k++)
+#pragma unroll
+            for (int p = 0; p < 2; p++) { acc[k][p][0] = U128{0, 0}; acc[k][p][1] = U128{0, 0}; }
+        int since = 0;
+        for (int c = 0; c < job.C; c++) {
+            const ulonglong2 a0 = __ldg(reinterpret_cast<const ulonglong2*>(ins[c] + x));
+            const ulonglong2 a1 = __ldg(reinterpret_cast<const ulonglong2*>(ins[c] + pstride + x));
+#pragma unroll
+            for (int k = 0; k < OT; k++) {
+                if (j0 + k >= job.J) break;
+                const ulonglong2 pv =
+                    __ldcs(reinterpret_cast<const ulonglong2*>(pt_ptrs[(long long)(j0 + k) * job.C + c] + loff + x));
+                mac128(acc[k][0][0], a0.x, pv.x);
+                mac128(acc[k][0][1], a0.y, pv.y);
+                mac128(acc[k][1][0], a1.x, pv.x);
+                mac128(acc[k][1][1], a1.y, pv.y);
+            }
+            if (++since == job.red_every) {
+                since = 0;
+#pragma unroll
+                for (int k = 0; k < OT; k++)
+#pragma unroll
+                    for (int p = 0; p < 2; p++)
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            acc[k][p][h].lo = barrett128(acc[k][p][h].lo, acc[k][p][h].hi, md);
+                            acc[k][p][h].hi = 0;
+                        }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < OT; k++) {
+            if (j0 + k >= job.J) break;
+#pragma unroll
+            for (int p = 0; p < 2; p++)
+                *reinterpret_cast<ulonglong2*>(out_ptrs[j0 + k] + p * pstride + loff + x) =
+                    make_ulonglong2(barrett128(acc[k][p][0].lo, acc[k][p][0].hi, md),
+                                    barrett128(acc[k][p][1].lo, acc[k][p][1].hi, md));
+        }
+    }
+}
+
+cudaError_t launch_mulplain_acc(const uint64_t* const* in_ptrs, const uint64_t* const* pt_ptrs,
+                                uint64_t* const* out_ptrs, const MpaJob& job, const Mod* mods, cudaStream_t st) {
+    const long long N = 1ll << job.log_n;
+    dim3 grid((unsigned)((N / 2 + 255) / 256), job.l1, 1);
+    const size_t smem = (size_t)job.C * sizeof(void*);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_mulplain_acc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_mulplain_acc<<<grid, 256, smem, st>>>(in_ptrs, pt_ptrs, out_ptrs, job, mods);
     return cudaGetLastError();
 }
 

@@ -20,6 +20,7 @@
 
 #include "../../include/hisa.h"
 #include "launch.h"
+#include "ntt_f64.cuh"
 
 using namespace hisa;
 typedef unsigned __int128 u128;
@@ -1224,7 +1225,7 @@ static int normalize_rot(const hisa_ctx* c, int64_t k, uint64_t* out) {
 static uint64_t galois(const hisa_ctx* c, uint64_t k) { return h_pow(5, k, 2 * c->N); }
 
 // rotation of nz ciphertexts (same level, same amount, own key switch each): batched K4 path
-static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_t** outs) {
+static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_t** outs, bool add_input = false) {
     const int level = in[0]->level, l1 = level + 1;
     const long long N = (long long)c->N;
     auto it = c->rot_keys.find(k);
@@ -1247,7 +1248,14 @@ static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_
     kb.add_polys = 1;
     kb.add_a = 0;
     RET(keyswitch(c, nz, level, it->second, kb));
-    KL("automorphism", launch_automorphism(pres, outs, nz, 2 * l1, c->log_n, gs, c->stream));
+    if (add_input) {   // rotate-and-sum step: out = in + rot(in), the add fused into the permutation
+        const uint64_t* adds[MAXB];
+        for (int z = 0; z < nz; z++) adds[z] = in[z]->ptr;
+        KL("automorphism", launch_automorphism_add(pres, outs, adds, nz, 2 * l1, l1, c->log_n, gs, c->d_mods,
+                                                   c->stream));
+    } else {
+        KL("automorphism", launch_automorphism(pres, outs, nz, 2 * l1, c->log_n, gs, c->stream));
+    }
     dfree(c, pre);
     return HISA_OK;
 }
@@ -1370,6 +1378,81 @@ extern "C" int hisa_rot_left_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int
         for (int z = 0; z < nz; z++)
             outs[i0 + z] = new_handle(c, OBJ_CT, res[z], objs[i0 + z]->level, 2, objs[i0 + z]->scale);
     }
+    return HISA_OK;
+}
+
+extern "C" int hisa_rot_add_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int64_t k, hisa_ct* outs) {
+    CHECK_CTX(c);
+    if ((!in || !outs) && n) return fail(HISA_E_PARAMS, "null argument");
+    if (n == 0) return HISA_OK;
+    std::vector<Obj*> objs(n);
+    for (size_t i = 0; i < n; i++) {
+        objs[i] = get_obj(c, in[i], OBJ_CT);
+        if (!objs[i]) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle at %zu", i);
+        if (objs[i]->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext at %zu", i);
+        if (objs[i]->level != objs[0]->level) return fail(HISA_E_LEVEL_MISMATCH, "batch levels differ");
+    }
+    uint64_t kk;
+    normalize_rot(c, k, &kk);
+    if (kk == 0) {   // x + rot(x, 0) = 2x
+        for (size_t i = 0; i < n; i++) RET(hisa_add(c, in[i], in[i], &outs[i]));
+        return HISA_OK;
+    }
+    if (!c->rot_keys.count(kk)) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk);
+    for (size_t i0 = 0; i0 < n; i0 += MAXB) {
+        const int nz = (int)std::min((size_t)MAXB, n - i0);
+        uint64_t* res[MAXB];
+        RET(rotate_batch(c, objs.data() + i0, nz, kk, res, true));
+        for (int z = 0; z < nz; z++)
+            outs[i0 + z] = new_handle(c, OBJ_CT, res[z], objs[i0 + z]->level, 2, objs[i0 + z]->scale);
+    }
+    return HISA_OK;
+}
+
+extern "C" int hisa_mul_plain_accumulate(hisa_ctx* c, const hisa_ct* in, size_t C, const hisa_pt* pts, size_t J,
+                                         hisa_ct* outs) {
+    CHECK_CTX(c);
+    if (!in || !pts || !outs || C == 0 || J == 0) return fail(HISA_E_PARAMS, "bad arguments");
+    std::vector<Obj*> ci(C), pi(C * J);
+    for (size_t i = 0; i < C; i++) {
+        ci[i] = get_obj(c, in[i], OBJ_CT);
+        if (!ci[i]) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle at %zu", i);
+        if (ci[i]->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly input");
+        if (ci[i]->level != ci[0]->level) return fail(HISA_E_LEVEL_MISMATCH, "input levels differ");
+        if (!scale_eq(ci[i]->scale, ci[0]->scale)) return fail(HISA_E_SCALE_MISMATCH, "input scales differ");
+    }
+    for (size_t i = 0; i < C * J; i++) {
+        pi[i] = get_obj(c, pts[i], OBJ_PT);
+        if (!pi[i]) return fail(HISA_E_INVALID_HANDLE, "invalid plaintext handle at %zu", i);
+        if (pi[i]->level != ci[0]->level) return fail(HISA_E_LEVEL_MISMATCH, "plaintext level at %zu", i);
+        if (!scale_eq(pi[i]->scale, pi[0]->scale)) return fail(HISA_E_SCALE_MISMATCH, "plaintext scales differ");
+    }
+    const int level = ci[0]->level, l1 = level + 1;
+    const long long N = (long long)c->N;
+    std::vector<const uint64_t*> ip(C), pp(C * J);
+    std::vector<uint64_t*> op(J);
+    for (size_t i = 0; i < C; i++) ip[i] = ci[i]->ptr;
+    for (size_t i = 0; i < C * J; i++) pp[i] = pi[i]->ptr;
+    for (size_t j = 0; j < J; j++) {
+        op[j] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        if (!op[j]) return fail(HISA_E_OOM, "mul_plain_accumulate outputs");
+    }
+    void** dev = (void**)dalloc(c, (C + C * J + J) * sizeof(void*));
+    if (!dev) return fail(HISA_E_OOM, "pointer arrays");
+    std::vector<void*> host(C + C * J + J);
+    for (size_t i = 0; i < C; i++) host[i] = (void*)ip[i];
+    for (size_t i = 0; i < C * J; i++) host[C + i] = (void*)pp[i];
+    for (size_t j = 0; j < J; j++) host[C + C * J + j] = op[j];
+    CK(cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+    uint64_t qmax = 0;
+    for (int i = 0; i < l1; i++) qmax = std::max(qmax, c->mod[i]);
+    const double terms = std::ldexp(1.0, 127) / ((double)qmax * (double)qmax);
+    MpaJob mj{(int)C, (int)J, l1, c->log_n, (int)std::min(1024.0, std::floor(terms) - 1)};
+    KL("mulplain_acc", launch_mulplain_acc((const uint64_t* const*)dev, (const uint64_t* const*)(dev + C),
+                                           (uint64_t* const*)(dev + C + C * J), mj, c->d_mods, c->stream));
+    CK(cudaStreamSynchronize(c->stream));   // the host pointer staging must outlive the copy
+    dfree(c, dev);
+    for (size_t j = 0; j < J; j++) outs[j] = new_handle(c, OBJ_CT, op[j], level, 2, ci[0]->scale * pi[0]->scale);
     return HISA_OK;
 }
 
@@ -1878,6 +1961,61 @@ __global__ void __launch_bounds__(256) k_mb_butterfly(uint64_t* out, uint64_t q,
     for (int e = 0; e < 16; e++) x ^= r[e];
     out[blockIdx.x * blockDim.x + threadIdx.x] = x;
 }
+// the same pattern with the exact FP64 butterfly of ntt_f64.cuh (centred-lazy doubles, q < 2^50):
+// the ceiling of the FP64-engine kernels
+__global__ void __launch_bounds__(256) k_mb_butterfly_f64(double* out, double q, double qinv, double w, int iters) {
+    double r[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) r[e] = (double)((threadIdx.x * 16 + e + blockIdx.x) % 1000003);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int st = 0; st < 4; st++) {
+            const int dist = 8 >> st;
+#pragma unroll
+            for (int e = 0; e < 16; e++) {
+                if (e & dist) continue;
+                const double X = redd(r[e], q, qinv);
+                const double T = mulred(r[e + dist], w, q, qinv);
+                r[e] = __dadd_rn(X, T);
+                r[e + dist] = __dsub_rn(X, T);
+            }
+        }
+    }
+    double x = 0;
+#pragma unroll
+    for (int e = 0; e < 16; e++) x += r[e];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x;
+}
+
+extern "C" int hisa_microbench_butterfly_f64(hisa_ctx* c, int iters, double* bfly_per_s) {
+    CHECK_CTX(c);
+    if (!bfly_per_s || iters <= 0) return fail(HISA_E_PARAMS, "bad arguments");
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * 8, threads = 256;
+    double* out = dalloc_t<double>(c, (size_t)blocks * threads);
+    if (!out) return fail(HISA_E_OOM, "microbench");
+    uint64_t q = 0;
+    for (int i = 0; i < c->L; i++)
+        if (c->mod[i] < (1ull << 50)) { q = c->mod[i]; break; }
+    if (!q) q = (1ull << 49) + 1;   // timing only
+    const double qd = (double)q, w = (double)(3 % q);
+    cudaEvent_t a = take_event(c), b = take_event(c);
+    k_mb_butterfly_f64<<<blocks, threads, 0, c->stream>>>(out, qd, 1.0 / qd, w, 4);
+    CK(cudaEventRecord(a, c->stream));
+    k_mb_butterfly_f64<<<blocks, threads, 0, c->stream>>>(out, qd, 1.0 / qd, w, iters);
+    CK(cudaEventRecord(b, c->stream));
+    CK(cudaEventSynchronize(b));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, a, b));
+    c->ev_pool.push_back(a);
+    c->ev_pool.push_back(b);
+    dfree(c, out);
+    *bfly_per_s = (double)blocks * threads * iters * 32.0 / (t * 1e-3);
+    return HISA_OK;
+}
+
 extern "C" int hisa_microbench_butterfly(hisa_ctx* c, int iters, double* bfly_per_s) {
     CHECK_CTX(c);
     if (!bfly_per_s || iters <= 0) return fail(HISA_E_PARAMS, "bad arguments");

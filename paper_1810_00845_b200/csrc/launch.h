@@ -39,6 +39,20 @@ cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, 
 cudaError_t launch_automorphism(const uint64_t* const* in, uint64_t* const* out, int nz, int nlimbs_total,
                                 int log_n, const uint64_t* gs, cudaStream_t st);
 
+// the same with an optional addend per batch entry: out = add + psi_g(in) (rotate-and-sum step);
+// limb index i of the nlimbs_total uses modulus mods[i % nl]
+cudaError_t launch_automorphism_add(const uint64_t* const* in, uint64_t* const* out, const uint64_t* const* add,
+                                    int nz, int nlimbs_total, int nl, int log_n, const uint64_t* gs, const Mod* mods,
+                                    cudaStream_t st);
+
+// mulPlain accumulation (FC): out_j = sum_c in_c (.) pt_{j,c}; device pointer arrays
+struct MpaJob {
+    int C, J, l1, log_n;
+    int red_every;
+};
+cudaError_t launch_mulplain_acc(const uint64_t* const* in_ptrs, const uint64_t* const* pt_ptrs,
+                                uint64_t* const* out_ptrs, const MpaJob& job, const Mod* mods, cudaStream_t st);
+
 // hoisted key-switch inner product (K7): for R rotation amounts sharing one ModUp output D,
 // acc_k[b|a][ri] = sum_j D[j][ri] (.) key_k[j][b|a][ri] -- an HBM stream of the R keys
 constexpr int MAXR = 8;

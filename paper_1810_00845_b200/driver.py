@@ -188,6 +188,19 @@ class Symbolic:
     def copy(self, a):
         return self._new(*self.cts[a])
 
+    def rot_add_batch(self, hs, k):
+        kk = k % self.slots
+        if kk:
+            self.rotations.add(kk)
+            self._count("rot", len(hs))
+        self._count("add", len(hs))
+        return [self._new(*self.cts[h]) for h in hs]
+
+    def mul_plain_accumulate(self, hs, pts, J):
+        lv, sc = self.cts[hs[0]]
+        self._count("mul_plain", len(pts))
+        return [self._new(lv, sc * pts[0][2]) for _ in range(J)]
+
     def encode(self, v, scale, level):
         self._count("encode")
         return ("pt", level, scale)
@@ -411,9 +424,9 @@ class EncryptedNet:
         input handles are freed unless consume=False (or amounts is empty)."""
         first = True
         for a in amounts:
-            rs = self.b.rot_left_batch(res, a)
-            nxt = [self.b.add(x, r) for x, r in zip(res, rs)]
-            self._free_all(rs + (res if consume or not first else []))
+            nxt = self.b.rot_add_batch(res, a)       # x + rot(x, a), add fused into the permutation
+            if consume or not first:
+                self._free_all(res)
             res, first = nxt, False
         return res
 
@@ -423,19 +436,12 @@ class EncryptedNet:
         Multi-GPU: reduce-scattered, so the result is this rank's owned rows."""
         own_in = self.owned(n_in)
         lv = self._level(cts[0]) if cts else None
-        sums = []
-        for jo in range(n_rows):
-            acc = None
-            for ci, ct in zip(own_in, cts):
-                pt = self._plaintext((key, li, jo, ci), lambda jo=jo, ci=ci: vals_fn(jo, ci), lv)
-                term = self.b.mul_plain(ct, pt)
-                if acc is None:
-                    acc = term
-                else:
-                    nxt = self.b.add(acc, term)
-                    self._free_all([acc, term])
-                    acc = nxt
-            sums.append(acc)
+        if cts:   # one fused mulPlain-accumulate launch over all rows (hisa_mul_plain_accumulate)
+            pts = [self._plaintext((key, li, jo, ci), lambda jo=jo, ci=ci: vals_fn(jo, ci), lv)
+                   for jo in range(n_rows) for ci in own_in]
+            sums = self.b.mul_plain_accumulate(list(cts), pts, n_rows)
+        else:
+            sums = [None] * n_rows
         if self.world > 1:
             from . import parallel
             return parallel.reduce_scatter_cts(self, sums, n_rows)

@@ -86,6 +86,8 @@ _SIGS = {
     "hisa_rot_left_batch": [_vp, _u64p, _csz, _ci64, _u64p],
     "hisa_conv_accumulate": [_vp, _u64p, _csz, _dp, _csz, _cd, _u64p],
     "hisa_conv_accumulate_dev": [_vp, _u64p, _csz, _dp, _csz, _cd, _vp],
+    "hisa_rot_add_batch": [_vp, _u64p, _csz, _ci64, _u64p],
+    "hisa_mul_plain_accumulate": [_vp, _u64p, _csz, _u64p, _csz, _u64p],
     "hisa_ct_adopt_sum": [_vp, _vp, _ci, _ci, _cd, _u64p],
     "hisa_ntt": [_vp, _cu64, _ci],
     "hisa_ntt_batch": [_vp, _u64p, _csz, _ci],
@@ -103,6 +105,7 @@ _SIGS = {
     "hisa_profile_read": [_vp, ctypes.c_char_p, _csz, _dp, _u64p, _csz, ctypes.POINTER(_csz)],
     "hisa_launch_count": [_vp, _u64p],
     "hisa_microbench_butterfly": [_vp, _ci, _dp],
+    "hisa_microbench_butterfly_f64": [_vp, _ci, _dp],
     "hisa_last_error": [],
 }
 
@@ -339,6 +342,22 @@ def hisa_conv_accumulate(ctx, cts, W, pt_scale: float = 0.0) -> list[int]:
     return [int(x) for x in outs]
 
 
+def hisa_rot_add_batch(ctx, cts, k: int) -> list[int]:
+    ins = _u64(list(cts))
+    outs = np.zeros(ins.size, dtype=np.uint64)
+    _chk(load().hisa_rot_add_batch(ctx, _ptr(ins, _u64p), ins.size, k, _ptr(outs, _u64p)))
+    return [int(x) for x in outs]
+
+
+def hisa_mul_plain_accumulate(ctx, cts, pts, J: int) -> list[int]:
+    """outs[j] = sum_c cts[c] * pts[j * C + c]."""
+    ins = _u64(list(cts))
+    p = _u64(list(pts))
+    outs = np.zeros(J, dtype=np.uint64)
+    _chk(load().hisa_mul_plain_accumulate(ctx, _ptr(ins, _u64p), ins.size, _ptr(p, _u64p), J, _ptr(outs, _u64p)))
+    return [int(x) for x in outs]
+
+
 def hisa_conv_accumulate_dev(ctx, cts, W, dev_out: int, pt_scale: float = 0.0):
     """Accumulation into caller device memory (uint64 [OC][2][l+1][N] at address dev_out)."""
     ins = _u64(list(cts))
@@ -439,6 +458,12 @@ def hisa_launch_count(ctx) -> int:
 def hisa_microbench_butterfly(ctx, iters: int = 2000) -> float:
     out = _cd()
     _chk(load().hisa_microbench_butterfly(ctx, iters, ctypes.byref(out)))
+    return out.value
+
+
+def hisa_microbench_butterfly_f64(ctx, iters: int = 2000) -> float:
+    out = _cd()
+    _chk(load().hisa_microbench_butterfly_f64(ctx, iters, ctypes.byref(out)))
     return out.value
 
 

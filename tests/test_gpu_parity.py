@@ -355,3 +355,22 @@ def test_conv_accumulate_large_t_worst_case(pair):
             term = o.mul_scalar(oc, float(W[oi, t]))
             acc = term if acc is None else o.add(acc, term)
         pair.same(outs[oi], acc)
+
+
+def test_fused_rot_add_and_mulplain_accumulate(pair):
+    """The fused driver kernels equal their HISA definitions bit for bit: rot_add_batch =
+    add(x, rotLeft(x, k)); mul_plain_accumulate = sum_c mulPlain(x_c, p_{j,c})."""
+    g, o = pair.g, pair.o
+    hs, os_ = zip(*[pair.ct(80 + i) for i in range(3)])
+    k = pair.rots[1]
+    for h, oc in zip(g.rot_add_batch(list(hs), k), os_):
+        pair.same(h, o.add(oc, o.rot_left(oc, k)))
+    C, J = 3, 5
+    pts = [pair.pt(90 + i) for i in range(C * J)]
+    outs = g.mul_plain_accumulate(list(hs), [p[0] for p in pts], J)
+    for j in range(J):
+        acc = None
+        for c in range(C):
+            term = o.mul_plain(os_[c], pts[j * C + c][1])
+            acc = term if acc is None else o.add(acc, term)
+        pair.same(outs[j], acc)
