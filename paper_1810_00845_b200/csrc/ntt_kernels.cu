@@ -67,16 +67,38 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
         cp_async8(&sm[G::addr(i & (Gc - 1), i >> lg)], &src[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))]);
     }
     cp_async_wait_all();
-    if (LOADMODE == LOAD_LIFT || fp) {   // each thread converts the words it copied
-        const uint64_t Qs = LOADMODE == LOAD_LIFT ? tb.mods[job.smod_map[a]].q : 0;
+    // each thread converts the words it copied
+    if (LOADMODE == LOAD_LIFT) {
+        const uint64_t Qs = tb.mods[job.smod_map[a]].q;
+        if (fp && (double)Qs < tb.f64_max_q) {
+            // FP64 centred lift: x in [0, Qs) -> x - Qs if x > Qs/2 (exact, |.| < 2^49), then
+            // reduced mod r into the centred-lazy range (ntt_f64.cuh)
+            const double2 qd = tb.modd[mi];
+            const double qs = (double)Qs, half = (double)(Qs >> 1);
+#pragma unroll 4
+            for (int k = 0; k < G::R; k++) {
+                const int i = threadIdx.x + k * nthr;
+                double* p = reinterpret_cast<double*>(&sm[G::addr(i & (Gc - 1), i >> lg)]);
+                double v = u2d(*reinterpret_cast<const uint64_t*>(p));
+                v = v > half ? __dsub_rn(v, qs) : v;
+                *p = redd(v, qd.x, qd.y);
+            }
+        } else {
+#pragma unroll 4
+            for (int k = 0; k < G::R; k++) {
+                const int i = threadIdx.x + k * nthr;
+                uint64_t* p = &sm[G::addr(i & (Gc - 1), i >> lg)];
+                const uint64_t v = lift_centered(*p, Qs, md);
+                if (fp) *reinterpret_cast<double*>(p) = u2d(v);
+                else *p = v;
+            }
+        }
+    } else if (fp) {
 #pragma unroll 4
         for (int k = 0; k < G::R; k++) {
             const int i = threadIdx.x + k * nthr;
             uint64_t* p = &sm[G::addr(i & (Gc - 1), i >> lg)];
-            uint64_t v = *p;
-            if (LOADMODE == LOAD_LIFT) v = lift_centered(v, Qs, md);
-            if (fp) *reinterpret_cast<double*>(p) = u2d(v);
-            else *p = v;
+            *reinterpret_cast<double*>(p) = u2d(*p);
         }
     }
     __syncthreads();
