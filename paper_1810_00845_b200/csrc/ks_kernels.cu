@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_i
     const Mod md = tb.mods[mi];
     const bool fp = (double)md.q < tb.f64_max_q;
     const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
+    const double qp52 = __dadd_rn(qd.x, 4503599627370496.0);
     constexpr int NTHR = GR * G::T;
     constexpr int EPT = G::R;   // elements per thread in the MAC phase (tile / threads)
     U128 acc0[EPT], acc1[EPT];
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_i
         for (int k = 0; k < EPT; k++) {
             const int i = threadIdx.x + k * NTHR;
             uint64_t D = sm[G::addr(i >> LOG_M, i & (G::M - 1))];   // int: < 4q
-            if (conv) D = d_canon(__longlong_as_double((long long)D), qd.x, qd.y);
+            if (conv) D = d_rep(__longlong_as_double((long long)D), qd.x, qd.y, qp52);   // < 1.5q
             mac128(acc0[k], D, __ldg(kb + i));
             mac128(acc1[k], D, __ldg(ka + i));
         }
@@ -83,6 +84,115 @@ __global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_i
         out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
         out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
     }
+}
+
+// Software-pipelined K4 (variant P): the D tile of digit j+1 is copied into the other half of a
+// double buffer (cp.async groups) and its key words are loaded into registers while digit j's
+// NTT stages run, so neither the tile copy nor the key stream sits on the critical path.
+template <int LOG_M, int LOG_R, int GR, int MINB>
+__global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip_pipe(KsJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R>;
+    extern __shared__ uint64_t sm[];
+    constexpr int TILE = GR * G::STRIDE;
+    const int nz = job.nz;
+    const int z = blockIdx.x % nz;
+    const int ri = blockIdx.y;
+    const int l1 = job.l1;
+    const int nri = l1 + 1;
+    const int log_n = tb.log_n;
+    const int row0 = (blockIdx.x / nz) * GR;
+    const long long off0 = (long long)row0 << LOG_M;
+    const int mi = job.mod_map[ri];
+    const Mod md = tb.mods[mi];
+    const bool fp = (double)md.q < tb.f64_max_q;
+    const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
+    const double qp52 = __dadd_rn(qd.x, 4503599627370496.0);
+    constexpr int NTHR = GR * G::T;
+    constexpr int EPT = G::R;
+    U128 acc0[EPT], acc1[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
+    const int g = threadIdx.x / G::T, t = threadIdx.x % G::T;
+    const long long kstride_j = 2ll * (job.L + 1) << log_n;
+    const long long kstride_p = (long long)(job.L + 1) << log_n;
+    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
+    auto issue_tile = [&](int j) {
+        const uint64_t* src = (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
+                                        : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
+        uint64_t* buf = sm + (j & 1) * TILE;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * NTHR;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[G::addr(i >> LOG_M, i & (G::M - 1))]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + i) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    uint64_t kb_next[EPT], ka_next[EPT];
+    auto load_keys = [&](int j) {
+        const uint64_t* kb = key_r + j * kstride_j;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * NTHR;
+            kb_next[k] = __ldg(kb + i);
+            ka_next[k] = __ldg(kb + kstride_p + i);
+        }
+    };
+    issue_tile(0);
+    load_keys(0);
+    for (int j = 0; j < l1; j++) {
+        uint64_t kb_cur[EPT], ka_cur[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; k++) { kb_cur[k] = kb_next[k]; ka_cur[k] = ka_next[k]; }
+        if (j + 1 < l1) {
+            issue_tile(j + 1);
+            load_keys(j + 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        uint64_t* buf = sm + (j & 1) * TILE;
+        const bool conv = fp && j != ri;
+        if (j != ri) {
+            if (fp)
+                fwd_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(buf), qd.x, qd.y,
+                                             tb.fwd_d + ((long long)mi << log_n), log_n - LOG_M,
+                                             (uint32_t)(row0 + g), g, t);
+            else
+                fwd_engine<LOG_M, LOG_R>(buf, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
+                                         (uint32_t)(row0 + g), g, t);
+        }
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * NTHR;
+            uint64_t D = buf[G::addr(i >> LOG_M, i & (G::M - 1))];
+            if (conv) D = d_rep(__longlong_as_double((long long)D), qd.x, qd.y, qp52);   // < 1.5q
+            mac128(acc0[k], D, kb_cur[k]);
+            mac128(acc1[k], D, ka_cur[k]);
+        }
+        __syncthreads();   // buffer (j & 1) is refilled by iteration j + 1's prefetch of j + 2
+    }
+    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
+    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
+#pragma unroll
+    for (int k = 0; k < EPT; k++) {
+        const int i = threadIdx.x + k * NTHR;
+        out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
+        out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
+    }
+}
+
+template <int LOG_M, int LOG_R, int GR, int MINB>
+static cudaError_t ks_ip_pipe_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+    using G = Geo<LOG_M, LOG_R>;
+    const int rows = 1 << (tb.log_n - LOG_M);
+    if (rows < GR) return cudaErrorInvalidValue;
+    constexpr int threads = GR * G::T;
+    const size_t smem = 2 * (size_t)GR * G::STRIDE * sizeof(uint64_t);
+    dim3 grid((rows / GR) * nz, job.l1 + 1, 1);
+    k_ks_ip_pipe<LOG_M, LOG_R, GR, MINB><<<grid, threads, smem, st>>>(job, tb);
+    return cudaGetLastError();
 }
 
 template <int LOG_M, int LOG_R, int GR, int MINB>
@@ -112,6 +222,11 @@ static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStrea
     switch (ks_variant()) {   // alternatives kept for re-measurement (profiles/r1_ks_variants.txt)
         case 7: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 4>(job, tb, nz, st); break;
         case 8: if (rows >= 8) return ks_ip_t<LOG_M, 3, 8, 1>(job, tb, nz, st); break;
+        case 10: return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
+        case 20: return ks_ip_pipe_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
+        case 21: return ks_ip_pipe_t<LOG_M, 2, 1, 6>(job, tb, nz, st);
+        case 22: if (rows >= 2) return ks_ip_pipe_t<LOG_M, 2, 2, 4>(job, tb, nz, st); break;
+        case 23: return ks_ip_pipe_t<LOG_M, 3, 1, 8>(job, tb, nz, st);
         default: break;
     }
     // default = variant 10 (measured best on B200 at N = 2^16, L = 24: radix-4 phases, one row

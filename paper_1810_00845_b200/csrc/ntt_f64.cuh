@@ -52,6 +52,15 @@ __device__ __forceinline__ uint64_t d_canon(double v, double q, double qinv) {
     return d2u(r);
 }
 
+// any centred-lazy value -> a uint64 representative in (q/2, 3q/2) (no compares): r = red(v) has
+// |r| <= (0.5 + eps) q, so r + q > 0; (r + q + 2^52) is exact (< 2^53) and its low 52 mantissa
+// bits are r + q.  Used where any representative < 2q will do (the key inner product's 128-bit
+// accumulation).
+__device__ __forceinline__ uint64_t d_rep(double v, double q, double qinv, double q_plus_2p52) {
+    const double r = redd(v, q, qinv);
+    return (uint64_t)__double_as_longlong(__dadd_rn(r, q_plus_2p52)) & 0xFFFFFFFFFFFFFull;
+}
+
 // forward CT stages [s0, s0 + LOG_M) on doubles in smem; mirrors fwd_engine (ntt.cuh) with
 // the FP64 butterfly; tw = doubles W = psi^brv(k) mod q
 template <int LOG_M, int LOG_R>
