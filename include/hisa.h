@@ -179,6 +179,10 @@ int hisa_mod_switch(hisa_ctx* ctx, hisa_ct ct, int drop, hisa_ct* out);
 int hisa_rot_left_hoisted(hisa_ctx* ctx, hisa_ct ct, const int64_t* k, size_t n, hisa_ct* outs);
 /* the same rotation amount on n ciphertexts of one level, batched launches; outs[n] */
 int hisa_rot_left_batch(hisa_ctx* ctx, const hisa_ct* in, size_t n, int64_t k, hisa_ct* outs);
+/* batched forms (one level per batch; results bit-identical to the per-ciphertext calls):
+ * outs[i] = a[i] * b[i] relinearised (hisa_mul), and outs[i] = rescale(in[i]) */
+int hisa_mul_batch(hisa_ctx* ctx, const hisa_ct* a, const hisa_ct* b, size_t n, hisa_ct* outs);
+int hisa_rescale_batch(hisa_ctx* ctx, const hisa_ct* in, size_t n, hisa_ct* outs);
 /* rotate-and-sum step ("reduction ... in log rotations"; A27): outs[i] = in[i] +
  * rotLeft(in[i], k) for n ciphertexts of one level, batched under one key, the addition fused into
  * the final permutation kernel.  Bit-identical to hisa_add(in, hisa_rot_left(in, k)). */

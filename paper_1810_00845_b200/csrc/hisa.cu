@@ -1133,6 +1133,19 @@ static int ks_moddown(hisa_ctx* c, int nz, int level, uint64_t* const* acc, uint
     return HISA_OK;
 }
 
+// ciphertexts per batched key-switch launch: up to MAXB, but the scratch of a batch (dtil, T1,
+// acc, ModDown temporaries: (l+1)(l+2) + 3(l+1) + 2(l+2) + 2 limbs per ciphertext, ~390 MiB at
+// N = 2^16, L = 24) is kept under ~4 GiB so large contexts with many resident keys batch less
+static int ks_chunk(const hisa_ctx* c, int level) {
+    const size_t l1 = (size_t)level + 1, l2 = l1 + 1;
+    const size_t per = (size_t)c->N * 8 * (l1 + l1 * l2 + 2 * l2 + 2 + 2 * l1 + 2 * l1);
+    const size_t budget = (size_t)4 << 30;
+    size_t n = budget / per;
+    if (n < 1) n = 1;
+    if (n > (size_t)MAXB) n = MAXB;
+    return (int)n;
+}
+
 // key switch of nz digits under ONE key: ModUp pass 1 -> fused pass 2 + key inner product (K4,
 // D never stored in NTT form) -> ModDown
 static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const KsBatch& kb) {
@@ -1205,6 +1218,58 @@ extern "C" int hisa_mul(hisa_ctx* c, hisa_ct a, hisa_ct b, hisa_ct* out) {
     oa->ptr = ot->ptr; oa->level = ot->level; oa->npolys = ot->npolys; oa->scale = ot->scale;
     ot->ptr = nullptr;
     hisa_free(c, t);
+    return HISA_OK;
+}
+
+// tensor + relinearisation of n pairs (one level), batched launches: the ct x ct product of the
+// activation square over all channels of a layer
+extern "C" int hisa_mul_batch(hisa_ctx* c, const hisa_ct* a, const hisa_ct* b, size_t n, hisa_ct* outs) {
+    CHECK_CTX(c);
+    if ((!a || !b || !outs) && n) return fail(HISA_E_PARAMS, "null argument");
+    if (n && !c->d_rlk) return fail(HISA_E_NO_KEY, "relinearisation key not generated");
+    std::vector<Obj*> oa(n), ob(n);
+    for (size_t i = 0; i < n; i++) {
+        oa[i] = get_obj(c, a[i], OBJ_CT);
+        ob[i] = get_obj(c, b[i], OBJ_CT);
+        if (!oa[i] || !ob[i]) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle at %zu", i);
+        if (oa[i]->npolys != 2 || ob[i]->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly operand");
+        if (oa[i]->level != ob[i]->level || oa[i]->level != oa[0]->level)
+            return fail(HISA_E_LEVEL_MISMATCH, "levels differ at %zu", i);
+    }
+    if (n == 0) return HISA_OK;
+    const int level = oa[0]->level, l1 = level + 1;
+    const long long N = (long long)c->N;
+    const size_t chunk = (size_t)ks_chunk(c, level);
+    for (size_t i0 = 0; i0 < n; i0 += chunk) {
+        const int nz = (int)std::min(chunk, n - i0);
+        uint64_t* t3 = dalloc_t<uint64_t>(c, (size_t)3 * l1 * N * nz);
+        if (!t3) return fail(HISA_E_OOM, "mul batch");
+        ElemJob ej = ejob(c, 2, level);
+        bool square = true;
+        for (int z = 0; z < nz; z++) {
+            ej.a[z] = oa[i0 + z]->ptr;
+            ej.b[z] = ob[i0 + z]->ptr;
+            ej.out[z] = t3 + (size_t)3 * l1 * N * z;
+            square = square && (a[i0 + z] == b[i0 + z]);
+        }
+        KL("elementwise", launch_elem(square ? EL_SQUARE_TENSOR : EL_TENSOR, ej, c->d_mods, nz, c->stream));
+        KsBatch kb;
+        memset(&kb, 0, sizeof kb);
+        uint64_t* res[MAXB];
+        for (int z = 0; z < nz; z++) {
+            res[z] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+            if (!res[z]) return fail(HISA_E_OOM, "mul batch");
+            kb.d[z] = ej.out[z] + 2 * l1 * N;
+            kb.out[z] = res[z];
+            kb.add[z] = ej.out[z];
+        }
+        kb.add_polys = 2;
+        kb.add_a = (long long)l1 * N;
+        RET(keyswitch(c, nz, level, c->d_rlk, kb));
+        dfree(c, t3);
+        for (int z = 0; z < nz; z++)
+            outs[i0 + z] = new_handle(c, OBJ_CT, res[z], level, 2, oa[i0 + z]->scale * ob[i0 + z]->scale);
+    }
     return HISA_OK;
 }
 
@@ -1371,8 +1436,9 @@ extern "C" int hisa_rot_left_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int
         return HISA_OK;
     }
     if (!c->rot_keys.count(kk)) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk);
-    for (size_t i0 = 0; i0 < n; i0 += MAXB) {
-        const int nz = (int)std::min((size_t)MAXB, n - i0);
+    const size_t chunk = (size_t)ks_chunk(c, objs[0]->level);
+    for (size_t i0 = 0; i0 < n; i0 += chunk) {
+        const int nz = (int)std::min(chunk, n - i0);
         uint64_t* res[MAXB];
         RET(rotate_batch(c, objs.data() + i0, nz, kk, res));
         for (int z = 0; z < nz; z++)
@@ -1399,8 +1465,9 @@ extern "C" int hisa_rot_add_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int6
         return HISA_OK;
     }
     if (!c->rot_keys.count(kk)) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk);
-    for (size_t i0 = 0; i0 < n; i0 += MAXB) {
-        const int nz = (int)std::min((size_t)MAXB, n - i0);
+    const size_t chunk = (size_t)ks_chunk(c, objs[0]->level);
+    for (size_t i0 = 0; i0 < n; i0 += chunk) {
+        const int nz = (int)std::min(chunk, n - i0);
         uint64_t* res[MAXB];
         RET(rotate_batch(c, objs.data() + i0, nz, kk, res, true));
         for (int z = 0; z < nz; z++)
@@ -1490,45 +1557,76 @@ extern "C" int hisa_rot_left_hoisted(hisa_ctx* c, hisa_ct h, const int64_t* k, s
 // ============================================================================================
 // rescale / divScalar (a8), modulus switch
 // ============================================================================================
-static int rescale_ptr(hisa_ctx* c, const Obj* o, uint64_t** res) {
-    const int l = o->level, l1 = l + 1, P = o->npolys;
+// rescale of nz ciphertexts of one level and poly count (batched launches)
+static int rescale_batch_ptr(hisa_ctx* c, const Obj* const* os, int nz, uint64_t** res) {
+    const int l = os[0]->level, l1 = l + 1, P = os[0]->npolys;
     const long long N = (long long)c->N;
-    uint64_t* out = dalloc_t<uint64_t>(c, (size_t)P * l * N);
-    uint64_t* tmp = dalloc_t<uint64_t>(c, (size_t)P * N + (size_t)P * l * N);
-    if (!out || !tmp) return fail(HISA_E_OOM, "rescale");
-    uint64_t* top = tmp;
-    uint64_t* r1 = tmp + (size_t)P * N;
+    const size_t per_tmp = (size_t)P * N + (size_t)P * l * N;
+    uint64_t* tmp = dalloc_t<uint64_t>(c, per_tmp * nz);
+    if (!tmp) return fail(HISA_E_OOM, "rescale");
+    for (int z = 0; z < nz; z++) {
+        res[z] = dalloc_t<uint64_t>(c, (size_t)P * l * N);
+        if (!res[z]) return fail(HISA_E_OOM, "rescale");
+    }
     Tables tb = c->tables();
     {   // INTT of the top limb of every poly
         PassJob j = job0();
-        j.src[0] = o->ptr + (long long)l * N; j.dst[0] = top;
+        for (int z = 0; z < nz; z++) { j.src[z] = os[z]->ptr + (long long)l * N; j.dst[z] = tmp + per_tmp * z; }
         j.nb = 1; j.src_a = (long long)l1 * N; j.dst_a = N;
         j.mod_map[0] = (uint8_t)l;
-        KL("rescale_intt_rows", launch_inv_passA(j, tb, P, 1, c->stream));
-        j.src[0] = top; j.src_a = N;
-        KL("rescale_intt_cols", launch_inv_passB(j, tb, P, 1, c->stream));
+        KL("rescale_intt_rows", launch_inv_passA(j, tb, P, nz, c->stream));
+        for (int z = 0; z < nz; z++) j.src[z] = tmp + per_tmp * z;
+        j.src_a = N;
+        KL("rescale_intt_cols", launch_inv_passB(j, tb, P, nz, c->stream));
     }
     {   // lift q_l -> q_i (i < l), forward pass 1
         PassJob j = job0();
-        j.src[0] = top; j.dst[0] = r1;
+        for (int z = 0; z < nz; z++) { j.src[z] = tmp + per_tmp * z; j.dst[z] = tmp + per_tmp * z + (size_t)P * N; }
         j.nb = l; j.src_a = N; j.src_b = 0; j.dst_a = (long long)l * N; j.dst_b = N;
         ident_map(j.mod_map, l);
         for (int a = 0; a < P; a++) j.smod_map[a] = (uint8_t)l;
-        KL("rescale_lift_cols", launch_fwd_pass1(j, tb, P * l, 1, true, c->stream));
+        KL("rescale_lift_cols", launch_fwd_pass1(j, tb, P * l, nz, true, c->stream));
     }
     {   // pass 2 + combine: out_i = (u_i - NTT_i(y)) q_l^-1
         PassJob j = job0();
-        j.src[0] = r1; j.dst[0] = out; j.aux[0] = o->ptr;
+        for (int z = 0; z < nz; z++) {
+            j.src[z] = tmp + per_tmp * z + (size_t)P * N;
+            j.dst[z] = res[z];
+            j.aux[z] = os[z]->ptr;
+        }
         j.nb = l;
         j.src_a = (long long)l * N; j.src_b = N;
         j.dst_a = (long long)l * N; j.dst_b = N;
         j.aux_a = (long long)l1 * N; j.aux_b = N;
         ident_map(j.mod_map, l);
         Tables tc = c->tables(c->d_qlinv + (size_t)l * (c->L + 1));
-        KL("rescale_combine_rows", launch_fwd_pass2(j, tc, P * l, 1, true, c->stream));
+        KL("rescale_combine_rows", launch_fwd_pass2(j, tc, P * l, nz, true, c->stream));
     }
     dfree(c, tmp);
-    *res = out;
+    return HISA_OK;
+}
+static int rescale_ptr(hisa_ctx* c, const Obj* o, uint64_t** res) { return rescale_batch_ptr(c, &o, 1, res); }
+
+extern "C" int hisa_rescale_batch(hisa_ctx* c, const hisa_ct* in, size_t n, hisa_ct* outs) {
+    CHECK_CTX(c);
+    if ((!in || !outs) && n) return fail(HISA_E_PARAMS, "null argument");
+    std::vector<Obj*> objs(n);
+    for (size_t i = 0; i < n; i++) {
+        objs[i] = get_obj(c, in[i], OBJ_CT);
+        if (!objs[i]) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle at %zu", i);
+        if (objs[i]->level != objs[0]->level || objs[i]->npolys != objs[0]->npolys)
+            return fail(HISA_E_LEVEL_MISMATCH, "batch shapes differ");
+    }
+    if (n && objs[0]->level == 0) return fail(HISA_E_MODULUS_EXHAUSTED, "rescale at level 0");
+    for (size_t i0 = 0; i0 < n; i0 += MAXB) {
+        const int nz = (int)std::min((size_t)MAXB, n - i0);
+        uint64_t* res[MAXB];
+        RET(rescale_batch_ptr(c, objs.data() + i0, nz, res));
+        for (int z = 0; z < nz; z++) {
+            const Obj* o = objs[i0 + z];
+            outs[i0 + z] = new_handle(c, OBJ_CT, res[z], o->level - 1, o->npolys, o->scale / (double)c->mod[o->level]);
+        }
+    }
     return HISA_OK;
 }
 
@@ -1586,13 +1684,17 @@ extern "C" int hisa_bootstrap(hisa_ctx* c, hisa_ct h) {
 struct ConvJob {
     int T, OC, l1, log_n;
     long long poly_stride;
-    int red_every;          // partial Barrett every this many terms (128-bit headroom: 2^127 / q^2)
+    int red_every;          // integer path: partial Barrett every this many terms (2^127 / q^2)
+    double f64_max_q;       // limbs with q below this accumulate on the FP64 pipe
 };
 // K8: out[o][x] = sum_t W[limb][o][t] in[t][x] mod q_limb -- a modular GEMM (OC x T) x (T x N)
 // per limb and poly.  CTA = 256 threads x 2 words (16-byte loads); OT outputs per pass held in
-// 128-bit register accumulators; the T input pointers and a TT-wide weight tile live in shared
-// memory (no dependent global loads in the t loop); inputs are re-read from L2 once per OT
-// outputs.  weights: [limb][OC][T] residues; in_ptrs: device array of T pointers; out_ptrs: OC.
+// register accumulators; the T input pointers and a TT-wide weight tile live in shared memory
+// (no dependent global loads in the t loop); inputs are re-read from L2 once per OT outputs.
+//   q >= 2^50: 128-bit integer accumulation (mac128, ~13 IMAD per MAC; IMAD-pipe bound).
+//   q <  2^50: exact FP64 (ntt_f64.cuh): t = mulred(x, w) (|t| < q) accumulated in a double,
+//              re-centred (redd) every floor(2^53 / q) - 1 terms: 7 FP64-pipe ops per MAC.
+// weights: [limb][OC][T] residues; in_ptrs: device array of T pointers; out_ptrs: OC.
 constexpr int CONV_OT = 8, CONV_TT = 256;
 __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restrict__ in_ptrs,
                                                   uint64_t* const* __restrict__ out_ptrs,
@@ -1605,24 +1707,54 @@ __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restr
     const int poly = blockIdx.z;
     const int limb = blockIdx.y;
     const Mod md = mods[limb];
+    const bool fp = (double)md.q < job.f64_max_q;
+    const double qd = (double)md.q, qinv = 1.0 / qd;
+    const int red_f = fp ? (int)fmin(8192.0, floor(9007199254740992.0 / qd) - 1.0) : 0;
     const long long off = (long long)poly * job.poly_stride + (long long)limb * N;
     const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
     for (int t = threadIdx.x; t < job.T; t += blockDim.x) ptrs[t] = in_ptrs[t] + off;
     const uint64_t* wl = w + (long long)limb * job.OC * job.T;
     for (int o0 = 0; o0 < job.OC; o0 += CONV_OT) {
         U128 acc[CONV_OT][2];
+        double facc[CONV_OT][2];
 #pragma unroll
-        for (int k = 0; k < CONV_OT; k++) { acc[k][0] = U128{0, 0}; acc[k][1] = U128{0, 0}; }
+        for (int k = 0; k < CONV_OT; k++) {
+            acc[k][0] = U128{0, 0}; acc[k][1] = U128{0, 0};
+            facc[k][0] = 0.0; facc[k][1] = 0.0;
+        }
         int since = 0;   // terms since the last partial reduction (carried across weight tiles)
         for (int t0 = 0; t0 < job.T; t0 += CONV_TT) {
             const int tn = min(CONV_TT, job.T - t0);
             __syncthreads();
             for (int i = threadIdx.x; i < CONV_OT * CONV_TT; i += blockDim.x) {
                 const int k = i / CONV_TT, tt = i % CONV_TT;
-                wsm[i] = (o0 + k < job.OC && tt < tn) ? wl[(long long)(o0 + k) * job.T + t0 + tt] : 0;
+                const uint64_t wv = (o0 + k < job.OC && tt < tn) ? wl[(long long)(o0 + k) * job.T + t0 + tt] : 0;
+                if (fp) reinterpret_cast<double*>(wsm)[i] = u2d(wv);
+                else wsm[i] = wv;
             }
             __syncthreads();
-            if (x < N) {
+            if (x >= N) continue;
+            if (fp) {
+                const double* wd = reinterpret_cast<const double*>(wsm);
+                for (int tt = 0; tt < tn; tt++) {
+                    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(ptrs[t0 + tt] + x));
+                    const double a0 = u2d(v.x), a1 = u2d(v.y);
+#pragma unroll
+                    for (int k = 0; k < CONV_OT; k++) {
+                        const double wk = wd[k * CONV_TT + tt];
+                        facc[k][0] = __dadd_rn(facc[k][0], mulred(a0, wk, qd, qinv));
+                        facc[k][1] = __dadd_rn(facc[k][1], mulred(a1, wk, qd, qinv));
+                    }
+                    if (++since == red_f) {
+                        since = 0;
+#pragma unroll
+                        for (int k = 0; k < CONV_OT; k++) {
+                            facc[k][0] = redd(facc[k][0], qd, qinv);
+                            facc[k][1] = redd(facc[k][1], qd, qinv);
+                        }
+                    }
+                }
+            } else {
                 for (int tt = 0; tt < tn; tt++) {
                     const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(ptrs[t0 + tt] + x));
 #pragma unroll
@@ -1647,10 +1779,16 @@ __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restr
         if (x < N) {
 #pragma unroll
             for (int k = 0; k < CONV_OT; k++)
-                if (o0 + k < job.OC)
-                    *reinterpret_cast<ulonglong2*>(out_ptrs[o0 + k] + off + x) =
-                        make_ulonglong2(barrett128(acc[k][0].lo, acc[k][0].hi, md),
-                                        barrett128(acc[k][1].lo, acc[k][1].hi, md));
+                if (o0 + k < job.OC) {
+                    ulonglong2 r;
+                    if (fp) {
+                        r = make_ulonglong2(d_canon(facc[k][0], qd, qinv), d_canon(facc[k][1], qd, qinv));
+                    } else {
+                        r = make_ulonglong2(barrett128(acc[k][0].lo, acc[k][0].hi, md),
+                                            barrett128(acc[k][1].lo, acc[k][1].hi, md));
+                    }
+                    *reinterpret_cast<ulonglong2*>(out_ptrs[o0 + k] + off + x) = r;
+                }
         }
     }
 }
@@ -1698,7 +1836,8 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
     uint64_t qmax = 0;
     for (int i = 0; i < l1; i++) qmax = std::max(qmax, c->mod[i]);
     const double terms = std::ldexp(1.0, 127) / ((double)qmax * (double)qmax);   // 128-bit headroom
-    ConvJob cj{(int)T, (int)OC, l1, c->log_n, (long long)l1 * N, (int)std::min(1024.0, std::floor(terms) - 1)};
+    ConvJob cj{(int)T, (int)OC, l1, c->log_n, (long long)l1 * N, (int)std::min(1024.0, std::floor(terms) - 1),
+               c->f64_max_q};
     dim3 grid((unsigned)((N / 2 + 255) / 256), l1, 2);
     const size_t smem = (size_t)T * sizeof(void*) + (size_t)CONV_OT * CONV_TT * 8;
     if (smem > 200 * 1024) return fail(HISA_E_PARAMS, "conv accumulation: T = %zu inputs too many", T);

@@ -188,6 +188,12 @@ class Symbolic:
     def copy(self, a):
         return self._new(*self.cts[a])
 
+    def mul_batch(self, a, b):
+        return [self.mul(x, y) for x, y in zip(a, b)]
+
+    def rescale_batch(self, hs):
+        return [self.rescale(h) for h in hs]
+
     def rot_add_batch(self, hs, k):
         kk = k % self.slots
         if kk:
@@ -306,12 +312,9 @@ class EncryptedNet:
             v = np.zeros(self.slots)
             v[idx] = 1.0
             return v
-        out = []
-        for ct in cts:
-            pt = self._plaintext(("mask", li), vals, self._level(ct))
-            m = self.b.mul_plain(ct, pt)
-            out.append(self.b.rescale(m))
-            self.b.free(m)
+        ms = [self.b.mul_plain(ct, self._plaintext(("mask", li), vals, self._level(ct))) for ct in cts]
+        out = self.b.rescale_batch(ms)
+        self._free_all(ms)
         return out, replace(lay, clean=True)
 
     def conv(self, cts, lay, layer, w, beta, li):
@@ -340,15 +343,9 @@ class EncryptedNet:
         self._free_all(temps)
         if masked:
             self._free_all(cts)
-        res = []
-        for h in outs:
-            r = self.b.rescale(h)
-            self.b.free(h)
-            if beta:
-                r2 = self.b.add_scalar(r, beta)
-                self.b.free(r)
-                r = r2
-            res.append(r)
+        res = self.b.rescale_batch(outs)
+        self._free_all(outs)
+        res = self._bias(res, beta)
         nl = Layout("hw", oc_n, (lay.H + 2 * p - k) // st + 1, (lay.W + 2 * p - k) // st + 1,
                     lay.hS * st, lay.wS * st, 0, False)
         return res, nl
@@ -364,16 +361,13 @@ class EncryptedNet:
 
     def act(self, cts, lay, square_only=False):
         """(A25) x'^2 + gamma: tensor + relinearize + rescale (+ addScalar): one level."""
-        out = []
-        for ct in cts:
-            sq = self.b.mul(ct, ct)
-            r = self.b.rescale(sq)
-            self.b.free(sq)
-            if not square_only and self.gamma:
-                r2 = self.b.add_scalar(r, self.gamma)
-                self.b.free(r)
-                r = r2
-            out.append(r)
+        sq = self.b.mul_batch(list(cts), list(cts))       # tensor + relin, batched
+        out = self.b.rescale_batch(sq)
+        self._free_all(sq)
+        if not square_only and self.gamma:
+            out2 = [self.b.add_scalar(r, self.gamma) for r in out]
+            self._free_all(out)
+            out = out2
         return out, replace(lay, clean=False)
 
     def avgpool(self, cts, lay):
@@ -481,7 +475,7 @@ class EncryptedNet:
         sums = self._mulplain_sums(reps, lay.C, n_groups, "fcrep", li, vals)
         if temp:
             self._free_all(reps)
-        res = [self.b.rescale(h) for h in sums]
+        res = self.b.rescale_batch(sums)
         self._free_all(sums)
         res = self._rotate_sum(res, [1 << t for t in range(int(math.log2(Bk)))])
         return self._bias(res, beta), Layout("rep", n_groups, H=R, hS=Bk, count=n_out)
@@ -501,7 +495,7 @@ class EncryptedNet:
                     v[r * Bk] = w[k, j]
             return v
         sums = self._mulplain_sums(cts, lay.C, n_out, "fcfromrep", li, vals)
-        res = [self.b.rescale(h) for h in sums]
+        res = self.b.rescale_batch(sums)
         self._free_all(sums)
         res = self._rotate_sum(res, [Bk << t for t in range(int(math.log2(R)))])
         return self._bias(res, beta), Layout("slot0", n_out)
@@ -517,7 +511,7 @@ class EncryptedNet:
         if lay.kind == "slot0":          # next FC reads slot 0: scalar MACs, fused
             own = self.owned(lay.C)
             outs = self._accumulate(list(cts), w[:, own.start:own.stop], n_out)
-            res = [self.b.rescale(h) for h in outs]
+            res = self.b.rescale_batch(outs)
             self._free_all(outs)
             return self._bias(res, beta), Layout("slot0", n_out)
         idx = lay.slots_of_valid()
@@ -529,7 +523,7 @@ class EncryptedNet:
             v[idx] = w[jo, ci * hw:(ci + 1) * hw]
             return v
         sums = self._mulplain_sums(cts, lay.C, n_out, "fc", li, vals)
-        res = [self.b.rescale(h) for h in sums]
+        res = self.b.rescale_batch(sums)
         self._free_all(sums)
         res = self._rotate_sum(res, [1 << t for t in range(steps)])   # slot 0 <- dot product
         return self._bias(res, beta), Layout("slot0", n_out)

@@ -87,6 +87,8 @@ _SIGS = {
     "hisa_conv_accumulate": [_vp, _u64p, _csz, _dp, _csz, _cd, _u64p],
     "hisa_conv_accumulate_dev": [_vp, _u64p, _csz, _dp, _csz, _cd, _vp],
     "hisa_rot_add_batch": [_vp, _u64p, _csz, _ci64, _u64p],
+    "hisa_mul_batch": [_vp, _u64p, _u64p, _csz, _u64p],
+    "hisa_rescale_batch": [_vp, _u64p, _csz, _u64p],
     "hisa_mul_plain_accumulate": [_vp, _u64p, _csz, _u64p, _csz, _u64p],
     "hisa_ct_adopt_sum": [_vp, _vp, _ci, _ci, _cd, _u64p],
     "hisa_ntt": [_vp, _cu64, _ci],
@@ -340,6 +342,20 @@ def hisa_conv_accumulate(ctx, cts, W, pt_scale: float = 0.0) -> list[int]:
     _chk(load().hisa_conv_accumulate(ctx, _ptr(ins, _u64p), ins.size, _ptr(w, _dp), oc, float(pt_scale),
                                      _ptr(outs, _u64p)))
     return [int(x) for x in outs]
+
+
+def hisa_mul_batch(ctx, a, b) -> list[int]:
+    x, y = _u64(list(a)), _u64(list(b))
+    outs = np.zeros(x.size, dtype=np.uint64)
+    _chk(load().hisa_mul_batch(ctx, _ptr(x, _u64p), _ptr(y, _u64p), x.size, _ptr(outs, _u64p)))
+    return [int(v) for v in outs]
+
+
+def hisa_rescale_batch(ctx, cts) -> list[int]:
+    x = _u64(list(cts))
+    outs = np.zeros(x.size, dtype=np.uint64)
+    _chk(load().hisa_rescale_batch(ctx, _ptr(x, _u64p), x.size, _ptr(outs, _u64p)))
+    return [int(v) for v in outs]
 
 
 def hisa_rot_add_batch(ctx, cts, k: int) -> list[int]:

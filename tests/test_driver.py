@@ -24,7 +24,7 @@ def _run_pair(net, W, img, oracle_layers=None):
     otrace = []
     ocs_out, olay_out = on.forward(ocs, olay, trace=otrace, stop_after=oracle_layers)
 
-    g = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, arena_bytes=24 << 30)
+    g = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, arena_bytes=96 << 30)
     assert g.moduli == on.o.moduli
     plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli)
     assert plan["rotations"] == on.amounts          # the compiler's key selection

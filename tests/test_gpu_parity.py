@@ -374,3 +374,16 @@ def test_fused_rot_add_and_mulplain_accumulate(pair):
             term = o.mul_plain(os_[c], pts[j * C + c][1])
             acc = term if acc is None else o.add(acc, term)
         pair.same(outs[j], acc)
+
+
+def test_batched_mul_and_rescale(pair):
+    """hisa_mul_batch / hisa_rescale_batch == the per-ciphertext hisa_mul / hisa_rescale."""
+    g, o = pair.g, pair.o
+    hs, os_ = zip(*[pair.ct(100 + i) for i in range(3)])
+    outs = g.mul_batch([hs[0], hs[1], hs[2]], [hs[0], hs[2], hs[2]])
+    pair.same(outs[0], o.mul(os_[0], os_[0]))
+    pair.same(outs[1], o.mul(os_[1], os_[2]))
+    pair.same(outs[2], o.mul(os_[2], os_[2]))
+    if o.L >= 2:
+        for h, oc in zip(g.rescale_batch(list(hs)), os_):
+            pair.same(h, o.rescale(oc))
