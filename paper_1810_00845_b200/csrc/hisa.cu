@@ -1685,17 +1685,18 @@ struct ConvJob {
     int T, OC, l1, log_n;
     long long poly_stride;
     int red_every;          // integer path: partial Barrett every this many terms (2^127 / q^2)
-    double f64_max_q;       // limbs with q below this accumulate on the FP64 pipe
+    uint8_t limb_map[MAXL]; // grid.y -> limb (one launch per engine class)
 };
 // K8: out[o][x] = sum_t W[limb][o][t] in[t][x] mod q_limb -- a modular GEMM (OC x T) x (T x N)
 // per limb and poly.  CTA = 256 threads x 2 words (16-byte loads); OT outputs per pass held in
-// register accumulators; the T input pointers and a TT-wide weight tile live in shared memory
-// (no dependent global loads in the t loop); inputs are re-read from L2 once per OT outputs.
-//   q >= 2^50: 128-bit integer accumulation (mac128, ~13 IMAD per MAC; IMAD-pipe bound).
-//   q <  2^50: exact FP64 (ntt_f64.cuh): t = mulred(x, w) (|t| < q) accumulated in a double,
-//              re-centred (redd) every floor(2^53 / q) - 1 terms: 7 FP64-pipe ops per MAC.
+// register accumulators; the T input pointers and a TT-wide weight tile live in shared memory;
+// the t loop keeps U input loads in flight (inputs are re-read from L2/HBM once per OT outputs).
+//   FP = false (q >= 2^50): 128-bit integer accumulation (mac128; IMAD-pipe bound).
+//   FP = true  (q <  2^50): exact FP64 (ntt_f64.cuh): t = mulred(x, w) (|t| < q) accumulated in a
+//              double, re-centred (redd) every floor(2^53 / q) - 1 terms: 7 FP64-pipe ops per MAC.
 // weights: [limb][OC][T] residues; in_ptrs: device array of T pointers; out_ptrs: OC.
-constexpr int CONV_OT = 8, CONV_TT = 256;
+constexpr int CONV_OT = 8, CONV_TT = 256, CONV_U = 4;
+template <bool FP>
 __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restrict__ in_ptrs,
                                                   uint64_t* const* __restrict__ out_ptrs,
                                                   const uint64_t* __restrict__ w, ConvJob job,
@@ -1705,22 +1706,21 @@ __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restr
     uint64_t* wsm = csm + job.T;                                               // [OT][TT]
     const long long N = 1ll << job.log_n;
     const int poly = blockIdx.z;
-    const int limb = blockIdx.y;
+    const int limb = job.limb_map[blockIdx.y];
     const Mod md = mods[limb];
-    const bool fp = (double)md.q < job.f64_max_q;
     const double qd = (double)md.q, qinv = 1.0 / qd;
-    const int red_f = fp ? (int)fmin(8192.0, floor(9007199254740992.0 / qd) - 1.0) : 0;
+    const int red = FP ? (int)fmin(8192.0, floor(9007199254740992.0 / qd) - 1.0) : job.red_every;
     const long long off = (long long)poly * job.poly_stride + (long long)limb * N;
     const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
     for (int t = threadIdx.x; t < job.T; t += blockDim.x) ptrs[t] = in_ptrs[t] + off;
     const uint64_t* wl = w + (long long)limb * job.OC * job.T;
     for (int o0 = 0; o0 < job.OC; o0 += CONV_OT) {
-        U128 acc[CONV_OT][2];
-        double facc[CONV_OT][2];
+        U128 acc[FP ? 1 : CONV_OT][2];
+        double facc[FP ? CONV_OT : 1][2];
 #pragma unroll
         for (int k = 0; k < CONV_OT; k++) {
-            acc[k][0] = U128{0, 0}; acc[k][1] = U128{0, 0};
-            facc[k][0] = 0.0; facc[k][1] = 0.0;
+            if constexpr (FP) { facc[k][0] = 0.0; facc[k][1] = 0.0; }
+            else { acc[k][0] = U128{0, 0}; acc[k][1] = U128{0, 0}; }
         }
         int since = 0;   // terms since the last partial reduction (carried across weight tiles)
         for (int t0 = 0; t0 < job.T; t0 += CONV_TT) {
@@ -1729,48 +1729,50 @@ __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restr
             for (int i = threadIdx.x; i < CONV_OT * CONV_TT; i += blockDim.x) {
                 const int k = i / CONV_TT, tt = i % CONV_TT;
                 const uint64_t wv = (o0 + k < job.OC && tt < tn) ? wl[(long long)(o0 + k) * job.T + t0 + tt] : 0;
-                if (fp) reinterpret_cast<double*>(wsm)[i] = u2d(wv);
+                if constexpr (FP) reinterpret_cast<double*>(wsm)[i] = u2d(wv);
                 else wsm[i] = wv;
             }
             __syncthreads();
             if (x >= N) continue;
-            if (fp) {
-                const double* wd = reinterpret_cast<const double*>(wsm);
-                for (int tt = 0; tt < tn; tt++) {
-                    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(ptrs[t0 + tt] + x));
-                    const double a0 = u2d(v.x), a1 = u2d(v.y);
+            for (int tb = 0; tb < tn; tb += CONV_U) {
+                ulonglong2 v[CONV_U];
 #pragma unroll
-                    for (int k = 0; k < CONV_OT; k++) {
-                        const double wk = wd[k * CONV_TT + tt];
-                        facc[k][0] = __dadd_rn(facc[k][0], mulred(a0, wk, qd, qinv));
-                        facc[k][1] = __dadd_rn(facc[k][1], mulred(a1, wk, qd, qinv));
-                    }
-                    if (++since == red_f) {
-                        since = 0;
+                for (int u = 0; u < CONV_U; u++)   // U loads in flight before the MACs
+                    v[u] = tb + u < tn ? __ldg(reinterpret_cast<const ulonglong2*>(ptrs[t0 + tb + u] + x))
+                                       : make_ulonglong2(0, 0);
+#pragma unroll
+                for (int u = 0; u < CONV_U; u++) {
+                    const int tt = tb + u;
+                    if (tt >= tn) continue;
+                    if constexpr (FP) {
+                        const double* wd = reinterpret_cast<const double*>(wsm);
+                        const double a0 = u2d(v[u].x), a1 = u2d(v[u].y);
 #pragma unroll
                         for (int k = 0; k < CONV_OT; k++) {
-                            facc[k][0] = redd(facc[k][0], qd, qinv);
-                            facc[k][1] = redd(facc[k][1], qd, qinv);
+                            const double wk = wd[k * CONV_TT + tt];
+                            facc[k][0] = __dadd_rn(facc[k][0], mulred(a0, wk, qd, qinv));
+                            facc[k][1] = __dadd_rn(facc[k][1], mulred(a1, wk, qd, qinv));
+                        }
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < CONV_OT; k++) {
+                            const uint64_t wk = wsm[k * CONV_TT + tt];
+                            mac128(acc[k][0], v[u].x, wk);
+                            mac128(acc[k][1], v[u].y, wk);
                         }
                     }
-                }
-            } else {
-                for (int tt = 0; tt < tn; tt++) {
-                    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(ptrs[t0 + tt] + x));
-#pragma unroll
-                    for (int k = 0; k < CONV_OT; k++) {
-                        const uint64_t wk = wsm[k * CONV_TT + tt];
-                        mac128(acc[k][0], v.x, wk);
-                        mac128(acc[k][1], v.y, wk);
-                    }
-                    if (++since == job.red_every) {   // keep the 128-bit sums bounded
+                    if (++since == red) {   // keep the accumulators bounded
                         since = 0;
 #pragma unroll
                         for (int k = 0; k < CONV_OT; k++)
 #pragma unroll
                             for (int h = 0; h < 2; h++) {
-                                acc[k][h].lo = barrett128(acc[k][h].lo, acc[k][h].hi, md);
-                                acc[k][h].hi = 0;
+                                if constexpr (FP) {
+                                    facc[k][h] = redd(facc[k][h], qd, qinv);
+                                } else {
+                                    acc[k][h].lo = barrett128(acc[k][h].lo, acc[k][h].hi, md);
+                                    acc[k][h].hi = 0;
+                                }
                             }
                     }
                 }
@@ -1781,12 +1783,9 @@ __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restr
             for (int k = 0; k < CONV_OT; k++)
                 if (o0 + k < job.OC) {
                     ulonglong2 r;
-                    if (fp) {
-                        r = make_ulonglong2(d_canon(facc[k][0], qd, qinv), d_canon(facc[k][1], qd, qinv));
-                    } else {
-                        r = make_ulonglong2(barrett128(acc[k][0].lo, acc[k][0].hi, md),
-                                            barrett128(acc[k][1].lo, acc[k][1].hi, md));
-                    }
+                    if constexpr (FP) r = make_ulonglong2(d_canon(facc[k][0], qd, qinv), d_canon(facc[k][1], qd, qinv));
+                    else r = make_ulonglong2(barrett128(acc[k][0].lo, acc[k][0].hi, md),
+                                             barrett128(acc[k][1].lo, acc[k][1].hi, md));
                     *reinterpret_cast<ulonglong2*>(out_ptrs[o0 + k] + off + x) = r;
                 }
         }
@@ -1836,15 +1835,30 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
     uint64_t qmax = 0;
     for (int i = 0; i < l1; i++) qmax = std::max(qmax, c->mod[i]);
     const double terms = std::ldexp(1.0, 127) / ((double)qmax * (double)qmax);   // 128-bit headroom
-    ConvJob cj{(int)T, (int)OC, l1, c->log_n, (long long)l1 * N, (int)std::min(1024.0, std::floor(terms) - 1),
-               c->f64_max_q};
-    dim3 grid((unsigned)((N / 2 + 255) / 256), l1, 2);
+    ConvJob cj;
+    memset(&cj, 0, sizeof cj);
+    cj.T = (int)T; cj.OC = (int)OC; cj.l1 = l1; cj.log_n = c->log_n; cj.poly_stride = (long long)l1 * N;
+    cj.red_every = (int)std::min(1024.0, std::floor(terms) - 1);
+    dim3 grid((unsigned)((N / 2 + 255) / 256), 1, 2);
     const size_t smem = (size_t)T * sizeof(void*) + (size_t)CONV_OT * CONV_TT * 8;
     if (smem > 200 * 1024) return fail(HISA_E_PARAMS, "conv accumulation: T = %zu inputs too many", T);
-    {
+    for (int fpc = 0; fpc < 2; fpc++) {   // one launch per butterfly-engine class of limbs
+        ConvJob j2 = cj;
+        int n = 0;
+        for (int i = 0; i < l1; i++)
+            if (((double)c->mod[i] < c->f64_max_q) == (fpc == 1)) j2.limb_map[n++] = (uint8_t)i;
+        if (!n) continue;
+        grid.y = n;
         ProfScope ps_(c, "conv_acc");
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k_conv_acc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_conv_acc<<<grid, 256, smem, c->stream>>>(dip, dop, dw, cj, c->d_mods);
+        if (fpc) {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(k_conv_acc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_conv_acc<true><<<grid, 256, smem, c->stream>>>(dip, dop, dw, j2, c->d_mods);
+        } else {
+            if (smem > 48 * 1024)
+                cudaFuncSetAttribute(k_conv_acc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_conv_acc<false><<<grid, 256, smem, c->stream>>>(dip, dop, dw, j2, c->d_mods);
+        }
         CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(c->stream));   // host staging vectors must outlive the copies
