@@ -177,6 +177,12 @@ int hisa_mod_switch(hisa_ctx* ctx, hisa_ct ct, int drop, hisa_ct* out);
  * with the exact centred ModUp / ModDown).  Device scratch: (l+1)(l+2) limbs for the shared
  * ModUp output plus ~(6l+8) limbs per amount in flight (chunks of 8 amounts). */
 int hisa_rot_left_hoisted(hisa_ctx* ctx, hisa_ct ct, const int64_t* k, size_t n, hisa_ct* outs);
+/* hoisted rotations of nct ciphertexts (one level) by the same n amounts: outs[i * n + r] =
+ * rotLeft(in[i], k[r]).  ModUp batched over ciphertexts, each rotation key word streamed once per
+ * group of up to 4 ciphertexts (K7), batched ModDown; bit-identical to hisa_rot_left.  The conv
+ * (all input channels x filter taps) and pooling pattern. */
+int hisa_rot_left_hoisted_batch(hisa_ctx* ctx, const hisa_ct* in, size_t nct, const int64_t* k, size_t n,
+                                hisa_ct* outs);
 /* the same rotation amount on n ciphertexts of one level, batched launches; outs[n] */
 int hisa_rot_left_batch(hisa_ctx* ctx, const hisa_ct* in, size_t n, int64_t k, hisa_ct* outs);
 /* batched forms (one level per batch; results bit-identical to the per-ciphertext calls):

@@ -1393,6 +1393,133 @@ static int rotate_hoisted(hisa_ctx* c, const Obj* o, const uint64_t* ks, int n, 
     return HISA_OK;
 }
 
+// hoisted rotations of nct ciphertexts (one level) by the same n non-zero amounts: batched ModUp
+// (nz ciphertexts per launch), K7 over groups of <= 4 ciphertexts x <= 4 keys (each key word
+// streamed once per group), batched ModDown and permutation.  outs[i * n + r] = rot(in_i, ks[r]).
+static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint64_t* ks, int n, uint64_t** outs) {
+    const int level = os[0]->level, l1 = level + 1, l2 = level + 2, L = c->L;
+    const long long N = (long long)c->N;
+    const size_t per_ct = (size_t)N * ((size_t)l1 + (size_t)l1 * l2);           // dtil, D
+    const size_t per_out = (size_t)N * (2 * l2 + 2 + 2 * l1 + 2 * l1);           // acc, ptmp, md, pre
+    constexpr int RK = 4;                                                         // keys per K7 launch
+    const size_t budget = (size_t)6 << 30;
+    int ct_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)MAXB, budget / ((per_ct + RK * per_out) * 8)));
+    ct_chunk = std::min(ct_chunk, nct);
+    for (int i = 0; i < nct * n; i++) {
+        outs[i] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        if (!outs[i]) return fail(HISA_E_OOM, "rotation output");
+    }
+    uint64_t* scratch = dalloc_t<uint64_t>(c, per_ct * ct_chunk + per_out * (size_t)ct_chunk * RK);
+    if (!scratch) return fail(HISA_E_OOM, "hoisted rotation scratch");
+    for (int c0 = 0; c0 < nct; c0 += ct_chunk) {
+        const int nc = std::min(ct_chunk, nct - c0);
+        uint64_t *dtil[MAXB], *D[MAXB];
+        const uint64_t* d1[MAXB];
+        for (int z = 0; z < nc; z++) {
+            dtil[z] = scratch + per_ct * z;
+            D[z] = dtil[z] + (size_t)l1 * N;
+            d1[z] = os[c0 + z]->ptr + l1 * N;
+        }
+        RET(ks_modup_pass1(c, nc, level, d1, dtil, D));
+        {   // ModUp pass 2 in place: D_{j,r} for r != q_j, fully reduced
+            PassJob j = job0();
+            for (int z = 0; z < nc; z++) { j.src[z] = D[z]; j.dst[z] = D[z]; }
+            j.nb = l2;
+            j.src_a = j.dst_a = (long long)l2 * N;
+            j.src_b = j.dst_b = N;
+            j.skip_diag = 1;
+            for (int ri = 0; ri < l2; ri++) j.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+            Tables tb = c->tables();
+            KL("ks_modup_rows", launch_fwd_pass2(j, tb, l1 * l2, nc, false, c->stream));
+        }
+        uint64_t* outbase = scratch + per_ct * ct_chunk;
+        for (int r0 = 0; r0 < n; r0 += RK) {
+            const int R = std::min(RK, n - r0);
+            // per-output scratch: output (z, r) at index z * R + r
+            auto acc_of = [&](int z, int r) { return outbase + per_out * (size_t)(z * R + r); };
+            for (int g0 = 0; g0 < nc; g0 += MAXCG) {
+                KsHoistMultiJob hj;
+                memset(&hj, 0, sizeof hj);
+                hj.cg = std::min(MAXCG, nc - g0);
+                for (int cg = 0; cg < hj.cg; cg++) {
+                    hj.D[cg] = D[g0 + cg];
+                    hj.diag[cg] = d1[g0 + cg];
+                    for (int r = 0; r < R; r++) hj.acc[cg][r] = acc_of(g0 + cg, r);
+                }
+                for (int r = 0; r < R; r++) hj.key[r] = c->rot_keys[ks[r0 + r]];
+                hj.l1 = l1;
+                hj.L = L;
+                for (int ri = 0; ri < l2; ri++) hj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+                KL("ks_ip_hoisted", launch_ks_ip_hoisted_multi(hj, R, c->d_mods, c->log_n, c->stream));
+            }
+            const int nout = nc * R;
+            for (int o0 = 0; o0 < nout; o0 += MAXB) {
+                const int m = std::min(MAXB, nout - o0);
+                uint64_t *acc[MAXB], *ptmp[MAXB], *md[MAXB];
+                const uint64_t* pres[MAXB];
+                uint64_t gs[MAXB];
+                KsBatch kb;
+                memset(&kb, 0, sizeof kb);
+                for (int q = 0; q < m; q++) {
+                    const int o = o0 + q, z = o / R, r = o % R;
+                    uint64_t* sp = acc_of(z, r);
+                    acc[q] = sp; sp += (size_t)2 * l2 * N;
+                    ptmp[q] = sp; sp += (size_t)2 * N;
+                    md[q] = sp; sp += (size_t)2 * l1 * N;
+                    pres[q] = sp;
+                    kb.out[q] = sp;
+                    kb.add[q] = os[c0 + z]->ptr;
+                    gs[q] = galois(c, ks[r0 + r]);
+                }
+                kb.add_polys = 1;
+                kb.add_a = 0;
+                RET(ks_moddown(c, m, level, acc, ptmp, md, kb));
+                uint64_t* dsts[MAXB];
+                for (int q = 0; q < m; q++) {
+                    const int o = o0 + q, z = o / R, r = o % R;
+                    dsts[q] = outs[(size_t)(c0 + z) * n + r0 + r];
+                }
+                KL("automorphism", launch_automorphism(pres, dsts, m, 2 * l1, c->log_n, gs, c->stream));
+            }
+        }
+    }
+    dfree(c, scratch);
+    return HISA_OK;
+}
+
+extern "C" int hisa_rot_left_hoisted_batch(hisa_ctx* c, const hisa_ct* in, size_t nct, const int64_t* k, size_t n,
+                                           hisa_ct* outs) {
+    CHECK_CTX(c);
+    if ((!in || !k || !outs) && nct && n) return fail(HISA_E_PARAMS, "null argument");
+    if (nct == 0 || n == 0) return HISA_OK;
+    std::vector<Obj*> objs(nct);
+    for (size_t i = 0; i < nct; i++) {
+        objs[i] = get_obj(c, in[i], OBJ_CT);
+        if (!objs[i]) return fail(HISA_E_INVALID_HANDLE, "invalid ciphertext handle at %zu", i);
+        if (objs[i]->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext at %zu", i);
+        if (objs[i]->level != objs[0]->level) return fail(HISA_E_LEVEL_MISMATCH, "batch levels differ");
+    }
+    std::vector<uint64_t> kk(n), amounts;
+    std::vector<size_t> nz_idx;
+    for (size_t r = 0; r < n; r++) {
+        normalize_rot(c, k[r], &kk[r]);
+        if (kk[r] && !c->rot_keys.count(kk[r]))
+            return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk[r]);
+        if (kk[r]) { nz_idx.push_back(r); amounts.push_back(kk[r]); }
+    }
+    for (size_t i = 0; i < nct; i++)
+        for (size_t r = 0; r < n; r++)
+            if (!kk[r]) RET(hisa_copy(c, in[i], &outs[i * n + r]));
+    if (amounts.empty()) return HISA_OK;
+    const int na = (int)amounts.size();
+    std::vector<uint64_t*> res((size_t)nct * na);
+    RET(rotate_hoisted_multi(c, objs.data(), (int)nct, amounts.data(), na, res.data()));
+    for (size_t i = 0; i < nct; i++)
+        for (int a = 0; a < na; a++)
+            outs[i * n + nz_idx[a]] = new_handle(c, OBJ_CT, res[i * na + a], objs[i]->level, 2, objs[i]->scale);
+    return HISA_OK;
+}
+
 static int rot_common(hisa_ctx* c, hisa_ct h, int64_t k, hisa_ct* out) {
     CHECK_CTX(c);
     GET_CT(o, h);

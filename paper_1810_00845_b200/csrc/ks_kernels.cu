@@ -305,4 +305,64 @@ cudaError_t launch_ks_ip_hoisted(const KsHoistJob& job, int R, const Mod* mods, 
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// K7 batched over ciphertexts: CG ciphertexts x R keys per thread-word (one word per thread),
+// 2 CG R 128-bit accumulators; the key words are loaded once for the CG ciphertexts.
+// ------------------------------------------------------------------------------------------
+template <int CG, int R>
+__global__ void __launch_bounds__(256) k_ks_ip_hoisted_multi(KsHoistMultiJob job, const Mod* __restrict__ mods,
+                                                             int log_n) {
+    const int ri = blockIdx.y;
+    const int l1 = job.l1, l2 = l1 + 1;
+    const long long N = 1ll << log_n;
+    const long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (x >= N) return;
+    const int mi = job.mod_map[ri];
+    const Mod md = mods[mi];
+    U128 acc[CG][R][2];
+#pragma unroll
+    for (int c = 0; c < CG; c++)
+#pragma unroll
+        for (int k = 0; k < R; k++) { acc[c][k][0] = U128{0, 0}; acc[c][k][1] = U128{0, 0}; }
+    const long long kstride_j = 2ll * (job.L + 1) * N;
+    const long long kstride_p = (long long)(job.L + 1) * N;
+    const long long koff = (long long)mi * N + x;
+    for (int j = 0; j < l1; j++) {
+        uint64_t d[CG];
+#pragma unroll
+        for (int c = 0; c < CG; c++) {
+            const uint64_t* src = (j == ri) ? job.diag[c] + (long long)j * N + x
+                                            : job.D[c] + ((long long)j * l2 + ri) * N + x;
+            d[c] = __ldcs(src);
+        }
+#pragma unroll
+        for (int k = 0; k < R; k++) {
+            const uint64_t* kb = job.key[k] + j * kstride_j + koff;
+            const uint64_t b = __ldcs(kb), a = __ldcs(kb + kstride_p);
+#pragma unroll
+            for (int c = 0; c < CG; c++) {
+                mac128(acc[c][k][0], d[c], b);
+                mac128(acc[c][k][1], d[c], a);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CG; c++)
+#pragma unroll
+        for (int k = 0; k < R; k++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+                job.acc[c][k][((long long)h * l2 + ri) * N + x] = barrett128(acc[c][k][h].lo, acc[c][k][h].hi, md);
+}
+
+cudaError_t launch_ks_ip_hoisted_multi(const KsHoistMultiJob& job, int R, const Mod* mods, int log_n, cudaStream_t st) {
+    const long long N = 1ll << log_n;
+    dim3 grid((unsigned)((N + 255) / 256), job.l1 + 1, 1);
+#define C(CGV, RV) if (job.cg == CGV && R == RV) { k_ks_ip_hoisted_multi<CGV, RV><<<grid, 256, 0, st>>>(job, mods, log_n); return cudaGetLastError(); }
+    C(4, 1) C(4, 2) C(4, 3) C(4, 4) C(2, 1) C(2, 2) C(2, 3) C(2, 4) C(3, 1) C(3, 2) C(3, 3) C(3, 4)
+    C(1, 1) C(1, 2) C(1, 3) C(1, 4)
+#undef C
+    return cudaErrorInvalidValue;
+}
+
 }  // namespace hisa

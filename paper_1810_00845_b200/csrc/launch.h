@@ -67,6 +67,18 @@ struct KsHoistJob {
 };
 cudaError_t launch_ks_ip_hoisted(const KsHoistJob& job, int R, const Mod* mods, int log_n, cudaStream_t st);
 
+// K7 over CG ciphertexts sharing the R keys (every key word streamed once per CG ciphertexts)
+constexpr int MAXCG = 4;
+struct KsHoistMultiJob {
+    const uint64_t* D[MAXCG];       // per ciphertext [j][ri][N] (diagonal blocks unused)
+    const uint64_t* diag[MAXCG];    // per ciphertext digit source [(l+1)][N]
+    const uint64_t* key[MAXR];      // R pre-permuted keys
+    uint64_t* acc[MAXCG][MAXR];     // out [2][l+2][N]
+    int l1, L, cg;
+    uint8_t mod_map[MAXL];
+};
+cudaError_t launch_ks_ip_hoisted_multi(const KsHoistMultiJob& job, int R, const Mod* mods, int log_n, cudaStream_t st);
+
 // int64 sum of <= 8 fully reduced residue arrays (the NCCL reduce-scatter output, a15) -> residues
 cudaError_t launch_reduce_sum(const int64_t* in, uint64_t* out, int npolys, int l1, int log_n, const Mod* mods,
                               cudaStream_t st);

@@ -153,6 +153,9 @@ class Symbolic:
             out.append(self._new(lv, sc))
         return out
 
+    def rot_left_hoisted_batch(self, hs, ks):
+        return [self.rot_left_hoisted(h, ks) for h in hs]
+
     def rot_left_batch(self, hs, k):
         kk = k % self.slots
         if kk:
@@ -330,8 +333,11 @@ class EncryptedNet:
                    for i in range(k) for j in range(k)]
         nz = [a for a in amounts if a]
         rotated, wcols, temps = [], [], []
-        for ci, ct in zip(own_in, cts):
-            rs = iter(self.b.rot_left_hoisted(ct, nz) if nz else [])
+        # every owned input channel x every non-zero tap: ModUps batched over channels, each key
+        # word streamed once per group of channels (hisa_rot_left_hoisted_batch)
+        allr = self.b.rot_left_hoisted_batch(list(cts), nz) if (nz and cts) else [[] for _ in cts]
+        for ci, ct, rl in zip(own_in, cts, allr):
+            rs = iter(rl)
             for a in amounts:                     # tap with amount 0 = the input itself
                 h = next(rs) if a else ct
                 rotated.append(h)
@@ -373,8 +379,8 @@ class EncryptedNet:
     def avgpool(self, cts, lay):
         """2x2 average pool (A26): x + rot(wS) + rot(hS) + rot(hS + wS), hoisted."""
         out = []
-        for ct in cts:
-            r = self.b.rot_left_hoisted(ct, [lay.wS, lay.hS, lay.hS + lay.wS])
+        allr = self.b.rot_left_hoisted_batch(list(cts), [lay.wS, lay.hS, lay.hS + lay.wS]) if cts else []
+        for ct, r in zip(cts, allr):
             s1 = self.b.add(ct, r[0])
             s2 = self.b.add(r[1], r[2])
             out.append(self.b.add(s1, s2))

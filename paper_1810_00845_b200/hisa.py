@@ -84,6 +84,7 @@ _SIGS = {
     "hisa_mod_switch": [_vp, _cu64, _ci, _u64p],
     "hisa_rot_left_hoisted": [_vp, _cu64, _i64p, _csz, _u64p],
     "hisa_rot_left_batch": [_vp, _u64p, _csz, _ci64, _u64p],
+    "hisa_rot_left_hoisted_batch": [_vp, _u64p, _csz, _i64p, _csz, _u64p],
     "hisa_conv_accumulate": [_vp, _u64p, _csz, _dp, _csz, _cd, _u64p],
     "hisa_conv_accumulate_dev": [_vp, _u64p, _csz, _dp, _csz, _cd, _vp],
     "hisa_rot_add_batch": [_vp, _u64p, _csz, _ci64, _u64p],
@@ -325,6 +326,17 @@ def hisa_rot_left_hoisted(ctx, ct: int, ks) -> list[int]:
     outs = np.zeros(k.size, dtype=np.uint64)
     _chk(load().hisa_rot_left_hoisted(ctx, ct, _ptr(k, _i64p), k.size, _ptr(outs, _u64p)))
     return [int(x) for x in outs]
+
+
+def hisa_rot_left_hoisted_batch(ctx, cts, ks) -> list[list[int]]:
+    """[[rotLeft(ct, k) for k in ks] for ct in cts] with shared ModUps and key streams."""
+    ins = _u64(list(cts))
+    k = np.ascontiguousarray(list(ks), dtype=np.int64)
+    outs = np.zeros(ins.size * k.size, dtype=np.uint64)
+    if ins.size and k.size:
+        _chk(load().hisa_rot_left_hoisted_batch(ctx, _ptr(ins, _u64p), ins.size, _ptr(k, _i64p), k.size,
+                                                _ptr(outs, _u64p)))
+    return [[int(x) for x in outs[i * k.size:(i + 1) * k.size]] for i in range(ins.size)]
 
 
 def hisa_rot_left_batch(ctx, cts, k: int) -> list[int]:

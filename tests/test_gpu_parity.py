@@ -387,3 +387,19 @@ def test_batched_mul_and_rescale(pair):
     if o.L >= 2:
         for h, oc in zip(g.rescale_batch(list(hs)), os_):
             pair.same(h, o.rescale(oc))
+
+
+def test_hoisted_batch_many_cts(pair):
+    """hisa_rot_left_hoisted_batch: 5 ciphertexts (K7 groups of 4 + 1) x 6 amounts (key chunks
+    of 4 + 2) incl. a zero amount, == per-ciphertext rotLeft bit for bit."""
+    g, o = pair.g, pair.o
+    extra = [5, 7, 9, 11, 13]
+    g.keygen(extra, False)
+    for k in extra:
+        o.add_rot_key(k)
+    hs, os_ = zip(*[pair.ct(110 + i) for i in range(5)])
+    ks = [5, 0, 7, 9, 11, 13]
+    outs = g.rot_left_hoisted_batch(list(hs), ks)
+    for i in (0, 3, 4):
+        for r, k in enumerate(ks):
+            pair.same(outs[i][r], o.rot_left(os_[i], k))
