@@ -20,6 +20,9 @@ template <int LOG_M, int LOG_R, int GR, int MINB>
 __global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip(KsJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
+    // GR == 1, FP64 engine: the row's 2^LOG_M - 1 twiddles are the same for every digit j ->
+    // staged once in shared memory after the tile (no global twiddle loads in the j loop)
+    double* tws = reinterpret_cast<double*>(sm + GR * G::STRIDE);
     // ciphertext index fastest: CTAs that read the same key tile are scheduled together (L2 reuse)
     const int nz = job.nz;
     const int z = blockIdx.x % nz;
@@ -43,6 +46,14 @@ __global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_i
     const long long kstride_j = 2ll * (job.L + 1) << log_n;
     const long long kstride_p = (long long)(job.L + 1) << log_n;
     const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
+    if (GR == 1 && fp) {
+        const double* twg = tb.fwd_d + ((long long)mi << log_n);
+        const int s0 = log_n - LOG_M;
+        for (int idx = threadIdx.x + 1; idx < G::M; idx += NTHR) {
+            const int u = 31 - __clz(idx), m = idx - (1 << u);
+            tws[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
+        }
+    }
     for (int j = 0; j < l1; j++) {
         const uint64_t* src = (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
                                         : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
@@ -56,7 +67,9 @@ __global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_i
         __syncthreads();
         const bool conv = fp && j != ri;   // FP64-engine output: centred-lazy doubles
         if (j != ri) {
-            if (fp)
+            if (fp && GR == 1)
+                fwd_engine_f64_rowtw<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y, tws, t);
+            else if (fp)
                 fwd_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y,
                                              tb.fwd_d + ((long long)mi << log_n), log_n - LOG_M,
                                              (uint32_t)(row0 + g), g, t);
@@ -195,13 +208,132 @@ static cudaError_t ks_ip_pipe_t(const KsJob& job, const Tables& tb, int nz, cuda
     return cudaGetLastError();
 }
 
+// K4 for one row per CTA with two digits in flight (variant 30, FP64 output primes): the
+// non-diagonal digits j != ri are processed in pairs -- both D tiles copied, both transformed by
+// one interleaved engine call (fwd_engine_f64_rowtw2, twiddles staged once in shared memory),
+// both multiplied into the same 128-bit accumulators -- then the diagonal digit (already in the
+// NTT domain) is multiplied in.  Integer-engine primes (q >= 2^50) fall back to one digit at a time.
+template <int LOG_M, int LOG_R, int MINB>
+__global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(KsJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R>;
+    extern __shared__ uint64_t sm[];
+    uint64_t* sa = sm;
+    uint64_t* sb = sm + G::STRIDE;
+    double* tws = reinterpret_cast<double*>(sm + 2 * G::STRIDE);
+    const int nz = job.nz;
+    const int z = blockIdx.x % nz;
+    const int ri = blockIdx.y;
+    const int l1 = job.l1;
+    const int nri = l1 + 1;
+    const int log_n = tb.log_n;
+    const int row0 = blockIdx.x / nz;
+    const long long off0 = (long long)row0 << LOG_M;
+    const int mi = job.mod_map[ri];
+    const Mod md = tb.mods[mi];
+    const bool fp = (double)md.q < tb.f64_max_q;
+    const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
+    const double qp52 = __dadd_rn(qd.x, 4503599627370496.0);
+    constexpr int NTHR = G::T;
+    constexpr int EPT = G::R;
+    U128 acc0[EPT], acc1[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
+    const int t = threadIdx.x;
+    const long long kstride_j = 2ll * (job.L + 1) << log_n;
+    const long long kstride_p = (long long)(job.L + 1) << log_n;
+    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
+    if (fp) {
+        const double* twg = tb.fwd_d + ((long long)mi << log_n);
+        const int s0 = log_n - LOG_M;
+        for (int idx = threadIdx.x + 1; idx < G::M; idx += NTHR) {
+            const int u = 31 - __clz(idx), m = idx - (1 << u);
+            tws[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
+        }
+    }
+    auto copy_tile = [&](uint64_t* dst, int j) {
+        const uint64_t* src = (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
+                                        : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * NTHR;
+            const unsigned s_ = (unsigned)__cvta_generic_to_shared(&dst[G::addr(0, i)]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_), "l"(src + i) : "memory");
+        }
+    };
+    auto mac_tile = [&](const uint64_t* buf, int j, bool conv) {
+        const uint64_t* kb = key_r + j * kstride_j;
+        const uint64_t* ka = kb + kstride_p;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * NTHR;
+            uint64_t D = buf[G::addr(0, i)];
+            if (conv) D = d_rep(__longlong_as_double((long long)D), qd.x, qd.y, qp52);   // < 1.5q
+            mac128(acc0[k], D, __ldg(kb + i));
+            mac128(acc1[k], D, __ldg(ka + i));
+        }
+    };
+    // digits j != ri, in pairs
+    int j = 0;
+    auto next_nd = [&](int from) { return from == ri ? from + 1 : from; };
+    j = next_nd(0);
+    while (j < l1) {
+        const int ja = j;
+        int jb = next_nd(ja + 1);
+        const bool two = fp && jb < l1;
+        copy_tile(sa, ja);
+        if (two) copy_tile(sb, jb);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        if (two) {
+            fwd_engine_f64_rowtw2<LOG_M, LOG_R>(reinterpret_cast<double*>(sa), reinterpret_cast<double*>(sb), qd.x,
+                                                qd.y, tws, t);
+            mac_tile(sa, ja, true);
+            mac_tile(sb, jb, true);
+            j = next_nd(jb + 1);
+        } else {
+            if (fp)
+                fwd_engine_f64_rowtw<LOG_M, LOG_R>(reinterpret_cast<double*>(sa), qd.x, qd.y, tws, t);
+            else
+                fwd_engine<LOG_M, LOG_R>(sa, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
+                                         (uint32_t)row0, 0, t);
+            mac_tile(sa, ja, fp);
+            j = next_nd(ja + 1);
+        }
+        __syncthreads();
+    }
+    if (ri < l1) {   // the diagonal digit: D_{ri, q_ri} = d_ri, already in the NTT domain
+        copy_tile(sa, ri);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        mac_tile(sa, ri, false);
+    }
+    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
+    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
+#pragma unroll
+    for (int k = 0; k < EPT; k++) {
+        const int i = threadIdx.x + k * NTHR;
+        out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
+        out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
+    }
+}
+
+template <int LOG_M, int LOG_R, int MINB>
+static cudaError_t ks_ip2_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+    using G = Geo<LOG_M, LOG_R>;
+    const int rows = 1 << (tb.log_n - LOG_M);
+    const size_t smem = (2 * (size_t)G::STRIDE + G::M) * sizeof(uint64_t);
+    dim3 grid(rows * nz, job.l1 + 1, 1);
+    k_ks_ip2<LOG_M, LOG_R, MINB><<<grid, G::T, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+
 template <int LOG_M, int LOG_R, int GR, int MINB>
 static cudaError_t ks_ip_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     using G = Geo<LOG_M, LOG_R>;
     const int rows = 1 << (tb.log_n - LOG_M);
     if (rows < GR) return cudaErrorInvalidValue;
     constexpr int threads = GR * G::T;
-    const size_t smem = (size_t)GR * G::STRIDE * sizeof(uint64_t);
+    const size_t smem = ((size_t)GR * G::STRIDE + (GR == 1 ? G::M : 0)) * sizeof(uint64_t);
     dim3 grid((rows / GR) * nz, job.l1 + 1, 1);
     k_ks_ip<LOG_M, LOG_R, GR, MINB><<<grid, threads, smem, st>>>(job, tb);
     return cudaGetLastError();
@@ -223,15 +355,22 @@ static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStrea
         case 7: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 4>(job, tb, nz, st); break;
         case 8: if (rows >= 8) return ks_ip_t<LOG_M, 3, 8, 1>(job, tb, nz, st); break;
         case 10: return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
+        case 30: return ks_ip2_t<LOG_M, 2, 8>(job, tb, nz, st);
+        case 31: return ks_ip2_t<LOG_M, 2, 6>(job, tb, nz, st);
+        case 32: return ks_ip2_t<LOG_M, 2, 10>(job, tb, nz, st);
+        case 33: return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
+        case 34: return ks_ip2_t<LOG_M, 2, 14>(job, tb, nz, st);
+        case 35: return ks_ip2_t<LOG_M, 2, 16>(job, tb, nz, st);
         case 20: return ks_ip_pipe_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
         case 21: return ks_ip_pipe_t<LOG_M, 2, 1, 6>(job, tb, nz, st);
         case 22: if (rows >= 2) return ks_ip_pipe_t<LOG_M, 2, 2, 4>(job, tb, nz, st); break;
         case 23: return ks_ip_pipe_t<LOG_M, 3, 1, 8>(job, tb, nz, st);
         default: break;
     }
-    // default = variant 10 (measured best on B200 at N = 2^16, L = 24: radix-4 phases, one row
-    // per CTA of 64 threads, >= 8 CTAs / SM; profiles/r1_ks_variants.txt)
-    return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
+    // default = variant 33 (measured best on B200 at N = 2^16, L = 24: one row per 64-thread CTA,
+    // radix-4 phases, two digits interleaved through the FP64 engine with the row's twiddles
+    // staged in shared memory, >= 12 CTAs / SM; profiles/r1_ks_variants.txt)
+    return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
 }
 
 cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {

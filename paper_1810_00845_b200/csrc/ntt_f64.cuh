@@ -112,6 +112,116 @@ __device__ __forceinline__ void fwd_engine_f64(double* sm, double q, double qinv
     }
 }
 
+// the same forward stages for ONE row group (row pass, g == 0) whose 2^LOG_M - 1 twiddles were
+// staged in shared memory: tws[(1 << u) + m] = psi^brv(2^(s0+u) + (row << u) + m), m < 2^u (the
+// key-switch inner product reuses one row's twiddles for every digit)
+template <int LOG_M, int LOG_R>
+__device__ __forceinline__ void fwd_engine_f64_rowtw(double* sm, double q, double qinv, const double* tws, int t) {
+    using G = Geo<LOG_M, LOG_R>;
+#pragma unroll
+    for (int u0 = 0; u0 < LOG_M; u0 += LOG_R) {
+        const int w = (LOG_M - u0) < LOG_R ? (LOG_M - u0) : LOG_R;
+        const int lo_bit = LOG_M - u0 - w;
+        const int per = G::R >> w;
+#pragma unroll
+        for (int x = 0; x < G::R; x++) {
+            if (x >= per) break;
+            const int o = t * per + x;
+            const int olow = o & ((1 << lo_bit) - 1);
+            const int ohigh = o >> lo_bit;
+            double reg[G::R];
+            int base = (ohigh << (lo_bit + w)) | olow;
+#pragma unroll
+            for (int e = 0; e < G::R; e++)
+                if (e < (1 << w)) reg[e] = sm[G::addr(0, base | (e << lo_bit))];
+#pragma unroll
+            for (int uu = 0; uu < LOG_R; uu++) {
+                if (uu >= w) break;
+                const int u = u0 + uu;
+                const int dist = 1 << (w - 1 - uu);
+                const int tbase = (1 << u) + (ohigh << uu);
+#pragma unroll
+                for (int k = 0; k < (1 << LOG_R); k++) {
+                    if (k >= (1 << uu)) break;
+                    const double W = tws[tbase + k];
+#pragma unroll
+                    for (int e0 = 0; e0 < G::R; e0++) {
+                        if (e0 >= dist) break;
+                        const int e = k * 2 * dist + e0;
+                        const double X = redd(reg[e], q, qinv);
+                        const double T = mulred(reg[e + dist], W, q, qinv);
+                        reg[e] = __dadd_rn(X, T);
+                        reg[e + dist] = __dsub_rn(X, T);
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < G::R; e++)
+                if (e < (1 << w)) sm[G::addr(0, base | (e << lo_bit))] = reg[e];
+        }
+        __syncthreads();
+    }
+}
+
+// two tiles of the same prime and row (two digits of the key-switch inner product) through the
+// staged-twiddle engine together: twice the independent FP64 dependency chains per thread
+template <int LOG_M, int LOG_R>
+__device__ __forceinline__ void fwd_engine_f64_rowtw2(double* sa, double* sb, double q, double qinv,
+                                                      const double* tws, int t) {
+    using G = Geo<LOG_M, LOG_R>;
+#pragma unroll
+    for (int u0 = 0; u0 < LOG_M; u0 += LOG_R) {
+        const int w = (LOG_M - u0) < LOG_R ? (LOG_M - u0) : LOG_R;
+        const int lo_bit = LOG_M - u0 - w;
+        const int per = G::R >> w;
+#pragma unroll
+        for (int x = 0; x < G::R; x++) {
+            if (x >= per) break;
+            const int o = t * per + x;
+            const int olow = o & ((1 << lo_bit) - 1);
+            const int ohigh = o >> lo_bit;
+            double ra[G::R], rb[G::R];
+            int base = (ohigh << (lo_bit + w)) | olow;
+#pragma unroll
+            for (int e = 0; e < G::R; e++)
+                if (e < (1 << w)) {
+                    ra[e] = sa[G::addr(0, base | (e << lo_bit))];
+                    rb[e] = sb[G::addr(0, base | (e << lo_bit))];
+                }
+#pragma unroll
+            for (int uu = 0; uu < LOG_R; uu++) {
+                if (uu >= w) break;
+                const int u = u0 + uu;
+                const int dist = 1 << (w - 1 - uu);
+                const int tbase = (1 << u) + (ohigh << uu);
+#pragma unroll
+                for (int k = 0; k < (1 << LOG_R); k++) {
+                    if (k >= (1 << uu)) break;
+                    const double W = tws[tbase + k];
+#pragma unroll
+                    for (int e0 = 0; e0 < G::R; e0++) {
+                        if (e0 >= dist) break;
+                        const int e = k * 2 * dist + e0;
+                        const double Xa = redd(ra[e], q, qinv), Xb = redd(rb[e], q, qinv);
+                        const double Ta = mulred(ra[e + dist], W, q, qinv), Tb = mulred(rb[e + dist], W, q, qinv);
+                        ra[e] = __dadd_rn(Xa, Ta);
+                        rb[e] = __dadd_rn(Xb, Tb);
+                        ra[e + dist] = __dsub_rn(Xa, Ta);
+                        rb[e + dist] = __dsub_rn(Xb, Tb);
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < G::R; e++)
+                if (e < (1 << w)) {
+                    sa[G::addr(0, base | (e << lo_bit))] = ra[e];
+                    sb[G::addr(0, base | (e << lo_bit))] = rb[e];
+                }
+        }
+        __syncthreads();
+    }
+}
+
 // inverse GS stages, mirrors inv_engine (ntt.cuh)
 template <int LOG_M, int LOG_R>
 __device__ __forceinline__ void inv_engine_f64(double* sm, double q, double qinv, const double* __restrict__ tw,
