@@ -8,17 +8,22 @@
 // FP64 step below is exact integer arithmetic (values are integers of magnitude < 2^53).
 //
 // Representation: a residue class v mod q is held as a double (an integer) of magnitude <= B q,
-// signed ("centred lazy").  Primitives (q < 2^50, qinv = fl(1/q)):
+// signed ("centred lazy").  Primitives (q < 2^50, qinv = fl(1/q)); bounds for the worst case
+// q -> 2^50 (smaller q only shrink the error terms):
 //   red(v)          = v - rint(v qinv) q                    exact (one FMA); |red(v)| <= (0.5 + B 2^-52) q
-//   mulred(a, w)    = a w - rint(fl(a w) qinv) q, computed exactly as
+//   mulred(a, w)    = a w - qt q with qt = rint(fl(fl(a w) qinv)), computed exactly as
 //                     h = fl(a w); l = fma(a, w, -h) (= a w - h exactly); t = fma(-qt, q, h) + l
-//                     the FMA result h - qt q is an integer of magnitude < 2^53 (exact), l is an
-//                     integer, |l| <= ulp(h)/2; |t| <= (0.5 + 0.375 |a|/q) q for 0 <= w < q
-//                     (three roundings in the quotient estimate: relative error <= 1.5 2^-52).
+//                     the FMA result h - qt q is an integer of magnitude < 2^53 (exact) and l is an
+//                     integer.  For |a| <= B q, 0 <= w < q: the quotient estimate has relative error
+//                     <= 3 2^-53, i.e. |qt - a w / q| <= 0.5 + 0.375 B, so |h - qt q| <= (0.5 + 0.375 B) q,
+//                     and |l| <= ulp(h)/2 <= 2^-53 B q^2 <= 0.125 B q  =>  |t| <= (0.5 + 0.5 B) q.
 // Forward CT butterfly (X, Y) -> (X' + t, X' - t), X' = red(X), t = mulred(Y, W):
-//   B_out = 0.5 + 0.5 + 0.375 B_in  -> fixed point B = 1.6 (inputs start at B = 1).
-// Inverse GS butterfly (X, Y) -> (red(X + Y), mulred(X - Y, W)):
-//   B_out = max(0.5, 0.5 + 0.75 B_in) -> fixed point B = 2 (|X - Y| <= 4q < 2^52).
+//   B_out = 0.5 + 0.5 + 0.5 B_in  -> fixed point B = 2 (inputs start at B <= 1): every value and
+//   every intermediate stays below 4 q^2 / 2^53 of ulp trouble; all magnitudes <= 2q < 2^51.
+// Inverse GS butterfly (X, Y) -> (red(X + Y), mulred(red(X - Y), W)):
+//   |red(X - Y)| <= 0.5q (+eps)  =>  |t| <= 0.75 q; B_out <= 0.75 for any number of stages.
+//   (Without re-centring the difference, B would grow by q/2 per stage: 16 stages could exceed
+//   2^53 / q for q near 2^50.)
 // Loads convert [0, q) uint64 -> double exactly (bit trick, x < 2^52); stores reduce fully:
 //   r = red(v); r += q if r < 0 -> [0, q), then back to uint64.
 #pragma once
@@ -261,7 +266,7 @@ __device__ __forceinline__ void inv_engine_f64(double* sm, double q, double qinv
                         const int e = k * 2 * dist + e0;
                         const double X = reg[e], Y = reg[e + dist];
                         reg[e] = redd(__dadd_rn(X, Y), q, qinv);
-                        reg[e + dist] = mulred(__dsub_rn(X, Y), W, q, qinv);
+                        reg[e + dist] = mulred(redd(__dsub_rn(X, Y), q, qinv), W, q, qinv);
                     }
                 }
             }
