@@ -1,0 +1,89 @@
+"""The exact-FP64 modular primitives of csrc/ntt_f64.cuh, emulated on the host with IEEE binary64
+(Python floats) and an exact FMA (integer arithmetic, one rounding): exactness (t == a w mod q)
+and the magnitude bounds the butterfly engines rely on, for q up to 2^50 and adversarial operands.
+"""
+import random
+from fractions import Fraction
+
+import pytest
+
+
+def fma(a: float, b: float, c: float) -> float:
+    """fl(a*b + c) with a single rounding (round-half-even): exact rational, then float()."""
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def redd(v: float, q: float, qinv: float) -> float:
+    return fma(-float(round(v * qinv)), q, v)
+
+
+def mulred(a: float, w: float, q: float, qinv: float) -> float:
+    h = a * w
+    l = fma(a, w, -h)
+    qt = float(round(h * qinv))
+    return fma(-qt, q, h) + l
+
+
+def _primes_near_2_50():
+    # q = 1 mod 2^17 (N = 2^16), the largest below 2^50 (config 2's 50-bit limbs), and 2^40-ish
+    out = []
+    for bits in (50, 40):
+        k = ((1 << bits) - 2) // (1 << 17)
+        while len([q for q in out if q.bit_length() == bits]) < 2:
+            q = k * (1 << 17) + 1
+            if all(q % p for p in range(3, 2000, 2)) and pow(3, q - 1, q) == 1:
+                out.append(q)
+            k -= 1
+    return out
+
+
+@pytest.mark.parametrize("q", _primes_near_2_50())
+def test_mulred_exact_and_bounded(q):
+    rng = random.Random(q)
+    qf, qinv = float(q), 1.0 / float(q)
+    for B in (0.5, 1.0, 2.0):                      # the engines' input bounds (|a| <= B q)
+        amax = int(B * q)
+        cases = [(amax, q - 1), (-amax, q - 1), (amax, 1), (0, q - 1), (amax - 1, (q - 1) // 2)]
+        cases += [(rng.randint(-amax, amax), rng.randrange(q)) for _ in range(4000)]
+        worst = 0.0
+        for a, w in cases:
+            t = mulred(float(a), float(w), qf, qinv)
+            assert t == int(t) and abs(t) < 2 ** 53
+            assert (int(t) - a * w) % q == 0, (a, w)
+            worst = max(worst, abs(t) / q)
+        assert worst <= 0.5 + 0.5 * B + 1e-9, (B, worst)   # ntt_f64.cuh: |t| <= (0.5 + 0.5 B) q
+
+
+@pytest.mark.parametrize("q", _primes_near_2_50())
+def test_butterfly_fixed_points(q):
+    """Forward CT (X, Y) -> (red X + t, red X - t) stays <= 2q over many stages; inverse GS
+    (X, Y) -> (red(X + Y), mulred(red(X - Y), W)) stays <= 0.75 q."""
+    rng = random.Random(q + 1)
+    qf, qinv = float(q), 1.0 / float(q)
+    for _ in range(300):
+        x, y = float(rng.randrange(q)), float(rng.randrange(q))
+        for _stage in range(16):
+            w = float(rng.randrange(q))
+            xr = redd(x, qf, qinv)
+            t = mulred(y, w, qf, qinv)
+            x, y = xr + t, xr - t
+            assert abs(x) <= 2 * q and abs(y) <= 2 * q
+        a, b = float(rng.randrange(q)), float(rng.randrange(q))
+        for _stage in range(16):
+            w = float(rng.randrange(q))
+            s = redd(a + b, qf, qinv)
+            d = mulred(redd(a - b, qf, qinv), w, qf, qinv)
+            assert (int(d) - ((int(a) - int(b)) % q) * int(w)) % q == 0
+            a, b = s, d
+            assert abs(a) <= 0.5 * q * (1 + 2 ** -40) and abs(b) <= 0.75 * q
+
+
+def test_bit_conversions():
+    """u2d / d2u bit tricks: x < 2^52 <-> double exactly (used at every load / store)."""
+    import struct
+    for x in (0, 1, (1 << 50) - 1, (1 << 52) - 1, 123456789012345):
+        bits = x | 0x4330000000000000
+        d = struct.unpack("<d", struct.pack("<Q", bits))[0] - 4503599627370496.0
+        assert d == float(x) and int(d) == x
+        back = struct.unpack("<Q", struct.pack("<d", d + 4503599627370496.0))[0] & ((1 << 52) - 1)
+        assert back == x
