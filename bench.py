@@ -137,11 +137,16 @@ def rotation_alg_bytes(log_n: int, l1: int, B: int) -> float:
     return (B * 4 * l1 + 2 * l1 * (l1 + 1)) * limb
 
 
+K7_KEYS_PER_LAUNCH = 4   # hisa.cu rotate_hoisted_multi (RK)
+
+
 def hoisted_ip_alg_bytes(log_n: int, l1: int, R: int) -> float:
-    """K7 inner product, one launch: D read once (l1 (l1+1) limbs), R keys (2 l1 (l1+1) limbs
-    each) streamed, R accumulators (2 (l1+1) limbs) written."""
+    """K7 inner products of one hoisted call with R amounts, one ciphertext: per launch (<= 4 keys)
+    D is read once (l1 (l1+1) limbs), each key (2 l1 (l1+1) limbs) streamed once, each
+    accumulator (2 (l1+1) limbs) written once."""
     limb = 8 * (1 << log_n)
-    return (l1 * (l1 + 1) + R * (2 * l1 * (l1 + 1) + 2 * (l1 + 1))) * limb
+    launches = -(-R // K7_KEYS_PER_LAUNCH)
+    return (launches * l1 * (l1 + 1) + R * (2 * l1 * (l1 + 1) + 2 * (l1 + 1))) * limb
 
 
 def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream):
@@ -170,7 +175,9 @@ def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream):
     ip_ms, ip_n = prof.get("ks_ip_hoisted", (0.0, 0))
     total = sum(v[0] for v in prof.values()) or 1.0
     per_launch = ip_ms / max(ip_n, 1)
-    alg = hoisted_ip_alg_bytes(log_n, L, R)
+    calls = len(cts) * steps
+    alg_call = hoisted_ip_alg_bytes(log_n, L, R)
+    alg = alg_call * calls / max(ip_n, 1)           # algorithmic bytes per launch
     hbm_peak = _hbm_peak()
     rot = len(cts) * R * steps
     return {"value": rot / (ms / 1e3), "unit": "rot/s", "amounts_per_modup": R, "ciphertexts": len(cts),
@@ -178,7 +185,7 @@ def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream):
             "roofline": {"bound": "hbm", "kernel": "ks_ip_hoisted", "achieved": alg / (per_launch / 1e3) / 1e9,
                          "peak": hbm_peak, "unit": "GB/s", "frac": alg / (per_launch / 1e3) / 1e9 / hbm_peak,
                          "alg_bytes_per_launch": alg, "launch_ms_avg": per_launch, "share_of_step": ip_ms / total,
-                         "traffic": _ncu_traffic("ks_ip_hoisted", log_n, L, R),
+                         "traffic": _ncu_traffic("ks_ip_hoisted", log_n, L, 8),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             "kernels": {n: {"ms": v[0], "launches": v[1], "share": v[0] / total}
                         for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}}
@@ -400,42 +407,77 @@ def main():
                    "gmodmul_s": kernel_units(n, log_n, L, B) * a.steps / (v[0] / 1e3) / 1e9 if v[0] else None}
                for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
 
-    # end-to-end through the C-ABI with pinned host buffers
+    # end-to-end through the C-ABI with pinned host buffers: every step copies its B input
+    # ciphertexts host -> device and its B results device -> host.  Pipelined over three streams
+    # (PyTorch streams / events as plumbing): the H2D of step i+1 and the D2H of step i-1 run
+    # while step i key-switches; hisa_ct_adopt_device / hisa_ct_device_view move the words
+    # between the torch staging tensors and libhisa's arena (device-to-device, ~50 us per step).
     e2e = None
     if not a.no_e2e:
         words = 2 * L * N
-        host_in = [torch.empty(words, dtype=torch.int64, pin_memory=True).numpy().view("uint64") for _ in range(B)]
+        host_in = [torch.empty(words, dtype=torch.int64, pin_memory=True) for _ in range(B)]
         for b in range(B):
-            host_in[b][:] = ctx.ct_export(cts[b]).ravel()
-        host_out = [torch.empty(words, dtype=torch.int64, pin_memory=True).numpy().view("uint64") for _ in range(B)]
-        from paper_1810_00845_b200.hisa import _chk, _ptr, _u64p, load
-        lib = load()
+            host_in[b].numpy().view("uint64")[:] = ctx.ct_export(cts[b]).ravel()
+        host_out = [torch.empty(words, dtype=torch.int64, pin_memory=True) for _ in range(B)]
+        dev = torch.device(f"cuda:{local}")
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        din = [[torch.empty(words, dtype=torch.int64, device=dev) for _ in range(B)] for _ in range(2)]
+        dout = [[torch.empty(words, dtype=torch.int64, device=dev) for _ in range(B)] for _ in range(2)]
+        ev_in = [torch.cuda.Event() for _ in range(2)]      # H2D of slot done
+        ev_used = [torch.cuda.Event() for _ in range(2)]    # compute finished reading din[slot]
+        ev_res = [torch.cuda.Event() for _ in range(2)]     # results of slot staged in dout
+        ev_out = [torch.cuda.Event() for _ in range(2)]     # D2H of slot done
+        for e in ev_used + ev_out:
+            e.record(stream)
+        from paper_1810_00845_b200.parallel import _DevArray
 
-        def e2e_step():
-            ins = [ctx.ct_import(host_in[b], L - 1, 2, 2.0 ** 40) for b in range(B)]
+        def e2e_step(i):
+            sl = i % 2
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(ev_used[sl])
+                for b in range(B):
+                    din[sl][b].copy_(host_in[b], non_blocking=True)
+                ev_in[sl].record(s_in)
+            stream.wait_event(ev_in[sl])
+            ins = [ctx.ct_adopt_device(din[sl][b].data_ptr(), L - 1, 2, 2.0 ** 40) for b in range(B)]
+            ev_used[sl].record(stream)
             outs = ctx.rot_left_batch(ins, k)
+            stream.wait_event(ev_out[sl])
             for b, h in enumerate(outs):
-                _chk(lib.hisa_ct_export(ctx.ctx, h, _ptr(host_out[b], _u64p), words))
-                ctx.free(h)
-            for h in ins:
+                ptr, w = ctx.ct_device_view(h)
+                dout[sl][b].copy_(torch.as_tensor(_DevArray(ptr, w), device=dev))
+            ev_res[sl].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_res[sl])
+                for b in range(B):
+                    host_out[b].copy_(dout[sl][b], non_blocking=True)
+                ev_out[sl].record(s_out)
+            for h in outs + ins:
                 ctx.free(h)
 
-        e2e_step()
+        for i in range(2):
+            e2e_step(i)
+        torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        torch.cuda.synchronize()
+        n_e2e = max(4, a.steps)
         t0 = time.perf_counter()
-        n_e2e = max(1, a.steps // 2)
-        for _ in range(n_e2e):
-            e2e_step()
+        for i in range(n_e2e):
+            e2e_step(i)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        # the results that reached the host are the rotation's (checked against a direct call)
+        ref = ctx.rot_left_batch(cts[:1], k)[0]
+        e2e_ok = bool((host_out[0].numpy().view("uint64") == ctx.ct_export(ref).ravel()).all())
+        ctx.free(ref)
         if dist:
             t = torch.tensor([dt], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
         e2e = {"value": world * B * n_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": B * words * 8,
-               "d2h_bytes_per_step": B * words * 8, "steps": n_e2e}
+               "d2h_bytes_per_step": B * words * 8, "steps": n_e2e,
+               "pipeline": "3 streams: H2D(i+1) || key switch(i) || D2H(i-1), pinned host buffers",
+               "result_check": e2e_ok}
 
     hoisted = None
     if not a.no_hoisted:

@@ -1671,11 +1671,17 @@ extern "C" int hisa_rot_left_hoisted(hisa_ctx* c, hisa_ct h, const int64_t* k, s
     }
     if (nz_idx.empty()) return HISA_OK;
     std::vector<uint64_t*> res(nz_idx.size());
+    // default: the multi-ciphertext K7 (<= 4 keys per launch, 1 word per thread) -- measured 78 %
+    // of HBM vs 69 % for the 8-key 2-word kernel (HISA_K7_VARIANT=2 keeps it for re-measurement)
+    static const int k7v = getenv("HISA_K7_VARIANT") ? atoi(getenv("HISA_K7_VARIANT")) : 0;
     if (nz_idx.size() == 1) {
         Obj* ins[1] = {o};
         RET(rotate_batch(c, ins, 1, amounts[0], res.data()));
-    } else {
+    } else if (k7v == 2) {
         RET(rotate_hoisted(c, o, amounts.data(), (int)amounts.size(), res.data()));
+    } else {
+        Obj* ins[1] = {o};
+        RET(rotate_hoisted_multi(c, ins, 1, amounts.data(), (int)amounts.size(), res.data()));
     }
     for (size_t r = 0; r < nz_idx.size(); r++) outs[nz_idx[r]] = new_handle(c, OBJ_CT, res[r], o->level, 2, o->scale);
     return HISA_OK;
