@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-inference", action="store_true")
     ap.add_argument("--hoist-r", type=int, default=8, help="rotation amounts per hoisted ModUp")
     ap.add_argument("--nets", default="tiny,lenet_small", help="encrypted-inference configs to time")
+    ap.add_argument("--policy-net", default="lenet_small",
+                    help="config on which exact vs power-of-two rotation keys are compared ('' = skip)")
     return ap.parse_args()
 
 
@@ -191,7 +193,7 @@ def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream):
                         for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}}
 
 
-def measure_inference(name, device, reps=3):
+def measure_inference(name, device, reps=3, rot_policy="exact"):
     """Encrypted CNN inference latency (BASELINE.json metric, configs 1 / 3): server-side
     forward from encrypted input resident on the GPU to encrypted output, CUDA events + wall
     clock; client encode/encrypt and decrypt/decode timed separately.  (Accuracy against the
@@ -207,11 +209,11 @@ def measure_inference(name, device, reps=3):
     torch.cuda.empty_cache()
     ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=device, arena_bytes=64 << 30)
     t0 = time.perf_counter()
-    plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli)
+    plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli, rot_policy=rot_policy)
     ctx.keygen(plan["rotations"], True)
     ctx.sync()
     t_keys = time.perf_counter() - t0
-    en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS)
+    en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS, rot_policy=rot_policy)
     stream = torch.cuda.current_stream(device)
     # warm-up pass: encodes (caches) the weight plaintexts once per model
     t0 = time.perf_counter()
@@ -250,7 +252,7 @@ def measure_inference(name, device, reps=3):
     ctx.close()
     ctx = None
     torch.cuda.empty_cache()
-    return {"config": name, "latency_s": float(np.median(lat)), "wall_s": float(np.median(walls)), "unit": "s",
+    return {"config": name, "rot_policy": rot_policy, "latency_s": float(np.median(lat)), "wall_s": float(np.median(walls)), "unit": "s",
             "reps": reps, "log_n": net["log_n"], "limbs": len(net["q_bits"]), "gpu_launches": launches,
             "client_encrypt_s": t_enc, "client_decrypt_s": t_dec, "keygen_s": t_keys,
             "first_pass_incl_weight_encoding_s": t_first, "levels_used": plan["levels_used"],
@@ -510,6 +512,16 @@ def main():
     if rank == 0:
         if not a.no_inference and world == 1:
             line["inference"] = [measure_inference(nm, local) for nm in a.nets.split(",") if nm]
+            # NEXT-2: CHET's exact rotation keys vs HEAAN's power-of-two keys with
+            # composed rotations (the paper's Fig. rotopt: 1.43-2.07x on CPU HEAAN)
+            if a.policy_net:
+                ex = next((i for i in line["inference"] if i["config"] == a.policy_net), None) or \
+                    measure_inference(a.policy_net, local)
+                p2 = measure_inference(a.policy_net, local, rot_policy="pow2")
+                line["rot_key_policy"] = {"config": a.policy_net, "exact_s": ex["latency_s"], "pow2_s": p2["latency_s"],
+                                          "exact_keys": ex["rotation_keys"], "pow2_keys": p2["rotation_keys"],
+                                          "speedup_exact_over_pow2": p2["latency_s"] / ex["latency_s"],
+                                          "paper_cpu_heaan": "1.43-2.07x (P:902-918), context only"}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -227,7 +227,13 @@ class EncryptedNet:
     `group` (torch.distributed process group, optional) shards every linear layer's input
     channels across ranks; None = single GPU."""
 
-    def __init__(self, backend, net: dict, weights, act_coeffs, group=None):
+    def __init__(self, backend, net: dict, weights, act_coeffs, group=None, rot_policy: str = "exact"):
+        """rot_policy: "exact" = one key per distinct rotation amount, chosen by the compiler
+        (CHET); "pow2" = HEAAN's default power-of-two keys (left and right),
+        every other amount composed from them (the baseline of the paper's Fig. rotopt)."""
+        if rot_policy not in ("exact", "pow2"):
+            raise ValueError(rot_policy)
+        self.rot_policy = rot_policy
         self.b = backend
         self.net = net
         self.folded, self.gamma = compile_weights(net, weights, act_coeffs)
@@ -243,10 +249,10 @@ class EncryptedNet:
 
     # ---- planning (symbolic execution) ------------------------------------------------------
     @staticmethod
-    def plan(net: dict, weights, act_coeffs, moduli):
+    def plan(net: dict, weights, act_coeffs, moduli, rot_policy: str = "exact"):
         """Level plan, distinct rotation amounts (keygen input), op counts."""
         sym = Symbolic(net["log_n"], moduli)
-        en = EncryptedNet(sym, net, weights, act_coeffs)
+        en = EncryptedNet(sym, net, weights, act_coeffs, rot_policy=rot_policy)
         lay = input_layout(net)
         top = len(moduli) - 2
         cts = [sym.fresh(top, net["scale"]) for _ in range(lay.C)]
@@ -286,6 +292,52 @@ class EncryptedNet:
             return np.concatenate([v[np.arange(lay.H) * lay.hS] for v in vals])[:lay.count]
         idx = lay.slots_of_valid()
         return np.stack([v[idx] for v in vals]).reshape(lay.C, lay.H, lay.W)
+
+    # ---- rotation key policy ----------------------------------------------------
+    def _pow2_steps(self, k: int):
+        """Signed power-of-two decomposition of a left rotation by k (non-adjacent form of k or
+        of k - slots, whichever has fewer terms): left rotations by 2^i and right rotations by
+        2^i (= left by slots - 2^i)."""
+        def naf(v):
+            out, i = [], 0
+            while v:
+                if v & 1:
+                    d = 2 - (v & 3)          # +1 or -1
+                    out.append(d << i)
+                    v -= d
+                v >>= 1
+                i += 1
+            return out
+        k %= self.slots
+        if k == 0:
+            return []
+        a, b = naf(k), naf(k - self.slots)
+        best = a if len(a) <= len(b) else b
+        return [x % self.slots for x in best]
+
+    def _rot_many(self, cts, amounts):
+        """[[rotLeft(ct, a) for a in amounts] for ct in cts]: exact keys -> hoisted batch (shared
+        ModUps); pow2 keys -> each amount composed from power-of-two rotations, batched over cts."""
+        if not cts or not amounts:
+            return [[] for _ in cts]
+        if self.rot_policy == "exact":
+            if len(amounts) == 1:        # one amount: the fused K4 batch (no materialised ModUp)
+                return [[h] for h in self.b.rot_left_batch(list(cts), amounts[0])]
+            return self.b.rot_left_hoisted_batch(list(cts), amounts)
+        out = [[None] * len(amounts) for _ in cts]
+        for ai, a in enumerate(amounts):
+            cur, own = list(cts), False
+            steps = self._pow2_steps(a)
+            if not steps:
+                cur = [self.b.copy(h) for h in cts]
+            for st in steps:
+                nxt = self.b.rot_left_batch(cur, st)
+                if own:
+                    self._free_all(cur)
+                cur, own = nxt, True
+            for i, h in enumerate(cur):
+                out[i][ai] = h
+        return out
 
     # ---- helpers --------------------------------------------------------------------------
     def _plaintext(self, key, values_fn, level):
@@ -335,7 +387,7 @@ class EncryptedNet:
         rotated, wcols, temps = [], [], []
         # every owned input channel x every non-zero tap: ModUps batched over channels, each key
         # word streamed once per group of channels (hisa_rot_left_hoisted_batch)
-        allr = self.b.rot_left_hoisted_batch(list(cts), nz) if (nz and cts) else [[] for _ in cts]
+        allr = self._rot_many(list(cts), nz) if (nz and cts) else [[] for _ in cts]
         for ci, ct, rl in zip(own_in, cts, allr):
             rs = iter(rl)
             for a in amounts:                     # tap with amount 0 = the input itself
@@ -379,7 +431,7 @@ class EncryptedNet:
     def avgpool(self, cts, lay):
         """2x2 average pool (A26): x + rot(wS) + rot(hS) + rot(hS + wS), hoisted."""
         out = []
-        allr = self.b.rot_left_hoisted_batch(list(cts), [lay.wS, lay.hS, lay.hS + lay.wS]) if cts else []
+        allr = self._rot_many(list(cts), [lay.wS, lay.hS, lay.hS + lay.wS]) if cts else []
         for ct, r in zip(cts, allr):
             s1 = self.b.add(ct, r[0])
             s2 = self.b.add(r[1], r[2])
@@ -424,7 +476,13 @@ class EncryptedNet:
         input handles are freed unless consume=False (or amounts is empty)."""
         first = True
         for a in amounts:
-            nxt = self.b.rot_add_batch(res, a)       # x + rot(x, a), add fused into the permutation
+            steps = self._pow2_steps(a) if self.rot_policy == "pow2" else [a]
+            if len(steps) == 1:
+                nxt = self.b.rot_add_batch(res, steps[0])   # x + rot(x, a), add fused into the permutation
+            else:
+                r = self._rot_many(res, [a])
+                nxt = [self.b.add(x, rr[0]) for x, rr in zip(res, r)]
+                self._free_all([rr[0] for rr in r])
             if consume or not first:
                 self._free_all(res)
             res, first = nxt, False
@@ -463,7 +521,7 @@ class EncryptedNet:
             raise ValueError(f"replicas R={R} x block {Bk} exceed {self.slots} slots")
         reps, temp = list(cts), masked
         for t in range(int(math.log2(R))):           # copies at r * Bk (right rotations)
-            rs = self.b.rot_left_batch(reps, self.slots - (Bk << t))
+            rs = [r[0] for r in self._rot_many(reps, [self.slots - (Bk << t)])]
             nxt = [self.b.add(x, r) for x, r in zip(reps, rs)]
             self._free_all(rs + (reps if temp else []))
             reps, temp = nxt, True

@@ -98,3 +98,26 @@ def test_driver_squeezenet_sampled():
     got, _o, ref = _run_pair(SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0), oracle_layers=1)
     assert got.shape == ref.shape == (10,)
     assert np.abs(got - ref).max() <= 1e-3, np.abs(got - ref).max()
+
+
+@pytest.mark.parametrize("name", ["tiny", "lenet_small"])
+def test_driver_pow2_rotation_keys(name):
+    """NEXT-2: HEAAN's power-of-two rotation keys with composed rotations give the
+    same network within the north-star tolerance (not bit-exact: each composed rotation adds its
+    own key-switch noise), with fewer keys than CHET's exact-amount selection."""
+    from oracle import plain
+    from paper_1810_00845_b200.driver import EncryptedNet
+    net, W, img = SN.NETS[name], SN.net_weights(name), SN.net_image(name, 2)
+    ref = plain.forward(net, img, W, SN.ACT_COEFFS)
+    g = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=3, arena_bytes=8 << 30)
+    p2 = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli, rot_policy="pow2")
+    ex = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli)
+    assert len(p2["rotations"]) < len(ex["rotations"])
+    assert all(((k & (k - 1)) == 0) or (((g.slots - k) & (g.slots - k - 1)) == 0) for k in p2["rotations"])
+    g.keygen(p2["rotations"], True)
+    en = EncryptedNet(g, net, W, SN.ACT_COEFFS, rot_policy="pow2")
+    cts, lay = en.encrypt_image(img)
+    out, lo = en.forward(cts, lay)
+    got = en.decrypt_output(out, lo)
+    g.close()
+    assert np.abs(got - ref).max() <= 1e-3
