@@ -17,6 +17,8 @@
 #include <map>
 #include <string>
 #include <vector>
+#include <thread>
+#include <atomic>
 
 #include "../../include/hisa.h"
 #include "launch.h"
@@ -914,6 +916,67 @@ extern "C" int hisa_encode(hisa_ctx* c, const double* v, size_t n, double scale,
     CK(cudaStreamSynchronize(c->stream));   // host vector m must outlive the copy
     dfree(c, dm);
     *out = new_handle(c, OBJ_PT, pt, level, 1, scale);
+    return HISA_OK;
+}
+
+// count plaintexts of n_per slot values each (v row-major), encoded on all host cores (the
+// exact-rounding encoder is host code, A7), then reduced into limbs and NTT-ed on the GPU in
+// batches: the once-per-model weight / mask plaintexts of a layer in one call
+extern "C" int hisa_encode_batch(hisa_ctx* c, const double* v, size_t n_per, size_t count, double scale, int level,
+                                 hisa_pt* outs) {
+    CHECK_CTX(c);
+    if ((!v || !outs) && count) return fail(HISA_E_PARAMS, "null argument");
+    if (count == 0) return HISA_OK;
+    if (n_per > c->N / 2) return fail(HISA_E_CAPACITY, "%zu values > N/2", n_per);
+    if (level < 0) level = c->L - 1;
+    if (level >= c->L) return fail(HISA_E_PARAMS, "level %d >= L", level);
+    if (!(scale > 0) || !std::isfinite(scale)) return fail(HISA_E_PARAMS, "bad scale");
+    for (size_t i = 0; i < n_per * count; i++)
+        if (!std::isfinite(v[i])) return fail(HISA_E_PARAMS, "non-finite slot value");
+    const uint64_t N = c->N;
+    enc_tables(c);
+    if (c->enc_cosq.empty()) {   // built before the threads share it (read-only afterwards)
+        c->enc_cosq.resize(2 * N);
+        for (uint64_t e = 0; e < 2 * N; e++) c->enc_cosq[e] = cosq(M_PIq * (__float128)e / (__float128)N);
+    }
+    const int l1 = level + 1;
+    const size_t chunk = 64;
+    std::vector<int64_t> m(chunk * N);
+    int64_t* dm = dalloc_t<int64_t>(c, chunk * N);
+    if (!dm) return fail(HISA_E_OOM, "encode batch staging");
+    unsigned nth = std::max(1u, std::thread::hardware_concurrency());
+    for (size_t i0 = 0; i0 < count; i0 += chunk) {
+        const size_t nc = std::min(chunk, count - i0);
+        std::vector<int> rc(nc, HISA_OK);
+        std::vector<std::string> err(nc);
+        std::vector<std::thread> th;
+        std::atomic<size_t> next(0);
+        for (unsigned t = 0; t < std::min<size_t>(nth, nc); t++)
+            th.emplace_back([&]() {
+                std::vector<int64_t> mm;
+                for (size_t i; (i = next.fetch_add(1)) < nc;) {
+                    rc[i] = encode_coeffs(c, v + (i0 + i) * n_per, n_per, scale, mm);
+                    if (rc[i] == HISA_OK) memcpy(&m[i * N], mm.data(), N * 8);
+                    else err[i] = hisa_last_error();
+                }
+            });
+        for (auto& t : th) t.join();
+        for (size_t i = 0; i < nc; i++)
+            if (rc[i] != HISA_OK) return fail(rc[i], "%s", err[i].c_str());
+        CK(cudaMemcpyAsync(dm, m.data(), nc * N * 8, cudaMemcpyHostToDevice, c->stream));
+        uint8_t mmap[MAXL];
+        ident_map(mmap, l1);
+        std::vector<uint64_t*> pts(nc);
+        for (size_t i = 0; i < nc; i++) {
+            pts[i] = dalloc_t<uint64_t>(c, (size_t)l1 * N);
+            if (!pts[i]) return fail(HISA_E_OOM, "encode batch");
+            CK(launch_int_to_limbs(dm + i * N, pts[i], mmap, l1, c->log_n, c->d_mods, c->stream));
+        }
+        RET(ntt_fwd(c, pts.data(), (int)nc, l1, mmap));
+        CK(cudaStreamSynchronize(c->stream));   // host staging m is reused by the next chunk
+        for (size_t i = 0; i < nc; i++) outs[i0 + i] = new_handle(c, OBJ_PT, pts[i], level, 1, scale);
+    }
+    dfree(c, dm);
     return HISA_OK;
 }
 

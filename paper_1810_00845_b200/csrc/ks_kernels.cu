@@ -213,7 +213,7 @@ static cudaError_t ks_ip_pipe_t(const KsJob& job, const Tables& tb, int nz, cuda
 // one interleaved engine call (fwd_engine_f64_rowtw2, twiddles staged once in shared memory),
 // both multiplied into the same 128-bit accumulators -- then the diagonal digit (already in the
 // NTT domain) is multiplied in.  Integer-engine primes (q >= 2^50) fall back to one digit at a time.
-template <int LOG_M, int LOG_R, int MINB>
+template <int LOG_M, int LOG_R, int MINB, bool PF = false>
 __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(KsJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
@@ -272,6 +272,29 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
             mac128(acc1[k], D, __ldg(ka + i));
         }
     };
+    // prefetched form: key words of a digit loaded before the NTT stages that precede their use
+    uint64_t pkb[2][PF ? EPT : 1], pka[2][PF ? EPT : 1];
+    auto prefetch = [&](int slot, int j) {
+        if constexpr (PF) {
+            const uint64_t* kb = key_r + j * kstride_j;
+#pragma unroll
+            for (int k = 0; k < EPT; k++) {
+                pkb[slot][k] = __ldg(kb + threadIdx.x + k * NTHR);
+                pka[slot][k] = __ldg(kb + kstride_p + threadIdx.x + k * NTHR);
+            }
+        }
+    };
+    auto mac_pref = [&](const uint64_t* buf, int slot) {
+        if constexpr (PF) {
+#pragma unroll
+            for (int k = 0; k < EPT; k++) {
+                const int i = threadIdx.x + k * NTHR;
+                const uint64_t D = d_rep(__longlong_as_double((long long)buf[G::addr(0, i)]), qd.x, qd.y, qp52);
+                mac128(acc0[k], D, pkb[slot][k]);
+                mac128(acc1[k], D, pka[slot][k]);
+            }
+        }
+    };
     // digits j != ri, in pairs
     int j = 0;
     auto next_nd = [&](int from) { return from == ri ? from + 1 : from; };
@@ -285,10 +308,16 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
         if (two) {
+            if constexpr (PF) { prefetch(0, ja); prefetch(1, jb); }
             fwd_engine_f64_rowtw2<LOG_M, LOG_R>(reinterpret_cast<double*>(sa), reinterpret_cast<double*>(sb), qd.x,
                                                 qd.y, tws, t);
-            mac_tile(sa, ja, true);
-            mac_tile(sb, jb, true);
+            if constexpr (PF) {
+                mac_pref(sa, 0);
+                mac_pref(sb, 1);
+            } else {
+                mac_tile(sa, ja, true);
+                mac_tile(sb, jb, true);
+            }
             j = next_nd(jb + 1);
         } else {
             if (fp)
@@ -317,13 +346,13 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
     }
 }
 
-template <int LOG_M, int LOG_R, int MINB>
+template <int LOG_M, int LOG_R, int MINB, bool PF = false>
 static cudaError_t ks_ip2_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     using G = Geo<LOG_M, LOG_R>;
     const int rows = 1 << (tb.log_n - LOG_M);
     const size_t smem = (2 * (size_t)G::STRIDE + G::M) * sizeof(uint64_t);
     dim3 grid(rows * nz, job.l1 + 1, 1);
-    k_ks_ip2<LOG_M, LOG_R, MINB><<<grid, G::T, smem, st>>>(job, tb);
+    k_ks_ip2<LOG_M, LOG_R, MINB, PF><<<grid, G::T, smem, st>>>(job, tb);
     return cudaGetLastError();
 }
 
@@ -352,19 +381,9 @@ template <int LOG_M>
 static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     const int rows = 1 << (tb.log_n - LOG_M);
     switch (ks_variant()) {   // alternatives kept for re-measurement (profiles/r1_ks_variants.txt)
-        case 7: if (rows >= 2) return ks_ip_t<LOG_M, 2, 2, 4>(job, tb, nz, st); break;
-        case 8: if (rows >= 8) return ks_ip_t<LOG_M, 3, 8, 1>(job, tb, nz, st); break;
         case 10: return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
-        case 30: return ks_ip2_t<LOG_M, 2, 8>(job, tb, nz, st);
-        case 31: return ks_ip2_t<LOG_M, 2, 6>(job, tb, nz, st);
-        case 32: return ks_ip2_t<LOG_M, 2, 10>(job, tb, nz, st);
-        case 33: return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
-        case 34: return ks_ip2_t<LOG_M, 2, 14>(job, tb, nz, st);
-        case 35: return ks_ip2_t<LOG_M, 2, 16>(job, tb, nz, st);
         case 20: return ks_ip_pipe_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
-        case 21: return ks_ip_pipe_t<LOG_M, 2, 1, 6>(job, tb, nz, st);
-        case 22: if (rows >= 2) return ks_ip_pipe_t<LOG_M, 2, 2, 4>(job, tb, nz, st); break;
-        case 23: return ks_ip_pipe_t<LOG_M, 3, 1, 8>(job, tb, nz, st);
+        case 41: return ks_ip2_t<LOG_M, 2, 12, true>(job, tb, nz, st);
         default: break;
     }
     // default = variant 33 (measured best on B200 at N = 2^16, L = 24: one row per 64-thread CTA,

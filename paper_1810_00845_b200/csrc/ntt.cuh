@@ -21,7 +21,8 @@
 
 namespace hisa {
 
-constexpr int MAXB = 32;     // ciphertexts per batched launch (pointer arrays passed by value)
+constexpr int MAXB = 128;    // ciphertexts per batched launch (pointer arrays passed by value;
+                             // CUDA 12 kernel parameter blocks up to 32 KB)
 constexpr int MAXL = 64;     // limbs per polynomial (moduli incl. special prime)
 
 // ------------------------------------------------------------------------------------------

@@ -348,9 +348,6 @@ static cudaError_t inv_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
 #define NTT_DISPATCH(FN, ...)                                                   \
     switch (ntt_variant()) {                                                    \
         case 1: return FN<LM, 4, 1>(__VA_ARGS__);                               \
-        case 2: return FN<LM, 3, 4>(__VA_ARGS__);                               \
-        case 3: return FN<LM, 3, 6>(__VA_ARGS__);                               \
-        case 4: return FN<LM, 3, 8>(__VA_ARGS__);                               \
         default: return FN<LM, 4, 4>(__VA_ARGS__);  /* measured best: radix-16, 4 CTAs/SM */ \
     }
 template <int LM>

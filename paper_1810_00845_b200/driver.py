@@ -214,6 +214,9 @@ class Symbolic:
         self._count("encode")
         return ("pt", level, scale)
 
+    def encode_batch(self, vs, scale, level):
+        return [self.encode(v, scale, level) for v in vs]
+
     def mul_plain(self, a, p):
         lv, sc = self.cts[a]
         self._count("mul_plain")
@@ -495,8 +498,15 @@ class EncryptedNet:
         own_in = self.owned(n_in)
         lv = self._level(cts[0]) if cts else None
         if cts:   # one fused mulPlain-accumulate launch over all rows (hisa_mul_plain_accumulate)
-            pts = [self._plaintext((key, li, jo, ci), lambda jo=jo, ci=ci: vals_fn(jo, ci), lv)
-                   for jo in range(n_rows) for ci in own_in]
+            keys = [((key, li, jo, ci), lv) for jo in range(n_rows) for ci in own_in]
+            missing = [(k, jo, ci) for k, (jo, ci) in zip(keys, [(jo, ci) for jo in range(n_rows) for ci in own_in])
+                       if k not in self._pts]
+            if missing:   # the layer's weight plaintexts, encoded once per model in one batch
+                hs = self.b.encode_batch(np.stack([vals_fn(jo, ci) for _k, jo, ci in missing]),
+                                         float(self.q[lv]), lv)
+                for (k, _jo, _ci), h in zip(missing, hs):
+                    self._pts[k] = h
+            pts = [self._pts[k] for k in keys]
             sums = self.b.mul_plain_accumulate(list(cts), pts, n_rows)
         else:
             sums = [None] * n_rows

@@ -63,6 +63,7 @@ _SIGS = {
     "hisa_copy": [_vp, _cu64, _u64p],
     "hisa_free": [_vp, _cu64],
     "hisa_encode": [_vp, _dp, _csz, _cd, _ci, _u64p],
+    "hisa_encode_batch": [_vp, _dp, _csz, _csz, _cd, _ci, _u64p],
     "hisa_decode": [_vp, _cu64, _dp, _csz],
     "hisa_rot_left": [_vp, _cu64, _ci64, _u64p],
     "hisa_rot_right": [_vp, _cu64, _ci64, _u64p],
@@ -241,6 +242,17 @@ def hisa_free(ctx, h: int):
 def hisa_encode(ctx, v, scale: float, level: int = -1) -> int:
     a = np.ascontiguousarray(v, dtype=np.float64)
     return _h1(load().hisa_encode, ctx, _ptr(a, _dp), a.size, float(scale), level)
+
+
+def hisa_encode_batch(ctx, vs, scale: float, level: int = -1) -> list[int]:
+    """vs: (count, n_per) array of slot values -> count plaintext handles."""
+    a = np.ascontiguousarray(vs, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError("vs must be 2-D (count, n_per)")
+    outs = np.zeros(a.shape[0], dtype=np.uint64)
+    _chk(load().hisa_encode_batch(ctx, _ptr(a, _dp), a.shape[1], a.shape[0], float(scale), level,
+                                  _ptr(outs, _u64p)))
+    return [int(x) for x in outs]
 
 
 def hisa_decode(ctx, pt: int, n: int) -> np.ndarray:

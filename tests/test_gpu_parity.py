@@ -403,3 +403,17 @@ def test_hoisted_batch_many_cts(pair):
     for i in (0, 3, 4):
         for r, k in enumerate(ks):
             pair.same(outs[i][r], o.rot_left(os_[i], k))
+
+
+def test_encode_batch_bit_exact(pair):
+    """hisa_encode_batch (host threads + batched GPU NTT) == the oracle's exact encoder (A7),
+    including sparse weight-like vectors and a ragged slot count."""
+    g, o = pair.g, pair.o
+    rng = np.random.default_rng(11)
+    vs = rng.normal(0, 0.1, (5, 40))
+    vs[1, ::3] = 0.0
+    vs[2, :] = 0.0
+    lv = o.L - 1
+    hs = g.encode_batch(vs, float(o.q[lv]), lv)
+    for h, v in zip(hs, vs):
+        assert (g.pt_export(h) == o.encode(v, float(o.q[lv]), lv).data).all()
