@@ -36,13 +36,15 @@ __device__ __forceinline__ bool job_limb(const PassJob& job, int& a, int& b) {
 // pass-1 -> pass-2 (and pass-A -> pass-B) intermediate of such a limb is stored as centred-lazy
 // doubles (|v| <= 2q), a format only the next pass of the same modulus reads.
 // ------------------------------------------------------------------------------------------
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+
 __device__ __forceinline__ bool use_f64(uint64_t q, const Tables& tb) { return (double)q < tb.f64_max_q; }
 
 // ------------------------------------------------------------------------------------------
 // forward pass 1: columns.  Tile = Gc consecutive columns (Gc = blockDim/T), M = M1 rows.
 // Input canonical (or lifted) residues; output lazy (int: [0, 4q); FP64: centred doubles).
 // ------------------------------------------------------------------------------------------
-template <int LOG_M, int LOG_R, int LOADMODE, int MINB>
+template <int LOG_M, int LOG_R, int LOADMODE, int MINB, int GC = 0>
 __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
@@ -51,16 +53,18 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
     const int z = blockIdx.z;
     const int log_n = tb.log_n;
     const int M2 = 1 << (log_n - LOG_M);
-    const int Gc = blockDim.x / G::T;
+    // GC > 0: the tile width is a compile-time constant, so the per-element (column, row)
+    // addressing of the load / lift / store loops folds into immediates
+    const int Gc = GC > 0 ? GC : blockDim.x / G::T;
     const int col0 = blockIdx.x * Gc;
     const int mi = job.mod_map[b];
     const Mod md = tb.mods[mi];
     const bool fp = use_f64(md.q, tb);
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
-    const int nthr = blockDim.x;
+    const int nthr = GC > 0 ? GC * G::T : blockDim.x;
     // coalesced asynchronous load, lanes along columns
-    const int lg = __ffs(Gc) - 1;
+    const int lg = GC > 0 ? ilog2c(GC) : __ffs(Gc) - 1;
 #pragma unroll 4
     for (int k = 0; k < G::R; k++) {
         const int i = threadIdx.x + k * nthr;
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) 
 // ------------------------------------------------------------------------------------------
 // inverse pass B: columns; multiplies by N^-1 and fully reduces.
 // ------------------------------------------------------------------------------------------
-template <int LOG_M, int LOG_R, int MINB>
+template <int LOG_M, int LOG_R, int MINB, int GC = 0>
 __global__ void __launch_bounds__(256, MINB) k_inv_cols(PassJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
@@ -246,15 +250,15 @@ __global__ void __launch_bounds__(256, MINB) k_inv_cols(PassJob job, Tables tb) 
     const int z = blockIdx.z;
     const int log_n = tb.log_n;
     const int M2 = 1 << (log_n - LOG_M);
-    const int Gc = blockDim.x / G::T;
+    const int Gc = GC > 0 ? GC : blockDim.x / G::T;
     const int col0 = blockIdx.x * Gc;
     const int mi = job.mod_map[b];
     const Mod md = tb.mods[mi];
     const bool fp = use_f64(md.q, tb);
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
-    const int nthr = blockDim.x;
-    const int lg = __ffs(Gc) - 1;
+    const int nthr = GC > 0 ? GC * G::T : blockDim.x;
+    const int lg = GC > 0 ? ilog2c(GC) : __ffs(Gc) - 1;
 #pragma unroll 4
     for (int k = 0; k < G::R; k++) {
         const int i = threadIdx.x + k * nthr;
@@ -316,8 +320,15 @@ static cudaError_t fwd_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     int threads, gx; size_t smem;
     launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
     dim3 grid(gx, nlimbs, nz);
-    if (lift) k_fwd_cols<LOG_M, LOG_R, LOAD_LIFT, MINB><<<grid, threads, smem, st>>>(job, tb);
-    else k_fwd_cols<LOG_M, LOG_R, LOAD_PLAIN, MINB><<<grid, threads, smem, st>>>(job, tb);
+    constexpr int FULL = 256 / Geo<LOG_M, LOG_R>::T;
+    const bool full = threads == 256;
+    if (lift) {
+        if (full) k_fwd_cols<LOG_M, LOG_R, LOAD_LIFT, MINB, FULL><<<grid, threads, smem, st>>>(job, tb);
+        else k_fwd_cols<LOG_M, LOG_R, LOAD_LIFT, MINB><<<grid, threads, smem, st>>>(job, tb);
+    } else {
+        if (full) k_fwd_cols<LOG_M, LOG_R, LOAD_PLAIN, MINB, FULL><<<grid, threads, smem, st>>>(job, tb);
+        else k_fwd_cols<LOG_M, LOG_R, LOAD_PLAIN, MINB><<<grid, threads, smem, st>>>(job, tb);
+    }
     return cudaGetLastError();
 }
 template <int LOG_M, int LOG_R, int MINB>
@@ -342,7 +353,9 @@ static cudaError_t inv_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     int threads, gx; size_t smem;
     launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
     dim3 grid(gx, nlimbs, nz);
-    k_inv_cols<LOG_M, LOG_R, MINB><<<grid, threads, smem, st>>>(job, tb);
+    constexpr int FULL = 256 / Geo<LOG_M, LOG_R>::T;
+    if (threads == 256) k_inv_cols<LOG_M, LOG_R, MINB, FULL><<<grid, threads, smem, st>>>(job, tb);
+    else k_inv_cols<LOG_M, LOG_R, MINB><<<grid, threads, smem, st>>>(job, tb);
     return cudaGetLastError();
 }
 #define NTT_DISPATCH(FN, ...)                                                   \
