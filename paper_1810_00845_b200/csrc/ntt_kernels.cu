@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
 // lazy pass-1 output.  STORE_PLAIN: full reduction.  STORE_COMBINE: out = (aux - v) * comb[mod]
 // (+ add if a < aux_limit).
 // ------------------------------------------------------------------------------------------
-template <int LOG_M, int LOG_R, int STOREMODE, int MINB>
+template <int LOG_M, int LOG_R, int STOREMODE, int MINB, int FULL = 0>
 __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) 
     if (!job_limb(job, a, b)) return;
     const int z = blockIdx.z;
     const int log_n = tb.log_n;
-    const int Gr = blockDim.x / G::T;
+    const int Gr = FULL ? 256 / G::T : blockDim.x / G::T;
     const int row0 = blockIdx.x * Gr;
     const int mi = job.mod_map[b];
     const Mod md = tb.mods[mi];
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) 
     const long long off0 = (long long)row0 << LOG_M;
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
-    const int nthr = blockDim.x;
+    const int nthr = FULL ? 256 : blockDim.x;   // FULL: compile-time, offsets fold
 #pragma unroll 4
     for (int k = 0; k < G::R; k++) {
         const int i = threadIdx.x + k * nthr;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_rows(PassJob job, Tables tb) 
 // ------------------------------------------------------------------------------------------
 // inverse pass A: rows; input canonical; stores lazily (int: [0, 2q); FP64: centred doubles)
 // ------------------------------------------------------------------------------------------
-template <int LOG_M, int LOG_R, int MINB>
+template <int LOG_M, int LOG_R, int MINB, int FULL = 0>
 __global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) 
     if (!job_limb(job, a, b)) return;
     const int z = blockIdx.z;
     const int log_n = tb.log_n;
-    const int Gr = blockDim.x / G::T;
+    const int Gr = FULL ? 256 / G::T : blockDim.x / G::T;
     const int row0 = blockIdx.x * Gr;
     const int mi = job.mod_map[b];
     const Mod md = tb.mods[mi];
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) 
     const long long off0 = (long long)row0 << LOG_M;
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
-    const int nthr = blockDim.x;
+    const int nthr = FULL ? 256 : blockDim.x;   // FULL: compile-time, offsets fold
 #pragma unroll 4
     for (int k = 0; k < G::R; k++) {
         const int i = threadIdx.x + k * nthr;
@@ -336,8 +336,13 @@ static cudaError_t fwd_rows_v(const PassJob& job, const Tables& tb, int nlimbs, 
     int threads, gx; size_t smem;
     launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
     dim3 grid(gx, nlimbs, nz);
-    if (combine) k_fwd_rows<LOG_M, LOG_R, STORE_COMBINE, MINB><<<grid, threads, smem, st>>>(job, tb);
-    else k_fwd_rows<LOG_M, LOG_R, STORE_PLAIN, MINB><<<grid, threads, smem, st>>>(job, tb);
+    if (threads == 256) {
+        if (combine) k_fwd_rows<LOG_M, LOG_R, STORE_COMBINE, MINB, 1><<<grid, threads, smem, st>>>(job, tb);
+        else k_fwd_rows<LOG_M, LOG_R, STORE_PLAIN, MINB, 1><<<grid, threads, smem, st>>>(job, tb);
+    } else {
+        if (combine) k_fwd_rows<LOG_M, LOG_R, STORE_COMBINE, MINB><<<grid, threads, smem, st>>>(job, tb);
+        else k_fwd_rows<LOG_M, LOG_R, STORE_PLAIN, MINB><<<grid, threads, smem, st>>>(job, tb);
+    }
     return cudaGetLastError();
 }
 template <int LOG_M, int LOG_R, int MINB>
@@ -345,7 +350,8 @@ static cudaError_t inv_rows_v(const PassJob& job, const Tables& tb, int nlimbs, 
     int threads, gx; size_t smem;
     launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
     dim3 grid(gx, nlimbs, nz);
-    k_inv_rows<LOG_M, LOG_R, MINB><<<grid, threads, smem, st>>>(job, tb);
+    if (threads == 256) k_inv_rows<LOG_M, LOG_R, MINB, 1><<<grid, threads, smem, st>>>(job, tb);
+    else k_inv_rows<LOG_M, LOG_R, MINB><<<grid, threads, smem, st>>>(job, tb);
     return cudaGetLastError();
 }
 template <int LOG_M, int LOG_R, int MINB>
