@@ -387,6 +387,8 @@ def main():
     # FP64-pipe engine for the 50-bit q_i (24 of 25 moduli) -> the denominator is the measured
     # FP64 butterfly peak, the faster of the two engines (the int-engine peak is reported beside it)
     peak_int = ctx.microbench_butterfly(2000)
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    sm_ghz = (ck.get("sm_mhz") or 1965.0) / 1e3
     peak_bfly = max(ctx.microbench_butterfly_f64(2000), peak_int)
     dom = max(prof.items(), key=lambda kv: kv[1][0]) if prof else ("none", (0.0, 0))
     dom_name, (dom_ms, dom_n) = dom
@@ -401,6 +403,10 @@ def main():
                 "unit": "Gmodmul/s", "frac": achieved / peak_bfly if peak_bfly else None, "traffic": traffic,
                 "peak_source": "measured: hisa_microbench_butterfly_f64 (register-resident exact FP64 butterflies, "
                                "all SMs; the faster engine)", "peak_int_engine": peak_int / 1e9,
+                "peak_derived": {"fp64_engine": sm_count * 64 * sm_ghz / 11.0,
+                                 "int_engine": sm_count * 64 * sm_ghz / 20.0, "unit": "Gbutterfly/s",
+                                 "model": "148 SMs x 64 lanes/clk (FP64 pipe; IMAD on the fma pipe) x SM clock "
+                                          "/ 11 FP64 ops or ~20 IMAD per butterfly (DESIGN.md 5)"},
                 "launch_ms_avg": dom_ms / max(dom_n, 1), "share_of_step": dom_ms / total_ms,
                 "rotation_hbm": {"alg_bytes_per_step": alg_bytes_step, "achieved_gbs": hbm_gbs,
                                  "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,

@@ -28,14 +28,49 @@ class _DevArray:
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False), "version": 3}
 
 
+def _host_staged(t, group) -> bool:
+    """gloo cannot reduce CUDA tensors: stage through host memory (transport only; used by the
+    multi-process emulation of several GPUs on one device in tests/test_multigpu_emulated.py --
+    NCCL, the production transport, takes device tensors directly)."""
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def exchange(buf, per: int, group):
     """Reduce-scatter (int64 SUM) of a [world * per, ...] partial buffer: returns this rank's
     [per, ...] block (the NCCL step of a15)."""
     import torch
     import torch.distributed as dist
+    if _host_staged(buf, group):
+        torch.cuda.current_stream().synchronize()
+        out = exchange(buf.cpu(), per, group)
+        return out.to(buf.device)
     out = torch.empty((per,) + tuple(buf.shape[1:]), dtype=buf.dtype, device=buf.device)
     dist.reduce_scatter_tensor(out, buf, op=dist.ReduceOp.SUM, group=group)
     return out
+
+
+def _all_gather(out, inp, group):
+    import torch
+    import torch.distributed as dist
+    if _host_staged(inp, group):
+        torch.cuda.current_stream().synchronize()
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+        return
+    dist.all_gather_into_tensor(out, inp, group=group)
+
+
+def _all_reduce_max(t, group):
+    import torch
+    import torch.distributed as dist
+    if _host_staged(t, group):
+        c = t.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.MAX, group=group)
+        t.copy_(c)
+        return
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
 
 
 def layer_meta(en, handles, device):
@@ -48,7 +83,7 @@ def layer_meta(en, handles, device):
     else:
         lv, sc = -1, 0.0
     t = torch.tensor([float(lv), float(sc)], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=en.group)
+    _all_reduce_max(t, en.group)
     return int(t[0].item()), float(t[1].item())
 
 
@@ -129,7 +164,7 @@ def gather_outputs(en, cts, n_out: int):
     if isinstance(en.b, Symbolic):
         buf = torch.zeros((per, 1), dtype=torch.int64)
         allb = torch.zeros((en.world * per, 1), dtype=torch.int64)
-        dist.all_gather_into_tensor(allb, buf, group=en.group)
+        _all_gather(allb, buf, en.group)
         return [en.b.fresh(lv, sc) for _ in range(n_out)]
     N = 2 * en.slots
     words = 2 * (lv + 1) * N
@@ -138,5 +173,5 @@ def gather_outputs(en, cts, n_out: int):
         ptr, w = en.b.ct_device_view(h)
         buf[i].copy_(torch.as_tensor(_DevArray(ptr, w), device=dev))
     allb = torch.empty((en.world * per, words), dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(allb, buf, group=en.group)
+    _all_gather(allb, buf, en.group)
     return [en.b.ct_adopt_device(allb[j].data_ptr(), lv, 2, sc) for j in range(n_out)]
