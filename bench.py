@@ -260,6 +260,45 @@ def measure_inference(name, device, reps=3, rot_policy="exact"):
             "kernel_share": {n: round(v[0] / total, 4) for n, v in top}}
 
 
+def measure_inference_sharded(name, local, dist, reps=2):
+    """Encrypted inference over all ranks: every linear layer's input channels sharded,
+    one reduce-scatter per linear layer, final all-gather; latency = max over ranks (CUDA events)."""
+    import torch
+    from synth import nets as SN
+    from paper_1810_00845_b200 import hisa as H
+    from paper_1810_00845_b200.driver import EncryptedNet
+    net, W, img = SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0)
+    torch.cuda.empty_cache()
+    ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=local, arena_bytes=64 << 30)
+    plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli)
+    ctx.keygen(plan["rotations"], True)
+    en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS, group=dist.group.WORLD)
+    stream = torch.cuda.current_stream(local)
+    lat = []
+    for r in range(reps + 1):                    # first pass encodes the weight plaintexts
+        cts, lay = en.encrypt_image(img)
+        mine = en.shard_input(cts)
+        ctx.sync()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out, lo = en.forward_gathered(mine, lay)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / 1e3], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if r:
+            lat.append(float(t.item()))
+        for h in out + mine:
+            ctx.free(h)
+    ctx.close()
+    ctx = None
+    torch.cuda.empty_cache()
+    return {"config": name, "latency_s": min(lat), "unit": "s", "n_gpus": dist.get_world_size(), "reps": reps,
+            "sharding": "input channels of every linear layer; NCCL reduce-scatter of int64 partial sums per "
+                        "layer; final all-gather (SURVEY 8e)"}
+
+
 def _hbm_peak():
     hbm_peak = 6549.8
     mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -339,7 +378,10 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        import datetime
+        # bounded collectives: a failing sharded-inference run must not hang the whole bench
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"),
+                                timeout=datetime.timedelta(seconds=300))
     B, L, log_n = a.batch, a.limbs, a.log_n
     N = 1 << log_n
     k = synth.rot_amount(a.seed, log_n, L)
@@ -515,7 +557,17 @@ def main():
     ctx.close()
     ctx = None
     torch.cuda.empty_cache()
+    sharded = None
+    if world > 1 and not a.no_inference:
+        sharded = []
+        for nm in [n for n in a.nets.split(",") if n]:
+            try:
+                sharded.append(measure_inference_sharded(nm, local, dist))
+            except Exception as exc:   # the rotation line must survive a failing network run
+                sharded.append({"config": nm, "error": f"{type(exc).__name__}: {exc}"[:300]})
     if rank == 0:
+        if sharded is not None:
+            line["inference"] = sharded
         if not a.no_inference and world == 1:
             line["inference"] = [measure_inference(nm, local) for nm in a.nets.split(",") if nm]
             # NEXT-2: CHET's exact rotation keys vs HEAAN's power-of-two keys with
