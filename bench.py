@@ -269,7 +269,8 @@ def measure_inference_sharded(name, local, dist, reps=2):
     from paper_1810_00845_b200.driver import EncryptedNet
     net, W, img = SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0)
     torch.cuda.empty_cache()
-    ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=local, arena_bytes=64 << 30)
+    arena = int(float(os.environ.get("HISA_BENCH_ARENA_GB", "64")) * (1 << 30))
+    ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=local, arena_bytes=arena)
     plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli)
     ctx.keygen(plan["rotations"], True)
     en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS, group=dist.group.WORLD)
@@ -286,7 +287,7 @@ def measure_inference_sharded(name, local, dist, reps=2):
         e1.record(stream)
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) / 1e3], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _allreduce_max(t)
         if r:
             lat.append(float(t.item()))
         for h in out + mine:
@@ -297,6 +298,17 @@ def measure_inference_sharded(name, local, dist, reps=2):
     return {"config": name, "latency_s": min(lat), "unit": "s", "n_gpus": dist.get_world_size(), "reps": reps,
             "sharding": "input channels of every linear layer; NCCL reduce-scatter of int64 partial sums per "
                         "layer; final all-gather (SURVEY 8e)"}
+
+
+def _allreduce_max(t):
+    """MAX all-reduce of a device scalar (NCCL directly; gloo via host memory)."""
+    import torch.distributed as dist
+    if dist.get_backend() == "gloo" and t.is_cuda:
+        c = t.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
 
 
 def _hbm_peak():
@@ -374,18 +386,22 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("HISA_BENCH_SHARED_DEVICE"):   # emulation on one GPU (tests only)
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         import datetime
         # bounded collectives: a failing sharded-inference run must not hang the whole bench
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"),
+        backend = os.environ.get("HISA_BENCH_BACKEND", "nccl")   # gloo: one-GPU emulation (tests only)
+        dist.init_process_group(backend, device_id=torch.device(f"cuda:{local}") if backend == "nccl" else None,
                                 timeout=datetime.timedelta(seconds=300))
     B, L, log_n = a.batch, a.limbs, a.log_n
     N = 1 << log_n
     k = synth.rot_amount(a.seed, log_n, L)
-    ctx = H.Context(log_n, [50] * L, 60, seed=a.seed, device=local)
+    arena = int(float(os.environ["HISA_BENCH_ARENA_GB"]) * (1 << 30)) if os.environ.get("HISA_BENCH_ARENA_GB") else None
+    ctx = H.Context(log_n, [50] * L, 60, seed=a.seed, device=local, arena_bytes=arena)
     ctx.keygen([k], False)
     cts = [ctx.ct_random(rank * B + b, L - 1) for b in range(B)]
     ctx.sync()
@@ -421,7 +437,7 @@ def main():
     ms_max = ms
     if dist:
         t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _allreduce_max(t)
         ms_max = float(t.item())
     value = world * B * a.steps / (ms_max / 1e3)
 
@@ -522,7 +538,7 @@ def main():
         ctx.free(ref)
         if dist:
             t = torch.tensor([dt], device=f"cuda:{local}", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            _allreduce_max(t)
             dt = float(t.item())
         e2e = {"value": world * B * n_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": B * words * 8,
                "d2h_bytes_per_step": B * words * 8, "steps": n_e2e,
@@ -538,7 +554,7 @@ def main():
         hoisted = measure_hoisted(ctx, cts[:2], amounts, max(2, a.steps // 2), a.warmup, log_n, L, stream)
         if dist:
             t = torch.tensor([hoisted["ms_per_step"]], device=f"cuda:{local}", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            _allreduce_max(t)
             hoisted["value"] = world * len(cts[:2]) * len(amounts) / (float(t.item()) / 1e3)
 
     cpu = None
