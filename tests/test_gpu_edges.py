@@ -1,0 +1,100 @@
+"""Edge cases of the C-ABI path (GPU): empty batches, level-0 ciphertexts (a key switch with a
+single digit), the smallest ring (N = 2^8), a large key-switch (N = 2^16, L = 40 limbs: 40 digits,
+3.4 GB key) sampled against the oracle, ragged slot counts, in-place forms and handle reuse."""
+import numpy as np
+import pytest
+
+from oracle.ckks import Oracle
+
+pytestmark = pytest.mark.gpu
+
+H = pytest.importorskip("paper_1810_00845_b200.hisa")
+
+
+def _pair(log_n, qb, pb, rots, seed=21, arena=4 << 30):
+    g = H.Context(log_n, qb, pb, seed=seed, arena_bytes=arena)
+    o = Oracle(log_n, qb, pb, seed=seed)
+    g.keygen(rots, True)
+    o.keygen(rot_amounts=rots)
+    return g, o
+
+
+def test_empty_batches_are_noops():
+    g, o = _pair(10, [60, 40], 60, [1])
+    assert g.rot_left_batch([], 1) == []
+    assert g.rot_left_hoisted_batch([], [1, 2]) == []
+    assert g.rescale_batch([]) == []
+    assert g.mul_batch([], []) == []
+    assert g.rot_add_batch([], 1) == []
+    a = g.ct_random(1, 1)
+    assert g.rot_left_hoisted(a, []) == []
+    assert g.encode_batch(np.zeros((0, 4)), 2.0 ** 40) == []
+    with pytest.raises(H.HisaError) as ei:           # more values than slots
+        g.encode_batch(np.zeros((2, g.slots + 1)), 2.0 ** 40)
+    assert ei.value.code == "CAPACITY"
+    g.close()
+
+
+def test_level_zero_keyswitch_and_smallest_ring():
+    """N = 2^8 (the smallest supported ring) and level 0: one digit, the key switch is
+    ModUp to {q_0, p}, inner product, ModDown."""
+    g, o = _pair(8, [60, 40, 40], 60, [1, 5])
+    a = g.ct_random(3, 0)
+    oa = o.bench_ct(3, 0)
+    for k in (1, 5):
+        assert (g.ct_export(g.rot_left(a, k)) == o.rot_left(oa, k).data).all()
+    t = g.mul_norelin(a, a)
+    g.relinearize(t)
+    assert (g.ct_export(t) == o.relinearize(o.mul_norelin(oa, oa)).data).all()
+    with pytest.raises(H.HisaError) as ei:
+        g.rescale(a)
+    assert ei.value.code == "MODULUS_EXHAUSTED"
+    hz = g.rot_left_hoisted(a, [1, 5, 0])
+    assert (g.ct_export(hz[1]) == o.rot_left(oa, 5).data).all()
+    assert (g.ct_export(hz[2]) == oa.data).all()
+    g.close()
+
+
+def test_ragged_and_full_slot_counts():
+    g, o = _pair(11, [60, 40], 60, [])
+    for n in (1, 3, 1023, 1024):
+        z = np.random.default_rng(n).uniform(-1, 1, n)
+        hp = g.encode(z, 2.0 ** 30)
+        assert (g.pt_export(hp) == o.encode(z, 2.0 ** 30).data).all()
+        assert np.abs(g.decode(hp, n) - z).max() < 1e-6
+    g.close()
+
+
+def test_inplace_forms_and_handle_reuse():
+    g, o = _pair(10, [60, 40, 40], 60, [2])
+    a, b = g.ct_random(4, 2), g.ct_random(5, 2)
+    oa, ob = o.bench_ct(4, 2), o.bench_ct(5, 2)
+    h = g.copy(a)
+    assert g.add(h, b, inplace=True) == h
+    assert (g.ct_export(h) == o.add(oa, ob).data).all()
+    g.rot_left(h, 2, inplace=True)
+    assert (g.ct_export(h) == o.rot_left(o.add(oa, ob), 2).data).all()
+    g.free(h)
+    for _ in range(50):            # slot reuse: generations make stale handles detectable
+        x = g.copy(a)
+        g.free(x)
+        with pytest.raises(H.HisaError) as ei:
+            g.ct_info(x)
+        assert ei.value.code == "INVALID_HANDLE"
+    g.close()
+
+
+@pytest.mark.slow
+def test_large_keyswitch_sampled():
+    """N = 2^16 with 40 x 50-bit limbs (dnum = 40): a 40-digit key switch, 3.4 GB key, bit-exact
+    with the oracle on one ciphertext; hoisted and batched paths agree with it."""
+    L = 40
+    g, o = _pair(16, [50] * L, 60, [7, 11], seed=2, arena=40 << 30)
+    a = g.ct_random(9, L - 1)
+    oa = o.bench_ct(9, L - 1)
+    want = o.rot_left(oa, 7).data
+    assert (g.ct_export(g.rot_left(a, 7)) == want).all()
+    hz = g.rot_left_hoisted(a, [7, 11])
+    assert (g.ct_export(hz[0]) == want).all()
+    assert (g.ct_export(g.rot_left_batch([a, a], 7)[1]) == want).all()
+    g.close()
