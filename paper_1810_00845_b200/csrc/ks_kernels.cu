@@ -232,7 +232,7 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
     const Mod md = tb.mods[mi];
     const bool fp = (double)md.q < tb.f64_max_q;
     const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
-    const double qp52 = __dadd_rn(qd.x, 4503599627370496.0);
+    const double tq52 = __dadd_rn(2.0 * qd.x, 4503599627370496.0);   // 2q + 2^52
     constexpr int NTHR = G::T;
     constexpr int EPT = G::R;
     U128 acc0[EPT], acc1[EPT];
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
         for (int k = 0; k < EPT; k++) {
             const int i = threadIdx.x + k * NTHR;
             uint64_t D = buf[G::addr(0, i)];
-            if (conv) D = d_rep(__longlong_as_double((long long)D), qd.x, qd.y, qp52);   // < 1.5q
+            if (conv) D = d_rep4(__longlong_as_double((long long)D), tq52);   // in [0, 4q]
             mac128(acc0[k], D, __ldg(kb + i));
             mac128(acc1[k], D, __ldg(ka + i));
         }
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
 #pragma unroll
             for (int k = 0; k < EPT; k++) {
                 const int i = threadIdx.x + k * NTHR;
-                const uint64_t D = d_rep(__longlong_as_double((long long)buf[G::addr(0, i)]), qd.x, qd.y, qp52);
+                const uint64_t D = d_rep4(__longlong_as_double((long long)buf[G::addr(0, i)]), tq52);
                 mac128(acc0[k], D, pkb[slot][k]);
                 mac128(acc1[k], D, pka[slot][k]);
             }

@@ -66,6 +66,13 @@ __device__ __forceinline__ uint64_t d_rep(double v, double q, double qinv, doubl
     return (uint64_t)__double_as_longlong(__dadd_rn(r, q_plus_2p52)) & 0xFFFFFFFFFFFFFull;
 }
 
+// a forward-engine output (|v| <= 2q, the fixed point above) -> uint64 representative in [0, 4q]
+// with one add: v + 2q + 2^52 is exact (< 2^53) and its low 52 bits are v + 2q.  For the 128-bit
+// key inner-product accumulation (products < 4 q^2 < 2^102, sums of <= 64 of them < 2^108).
+__device__ __forceinline__ uint64_t d_rep4(double v, double two_q_plus_2p52) {
+    return (uint64_t)__double_as_longlong(__dadd_rn(v, two_q_plus_2p52)) & 0xFFFFFFFFFFFFFull;
+}
+
 // forward CT stages [s0, s0 + LOG_M) on doubles in smem; mirrors fwd_engine (ntt.cuh) with
 // the FP64 butterfly; tw = doubles W = psi^brv(k) mod q
 template <int LOG_M, int LOG_R>
