@@ -107,12 +107,55 @@ class OracleNet:
     """The network on the oracle: keys for exactly the rotation amounts the lowering uses
     (the compiler's rotation-key selection)."""
 
-    def __init__(self, net: dict, weights, act_coeffs, seed: int = 0, nthreads=None):
+    def __init__(self, net: dict, weights, act_coeffs, seed: int = 0, nthreads=None, rot_policy: str = "exact"):
+        """rot_policy "exact": one key per distinct amount; "pow2": HEAAN's default
+        power-of-two keys, every rotation by k composed, least significant digit
+        first, from the non-adjacent form of k -- or of k - N/2 (right rotations) when that one
+        has strictly fewer non-zero digits."""
         self.net = net
+        self.rot_policy = rot_policy
         self.o = Oracle(net["log_n"], net["q_bits"], net["p_bits"], seed=seed, nthreads=nthreads)
         self.folded, self.gamma = fold(net, weights, act_coeffs)
-        self.amounts = sorted(self._rotation_amounts())
+        wanted = self._rotation_amounts()
+        if rot_policy == "pow2":
+            wanted = {st for k in wanted for st in self._steps(k)}
+        self.amounts = sorted(wanted)
         self.o.keygen(rot_amounts=self.amounts, relin=True)
+
+    def _steps(self, k):
+        s = self.o.slots
+        k %= s
+        if k == 0:
+            return []
+
+        def naf_digits(v):                       # signed-binary digits, least significant first
+            digits = []
+            pos = 0
+            while v != 0:
+                if v % 2 == 0:
+                    d = 0
+                else:
+                    d = 2 - (v % 4)              # v = 1 mod 4 -> +1, v = 3 mod 4 -> -1
+                    v -= d
+                if d:
+                    digits.append(d * 2 ** pos)
+                v //= 2
+                pos += 1
+            return digits
+        a, b = naf_digits(k), naf_digits(k - s)
+        return [d % s for d in (b if len(b) < len(a) else a)]
+
+    def _rot(self, ct, k):
+        """rotLeft under the key policy: one key switch (exact) or the composition (pow2)."""
+        o = self.o
+        if self.rot_policy == "exact":
+            return o.rot_left(ct, k)
+        steps = self._steps(k)
+        if not steps:
+            return o.copy(ct)
+        for st in steps:
+            ct = o.rot_left(ct, st)
+        return ct
 
     # ---- layout walk (same walk as forward, metadata only) -------------------------------
     def _input_layout(self):
@@ -211,7 +254,7 @@ class OracleNet:
         for ic in range(lay.C):
             for i in range(k):
                 for j in range(k):
-                    rotated[ic, i, j] = o.rot_left(cts[ic], lay.origin + (i - p) * lay.hS + (j - p) * lay.wS)
+                    rotated[ic, i, j] = self._rot(cts[ic], lay.origin + (i - p) * lay.hS + (j - p) * lay.wS)
         outs = []
         for oc in range(oc_n):
             acc = None                                   # zeroCipher (A21)
@@ -243,9 +286,9 @@ class OracleNet:
         o = self.o
         out = []
         for ct in cts:
-            y = o.add(ct, o.rot_left(ct, lay.wS))
-            y = o.add(y, o.rot_left(ct, lay.hS))
-            y = o.add(y, o.rot_left(ct, lay.hS + lay.wS))
+            y = o.add(ct, self._rot(ct, lay.wS))
+            y = o.add(y, self._rot(ct, lay.hS))
+            y = o.add(y, self._rot(ct, lay.hS + lay.wS))
             out.append(y)
         return out, Layout("hw", lay.C, lay.H // 2, lay.W // 2, lay.hS * 2, lay.wS * 2, lay.origin, False)
 
@@ -261,7 +304,7 @@ class OracleNet:
         for ct in cts:
             y = ct
             for t in range(int(math.log2(R))):
-                y = o.add(y, o.rot_right(y, bk * 2 ** t))
+                y = o.add(y, self._rot(y, o.slots - bk * 2 ** t))      # right rotation
             ys.append(y)
         sl = lay.valid_slots()
         hw = lay.H * lay.W
@@ -280,7 +323,7 @@ class OracleNet:
                 acc = term if acc is None else o.add(acc, term)
             acc = o.rescale(acc)
             for t in range(int(math.log2(bk))):
-                acc = o.add(acc, o.rot_left(acc, 2 ** t))
+                acc = o.add(acc, self._rot(acc, 2 ** t))
             if beta:
                 acc = o.add_scalar(acc, beta)
             outs.append(acc)
@@ -304,7 +347,7 @@ class OracleNet:
                     acc = term if acc is None else o.add(acc, term)
                 acc = o.rescale(acc)
                 for t in range(int(math.log2(lay.R))):
-                    acc = o.add(acc, o.rot_left(acc, lay.Bk * 2 ** t))
+                    acc = o.add(acc, self._rot(acc, lay.Bk * 2 ** t))
                 if beta:
                     acc = o.add_scalar(acc, beta)
                 outs.append(acc)
@@ -324,7 +367,7 @@ class OracleNet:
                     acc = term if acc is None else o.add(acc, term)
                 acc = o.rescale(acc)
                 for t in range(steps):
-                    acc = o.add(acc, o.rot_left(acc, 1 << t))
+                    acc = o.add(acc, self._rot(acc, 1 << t))
                 if beta:
                     acc = o.add_scalar(acc, beta)
                 outs.append(acc)
@@ -358,9 +401,9 @@ class OracleNet:
         for ct in cts:
             acc = ct
             for t in range(int(math.log2(lay.W))):
-                acc = o.add(acc, o.rot_left(acc, lay.wS * 2 ** t))
+                acc = o.add(acc, self._rot(acc, lay.wS * 2 ** t))
             for t in range(int(math.log2(lay.H))):
-                acc = o.add(acc, o.rot_left(acc, lay.hS * 2 ** t))
+                acc = o.add(acc, self._rot(acc, lay.hS * 2 ** t))
             out.append(acc)
         return out, Layout("slot0", lay.C, 1, 1)
 

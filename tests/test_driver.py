@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 H = pytest.importorskip("paper_1810_00845_b200.hisa")
 
 
-def _run_pair(net, W, img, oracle_layers=None):
+def _run_pair(net, W, img, oracle_layers=None, rot_policy="exact"):
     """GPU driver vs the oracle's lowering on identical seeded inputs; returns the decrypted
     GPU output, the oracle's (None if the oracle stops early) and the float64 reference."""
     from oracle import plain
@@ -19,17 +19,17 @@ def _run_pair(net, W, img, oracle_layers=None):
     from paper_1810_00845_b200.driver import EncryptedNet
 
     ref = plain.forward(net, img, W, SN.ACT_COEFFS)
-    on = OracleNet(net, W, SN.ACT_COEFFS, seed=0)
+    on = OracleNet(net, W, SN.ACT_COEFFS, seed=0, rot_policy=rot_policy)
     ocs, olay = on.encrypt_image(img)
     otrace = []
     ocs_out, olay_out = on.forward(ocs, olay, trace=otrace, stop_after=oracle_layers)
 
     g = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, arena_bytes=96 << 30)
     assert g.moduli == on.o.moduli
-    plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli)
+    plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli, rot_policy=rot_policy)
     assert plan["rotations"] == on.amounts          # the compiler's key selection
     g.keygen(plan["rotations"], True)
-    en = EncryptedNet(g, net, W, SN.ACT_COEFFS)
+    en = EncryptedNet(g, net, W, SN.ACT_COEFFS, rot_policy=rot_policy)
     cts, lay = en.encrypt_image(img)
     for h, oc in zip(cts, ocs):
         assert (g.ct_export(h) == oc.data).all(), "input encryption parity"
@@ -102,22 +102,18 @@ def test_driver_squeezenet_sampled():
 
 @pytest.mark.parametrize("name", ["tiny", "lenet_small"])
 def test_driver_pow2_rotation_keys(name):
-    """NEXT-2: HEAAN's power-of-two rotation keys with composed rotations give the
-    same network within the north-star tolerance (not bit-exact: each composed rotation adds its
-    own key-switch noise), with fewer keys than CHET's exact-amount selection."""
-    from oracle import plain
+    """NEXT-2: HEAAN's power-of-two rotation keys with composed rotations: the GPU
+    driver and the oracle's independent composition agree bit for bit after every layer, use
+    fewer keys than CHET's exact-amount selection, and decrypt within the north-star tolerance."""
     from paper_1810_00845_b200.driver import EncryptedNet
-    net, W, img = SN.NETS[name], SN.net_weights(name), SN.net_image(name, 2)
-    ref = plain.forward(net, img, W, SN.ACT_COEFFS)
-    g = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=3, arena_bytes=8 << 30)
-    p2 = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli, rot_policy="pow2")
-    ex = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli)
+    from oracle.ckks import Oracle
+    net, W = SN.NETS[name], SN.net_weights(name)
+    mod = Oracle(net["log_n"], net["q_bits"], net["p_bits"]).moduli
+    p2 = EncryptedNet.plan(net, W, SN.ACT_COEFFS, mod, rot_policy="pow2")
+    ex = EncryptedNet.plan(net, W, SN.ACT_COEFFS, mod)
+    s = (1 << net["log_n"]) // 2
     assert len(p2["rotations"]) < len(ex["rotations"])
-    assert all(((k & (k - 1)) == 0) or (((g.slots - k) & (g.slots - k - 1)) == 0) for k in p2["rotations"])
-    g.keygen(p2["rotations"], True)
-    en = EncryptedNet(g, net, W, SN.ACT_COEFFS, rot_policy="pow2")
-    cts, lay = en.encrypt_image(img)
-    out, lo = en.forward(cts, lay)
-    got = en.decrypt_output(out, lo)
-    g.close()
+    assert all(((k & (k - 1)) == 0) or (((s - k) & (s - k - 1)) == 0) for k in p2["rotations"])
+    got, ogot, ref = _run_pair(net, W, SN.net_image(name, 2), rot_policy="pow2")
     assert np.abs(got - ref).max() <= 1e-3
+    assert np.abs(got - ogot).max() < 1e-9

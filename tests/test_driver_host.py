@@ -298,3 +298,27 @@ def test_multirank_gloo_world2():
     assert hoisted == single["counts"]["rot_hoisted"]
     mulp = sum(got[r]["counts"].get("mul_plain", 0) for r in range(world))
     assert mulp == single["counts"]["mul_plain"]
+
+
+def test_oracle_pow2_policy_matches_float64_and_planner():
+    """NEXT-2 pin: the oracle's power-of-two composition (signed-binary digits) decrypts within
+    1e-3 of the float64 network on every lowering branch, its key set is powers of two (left or
+    right), and the product planner selects the same keys."""
+    from oracle import plain
+    from oracle.nets import OracleNet
+    from paper_1810_00845_b200.driver import EncryptedNet
+    W = _mini_weights()
+    img = SN._image(5, MINI["input"])
+    on = OracleNet(MINI, W, SN.ACT_COEFFS, rot_policy="pow2")
+    s = on.o.slots
+    assert all((k & (k - 1)) == 0 or ((s - k) & (s - k - 1)) == 0 for k in on.amounts)
+    # composition is exact in Z_s: the steps of every amount sum to it
+    for k in (1, 3, 7, 13, 31, s - 3, s // 2 + 5):
+        assert sum(on._steps(k)) % s == k % s
+    cts, lay = on.encrypt_image(img)
+    out, ol = on.forward(cts, lay)
+    got = on.decrypt_output(out, ol)
+    ref = plain.forward(MINI, img, W, SN.ACT_COEFFS)
+    assert np.abs(got - ref).max() <= 1e-3
+    pl = EncryptedNet.plan(MINI, W, SN.ACT_COEFFS, on.o.moduli, rot_policy="pow2")
+    assert pl["rotations"] == on.amounts
