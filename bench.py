@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-inference", action="store_true")
     ap.add_argument("--hoist-r", type=int, default=8, help="rotation amounts per hoisted ModUp")
     ap.add_argument("--nets", default="tiny,lenet_small", help="encrypted-inference configs to time")
+    ap.add_argument("--tiling", default="lenet_large",
+                    help="config whose HW-tiled vs CHW-tiled (config + '_chw') latencies are compared ('' = skip)")
     ap.add_argument("--policy-net", default="lenet_small",
                     help="config on which exact vs power-of-two rotation keys are compared ('' = skip)")
     return ap.parse_args()
@@ -586,6 +588,15 @@ def main():
             line["inference"] = sharded
         if not a.no_inference and world == 1:
             line["inference"] = [measure_inference(nm, local) for nm in a.nets.split(",") if nm]
+            # NEXT-1: HW tiling vs CHW tiling of the second conv (the paper's layout
+            # comparison, Fig. tilings)
+            if a.tiling:
+                hw = next((i for i in line["inference"] if i["config"] == a.tiling), None) or \
+                    measure_inference(a.tiling, local)
+                chw = measure_inference(a.tiling + "_chw", local)
+                line["tiling"] = {"config": a.tiling, "hw_s": hw["latency_s"], "chw_s": chw["latency_s"],
+                                  "speedup_chw_over_hw": hw["latency_s"] / chw["latency_s"],
+                                  "chw_first_pass_incl_weight_encoding_s": chw["first_pass_incl_weight_encoding_s"]}
             # NEXT-2: CHET's exact rotation keys vs HEAAN's power-of-two keys with
             # composed rotations (the paper's Fig. rotopt: 1.43-2.07x on CPU HEAAN)
             if a.policy_net:

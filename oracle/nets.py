@@ -41,6 +41,14 @@ Lowering readings, in the order t
   fire     (config 5, A33) squeeze = conv 1x1 + act; mask (the 3x3 expand's SAME padding needs
            zeros); e1 = conv 1x1 + act and e3 = conv 3x3 SAME + act on the masked
            squeeze output; output channels = e1 then e3 (concatenation is metadata).
+  conv CHW (NEXT-1; layer field "chw", stride 1): mask if not clean; block stride
+           CS = 2^ceil(log2(span + 2 pad_off)) with pad_off = p hS + p wS, G = (N/2) / CS channels
+           per ciphertext; channel c goes to ciphertext c // G, block g = c % G, by a right
+           rotation of g CS + pad_off - origin, and the channels of a ciphertext are added; per
+           packed ciphertext and tap (i, j): rotLeft by (i - p) hS + (j - p) wS; per output channel:
+           sum over (packed ciphertext, tap) of mulPlain with W'[oc, c, i, j] on block g's valid
+           slots (scale q_top), rescale, acc += rot(acc, CS 2^t) for t < log2 G, add beta.
+           Output: HW layout, origin pad_off (block 0), not clean.
   gap      global average pool: acc += rot(acc, wS 2^t) (t < log2 W), then hS 2^t (t < log2 H);
            slot 0 holds the sum; 1/(H W) folded into the preceding linear layer (A26).
 """
@@ -79,7 +87,7 @@ def fold(net: dict, weights, act_coeffs):
             pools += 1
             h, w_ = h // 2, w_ // 2
         if layer[0] == "conv":
-            _, _oc, k, st, p = layer
+            _, _oc, k, st, p = layer[:5]
             h, w_ = (h + 2 * p - k) // st + 1, (w_ + 2 * p - k) // st + 1
         if layer[0] in ("conv", "fc"):
             if layer[0] == "fc":
@@ -171,8 +179,21 @@ class OracleNet:
         amts = set()
         for layer in self.net["layers"]:
             kind = layer[0]
-            if kind == "conv":
-                _, oc, k, st, p = layer
+            if kind == "conv" and len(layer) > 5 and layer[5] == "chw":
+                _, oc, k, st, p = layer[:5]
+                pad_off = p * lay.hS + p * lay.wS
+                span = (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+                cs = 2 ** math.ceil(math.log2(span + 2 * pad_off))
+                G = max(1, s // cs)
+                for g in range(min(G, lay.C)):
+                    amts.add((s - (g * cs + pad_off - lay.origin) % s) % s)
+                for i in range(k):
+                    for j in range(k):
+                        amts.add(((i - p) * lay.hS + (j - p) * lay.wS) % s)
+                amts.update(cs * 2 ** t for t in range(int(math.log2(G))))
+                lay = Layout("hw", oc, lay.H, lay.W, lay.hS, lay.wS, pad_off, False)
+            elif kind == "conv":
+                _, oc, k, st, p = layer[:5]
                 for i in range(k):
                     for j in range(k):
                         amts.add((lay.origin + (i - p) * lay.hS + (j - p) * lay.wS) % s)
@@ -246,8 +267,10 @@ class OracleNet:
 
     def conv(self, cts, lay, layer, w, beta):
         """Alg. 1 with the rotations code-motioned out of the oc loop."""
+        if len(layer) > 5 and layer[5] == "chw":
+            return self.conv_chw(cts, lay, layer, w, beta)
         o = self.o
-        _, oc_n, k, st, p = layer
+        _, oc_n, k, st, p = layer[:5]
         if p > 0 and not lay.clean:
             cts, lay = self._mask(cts, lay)
         rotated = {}
@@ -270,6 +293,59 @@ class OracleNet:
         nl = Layout("hw", oc_n, (lay.H + 2 * p - k) // st + 1, (lay.W + 2 * p - k) // st + 1,
                     lay.hS * st, lay.wS * st, 0, False)
         return outs, nl
+
+    def conv_chw(self, cts, lay, layer, w, beta):
+        o = self.o
+        _, oc_n, k, st, p = layer[:5]
+        assert st == 1, "CHW conv: stride 1"
+        if not lay.clean:
+            cts, lay = self._mask(cts, lay)
+        s = o.slots
+        pad_off = p * lay.hS + p * lay.wS
+        span = (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+        cs = 2 ** math.ceil(math.log2(span + 2 * pad_off))
+        G = max(1, s // cs)
+        C = lay.C
+        npk = -(-C // G)
+        packed = []
+        for kk in range(npk):
+            acc = None
+            for g in range(G):
+                c = kk * G + g
+                if c >= C:
+                    break
+                shift = (g * cs + pad_off - lay.origin) % s
+                r = self._rot(cts[c], (s - shift) % s)
+                acc = r if acc is None else o.add(acc, r)
+            packed.append(acc)
+        rel = [y * lay.hS + x * lay.wS for y in range(lay.H) for x in range(lay.W)]
+        rot = {}
+        for kk in range(npk):
+            for i in range(k):
+                for j in range(k):
+                    rot[kk, i, j] = self._rot(packed[kk], (i - p) * lay.hS + (j - p) * lay.wS)
+        outs = []
+        for oc in range(oc_n):
+            acc = None
+            for kk in range(npk):
+                for i in range(k):
+                    for j in range(k):
+                        v = np.zeros(s)
+                        for g in range(G):
+                            c = kk * G + g
+                            if c < C:
+                                for r_ in rel:
+                                    v[g * cs + pad_off + r_] = w[oc, c, i, j]
+                        x = rot[kk, i, j]
+                        term = o.mul_plain(x, o.encode(v, float(o.q[x.level]), x.level))
+                        acc = term if acc is None else o.add(acc, term)
+            acc = o.rescale(acc)
+            for t in range(int(math.log2(G))):
+                acc = o.add(acc, self._rot(acc, cs * 2 ** t))
+            if beta:
+                acc = o.add_scalar(acc, beta)
+            outs.append(acc)
+        return outs, Layout("hw", oc_n, lay.H, lay.W, lay.hS, lay.wS, pad_off, False)
 
     def act(self, cts, lay, square_only=False):
         o = self.o

@@ -52,7 +52,7 @@ def forward(net: dict, image: np.ndarray, weights, act_coeffs) -> np.ndarray:
     for layer in net["layers"]:
         kind = layer[0]
         if kind == "conv":
-            _, _oc, _k, s, p = layer
+            _, _oc, _k, s, p = layer[:5]
             x = conv2d(x, weights[wi], s, p)
             wi += 1
         elif kind == "act":

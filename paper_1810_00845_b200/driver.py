@@ -85,7 +85,7 @@ def compile_weights(net: dict, weights, act_coeffs):
         elif kind in ("conv", "fc"):
             nxt = layers[i + 1][0] if i + 1 < len(layers) else None
             if kind == "conv":
-                _, oc, k, st, p = layer
+                _, oc, k, st, p = layer[:5]
                 h, w = (h + 2 * p - k) // st + 1, (w + 2 * p - k) // st + 1
                 c = oc
             else:
@@ -375,9 +375,103 @@ class EncryptedNet:
         self._free_all(ms)
         return out, replace(lay, clean=True)
 
+    @staticmethod
+    def chw_geometry(lay, k, p, slots):
+        """CHW tiling of a stride-1 conv input (NEXT-1): channel block stride CS (a power of two
+        holding the plane plus the SAME padding on both sides), channels per ciphertext G, data
+        offset of a channel inside its block."""
+        pad_off = p * lay.hS + p * lay.wS
+        span = (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+        cs = 1 << math.ceil(math.log2(span + 2 * pad_off))
+        return cs, max(1, slots // cs), pad_off
+
+    def conv_chw(self, cts, lay, layer, w, beta, li):
+        """CHW-tiled conv2d (NEXT-1), stride 1: G channels packed per ciphertext at
+        block stride CS; the K^2 - 1 tap rotations are hoisted per PACKED ciphertext (G channels
+        per key switch); per output channel one mulPlain per (packed ciphertext, tap) with the
+        tap's weights laid on each channel block (the "mulv is required" of P:722), one rescale,
+        then log2 G rotate-and-sum steps across blocks ("2 log(C) rotations"); the output
+        channel lands in block 0 (HW layout, origin = the block data offset)."""
+        _, oc_n, k, st, p = layer[:5]
+        if st != 1:
+            raise ValueError("CHW conv lowering supports stride 1")
+        if self.world > 1:
+            raise NotImplementedError("CHW conv is single-GPU in this build")
+        if not lay.clean:
+            cts, lay = self.mask(cts, lay, li)
+            masked = True
+        else:
+            masked = False
+        C = lay.C
+        cs, G, pad_off = self.chw_geometry(lay, k, p, self.slots)
+        npk = -(-C // G)
+        # pack: channel c -> packed ciphertext c // G, block c % G (right rotation by its offset)
+        packed = [None] * npk
+        for g in range(G):
+            chans = [c for c in range(g, C, G)]
+            if not chans:
+                continue
+            shift = (g * cs + pad_off - lay.origin) % self.slots
+            amt = (self.slots - shift) % self.slots
+            if amt:
+                rs = [r[0] for r in self._rot_many([cts[c] for c in chans], [amt])]
+            else:
+                rs = [self.b.copy(cts[c]) for c in chans]
+            for c, r in zip(chans, rs):
+                kk = c // G
+                if packed[kk] is None:
+                    packed[kk] = r
+                else:
+                    nxt = self.b.add(packed[kk], r)
+                    self._free_all([packed[kk], r])
+                    packed[kk] = nxt
+        if masked:
+            self._free_all(cts)
+        taps = [(i, j) for i in range(k) for j in range(k)]
+        amounts = [((i - p) * lay.hS + (j - p) * lay.wS) % self.slots for i, j in taps]
+        nz = [a for a in amounts if a]
+        rot_all = self._rot_many(packed, nz)
+        inputs, temps = [], []
+        for x, rl in zip(packed, rot_all):
+            it = iter(rl)
+            for a in amounts:
+                h = next(it) if a else x
+                inputs.append(h)
+                if a:
+                    temps.append(h)
+        lv = self._level(packed[0])
+        rel = lay.slots_of_valid() - lay.origin       # plane positions relative to the data origin
+
+        def vals(oc, kk, t):
+            i, j = taps[t]
+            v = np.zeros(self.slots)
+            for g in range(G):
+                c = kk * G + g
+                if c < C:
+                    v[g * cs + pad_off + rel] = w[oc, c, i, j]
+            return v
+        keys = [(("chw", li, oc, kk, t), lv) for oc in range(oc_n) for kk in range(npk) for t in range(len(taps))]
+        todo = [(key, oc, kk, t) for key, (oc, kk, t) in
+                zip(keys, [(oc, kk, t) for oc in range(oc_n) for kk in range(npk) for t in range(len(taps))])
+                if key not in self._pts]
+        for c0 in range(0, len(todo), 256):          # weight plaintexts, once per model, in batches
+            chunk = todo[c0:c0 + 256]
+            hs = self.b.encode_batch(np.stack([vals(oc, kk, t) for _k, oc, kk, t in chunk]), float(self.q[lv]), lv)
+            for (key, _o, _kk, _t), h in zip(chunk, hs):
+                self._pts[key] = h
+        sums = self.b.mul_plain_accumulate(inputs, [self._pts[key] for key in keys], oc_n)
+        self._free_all(temps + packed)
+        res = self.b.rescale_batch(sums)
+        self._free_all(sums)
+        res = self._rotate_sum(res, [cs << t for t in range(int(math.log2(G)))])
+        res = self._bias(res, beta)
+        return res, Layout("hw", oc_n, lay.H, lay.W, lay.hS, lay.wS, pad_off, False)
+
     def conv(self, cts, lay, layer, w, beta, li):
         """Alg. 1: hoisted rotations per input channel + fused accumulation."""
-        _, oc_n, k, st, p = layer
+        if len(layer) > 5 and layer[5] == "chw":
+            return self.conv_chw(cts, lay, layer, w, beta, li)
+        _, oc_n, k, st, p = layer[:5]
         own_in = self.owned(lay.C)
         if p > 0 and not lay.clean:
             cts, lay = self.mask(cts, lay, li)

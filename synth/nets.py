@@ -7,7 +7,8 @@ rotation amounts, folding, masks, level plan) is implemented independently by
 ``paper_1810_00845_b200/driver.py`` and ``oracle/nets.py``.
 
 Layer tuples (PyTorch semantics for the float64 definition):
-    ("conv", oc, k, stride, pad)   cross-correlation, zero padding `pad`
+    ("conv", oc, k, stride, pad[, "chw"])   cross-correlation, zero padding `pad`; "chw" selects the
+                                   CHW-tiled encrypted lowering (NEXT-1), not semantics
     ("act",)                       a0 + a1 x + a2 x^2 with ACT_COEFFS (A25)
     ("square",)                    x^2 (config 1)
     ("avgpool",)                   2x2, stride 2
@@ -40,6 +41,12 @@ NETS = {
                         layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2), ("act",),
                                 ("avgpool",), ("fc", 512, 16), ("act",), ("fc", 10)],
                         sigma=[0.05, 0.05, 0.05, 0.05]),
+    # config 4 with its second conv CHW-tiled (several channels per ciphertext; the paper's
+    # layout comparison, Fig. tilings)
+    "lenet_large_chw": dict(log_n=15, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
+                            layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2, "chw"),
+                                    ("act",), ("avgpool",), ("fc", 512, 16), ("act",), ("fc", 10)],
+                            sigma=[0.05, 0.05, 0.05, 0.05]),
     # config 5: SqueezeNet-CIFAR-shaped (A33: conv1 + 4 fire modules + 1x1 conv + global avg pool;
     # 1 + 4*2 + 1 = 10 conv layers, 9 activations), N = 2^16, 24 limbs
     "squeezenet": dict(log_n=16, q_bits=[60] + [40] * 23, p_bits=60, scale=2.0 ** 40, input=(3, 32, 32),
@@ -57,7 +64,7 @@ def linear_shapes(name: str):
     shapes = []
     for layer in net["layers"]:
         if layer[0] == "conv":
-            _, oc, k, s, p = layer
+            _, oc, k, s, p = layer[:5]
             shapes.append((oc, c, k, k))
             c, h, w = oc, (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
         elif layer[0] == "avgpool":

@@ -62,15 +62,15 @@ def test_driver_bit_exact_and_accurate(name):
     assert np.abs(got - ogot).max() < 1e-9
 
 
-@pytest.mark.parametrize("which", ["every_branch", "replicas", "squeezenet_kinds"])
+@pytest.mark.parametrize("which", ["every_branch", "replicas", "squeezenet_kinds", "chw"])
 def test_driver_small_nets_bit_exact(which):
     """Every lowering branch (mask + SAME conv after a pool, both FC forms; replica FC and FC
     from the replica layout; fire modules and global average pool) bit-exact against the
     oracle at N = 2^11."""
-    from tests.test_driver_host import (MINI, MINI_REP, MINI_SQ, _mini_rep_weights, _mini_sq_weights,
-                                        _mini_weights)
+    from tests.test_driver_host import (MINI, MINI_CHW, MINI_REP, MINI_SQ, _mini_chw_weights, _mini_rep_weights,
+                                        _mini_sq_weights, _mini_weights)
     net, W = {"every_branch": (MINI, _mini_weights()), "replicas": (MINI_REP, _mini_rep_weights()),
-              "squeezenet_kinds": (MINI_SQ, _mini_sq_weights())}[which]
+              "squeezenet_kinds": (MINI_SQ, _mini_sq_weights()), "chw": (MINI_CHW, _mini_chw_weights())}[which]
     img = SN._image(5, net["input"])
     got, ogot, ref = _run_pair(net, W, img)
     assert np.abs(got - ref).max() <= 1e-3
@@ -117,3 +117,13 @@ def test_driver_pow2_rotation_keys(name):
     got, ogot, ref = _run_pair(net, W, SN.net_image(name, 2), rot_policy="pow2")
     assert np.abs(got - ref).max() <= 1e-3
     assert np.abs(got - ogot).max() < 1e-9
+
+
+@pytest.mark.slow
+def test_driver_lenet_large_chw():
+    """NEXT-1 at config-4 size: LeNet-large with its second conv CHW-tiled (8 channels per
+    ciphertext) decrypts within 1e-3 of the float64 network, and its first layers are bit-exact
+    with the oracle (the CHW lowering itself is bit-exact on MINI_CHW above)."""
+    name = "lenet_large_chw"
+    got, _o, ref = _run_pair(SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0), oracle_layers=2)
+    assert np.abs(got - ref).max() <= 1e-3, np.abs(got - ref).max()

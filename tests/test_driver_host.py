@@ -54,6 +54,18 @@ def _mini_sq_weights():
     return [SN._weights(31 + i, s, 0.5) for i, s in enumerate(shapes)]
 
 
+# CHW-tiled second conv (NEXT-1): pooled 4x4 planes (hS 20, wS 2), SAME 3x3 -> block stride 128,
+# 8 channels per ciphertext (4 channels -> one packed ciphertext), then FC
+MINI_CHW = dict(log_n=11, q_bits=[60] + [40] * 6, p_bits=60, scale=2.0 ** 40, input=(2, 8, 8),
+                layers=[("conv", 4, 3, 1, 1), ("act",), ("avgpool",), ("conv", 3, 3, 1, 1, "chw"), ("act",),
+                        ("fc", 2)], sigma=[0.3, 0.3, 0.3])
+
+
+def _mini_chw_weights():
+    shapes = [(4, 2, 3, 3), (3, 4, 3, 3), (2, 3 * 4 * 4)]
+    return [SN._weights(51 + i, s, 0.3) for i, s in enumerate(shapes)]
+
+
 def _mini_weights():
     shapes = [(2, 2, 3, 3), (2, 2, 3, 3), (3, 2 * 4 * 4), (2, 3)]
     return [SN._weights(77 + i, s, 0.3) for i, s in enumerate(shapes)]
@@ -322,3 +334,23 @@ def test_oracle_pow2_policy_matches_float64_and_planner():
     assert np.abs(got - ref).max() <= 1e-3
     pl = EncryptedNet.plan(MINI, W, SN.ACT_COEFFS, on.o.moduli, rot_policy="pow2")
     assert pl["rotations"] == on.amounts
+
+
+def test_oracle_chw_conv_matches_float64_and_planner():
+    """NEXT-1 pin: the oracle's CHW-tiled conv (packing, per-block mulPlain, cross-block
+    rotate-and-sum) decrypts within 1e-3 of the float64 network; the planner agrees on keys."""
+    from oracle import plain
+    from oracle.nets import OracleNet
+    from paper_1810_00845_b200.driver import EncryptedNet
+    W = _mini_chw_weights()
+    img = SN._image(12, MINI_CHW["input"])
+    on = OracleNet(MINI_CHW, W, SN.ACT_COEFFS)
+    cts, lay = on.encrypt_image(img)
+    out, ol = on.forward(cts, lay)
+    got = on.decrypt_output(out, ol)
+    ref = plain.forward(MINI_CHW, img, W, SN.ACT_COEFFS)
+    assert got.shape == ref.shape == (2,)
+    assert np.abs(got - ref).max() <= 1e-3, (got, ref)
+    pl = EncryptedNet.plan(MINI_CHW, W, SN.ACT_COEFFS, on.o.moduli)
+    assert pl["rotations"] == on.amounts
+    assert pl["levels_used"] == 6
