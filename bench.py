@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--nets", default="tiny,lenet_small", help="encrypted-inference configs to time")
     ap.add_argument("--tiling", default="lenet_large",
                     help="config whose HW-tiled vs CHW-tiled (config + '_chw') latencies are compared ('' = skip)")
+    ap.add_argument("--replica-sweep", default="",
+                    help="config whose first FC is timed with R = 1, 2, 4, 8 replicas (NEXT-3), e.g. lenet_small")
     ap.add_argument("--policy-net", default="lenet_small",
                     help="config on which exact vs power-of-two rotation keys are compared ('' = skip)")
     return ap.parse_args()
@@ -195,6 +197,23 @@ def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream):
                         for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}}
 
 
+def _net_variant(name, fc_replicas=None):
+    """A config with its first HW-input FC lowered with `fc_replicas` replicas (NEXT-3)."""
+    from synth import nets as SN
+    if fc_replicas is None:
+        return name
+    import copy
+    net = copy.deepcopy(SN.NETS[name])
+    for i, layer in enumerate(net["layers"]):
+        if layer[0] == "fc":
+            net["layers"][i] = ("fc", layer[1], fc_replicas)
+            break
+    key = f"{name}_fcR{fc_replicas}"
+    SN.NETS[key] = net
+    SN.NETS.setdefault("_weights_alias", {})[key] = name
+    return key
+
+
 def measure_inference(name, device, reps=3, rot_policy="exact"):
     """Encrypted CNN inference latency (BASELINE.json metric, configs 1 / 3): server-side
     forward from encrypted input resident on the GPU to encrypted output, CUDA events + wall
@@ -206,8 +225,9 @@ def measure_inference(name, device, reps=3, rot_policy="exact"):
     from paper_1810_00845_b200 import hisa as H
     from paper_1810_00845_b200.driver import EncryptedNet
     net = SN.NETS[name]
-    W = SN.net_weights(name)
-    img = SN.net_image(name, 0)
+    base = SN.NETS.get("_weights_alias", {}).get(name, name)   # replica variants share the weights
+    W = SN.net_weights(base)
+    img = SN.net_image(base, 0)
     torch.cuda.empty_cache()
     ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=device, arena_bytes=64 << 30)
     t0 = time.perf_counter()
@@ -597,6 +617,11 @@ def main():
                 line["tiling"] = {"config": a.tiling, "hw_s": hw["latency_s"], "chw_s": chw["latency_s"],
                                   "speedup_chw_over_hw": hw["latency_s"] / chw["latency_s"],
                                   "chw_first_pass_incl_weight_encoding_s": chw["first_pass_incl_weight_encoding_s"]}
+            # NEXT-3: replicas trade mulPlain for rotations
+            if a.replica_sweep:
+                line["replica_sweep"] = {"config": a.replica_sweep, "latency_s": {
+                    f"R{r}": measure_inference(_net_variant(a.replica_sweep, r), local)["latency_s"]
+                    for r in (1, 2, 4, 8)}}
             # NEXT-2: CHET's exact rotation keys vs HEAAN's power-of-two keys with
             # composed rotations (the paper's Fig. rotopt: 1.43-2.07x on CPU HEAAN)
             if a.policy_net:

@@ -32,9 +32,10 @@ NETS = {
     # config 1: tiny encrypted conv (BASELINE.json configs[0])
     "tiny": dict(log_n=13, q_bits=[60, 40, 40], p_bits=60, scale=2.0 ** 40, input=(1, 8, 8),
                  layers=[("conv", 2, 3, 1, 0), ("square",)], sigma=[0.1]),
-    # config 3: LeNet-5-small-shaped (A31: pad 1 -> 30x30, 5x5 stride 2 -> 13x13x5 = 845)
+    # config 3: LeNet-5-small-shaped (A31: pad 1 -> 30x30, 5x5 stride 2 -> 13x13x5 = 845); FC1
+    # lowered with R = 8 replicas (A27: the measured-cheaper lowering on B200, 6 of 6 levels)
     "lenet_small": dict(log_n=14, q_bits=[60] + [40] * 6, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
-                        layers=[("conv", 5, 5, 2, 1), ("act",), ("fc", 100), ("act",), ("fc", 10)],
+                        layers=[("conv", 5, 5, 2, 1), ("act",), ("fc", 100, 8), ("act",), ("fc", 10)],
                         sigma=[0.1, 0.1, 0.1]),
     # config 4: LeNet-5-large-shaped (A32: SAME 5x5 convs, 28 -> 14 -> 7, 7*7*64 = 3136)
     "lenet_large": dict(log_n=15, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),

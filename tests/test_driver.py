@@ -127,3 +127,14 @@ def test_driver_lenet_large_chw():
     name = "lenet_large_chw"
     got, _o, ref = _run_pair(SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0), oracle_layers=2)
     assert np.abs(got - ref).max() <= 1e-3, np.abs(got - ref).max()
+
+
+def test_driver_lenet_small_fc_r1():
+    """Config 3 with FC1 lowered with R = 1 (one ciphertext per neuron, A27): bit-exact with the
+    oracle after every layer, within 1e-3 of float64 (config 3's default lowering is R = 8)."""
+    import copy
+    net = copy.deepcopy(SN.NETS["lenet_small"])
+    net["layers"][2] = ("fc", 100)
+    got, ogot, ref = _run_pair(net, SN.net_weights("lenet_small"), SN.net_image("lenet_small", 4))
+    assert np.abs(got - ref).max() <= 1e-3
+    assert np.abs(got - ogot).max() < 1e-9

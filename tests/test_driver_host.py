@@ -97,12 +97,20 @@ def test_plan_spec_example_rotation_set():
 
 def test_plan_lenet_small_levels():
     from paper_1810_00845_b200.driver import EncryptedNet
+    import copy
     net = SN.NETS["lenet_small"]
     pl = EncryptedNet.plan(net, SN.net_weights("lenet_small"), SN.ACT_COEFFS, _moduli(net))
-    assert pl["levels_used"] == 5                                    # A28: 5 of 6
+    assert pl["levels_used"] == 6                                    # FC1 with R = 8: mask + 5 = 6 of 6
     assert pl["counts"]["rot_hoisted"] == 24
+    # R = 8: replicate 5 channels (3 rotations each), 13 groups x 10 rotate-and-sum steps inside
+    # the 1024-slot blocks, FC2 reads the replica layout: 10 outputs x 3 cross-block steps
+    assert pl["counts"]["rot"] == 5 * 3 + 13 * 10 + 10 * 3
+    r1 = copy.deepcopy(net)
+    r1["layers"][2] = ("fc", 100)
+    pl1 = EncryptedNet.plan(r1, SN.net_weights("lenet_small"), SN.ACT_COEFFS, _moduli(net))
+    assert pl1["levels_used"] == 5                                   # A28 with R = 1: 5 of 6
     # FC1 rotate-and-sum: 100 neurons x ceil(log2(12*60 + 12*2 + 1)) = 10 steps
-    assert pl["counts"]["rot"] == 100 * 10
+    assert pl1["counts"]["rot"] == 100 * 10
 
 
 def test_fold_identity():
