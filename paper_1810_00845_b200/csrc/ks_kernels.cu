@@ -346,6 +346,121 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
     }
 }
 
+// K4 with NT digits in flight (variant 50+): generalises k_ks_ip2; the digits j != ri are taken
+// NT at a time (the last group may be smaller), then the diagonal digit
+template <int LOG_M, int LOG_R, int MINB, int NT>
+__global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ipN(KsJob job, Tables tb) {
+    using G = Geo<LOG_M, LOG_R>;
+    extern __shared__ uint64_t sm[];
+    double* tws = reinterpret_cast<double*>(sm + NT * G::STRIDE);
+    const int nz = job.nz;
+    const int z = blockIdx.x % nz;
+    const int ri = blockIdx.y;
+    const int l1 = job.l1;
+    const int nri = l1 + 1;
+    const int log_n = tb.log_n;
+    const int row0 = blockIdx.x / nz;
+    const long long off0 = (long long)row0 << LOG_M;
+    const int mi = job.mod_map[ri];
+    const Mod md = tb.mods[mi];
+    const bool fp = (double)md.q < tb.f64_max_q;
+    const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
+    const double tq52 = __dadd_rn(2.0 * qd.x, 4503599627370496.0);
+    constexpr int NTHR = G::T;
+    constexpr int EPT = G::R;
+    U128 acc0[EPT], acc1[EPT];
+#pragma unroll
+    for (int k = 0; k < EPT; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
+    const int t = threadIdx.x;
+    const long long kstride_j = 2ll * (job.L + 1) << log_n;
+    const long long kstride_p = (long long)(job.L + 1) << log_n;
+    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
+    if (fp) {
+        const double* twg = tb.fwd_d + ((long long)mi << log_n);
+        const int s0 = log_n - LOG_M;
+        for (int idx = threadIdx.x + 1; idx < G::M; idx += NTHR) {
+            const int u = 31 - __clz(idx), m = idx - (1 << u);
+            tws[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
+        }
+    }
+    auto copy_tile = [&](uint64_t* dst, int j) {
+        const uint64_t* src = (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
+                                        : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * NTHR;
+            const unsigned s_ = (unsigned)__cvta_generic_to_shared(&dst[G::addr(0, i)]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_), "l"(src + i) : "memory");
+        }
+    };
+    auto mac_tile = [&](const uint64_t* buf, int j, bool conv) {
+        const uint64_t* kb = key_r + j * kstride_j;
+        const uint64_t* ka = kb + kstride_p;
+#pragma unroll
+        for (int k = 0; k < EPT; k++) {
+            const int i = threadIdx.x + k * NTHR;
+            uint64_t D = buf[G::addr(0, i)];
+            if (conv) D = d_rep4(__longlong_as_double((long long)D), tq52);
+            mac128(acc0[k], D, __ldg(kb + i));
+            mac128(acc1[k], D, __ldg(ka + i));
+        }
+    };
+    int js[NT];
+    int j = (ri == 0) ? 1 : 0;
+    while (j < l1) {
+        int n = 0;
+        while (n < NT && j < l1) {
+            js[n++] = j;
+            j++;
+            if (j == ri) j++;
+        }
+        for (int m = 0; m < n; m++) copy_tile(sm + m * G::STRIDE, js[m]);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        if (fp && n == NT) {
+            double* tl[NT];
+#pragma unroll
+            for (int m = 0; m < NT; m++) tl[m] = reinterpret_cast<double*>(sm + m * G::STRIDE);
+            fwd_engine_f64_rowtwN<LOG_M, LOG_R, NT>(tl, qd.x, qd.y, tws, t);
+        } else {
+            for (int m = 0; m < n; m++) {
+                if (fp)
+                    fwd_engine_f64_rowtw<LOG_M, LOG_R>(reinterpret_cast<double*>(sm + m * G::STRIDE), qd.x, qd.y, tws,
+                                                       t);
+                else
+                    fwd_engine<LOG_M, LOG_R>(sm + m * G::STRIDE, md.q, tb.fwd + ((long long)mi << log_n),
+                                             log_n - LOG_M, (uint32_t)row0, 0, t);
+            }
+        }
+        for (int m = 0; m < n; m++) mac_tile(sm + m * G::STRIDE, js[m], fp);
+        __syncthreads();
+    }
+    if (ri < l1) {
+        copy_tile(sm, ri);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        mac_tile(sm, ri, false);
+    }
+    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
+    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
+#pragma unroll
+    for (int k = 0; k < EPT; k++) {
+        const int i = threadIdx.x + k * NTHR;
+        out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
+        out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
+    }
+}
+
+template <int LOG_M, int LOG_R, int MINB, int NT>
+static cudaError_t ks_ipN_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+    using G = Geo<LOG_M, LOG_R>;
+    const int rows = 1 << (tb.log_n - LOG_M);
+    const size_t smem = ((size_t)NT * G::STRIDE + G::M) * sizeof(uint64_t);
+    dim3 grid(rows * nz, job.l1 + 1, 1);
+    k_ks_ipN<LOG_M, LOG_R, MINB, NT><<<grid, G::T, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+
 template <int LOG_M, int LOG_R, int MINB, bool PF = false>
 static cudaError_t ks_ip2_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     using G = Geo<LOG_M, LOG_R>;
@@ -384,6 +499,7 @@ static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStrea
         case 10: return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
         case 20: return ks_ip_pipe_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
         case 41: return ks_ip2_t<LOG_M, 2, 12, true>(job, tb, nz, st);
+        case 55: return ks_ipN_t<LOG_M, 2, 12, 3>(job, tb, nz, st);
         default: break;
     }
     // default = variant 33 (measured best on B200 at N = 2^16, L = 24: one row per 64-thread CTA,
