@@ -213,6 +213,9 @@ struct hisa_ctx {
     // cis(pi t / N), t < N
     std::vector<std::complex<long double>> enc_root, enc_twist;
     std::vector<__float128> enc_cosq;   // binary128 cos(pi e / N), e < 2N (near-tie recomputation, A7)
+    uint32_t* d_enc_pos = nullptr;      // GPU encode: bit-reversed positions of the 2 x N/2 slot images
+    cdd* d_enc_root = nullptr;          // e^{2 pi i k / N}, k < N/2, double-double from binary128
+    cdd* d_enc_twist = nullptr;         // e^{i pi t / N}, t < N
     // profiling: CUDA events around every launch on the context stream (hisa_profile)
     bool prof_on = false;
     struct ProfRec { const char* name; cudaEvent_t a, b; };
@@ -849,46 +852,113 @@ static void fft_ld(const hisa_ctx* c, std::vector<cld>& a, int sign) {
     }
 }
 
-static int encode_coeffs(hisa_ctx* c, const double* z, size_t n, double scale, std::vector<int64_t>& m) {
+// one coefficient exactly: binary128 direct sum of v_t (the A7 near-tie path); same operation
+// order as the oracle's (oracle/ckks_oracle.c enc_value_q)
+static int exact_coeff_q(hisa_ctx* c, const double* z, size_t n, double scale, uint64_t t, int64_t* out) {
     const uint64_t N = c->N, twoN = 2 * N;
-    std::vector<cld> A(N, cld(0, 0));
-    std::vector<uint64_t> pow5(n);
+    std::vector<__float128>& cq = c->enc_cosq;
+    if (cq.empty()) {
+        cq.resize(twoN);
+        for (uint64_t e = 0; e < twoN; e++) cq[e] = cosq(M_PIq * (__float128)e / (__float128)N);
+    }
+    __float128 acc = 0;
     uint64_t k = 1;
     for (size_t j = 0; j < n; j++) {
-        pow5[j] = k;
-        A[(k - 1) / 2] += cld((long double)z[j], 0);
-        const uint64_t kc = twoN - k;
-        A[(kc - 1) / 2] += cld((long double)z[j], 0);
+        if (z[j] != 0.0) acc += 2 * (__float128)z[j] * cq[(uint64_t)((u128)k * t % twoN)];
         k = k * 5 % twoN;
     }
-    enc_tables(c);
-    fft_ld(c, A, -1);   // F[t] = sum_m A[m] e^{-2 pi i m t / N}
-    m.assign(N, 0);
-    std::vector<__float128>& cq = c->enc_cosq;
-    for (uint64_t t = 0; t < N; t++) {
-        const cld tw = std::conj(c->enc_twist[t]);
-        const long double v = (A[t] * tw).real() * (long double)scale / (long double)N;
-        const long double av = fabsl(v);
-        const long double fr = av - floorl(av);
-        long double r;
-        if (fabsl(fr - 0.5L) < 0x1p-12L) {   // near tie: binary128 direct sum (A7)
-            if (cq.empty()) {
-                cq.resize(twoN);
-                for (uint64_t e = 0; e < twoN; e++) cq[e] = cosq(M_PIq * (__float128)e / (__float128)N);
-            }
-            __float128 acc = 0;
-            for (size_t j = 0; j < n; j++)
-                if (z[j] != 0.0) acc += 2 * (__float128)z[j] * cq[(uint64_t)((u128)pow5[j] * t % twoN)];
-            acc = acc * (__float128)scale / (__float128)N;
-            __float128 rq = floorq(fabsq(acc) + 0.5Q);
-            r = (long double)(acc < 0 ? -rq : rq);
-        } else {
-            r = floorl(av + 0.5L);
-            if (v < 0) r = -r;
-        }
-        if (!(fabsl(r) < 0x1p62L)) return fail(HISA_E_PARAMS, "encoded coefficient exceeds 2^62");
-        m[t] = (int64_t)r;
+    acc = acc * (__float128)scale / (__float128)N;
+    __float128 rq = floorq(fabsq(acc) + 0.5Q);
+    const __float128 r = acc < 0 ? -rq : rq;
+    if (!(fabsq(r) < 0x1p62Q)) return fail(HISA_E_PARAMS, "encoded coefficient exceeds 2^62");
+    *out = (int64_t)r;
+    return HISA_OK;
+}
+
+static int enc_gpu_tables(hisa_ctx* c) {
+    if (c->d_enc_root) return HISA_OK;
+    const uint64_t N = c->N, twoN = 2 * N;
+    std::vector<uint32_t> pos(N);
+    uint64_t k = 1;
+    for (uint64_t j = 0; j < N / 2; j++) {      // slot j -> positions (k-1)/2 and (2N-k-1)/2, bit-reversed
+        pos[2 * j] = h_brv((uint32_t)((k - 1) / 2), c->log_n);
+        pos[2 * j + 1] = h_brv((uint32_t)((twoN - k - 1) / 2), c->log_n);
+        k = k * 5 % twoN;
     }
+    auto to_dd = [](__float128 x) { const double hi = (double)x; return dd{hi, (double)(x - (__float128)hi)}; };
+    std::vector<cdd> root(N / 2), twist(N);
+    for (uint64_t i = 0; i < N / 2; i++) {
+        const __float128 a = 2 * M_PIq * (__float128)i / (__float128)N;
+        root[i] = cdd{to_dd(cosq(a)), to_dd(sinq(a))};
+    }
+    for (uint64_t t = 0; t < N; t++) {
+        const __float128 a = M_PIq * (__float128)t / (__float128)N;
+        twist[t] = cdd{to_dd(cosq(a)), to_dd(sinq(a))};
+    }
+    auto up = [&](void** dptr, const void* src, size_t bytes) -> bool {
+        if (cudaMalloc(dptr, bytes) != cudaSuccess) return false;
+        c->table_allocs.push_back(*dptr);
+        return cudaMemcpy(*dptr, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+    };
+    if (!up((void**)&c->d_enc_pos, pos.data(), N * 4) || !up((void**)&c->d_enc_root, root.data(), N / 2 * sizeof(cdd)) ||
+        !up((void**)&c->d_enc_twist, twist.data(), N * sizeof(cdd))) {
+        cudaGetLastError();
+        return fail(HISA_E_CUDA, "encode table upload failed");
+    }
+    return HISA_OK;
+}
+
+// GPU encode (NEXT-4) of count rows of n_per slot values into int64 coefficients dm[count][N]:
+// double-double FFT, exact rounding except inside a tie window sized from the dd error bound,
+// those few coefficients recomputed exactly (binary128) on the host.  Equal to the host / oracle
+// exact encoding (A7) bit for bit.
+static int encode_to_device(hisa_ctx* c, const double* v, size_t n_per, size_t count, double scale, int64_t* dm) {
+    RET(enc_gpu_tables(c));
+    const uint64_t N = c->N;
+    // error bound of the dd FFT: |err(v_t)| <= log2(N) * c * 2^-104 * (scale/N) * 2 sum_j |z_j|;
+    // take 2^-88 * scale * (2/N) sum |z| (>= 2^10 margin) and never below 2^-40
+    double smax = 0;
+    for (size_t p = 0; p < count; p++) {
+        double sa = 0;
+        for (size_t j = 0; j < n_per; j++) sa += fabs(v[p * n_per + j]);
+        smax = std::max(smax, sa);
+    }
+    const double window = std::max(0x1p-40, 0x1p-88 * scale * 2.0 * smax / (double)N);
+    if (window > 0x1p-4) return fail(HISA_E_PARAMS, "scale too large for exact GPU encoding");
+    const unsigned int max_flags = 4096;
+    const size_t zbytes = std::max<size_t>(8, n_per * count * 8);
+    double* dz = (double*)dalloc(c, zbytes);
+    cdd* A = dalloc_t<cdd>(c, (size_t)N * count);
+    uint32_t* flags = dalloc_t<uint32_t>(c, max_flags + 4);
+    if (!dz || !A || !flags) return fail(HISA_E_OOM, "encode scratch");
+    unsigned int* nflag = flags + max_flags;
+    int* overflow = (int*)(flags + max_flags + 1);
+    CK(cudaMemsetAsync(nflag, 0, 8, c->stream));
+    if (n_per) CK(cudaMemcpyAsync(dz, v, n_per * count * 8, cudaMemcpyHostToDevice, c->stream));
+    {
+        ProfScope ps_(c, "encode_fft");
+        CK(launch_encode_fft(dz, n_per, count, c->d_enc_pos, c->d_enc_root, c->d_enc_twist, scale / (double)N,
+                             window, c->log_n, A, dm, flags, nflag, max_flags, overflow, c->stream));
+    }
+    unsigned int hf[2];
+    CK(cudaMemcpyAsync(hf, nflag, 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (hf[1]) return fail(HISA_E_PARAMS, "encoded coefficient exceeds 2^62");
+    if (hf[0]) {   // near ties: exact binary128 recomputation on the host
+        if (hf[0] > max_flags) return fail(HISA_E_PARAMS, "too many near-tie coefficients (%u)", hf[0]);
+        std::vector<uint32_t> idx(hf[0]);
+        std::vector<int64_t> val(hf[0]);
+        CK(cudaMemcpy(idx.data(), flags, hf[0] * 4, cudaMemcpyDeviceToHost));
+        for (unsigned int i = 0; i < hf[0]; i++) {
+            const uint64_t p = idx[i] / N, t = idx[i] % N;
+            RET(exact_coeff_q(c, v + p * n_per, n_per, scale, t, &val[i]));
+            CK(cudaMemcpyAsync(dm + idx[i], &val[i], 8, cudaMemcpyHostToDevice, c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    dfree(c, dz);
+    dfree(c, A);
+    dfree(c, flags);
     return HISA_OK;
 }
 
@@ -901,19 +971,16 @@ extern "C" int hisa_encode(hisa_ctx* c, const double* v, size_t n, double scale,
     if (!(scale > 0) || !std::isfinite(scale)) return fail(HISA_E_PARAMS, "bad scale");
     for (size_t i = 0; i < n; i++)
         if (!std::isfinite(v[i])) return fail(HISA_E_PARAMS, "non-finite slot value");
-    std::vector<int64_t> m;
-    RET(encode_coeffs(c, v, n, scale, m));
     const int l1 = level + 1;
     int64_t* dm = dalloc_t<int64_t>(c, c->N);
     uint64_t* pt = dalloc_t<uint64_t>(c, (size_t)l1 * c->N);
     if (!dm || !pt) return fail(HISA_E_OOM, "encode");
-    CK(cudaMemcpyAsync(dm, m.data(), c->N * 8, cudaMemcpyHostToDevice, c->stream));
+    RET(encode_to_device(c, v, n, 1, scale, dm));
     uint8_t mm[MAXL];
     ident_map(mm, l1);
     CK(launch_int_to_limbs(dm, pt, mm, l1, c->log_n, c->d_mods, c->stream));
     uint64_t* pp[1] = {pt};
     RET(ntt_fwd(c, pp, 1, l1, mm));
-    CK(cudaStreamSynchronize(c->stream));   // host vector m must outlive the copy
     dfree(c, dm);
     *out = new_handle(c, OBJ_PT, pt, level, 1, scale);
     return HISA_OK;
@@ -922,6 +989,9 @@ extern "C" int hisa_encode(hisa_ctx* c, const double* v, size_t n, double scale,
 // count plaintexts of n_per slot values each (v row-major), encoded on all host cores (the
 // exact-rounding encoder is host code, A7), then reduced into limbs and NTT-ed on the GPU in
 // batches: the once-per-model weight / mask plaintexts of a layer in one call
+// count plaintexts of n_per slot values each (v row-major): the exact encoding (A7) of every row
+// on the GPU in chunks (double-double FFT, encode_to_device), limbs + NTT batched: a layer's
+// weight / mask plaintexts in one call
 extern "C" int hisa_encode_batch(hisa_ctx* c, const double* v, size_t n_per, size_t count, double scale, int level,
                                  hisa_pt* outs) {
     CHECK_CTX(c);
@@ -934,38 +1004,16 @@ extern "C" int hisa_encode_batch(hisa_ctx* c, const double* v, size_t n_per, siz
     for (size_t i = 0; i < n_per * count; i++)
         if (!std::isfinite(v[i])) return fail(HISA_E_PARAMS, "non-finite slot value");
     const uint64_t N = c->N;
-    enc_tables(c);
-    if (c->enc_cosq.empty()) {   // built before the threads share it (read-only afterwards)
-        c->enc_cosq.resize(2 * N);
-        for (uint64_t e = 0; e < 2 * N; e++) c->enc_cosq[e] = cosq(M_PIq * (__float128)e / (__float128)N);
-    }
     const int l1 = level + 1;
-    const size_t chunk = 64;
-    std::vector<int64_t> m(chunk * N);
+    // chunk so the dd FFT workspace (32 B per coefficient) stays near 128 MiB
+    const size_t chunk = std::max<size_t>(1, std::min<size_t>(MAXB, ((size_t)128 << 20) / (N * sizeof(cdd))));
     int64_t* dm = dalloc_t<int64_t>(c, chunk * N);
     if (!dm) return fail(HISA_E_OOM, "encode batch staging");
-    unsigned nth = std::max(1u, std::thread::hardware_concurrency());
+    uint8_t mmap[MAXL];
+    ident_map(mmap, l1);
     for (size_t i0 = 0; i0 < count; i0 += chunk) {
         const size_t nc = std::min(chunk, count - i0);
-        std::vector<int> rc(nc, HISA_OK);
-        std::vector<std::string> err(nc);
-        std::vector<std::thread> th;
-        std::atomic<size_t> next(0);
-        for (unsigned t = 0; t < std::min<size_t>(nth, nc); t++)
-            th.emplace_back([&]() {
-                std::vector<int64_t> mm;
-                for (size_t i; (i = next.fetch_add(1)) < nc;) {
-                    rc[i] = encode_coeffs(c, v + (i0 + i) * n_per, n_per, scale, mm);
-                    if (rc[i] == HISA_OK) memcpy(&m[i * N], mm.data(), N * 8);
-                    else err[i] = hisa_last_error();
-                }
-            });
-        for (auto& t : th) t.join();
-        for (size_t i = 0; i < nc; i++)
-            if (rc[i] != HISA_OK) return fail(rc[i], "%s", err[i].c_str());
-        CK(cudaMemcpyAsync(dm, m.data(), nc * N * 8, cudaMemcpyHostToDevice, c->stream));
-        uint8_t mmap[MAXL];
-        ident_map(mmap, l1);
+        RET(encode_to_device(c, v + i0 * n_per, n_per, nc, scale, dm));
         std::vector<uint64_t*> pts(nc);
         for (size_t i = 0; i < nc; i++) {
             pts[i] = dalloc_t<uint64_t>(c, (size_t)l1 * N);
@@ -973,7 +1021,6 @@ extern "C" int hisa_encode_batch(hisa_ctx* c, const double* v, size_t n_per, siz
             CK(launch_int_to_limbs(dm + i * N, pts[i], mmap, l1, c->log_n, c->d_mods, c->stream));
         }
         RET(ntt_fwd(c, pts.data(), (int)nc, l1, mmap));
-        CK(cudaStreamSynchronize(c->stream));   // host staging m is reused by the next chunk
         for (size_t i = 0; i < nc; i++) outs[i0 + i] = new_handle(c, OBJ_PT, pts[i], level, 1, scale);
     }
     dfree(c, dm);

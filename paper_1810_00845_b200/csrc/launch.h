@@ -96,6 +96,15 @@ struct KsJob {
 };
 cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st);
 
+// GPU encode (NEXT-4, A7) -- encode_kernels.cu: double-double FFT + exact rounding with near-tie
+// flags.  dd = unevaluated sum hi + lo; cdd = complex.
+struct dd { double hi, lo; };
+struct cdd { dd re, im; };
+cudaError_t launch_encode_fft(const double* z_dev, size_t n_per, size_t count, const uint32_t* pos_brv,
+                              const cdd* root, const cdd* twist, double scale_over_n, double window, int log_n,
+                              cdd* A, int64_t* m, uint32_t* flags, unsigned int* nflag, unsigned int max_flags,
+                              int* overflow, cudaStream_t st);
+
 // samplers (ChaCha20, A11) -- rng_kernels.cu
 cudaError_t launch_sample_uniform(uint64_t* out, uint64_t seed, uint32_t tag, const uint64_t* index_per_limb_host,
                                   const uint8_t* mod_per_limb_host, int nlimbs, int log_n, const Mod* mods,

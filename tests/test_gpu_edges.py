@@ -98,3 +98,23 @@ def test_large_keyswitch_sampled():
     assert (g.ct_export(hz[0]) == want).all()
     assert (g.ct_export(g.rot_left_batch([a, a], 7)[1]) == want).all()
     g.close()
+
+
+def test_gpu_encode_exact_ties():
+    """NEXT-4 GPU encode: exact half-integer coefficients (a constant vector z = k + 1/2 at scale 1
+    encodes to the constant polynomial, P-ENC-1) fall in the near-tie window, are recomputed
+    exactly in binary128 and rounded half away from zero (A7) -- equal to the oracle."""
+    g, o = _pair(12, [60, 40], 60, [])
+    for c in (2.5, -3.5, 0.5, 1234567.5):
+        z = np.full(g.slots, c)
+        h = g.encode(z, 1.0)
+        want = o.encode(z, 1.0)
+        assert (g.pt_export(h) == want.data).all(), c
+        coeffs = o.intt(want.data[0:1].copy(), 0)[0]
+        q0 = o.q[0]
+        m0 = int(coeffs[0]) if coeffs[0] <= q0 // 2 else int(coeffs[0]) - q0
+        assert m0 == (int(abs(c) + 0.5) * (1 if c > 0 else -1))
+    hs = g.encode_batch(np.stack([np.full(g.slots, 2.5), np.linspace(-1, 1, g.slots)]), 2.0 ** 40)
+    assert (g.pt_export(hs[0]) == o.encode(np.full(g.slots, 2.5), 2.0 ** 40).data).all()
+    assert (g.pt_export(hs[1]) == o.encode(np.linspace(-1, 1, g.slots), 2.0 ** 40).data).all()
+    g.close()
