@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--no-inference", action="store_true")
     ap.add_argument("--hoist-r", type=int, default=8, help="rotation amounts per hoisted ModUp")
     ap.add_argument("--nets", default="tiny,lenet_small", help="encrypted-inference configs to time")
+    ap.add_argument("--oracle-nets", default="tiny,lenet_small",
+                    help="configs whose oracle inference latency is timed on the host cores (cpu_baseline)")
     ap.add_argument("--tiling", default="lenet_large",
                     help="config whose HW-tiled vs CHW-tiled (config + '_chw') latencies are compared ('' = skip)")
     ap.add_argument("--replica-sweep", default="",
@@ -333,6 +335,26 @@ def _allreduce_max(t):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
 
 
+# the paper's CPU latencies for the same network families (context only: non-RNS HEAAN, different
+# parameters, 2x Xeon E5-2667v3 with 16 threads)
+PAPER_CPU_S = {"lenet_small": (8.0, "P:852"), "lenet_large": (265.0, "P:854"), "squeezenet": (1342.0, "P:856")}
+
+
+def oracle_inference(name):
+    """cpu_baseline leg for the inference metric: the oracle's encrypted network (oracle/nets.py,
+    Alg. 1 written literally) on all host cores, one image, server-side forward only."""
+    from synth import nets as SN
+    from oracle.nets import OracleNet
+    net, W, img = SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0)
+    on = OracleNet(net, W, SN.ACT_COEFFS, seed=0)
+    cts, lay = on.encrypt_image(img)
+    t0 = time.perf_counter()
+    on.forward(cts, lay)
+    dt = time.perf_counter() - t0
+    return {"value": dt, "unit": "s", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"one {name} image, the whole encrypted network (server side)"}
+
+
 def _hbm_peak():
     hbm_peak = 6549.8
     mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -608,6 +630,13 @@ def main():
             line["inference"] = sharded
         if not a.no_inference and world == 1:
             line["inference"] = [measure_inference(nm, local) for nm in a.nets.split(",") if nm]
+            for inf in line["inference"]:
+                if inf["config"] in PAPER_CPU_S:
+                    sec, cite = PAPER_CPU_S[inf["config"]]
+                    inf["paper_cpu_context"] = {"latency_s": sec, "cite": cite,
+                                                "hardware": "2x Xeon E5-2667v3, 16 threads, non-RNS HEAAN"}
+                if not a.no_cpu_baseline and inf["config"] in a.oracle_nets.split(","):
+                    inf["cpu_baseline"] = oracle_inference(inf["config"])
             # NEXT-1: HW tiling vs CHW tiling of the second conv (the paper's layout
             # comparison, Fig. tilings)
             if a.tiling:
