@@ -222,7 +222,8 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
     double* tws = reinterpret_cast<double*>(sm + 2 * G::STRIDE);
     const int nz = job.nz;
     const int z = blockIdx.x % nz;
-    const int ri = blockIdx.y;
+    // the special prime's CTAs (integer engine, slower) first, so they do not form the tail
+    const int ri = blockIdx.y == 0 ? job.l1 : (int)blockIdx.y - 1;
     const int l1 = job.l1;
     const int nri = l1 + 1;
     const int log_n = tb.log_n;

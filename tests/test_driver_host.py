@@ -362,3 +362,29 @@ def test_oracle_chw_conv_matches_float64_and_planner():
     pl = EncryptedNet.plan(MINI_CHW, W, SN.ACT_COEFFS, on.o.moduli)
     assert pl["rotations"] == on.amounts
     assert pl["levels_used"] == 6
+
+
+def test_plain_reference_ops_match_torch():
+    """Pins oracle/plain.py (the float64 definition the decrypted outputs are held to) against an
+    independent library routine: torch.nn.functional conv2d / avg_pool2d / linear in float64,
+    including strided, padded and multi-channel cases."""
+    import torch
+    import torch.nn.functional as F
+    from oracle import plain
+    rng = np.random.default_rng(3)
+    for (c, h, w, oc, k, s, p) in [(1, 8, 8, 2, 3, 1, 0), (1, 28, 28, 5, 5, 2, 1), (3, 9, 7, 4, 3, 1, 1),
+                                   (2, 6, 6, 3, 1, 1, 0)]:
+        x = rng.normal(size=(c, h, w))
+        wt = rng.normal(size=(oc, c, k, k))
+        want = F.conv2d(torch.from_numpy(x)[None], torch.from_numpy(wt), stride=s, padding=p)[0].numpy()
+        assert np.allclose(plain.conv2d(x, wt, s, p), want, atol=1e-12)
+    x = rng.normal(size=(4, 14, 14))
+    assert np.allclose(plain.avgpool2(x), F.avg_pool2d(torch.from_numpy(x)[None], 2)[0].numpy(), atol=1e-14)
+    net = dict(layers=[("conv", 2, 3, 1, 1), ("act",), ("avgpool",), ("fc", 3)], input=(1, 6, 6))
+    W = [rng.normal(size=(2, 1, 3, 3)), rng.normal(size=(3, 18))]
+    img = rng.uniform(size=(1, 6, 6))
+    y = F.conv2d(torch.from_numpy(img)[None], torch.from_numpy(W[0]), padding=1)
+    y = 0.0 + 0.5 * y + 0.25 * y * y
+    y = F.avg_pool2d(y, 2).reshape(-1)
+    want = F.linear(y, torch.from_numpy(W[1])).numpy()
+    assert np.allclose(plain.forward(net, img, W, SN.ACT_COEFFS), want, atol=1e-12)
