@@ -473,8 +473,9 @@ extern "C" int hisa_ctx_create(const hisa_params* p, hisa_ctx** out) {
             const uint64_t w = pw[h_brv((uint32_t)k, c->log_n)], wi = pwi[h_brv((uint32_t)k, c->log_n)];
             fwd[(size_t)m * N + k] = make_ulonglong2(w, shoup(w, q));
             inv[(size_t)m * N + k] = make_ulonglong2(wi, shoup(wi, q));
-            fwd_d[(size_t)m * N + k] = (double)w;    // exact: w < q < 2^50 where used
-            inv_d[(size_t)m * N + k] = (double)wi;
+            // centred (|W| <= q/2; exact where used, q < 2^50): halves the mulred bound (ntt_f64.cuh)
+            fwd_d[(size_t)m * N + k] = w > q / 2 ? -(double)(q - w) : (double)w;
+            inv_d[(size_t)m * N + k] = wi > q / 2 ? -(double)(q - wi) : (double)wi;
         }
         const uint64_t ni = h_inv(N % q, q);
         ninv[m] = make_ulonglong2(ni, shoup(ni, q));
@@ -2365,12 +2366,12 @@ __global__ void __launch_bounds__(256) k_mb_butterfly_f64(double* out, double q,
     for (int e = 0; e < 16; e++) r[e] = (double)((threadIdx.x * 16 + e + blockIdx.x) % 1000003);
     for (int it = 0; it < iters; it++) {
 #pragma unroll
-        for (int st = 0; st < 4; st++) {
-            const int dist = 8 >> st;
+        for (int st = 0; st < 8; st++) {   // one 8-stage pass with the engines' lazy schedule
+            const int dist = 8 >> (st & 3);
 #pragma unroll
             for (int e = 0; e < 16; e++) {
                 if (e & dist) continue;
-                const double X = redd(r[e], q, qinv);
+                const double X = full_stage(st, 8) ? redd(r[e], q, qinv) : r[e];
                 const double T = mulred(r[e + dist], w, q, qinv);
                 r[e] = __dadd_rn(X, T);
                 r[e + dist] = __dsub_rn(X, T);
@@ -2408,7 +2409,7 @@ extern "C" int hisa_microbench_butterfly_f64(hisa_ctx* c, int iters, double* bfl
     c->ev_pool.push_back(a);
     c->ev_pool.push_back(b);
     dfree(c, out);
-    *bfly_per_s = (double)blocks * threads * iters * 32.0 / (t * 1e-3);
+    *bfly_per_s = (double)blocks * threads * iters * 64.0 / (t * 1e-3);
     return HISA_OK;
 }
 

@@ -14,12 +14,17 @@
 //   mulred(a, w)    = a w - qt q with qt = rint(fl(fl(a w) qinv)), computed exactly as
 //                     h = fl(a w); l = fma(a, w, -h) (= a w - h exactly); t = fma(-qt, q, h) + l
 //                     the FMA result h - qt q is an integer of magnitude < 2^53 (exact) and l is an
-//                     integer.  For |a| <= B q, 0 <= w < q: the quotient estimate has relative error
-//                     <= 3 2^-53, i.e. |qt - a w / q| <= 0.5 + 0.375 B, so |h - qt q| <= (0.5 + 0.375 B) q,
-//                     and |l| <= ulp(h)/2 <= 2^-53 B q^2 <= 0.125 B q  =>  |t| <= (0.5 + 0.5 B) q.
-// Forward CT butterfly (X, Y) -> (X' + t, X' - t), X' = red(X), t = mulred(Y, W):
-//   B_out = 0.5 + 0.5 + 0.5 B_in  -> fixed point B = 2 (inputs start at B <= 1): every value and
-//   every intermediate stays below 4 q^2 / 2^53 of ulp trouble; all magnitudes <= 2q < 2^51.
+//                     integer.  The quotient estimate errs by <= 0.5 + 2^-52 |h| / q and
+//                     |l| <= 2^-53 |a w|, so |t| <= q/2 + 1.5 2^-52 |a w|.  Twiddles are stored
+//                     centred (|W| <= q/2): |t| <= q/2 + 0.75 2^-52 |a| q, i.e. for |a| <= B q,
+//                     q < 2^50: |t| <= (0.5 + 3/16 B) q.  (tests/test_f64_arith.py)
+// Forward CT butterfly (X, Y) -> (X' + t, X' - t), t = mulred(Y, W), on a lazy schedule
+// (full_stage): a "full" stage re-centres X' = red(X), B' = 1 + 3/16 B; the other stages add X
+// unreduced, B' = 19/16 B + 1/2.  Full stages are u % 3 == 0 and the pass's last stage, so from
+// any pass input B <= 3.3 (or any |v| <= 2^50, e.g. a lifted wider residue: stage 0 is full) the
+// magnitudes stay <= 3.3 q < 2^51.8 and every pass output is <= 1.6 q
+// (8 stages: 1.19, 1.91, 2.77 | 1.52, 2.30, 3.23 | 1.61, 1.30 from B = 1): 4 of 8 stages skip
+// the 3-op re-centring of X (9.5 instead of 11 FP64 ops per butterfly on average).
 // Inverse GS butterfly (X, Y) -> (red(X + Y), mulred(red(X - Y), W)):
 //   |red(X - Y)| <= 0.5q (+eps)  =>  |t| <= 0.75 q; B_out <= 0.75 for any number of stages.
 //   (Without re-centring the difference, B would grow by q/2 per stage: 16 stages could exceed
@@ -73,6 +78,10 @@ __device__ __forceinline__ uint64_t d_rep4(double v, double two_q_plus_2p52) {
     return (uint64_t)__double_as_longlong(__dadd_rn(v, two_q_plus_2p52)) & 0xFFFFFFFFFFFFFull;
 }
 
+// the lazy forward schedule: stage u of a pass re-centres X (a "full" butterfly) only when
+// u % 3 == 0 or u is the pass's last stage; the other stages add X unreduced (header: bounds)
+__host__ __device__ constexpr bool full_stage(int u, int log_m) { return u % 3 == 0 || u == log_m - 1; }
+
 // forward CT stages [s0, s0 + LOG_M) on doubles in smem; mirrors fwd_engine (ntt.cuh) with
 // the FP64 butterfly; tw = doubles W = psi^brv(k) mod q
 template <int LOG_M, int LOG_R>
@@ -109,7 +118,7 @@ __device__ __forceinline__ void fwd_engine_f64(double* sm, double q, double qinv
                     for (int e0 = 0; e0 < G::R; e0++) {
                         if (e0 >= dist) break;
                         const int e = k * 2 * dist + e0;
-                        const double X = redd(reg[e], q, qinv);
+                        const double X = full_stage(u, LOG_M) ? redd(reg[e], q, qinv) : reg[e];
                         const double T = mulred(reg[e + dist], W, q, qinv);
                         reg[e] = __dadd_rn(X, T);
                         reg[e + dist] = __dsub_rn(X, T);
@@ -160,7 +169,7 @@ __device__ __forceinline__ void fwd_engine_f64_rowtw(double* sm, double q, doubl
                     for (int e0 = 0; e0 < G::R; e0++) {
                         if (e0 >= dist) break;
                         const int e = k * 2 * dist + e0;
-                        const double X = redd(reg[e], q, qinv);
+                        const double X = full_stage(u, LOG_M) ? redd(reg[e], q, qinv) : reg[e];
                         const double T = mulred(reg[e + dist], W, q, qinv);
                         reg[e] = __dadd_rn(X, T);
                         reg[e + dist] = __dsub_rn(X, T);
@@ -214,7 +223,8 @@ __device__ __forceinline__ void fwd_engine_f64_rowtw2(double* sa, double* sb, do
                     for (int e0 = 0; e0 < G::R; e0++) {
                         if (e0 >= dist) break;
                         const int e = k * 2 * dist + e0;
-                        const double Xa = redd(ra[e], q, qinv), Xb = redd(rb[e], q, qinv);
+                        const bool fs = full_stage(u, LOG_M);
+                        const double Xa = fs ? redd(ra[e], q, qinv) : ra[e], Xb = fs ? redd(rb[e], q, qinv) : rb[e];
                         const double Ta = mulred(ra[e + dist], W, q, qinv), Tb = mulred(rb[e + dist], W, q, qinv);
                         ra[e] = __dadd_rn(Xa, Ta);
                         rb[e] = __dadd_rn(Xb, Tb);
@@ -274,7 +284,7 @@ __device__ __forceinline__ void fwd_engine_f64_rowtwN(double* const* tiles, doub
                         const int e = k * 2 * dist + e0;
 #pragma unroll
                         for (int n = 0; n < NT; n++) {
-                            const double X = redd(r[n][e], q, qinv);
+                            const double X = full_stage(u, LOG_M) ? redd(r[n][e], q, qinv) : r[n][e];
                             const double T = mulred(r[n][e + dist], W, q, qinv);
                             r[n][e] = __dadd_rn(X, T);
                             r[n][e + dist] = __dsub_rn(X, T);

@@ -63,31 +63,36 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
     const int nthr = GC > 0 ? GC * G::T : blockDim.x;
-    // coalesced asynchronous load, lanes along columns
     const int lg = GC > 0 ? ilog2c(GC) : __ffs(Gc) - 1;
+    const uint64_t Qs = LOADMODE == LOAD_LIFT ? tb.mods[job.smod_map[a]].q : 0;
+    if (fp && (LOADMODE != LOAD_LIFT || (double)Qs < tb.f64_max_q)) {
+        // FP64 limb: coalesced loads straight into registers, converted (and, for ModUp, lifted:
+        // x in [0, Qs) -> x - Qs if x > Qs/2, exact, |.| < 2^49 -- the engine's first stage
+        // re-centres any |v| < 8q) and stored once into the swizzled tile
+        double* smd = reinterpret_cast<double*>(sm);
+        const double qs = (double)Qs, half = (double)(Qs >> 1);
+        uint64_t v[G::R];
+#pragma unroll
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
+            v[k] = __ldg(&src[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))]);
+        }
+#pragma unroll
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
+            double d = u2d(v[k]);
+            if (LOADMODE == LOAD_LIFT) d = d > half ? __dsub_rn(d, qs) : d;
+            smd[G::addr(i & (Gc - 1), i >> lg)] = d;
+        }
+    } else {
+        // coalesced asynchronous load, lanes along columns
 #pragma unroll 4
-    for (int k = 0; k < G::R; k++) {
-        const int i = threadIdx.x + k * nthr;
-        cp_async8(&sm[G::addr(i & (Gc - 1), i >> lg)], &src[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))]);
-    }
-    cp_async_wait_all();
-    // each thread converts the words it copied
-    if (LOADMODE == LOAD_LIFT) {
-        const uint64_t Qs = tb.mods[job.smod_map[a]].q;
-        if (fp && (double)Qs < tb.f64_max_q) {
-            // FP64 centred lift: x in [0, Qs) -> x - Qs if x > Qs/2 (exact, |.| < 2^49), then
-            // reduced mod r into the centred-lazy range (ntt_f64.cuh)
-            const double2 qd = tb.modd[mi];
-            const double qs = (double)Qs, half = (double)(Qs >> 1);
-#pragma unroll 4
-            for (int k = 0; k < G::R; k++) {
-                const int i = threadIdx.x + k * nthr;
-                double* p = reinterpret_cast<double*>(&sm[G::addr(i & (Gc - 1), i >> lg)]);
-                double v = u2d(*reinterpret_cast<const uint64_t*>(p));
-                v = v > half ? __dsub_rn(v, qs) : v;
-                *p = redd(v, qd.x, qd.y);
-            }
-        } else {
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
+            cp_async8(&sm[G::addr(i & (Gc - 1), i >> lg)], &src[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))]);
+        }
+        cp_async_wait_all();
+        if (LOADMODE == LOAD_LIFT) {   // integer lift (source or target >= 2^50)
 #pragma unroll 4
             for (int k = 0; k < G::R; k++) {
                 const int i = threadIdx.x + k * nthr;
@@ -96,13 +101,6 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
                 if (fp) *reinterpret_cast<double*>(p) = u2d(v);
                 else *p = v;
             }
-        }
-    } else if (fp) {
-#pragma unroll 4
-        for (int k = 0; k < G::R; k++) {
-            const int i = threadIdx.x + k * nthr;
-            uint64_t* p = &sm[G::addr(i & (Gc - 1), i >> lg)];
-            *reinterpret_cast<double*>(p) = u2d(*p);
         }
     }
     __syncthreads();
@@ -208,18 +206,22 @@ __global__ void __launch_bounds__(256, MINB) k_inv_rows(PassJob job, Tables tb) 
     const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
     const int nthr = FULL ? 256 : blockDim.x;   // FULL: compile-time, offsets fold
-#pragma unroll 4
-    for (int k = 0; k < G::R; k++) {
-        const int i = threadIdx.x + k * nthr;
-        cp_async8(&sm[G::addr(i >> LOG_M, i & (G::M - 1))], &src[i]);
-    }
-    cp_async_wait_all();
-    if (fp) {
+    if (fp) {   // FP64 limb: loads straight into registers, converted, stored once
+        uint64_t v[G::R];
+#pragma unroll
+        for (int k = 0; k < G::R; k++) v[k] = __ldg(&src[threadIdx.x + k * nthr]);
+#pragma unroll
+        for (int k = 0; k < G::R; k++) {
+            const int i = threadIdx.x + k * nthr;
+            reinterpret_cast<double*>(sm)[G::addr(i >> LOG_M, i & (G::M - 1))] = u2d(v[k]);
+        }
+    } else {
 #pragma unroll 4
         for (int k = 0; k < G::R; k++) {
-            uint64_t* p = &sm[G::addr((threadIdx.x + k * nthr) >> LOG_M, (threadIdx.x + k * nthr) & (G::M - 1))];
-            *reinterpret_cast<double*>(p) = u2d(*p);
+            const int i = threadIdx.x + k * nthr;
+            cp_async8(&sm[G::addr(i >> LOG_M, i & (G::M - 1))], &src[i]);
         }
+        cp_async_wait_all();
     }
     __syncthreads();
     int g, t;

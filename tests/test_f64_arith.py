@@ -87,3 +87,77 @@ def test_bit_conversions():
         assert d == float(x) and int(d) == x
         back = struct.unpack("<Q", struct.pack("<d", d + 4503599627370496.0))[0] & ((1 << 52) - 1)
         assert back == x
+
+
+def _full_stage(u: int, log_m: int) -> bool:
+    """ntt_f64.cuh full_stage: X is re-centred at stages u % 3 == 0 and at the pass's last stage."""
+    return u % 3 == 0 or u == log_m - 1
+
+
+def _bound_recurrence(log_m: int, b_in: float):
+    """The header's worst-case magnitude bounds (units of q) per stage, centred twiddles:
+    full stage B' = 1 + 3/16 B (+ eps), lazy stage B' = 19/16 B + 1/2."""
+    out, b = [], b_in
+    for u in range(log_m):
+        b = (1.0 + 0.1875 * b) if _full_stage(u, log_m) else (1.1875 * b + 0.5)
+        out.append(b * (1 + 2 ** -40))
+    return out
+
+
+@pytest.mark.parametrize("q", _primes_near_2_50())
+@pytest.mark.parametrize("log_m", [2, 4, 5, 6, 7, 8])
+def test_lazy_forward_schedule_exact_and_bounded(q, log_m):
+    """The forward engines' lazy schedule (centred twiddles |W| <= q/2, X left unreduced except at
+    full stages) over two chained passes: every value is an exact integer < 2^53 congruent to the
+    textbook butterfly's, magnitudes stay within the header's recurrence, and each pass's output is
+    <= 2q (the key inner product's d_rep4 precondition).  Operands: random, plus a greedy adversary
+    that picks the twiddle maximising |t| among extreme candidates at every butterfly."""
+    rng = random.Random(q * 7 + log_m)
+    qf, qinv = float(q), 1.0 / float(q)
+    M = 1 << log_m
+    half = (q - 1) // 2
+    cands = [half, -half, half - 1, -(half - 1), 1, -1]
+    for trial in range(6):
+        adversary = trial % 2 == 1
+        x = [float(rng.randrange(q)) for _ in range(M)]          # canonical input, B <= 1
+        xi = [int(v) % q for v in x]
+        b_in = 1.0
+        for _pass in range(2):
+            bounds = _bound_recurrence(log_m, b_in)
+            for u in range(log_m):
+                dist = M >> (u + 1)
+                full = _full_stage(u, log_m)
+                for blk in range(0, M, 2 * dist):
+                    w = rng.choice(cands) if not adversary else None
+                    for e in range(blk, blk + dist):
+                        X = redd(x[e], qf, qinv) if full else x[e]
+                        if adversary:   # the twiddle maximising |t| for this operand
+                            ts = [(abs(mulred(x[e + dist], float(c), qf, qinv)), c) for c in cands[:2]]
+                            w = max(ts)[1]
+                        t = mulred(x[e + dist], float(w), qf, qinv)
+                        assert t == int(t) and abs(t) < 2 ** 53
+                        ti = (xi[e + dist] * w) % q
+                        assert (int(t) - ti) % q == 0
+                        x[e], x[e + dist] = X + t, X - t
+                        xi[e], xi[e + dist] = (xi[e] + ti) % q, (xi[e] - ti) % q
+                top = max(abs(v) for v in x)
+                assert top < 2 ** 52.6 and top <= bounds[u] * q, (u, top / q, bounds[u])
+            assert all((int(v) - vi) % q == 0 for v, vi in zip(x, xi))
+            assert max(abs(v) for v in x) <= 2 * q
+            b_in = max(abs(v) for v in x) / q
+
+
+def test_lazy_schedule_accepts_wide_lift():
+    """ModUp lifts a 50-bit source residue (|v| < 2^49, centred) into a 40-bit target without a
+    separate reduction: the first (full) stage re-centres X and mulred's bound is absolute,
+    |t| <= q/2 + 0.75 2^-52 |a| q."""
+    q = [p for p in _primes_near_2_50() if p.bit_length() == 40][0]
+    qf, qinv = float(q), 1.0 / float(q)
+    rng = random.Random(5)
+    for _ in range(2000):
+        a = float(rng.randint(-(1 << 49), 1 << 49))
+        w = rng.randint(-((q - 1) // 2), (q - 1) // 2)
+        t = mulred(a, float(w), qf, qinv)
+        assert t == int(t) and (int(t) - int(a) * w) % q == 0
+        assert abs(t) <= q / 2 + 0.75 * 2 ** -52 * abs(a) * q + 1
+        assert abs(redd(a, qf, qinv)) <= 0.5 * q + 1
