@@ -2,6 +2,7 @@
 // (a8), ModUp and ModDown (a5).  See ntt.cuh for the decomposition.
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <type_traits>
 #include "ntt.cuh"
 #include "ntt_f64.cuh"
 #include "launch.h"
@@ -118,6 +119,120 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
         const int i = threadIdx.x + k * nthr;
         dst[(long long)(i >> lg) * M2 + col0 + (i & (Gc - 1))] = sm[G::addr(i & (Gc - 1), i >> lg)];   // lazy
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// forward pass 1 for M1 = 256 with radix-16 phases, register-direct (the N = 2^16 form): a CTA
+// owns 16 consecutive columns; thread (g = tid % 16, t = tid / 16) loads rows t + 16e (e < 16) of
+// column g straight into registers -- exactly phase 1's operands, and a warp's loads are two
+// 128-byte row segments -- runs phase 1 (stages 0-3) in registers, exchanges once through the
+// padded shared tile, runs phase 2 (stages 4-7) on rows 16t + e and stores them from registers
+// (again two 128-byte segments per warp store).  One shared-memory round trip per element
+// instead of three, one barrier.
+// ------------------------------------------------------------------------------------------
+template <typename V, bool FP>
+__device__ __forceinline__ void col_phase16(V (&r)[16], int u0, int ohigh, const void* twp, double q, double qinv,
+                                            uint64_t qi) {
+#pragma unroll
+    for (int uu = 0; uu < 4; uu++) {
+        const int u = u0 + uu;
+        const int dist = 8 >> uu;
+        const int tbase = (1 << u) + (ohigh << uu);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (k >= (1 << uu)) break;
+            if constexpr (FP) {
+                const double W = __ldg(reinterpret_cast<const double*>(twp) + tbase + k);
+#pragma unroll
+                for (int e0 = 0; e0 < 8; e0++) {
+                    if (e0 >= dist) break;
+                    const int e = k * 2 * dist + e0;
+                    const double X = full_stage(u, 8) ? redd(r[e], q, qinv) : r[e];
+                    const double T = mulred(r[e + dist], W, q, qinv);
+                    r[e] = __dadd_rn(X, T);
+                    r[e + dist] = __dsub_rn(X, T);
+                }
+            } else {
+                const ulonglong2 W = __ldg(reinterpret_cast<const ulonglong2*>(twp) + tbase + k);
+                const uint64_t q2 = 2 * qi;
+#pragma unroll
+                for (int e0 = 0; e0 < 8; e0++) {
+                    if (e0 >= dist) break;
+                    const int e = k * 2 * dist + e0;
+                    uint64_t X = r[e];
+                    X = X >= q2 ? X - q2 : X;
+                    const uint64_t Tm = mul_shoup_lazy(r[e + dist], W.x, W.y, qi);
+                    r[e] = X + Tm;
+                    r[e + dist] = X - Tm + q2;
+                }
+            }
+        }
+    }
+}
+
+template <bool FP, int LOADMODE>
+__device__ __forceinline__ void fwd_cols_r16_body(const PassJob& job, const Tables& tb, const uint64_t* src,
+                                                  uint64_t* dst, int mi, const Mod& md, int a, int col0, int M2) {
+    using G = Geo<8, 4>;
+    extern __shared__ uint64_t sm[];
+    const int g = threadIdx.x & 15, t = threadIdx.x >> 4;
+    using V = typename std::conditional<FP, double, uint64_t>::type;
+    V r[16];
+    {
+        uint64_t v[16];
+#pragma unroll
+        for (int e = 0; e < 16; e++) v[e] = __ldg(&src[(long long)(t + 16 * e) * M2 + col0 + g]);
+        const uint64_t Qs = LOADMODE == LOAD_LIFT ? tb.mods[job.smod_map[a]].q : 0;
+        const bool fast_lift = FP && (double)Qs < tb.f64_max_q;
+        const double qs = (double)Qs, half = (double)(Qs >> 1);
+#pragma unroll
+        for (int e = 0; e < 16; e++) {
+            if constexpr (FP) {
+                if (LOADMODE == LOAD_LIFT && !fast_lift) {
+                    r[e] = u2d(lift_centered(v[e], Qs, md));
+                } else {
+                    double d = u2d(v[e]);
+                    if (LOADMODE == LOAD_LIFT) d = d > half ? __dsub_rn(d, qs) : d;
+                    r[e] = d;
+                }
+            } else {
+                r[e] = LOADMODE == LOAD_LIFT ? lift_centered(v[e], Qs, md) : v[e];
+            }
+        }
+    }
+    const double2 qd = FP ? tb.modd[mi] : make_double2(0, 0);
+    const void* twp = FP ? (const void*)(tb.fwd_d + ((long long)mi << tb.log_n))
+                         : (const void*)(tb.fwd + ((long long)mi << tb.log_n));
+    col_phase16<V, FP>(r, 0, 0, twp, qd.x, qd.y, md.q);
+    V* tile = reinterpret_cast<V*>(sm);
+#pragma unroll
+    for (int e = 0; e < 16; e++) tile[G::addr(g, t + 16 * e)] = r[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; e++) r[e] = tile[G::addr(g, 16 * t + e)];
+    col_phase16<V, FP>(r, 4, t, twp, qd.x, qd.y, md.q);
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        uint64_t w;
+        if constexpr (FP) w = (uint64_t)__double_as_longlong(r[e]);
+        else w = r[e];
+        dst[(long long)(16 * t + e) * M2 + col0 + g] = w;   // lazy
+    }
+}
+
+template <int LOADMODE>
+__global__ void __launch_bounds__(256, 4) k_fwd_cols_r16(PassJob job, Tables tb) {
+    int a, b;
+    if (!job_limb(job, a, b)) return;
+    const int z = blockIdx.z;
+    const int M2 = 1 << (tb.log_n - 8);
+    const int col0 = blockIdx.x * 16;
+    const int mi = job.mod_map[b];
+    const Mod md = tb.mods[mi];
+    const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
+    uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
+    if (use_f64(md.q, tb)) fwd_cols_r16_body<true, LOADMODE>(job, tb, src, dst, mi, md, a, col0, M2);
+    else fwd_cols_r16_body<false, LOADMODE>(job, tb, src, dst, mi, md, a, col0, M2);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -324,6 +439,13 @@ static cudaError_t fwd_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     dim3 grid(gx, nlimbs, nz);
     constexpr int FULL = 256 / Geo<LOG_M, LOG_R>::T;
     const bool full = threads == 256;
+    if constexpr (LOG_M == 8 && LOG_R == 4) {
+        if (full && ntt_variant() != 2) {   // register-direct radix-16 form (variant 2: smem engine)
+            if (lift) k_fwd_cols_r16<LOAD_LIFT><<<grid, 256, smem, st>>>(job, tb);
+            else k_fwd_cols_r16<LOAD_PLAIN><<<grid, 256, smem, st>>>(job, tb);
+            return cudaGetLastError();
+        }
+    }
     if (lift) {
         if (full) k_fwd_cols<LOG_M, LOG_R, LOAD_LIFT, MINB, FULL><<<grid, threads, smem, st>>>(job, tb);
         else k_fwd_cols<LOG_M, LOG_R, LOAD_LIFT, MINB><<<grid, threads, smem, st>>>(job, tb);
