@@ -8,6 +8,7 @@
 // D never touches HBM in its NTT form; the key is streamed once per ciphertext.
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <type_traits>
 #include "ntt_f64.cuh"
 #include "launch.h"
 
@@ -347,6 +348,188 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
     }
 }
 
+// K4 register-direct (variant 80): the FP64 rows of k_ks_ip2 without the staging round trips.
+// M = 256 as four radix-4 phases over 64 threads: phase 0's operands (elements t + 64e) are
+// loaded from the pass-1 output straight into registers (a warp reads 256 contiguous bytes per
+// load), phases exchange through the swizzled shared tiles, and phase 3 leaves thread t holding
+// elements 4t + e, which are multiplied into the accumulators from registers with the key words
+// read as two 16-byte vectors.  Two digits in flight as in k_ks_ip2; the special prime's row
+// (integer engine) runs the k_ks_ip2 path.
+template <int MINB>
+__global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
+    constexpr int LOG_M = 8, LOG_R = 2;
+    using G = Geo<LOG_M, LOG_R>;
+    extern __shared__ uint64_t sm[];
+    uint64_t* sa = sm;
+    uint64_t* sb = sm + G::STRIDE;
+    double* tws = reinterpret_cast<double*>(sm + 2 * G::STRIDE);
+    const int nz = job.nz;
+    const int z = blockIdx.x % nz;
+    const int ri = blockIdx.y == 0 ? job.l1 : (int)blockIdx.y - 1;   // special prime first
+    const int l1 = job.l1;
+    const int nri = l1 + 1;
+    const int log_n = tb.log_n;
+    const int row0 = blockIdx.x / nz;
+    const long long off0 = (long long)row0 << LOG_M;
+    const int mi = job.mod_map[ri];
+    const Mod md = tb.mods[mi];
+    const bool fp = (double)md.q < tb.f64_max_q;
+    const int t = threadIdx.x;
+    const long long kstride_j = 2ll * (job.L + 1) << log_n;
+    const long long kstride_p = (long long)(job.L + 1) << log_n;
+    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
+    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
+    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
+    auto tile_src = [&](int j) -> const uint64_t* {
+        return (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
+                         : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
+    };
+    U128 acc0[4], acc1[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
+    if (!fp) {   // integer-engine row: staged engine, elements t + 64k
+        for (int j = 0; j < l1 + 1; j++) {
+            if (j == l1 && ri >= l1) break;
+            const int jj = j == l1 ? ri : j;
+            if (j < l1 && j == ri) continue;
+            const uint64_t* src = tile_src(jj);
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int i = t + k * 64;
+                const unsigned s_ = (unsigned)__cvta_generic_to_shared(&sa[G::addr(0, i)]);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_), "l"(src + i) : "memory");
+            }
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncthreads();
+            if (j < l1)
+                fwd_engine<LOG_M, LOG_R>(sa, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M, (uint32_t)row0, 0, t);
+            const uint64_t* kb = key_r + jj * kstride_j;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int i = t + k * 64;
+                const uint64_t D = sa[G::addr(0, i)];
+                mac128(acc0[k], D, __ldg(kb + i));
+                mac128(acc1[k], D, __ldg(kb + kstride_p + i));
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            out0[t + k * 64] = barrett128(acc0[k].lo, acc0[k].hi, md);
+            out1[t + k * 64] = barrett128(acc1[k].lo, acc1[k].hi, md);
+        }
+        return;
+    }
+    const double2 qd = tb.modd[mi];
+    const double q = qd.x, qinv = qd.y;
+    const double tq52 = __dadd_rn(2.0 * q, 4503599627370496.0);   // 2q + 2^52
+    {
+        const double* twg = tb.fwd_d + ((long long)mi << log_n);
+        const int s0 = log_n - LOG_M;
+        for (int idx = t + 1; idx < G::M; idx += 64) {
+            const int u = 31 - __clz(idx), m = idx - (1 << u);
+            tws[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
+        }
+    }
+    __syncthreads();
+    // ND digits (1 or 2) through the four phases, then MAC from registers
+    auto run = [&](auto nd_c, int ja, int jb) {
+        constexpr int ND = decltype(nd_c)::value;
+        double r[ND][4];
+        const uint64_t* src[2] = {tile_src(ja), tile_src(jb)};
+#pragma unroll
+        for (int n = 0; n < ND; n++)
+#pragma unroll
+            for (int e = 0; e < 4; e++) r[n][e] = __longlong_as_double((long long)__ldcs(src[n] + t + 64 * e));
+        uint64_t* tl[2] = {sa, sb};
+#pragma unroll
+        for (int ph = 0; ph < 4; ph++) {
+            const int u0 = 2 * ph;
+            const int lo_bit = 6 - u0;
+            const int olow = t & ((1 << lo_bit) - 1), ohigh = t >> lo_bit;
+            const int base = (ohigh << (lo_bit + 2)) | olow;
+            if (ph > 0) {
+#pragma unroll
+                for (int n = 0; n < ND; n++)
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        r[n][e] = reinterpret_cast<const double*>(tl[n])[G::addr(0, base | (e << lo_bit))];
+            }
+#pragma unroll
+            for (int uu = 0; uu < 2; uu++) {
+                const int u = u0 + uu;
+                const int dist = 2 >> uu;
+                const int tbase = (1 << u) + (ohigh << uu);
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    if (k >= (1 << uu)) break;
+                    const double W = tws[tbase + k];
+#pragma unroll
+                    for (int e0 = 0; e0 < 2; e0++) {
+                        if (e0 >= dist) break;
+                        const int e = k * 2 * dist + e0;
+#pragma unroll
+                        for (int n = 0; n < ND; n++) {
+                            const double X = full_stage(u, LOG_M) ? redd(r[n][e], q, qinv) : r[n][e];
+                            const double T = mulred(r[n][e + dist], W, q, qinv);
+                            r[n][e] = __dadd_rn(X, T);
+                            r[n][e + dist] = __dsub_rn(X, T);
+                        }
+                    }
+                }
+            }
+            if (ph < 3) {
+                if (ph == 0) __syncthreads();   // the previous round's phase-3 reads are done
+#pragma unroll
+                for (int n = 0; n < ND; n++)
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        reinterpret_cast<double*>(tl[n])[G::addr(0, base | (e << lo_bit))] = r[n][e];
+                __syncthreads();
+            }
+        }
+        // phase 3 left elements 4t + e in registers
+#pragma unroll
+        for (int n = 0; n < ND; n++) {
+            const uint64_t* kb = key_r + (n == 0 ? ja : jb) * kstride_j + 4 * t;
+            const ulonglong2 b0 = __ldg(reinterpret_cast<const ulonglong2*>(kb));
+            const ulonglong2 b1 = __ldg(reinterpret_cast<const ulonglong2*>(kb) + 1);
+            const ulonglong2 a0 = __ldg(reinterpret_cast<const ulonglong2*>(kb + kstride_p));
+            const ulonglong2 a1 = __ldg(reinterpret_cast<const ulonglong2*>(kb + kstride_p) + 1);
+            const uint64_t kbv[4] = {b0.x, b0.y, b1.x, b1.y}, kav[4] = {a0.x, a0.y, a1.x, a1.y};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const uint64_t D = d_rep4(r[n][e], tq52);
+                mac128(acc0[e], D, kbv[e]);
+                mac128(acc1[e], D, kav[e]);
+            }
+        }
+    };
+    const int n_nd = l1 - 1;                                  // fp rows: ri < l1
+    auto digit = [&](int idx) { return idx < ri ? idx : idx + 1; };
+    int idx = 0;
+    for (; idx + 1 < n_nd; idx += 2) run(std::integral_constant<int, 2>(), digit(idx), digit(idx + 1));
+    if (idx < n_nd) run(std::integral_constant<int, 1>(), digit(idx), digit(idx));
+    {   // the diagonal digit: d_ri, already in the NTT domain (canonical), elements 4t + e
+        const uint64_t* src = tile_src(ri) + 4 * t;
+        const ulonglong2 d0 = __ldg(reinterpret_cast<const ulonglong2*>(src));
+        const ulonglong2 d1 = __ldg(reinterpret_cast<const ulonglong2*>(src) + 1);
+        const uint64_t dv[4] = {d0.x, d0.y, d1.x, d1.y};
+        const uint64_t* kb = key_r + ri * kstride_j + 4 * t;
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            mac128(acc0[e], dv[e], __ldg(kb + e));
+            mac128(acc1[e], dv[e], __ldg(kb + kstride_p + e));
+        }
+    }
+    ulonglong2* o0 = reinterpret_cast<ulonglong2*>(out0 + 4 * t);
+    ulonglong2* o1 = reinterpret_cast<ulonglong2*>(out1 + 4 * t);
+    o0[0] = make_ulonglong2(barrett128(acc0[0].lo, acc0[0].hi, md), barrett128(acc0[1].lo, acc0[1].hi, md));
+    o0[1] = make_ulonglong2(barrett128(acc0[2].lo, acc0[2].hi, md), barrett128(acc0[3].lo, acc0[3].hi, md));
+    o1[0] = make_ulonglong2(barrett128(acc1[0].lo, acc1[0].hi, md), barrett128(acc1[1].lo, acc1[1].hi, md));
+    o1[1] = make_ulonglong2(barrett128(acc1[2].lo, acc1[2].hi, md), barrett128(acc1[3].lo, acc1[3].hi, md));
+}
+
 // K4 with NT digits in flight (variant 50+): generalises k_ks_ip2; the digits j != ri are taken
 // NT at a time (the last group may be smaller), then the diagonal digit
 template <int LOG_M, int LOG_R, int MINB, int NT>
@@ -462,6 +645,16 @@ static cudaError_t ks_ipN_t(const KsJob& job, const Tables& tb, int nz, cudaStre
     return cudaGetLastError();
 }
 
+template <int MINB>
+static cudaError_t ks_ip5_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+    using G = Geo<8, 2>;
+    const int rows = 1 << (tb.log_n - 8);
+    const size_t smem = (2 * (size_t)G::STRIDE + G::M) * sizeof(uint64_t);
+    dim3 grid(rows * nz, job.l1 + 1, 1);
+    k_ks_ip5<MINB><<<grid, 64, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+
 template <int LOG_M, int LOG_R, int MINB, bool PF = false>
 static cudaError_t ks_ip2_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     using G = Geo<LOG_M, LOG_R>;
@@ -501,11 +694,15 @@ static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStrea
         case 20: return ks_ip_pipe_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
         case 41: return ks_ip2_t<LOG_M, 2, 12, true>(job, tb, nz, st);
         case 55: return ks_ipN_t<LOG_M, 2, 12, 3>(job, tb, nz, st);
+        case 33: return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
+        case 80: if constexpr (LOG_M == 8) return ks_ip5_t<12>(job, tb, nz, st); break;
         default: break;
     }
-    // default = variant 33 (measured best on B200 at N = 2^16, L = 24: one row per 64-thread CTA,
-    // radix-4 phases, two digits interleaved through the FP64 engine with the row's twiddles
-    // staged in shared memory, >= 12 CTAs / SM; profiles/r1_ks_variants.txt)
+    // default (measured best on B200 at N = 2^16, L = 24; profiles/r1_ks_variants.txt): M = 256
+    // rows -> the register-direct two-digit kernel (variant 81, >= 10 CTAs / SM); other row
+    // lengths -> variant 33 (one row per 64-thread CTA, radix-4 phases, two digits interleaved
+    // through the FP64 engine with the row's twiddles staged in shared memory, >= 12 CTAs / SM)
+    if constexpr (LOG_M == 8) return ks_ip5_t<10>(job, tb, nz, st);
     return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
 }
 
