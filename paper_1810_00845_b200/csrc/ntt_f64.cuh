@@ -81,6 +81,9 @@ __device__ __forceinline__ uint64_t d_rep4(double v, double two_q_plus_2p52) {
 // the lazy forward schedule: stage u of a pass re-centres X (a "full" butterfly) only when
 // u % 3 == 0 or u is the pass's last stage; the other stages add X unreduced (header: bounds)
 __host__ __device__ constexpr bool full_stage(int u, int log_m) { return u % 3 == 0 || u == log_m - 1; }
+// column passes (whose outputs only feed a row pass, which starts with a full stage) may leave
+// the last stage lazy: outputs <= 2.41 q instead of 1.6 q (tests/test_f64_arith.py)
+__host__ __device__ constexpr bool full_stage_cols(int u) { return u % 3 == 0; }
 
 // forward CT stages [s0, s0 + LOG_M) on doubles in smem; mirrors fwd_engine (ntt.cuh) with
 // the FP64 butterfly; tw = doubles W = psi^brv(k) mod q

@@ -147,7 +147,7 @@ __device__ __forceinline__ void col_phase16(V (&r)[16], int u0, int ohigh, const
                 for (int e0 = 0; e0 < 8; e0++) {
                     if (e0 >= dist) break;
                     const int e = k * 2 * dist + e0;
-                    const double X = full_stage(u, 8) ? redd(r[e], q, qinv) : r[e];
+                    const double X = full_stage_cols(u) ? redd(r[e], q, qinv) : r[e];
                     const double T = mulred(r[e + dist], W, q, qinv);
                     r[e] = __dadd_rn(X, T);
                     r[e + dist] = __dsub_rn(X, T);
@@ -220,8 +220,8 @@ __device__ __forceinline__ void fwd_cols_r16_body(const PassJob& job, const Tabl
     }
 }
 
-template <int LOADMODE>
-__global__ void __launch_bounds__(256, 4) k_fwd_cols_r16(PassJob job, Tables tb) {
+template <int LOADMODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fwd_cols_r16(PassJob job, Tables tb) {
     int a, b;
     if (!job_limb(job, a, b)) return;
     const int z = blockIdx.z;
@@ -441,8 +441,8 @@ static cudaError_t fwd_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     const bool full = threads == 256;
     if constexpr (LOG_M == 8 && LOG_R == 4) {
         if (full && ntt_variant() != 2) {   // register-direct radix-16 form (variant 2: smem engine)
-            if (lift) k_fwd_cols_r16<LOAD_LIFT><<<grid, 256, smem, st>>>(job, tb);
-            else k_fwd_cols_r16<LOAD_PLAIN><<<grid, 256, smem, st>>>(job, tb);
+            if (lift) k_fwd_cols_r16<LOAD_LIFT, 4><<<grid, 256, smem, st>>>(job, tb);   // MINB 3: slower
+            else k_fwd_cols_r16<LOAD_PLAIN, 4><<<grid, 256, smem, st>>>(job, tb);
             return cudaGetLastError();
         }
     }

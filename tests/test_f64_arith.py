@@ -89,17 +89,19 @@ def test_bit_conversions():
         assert back == x
 
 
-def _full_stage(u: int, log_m: int) -> bool:
-    """ntt_f64.cuh full_stage: X is re-centred at stages u % 3 == 0 and at the pass's last stage."""
-    return u % 3 == 0 or u == log_m - 1
+def _full_stage(u: int, log_m: int, last_full: bool = True) -> bool:
+    """ntt_f64.cuh full_stage: X is re-centred at stages u % 3 == 0 and at the pass's last stage
+    (full_stage_cols, last_full=False: column passes, whose outputs feed a row pass, skip the
+    latter)."""
+    return u % 3 == 0 or (last_full and u == log_m - 1)
 
 
-def _bound_recurrence(log_m: int, b_in: float):
+def _bound_recurrence(log_m: int, b_in: float, last_full: bool = True):
     """The header's worst-case magnitude bounds (units of q) per stage, centred twiddles:
     full stage B' = 1 + 3/16 B (+ eps), lazy stage B' = 19/16 B + 1/2."""
     out, b = [], b_in
     for u in range(log_m):
-        b = (1.0 + 0.1875 * b) if _full_stage(u, log_m) else (1.1875 * b + 0.5)
+        b = (1.0 + 0.1875 * b) if _full_stage(u, log_m, last_full) else (1.1875 * b + 0.5)
         out.append(b * (1 + 2 ** -40))
     return out
 
@@ -123,10 +125,11 @@ def test_lazy_forward_schedule_exact_and_bounded(q, log_m):
         xi = [int(v) % q for v in x]
         b_in = 1.0
         for _pass in range(2):
-            bounds = _bound_recurrence(log_m, b_in)
+            last_full = _pass == 1          # pass 0 = a column pass (full_stage_cols)
+            bounds = _bound_recurrence(log_m, b_in, last_full)
             for u in range(log_m):
                 dist = M >> (u + 1)
-                full = _full_stage(u, log_m)
+                full = _full_stage(u, log_m, last_full)
                 for blk in range(0, M, 2 * dist):
                     w = rng.choice(cands) if not adversary else None
                     for e in range(blk, blk + dist):
@@ -143,7 +146,7 @@ def test_lazy_forward_schedule_exact_and_bounded(q, log_m):
                 top = max(abs(v) for v in x)
                 assert top < 2 ** 52.6 and top <= bounds[u] * q, (u, top / q, bounds[u])
             assert all((int(v) - vi) % q == 0 for v, vi in zip(x, xi))
-            assert max(abs(v) for v in x) <= 2 * q
+            assert max(abs(v) for v in x) <= (2 * q if last_full else 2.5 * q)
             b_in = max(abs(v) for v in x) / q
 
 
