@@ -130,14 +130,17 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
 // (again two 128-byte segments per warp store).  One shared-memory round trip per element
 // instead of three, one barrier.
 // ------------------------------------------------------------------------------------------
+// four radix-2 stages u0 .. u0 + 3 of a 256-point pass on 16 register operands (stride 8 >> uu);
+// twiddle index 2^(s0+u) + (high << u) + (ohigh << uu) + k as in fwd_engine.  FP64 stages re-centre
+// X at u % 3 == 0 only (outputs feed a pass that starts with a full stage, or a full reduction).
 template <typename V, bool FP>
 __device__ __forceinline__ void col_phase16(V (&r)[16], int u0, int ohigh, const void* twp, double q, double qinv,
-                                            uint64_t qi) {
+                                            uint64_t qi, int s0 = 0, uint32_t high = 0) {
 #pragma unroll
     for (int uu = 0; uu < 4; uu++) {
         const int u = u0 + uu;
         const int dist = 8 >> uu;
-        const int tbase = (1 << u) + (ohigh << uu);
+        const uint32_t tbase = (1u << (s0 + u)) + (high << u) + ((uint32_t)ohigh << uu);
 #pragma unroll
         for (int k = 0; k < 8; k++) {
             if (k >= (1 << uu)) break;
@@ -233,6 +236,82 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols_r16(PassJob job, Tables 
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
     if (use_f64(md.q, tb)) fwd_cols_r16_body<true, LOADMODE>(job, tb, src, dst, mi, md, a, col0, M2);
     else fwd_cols_r16_body<false, LOADMODE>(job, tb, src, dst, mi, md, a, col0, M2);
+}
+
+// forward pass 2 for M2 = 256, radix-16, register-direct load: thread (g = tid / 16, t = tid % 16)
+// of a 16-row tile loads elements t + 16e of row g straight into registers (two 128-byte segments
+// per warp load), phase 1 in registers, one exchange, phase 2, then the results go through the
+// shared tile once more so the (combining) stores stay coalesced.
+template <bool FP, int STOREMODE>
+__device__ __forceinline__ void fwd_rows_r16_body(const PassJob& job, const Tables& tb, const uint64_t* src,
+                                                  uint64_t* dst, int mi, const Mod& md, int a, int b, int z,
+                                                  int row0, long long off0) {
+    using G = Geo<8, 4>;
+    extern __shared__ uint64_t sm[];
+    const int g = threadIdx.x >> 4, t = threadIdx.x & 15;
+    using V = typename std::conditional<FP, double, uint64_t>::type;
+    V r[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const uint64_t w = __ldg(&src[g * 256 + t + 16 * e]);
+        if constexpr (FP) r[e] = __longlong_as_double((long long)w);   // lazy pass-1 doubles
+        else r[e] = w;
+    }
+    const double2 qd = FP ? tb.modd[mi] : make_double2(0, 0);
+    const void* twp = FP ? (const void*)(tb.fwd_d + ((long long)mi << tb.log_n))
+                         : (const void*)(tb.fwd + ((long long)mi << tb.log_n));
+    const int s0 = tb.log_n - 8;
+    const uint32_t high = (uint32_t)(row0 + g);
+    col_phase16<V, FP>(r, 0, 0, twp, qd.x, qd.y, md.q, s0, high);
+    V* tile = reinterpret_cast<V*>(sm);
+#pragma unroll
+    for (int e = 0; e < 16; e++) tile[G::addr(g, t + 16 * e)] = r[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; e++) r[e] = tile[G::addr(g, 16 * t + e)];
+    col_phase16<V, FP>(r, 4, t, twp, qd.x, qd.y, md.q, s0, high);
+#pragma unroll
+    for (int e = 0; e < 16; e++) tile[G::addr(g, 16 * t + e)] = r[e];
+    __syncthreads();
+    auto canon = [&](int idx) -> uint64_t {
+        if constexpr (FP) return d_canon(tile[idx], qd.x, qd.y);
+        else return reduce4(tile[idx], md.q);
+    };
+    if (STOREMODE == STORE_PLAIN) {
+#pragma unroll 4
+        for (int k = 0; k < 16; k++) {
+            const int i = threadIdx.x + k * 256;
+            dst[i] = canon(G::addr(i >> 8, i & 255));
+        }
+    } else {
+        const uint64_t* aux = job.aux[z] + a * job.aux_a + b * job.aux_b + off0;
+        const ulonglong2 cm = tb.comb[mi];
+        const bool has_add = job.add[z] != nullptr && a < job.aux_limit;
+        const uint64_t* add = has_add ? job.add[z] + a * job.add_a + b * job.add_b + off0 : nullptr;
+#pragma unroll 4
+        for (int k = 0; k < 16; k++) {
+            const int i = threadIdx.x + k * 256;
+            const uint64_t v = canon(G::addr(i >> 8, i & 255));
+            uint64_t rr = mul_shoup(sub_mod(aux[i], v, md.q), cm.x, cm.y, md.q);
+            if (has_add) rr = add_mod(rr, add[i], md.q);
+            dst[i] = rr;
+        }
+    }
+}
+
+template <int STOREMODE>
+__global__ void __launch_bounds__(256, 4) k_fwd_rows_r16(PassJob job, Tables tb) {
+    int a, b;
+    if (!job_limb(job, a, b)) return;
+    const int z = blockIdx.z;
+    const int row0 = blockIdx.x * 16;
+    const int mi = job.mod_map[b];
+    const Mod md = tb.mods[mi];
+    const long long off0 = (long long)row0 << 8;
+    const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b + off0;
+    uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + off0;
+    if (use_f64(md.q, tb)) fwd_rows_r16_body<true, STOREMODE>(job, tb, src, dst, mi, md, a, b, z, row0, off0);
+    else fwd_rows_r16_body<false, STOREMODE>(job, tb, src, dst, mi, md, a, b, z, row0, off0);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -460,6 +539,13 @@ static cudaError_t fwd_rows_v(const PassJob& job, const Tables& tb, int nlimbs, 
     int threads, gx; size_t smem;
     launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
     dim3 grid(gx, nlimbs, nz);
+    if constexpr (LOG_M == 8 && LOG_R == 4) {
+        if (threads == 256 && ntt_variant() != 2) {   // register-direct radix-16 form
+            if (combine) k_fwd_rows_r16<STORE_COMBINE><<<grid, 256, smem, st>>>(job, tb);
+            else k_fwd_rows_r16<STORE_PLAIN><<<grid, 256, smem, st>>>(job, tb);
+            return cudaGetLastError();
+        }
+    }
     if (threads == 256) {
         if (combine) k_fwd_rows<LOG_M, LOG_R, STORE_COMBINE, MINB, 1><<<grid, threads, smem, st>>>(job, tb);
         else k_fwd_rows<LOG_M, LOG_R, STORE_PLAIN, MINB, 1><<<grid, threads, smem, st>>>(job, tb);

@@ -108,7 +108,8 @@ def _bound_recurrence(log_m: int, b_in: float, last_full: bool = True):
 
 @pytest.mark.parametrize("q", _primes_near_2_50())
 @pytest.mark.parametrize("log_m", [2, 4, 5, 6, 7, 8])
-def test_lazy_forward_schedule_exact_and_bounded(q, log_m):
+@pytest.mark.parametrize("row_last_full", [True, False])
+def test_lazy_forward_schedule_exact_and_bounded(q, log_m, row_last_full):
     """The forward engines' lazy schedule (centred twiddles |W| <= q/2, X left unreduced except at
     full stages) over two chained passes: every value is an exact integer < 2^53 congruent to the
     textbook butterfly's, magnitudes stay within the header's recurrence, and each pass's output is
@@ -125,7 +126,9 @@ def test_lazy_forward_schedule_exact_and_bounded(q, log_m):
         xi = [int(v) % q for v in x]
         b_in = 1.0
         for _pass in range(2):
-            last_full = _pass == 1          # pass 0 = a column pass (full_stage_cols)
+            # pass 0 = a column pass (full_stage_cols); pass 1 = a row pass: full last stage
+            # (K4, whose d_rep4 needs <= 2q) or lazy (the register-direct rows, canonicalised)
+            last_full = _pass == 1 and row_last_full
             bounds = _bound_recurrence(log_m, b_in, last_full)
             for u in range(log_m):
                 dist = M >> (u + 1)
