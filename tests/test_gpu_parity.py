@@ -20,6 +20,9 @@ PARAMS = {
     "c1_n13": (13, [60, 40, 40], 60),
     "c2_n14": (14, [50] * 8, 60),
     "n15_odd": (15, [60, 40, 40, 40], 60),
+    # N = 2^16 runs the register-direct M = 256 kernels (k_fwd_cols_r16 / k_fwd_rows_r16 / K4
+    # k_ks_ip5); mixed 60 / 50 / 40-bit moduli: integer-engine rows and wide FP64 lifts
+    "n16_mixed": (16, [60, 50, 40, 50], 60),
 }
 SEED = 1234
 
@@ -167,7 +170,9 @@ def test_encode_encrypt_decrypt_bit_exact(pair):
         hd = g.decrypt(hc)
         od = o.decrypt(oc)
         assert (g.pt_export(hd) == od.data).all()
-        assert np.abs(g.decode(hd, n) - z).max() < 2.0 ** -20
+        # fresh-encryption noise in a slot grows ~ N (sqrt(N) coefficient noise x sqrt(N) slot sum;
+        # measured 1.1e-6 at N = 2^16, scale 2^40): 2^-20 up to N = 2^15, x N / 2^15 beyond
+        assert np.abs(g.decode(hd, n) - z).max() < 2.0 ** -20 * max(1, o.N >> 15)
         assert np.abs(g.decode(hd, n) - o.decode(od, n)).max() < 1e-12
 
 
@@ -189,14 +194,15 @@ def test_semantics_rotation_mul(pair):
     g, o = pair.g, pair.o
     z = np.random.default_rng(1).uniform(0, 1, o.slots)
     c = g.encrypt(g.encode(z, 2.0 ** 40))
+    grow = max(1, o.N >> 15)          # slot noise ~ N (see test_encode_encrypt_decrypt_bit_exact)
     for k in pair.rots:
         r = g.decode(g.decrypt(g.rot_left(c, k)), o.slots)
-        assert np.abs(r - np.roll(z, -k)).max() < 1e-6
+        assert np.abs(r - np.roll(z, -k)).max() < 1e-6 * grow
     if o.L >= 2:
         sq = g.rescale(g.mul(c, c))
         _, _, sc = g.ct_info(sq)
         # fresh-noise bound ~ N sigma ||s|| / scale; with 50-bit primes the rescaled scale is 2^30
-        tol = 1e-5 * max(1.0, 2.0 ** 40 / sc)
+        tol = 1e-5 * max(1.0, 2.0 ** 40 / sc) * grow
         assert np.abs(g.decode(g.decrypt(sq), o.slots) - z * z).max() < tol
 
 
