@@ -1,0 +1,207 @@
+// conv_tc_kernels.cu -- the conv accumulation (a9, K8) on the 5th-generation tensor cores.
+//
+//   out[o][x] = sum_t X[o][t] in[t][x]  mod q      (X: weight residues, in: ciphertext words)
+//
+// is a dense contraction (OC x T weights against T x words inputs), exact in integers.  Both
+// operands are split into P = ceil(log2 q / 8) unsigned bytes, a = sum_i a_i 2^(8i), x = sum_j
+// x_j 2^(8j), and the byte products are accumulated by tcgen05.mma.kind::i8 (u8 x u8 -> s32) in
+// tensor memory:
+//
+//   sum_t x a = sum_s 2^(8s) C_s,   C_s = sum_{i+j=s} sum_t a_i x_j   (s < 2P - 1)
+//
+// One CTA (128 threads, 4 warps) owns 128 consecutive words of one (poly, limb) -- the MMA's
+// M = 128 rows -- and a tile of 16 outputs.  Per K-chunk of 32 inputs t: every thread loads its
+// word of the 32 inputs (coalesced), splits them into the P byte planes A_i [128 x 32] written to
+// shared memory in the canonical K-major no-swizzle layout; the weight planes B [(j, o) = 16P rows
+// x 32] arrive pre-split from a host-built image; one elected thread issues P MMAs
+// D[:, 16 i + (16 j + o)] += A_i B^T, i.e. MMA i writes at TMEM column offset 16 i, so byte
+// product (i, j) lands in diagonal block s = i + j (no cross-term bookkeeping; TMEM is zeroed
+// first).  Epilogue: each thread reads its row's 2P - 1 diagonal sums (C_s < P T 255^2 < 2^31) and
+// forms sum_s C_s 2^(8s) as two 128-bit halves (s < 8, s >= 8), reduced with two Barrett steps.
+// Bit-exact integer arithmetic: the same residues as the FP64 / 128-bit CUDA-core kernel.
+#include <cuda_runtime.h>
+#include <cstdint>
+#include "launch.h"
+#include "modarith.cuh"
+
+namespace hisa {
+
+constexpr int CTC_ROWS = 128, CTC_K = 32, CTC_OT = 16;
+constexpr int CTC_PLANE = CTC_ROWS * CTC_K;   // bytes per A plane (4 KiB)
+constexpr int CTC_BIMG = 8 * 512;             // bytes per weight image slot (P <= 8)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// SM100 shared-memory matrix descriptor, K-major, no swizzle: core matrices of 8 rows x 16 bytes
+// stored contiguously (128 B); LBO = byte distance between the two K-halves of a 32-byte row
+// chunk, SBO = byte distance between 8-row groups; version 1 (bits 46-47).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+// instruction descriptor, kind::i8: D s32 (bits 4-5 = 2), A/B unsigned 8-bit, both K-major,
+// N >> 3 at bits 17-22, M >> 4 at bits 24-28
+__device__ __forceinline__ uint32_t umma_idesc_u8(int m, int n) {
+    return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_u8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t done = 0;
+    for (long long spin = 0; !done; spin++) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase)
+            : "memory");
+        if (spin > (1ll << 28)) __trap();   // never hang the device: fail loudly instead
+    }
+}
+__device__ __forceinline__ uint32_t pick_byte(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t i) {
+    // byte i (0..3) of each of a, b, c, d -> one word (a in the low byte)
+    const uint32_t sel = i | ((i + 4) << 4);
+    const uint32_t lo = __byte_perm(a, b, sel), hi = __byte_perm(c, d, sel);
+    return __byte_perm(lo, hi, 0x5410);
+}
+
+__global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restrict__ in_ptrs,
+                                                 uint64_t* const* __restrict__ out_ptrs,
+                                                 const uint8_t* __restrict__ wimg, ConvTcJob job,
+                                                 const Mod* __restrict__ mods) {
+    extern __shared__ __align__(1024) uint8_t ctc_sm[];
+    uint8_t* sA = ctc_sm;                       // [P][128 rows x 32 bytes], canonical K-major
+    uint8_t* sB = ctc_sm + 8 * CTC_PLANE;       // [16 P rows x 32 bytes]
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_slot;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const long long N = 1ll << job.log_n;
+    const int limb = job.limb_map[blockIdx.y];
+    const int P = job.P[limb];
+    const Mod md = mods[limb];
+    const long long off = (long long)blockIdx.z * job.poly_stride + (long long)limb * N + (long long)blockIdx.x * CTC_ROWS;
+    const uint32_t bar = smem_u32(&mbar);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = tmem_slot;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const int ndiag = 2 * P - 1;
+    const uint32_t idesc = umma_idesc_u8(CTC_ROWS, 16 * P);
+    const uint64_t bdesc = umma_desc(smem_u32(sB), 128, 256);
+    uint32_t phase = 0;
+    // this thread's row in the canonical layout: group tid / 8 at 256 B, row tid % 8 at 16 B
+    uint8_t* arow = sA + (tid >> 3) * 256 + (tid & 7) * 16;
+    for (int oct = 0; oct < job.n_oct; oct++) {
+        // zero this thread's TMEM lane over the diagonal blocks
+        for (int s = 0; s < ndiag; s++) {
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+                "%1, %1, %1, %1};\n" ::"r"(lane_base + 16 * s),
+                "r"(0u));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        for (int ch = 0; ch < job.n_chunks; ch++) {
+            // inputs: this thread's word of 32 inputs, split into byte planes
+            uint32_t lo[CTC_K], hi[CTC_K];
+#pragma unroll
+            for (int k = 0; k < CTC_K; k++) {
+                const int t = ch * CTC_K + k;
+                const uint64_t v = t < job.T ? __ldg(in_ptrs[t] + off + tid) : 0ull;
+                lo[k] = (uint32_t)v;
+                hi[k] = (uint32_t)(v >> 32);
+            }
+            for (int i = 0; i < P; i++) {
+                const uint32_t* src = i < 4 ? lo : hi;
+                const uint32_t bi = (uint32_t)(i & 3);
+                uint32_t w[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) w[u] = pick_byte(src[4 * u], src[4 * u + 1], src[4 * u + 2], src[4 * u + 3], bi);
+                *reinterpret_cast<uint4*>(arow + i * CTC_PLANE) = make_uint4(w[0], w[1], w[2], w[3]);        // k 0-15
+                *reinterpret_cast<uint4*>(arow + i * CTC_PLANE + 128) = make_uint4(w[4], w[5], w[6], w[7]);  // k 16-31
+            }
+            // weights: the pre-split image of (limb, output tile, chunk)
+            const uint4* wsrc = reinterpret_cast<const uint4*>(
+                wimg + (((size_t)limb * job.n_oct + oct) * job.n_chunks + ch) * CTC_BIMG);
+            for (int u = tid; u < 32 * P; u += 128) reinterpret_cast<uint4*>(sB)[u] = __ldg(wsrc + u);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncthreads();
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (tid == 0) {
+                for (int i = 0; i < P; i++)
+                    mma_u8(tmem + 16 * i, umma_desc(smem_u32(sA + i * CTC_PLANE), 128, 256), bdesc, idesc, 1u);
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+                             : "memory");
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        }
+        // epilogue: row tid, outputs oct*16 + o, in two groups of 8
+        const uint64_t* dummy = nullptr;
+        (void)dummy;
+        for (int og = 0; og < 2; og++) {
+            U128 accl[8], acch[8];
+#pragma unroll
+            for (int o = 0; o < 8; o++) { accl[o] = U128{0, 0}; acch[o] = U128{0, 0}; }
+            for (int s = 0; s < ndiag; s++) {
+                uint32_t r[8];
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                               "=r"(r[7])
+                             : "r"(lane_base + 16 * s + 8 * og));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                const int sh = 8 * (s & 7);
+#pragma unroll
+                for (int o = 0; o < 8; o++) {
+                    const uint64_t cv = (uint64_t)r[o];
+                    const uint64_t l = sh ? cv << sh : cv, h = sh ? cv >> (64 - sh) : 0;
+                    U128& a = s < 8 ? accl[o] : acch[o];
+                    a.lo += l;
+                    a.hi += h + (a.lo < l);
+                }
+            }
+#pragma unroll
+            for (int o = 0; o < 8; o++) {
+                const int oo = oct * CTC_OT + og * 8 + o;
+                if (oo >= job.OC) continue;
+                // value = accl + acch 2^64: reduce the high half first (accl.hi < 2^32, r < 2^60)
+                const uint64_t rh = barrett128(acch[o].lo, acch[o].hi, md);
+                out_ptrs[oo][off + tid] = barrett128(accl[o].lo, accl[o].hi + rh, md);
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+}
+
+size_t conv_tc_smem_bytes() { return 8 * CTC_PLANE + CTC_BIMG; }
+
+cudaError_t launch_conv_tc(const uint64_t* const* in_ptrs, uint64_t* const* out_ptrs, const uint8_t* wimg,
+                           const ConvTcJob& job, int nlimbs, const Mod* mods, cudaStream_t st) {
+    const long long N = 1ll << job.log_n;
+    if (N % CTC_ROWS) return cudaErrorInvalidValue;
+    const size_t smem = conv_tc_smem_bytes();
+    cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((unsigned)(N / CTC_ROWS), (unsigned)nlimbs, 2);
+    k_conv_tc<<<grid, 128, smem, st>>>(in_ptrs, out_ptrs, wimg, job, mods);
+    return cudaGetLastError();
+}
+
+}  // namespace hisa

@@ -2036,6 +2036,16 @@ __global__ void __launch_bounds__(256) k_conv_acc(const uint64_t* const* __restr
     }
 }
 
+// K8 engine: tensor cores (conv_tc_kernels.cu) by default; HISA_CONV_TC=0 selects the CUDA-core
+// kernel below (FP64 / 128-bit MACs), kept as the measured alternative
+static bool conv_tc_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("HISA_CONV_TC");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
 static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const double* W, size_t OC, double pt_scale,
                            hisa_ct* outs, uint64_t* dev_out) {
     CHECK_CTX(c);
@@ -2086,6 +2096,52 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
     dim3 grid((unsigned)((N / 2 + 255) / 256), 1, 2);
     const size_t smem = (size_t)T * sizeof(void*) + (size_t)CONV_OT * CONV_TT * 8;
     if (smem > 200 * 1024) return fail(HISA_E_PARAMS, "conv accumulation: T = %zu inputs too many", T);
+    if (conv_tc_enabled() && N % 128 == 0 && T <= 4096) {
+        // tensor-core path (conv_tc_kernels.cu): weight byte planes pre-split into the MMA's shared
+        // memory image per (limb, 16-output tile, 32-input chunk)
+        const int n_chunks = (int)((T + 31) / 32), n_oct = (int)((OC + 15) / 16);
+        const size_t slot = 8 * 512;
+        std::vector<uint8_t> img((size_t)l1 * n_oct * n_chunks * slot, 0);
+        ConvTcJob tj;
+        memset(&tj, 0, sizeof tj);
+        tj.T = (int)T; tj.OC = (int)OC; tj.log_n = c->log_n; tj.n_chunks = n_chunks; tj.n_oct = n_oct;
+        tj.poly_stride = (long long)l1 * N;
+        for (int i = 0; i < l1; i++) {
+            int P = 0;
+            for (uint64_t q = c->mod[i] - 1; q; q >>= 8) P++;
+            tj.P[i] = (uint8_t)P;
+            tj.limb_map[i] = (uint8_t)i;
+            for (int oct = 0; oct < n_oct; oct++)
+                for (int ch = 0; ch < n_chunks; ch++) {
+                    uint8_t* b = img.data() + (((size_t)i * n_oct + oct) * n_chunks + ch) * slot;
+                    for (int j = 0; j < P; j++)
+                        for (int ol = 0; ol < 16; ol++) {
+                            const size_t o = (size_t)oct * 16 + ol;
+                            const int n = j * 16 + ol;
+                            for (int k = 0; k < 32; k++) {
+                                const size_t t = (size_t)ch * 32 + k;
+                                const uint64_t w = (o < OC && t < T) ? wres[((size_t)i * OC + o) * T + t] : 0;
+                                b[(n / 8) * 256 + (k / 16) * 128 + (n % 8) * 16 + (k % 16)] = (uint8_t)(w >> (8 * j));
+                            }
+                        }
+                }
+        }
+        uint8_t* dimg = (uint8_t*)dalloc(c, img.size());
+        if (!dimg) return fail(HISA_E_OOM, "conv weight image");
+        CK(cudaMemcpyAsync(dimg, img.data(), img.size(), cudaMemcpyHostToDevice, c->stream));
+        {
+            ProfScope ps_(c, "conv_acc");
+            CK(launch_conv_tc(dip, dop, dimg, tj, l1, c->d_mods, c->stream));
+        }
+        CK(cudaStreamSynchronize(c->stream));
+        dfree(c, dimg);
+        dfree(c, dw);
+        dfree(c, (void*)dip);
+        dfree(c, (void*)dop);
+        if (outs)
+            for (size_t o = 0; o < OC; o++) outs[o] = new_handle(c, OBJ_CT, optr[o], level, 2, objs[0]->scale * ps);
+        return HISA_OK;
+    }
     for (int fpc = 0; fpc < 2; fpc++) {   // one launch per butterfly-engine class of limbs
         ConvJob j2 = cj;
         int n = 0;

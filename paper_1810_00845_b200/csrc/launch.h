@@ -96,6 +96,17 @@ struct KsJob {
 };
 cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st);
 
+// K8 on the tensor cores (conv_tc_kernels.cu): byte-split u8 x u8 -> s32 tcgen05 MMAs
+struct ConvTcJob {
+    int T, OC, log_n, n_chunks, n_oct;
+    long long poly_stride;
+    uint8_t limb_map[MAXL];       // grid.y -> limb
+    uint8_t P[MAXL];              // byte planes per limb: ceil(bits(q) / 8)
+};
+size_t conv_tc_smem_bytes();
+cudaError_t launch_conv_tc(const uint64_t* const* in_ptrs, uint64_t* const* out_ptrs, const uint8_t* wimg,
+                           const ConvTcJob& job, int nlimbs, const Mod* mods, cudaStream_t st);
+
 // GPU encode (NEXT-4, A7) -- encode_kernels.cu: double-double FFT + exact rounding with near-tie
 // flags.  dd = unevaluated sum hi + lo; cdd = complex.
 struct dd { double hi, lo; };
