@@ -29,6 +29,9 @@ namespace hisa {
 constexpr int CTC_ROWS = 128, CTC_K = 32, CTC_OT = 16;
 constexpr int CTC_PLANE = CTC_ROWS * CTC_K;   // bytes per A plane (4 KiB)
 constexpr int CTC_BIMG = 8 * 512;             // bytes per weight image slot (P <= 8)
+constexpr int CTC_TMEM = 256;                 // TMEM columns per CTA (two CTAs per SM)
+constexpr int CTC_MAXG = 1;                   // output tiles per pass (TMEM: G (2P - 1) 16 <= CTC_TMEM;
+                                              // 512 columns / 3 tiles measured slower: one CTA per SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -54,12 +57,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
     for (long long spin = 0; !done; spin++) {
         asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}\n"
             : "=r"(done)
             : "r"(bar), "r"(phase)
             : "memory");
-        if (spin > (1ll << 28)) __trap();   // never hang the device: fail loudly instead
+        if (spin > (1ll << 22)) __trap();   // never hang the device: fail loudly instead
     }
 }
 __device__ __forceinline__ uint32_t pick_byte(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t i) {
@@ -74,9 +77,11 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
                                                  const uint8_t* __restrict__ wimg, ConvTcJob job,
                                                  const Mod* __restrict__ mods) {
     extern __shared__ __align__(1024) uint8_t ctc_sm[];
-    uint8_t* sA = ctc_sm;                       // [P][128 rows x 32 bytes], canonical K-major
-    uint8_t* sB = ctc_sm + 8 * CTC_PLANE;       // [16 P rows x 32 bytes]
-    __shared__ __align__(8) uint64_t mbar;
+    // two buffers: buffer b = [P planes of A, 128 rows x 32 bytes][B: 16 P rows x 32 bytes]
+    constexpr int BUF = 8 * CTC_PLANE + CTC_MAXG * CTC_BIMG;
+    // the T input pointers (offset to this tile) staged once, after the two operand buffers
+    const uint64_t** sptr = reinterpret_cast<const uint64_t**>(ctc_sm + 2 * BUF);
+    __shared__ __align__(8) uint64_t mbar[2];
     __shared__ uint32_t tmem_slot;
     const int tid = threadIdx.x, warp = tid >> 5;
     const long long N = 1ll << job.log_n;
@@ -84,13 +89,15 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
     const int P = job.P[limb];
     const Mod md = mods[limb];
     const long long off = (long long)blockIdx.z * job.poly_stride + (long long)limb * N + (long long)blockIdx.x * CTC_ROWS;
-    const uint32_t bar = smem_u32(&mbar);
+    const uint32_t bar0 = smem_u32(&mbar[0]), bar1 = smem_u32(&mbar[1]);
+    for (int t = tid; t < job.T; t += 128) sptr[t] = in_ptrs[t] + off;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar1));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -100,13 +107,16 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
     const int ndiag = 2 * P - 1;
     const uint32_t idesc = umma_idesc_u8(CTC_ROWS, 16 * P);
-    const uint64_t bdesc = umma_desc(smem_u32(sB), 128, 256);
-    uint32_t phase = 0;
+    uint32_t ph0 = 0, ph1 = 0;
+    bool pend0 = false, pend1 = false;
     // this thread's row in the canonical layout: group tid / 8 at 256 B, row tid % 8 at 16 B
-    uint8_t* arow = sA + (tid >> 3) * 256 + (tid & 7) * 16;
-    for (int oct = 0; oct < job.n_oct; oct++) {
-        // zero this thread's TMEM lane over the diagonal blocks
-        for (int s = 0; s < ndiag; s++) {
+    const int arow_off = (tid >> 3) * 256 + (tid & 7) * 16;
+    // G output tiles per pass share every input split (TMEM holds G x (2P - 1) x 16 columns)
+    const int G = min(CTC_MAXG, CTC_TMEM / (16 * ndiag));
+    for (int oct0 = 0; oct0 < job.n_oct; oct0 += G) {
+        const int ng = min(G, job.n_oct - oct0);
+        // zero this thread's TMEM lane over the diagonal blocks of the pass
+        for (int s = 0; s < ng * ndiag; s++) {
             asm volatile(
                 "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
                 "%1, %1, %1, %1};\n" ::"r"(lane_base + 16 * s),
@@ -114,46 +124,59 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
         }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         for (int ch = 0; ch < job.n_chunks; ch++) {
-            // inputs: this thread's word of 32 inputs, split into byte planes
+            const int b = ch & 1;
+            uint8_t* sA = ctc_sm + b * BUF;
+            uint8_t* sB = sA + 8 * CTC_PLANE;
+            // inputs of this chunk (loads in flight while the other buffer's MMAs run)
             uint32_t lo[CTC_K], hi[CTC_K];
 #pragma unroll
             for (int k = 0; k < CTC_K; k++) {
                 const int t = ch * CTC_K + k;
-                const uint64_t v = t < job.T ? __ldg(in_ptrs[t] + off + tid) : 0ull;
+                const uint64_t v = t < job.T ? __ldg(sptr[t] + tid) : 0ull;
                 lo[k] = (uint32_t)v;
                 hi[k] = (uint32_t)(v >> 32);
             }
+            // the MMAs that last read this buffer (chunk ch - 2) must be complete
+            if (b == 0 && pend0) { mbar_wait(bar0, ph0); ph0 ^= 1; pend0 = false; }
+            if (b == 1 && pend1) { mbar_wait(bar1, ph1); ph1 ^= 1; pend1 = false; }
             for (int i = 0; i < P; i++) {
                 const uint32_t* src = i < 4 ? lo : hi;
                 const uint32_t bi = (uint32_t)(i & 3);
                 uint32_t w[8];
 #pragma unroll
                 for (int u = 0; u < 8; u++) w[u] = pick_byte(src[4 * u], src[4 * u + 1], src[4 * u + 2], src[4 * u + 3], bi);
-                *reinterpret_cast<uint4*>(arow + i * CTC_PLANE) = make_uint4(w[0], w[1], w[2], w[3]);        // k 0-15
-                *reinterpret_cast<uint4*>(arow + i * CTC_PLANE + 128) = make_uint4(w[4], w[5], w[6], w[7]);  // k 16-31
+                *reinterpret_cast<uint4*>(sA + i * CTC_PLANE + arow_off) = make_uint4(w[0], w[1], w[2], w[3]);        // k 0-15
+                *reinterpret_cast<uint4*>(sA + i * CTC_PLANE + arow_off + 128) = make_uint4(w[4], w[5], w[6], w[7]);  // k 16-31
             }
-            // weights: the pre-split image of (limb, output tile, chunk)
-            const uint4* wsrc = reinterpret_cast<const uint4*>(
-                wimg + (((size_t)limb * job.n_oct + oct) * job.n_chunks + ch) * CTC_BIMG);
-            for (int u = tid; u < 32 * P; u += 128) reinterpret_cast<uint4*>(sB)[u] = __ldg(wsrc + u);
+            // weights: the pre-split images of (limb, output tile, chunk) for the pass's tiles
+            for (int g = 0; g < ng; g++) {
+                const uint4* wsrc = reinterpret_cast<const uint4*>(
+                    wimg + (((size_t)limb * job.n_oct + oct0 + g) * job.n_chunks + ch) * CTC_BIMG);
+                for (int u = tid; u < 32 * P; u += 128) reinterpret_cast<uint4*>(sB + g * CTC_BIMG)[u] = __ldg(wsrc + u);
+            }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncthreads();
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             if (tid == 0) {
-                for (int i = 0; i < P; i++)
-                    mma_u8(tmem + 16 * i, umma_desc(smem_u32(sA + i * CTC_PLANE), 128, 256), bdesc, idesc, 1u);
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
-                             : "memory");
+                for (int g = 0; g < ng; g++) {
+                    const uint64_t bdesc = umma_desc(smem_u32(sB + g * CTC_BIMG), 128, 256);
+                    for (int i = 0; i < P; i++)
+                        mma_u8(tmem + 16 * (g * ndiag + i), umma_desc(smem_u32(sA + i * CTC_PLANE), 128, 256), bdesc,
+                               idesc, 1u);
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                             ::"r"(b ? bar1 : bar0) : "memory");
             }
-            mbar_wait(bar, phase);
-            phase ^= 1;
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (b == 0) pend0 = true; else pend1 = true;
         }
-        // epilogue: row tid, outputs oct*16 + o, in two groups of 8
-        const uint64_t* dummy = nullptr;
-        (void)dummy;
-        for (int og = 0; og < 2; og++) {
+        if (pend0) { mbar_wait(bar0, ph0); ph0 ^= 1; pend0 = false; }
+        if (pend1) { mbar_wait(bar1, ph1); ph1 ^= 1; pend1 = false; }
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        // epilogue: row tid, outputs (oct0 + g) * 16 + o, in halves of 8
+        for (int gh = 0; gh < 2 * ng; gh++) {
+            const int g = gh >> 1, og = gh & 1;
+            const int oct = oct0 + g;
             U128 accl[8], acch[8];
 #pragma unroll
             for (int o = 0; o < 8; o++) { accl[o] = U128{0, 0}; acch[o] = U128{0, 0}; }
@@ -162,7 +185,7 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
                 asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
                              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
                                "=r"(r[7])
-                             : "r"(lane_base + 16 * s + 8 * og));
+                             : "r"(lane_base + 16 * (g * ndiag + s) + 8 * og));
                 asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
                 const int sh = 8 * (s & 7);
 #pragma unroll
@@ -191,13 +214,13 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
 }
 
-size_t conv_tc_smem_bytes() { return 8 * CTC_PLANE + CTC_BIMG; }
+size_t conv_tc_smem_bytes(int T) { return 2 * (8 * CTC_PLANE + CTC_MAXG * CTC_BIMG) + (size_t)T * sizeof(void*); }
 
 cudaError_t launch_conv_tc(const uint64_t* const* in_ptrs, uint64_t* const* out_ptrs, const uint8_t* wimg,
                            const ConvTcJob& job, int nlimbs, const Mod* mods, cudaStream_t st) {
     const long long N = 1ll << job.log_n;
     if (N % CTC_ROWS) return cudaErrorInvalidValue;
-    const size_t smem = conv_tc_smem_bytes();
+    const size_t smem = conv_tc_smem_bytes(job.T);
     cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)(N / CTC_ROWS), (unsigned)nlimbs, 2);
     k_conv_tc<<<grid, 128, smem, st>>>(in_ptrs, out_ptrs, wimg, job, mods);

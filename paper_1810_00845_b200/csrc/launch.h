@@ -103,7 +103,7 @@ struct ConvTcJob {
     uint8_t limb_map[MAXL];       // grid.y -> limb
     uint8_t P[MAXL];              // byte planes per limb: ceil(bits(q) / 8)
 };
-size_t conv_tc_smem_bytes();
+size_t conv_tc_smem_bytes(int T);
 cudaError_t launch_conv_tc(const uint64_t* const* in_ptrs, uint64_t* const* out_ptrs, const uint8_t* wimg,
                            const ConvTcJob& job, int nlimbs, const Mod* mods, cudaStream_t st);
 
