@@ -214,6 +214,44 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
 }
 
+// weight image on the device: X = llround(W[o][t] * ps) (C semantics: half away from zero; exact
+// -- |v| < 2^52 makes v +- 0.5 exact, larger |v| are integers), residue X mod q_limb in [0, q), byte
+// j -> slot (limb, output tile, chunk) at row n = 16 j + o_local, column k, canonical K-major
+// no-swizzle layout (the MMA's B operand image).  One thread per image byte.
+__global__ void k_conv_tc_wimg(const double* __restrict__ W, double ps, int T, int OC, int n_oct, int n_chunks,
+                               const Mod* __restrict__ mods, const uint8_t* __restrict__ Pl, uint8_t* img,
+                               long long total) {
+    const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (id >= total) return;
+    const int byte = (int)(id % CTC_BIMG);
+    long long slot = id / CTC_BIMG;
+    const int ch = (int)(slot % n_chunks);
+    slot /= n_chunks;
+    const int oct = (int)(slot % n_oct);
+    const int limb = (int)(slot / n_oct);
+    // invert the canonical layout: byte = (n / 8) 256 + (k / 16) 128 + (n % 8) 16 + k % 16
+    const int n = (byte / 256) * 8 + (byte % 128) / 16, k = ((byte % 256) / 128) * 16 + byte % 16;
+    const int j = n / 16, o = oct * 16 + n % 16, t = ch * 32 + k;
+    uint8_t out = 0;
+    if (j < Pl[limb] && o < OC && t < T) {
+        const double v = W[(long long)o * T + t] * ps;
+        const double r = fabs(v) >= 4503599627370496.0 ? v : trunc(v + copysign(0.5, v));
+        const long long X = (long long)r;
+        const long long q = (long long)mods[limb].q;
+        long long m = X % q;
+        if (m < 0) m += q;
+        out = (uint8_t)((unsigned long long)m >> (8 * j));
+    }
+    img[id] = out;
+}
+
+cudaError_t launch_conv_tc_wimg(const double* W, double ps, int T, int OC, int n_oct, int n_chunks, int l1,
+                                const Mod* mods, const uint8_t* Pl, uint8_t* img, cudaStream_t st) {
+    const long long total = (long long)l1 * n_oct * n_chunks * CTC_BIMG;
+    k_conv_tc_wimg<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(W, ps, T, OC, n_oct, n_chunks, mods, Pl, img, total);
+    return cudaGetLastError();
+}
+
 size_t conv_tc_smem_bytes(int T) { return 2 * (8 * CTC_PLANE + CTC_MAXG * CTC_BIMG) + (size_t)T * sizeof(void*); }
 
 cudaError_t launch_conv_tc(const uint64_t* const* in_ptrs, uint64_t* const* out_ptrs, const uint8_t* wimg,

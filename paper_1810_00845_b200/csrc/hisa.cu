@@ -2060,18 +2060,14 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
     }
     const int level = objs[0]->level, l1 = level + 1;
     const double ps = pt_scale == 0.0 ? (double)c->mod[level] : pt_scale;
-    std::vector<uint64_t> wres((size_t)OC * T * l1);   // [limb][OC][T]
-    for (size_t o = 0; o < OC; o++)
-        for (size_t t = 0; t < T; t++) {
-            const double v = W[o * T + t] * ps;
-            if (!std::isfinite(v) || fabs(v) >= 0x1p62) return fail(HISA_E_PARAMS, "weight out of range");
-            const long long X = llround(v);
-            for (int i = 0; i < l1; i++) {
-                const uint64_t q = c->mod[i];
-                wres[((size_t)i * OC + o) * T + t] = (uint64_t)(((__int128)X % (__int128)q + q) % q);
-            }
-        }
+    for (size_t i = 0; i < OC * T; i++) {
+        const double v = W[i] * ps;
+        if (!std::isfinite(v) || fabs(v) >= 0x1p62) return fail(HISA_E_PARAMS, "weight out of range");
+    }
     const long long N = (long long)c->N;
+    const bool use_tc = conv_tc_enabled() && N % 128 == 0 && T <= 4096;
+    if (!use_tc && (size_t)T * sizeof(void*) + (size_t)CONV_OT * CONV_TT * 8 > 200 * 1024)
+        return fail(HISA_E_PARAMS, "conv accumulation: T = %zu inputs too many", T);
     std::vector<uint64_t*> optr(OC);
     for (size_t o = 0; o < OC; o++) {
         optr[o] = dev_out ? dev_out + (size_t)o * 2 * l1 * N : dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
@@ -2079,29 +2075,15 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
     }
     std::vector<const uint64_t*> iptr(T);
     for (size_t t = 0; t < T; t++) iptr[t] = objs[t]->ptr;
-    uint64_t* dw = dalloc_t<uint64_t>(c, wres.size());
     const uint64_t** dip = (const uint64_t**)dalloc(c, T * sizeof(void*));
     uint64_t** dop = (uint64_t**)dalloc(c, OC * sizeof(void*));
-    if (!dw || !dip || !dop) return fail(HISA_E_OOM, "conv scratch");
-    CK(cudaMemcpyAsync(dw, wres.data(), wres.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    if (!dip || !dop) return fail(HISA_E_OOM, "conv scratch");
     CK(cudaMemcpyAsync(dip, iptr.data(), T * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dop, optr.data(), OC * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
-    uint64_t qmax = 0;
-    for (int i = 0; i < l1; i++) qmax = std::max(qmax, c->mod[i]);
-    const double terms = std::ldexp(1.0, 127) / ((double)qmax * (double)qmax);   // 128-bit headroom
-    ConvJob cj;
-    memset(&cj, 0, sizeof cj);
-    cj.T = (int)T; cj.OC = (int)OC; cj.l1 = l1; cj.log_n = c->log_n; cj.poly_stride = (long long)l1 * N;
-    cj.red_every = (int)std::min(1024.0, std::floor(terms) - 1);
-    dim3 grid((unsigned)((N / 2 + 255) / 256), 1, 2);
-    const size_t smem = (size_t)T * sizeof(void*) + (size_t)CONV_OT * CONV_TT * 8;
-    if (smem > 200 * 1024) return fail(HISA_E_PARAMS, "conv accumulation: T = %zu inputs too many", T);
-    if (conv_tc_enabled() && N % 128 == 0 && T <= 4096) {
-        // tensor-core path (conv_tc_kernels.cu): weight byte planes pre-split into the MMA's shared
-        // memory image per (limb, 16-output tile, 32-input chunk)
+    if (use_tc) {
+        // tensor-core path (conv_tc_kernels.cu): weights rounded, reduced and byte-split into the
+        // MMA's shared-memory image per (limb, 16-output tile, 32-input chunk) on the device
         const int n_chunks = (int)((T + 31) / 32), n_oct = (int)((OC + 15) / 16);
-        const size_t slot = 8 * 512;
-        std::vector<uint8_t> img((size_t)l1 * n_oct * n_chunks * slot, 0);
         ConvTcJob tj;
         memset(&tj, 0, sizeof tj);
         tj.T = (int)T; tj.OC = (int)OC; tj.log_n = c->log_n; tj.n_chunks = n_chunks; tj.n_oct = n_oct;
@@ -2111,37 +2093,50 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
             for (uint64_t q = c->mod[i] - 1; q; q >>= 8) P++;
             tj.P[i] = (uint8_t)P;
             tj.limb_map[i] = (uint8_t)i;
-            for (int oct = 0; oct < n_oct; oct++)
-                for (int ch = 0; ch < n_chunks; ch++) {
-                    uint8_t* b = img.data() + (((size_t)i * n_oct + oct) * n_chunks + ch) * slot;
-                    for (int j = 0; j < P; j++)
-                        for (int ol = 0; ol < 16; ol++) {
-                            const size_t o = (size_t)oct * 16 + ol;
-                            const int n = j * 16 + ol;
-                            for (int k = 0; k < 32; k++) {
-                                const size_t t = (size_t)ch * 32 + k;
-                                const uint64_t w = (o < OC && t < T) ? wres[((size_t)i * OC + o) * T + t] : 0;
-                                b[(n / 8) * 256 + (k / 16) * 128 + (n % 8) * 16 + (k % 16)] = (uint8_t)(w >> (8 * j));
-                            }
-                        }
-                }
         }
-        uint8_t* dimg = (uint8_t*)dalloc(c, img.size());
-        if (!dimg) return fail(HISA_E_OOM, "conv weight image");
-        CK(cudaMemcpyAsync(dimg, img.data(), img.size(), cudaMemcpyHostToDevice, c->stream));
+        const size_t img_bytes = (size_t)l1 * n_oct * n_chunks * 8 * 512;
+        uint8_t* dimg = (uint8_t*)dalloc(c, img_bytes);
+        double* dW = dalloc_t<double>(c, OC * T);
+        uint8_t* dP = (uint8_t*)dalloc(c, MAXL);
+        if (!dimg || !dW || !dP) return fail(HISA_E_OOM, "conv weight image");
+        CK(cudaMemcpyAsync(dW, W, OC * T * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(dP, tj.P, MAXL, cudaMemcpyHostToDevice, c->stream));
         {
             ProfScope ps_(c, "conv_acc");
+            CK(launch_conv_tc_wimg(dW, ps, (int)T, (int)OC, n_oct, n_chunks, l1, c->d_mods, dP, dimg, c->stream));
             CK(launch_conv_tc(dip, dop, dimg, tj, l1, c->d_mods, c->stream));
         }
-        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaStreamSynchronize(c->stream));   // host staging vectors must outlive the copies
         dfree(c, dimg);
-        dfree(c, dw);
+        dfree(c, (void*)dW);
+        dfree(c, (void*)dP);
         dfree(c, (void*)dip);
         dfree(c, (void*)dop);
         if (outs)
             for (size_t o = 0; o < OC; o++) outs[o] = new_handle(c, OBJ_CT, optr[o], level, 2, objs[0]->scale * ps);
         return HISA_OK;
     }
+    std::vector<uint64_t> wres((size_t)OC * T * l1);   // [limb][OC][T]
+    for (size_t o = 0; o < OC; o++)
+        for (size_t t = 0; t < T; t++) {
+            const long long X = llround(W[o * T + t] * ps);
+            for (int i = 0; i < l1; i++) {
+                const uint64_t q = c->mod[i];
+                wres[((size_t)i * OC + o) * T + t] = (uint64_t)(((__int128)X % (__int128)q + q) % q);
+            }
+        }
+    uint64_t* dw = dalloc_t<uint64_t>(c, wres.size());
+    if (!dw) return fail(HISA_E_OOM, "conv scratch");
+    CK(cudaMemcpyAsync(dw, wres.data(), wres.size() * 8, cudaMemcpyHostToDevice, c->stream));
+    uint64_t qmax = 0;
+    for (int i = 0; i < l1; i++) qmax = std::max(qmax, c->mod[i]);
+    const double terms = std::ldexp(1.0, 127) / ((double)qmax * (double)qmax);   // 128-bit headroom
+    ConvJob cj;
+    memset(&cj, 0, sizeof cj);
+    cj.T = (int)T; cj.OC = (int)OC; cj.l1 = l1; cj.log_n = c->log_n; cj.poly_stride = (long long)l1 * N;
+    cj.red_every = (int)std::min(1024.0, std::floor(terms) - 1);
+    dim3 grid((unsigned)((N / 2 + 255) / 256), 1, 2);
+    const size_t smem = (size_t)T * sizeof(void*) + (size_t)CONV_OT * CONV_TT * 8;
     for (int fpc = 0; fpc < 2; fpc++) {   // one launch per butterfly-engine class of limbs
         ConvJob j2 = cj;
         int n = 0;
