@@ -24,13 +24,18 @@
 #include "launch.h"
 #include "modarith.cuh"
 
+#ifndef CTC_TMEM_COLS
+#define CTC_TMEM_COLS 256
+#define CTC_MAXG_TILES 1
+#endif
+
 namespace hisa {
 
 constexpr int CTC_ROWS = 128, CTC_K = 32, CTC_OT = 16;
 constexpr int CTC_PLANE = CTC_ROWS * CTC_K;   // bytes per A plane (4 KiB)
 constexpr int CTC_BIMG = 8 * 512;             // bytes per weight image slot (P <= 8)
-constexpr int CTC_TMEM = 256;                 // TMEM columns per CTA (two CTAs per SM)
-constexpr int CTC_MAXG = 1;                   // output tiles per pass (TMEM: G (2P - 1) 16 <= CTC_TMEM;
+constexpr int CTC_TMEM = CTC_TMEM_COLS;       // TMEM columns per CTA
+constexpr int CTC_MAXG = CTC_MAXG_TILES;      // output tiles per pass (TMEM: G (2P - 1) 16 <= CTC_TMEM;
                                               // 512 columns / 3 tiles measured slower: one CTA per SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
     const uint32_t bar0 = smem_u32(&mbar[0]), bar1 = smem_u32(&mbar[1]);
     for (int t = tid; t < job.T; t += 128) sptr[t] = in_ptrs[t] + off;
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(&tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)), "n"(CTC_TMEM));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     }
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(CTC_TMEM));
 }
 
 // weight image on the device: X = llround(W[o][t] * ps) (C semantics: half away from zero; exact
