@@ -118,3 +118,47 @@ def test_gpu_encode_exact_ties():
     assert (g.pt_export(hs[0]) == o.encode(np.full(g.slots, 2.5), 2.0 ** 40).data).all()
     assert (g.pt_export(hs[1]) == o.encode(np.linspace(-1, 1, g.slots), 2.0 ** 40).data).all()
     g.close()
+
+
+_ENGINE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_1810_00845_b200 import hisa as H
+g = H.Context(16, [60, 50, 40], 60, seed=4, arena_bytes=8 << 30)
+rng = np.random.default_rng(2)
+T, OC = 45, 19                      # ragged chunk (32 + 13) and output tile (16 + 3)
+hs = [g.ct_random(t, 2) for t in range(T)]
+W = rng.normal(0, 0.3, (OC, T))
+W[0, :] = -W[1, :]                  # negative residues (all byte planes set)
+outs = g.conv_accumulate(hs, W.ravel(), 2.0 ** 30)
+np.save(sys.argv[1], np.stack([g.ct_export(h) for h in outs]))
+"""
+
+
+def test_conv_engines_bit_identical(tmp_path):
+    """K8 on the tensor cores (default) and on the CUDA cores (HISA_CONV_TC=0, read once per
+    process) give the same words, at N = 2^16 with 60 / 50 / 40-bit limbs (8 / 7 / 5 byte planes),
+    a ragged input chunk and a ragged output tile; the tensor-core result also equals the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for tc in ("1", "0"):
+        out = tmp_path / f"conv_{tc}.npy"
+        env = dict(os.environ, HISA_CONV_TC=tc)
+        subprocess.run([sys.executable, "-c", _ENGINE_SCRIPT % root, str(out)], env=env, check=True, timeout=600)
+        res[tc] = np.load(out)
+    assert res["1"].shape == res["0"].shape and (res["1"] == res["0"]).all()
+    o = Oracle(16, [60, 50, 40], 60, seed=4)
+    rng = np.random.default_rng(2)
+    T, OC = 45, 19
+    W = rng.normal(0, 0.3, (OC, T))
+    W[0, :] = -W[1, :]
+    cts = [o.bench_ct(t, 2) for t in range(T)]
+    for oc in (0, 7, 18):
+        acc = None
+        for t in range(T):
+            term = o.mul_scalar(cts[t], float(W[oc, t]), 2.0 ** 30)
+            acc = term if acc is None else o.add(acc, term)
+        assert (res["1"][oc] == acc.data).all(), oc
