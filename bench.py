@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--no-hoisted", action="store_true")
     ap.add_argument("--no-inference", action="store_true")
     ap.add_argument("--hoist-r", type=int, default=8, help="rotation amounts per hoisted ModUp")
-    ap.add_argument("--nets", default="tiny,lenet_small", help="encrypted-inference configs to time")
+    ap.add_argument("--nets", default="tiny,lenet_small,lenet_large", help="encrypted-inference configs to time")
     ap.add_argument("--oracle-nets", default="tiny,lenet_small",
                     help="configs whose oracle inference latency is timed on the host cores (cpu_baseline)")
     ap.add_argument("--tiling", default="lenet_large",
