@@ -31,7 +31,7 @@
 
 namespace hisa {
 
-constexpr int CTC_ROWS = 128, CTC_K = 32, CTC_OT = 16;
+constexpr int CTC_ROWS = 128, CTC_K = 32, CTC_OT = 16, CTC_THREADS = 256;
 constexpr int CTC_PLANE = CTC_ROWS * CTC_K;   // bytes per A plane (4 KiB)
 constexpr int CTC_BIMG = 8 * 512;             // bytes per weight image slot (P <= 8)
 constexpr int CTC_TMEM = CTC_TMEM_COLS;       // TMEM columns per CTA
@@ -77,7 +77,7 @@ __device__ __forceinline__ uint32_t pick_byte(uint32_t a, uint32_t b, uint32_t c
     return __byte_perm(lo, hi, 0x5410);
 }
 
-__global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restrict__ in_ptrs,
+__global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* __restrict__ in_ptrs,
                                                  uint64_t* const* __restrict__ out_ptrs,
                                                  const uint8_t* __restrict__ wimg, ConvTcJob job,
                                                  const Mod* __restrict__ mods) {
@@ -86,100 +86,107 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
     constexpr int BUF = 8 * CTC_PLANE + CTC_MAXG * CTC_BIMG;
     // the T input pointers (offset to this tile) staged once, after the two operand buffers
     const uint64_t** sptr = reinterpret_cast<const uint64_t**>(ctc_sm + 2 * BUF);
-    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ __align__(8) uint64_t mbar[1];
     __shared__ uint32_t tmem_slot;
-    const int tid = threadIdx.x, warp = tid >> 5;
+    // two warpgroups: warpgroup wg splits the K-chunks 2 step + wg into its own operand buffer;
+    // thread r = tid % 128 owns row r (TMEM lane r: warp w reads lanes 32 (w % 4) ..)
+    const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, r = tid & 127;
     const long long N = 1ll << job.log_n;
     const int limb = job.limb_map[blockIdx.y];
     const int P = job.P[limb];
     const Mod md = mods[limb];
     const long long off = (long long)blockIdx.z * job.poly_stride + (long long)limb * N + (long long)blockIdx.x * CTC_ROWS;
-    const uint32_t bar0 = smem_u32(&mbar[0]), bar1 = smem_u32(&mbar[1]);
-    for (int t = tid; t < job.T; t += 128) sptr[t] = in_ptrs[t] + off;
+    const uint32_t bar0 = smem_u32(&mbar[0]);
+    for (int t = tid; t < job.T; t += CTC_THREADS) sptr[t] = in_ptrs[t] + off;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)), "n"(CTC_TMEM));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar0));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar1));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_slot;
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const int ndiag = 2 * P - 1;
     const uint32_t idesc = umma_idesc_u8(CTC_ROWS, 16 * P);
-    uint32_t ph0 = 0, ph1 = 0;
-    bool pend0 = false, pend1 = false;
-    // this thread's row in the canonical layout: group tid / 8 at 256 B, row tid % 8 at 16 B
-    const int arow_off = (tid >> 3) * 256 + (tid & 7) * 16;
+    uint32_t ph0 = 0;
+    bool pend = false;
+    // this thread's row in the canonical layout: group r / 8 at 256 B, row r % 8 at 16 B
+    const int arow_off = (r >> 3) * 256 + (r & 7) * 16;
+    uint8_t* sA = ctc_sm + wg * BUF;
+    uint8_t* sB = sA + 8 * CTC_PLANE;
+    const int n_steps = (job.n_chunks + 1) / 2;
     // G output tiles per pass share every input split (TMEM holds G x (2P - 1) x 16 columns)
     const int G = min(CTC_MAXG, CTC_TMEM / (16 * ndiag));
     for (int oct0 = 0; oct0 < job.n_oct; oct0 += G) {
         const int ng = min(G, job.n_oct - oct0);
-        // zero this thread's TMEM lane over the diagonal blocks of the pass
-        for (int s = 0; s < ng * ndiag; s++) {
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
-                "%1, %1, %1, %1};\n" ::"r"(lane_base + 16 * s),
-                "r"(0u));
+        if (wg == 0) {   // zero the pass's diagonal blocks (warpgroup 0 covers all 128 lanes)
+            for (int s = 0; s < ng * ndiag; s++) {
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+                    "%1, %1, %1, %1};\n" ::"r"(lane_base + 16 * s),
+                    "r"(0u));
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        for (int ch = 0; ch < job.n_chunks; ch++) {
-            const int b = ch & 1;
-            uint8_t* sA = ctc_sm + b * BUF;
-            uint8_t* sB = sA + 8 * CTC_PLANE;
-            // inputs of this chunk (loads in flight while the other buffer's MMAs run)
+        for (int step = 0; step < n_steps; step++) {
+            const int ch = 2 * step + wg;
+            const bool active = ch < job.n_chunks;
+            // this warpgroup's chunk: loads in flight before waiting for the previous step's MMAs
             uint32_t lo[CTC_K], hi[CTC_K];
 #pragma unroll
             for (int k = 0; k < CTC_K; k++) {
                 const int t = ch * CTC_K + k;
-                const uint64_t v = t < job.T ? __ldg(sptr[t] + tid) : 0ull;
+                const uint64_t v = (active && t < job.T) ? __ldg(sptr[t] + r) : 0ull;
                 lo[k] = (uint32_t)v;
                 hi[k] = (uint32_t)(v >> 32);
             }
-            // the MMAs that last read this buffer (chunk ch - 2) must be complete
-            if (b == 0 && pend0) { mbar_wait(bar0, ph0); ph0 ^= 1; pend0 = false; }
-            if (b == 1 && pend1) { mbar_wait(bar1, ph1); ph1 ^= 1; pend1 = false; }
-            for (int i = 0; i < P; i++) {
-                const uint32_t* src = i < 4 ? lo : hi;
-                const uint32_t bi = (uint32_t)(i & 3);
-                uint32_t w[8];
+            if (pend) { mbar_wait(bar0, ph0); ph0 ^= 1; pend = false; }
+            if (active) {
+                for (int i = 0; i < P; i++) {
+                    const uint32_t* src = i < 4 ? lo : hi;
+                    const uint32_t bi = (uint32_t)(i & 3);
+                    uint32_t w[8];
 #pragma unroll
-                for (int u = 0; u < 8; u++) w[u] = pick_byte(src[4 * u], src[4 * u + 1], src[4 * u + 2], src[4 * u + 3], bi);
-                *reinterpret_cast<uint4*>(sA + i * CTC_PLANE + arow_off) = make_uint4(w[0], w[1], w[2], w[3]);        // k 0-15
-                *reinterpret_cast<uint4*>(sA + i * CTC_PLANE + arow_off + 128) = make_uint4(w[4], w[5], w[6], w[7]);  // k 16-31
-            }
-            // weights: the pre-split images of (limb, output tile, chunk) for the pass's tiles
-            for (int g = 0; g < ng; g++) {
-                const uint4* wsrc = reinterpret_cast<const uint4*>(
-                    wimg + (((size_t)limb * job.n_oct + oct0 + g) * job.n_chunks + ch) * CTC_BIMG);
-                for (int u = tid; u < 32 * P; u += 128) reinterpret_cast<uint4*>(sB + g * CTC_BIMG)[u] = __ldg(wsrc + u);
+                    for (int u = 0; u < 8; u++)
+                        w[u] = pick_byte(src[4 * u], src[4 * u + 1], src[4 * u + 2], src[4 * u + 3], bi);
+                    *reinterpret_cast<uint4*>(sA + i * CTC_PLANE + arow_off) = make_uint4(w[0], w[1], w[2], w[3]);
+                    *reinterpret_cast<uint4*>(sA + i * CTC_PLANE + arow_off + 128) = make_uint4(w[4], w[5], w[6], w[7]);
+                }
+                // weights: the pre-split images of (limb, output tile, chunk) for the pass's tiles
+                for (int g = 0; g < ng; g++) {
+                    const uint4* wsrc = reinterpret_cast<const uint4*>(
+                        wimg + (((size_t)limb * job.n_oct + oct0 + g) * job.n_chunks + ch) * CTC_BIMG);
+                    for (int u = r; u < 32 * P; u += 128) reinterpret_cast<uint4*>(sB + g * CTC_BIMG)[u] = __ldg(wsrc + u);
+                }
             }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncthreads();
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             if (tid == 0) {
-                for (int g = 0; g < ng; g++) {
-                    const uint64_t bdesc = umma_desc(smem_u32(sB + g * CTC_BIMG), 128, 256);
-                    for (int i = 0; i < P; i++)
-                        mma_u8(tmem + 16 * (g * ndiag + i), umma_desc(smem_u32(sA + i * CTC_PLANE), 128, 256), bdesc,
-                               idesc, 1u);
+                for (int h = 0; h < 2 && 2 * step + h < job.n_chunks; h++) {
+                    uint8_t* a_ = ctc_sm + h * BUF;
+                    for (int g = 0; g < ng; g++) {
+                        const uint64_t bdesc = umma_desc(smem_u32(a_ + 8 * CTC_PLANE + g * CTC_BIMG), 128, 256);
+                        for (int i = 0; i < P; i++)
+                            mma_u8(tmem + 16 * (g * ndiag + i), umma_desc(smem_u32(a_ + i * CTC_PLANE), 128, 256),
+                                   bdesc, idesc, 1u);
+                    }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-                             ::"r"(b ? bar1 : bar0) : "memory");
+                             ::"r"(bar0) : "memory");
             }
-            if (b == 0) pend0 = true; else pend1 = true;
+            pend = true;
         }
-        if (pend0) { mbar_wait(bar0, ph0); ph0 ^= 1; pend0 = false; }
-        if (pend1) { mbar_wait(bar1, ph1); ph1 ^= 1; pend1 = false; }
+        if (pend) { mbar_wait(bar0, ph0); ph0 ^= 1; pend = false; }
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         // epilogue: row tid, outputs (oct0 + g) * 16 + o, in halves of 8
-        for (int gh = 0; gh < 2 * ng; gh++) {
+        for (int gh = wg; gh < 2 * ng; gh += 2) {   // warpgroup wg: halves og = wg
             const int g = gh >> 1, og = gh & 1;
             const int oct = oct0 + g;
             U128 accl[8], acch[8];
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(128) k_conv_tc(const uint64_t* const* __restri
                 if (oo >= job.OC) continue;
                 // value = accl + acch 2^64: reduce the high half first (accl.hi < 2^32, r < 2^60)
                 const uint64_t rh = barrett128(acch[o].lo, acch[o].hi, md);
-                out_ptrs[oo][off + tid] = barrett128(accl[o].lo, accl[o].hi + rh, md);
+                out_ptrs[oo][off + r] = barrett128(accl[o].lo, accl[o].hi + rh, md);
             }
         }
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -266,7 +273,7 @@ cudaError_t launch_conv_tc(const uint64_t* const* in_ptrs, uint64_t* const* out_
     const size_t smem = conv_tc_smem_bytes(job.T);
     cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)(N / CTC_ROWS), (unsigned)nlimbs, 2);
-    k_conv_tc<<<grid, 128, smem, st>>>(in_ptrs, out_ptrs, wimg, job, mods);
+    k_conv_tc<<<grid, CTC_THREADS, smem, st>>>(in_ptrs, out_ptrs, wimg, job, mods);
     return cudaGetLastError();
 }
 
