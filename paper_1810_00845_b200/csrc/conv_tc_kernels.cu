@@ -60,14 +60,15 @@ __device__ __forceinline__ void mma_u8(uint32_t d_tmem, uint64_t a, uint64_t b, 
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
-    for (long long spin = 0; !done; spin++) {
+    const long long t0 = clock64();
+    while (!done) {
         asm volatile(
             "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}\n"
             : "=r"(done)
             : "r"(bar), "r"(phase)
             : "memory");
-        if (spin > (1ll << 22)) __trap();   // never hang the device: fail loudly instead
+        if (!done && clock64() - t0 > (1ll << 32)) __trap();   // ~2 s: never hang the device, fail loudly
     }
 }
 __device__ __forceinline__ uint32_t pick_byte(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t i) {
