@@ -151,11 +151,20 @@ __global__ void __launch_bounds__(256) k_automorphism(PtrPack pk, int log_n) {
     uint64_t* out = pk.out[z] + ((long long)limb << log_n);
     const uint64_t* add = pk.add[z] ? pk.add[z] + ((long long)limb << log_n) : nullptr;
     const uint64_t q = add ? pk.mods[limb % pk.nl].q : 0;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+    // word pairs (j, j + 1), j even: their sources are the pair (s, s ^ 1) -- j and j + 1 differ in
+    // the top bit of brev(j), which moves (e - 1) / 2 by N / 2 (g odd), i.e. flips bit 0 of the
+    // source -- so both directions are 16-byte accesses
+    for (uint32_t j = 2 * (blockIdx.x * blockDim.x + threadIdx.x); j < N; j += 2 * gridDim.x * blockDim.x) {
         const uint32_t bj = __brev(j) >> (32 - log_n);
         const uint64_t e = ((2ull * bj + 1) * g) & mask2n;
         const uint32_t src = __brev((uint32_t)((e - 1) >> 1)) >> (32 - log_n);
-        out[j] = add ? add_mod(in[src], add[j], q) : in[src];
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(in + (src & ~1u));
+        ulonglong2 o = (src & 1) ? make_ulonglong2(v.y, v.x) : v;
+        if (add) {
+            const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(add + j);
+            o = make_ulonglong2(add_mod(o.x, a.x, q), add_mod(o.y, a.y, q));
+        }
+        *reinterpret_cast<ulonglong2*>(out + j) = o;
     }
 }
 
@@ -177,7 +186,7 @@ cudaError_t launch_automorphism_add(const uint64_t* const* in, uint64_t* const* 
             pz.out[z] += ((long long)l0 << log_n);
             if (pz.add[z]) pz.add[z] += ((long long)l0 << log_n);
         }
-        dim3 grid((N + 255) / 256, nlc, nz);
+        dim3 grid((N / 2 + 255) / 256, nlc, nz);
         k_automorphism<<<grid, 256, 0, st>>>(pz, log_n);
     }
     return cudaGetLastError();
@@ -194,7 +203,7 @@ cudaError_t launch_automorphism(const uint64_t* const* in, uint64_t* const* out,
         const int nl = nlimbs_total - l0 < 65535 ? nlimbs_total - l0 : 65535;
         PtrPack pz = pk;
         for (int z = 0; z < nz; z++) { pz.in[z] += ((long long)l0 << log_n); pz.out[z] += ((long long)l0 << log_n); }
-        dim3 grid((N + 255) / 256, nl, nz);
+        dim3 grid((N / 2 + 255) / 256, nl, nz);
         k_automorphism<<<grid, 256, 0, st>>>(pz, log_n);
     }
     return cudaGetLastError();
