@@ -574,11 +574,9 @@ static cudaError_t inv_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     else k_inv_cols<LOG_M, LOG_R, MINB><<<grid, threads, smem, st>>>(job, tb);
     return cudaGetLastError();
 }
-#define NTT_DISPATCH(FN, ...)                                                   \
-    switch (ntt_variant()) {                                                    \
-        case 1: return FN<LM, 4, 1>(__VA_ARGS__);                               \
-        default: return FN<LM, 4, 4>(__VA_ARGS__);  /* measured best: radix-16, 4 CTAs/SM */ \
-    }
+// radix-16 phases, __launch_bounds__(256, 4): measured best (MINB 1 / radix-4 variants removed,
+// profiles/r1_ks_variants.txt); HISA_NTT_VARIANT=2 selects the shared-memory engine at M = 256
+#define NTT_DISPATCH(FN, ...) return FN<LM, 4, 4>(__VA_ARGS__);
 template <int LM>
 static cudaError_t fwd_cols_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, int lift, cudaStream_t st) {
     NTT_DISPATCH(fwd_cols_v, job, tb, nlimbs, nz, lift, st)
