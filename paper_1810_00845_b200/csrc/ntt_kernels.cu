@@ -277,11 +277,13 @@ __device__ __forceinline__ void fwd_rows_r16_body(const PassJob& job, const Tabl
         if constexpr (FP) return d_canon(tile[idx], qd.x, qd.y);
         else return reduce4(tile[idx], md.q);
     };
+    // word pairs (i, i + 1) of one row: 16-byte loads of the combine inputs and 16-byte stores
     if (STOREMODE == STORE_PLAIN) {
 #pragma unroll 4
-        for (int k = 0; k < 16; k++) {
-            const int i = threadIdx.x + k * 256;
-            dst[i] = canon(G::addr(i >> 8, i & 255));
+        for (int k = 0; k < 8; k++) {
+            const int i = 2 * (threadIdx.x + k * 256);
+            *reinterpret_cast<ulonglong2*>(dst + i) =
+                make_ulonglong2(canon(G::addr(i >> 8, i & 255)), canon(G::addr(i >> 8, (i & 255) + 1)));
         }
     } else {
         const uint64_t* aux = job.aux[z] + a * job.aux_a + b * job.aux_b + off0;
@@ -289,12 +291,18 @@ __device__ __forceinline__ void fwd_rows_r16_body(const PassJob& job, const Tabl
         const bool has_add = job.add[z] != nullptr && a < job.aux_limit;
         const uint64_t* add = has_add ? job.add[z] + a * job.add_a + b * job.add_b + off0 : nullptr;
 #pragma unroll 4
-        for (int k = 0; k < 16; k++) {
-            const int i = threadIdx.x + k * 256;
-            const uint64_t v = canon(G::addr(i >> 8, i & 255));
-            uint64_t rr = mul_shoup(sub_mod(aux[i], v, md.q), cm.x, cm.y, md.q);
-            if (has_add) rr = add_mod(rr, add[i], md.q);
-            dst[i] = rr;
+        for (int k = 0; k < 8; k++) {
+            const int i = 2 * (threadIdx.x + k * 256);
+            const ulonglong2 ax = *reinterpret_cast<const ulonglong2*>(aux + i);
+            const uint64_t v0 = canon(G::addr(i >> 8, i & 255)), v1 = canon(G::addr(i >> 8, (i & 255) + 1));
+            uint64_t r0 = mul_shoup(sub_mod(ax.x, v0, md.q), cm.x, cm.y, md.q);
+            uint64_t r1 = mul_shoup(sub_mod(ax.y, v1, md.q), cm.x, cm.y, md.q);
+            if (has_add) {
+                const ulonglong2 ad = *reinterpret_cast<const ulonglong2*>(add + i);
+                r0 = add_mod(r0, ad.x, md.q);
+                r1 = add_mod(r1, ad.y, md.q);
+            }
+            *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(r0, r1);
         }
     }
 }
