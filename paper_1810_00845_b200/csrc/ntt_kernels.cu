@@ -322,6 +322,101 @@ __global__ void __launch_bounds__(256, 4) k_fwd_rows_r16(PassJob job, Tables tb)
     else fwd_rows_r16_body<false, STOREMODE>(job, tb, src, dst, mi, md, a, b, z, row0, off0);
 }
 
+// inverse pass B for M1 = 256, register-direct (the mirror of k_fwd_cols_r16): thread (g = tid % 16,
+// t = tid / 16) loads rows 16 t + e of column g (inverse phase 1's operands, two 128-byte segments
+// per warp load), one exchange, phase 2 on rows t + 16 e, N^-1 and the full reduction in
+// registers, coalesced stores.
+template <typename V, bool FP>
+__device__ __forceinline__ void inv_phase16(V (&r)[16], int b0, int ohigh, const void* twp, double q, double qinv,
+                                            uint64_t qi, int v0, int log_n) {
+#pragma unroll
+    for (int uu = 0; uu < 4; uu++) {
+        const int bit = b0 + uu;
+        const int v = v0 + bit;
+        const int dist = 1 << uu;
+        const uint32_t tbase = (1u << (log_n - v - 1)) + ((uint32_t)ohigh << (4 - uu - 1));
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (k >= (1 << (4 - uu - 1))) break;
+            if constexpr (FP) {
+                const double W = __ldg(reinterpret_cast<const double*>(twp) + tbase + k);
+#pragma unroll
+                for (int e0 = 0; e0 < 8; e0++) {
+                    if (e0 >= dist) break;
+                    const int e = k * 2 * dist + e0;
+                    const double X = r[e], Y = r[e + dist];
+                    r[e] = redd(__dadd_rn(X, Y), q, qinv);
+                    r[e + dist] = mulred(redd(__dsub_rn(X, Y), q, qinv), W, q, qinv);
+                }
+            } else {
+                const ulonglong2 W = __ldg(reinterpret_cast<const ulonglong2*>(twp) + tbase + k);
+                const uint64_t q2 = 2 * qi;
+#pragma unroll
+                for (int e0 = 0; e0 < 8; e0++) {
+                    if (e0 >= dist) break;
+                    const int e = k * 2 * dist + e0;
+                    const uint64_t X = r[e], Y = r[e + dist];
+                    const uint64_t sm_ = X + Y;
+                    r[e] = sm_ >= q2 ? sm_ - q2 : sm_;
+                    r[e + dist] = mul_shoup_lazy(X - Y + q2, W.x, W.y, qi);
+                }
+            }
+        }
+    }
+}
+
+template <bool FP>
+__device__ __forceinline__ void inv_cols_r16_body(const Tables& tb, const uint64_t* src, uint64_t* dst, int mi,
+                                                  const Mod& md, int col0, int M2) {
+    using G = Geo<8, 4>;
+    extern __shared__ uint64_t sm[];
+    const int g = threadIdx.x & 15, t = threadIdx.x >> 4;
+    using V = typename std::conditional<FP, double, uint64_t>::type;
+    V r[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        const uint64_t w = __ldg(&src[(long long)(16 * t + e) * M2 + col0 + g]);
+        if constexpr (FP) r[e] = __longlong_as_double((long long)w);
+        else r[e] = w;
+    }
+    const double2 qd = FP ? tb.modd[mi] : make_double2(0, 0);
+    const void* twp = FP ? (const void*)(tb.inv_d + ((long long)mi << tb.log_n))
+                         : (const void*)(tb.inv + ((long long)mi << tb.log_n));
+    const int v0 = tb.log_n - 8;
+    inv_phase16<V, FP>(r, 0, t, twp, qd.x, qd.y, md.q, v0, tb.log_n);
+    V* tile = reinterpret_cast<V*>(sm);
+#pragma unroll
+    for (int e = 0; e < 16; e++) tile[G::addr(g, 16 * t + e)] = r[e];
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; e++) r[e] = tile[G::addr(g, t + 16 * e)];
+    inv_phase16<V, FP>(r, 4, 0, twp, qd.x, qd.y, md.q, v0, tb.log_n);
+    if constexpr (FP) {
+        const double ni = tb.ninv_d[mi];
+#pragma unroll
+        for (int e = 0; e < 16; e++)
+            dst[(long long)(t + 16 * e) * M2 + col0 + g] = d_canon(mulred(r[e], ni, qd.x, qd.y), qd.x, qd.y);
+    } else {
+        const ulonglong2 ni = tb.ninv[mi];
+#pragma unroll
+        for (int e = 0; e < 16; e++) dst[(long long)(t + 16 * e) * M2 + col0 + g] = mul_shoup(r[e], ni.x, ni.y, md.q);
+    }
+}
+
+__global__ void __launch_bounds__(256, 4) k_inv_cols_r16(PassJob job, Tables tb) {
+    int a, b;
+    if (!job_limb(job, a, b)) return;
+    const int z = blockIdx.z;
+    const int M2 = 1 << (tb.log_n - 8);
+    const int col0 = blockIdx.x * 16;
+    const int mi = job.mod_map[b];
+    const Mod md = tb.mods[mi];
+    const uint64_t* src = job.src[z] + a * job.src_a + b * job.src_b;
+    uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
+    if (use_f64(md.q, tb)) inv_cols_r16_body<true>(tb, src, dst, mi, md, col0, M2);
+    else inv_cols_r16_body<false>(tb, src, dst, mi, md, col0, M2);
+}
+
 // ------------------------------------------------------------------------------------------
 // forward pass 2: rows (contiguous).  Tile = Gr consecutive rows of M = M2 words.  Input = the
 // lazy pass-1 output.  STORE_PLAIN: full reduction.  STORE_COMBINE: out = (aux - v) * comb[mod]
@@ -578,6 +673,12 @@ static cudaError_t inv_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
     dim3 grid(gx, nlimbs, nz);
     constexpr int FULL = 256 / Geo<LOG_M, LOG_R>::T;
+    if constexpr (LOG_M == 8 && LOG_R == 4) {
+        if (threads == 256 && ntt_variant() != 2) {   // register-direct radix-16 form
+            k_inv_cols_r16<<<grid, 256, smem, st>>>(job, tb);
+            return cudaGetLastError();
+        }
+    }
     if (threads == 256) k_inv_cols<LOG_M, LOG_R, MINB, FULL><<<grid, threads, smem, st>>>(job, tb);
     else k_inv_cols<LOG_M, LOG_R, MINB><<<grid, threads, smem, st>>>(job, tb);
     return cudaGetLastError();
