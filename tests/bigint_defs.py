@@ -90,3 +90,73 @@ def centered(x: int, m: int) -> int:
 def round_div(a: int, d: int) -> int:
     """round(a / d) for odd d (no ties), exact integers."""
     return (2 * a + d) // (2 * d)
+
+
+# ---------------------------------------------------------------- exact encoding (A7) at tiny N
+from decimal import Decimal, localcontext  # noqa: E402
+from fractions import Fraction  # noqa: E402
+
+_DEC_PREC = 90
+
+
+def _atan_inv(n: int) -> Decimal:
+    """atan(1/n) by its Taylor series (|1/n| <= 1/5), at the current Decimal precision."""
+    x = Decimal(1) / n
+    x2 = x * x
+    term, acc, k = x, x, 1
+    eps = Decimal(10) ** (-_DEC_PREC - 5)
+    while abs(term) > eps:
+        term = -term * x2
+        acc += term / (2 * k + 1)
+        k += 1
+    return acc
+
+
+def dec_pi() -> Decimal:
+    """Machin: pi = 16 atan(1/5) - 4 atan(1/239)."""
+    with localcontext() as ctx:
+        ctx.prec = _DEC_PREC + 10
+        return +(16 * _atan_inv(5) - 4 * _atan_inv(239))
+
+
+def dec_cos(x: Decimal) -> Decimal:
+    """cos(x) by its Taylor series, |x| <= 2 pi, ~90 significant digits."""
+    with localcontext() as ctx:
+        ctx.prec = _DEC_PREC + 20
+        x2 = x * x
+        term, acc, k = Decimal(1), Decimal(1), 0
+        eps = Decimal(10) ** (-_DEC_PREC - 10)
+        while abs(term) > eps or k < 4:
+            term = -term * x2 / ((2 * k + 1) * (2 * k + 2))
+            acc += term
+            k += 1
+        return +acc
+
+
+def encode_values_exact(z, scale: float, N: int):
+    """A7's real values v_t = (Delta/N) sum_{j<n} 2 z_j cos(pi (5^j t mod 2N) / N), t < N, to ~85
+    significant digits (every double z_j and the scale enter exactly)."""
+    pi = dec_pi()
+    cos_tab = {}
+    out = []
+    with localcontext() as ctx:
+        ctx.prec = _DEC_PREC
+        for t in range(N):
+            acc = Decimal(0)
+            for j, zj in enumerate(z):
+                if zj == 0.0:
+                    continue
+                e = (pow(5, j, 2 * N) * t) % (2 * N)
+                if e not in cos_tab:
+                    cos_tab[e] = dec_cos(pi * e / N)
+                acc += 2 * Decimal(float(zj)) * cos_tab[e]
+            out.append(acc * Decimal(float(scale)) / N)
+    return out
+
+
+def round_half_away(v) -> int:
+    """round half away from zero of an exact Decimal / Fraction / int."""
+    f = Fraction(v)
+    h = abs(f) + Fraction(1, 2)
+    r = h.numerator // h.denominator          # floor(|v| + 1/2)
+    return r if f >= 0 else -r

@@ -5,6 +5,7 @@ with Python big integers at tiny N, a closed form, an invariant, a library routi
 printed in the paper/spec (tests/golden, cited).  See DESIGN.md "Pins".
 """
 import json
+from fractions import Fraction
 import math
 import os
 
@@ -199,9 +200,62 @@ def test_encode_constant_closed_form_and_spec_examples():
     for case in g["cases"]:
         m = o.encode_coeffs(np.full(o.slots, case["value"]), case["scale"])
         assert m[0] == case["constant_coeff"] and (m[1:] == 0).all()
-    for c in (0.123456789, -2.5, 1.0):
+    for c in (0.123456789, -2.5, 1.0, -0.3):
         m = o.encode_coeffs(np.full(o.slots, c), 2.0 ** 40)
-        assert m[0] == ckks.llround(c * 2.0 ** 40) and (m[1:] == 0).all()
+        # P-ENC-1 closed form, rounded exactly (A7): round-half-away(c Delta) of the exact real
+        assert m[0] == D.round_half_away(Fraction(c) * 2 ** 40) and (m[1:] == 0).all()
+
+
+def test_llround_ties_literal():
+    """A20: scalars are X = llround(x scale), round half AWAY from zero of the double, exactly
+    (the classic floor(x + 0.5) bugs at 0.49999999999999994 and 2^52 + 1 included)."""
+    cases = {2.5: 3, -2.5: -3, 0.5: 1, -0.5: -1, 1.5: 2, -1.5: -2, 0.49999999999999994: 0,
+             -0.49999999999999994: 0, 4503599627370497.0: 4503599627370497, 2.0 ** 61 + 0.0: 2 ** 61,
+             1099511627775.5: 1099511627776, -1099511627775.5: -1099511627776, 7.0: 7}
+    for x, want in cases.items():
+        assert ckks.llround(x) == want, x
+
+
+def test_encode_exact_ties_closed_form():
+    """A7 exact ties: a constant slot vector c at scale 1 encodes to the constant polynomial with
+    m_0 = c exactly (P-ENC-1: the t = 0 sum has only exact terms), so c = k + 1/2 is an exact
+    tie -- rounded half away from zero, every other coefficient 0."""
+    o = Oracle(10, [60, 40], 60, nthreads=2)
+    for c, want in ((2.5, 3), (-3.5, -4), (0.5, 1), (-0.5, -1), (1234567.5, 1234568), (-7.5, -8)):
+        m = o.encode_coeffs(np.full(o.slots, c), 1.0)
+        assert m[0] == want and (m[1:] == 0).all(), (c, m[:4])
+
+
+def test_encode_near_ties_match_exact_real_rounding():
+    """A7 near ties: at N = 16, slot vectors tuned (through z_0) so that a chosen coefficient lies
+    within 2^-14 .. 2^-34 of a half-integer, above and below it, for positive and negative
+    values; EVERY coefficient must equal round-half-away of the exact real v_t (Decimal sums to
+    ~85 digits, tests/bigint_defs.py) -- this exercises the oracle's binary128 recomputation
+    window (2^-12) and its long-double path on the same vectors."""
+    from decimal import Decimal, localcontext
+    o = Oracle(4, [60], 60, nthreads=1)
+    N, s = o.N, o.slots
+    rng = np.random.default_rng(11)
+    pi = D.dec_pi()
+    in_window = set()
+    for case, (t, K, delta) in enumerate([(1, 1000, 2.0 ** -14), (3, -2000, -2.0 ** -20), (5, 777777, 2.0 ** -30),
+                                          (2, -31, 2.0 ** -34), (7, 123456, -2.0 ** -26), (6, -500000, 2.0 ** -16)]):
+        z = rng.uniform(-1, 1, s)
+        scale = 2.0 ** 20
+        with localcontext() as ctx:
+            ctx.prec = 90
+            rest = D.encode_values_exact(np.r_[0.0, z[1:]], scale, N)[t]
+            coef = Decimal(float(scale)) / N * 2 * D.dec_cos(pi * t / N)      # d v_t / d z_0
+            target = Decimal(K) + (Decimal("0.5") if K >= 0 else Decimal("-0.5")) + Decimal(delta)
+            z[0] = float((target - rest) / coef)
+        v = D.encode_values_exact(z, scale, N)
+        want = [D.round_half_away(x) for x in v]
+        got = o.encode_coeffs(z, scale)
+        assert [int(x) for x in got] == want, case
+        frac = abs(v[t]) - int(abs(v[t]))
+        if abs(frac - Decimal("0.5")) < Decimal(2) ** -12:
+            in_window.add((v[t] > 0, frac > Decimal("0.5")))
+    assert in_window == {(True, True), (True, False), (False, True), (False, False)}
 
 
 def test_encode_matches_canonical_embedding():
