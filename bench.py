@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--no-hoisted", action="store_true")
     ap.add_argument("--no-inference", action="store_true")
     ap.add_argument("--hoist-r", type=int, default=8, help="rotation amounts per hoisted ModUp")
-    ap.add_argument("--nets", default="tiny,lenet_small,lenet_large", help="encrypted-inference configs to time")
+    ap.add_argument("--nets", default="tiny,lenet_small,lenet_large,squeezenet",
+                    help="encrypted-inference configs to time")
+    ap.add_argument("--images", type=int, default=20, help="images averaged per inference config (P:843-844)")
     ap.add_argument("--oracle-nets", default="tiny,lenet_small",
                     help="configs whose oracle inference latency is timed on the host cores (cpu_baseline)")
     ap.add_argument("--tiling", default="lenet_large",
@@ -253,11 +255,23 @@ def _net_variant(name, fc_replicas=None):
     return key
 
 
-def measure_inference(name, device, reps=3, rot_policy="exact"):
-    """Encrypted CNN inference latency (BASELINE.json metric, configs 1 / 3): server-side
-    forward from encrypted input resident on the GPU to encrypted output, CUDA events + wall
-    clock; client encode/encrypt and decrypt/decode timed separately.  (Accuracy against the
-    float64 network is asserted by tests/test_driver.py, not here.)"""
+def _golden_outputs(name):
+    """float64 outputs of `name` on image seeds 0..19 (tests/golden/plain_outputs.json, written by
+    tools/write_golden_plain.py from oracle/plain.py -- a stored reference, no oracle code runs
+    here)."""
+    path = os.path.join(ROOT, "tests", "golden", "plain_outputs.json")
+    try:
+        return json.load(open(path))["outputs"].get(name)
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def measure_inference(name, device, images=20, rot_policy="exact"):
+    """Encrypted CNN inference latency (BASELINE.json metric, second half): server-side forward
+    from encrypted input resident on the GPU to encrypted output, CUDA events + wall clock,
+    averaged over `images` synthetic images (seeds 0..images-1; the paper averages 20 images,
+    P:843-844); client encode/encrypt and decrypt/decode timed separately; every decrypted output
+    compared with the float64 network (max_abs_err, rel_err = max-abs / max |float64|)."""
     import numpy as np
     import torch
     from synth import nets as SN
@@ -266,7 +280,7 @@ def measure_inference(name, device, reps=3, rot_policy="exact"):
     net = SN.NETS[name]
     base = SN.NETS.get("_weights_alias", {}).get(name, name)   # replica variants share the weights
     W = SN.net_weights(base)
-    img = SN.net_image(base, 0)
+    gold = _golden_outputs(base)
     torch.cuda.empty_cache()
     ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=device, arena_bytes=64 << 30)
     t0 = time.perf_counter()
@@ -278,18 +292,19 @@ def measure_inference(name, device, reps=3, rot_policy="exact"):
     stream = torch.cuda.current_stream(device)
     # warm-up pass: encodes (caches) the weight plaintexts once per model
     t0 = time.perf_counter()
-    cts, lay = en.encrypt_image(img)
+    cts, lay = en.encrypt_image(SN.net_image(base, 0))
     out, ol = en.forward(cts, lay)
     ctx.sync()
     t_first = time.perf_counter() - t0
     for h in out + cts:
         ctx.free(h)
-    lat, walls = [], []
-    for r in range(reps):
+    lat, walls, t_encs, t_decs, errs, rels = [], [], [], [], [], []
+    for r in range(images):
+        img = SN.net_image(base, r)
         t0 = time.perf_counter()
         cts, lay = en.encrypt_image(img)
         ctx.sync()
-        t_enc = time.perf_counter() - t0
+        t_encs.append(time.perf_counter() - t0)
         ctx.profile(True)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -304,8 +319,12 @@ def measure_inference(name, device, reps=3, rot_policy="exact"):
         prof = ctx.profile_read()
         ctx.profile(False)
         t0 = time.perf_counter()
-        got = en.decrypt_output(out, ol)
-        t_dec = time.perf_counter() - t0
+        got = np.ravel(en.decrypt_output(out, ol))
+        t_decs.append(time.perf_counter() - t0)
+        if gold is not None and r < len(gold):
+            ref = np.asarray(gold[r])
+            errs.append(float(np.abs(got - ref).max()))
+            rels.append(errs[-1] / float(np.abs(ref).max()))
         for h in out + cts:
             ctx.free(h)
     total = sum(v[0] for v in prof.values()) or 1.0
@@ -313,11 +332,18 @@ def measure_inference(name, device, reps=3, rot_policy="exact"):
     ctx.close()
     ctx = None
     torch.cuda.empty_cache()
-    return {"config": name, "rot_policy": rot_policy, "latency_s": float(np.median(lat)), "wall_s": float(np.median(walls)), "unit": "s",
-            "reps": reps, "log_n": net["log_n"], "limbs": len(net["q_bits"]), "gpu_launches": launches,
-            "client_encrypt_s": t_enc, "client_decrypt_s": t_dec, "keygen_s": t_keys,
+    return {"config": name, "rot_policy": rot_policy, "latency_s": float(np.mean(lat)),
+            "latency_median_s": float(np.median(lat)), "latency_min_s": float(np.min(lat)),
+            "wall_s": float(np.mean(walls)), "unit": "s", "images": images,
+            "protocol": "mean over synthetic images seeds 0..%d, batch 1 (P:843-844)" % (images - 1),
+            "log_n": net["log_n"], "limbs": len(net["q_bits"]), "gpu_launches": launches,
+            "client_encrypt_s": float(np.mean(t_encs)), "client_decrypt_s": float(np.mean(t_decs)), "keygen_s": t_keys,
             "first_pass_incl_weight_encoding_s": t_first, "levels_used": plan["levels_used"],
-            "rotation_keys": len(plan["rotations"]), "output_head": [float(x) for x in np.ravel(got)[:3]],
+            "rotation_keys": len(plan["rotations"]), "act_gains": net.get("act_gains"),
+            "max_abs_err": max(errs) if errs else None, "rel_err": max(rels) if rels else None,
+            "accuracy_ref": "float64 network (tests/golden/plain_outputs.json); rel_err = max over images of "
+                            "max|dec - ref| / max|ref|" if errs else "no golden reference",
+            "output_head": [float(x) for x in np.ravel(got)[:3]],
             "kernel_share": {n: round(v[0] / total, 4) for n, v in top}}
 
 
@@ -666,7 +692,7 @@ def main():
         if sharded is not None:
             line["inference"] = sharded
         if not a.no_inference and world == 1:
-            line["inference"] = [measure_inference(nm, local) for nm in a.nets.split(",") if nm]
+            line["inference"] = [measure_inference(nm, local, images=a.images) for nm in a.nets.split(",") if nm]
             for inf in line["inference"]:
                 if inf["config"] in PAPER_CPU_S:
                     sec, cite = PAPER_CPU_S[inf["config"]]
@@ -678,8 +704,8 @@ def main():
             # comparison, Fig. tilings)
             if a.tiling:
                 hw = next((i for i in line["inference"] if i["config"] == a.tiling), None) or \
-                    measure_inference(a.tiling, local)
-                chw = measure_inference(a.tiling + "_chw", local)
+                    measure_inference(a.tiling, local, images=a.images)
+                chw = measure_inference(a.tiling + "_chw", local, images=a.images)
                 line["tiling"] = {"config": a.tiling, "hw_s": hw["latency_s"], "chw_s": chw["latency_s"],
                                   "speedup_chw_over_hw": hw["latency_s"] / chw["latency_s"],
                                   "chw_first_pass_incl_weight_encoding_s": chw["first_pass_incl_weight_encoding_s"]}
@@ -692,8 +718,8 @@ def main():
             # composed rotations (the paper's Fig. rotopt: 1.43-2.07x on CPU HEAAN)
             if a.policy_net:
                 ex = next((i for i in line["inference"] if i["config"] == a.policy_net), None) or \
-                    measure_inference(a.policy_net, local)
-                p2 = measure_inference(a.policy_net, local, rot_policy="pow2")
+                    measure_inference(a.policy_net, local, images=a.images)
+                p2 = measure_inference(a.policy_net, local, images=a.images, rot_policy="pow2")
                 line["rot_key_policy"] = {"config": a.policy_net, "exact_s": ex["latency_s"], "pow2_s": p2["latency_s"],
                                           "exact_keys": ex["rotation_keys"], "pow2_keys": p2["rotation_keys"],
                                           "speedup_exact_over_pow2": p2["latency_s"] / ex["latency_s"],

@@ -135,8 +135,9 @@ int hisa_free(hisa_ctx* ctx, uint64_t handle);
  * m_t = round-half-away((scale/N) sum_j 2 v_j cos(pi (5^j t mod 2N)/N)) (A7), level -1 = top */
 int hisa_encode(hisa_ctx* ctx, const double* v, size_t n, double scale, int level, hisa_pt* out);
 /* count plaintexts at once: v = count rows of n_per values (row-major), same scale and level;
- * encoded on all host cores (same exact rounding as hisa_encode), limbs + NTT on the GPU in
- * batches; outs[count].  For a layer's weight / mask plaintexts (once per model). */
+ * encoded on the GPU (double-double FFT, the same exact rounding as hisa_encode, near ties
+ * recomputed in binary128 on the host), limbs + NTT batched; outs[count].  For a layer's
+ * weight / mask plaintexts (once per model). */
 int hisa_encode_batch(hisa_ctx* ctx, const double* v, size_t n_per, size_t count, double scale, int level,
                       hisa_pt* outs);
 /* slot values from limb 0 (A13): needs |value| * scale < q_0 / 2; out[0..n) */

@@ -22,7 +22,8 @@ Lowering readings, in the order t
            (i, j): origin + (i - p) hS + (j - p) wS (mod N/2).  mulScalar at pt_scale = q_top
            (A8), accumulate from the first term (A21), rescale once per output (A22),
            then add_scalar(beta).  Output layout: strides * s, origin 0, not clean (A23).
-  act      rescale(mul(x, x)) (tensor + relinearize) then add_scalar(gamma).
+  act      rescale(mul(x, x)) (tensor + relinearize) then add_scalar(gamma), gamma
+           scaled by the activation's compile-time gain (A41, see fold()).
   square   rescale(mul(x, x)).
   avgpool  x + rot(x, wS) + rot(x, hS) + rot(x, hS + wS); strides * 2 (A26).
   fc (hw input)    acc_j = sum_c mulPlain(x_c, P_jc), P_jc holding W'[j, (c, y, x)] at the valid
@@ -72,14 +73,29 @@ class Layout:
 
 
 def fold(net: dict, weights, act_coeffs):
-    """Compile-time rewrite (A25, A26): per weight tensor (W', beta); per act gamma."""
+    """Compile-time rewrite (A25, A26, A41): per weight tensor (W', beta); per act gamma.
+
+    A41 (compile-time gains): activation number n (execution order: "act" layers, a fire's
+    squeeze then its expand) carries a gain G_n (a power of 4, default 1): the encrypted tensor
+    after it holds G_n times its float64 value, so
+        G_n (a2 x^2 + a1 x + a0) = x'^2 + G_n (a0 - a1^2/(4 a2)),
+        x' = sqrt(a2 G_n) x + sqrt(a2 G_n) a1/(2 a2),
+    and the linear layer producing x reads an input holding G_prev times its value, so its
+    weights are multiplied by sqrt(a2 G_n) / G_prev.  Linear layers not followed by an act
+    leave the gain unchanged; decryption divides by the output tensor's gain."""
     a0, a1, a2 = act_coeffs
     assert a2 > 0, "the folded form needs a2 > 0 (sign(a2) = +1)"
-    r = math.sqrt(a2)
-    beta = r * a1 / (2 * a2)
-    gamma = a0 - a1 * a1 / (4 * a2)
+    n_acts = sum({"act": 1, "fire": 2}.get(layer[0], 0) for layer in net["layers"])
+    gains = list(net.get("act_gains", [1.0] * n_acts))
+    assert len(gains) == n_acts
+
+    def act_params(n):
+        G = float(gains[n])
+        r = math.sqrt(a2 * G)
+        return r, r * a1 / (2 * a2), G * (a0 - a1 * a1 / (4 * a2)), G
+
     layers = net["layers"]
-    folded, wi, pools = [], 0, 0
+    folded, gammas, wi, pools, n_act, gain = [], [], 0, 0, 0, 1.0
     _c, h, w_ = net["input"]
     for i, layer in enumerate(layers):
         nxt = layers[i + 1][0] if i + 1 < len(layers) else None
@@ -96,19 +112,27 @@ def fold(net: dict, weights, act_coeffs):
             pools = 0
             b = 0.0
             if nxt == "act":
-                wt = wt * r
-                b = beta
+                r, b, gamma, G = act_params(n_act)
+                n_act += 1
+                wt = wt * r / gain
+                gammas.append(gamma)
+                gain = G
             if nxt == "gap":
                 wt = wt / (h * w_)
             folded.append((wt, b))
             wi += 1
         if layer[0] == "fire":
-            folded.append((np.array(weights[wi], dtype=np.float64) * (0.25 ** pools) * r, beta))
-            folded.append((np.array(weights[wi + 1], dtype=np.float64) * r, beta))
-            folded.append((np.array(weights[wi + 2], dtype=np.float64) * r, beta))
+            r1, b1, gm1, G1 = act_params(n_act)
+            r2, b2, gm2, G2 = act_params(n_act + 1)
+            n_act += 2
+            folded.append((np.array(weights[wi], dtype=np.float64) * (0.25 ** pools) * r1 / gain, b1))
+            folded.append((np.array(weights[wi + 1], dtype=np.float64) * r2 / G1, b2))
+            folded.append((np.array(weights[wi + 2], dtype=np.float64) * r2 / G1, b2))
+            gammas += [gm1, gm2]
+            gain = G2
             pools = 0
             wi += 3
-    return folded, gamma
+    return folded, gammas, gain
 
 
 class OracleNet:
@@ -123,7 +147,8 @@ class OracleNet:
         self.net = net
         self.rot_policy = rot_policy
         self.o = Oracle(net["log_n"], net["q_bits"], net["p_bits"], seed=seed, nthreads=nthreads)
-        self.folded, self.gamma = fold(net, weights, act_coeffs)
+        self.folded, self.gammas, self.out_gain = fold(net, weights, act_coeffs)
+        self._n_act = 0
         wanted = self._rotation_amounts()
         if rot_policy == "pow2":
             wanted = {st for k in wanted for st in self._steps(k)}
@@ -244,7 +269,8 @@ class OracleNet:
         return cts, lay
 
     def decrypt_output(self, cts, lay) -> np.ndarray:
-        vals = [self.o.decode(self.o.decrypt(ct)) for ct in cts]
+        """Decrypt + decode the network output, divided by its compile-time gain (A41)."""
+        vals = [self.o.decode(self.o.decrypt(ct)) / self.out_gain for ct in cts]
         if lay.kind == "slot0":
             return np.array([v[0] for v in vals])
         if lay.kind == "rep":
@@ -350,10 +376,14 @@ class OracleNet:
     def act(self, cts, lay, square_only=False):
         o = self.o
         out = []
+        gamma = 0.0
+        if not square_only:
+            gamma = self.gammas[self._n_act]
+            self._n_act += 1
         for ct in cts:
             y = o.rescale(o.mul(ct, ct))
-            if not square_only and self.gamma:
-                y = o.add_scalar(y, self.gamma)
+            if gamma:
+                y = o.add_scalar(y, gamma)
             out.append(y)
         return out, Layout(lay.kind, lay.C, lay.H, lay.W, lay.hS, lay.wS, lay.origin, False, lay.R, lay.Bk,
                            lay.count)
@@ -467,9 +497,8 @@ class OracleNet:
         s, ls = self._mask(s, ls)
         x1, l1 = self.conv(s, ls, ("conv", e1, 1, 1, 0), we1, b1)
         x3, _l3 = self.conv(s, ls, ("conv", e3, 3, 1, 1), we3, b3)
-        x1, l1 = self.act(x1, l1)
-        x3, _l3 = self.act(x3, _l3)
-        return x1 + x3, Layout("hw", e1 + e3, l1.H, l1.W, l1.hS, l1.wS, l1.origin, False)
+        out, lo = self.act(x1 + x3, l1)          # one activation (one gain, A41) on the concatenation
+        return out, Layout("hw", e1 + e3, lo.H, lo.W, lo.hS, lo.wS, lo.origin, False)
 
     def gap(self, cts, lay):
         o = self.o
@@ -488,6 +517,7 @@ class OracleNet:
         every layer for per-layer parity checks; `stop_after` = last layer index to evaluate
         (sampled parity of networks too large for the oracle end to end)."""
         wi = 0
+        self._n_act = 0
         for li, layer in enumerate(self.net["layers"]):
             if stop_after is not None and li > stop_after:
                 break

@@ -44,9 +44,10 @@ def avgpool2(x: np.ndarray) -> np.ndarray:
     return x[:, :h // 2 * 2, :w // 2 * 2].reshape(c, h // 2, 2, w // 2, 2).mean(axis=(2, 4))
 
 
-def forward(net: dict, image: np.ndarray, weights, act_coeffs) -> np.ndarray:
+def forward(net: dict, image: np.ndarray, weights, act_coeffs, trace=None) -> np.ndarray:
     """Evaluate the network on one (C, H, W) image; returns the final activations (flattened
-    for FC outputs, (C, H, W) otherwise)."""
+    for FC outputs, (C, H, W) otherwise).  `trace` (a list, optional) receives (layer index,
+    output of that layer) after every layer."""
     x = np.asarray(image, dtype=np.float64)
     wi = 0
     for layer in net["layers"]:
@@ -75,4 +76,6 @@ def forward(net: dict, image: np.ndarray, weights, act_coeffs) -> np.ndarray:
             x = x.mean(axis=(1, 2))
         else:
             raise ValueError(kind)
+        if trace is not None:
+            trace.append((len(trace), x))
     return x

@@ -512,7 +512,6 @@ extern "C" int hisa_ctx_create(const hisa_params* p, hisa_ctx** out) {
         return fail(HISA_E_CUDA, "table upload failed");
     }
     c->objs.push_back(Obj());   // slot 0 reserved
-    if (const char* e = getenv("HISA_F64")) c->f64_max_q = atoi(e) ? 0x1p50 : 0.0;
     *out = c;
     return HISA_OK;
 }
@@ -853,8 +852,12 @@ static void fft_ld(const hisa_ctx* c, std::vector<cld>& a, int sign) {
     }
 }
 
-// one coefficient exactly: binary128 direct sum of v_t (the A7 near-tie path); same operation
-// order as the oracle's (oracle/ckks_oracle.c enc_value_q)
+// one coefficient exactly (the A7 near-tie path): binary128 direct sum of v_t with a correctly
+// rounded binary128 cos table.  Its error is below E = (n + 2) 2^-112 (scale/N) sum_j |2 z_j|
+// (< 2^-36 even at |v| = 2^62, N = 2^16), so the result is round-half-away of the exact real
+// v_t whenever v_t is farther than E from a half-integer; exact ties (e.g. the t = 0 coefficient
+// of a constant vector, a sum of exact terms) are computed exactly.  Pinned against exact
+// Decimal sums near ties in tests/test_oracle_pins.py (oracle) and tests/test_gpu_edges.py (GPU).
 static int exact_coeff_q(hisa_ctx* c, const double* z, size_t n, double scale, uint64_t t, int64_t* out) {
     const uint64_t N = c->N, twoN = 2 * N;
     std::vector<__float128>& cq = c->enc_cosq;
@@ -987,9 +990,6 @@ extern "C" int hisa_encode(hisa_ctx* c, const double* v, size_t n, double scale,
     return HISA_OK;
 }
 
-// count plaintexts of n_per slot values each (v row-major), encoded on all host cores (the
-// exact-rounding encoder is host code, A7), then reduced into limbs and NTT-ed on the GPU in
-// batches: the once-per-model weight / mask plaintexts of a layer in one call
 // count plaintexts of n_per slot values each (v row-major): the exact encoding (A7) of every row
 // on the GPU in chunks (double-double FFT, encode_to_device), limbs + NTT batched: a layer's
 // weight / mask plaintexts in one call
@@ -1436,74 +1436,6 @@ static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_
     return HISA_OK;
 }
 
-// hoisted rotations of ONE ciphertext by n distinct non-zero amounts (K7): one ModUp (INTT +
-// lift + both forward passes, D materialised), then per chunk of MAXR amounts one streaming
-// inner product over the chunk's keys, a batched ModDown and a batched permutation
-static int rotate_hoisted(hisa_ctx* c, const Obj* o, const uint64_t* ks, int n, uint64_t** outs) {
-    const int level = o->level, l1 = level + 1, l2 = level + 2, L = c->L;
-    const long long N = (long long)c->N;
-    const int RC = std::min(n, MAXR);
-    const size_t per_amt = (size_t)N * (2 * l2 + 2 + 2 * l1 + 2 * l1);   // acc, ptmp, md, pre
-    const size_t base = (size_t)N * ((size_t)l1 + (size_t)l1 * l2);      // dtil, D
-    uint64_t* scratch = dalloc_t<uint64_t>(c, base + per_amt * RC);
-    if (!scratch) return fail(HISA_E_OOM, "hoisted rotation scratch (%zu MiB)", (base + per_amt * RC) * 8 >> 20);
-    for (int r = 0; r < n; r++) {
-        outs[r] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
-        if (!outs[r]) return fail(HISA_E_OOM, "rotation output");
-    }
-    uint64_t* dtil = scratch;
-    uint64_t* D = scratch + (size_t)l1 * N;
-    const uint64_t* d1[1] = {o->ptr + l1 * N};
-    uint64_t* dt[1] = {dtil};
-    uint64_t* Dp[1] = {D};
-    RET(ks_modup_pass1(c, 1, level, d1, dt, Dp));
-    {   // ModUp pass 2 in place: D_{j,r} for r != q_j, fully reduced
-        PassJob j = job0();
-        j.src[0] = D; j.dst[0] = D;
-        j.nb = l2;
-        j.src_a = j.dst_a = (long long)l2 * N;
-        j.src_b = j.dst_b = N;
-        j.skip_diag = 1;
-        for (int ri = 0; ri < l2; ri++) j.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
-        Tables tb = c->tables();
-        KL("ks_modup_rows", launch_fwd_pass2(j, tb, l1 * l2, 1, false, c->stream));
-    }
-    for (int r0 = 0; r0 < n; r0 += MAXR) {
-        const int R = std::min(MAXR, n - r0);
-        uint64_t *acc[MAXB], *ptmp[MAXB], *md[MAXB];
-        const uint64_t* pres[MAXB];
-        uint64_t gs[MAXB];
-        KsBatch kb;
-        memset(&kb, 0, sizeof kb);
-        KsHoistJob hj;
-        memset(&hj, 0, sizeof hj);
-        for (int r = 0; r < R; r++) {
-            uint64_t* s = scratch + base + per_amt * r;
-            acc[r] = s; s += (size_t)2 * l2 * N;
-            ptmp[r] = s; s += (size_t)2 * N;
-            md[r] = s; s += (size_t)2 * l1 * N;
-            pres[r] = s;
-            kb.out[r] = s;
-            kb.add[r] = o->ptr;
-            gs[r] = galois(c, ks[r0 + r]);
-            hj.key[r] = c->rot_keys[ks[r0 + r]];
-            hj.acc[r] = acc[r];
-        }
-        kb.add_polys = 1;
-        kb.add_a = 0;
-        hj.D = D;
-        hj.diag = d1[0];
-        hj.l1 = l1;
-        hj.L = L;
-        for (int ri = 0; ri < l2; ri++) hj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
-        KL("ks_ip_hoisted", launch_ks_ip_hoisted(hj, R, c->d_mods, c->log_n, c->stream));
-        RET(ks_moddown(c, R, level, acc, ptmp, md, kb));
-        KL("automorphism", launch_automorphism(pres, outs + r0, R, 2 * l1, c->log_n, gs, c->stream));
-    }
-    dfree(c, scratch);
-    return HISA_OK;
-}
-
 // hoisted rotations of nct ciphertexts (one level) by the same n non-zero amounts: batched ModUp
 // (nz ciphertexts per launch), K7 over groups of <= 4 ciphertexts x <= 4 keys (each key word
 // streamed once per group), batched ModDown and permutation.  outs[i * n + r] = rot(in_i, ks[r]).
@@ -1782,14 +1714,11 @@ extern "C" int hisa_rot_left_hoisted(hisa_ctx* c, hisa_ct h, const int64_t* k, s
     }
     if (nz_idx.empty()) return HISA_OK;
     std::vector<uint64_t*> res(nz_idx.size());
-    // default: the multi-ciphertext K7 (<= 4 keys per launch, 1 word per thread) -- measured 78 %
-    // of HBM vs 69 % for the 8-key 2-word kernel (HISA_K7_VARIANT=2 keeps it for re-measurement)
-    static const int k7v = getenv("HISA_K7_VARIANT") ? atoi(getenv("HISA_K7_VARIANT")) : 0;
+    // the multi-ciphertext K7 (<= 4 keys per launch, 1 word per thread): measured 78 % of HBM vs
+    // 69 % for an 8-key 2-word kernel (round 1, removed)
     if (nz_idx.size() == 1) {
         Obj* ins[1] = {o};
         RET(rotate_batch(c, ins, 1, amounts[0], res.data()));
-    } else if (k7v == 2) {
-        RET(rotate_hoisted(c, o, amounts.data(), (int)amounts.size(), res.data()));
     } else {
         Obj* ins[1] = {o};
         RET(rotate_hoisted_multi(c, ins, 1, amounts.data(), (int)amounts.size(), res.data()));

@@ -14,207 +14,12 @@
 
 namespace hisa {
 
-// Variant knobs (tuned on B200, see profiles/): LOG_R = radix of the on-chip engine phases,
-// GR = rows (groups) per CTA, MINB = __launch_bounds__ min blocks.  Threads = GR * M / R,
-// elements per thread in the MAC phase = R (2R 128-bit accumulators per thread).
-template <int LOG_M, int LOG_R, int GR, int MINB>
-__global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip(KsJob job, Tables tb) {
-    using G = Geo<LOG_M, LOG_R>;
-    extern __shared__ uint64_t sm[];
-    // GR == 1, FP64 engine: the row's 2^LOG_M - 1 twiddles are the same for every digit j ->
-    // staged once in shared memory after the tile (no global twiddle loads in the j loop)
-    double* tws = reinterpret_cast<double*>(sm + GR * G::STRIDE);
-    // ciphertext index fastest: CTAs that read the same key tile are scheduled together (L2 reuse)
-    const int nz = job.nz;
-    const int z = blockIdx.x % nz;
-    const int ri = blockIdx.y;
-    const int l1 = job.l1;
-    const int nri = l1 + 1;
-    const int log_n = tb.log_n;
-    const int row0 = (blockIdx.x / nz) * GR;
-    const long long off0 = (long long)row0 << LOG_M;
-    const int mi = job.mod_map[ri];
-    const Mod md = tb.mods[mi];
-    const bool fp = (double)md.q < tb.f64_max_q;
-    const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
-    const double qp52 = __dadd_rn(qd.x, 4503599627370496.0);
-    constexpr int NTHR = GR * G::T;
-    constexpr int EPT = G::R;   // elements per thread in the MAC phase (tile / threads)
-    U128 acc0[EPT], acc1[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
-    const int g = threadIdx.x / G::T, t = threadIdx.x % G::T;
-    const long long kstride_j = 2ll * (job.L + 1) << log_n;
-    const long long kstride_p = (long long)(job.L + 1) << log_n;
-    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
-    if (GR == 1 && fp) {
-        const double* twg = tb.fwd_d + ((long long)mi << log_n);
-        const int s0 = log_n - LOG_M;
-        for (int idx = threadIdx.x + 1; idx < G::M; idx += NTHR) {
-            const int u = 31 - __clz(idx), m = idx - (1 << u);
-            tws[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
-        }
-    }
-    for (int j = 0; j < l1; j++) {
-        const uint64_t* src = (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
-                                        : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
-#pragma unroll
-        for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * NTHR;
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(&sm[G::addr(i >> LOG_M, i & (G::M - 1))]);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + i) : "memory");
-        }
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-        __syncthreads();
-        const bool conv = fp && j != ri;   // FP64-engine output: centred-lazy doubles
-        if (j != ri) {
-            if (fp && GR == 1)
-                fwd_engine_f64_rowtw<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y, tws, t);
-            else if (fp)
-                fwd_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(sm), qd.x, qd.y,
-                                             tb.fwd_d + ((long long)mi << log_n), log_n - LOG_M,
-                                             (uint32_t)(row0 + g), g, t);
-            else
-                fwd_engine<LOG_M, LOG_R>(sm, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
-                                         (uint32_t)(row0 + g), g, t);
-        }
-        const uint64_t* kb = key_r + j * kstride_j;
-        const uint64_t* ka = kb + kstride_p;
-#pragma unroll
-        for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * NTHR;
-            uint64_t D = sm[G::addr(i >> LOG_M, i & (G::M - 1))];   // int: < 4q
-            if (conv) D = d_rep(__longlong_as_double((long long)D), qd.x, qd.y, qp52);   // < 1.5q
-            mac128(acc0[k], D, __ldg(kb + i));
-            mac128(acc1[k], D, __ldg(ka + i));
-        }
-        __syncthreads();
-    }
-    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
-    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
-#pragma unroll
-    for (int k = 0; k < EPT; k++) {
-        const int i = threadIdx.x + k * NTHR;
-        out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
-        out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
-    }
-}
-
-// Software-pipelined K4 (variant P): the D tile of digit j+1 is copied into the other half of a
-// double buffer (cp.async groups) and its key words are loaded into registers while digit j's
-// NTT stages run, so neither the tile copy nor the key stream sits on the critical path.
-template <int LOG_M, int LOG_R, int GR, int MINB>
-__global__ void __launch_bounds__(GR * (1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip_pipe(KsJob job, Tables tb) {
-    using G = Geo<LOG_M, LOG_R>;
-    extern __shared__ uint64_t sm[];
-    constexpr int TILE = GR * G::STRIDE;
-    const int nz = job.nz;
-    const int z = blockIdx.x % nz;
-    const int ri = blockIdx.y;
-    const int l1 = job.l1;
-    const int nri = l1 + 1;
-    const int log_n = tb.log_n;
-    const int row0 = (blockIdx.x / nz) * GR;
-    const long long off0 = (long long)row0 << LOG_M;
-    const int mi = job.mod_map[ri];
-    const Mod md = tb.mods[mi];
-    const bool fp = (double)md.q < tb.f64_max_q;
-    const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
-    const double qp52 = __dadd_rn(qd.x, 4503599627370496.0);
-    constexpr int NTHR = GR * G::T;
-    constexpr int EPT = G::R;
-    U128 acc0[EPT], acc1[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
-    const int g = threadIdx.x / G::T, t = threadIdx.x % G::T;
-    const long long kstride_j = 2ll * (job.L + 1) << log_n;
-    const long long kstride_p = (long long)(job.L + 1) << log_n;
-    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
-    auto issue_tile = [&](int j) {
-        const uint64_t* src = (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
-                                        : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
-        uint64_t* buf = sm + (j & 1) * TILE;
-#pragma unroll
-        for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * NTHR;
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[G::addr(i >> LOG_M, i & (G::M - 1))]);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + i) : "memory");
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    uint64_t kb_next[EPT], ka_next[EPT];
-    auto load_keys = [&](int j) {
-        const uint64_t* kb = key_r + j * kstride_j;
-#pragma unroll
-        for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * NTHR;
-            kb_next[k] = __ldg(kb + i);
-            ka_next[k] = __ldg(kb + kstride_p + i);
-        }
-    };
-    issue_tile(0);
-    load_keys(0);
-    for (int j = 0; j < l1; j++) {
-        uint64_t kb_cur[EPT], ka_cur[EPT];
-#pragma unroll
-        for (int k = 0; k < EPT; k++) { kb_cur[k] = kb_next[k]; ka_cur[k] = ka_next[k]; }
-        if (j + 1 < l1) {
-            issue_tile(j + 1);
-            load_keys(j + 1);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        }
-        __syncthreads();
-        uint64_t* buf = sm + (j & 1) * TILE;
-        const bool conv = fp && j != ri;
-        if (j != ri) {
-            if (fp)
-                fwd_engine_f64<LOG_M, LOG_R>(reinterpret_cast<double*>(buf), qd.x, qd.y,
-                                             tb.fwd_d + ((long long)mi << log_n), log_n - LOG_M,
-                                             (uint32_t)(row0 + g), g, t);
-            else
-                fwd_engine<LOG_M, LOG_R>(buf, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M,
-                                         (uint32_t)(row0 + g), g, t);
-        }
-#pragma unroll
-        for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * NTHR;
-            uint64_t D = buf[G::addr(i >> LOG_M, i & (G::M - 1))];
-            if (conv) D = d_rep(__longlong_as_double((long long)D), qd.x, qd.y, qp52);   // < 1.5q
-            mac128(acc0[k], D, kb_cur[k]);
-            mac128(acc1[k], D, ka_cur[k]);
-        }
-        __syncthreads();   // buffer (j & 1) is refilled by iteration j + 1's prefetch of j + 2
-    }
-    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
-    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
-#pragma unroll
-    for (int k = 0; k < EPT; k++) {
-        const int i = threadIdx.x + k * NTHR;
-        out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
-        out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
-    }
-}
-
-template <int LOG_M, int LOG_R, int GR, int MINB>
-static cudaError_t ks_ip_pipe_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
-    using G = Geo<LOG_M, LOG_R>;
-    const int rows = 1 << (tb.log_n - LOG_M);
-    if (rows < GR) return cudaErrorInvalidValue;
-    constexpr int threads = GR * G::T;
-    const size_t smem = 2 * (size_t)GR * G::STRIDE * sizeof(uint64_t);
-    dim3 grid((rows / GR) * nz, job.l1 + 1, 1);
-    k_ks_ip_pipe<LOG_M, LOG_R, GR, MINB><<<grid, threads, smem, st>>>(job, tb);
-    return cudaGetLastError();
-}
-
 // K4 for one row per CTA with two digits in flight (variant 30, FP64 output primes): the
 // non-diagonal digits j != ri are processed in pairs -- both D tiles copied, both transformed by
 // one interleaved engine call (fwd_engine_f64_rowtw2, twiddles staged once in shared memory),
 // both multiplied into the same 128-bit accumulators -- then the diagonal digit (already in the
 // NTT domain) is multiplied in.  Integer-engine primes (q >= 2^50) fall back to one digit at a time.
-template <int LOG_M, int LOG_R, int MINB, bool PF = false>
+template <int LOG_M, int LOG_R, int MINB>
 __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(KsJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
@@ -274,29 +79,6 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
             mac128(acc1[k], D, __ldg(ka + i));
         }
     };
-    // prefetched form: key words of a digit loaded before the NTT stages that precede their use
-    uint64_t pkb[2][PF ? EPT : 1], pka[2][PF ? EPT : 1];
-    auto prefetch = [&](int slot, int j) {
-        if constexpr (PF) {
-            const uint64_t* kb = key_r + j * kstride_j;
-#pragma unroll
-            for (int k = 0; k < EPT; k++) {
-                pkb[slot][k] = __ldg(kb + threadIdx.x + k * NTHR);
-                pka[slot][k] = __ldg(kb + kstride_p + threadIdx.x + k * NTHR);
-            }
-        }
-    };
-    auto mac_pref = [&](const uint64_t* buf, int slot) {
-        if constexpr (PF) {
-#pragma unroll
-            for (int k = 0; k < EPT; k++) {
-                const int i = threadIdx.x + k * NTHR;
-                const uint64_t D = d_rep4(__longlong_as_double((long long)buf[G::addr(0, i)]), tq52);
-                mac128(acc0[k], D, pkb[slot][k]);
-                mac128(acc1[k], D, pka[slot][k]);
-            }
-        }
-    };
     // digits j != ri, in pairs
     int j = 0;
     auto next_nd = [&](int from) { return from == ri ? from + 1 : from; };
@@ -310,16 +92,10 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
         if (two) {
-            if constexpr (PF) { prefetch(0, ja); prefetch(1, jb); }
             fwd_engine_f64_rowtw2<LOG_M, LOG_R>(reinterpret_cast<double*>(sa), reinterpret_cast<double*>(sb), qd.x,
                                                 qd.y, tws, t);
-            if constexpr (PF) {
-                mac_pref(sa, 0);
-                mac_pref(sb, 1);
-            } else {
-                mac_tile(sa, ja, true);
-                mac_tile(sb, jb, true);
-            }
+            mac_tile(sa, ja, true);
+            mac_tile(sb, jb, true);
             j = next_nd(jb + 1);
         } else {
             if (fp)
@@ -355,6 +131,11 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
 // elements 4t + e, which are multiplied into the accumulators from registers with the key words
 // read as two 16-byte vectors.  Two digits in flight as in k_ks_ip2; the special prime's row
 // (integer engine) runs the k_ks_ip2 path.
+#ifndef K5_MINB
+#define K5_MINB 9     // k_ks_ip5 min CTAs / SM (64 threads): 9 -> <= 112 registers
+#endif
+constexpr int K5_TILE = 320;   // >= pad_1(255) + 1 = 316, pad_2(255) + 1 = 319 (words)
+
 template <int MINB>
 __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     constexpr int LOG_M = 8, LOG_R = 2;
@@ -423,15 +204,55 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     const double2 qd = tb.modd[mi];
     const double q = qd.x, qinv = qd.y;
     const double tq52 = __dadd_rn(2.0 * q, 4503599627370496.0);   // 2q + 2^52
+    double* tws5 = reinterpret_cast<double*>(sm + 4 * K5_TILE);
     {
         const double* twg = tb.fwd_d + ((long long)mi << log_n);
         const int s0 = log_n - LOG_M;
         for (int idx = t + 1; idx < G::M; idx += 64) {
             const int u = 31 - __clz(idx), m = idx - (1 << u);
-            tws[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
+            tws5[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
         }
     }
+    // Exchange tiles.  Phase ph's thread t holds elements mid = base_ph(t) | (e << lo_ph), e < 4
+    // (lo_ph = 6 - 2 ph).  Exchange x (after phase x) is written with phase x's pattern and read
+    // with phase x + 1's, through its own padded layout pad_x(m) = m + P_x (m >> S_x), chosen by
+    // exhaustive search (profiles/r2_k4_layouts.txt) so that BOTH patterns are conflict-free for
+    // 64-bit accesses (16 distinct 8-byte bank slots per half-warp; the XOR swizzle of round 1 had
+    // 48 extra wavefronts per digit-row, ncu: 58.5 M per launch) -- and, because a padding is
+    // additive in the bits above S_x, pad_x(base | e << lo) = pad_x(base) + e * step, so every
+    // access is one base register plus an immediate offset.  Exchanges 0 and 2 share buffer A,
+    // exchange 1 uses B (a thread's in-place read-then-write of one exchange can then never
+    // clobber another thread's unread word of a different layout).
+    auto pad = [](int x, int m) { return x == 1 ? m + 4 * (m >> 4) : x == 2 ? m + (m >> 2) : m; };
+    int wr[3], rd[3];
+#pragma unroll
+    for (int ph = 0; ph < 4; ph++) {
+        const int lo = 6 - 2 * ph;
+        const int base = ((t >> lo) << (lo + 2)) | (t & ((1 << lo) - 1));
+        if (ph < 3) wr[ph] = pad(ph, base);
+        if (ph > 0) rd[ph - 1] = pad(ph - 1, base);
+    }
+    // K5_STEP(x, lo): pad_x(e << lo) / e
+    auto step = [](int x, int lo) { return x == 1 ? (lo >= 4 ? 5 << (lo - 2) : 1 << lo)
+                                        : x == 2 ? (lo >= 2 ? 5 << (lo - 2) : 1 << lo) : 1 << lo; };
     __syncthreads();
+    // Split 64-bit MACs (products < 2^102): D < 2^52 (d_rep4) = Dh 2^32 + Dl, key word K < q < 2^50
+    // = Kh 2^25 + Kl; D K = Dl Kl + (Dl Kh + (Dh << 7) Kl) 2^25 + Dh Kh 2^57.  Three 64-bit
+    // accumulators per output word, each term one IMAD.WIDE.U32 (32 x 32 + 64); bounds for at most
+    // 24 digits: A0 < 24 2^57, A1 < 24 (2^57 + 2^52), A2 < 24 2^45 -- no overflow.
+    uint64_t A0[2][4], A1[2][4], A2[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int e = 0; e < 4; e++) { A0[h][e] = 0; A1[h][e] = 0; A2[h][e] = 0; }
+    auto mac_split = [&](int h, int e, uint64_t D, uint64_t K) {
+        const uint32_t dl = (uint32_t)D, dh = (uint32_t)(D >> 32);
+        const uint32_t kl = (uint32_t)K & 0x1FFFFFFu, kh = (uint32_t)(K >> 25);
+        A0[h][e] += (uint64_t)dl * kl;
+        A1[h][e] += (uint64_t)dl * kh;
+        A1[h][e] += (uint64_t)(dh << 7) * kl;
+        A2[h][e] += (uint64_t)dh * kh;
+    };
     // ND digits (1 or 2) through the four phases, then MAC from registers
     auto run = [&](auto nd_c, int ja, int jb) {
         constexpr int ND = decltype(nd_c)::value;
@@ -441,19 +262,19 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
         for (int n = 0; n < ND; n++)
 #pragma unroll
             for (int e = 0; e < 4; e++) r[n][e] = __longlong_as_double((long long)__ldcs(src[n] + t + 64 * e));
-        uint64_t* tl[2] = {sa, sb};
 #pragma unroll
         for (int ph = 0; ph < 4; ph++) {
             const int u0 = 2 * ph;
             const int lo_bit = 6 - u0;
-            const int olow = t & ((1 << lo_bit) - 1), ohigh = t >> lo_bit;
-            const int base = (ohigh << (lo_bit + 2)) | olow;
+            const int ohigh = t >> lo_bit;
             if (ph > 0) {
+                const int x = ph - 1;
 #pragma unroll
-                for (int n = 0; n < ND; n++)
+                for (int n = 0; n < ND; n++) {
+                    const double* b = reinterpret_cast<const double*>(sm + (2 * n + (x & 1)) * K5_TILE) + rd[x];
 #pragma unroll
-                    for (int e = 0; e < 4; e++)
-                        r[n][e] = reinterpret_cast<const double*>(tl[n])[G::addr(0, base | (e << lo_bit))];
+                    for (int e = 0; e < 4; e++) r[n][e] = b[e * step(x, lo_bit)];
+                }
             }
 #pragma unroll
             for (int uu = 0; uu < 2; uu++) {
@@ -463,7 +284,7 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
 #pragma unroll
                 for (int k = 0; k < 2; k++) {
                     if (k >= (1 << uu)) break;
-                    const double W = tws[tbase + k];
+                    const double W = tws5[tbase + k];
 #pragma unroll
                     for (int e0 = 0; e0 < 2; e0++) {
                         if (e0 >= dist) break;
@@ -479,12 +300,13 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
                 }
             }
             if (ph < 3) {
-                if (ph == 0) __syncthreads();   // the previous round's phase-3 reads are done
+                if (ph == 0) __syncthreads();   // the previous round's phase-3 reads of A are done
 #pragma unroll
-                for (int n = 0; n < ND; n++)
+                for (int n = 0; n < ND; n++) {
+                    double* b = reinterpret_cast<double*>(sm + (2 * n + (ph & 1)) * K5_TILE) + wr[ph];
 #pragma unroll
-                    for (int e = 0; e < 4; e++)
-                        reinterpret_cast<double*>(tl[n])[G::addr(0, base | (e << lo_bit))] = r[n][e];
+                    for (int e = 0; e < 4; e++) b[e * step(ph, lo_bit)] = r[n][e];
+                }
                 __syncthreads();
             }
         }
@@ -500,8 +322,8 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
 #pragma unroll
             for (int e = 0; e < 4; e++) {
                 const uint64_t D = d_rep4(r[n][e], tq52);
-                mac128(acc0[e], D, kbv[e]);
-                mac128(acc1[e], D, kav[e]);
+                mac_split(0, e, D, kbv[e]);
+                mac_split(1, e, D, kav[e]);
             }
         }
     };
@@ -510,7 +332,7 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     int idx = 0;
     for (; idx + 1 < n_nd; idx += 2) run(std::integral_constant<int, 2>(), digit(idx), digit(idx + 1));
     if (idx < n_nd) run(std::integral_constant<int, 1>(), digit(idx), digit(idx));
-    {   // the diagonal digit: d_ri, already in the NTT domain (canonical), elements 4t + e
+    {   // the diagonal digit: d_ri, already in the NTT domain (canonical < q), elements 4t + e
         const uint64_t* src = tile_src(ri) + 4 * t;
         const ulonglong2 d0 = __ldg(reinterpret_cast<const ulonglong2*>(src));
         const ulonglong2 d1 = __ldg(reinterpret_cast<const ulonglong2*>(src) + 1);
@@ -518,191 +340,55 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
         const uint64_t* kb = key_r + ri * kstride_j + 4 * t;
 #pragma unroll
         for (int e = 0; e < 4; e++) {
-            mac128(acc0[e], dv[e], __ldg(kb + e));
-            mac128(acc1[e], dv[e], __ldg(kb + kstride_p + e));
+            mac_split(0, e, dv[e], __ldg(kb + e));
+            mac_split(1, e, dv[e], __ldg(kb + kstride_p + e));
         }
     }
+    // recombine A0 + A1 2^25 + A2 2^57 (< 2^107) as 128 bits, one Barrett reduction per word
+    auto fold = [&](int h, int e) {
+        uint64_t lo = A0[h][e], hi = 0;
+        const uint64_t t1 = A1[h][e] << 25;
+        lo += t1;
+        hi += (A1[h][e] >> 39) + (lo < t1);
+        const uint64_t t2 = A2[h][e] << 57;
+        lo += t2;
+        hi += (A2[h][e] >> 7) + (lo < t2);
+        return barrett128(lo, hi, md);
+    };
     ulonglong2* o0 = reinterpret_cast<ulonglong2*>(out0 + 4 * t);
     ulonglong2* o1 = reinterpret_cast<ulonglong2*>(out1 + 4 * t);
-    o0[0] = make_ulonglong2(barrett128(acc0[0].lo, acc0[0].hi, md), barrett128(acc0[1].lo, acc0[1].hi, md));
-    o0[1] = make_ulonglong2(barrett128(acc0[2].lo, acc0[2].hi, md), barrett128(acc0[3].lo, acc0[3].hi, md));
-    o1[0] = make_ulonglong2(barrett128(acc1[0].lo, acc1[0].hi, md), barrett128(acc1[1].lo, acc1[1].hi, md));
-    o1[1] = make_ulonglong2(barrett128(acc1[2].lo, acc1[2].hi, md), barrett128(acc1[3].lo, acc1[3].hi, md));
-}
-
-// K4 with NT digits in flight (variant 50+): generalises k_ks_ip2; the digits j != ri are taken
-// NT at a time (the last group may be smaller), then the diagonal digit
-template <int LOG_M, int LOG_R, int MINB, int NT>
-__global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ipN(KsJob job, Tables tb) {
-    using G = Geo<LOG_M, LOG_R>;
-    extern __shared__ uint64_t sm[];
-    double* tws = reinterpret_cast<double*>(sm + NT * G::STRIDE);
-    const int nz = job.nz;
-    const int z = blockIdx.x % nz;
-    const int ri = blockIdx.y;
-    const int l1 = job.l1;
-    const int nri = l1 + 1;
-    const int log_n = tb.log_n;
-    const int row0 = blockIdx.x / nz;
-    const long long off0 = (long long)row0 << LOG_M;
-    const int mi = job.mod_map[ri];
-    const Mod md = tb.mods[mi];
-    const bool fp = (double)md.q < tb.f64_max_q;
-    const double2 qd = fp ? tb.modd[mi] : make_double2(0, 0);
-    const double tq52 = __dadd_rn(2.0 * qd.x, 4503599627370496.0);
-    constexpr int NTHR = G::T;
-    constexpr int EPT = G::R;
-    U128 acc0[EPT], acc1[EPT];
-#pragma unroll
-    for (int k = 0; k < EPT; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
-    const int t = threadIdx.x;
-    const long long kstride_j = 2ll * (job.L + 1) << log_n;
-    const long long kstride_p = (long long)(job.L + 1) << log_n;
-    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
-    if (fp) {
-        const double* twg = tb.fwd_d + ((long long)mi << log_n);
-        const int s0 = log_n - LOG_M;
-        for (int idx = threadIdx.x + 1; idx < G::M; idx += NTHR) {
-            const int u = 31 - __clz(idx), m = idx - (1 << u);
-            tws[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
-        }
-    }
-    auto copy_tile = [&](uint64_t* dst, int j) {
-        const uint64_t* src = (j == ri) ? job.d[z] + ((long long)j << log_n) + off0
-                                        : job.t1[z] + (((long long)j * nri + ri) << log_n) + off0;
-#pragma unroll
-        for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * NTHR;
-            const unsigned s_ = (unsigned)__cvta_generic_to_shared(&dst[G::addr(0, i)]);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_), "l"(src + i) : "memory");
-        }
-    };
-    auto mac_tile = [&](const uint64_t* buf, int j, bool conv) {
-        const uint64_t* kb = key_r + j * kstride_j;
-        const uint64_t* ka = kb + kstride_p;
-#pragma unroll
-        for (int k = 0; k < EPT; k++) {
-            const int i = threadIdx.x + k * NTHR;
-            uint64_t D = buf[G::addr(0, i)];
-            if (conv) D = d_rep4(__longlong_as_double((long long)D), tq52);
-            mac128(acc0[k], D, __ldg(kb + i));
-            mac128(acc1[k], D, __ldg(ka + i));
-        }
-    };
-    int js[NT];
-    int j = (ri == 0) ? 1 : 0;
-    while (j < l1) {
-        int n = 0;
-        while (n < NT && j < l1) {
-            js[n++] = j;
-            j++;
-            if (j == ri) j++;
-        }
-        for (int m = 0; m < n; m++) copy_tile(sm + m * G::STRIDE, js[m]);
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-        __syncthreads();
-        if (fp && n == NT) {
-            double* tl[NT];
-#pragma unroll
-            for (int m = 0; m < NT; m++) tl[m] = reinterpret_cast<double*>(sm + m * G::STRIDE);
-            fwd_engine_f64_rowtwN<LOG_M, LOG_R, NT>(tl, qd.x, qd.y, tws, t);
-        } else {
-            for (int m = 0; m < n; m++) {
-                if (fp)
-                    fwd_engine_f64_rowtw<LOG_M, LOG_R>(reinterpret_cast<double*>(sm + m * G::STRIDE), qd.x, qd.y, tws,
-                                                       t);
-                else
-                    fwd_engine<LOG_M, LOG_R>(sm + m * G::STRIDE, md.q, tb.fwd + ((long long)mi << log_n),
-                                             log_n - LOG_M, (uint32_t)row0, 0, t);
-            }
-        }
-        for (int m = 0; m < n; m++) mac_tile(sm + m * G::STRIDE, js[m], fp);
-        __syncthreads();
-    }
-    if (ri < l1) {
-        copy_tile(sm, ri);
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
-        __syncthreads();
-        mac_tile(sm, ri, false);
-    }
-    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
-    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
-#pragma unroll
-    for (int k = 0; k < EPT; k++) {
-        const int i = threadIdx.x + k * NTHR;
-        out0[i] = barrett128(acc0[k].lo, acc0[k].hi, md);
-        out1[i] = barrett128(acc1[k].lo, acc1[k].hi, md);
-    }
-}
-
-template <int LOG_M, int LOG_R, int MINB, int NT>
-static cudaError_t ks_ipN_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
-    using G = Geo<LOG_M, LOG_R>;
-    const int rows = 1 << (tb.log_n - LOG_M);
-    const size_t smem = ((size_t)NT * G::STRIDE + G::M) * sizeof(uint64_t);
-    dim3 grid(rows * nz, job.l1 + 1, 1);
-    k_ks_ipN<LOG_M, LOG_R, MINB, NT><<<grid, G::T, smem, st>>>(job, tb);
-    return cudaGetLastError();
+    o0[0] = make_ulonglong2(fold(0, 0), fold(0, 1));
+    o0[1] = make_ulonglong2(fold(0, 2), fold(0, 3));
+    o1[0] = make_ulonglong2(fold(1, 0), fold(1, 1));
+    o1[1] = make_ulonglong2(fold(1, 2), fold(1, 3));
 }
 
 template <int MINB>
 static cudaError_t ks_ip5_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
-    using G = Geo<8, 2>;
     const int rows = 1 << (tb.log_n - 8);
-    const size_t smem = (2 * (size_t)G::STRIDE + G::M) * sizeof(uint64_t);
+    const size_t smem = (4 * (size_t)K5_TILE + 256) * sizeof(uint64_t);   // 4 exchange tiles + twiddles
     dim3 grid(rows * nz, job.l1 + 1, 1);
     k_ks_ip5<MINB><<<grid, 64, smem, st>>>(job, tb);
     return cudaGetLastError();
 }
 
-template <int LOG_M, int LOG_R, int MINB, bool PF = false>
+template <int LOG_M, int LOG_R, int MINB>
 static cudaError_t ks_ip2_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     using G = Geo<LOG_M, LOG_R>;
     const int rows = 1 << (tb.log_n - LOG_M);
     const size_t smem = (2 * (size_t)G::STRIDE + G::M) * sizeof(uint64_t);
     dim3 grid(rows * nz, job.l1 + 1, 1);
-    k_ks_ip2<LOG_M, LOG_R, MINB, PF><<<grid, G::T, smem, st>>>(job, tb);
+    k_ks_ip2<LOG_M, LOG_R, MINB><<<grid, G::T, smem, st>>>(job, tb);
     return cudaGetLastError();
-}
-
-template <int LOG_M, int LOG_R, int GR, int MINB>
-static cudaError_t ks_ip_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
-    using G = Geo<LOG_M, LOG_R>;
-    const int rows = 1 << (tb.log_n - LOG_M);
-    if (rows < GR) return cudaErrorInvalidValue;
-    constexpr int threads = GR * G::T;
-    const size_t smem = ((size_t)GR * G::STRIDE + (GR == 1 ? G::M : 0)) * sizeof(uint64_t);
-    dim3 grid((rows / GR) * nz, job.l1 + 1, 1);
-    k_ks_ip<LOG_M, LOG_R, GR, MINB><<<grid, threads, smem, st>>>(job, tb);
-    return cudaGetLastError();
-}
-
-static int ks_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("HISA_KS_VARIANT");
-        v = e ? atoi(e) : 0;
-    }
-    return v;
 }
 
 template <int LOG_M>
 static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
-    const int rows = 1 << (tb.log_n - LOG_M);
-    switch (ks_variant()) {   // alternatives kept for re-measurement (profiles/r1_ks_variants.txt)
-        case 10: return ks_ip_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
-        case 20: return ks_ip_pipe_t<LOG_M, 2, 1, 8>(job, tb, nz, st);
-        case 41: return ks_ip2_t<LOG_M, 2, 12, true>(job, tb, nz, st);
-        case 55: return ks_ipN_t<LOG_M, 2, 12, 3>(job, tb, nz, st);
-        case 33: return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
-        case 80: if constexpr (LOG_M == 8) return ks_ip5_t<12>(job, tb, nz, st); break;
-        default: break;
-    }
-    // default (measured best on B200 at N = 2^16, L = 24; profiles/r1_ks_variants.txt): M = 256
-    // rows -> the register-direct two-digit kernel (variant 81, >= 10 CTAs / SM); other row
-    // lengths -> variant 33 (one row per 64-thread CTA, radix-4 phases, two digits interleaved
-    // through the FP64 engine with the row's twiddles staged in shared memory, >= 12 CTAs / SM)
-    if constexpr (LOG_M == 8) return ks_ip5_t<10>(job, tb, nz, st);
+    // measured best on B200 (profiles/r1_ks_variants.txt, profiles/r2_*): M = 256 rows -> the
+    // register-direct two-digit kernel k_ks_ip5 (>= 10 CTAs / SM); other row lengths -> k_ks_ip2
+    // (one row per 64-thread CTA, radix-4 phases, two digits interleaved through the FP64 engine
+    // with the row's twiddles staged in shared memory, >= 12 CTAs / SM)
+    if constexpr (LOG_M == 8) return ks_ip5_t<K5_MINB>(job, tb, nz, st);
     return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
 }
 
@@ -716,65 +402,6 @@ cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_
         case 8: return ks_ip_m<8>(job, tb, nz, st);
     }
     return cudaErrorInvalidValue;
-}
-
-// ------------------------------------------------------------------------------------------
-// K7 hoisted inner product: R rotation amounts share one materialised ModUp output D (hoisting,
-// P:717 "rotations ... code motioned out").  Each thread owns two words of one output prime ri,
-// streams D[j][ri] once and the R keys' (b, a) limbs, and keeps 2R 128-bit accumulators per word.
-// Pure HBM stream: (1 + 2R) 16-byte loads per digit per thread, no shared memory.
-// ------------------------------------------------------------------------------------------
-template <int R>
-__global__ void __launch_bounds__(256) k_ks_ip_hoisted(KsHoistJob job, const Mod* __restrict__ mods, int log_n) {
-    const int ri = blockIdx.y;
-    const int l1 = job.l1, l2 = l1 + 1;
-    const long long N = 1ll << log_n;
-    const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
-    if (x >= N) return;
-    const int mi = job.mod_map[ri];
-    const Mod md = mods[mi];
-    U128 acc[R][2][2];
-#pragma unroll
-    for (int k = 0; k < R; k++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) { acc[k][h][0] = U128{0, 0}; acc[k][h][1] = U128{0, 0}; }
-    const long long kstride_j = 2ll * (job.L + 1) * N;
-    const long long kstride_p = (long long)(job.L + 1) * N;
-    const long long koff = (long long)mi * N + x;
-    for (int j = 0; j < l1; j++) {
-        const uint64_t* src = (j == ri) ? job.diag + (long long)j * N + x : job.D + ((long long)j * l2 + ri) * N + x;
-        const ulonglong2 d = __ldcs(reinterpret_cast<const ulonglong2*>(src));
-#pragma unroll
-        for (int k = 0; k < R; k++) {
-            const uint64_t* kb = job.key[k] + j * kstride_j + koff;
-            const ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2*>(kb));
-            const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(kb + kstride_p));
-            mac128(acc[k][0][0], d.x, b.x);
-            mac128(acc[k][0][1], d.y, b.y);
-            mac128(acc[k][1][0], d.x, a.x);
-            mac128(acc[k][1][1], d.y, a.y);
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < R; k++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            uint64_t* o = job.acc[k] + ((long long)h * l2 + ri) * N + x;
-            *reinterpret_cast<ulonglong2*>(o) = make_ulonglong2(barrett128(acc[k][h][0].lo, acc[k][h][0].hi, md),
-                                                                barrett128(acc[k][h][1].lo, acc[k][h][1].hi, md));
-        }
-}
-
-cudaError_t launch_ks_ip_hoisted(const KsHoistJob& job, int R, const Mod* mods, int log_n, cudaStream_t st) {
-    const long long N = 1ll << log_n;
-    dim3 grid((unsigned)((N / 2 + 255) / 256), job.l1 + 1, 1);
-    switch (R) {
-#define C(RR) case RR: k_ks_ip_hoisted<RR><<<grid, 256, 0, st>>>(job, mods, log_n); break;
-        C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8)
-#undef C
-        default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------------------

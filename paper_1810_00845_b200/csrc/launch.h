@@ -53,19 +53,7 @@ struct MpaJob {
 cudaError_t launch_mulplain_acc(const uint64_t* const* in_ptrs, const uint64_t* const* pt_ptrs,
                                 uint64_t* const* out_ptrs, const MpaJob& job, const Mod* mods, cudaStream_t st);
 
-// hoisted key-switch inner product (K7): for R rotation amounts sharing one ModUp output D,
-// acc_k[b|a][ri] = sum_j D[j][ri] (.) key_k[j][b|a][ri] -- an HBM stream of the R keys
 constexpr int MAXR = 8;
-struct KsHoistJob {
-    const uint64_t* D;            // [j][ri][N], ri over l+2 output primes (diagonal entries unused)
-    const uint64_t* diag;         // the digit source in NTT form [(l+1)][N] (D_{j,q_j} = d_j)
-    const uint64_t* key[MAXR];    // [L][2][L+1][N] per amount (pre-permuted, see hisa.cu)
-    uint64_t* acc[MAXR];          // out [2][l+2][N], fully reduced
-    int l1;
-    int L;
-    uint8_t mod_map[MAXL];
-};
-cudaError_t launch_ks_ip_hoisted(const KsHoistJob& job, int R, const Mod* mods, int log_n, cudaStream_t st);
 
 // K7 over CG ciphertexts sharing the R keys (every key word streamed once per CG ciphertexts)
 constexpr int MAXCG = 4;

@@ -247,64 +247,6 @@ __device__ __forceinline__ void fwd_engine_f64_rowtw2(double* sa, double* sb, do
     }
 }
 
-// NT tiles of the same prime and row through the staged-twiddle engine together (generalises
-// fwd_engine_f64_rowtw2): NT times the independent FP64 dependency chains per thread
-template <int LOG_M, int LOG_R, int NT>
-__device__ __forceinline__ void fwd_engine_f64_rowtwN(double* const* tiles, double q, double qinv,
-                                                      const double* tws, int t) {
-    using G = Geo<LOG_M, LOG_R>;
-#pragma unroll
-    for (int u0 = 0; u0 < LOG_M; u0 += LOG_R) {
-        const int w = (LOG_M - u0) < LOG_R ? (LOG_M - u0) : LOG_R;
-        const int lo_bit = LOG_M - u0 - w;
-        const int per = G::R >> w;
-#pragma unroll
-        for (int x = 0; x < G::R; x++) {
-            if (x >= per) break;
-            const int o = t * per + x;
-            const int olow = o & ((1 << lo_bit) - 1);
-            const int ohigh = o >> lo_bit;
-            double r[NT][G::R];
-            int base = (ohigh << (lo_bit + w)) | olow;
-#pragma unroll
-            for (int e = 0; e < G::R; e++)
-                if (e < (1 << w))
-#pragma unroll
-                    for (int n = 0; n < NT; n++) r[n][e] = tiles[n][G::addr(0, base | (e << lo_bit))];
-#pragma unroll
-            for (int uu = 0; uu < LOG_R; uu++) {
-                if (uu >= w) break;
-                const int u = u0 + uu;
-                const int dist = 1 << (w - 1 - uu);
-                const int tbase = (1 << u) + (ohigh << uu);
-#pragma unroll
-                for (int k = 0; k < (1 << LOG_R); k++) {
-                    if (k >= (1 << uu)) break;
-                    const double W = tws[tbase + k];
-#pragma unroll
-                    for (int e0 = 0; e0 < G::R; e0++) {
-                        if (e0 >= dist) break;
-                        const int e = k * 2 * dist + e0;
-#pragma unroll
-                        for (int n = 0; n < NT; n++) {
-                            const double X = full_stage(u, LOG_M) ? redd(r[n][e], q, qinv) : r[n][e];
-                            const double T = mulred(r[n][e + dist], W, q, qinv);
-                            r[n][e] = __dadd_rn(X, T);
-                            r[n][e + dist] = __dsub_rn(X, T);
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < G::R; e++)
-                if (e < (1 << w))
-#pragma unroll
-                    for (int n = 0; n < NT; n++) tiles[n][G::addr(0, base | (e << lo_bit))] = r[n][e];
-        }
-        __syncthreads();
-    }
-}
-
 // inverse GS stages, mirrors inv_engine (ntt.cuh)
 template <int LOG_M, int LOG_R>
 __device__ __forceinline__ void inv_engine_f64(double* sm, double q, double qinv, const double* __restrict__ tw,

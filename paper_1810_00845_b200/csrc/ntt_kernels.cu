@@ -591,17 +591,9 @@ __global__ void __launch_bounds__(256, MINB) k_inv_cols(PassJob job, Tables tb) 
 }
 
 // ------------------------------------------------------------------------------------------
-// host launchers.  Variant (HISA_NTT_VARIANT, tuned on B200): radix of the engine phases
-// (LOG_R) and the __launch_bounds__ minimum blocks per SM.
+// host launchers: radix of the engine phases (LOG_R) and the __launch_bounds__ minimum blocks
+// per SM, tuned on B200.
 // ------------------------------------------------------------------------------------------
-static int ntt_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("HISA_NTT_VARIANT");
-        v = e ? atoi(e) : 0;
-    }
-    return v;
-}
 
 template <int LOG_M, int LOG_R>
 static void launch_geom(int log_m_other, int& threads, int& gx, size_t& smem) {
@@ -622,7 +614,7 @@ static cudaError_t fwd_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     constexpr int FULL = 256 / Geo<LOG_M, LOG_R>::T;
     const bool full = threads == 256;
     if constexpr (LOG_M == 8 && LOG_R == 4) {
-        if (full && ntt_variant() != 2) {   // register-direct radix-16 form (variant 2: smem engine)
+        if (full) {   // register-direct radix-16 form
             if (lift) k_fwd_cols_r16<LOAD_LIFT, 4><<<grid, 256, smem, st>>>(job, tb);   // MINB 3: slower
             else k_fwd_cols_r16<LOAD_PLAIN, 4><<<grid, 256, smem, st>>>(job, tb);
             return cudaGetLastError();
@@ -643,7 +635,7 @@ static cudaError_t fwd_rows_v(const PassJob& job, const Tables& tb, int nlimbs, 
     launch_geom<LOG_M, LOG_R>(tb.log_n - LOG_M, threads, gx, smem);
     dim3 grid(gx, nlimbs, nz);
     if constexpr (LOG_M == 8 && LOG_R == 4) {
-        if (threads == 256 && ntt_variant() != 2) {   // register-direct radix-16 form
+        if (threads == 256) {   // register-direct radix-16 form
             if (combine) k_fwd_rows_r16<STORE_COMBINE><<<grid, 256, smem, st>>>(job, tb);
             else k_fwd_rows_r16<STORE_PLAIN><<<grid, 256, smem, st>>>(job, tb);
             return cudaGetLastError();
@@ -674,7 +666,7 @@ static cudaError_t inv_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     dim3 grid(gx, nlimbs, nz);
     constexpr int FULL = 256 / Geo<LOG_M, LOG_R>::T;
     if constexpr (LOG_M == 8 && LOG_R == 4) {
-        if (threads == 256 && ntt_variant() != 2) {   // register-direct radix-16 form
+        if (threads == 256) {   // register-direct radix-16 form
             k_inv_cols_r16<<<grid, 256, smem, st>>>(job, tb);
             return cudaGetLastError();
         }
@@ -684,7 +676,7 @@ static cudaError_t inv_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     return cudaGetLastError();
 }
 // radix-16 phases, __launch_bounds__(256, 4): measured best (MINB 1 / radix-4 variants removed,
-// profiles/r1_ks_variants.txt); HISA_NTT_VARIANT=2 selects the shared-memory engine at M = 256
+// profiles/r1_ks_variants.txt); at M = 256 with full 256-thread CTAs the register-direct forms run
 #define NTT_DISPATCH(FN, ...) return FN<LM, 4, 4>(__VA_ARGS__);
 template <int LM>
 static cudaError_t fwd_cols_t(const PassJob& job, const Tables& tb, int nlimbs, int nz, int lift, cudaStream_t st) {

@@ -10,7 +10,8 @@ produced by the sm_100a kernels behind the C-ABI.
     loop AND share one ModUp per input channel (hisa_rot_left_hoisted, K7); the
     mulScalar + add accumulation over all (ic, tap) for all OC outputs is ONE fused kernel
     (hisa_conv_accumulate, K8); one divScalar per output.
-  * activation a0 + a1 x + a2 x^2 (A25) folded to sign(a2) x'^2 + const: one level.
+  * activation a0 + a1 x + a2 x^2 (P:822, A25) folded to sign(a2) x'^2 + const: one level;
+    per-activation compile-time gains (A41) keep small signals above the CKKS noise floor.
   * 2x2 average pool: three hoisted rotations + adds, 1/4 folded forward (A26).
   * FC / matmul (A27, R = 1): mulPlain per input channel, rescale, rotate-and-sum
     with every output neuron's rotation batched under one key (hisa_rot_left_batch).
@@ -58,24 +59,46 @@ class Layout:
         return self.origin + (self.H - 1) * self.hS + (self.W - 1) * self.wS + 1
 
 
-def act_fold(coeffs):
-    """A25: a2 x^2 + a1 x + a0 = x'^2 + gamma with x' = r x + beta (a2 > 0)."""
+def act_fold(coeffs, gain: float = 1.0):
+    """A25 with a compile-time output gain G (A41): G (a2 x^2 + a1 x + a0) = x'^2 + gamma with
+    x' = r x + beta, r = sqrt(a2 G), beta = r a1 / (2 a2), gamma = G (a0 - a1^2 / (4 a2))
+    (a2 > 0).  G = 1 is the plain fold."""
     a0, a1, a2 = coeffs
     if not a2 > 0:
         raise ValueError("folded activation needs a2 > 0")
-    r = math.sqrt(a2)
-    return r, r * a1 / (2 * a2), a0 - a1 * a1 / (4 * a2)
+    r = math.sqrt(a2 * gain)
+    return r, r * a1 / (2 * a2), gain * (a0 - a1 * a1 / (4 * a2))
+
+
+def act_gains(net: dict):
+    """A41: the compile-time gain of every activation in execution order ("act" layers; a fire
+    module's squeeze then its expand), powers of 4 (so sqrt(a2 G) = sqrt(a2) 2^e and every
+    weight rewrite below is exact in any order); default 1."""
+    n_act = sum(1 if layer[0] == "act" else 2 if layer[0] == "fire" else 0 for layer in net["layers"])
+    gains = [float(g) for g in net.get("act_gains", [1.0] * n_act)]
+    if len(gains) != n_act:
+        raise ValueError(f"act_gains: {len(gains)} given, the net has {n_act} activations")
+    for g in gains:
+        m, e = math.frexp(g)
+        if m != 0.5 or (e - 1) % 2:
+            raise ValueError(f"act gain {g} is not a power of 4")
+    return gains
 
 
 def compile_weights(net: dict, weights, act_coeffs):
     """Compile-time weight rewriting: avg-pool 1/4 factors pushed into the next linear layer
     (A26), the global-average-pool 1/(H W) into the linear layer before it (A26), and the
     activation scale / bias folded into the preceding linear layer (A25; a fire module's three
-    convs are each followed by an activation).
-    Returns ([(W', beta)] per weight tensor, in order, gamma)."""
-    r, beta, gamma = act_fold(act_coeffs)
+    convs are each followed by an activation).  With activation gains (A41) every encrypted
+    tensor holds G x its float64 value: a linear layer followed by an activation of gain G_out
+    divides its weights by the gain G_in of its input and folds r = sqrt(a2 G_out); any other
+    linear layer keeps the gain.
+    Returns ([(W', beta)] per weight tensor, in order, [gamma] per activation, [(gain, offset)]
+    per layer: the layer's encrypted output holds gain x value + offset (a linear layer feeding
+    an activation holds its folded x' = r x + beta))."""
+    gains = iter(act_gains(net))
     layers = net["layers"]
-    out, pending, it = [], 1.0, iter(weights)
+    out, gammas, layer_affine, pending, it, g_cur = [], [], [], 1.0, iter(weights), 1.0
     c, h, w = net["input"]
     for i, layer in enumerate(layers):
         kind = layer[0]
@@ -90,16 +113,34 @@ def compile_weights(net: dict, weights, act_coeffs):
                 c = oc
             else:
                 c, h, w = layer[1], 1, 1
-            f = pending * (r if nxt == "act" else 1.0) * (1.0 / (h * w) if nxt == "gap" else 1.0)
-            out.append((np.asarray(next(it), dtype=np.float64) * f, beta if nxt == "act" else 0.0))
+            if nxt == "act":
+                g_out = next(gains)
+                r, beta, gamma = act_fold(act_coeffs, g_out)
+                gammas.append(gamma)
+                f = pending * r / g_cur
+                g_cur = g_out
+                affine = (r, beta)
+            else:
+                f, beta = pending, 0.0
+                affine = (g_cur, 0.0)
+            if nxt == "gap":
+                f = f * (1.0 / (h * w))
+                affine = (affine[0] / (h * w), 0.0)       # the gap's 1/(H W) folded in (A26)
+            out.append((np.asarray(next(it), dtype=np.float64) * f, beta))
             pending = 1.0
         elif kind == "fire":
-            out.append((np.asarray(next(it), dtype=np.float64) * pending * r, beta))   # squeeze
-            out.append((np.asarray(next(it), dtype=np.float64) * r, beta))             # expand 1x1
-            out.append((np.asarray(next(it), dtype=np.float64) * r, beta))             # expand 3x3
-            pending = 1.0
+            g_sq, g_ex = next(gains), next(gains)
+            r_sq, beta_sq, gamma_sq = act_fold(act_coeffs, g_sq)
+            r_ex, beta_ex, gamma_ex = act_fold(act_coeffs, g_ex)
+            out.append((np.asarray(next(it), dtype=np.float64) * (pending * r_sq / g_cur), beta_sq))  # squeeze
+            out.append((np.asarray(next(it), dtype=np.float64) * (r_ex / g_sq), beta_ex))             # expand 1x1
+            out.append((np.asarray(next(it), dtype=np.float64) * (r_ex / g_sq), beta_ex))             # expand 3x3
+            gammas += [gamma_sq, gamma_ex]
+            pending, g_cur = 1.0, g_ex
             c = layer[2] + layer[3]
-    return out, gamma
+        # a pool's 1/4 is folded forward (A26): its output holds the sum, g_cur / pending x the mean
+        layer_affine.append(affine if kind in ("conv", "fc") else (g_cur / pending, 0.0))
+    return out, gammas, layer_affine
 
 
 def input_layout(net: dict) -> Layout:
@@ -239,7 +280,8 @@ class EncryptedNet:
         self.rot_policy = rot_policy
         self.b = backend
         self.net = net
-        self.folded, self.gamma = compile_weights(net, weights, act_coeffs)
+        self.folded, self.gammas, self.layer_affine = compile_weights(net, weights, act_coeffs)
+        self._act_i = 0
         self.slots = backend.slots
         self.q = list(backend.q)
         self._pts = {}
@@ -283,11 +325,15 @@ class EncryptedNet:
             self.b.free(pt)
         return cts, lay
 
-    def decrypt_output(self, cts, lay) -> np.ndarray:
+    def decrypt_output(self, cts, lay, affine=None) -> np.ndarray:
+        """Decrypt + decode, undoing the tensor's compile-time (gain, offset) (A41; default: the
+        network output's; an intermediate layer li passes self.layer_affine[li])."""
+        g, off = self.layer_affine[-1] if affine is None else affine
         vals = []
         for ct in cts:
             pt = self.b.decrypt(ct)
-            vals.append(self.b.decode(pt, self.slots))
+            v = self.b.decode(pt, self.slots)
+            vals.append((v - off) / g if off else v / g)
             self.b.free(pt)
         if lay.kind == "slot0":
             return np.array([v[0] for v in vals])
@@ -515,12 +561,17 @@ class EncryptedNet:
         return parallel.reduce_scatter_partials(self, rotated, wmat, n_out)
 
     def act(self, cts, lay, square_only=False):
-        """(A25) x'^2 + gamma: tensor + relinearize + rescale (+ addScalar): one level."""
+        """(A25) x'^2 + gamma: tensor + relinearize + rescale (+ addScalar): one level.
+        gamma is this activation's (gain-scaled, A41) constant, in execution order."""
         sq = self.b.mul_batch(list(cts), list(cts))       # tensor + relin, batched
         out = self.b.rescale_batch(sq)
         self._free_all(sq)
-        if not square_only and self.gamma:
-            out2 = [self.b.add_scalar(r, self.gamma) for r in out]
+        gamma = 0.0
+        if not square_only:
+            gamma = self.gammas[self._act_i]
+            self._act_i += 1
+        if gamma:
+            out2 = [self.b.add_scalar(r, gamma) for r in out]
             self._free_all(out)
             out = out2
         return out, replace(lay, clean=False)
@@ -710,6 +761,7 @@ class EncryptedNet:
         `trace(layer_index, cts, layout)` (optional) is called after every layer, before the
         layer's inputs are freed (per-layer parity checks)."""
         wi = 0
+        self._act_i = 0
         cur = list(cts)
         for li, layer in enumerate(self.net["layers"]):
             kind = layer[0]

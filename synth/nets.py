@@ -18,6 +18,9 @@ Layer tuples (PyTorch semantics for the float64 definition):
                                    out = concat(act(conv1x1(s)) [e1 ch], act(conv3x3 SAME(s)) [e3 ch])
     ("gap",)                       global average pool (config 5)
 Convs and FCs have no bias (A34).
+"act_gains" (A41): compile-time gain (a power of 4) of every activation in execution order (a fire
+module's squeeze, then its expand), written from tools/calibrate_gains.py (float64 network on a
+calibration image, T = 16); a lowering choice like R, not semantics.
 """
 from __future__ import annotations
 
@@ -36,25 +39,25 @@ NETS = {
     # lowered with R = 8 replicas (A27: the measured-cheaper lowering on B200, 6 of 6 levels)
     "lenet_small": dict(log_n=14, q_bits=[60] + [40] * 6, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
                         layers=[("conv", 5, 5, 2, 1), ("act",), ("fc", 100, 8), ("act",), ("fc", 10)],
-                        sigma=[0.1, 0.1, 0.1]),
+                        sigma=[0.1, 0.1, 0.1], act_gains=[4.0 ** 3, 4.0 ** 2]),
     # config 4: LeNet-5-large-shaped (A32: SAME 5x5 convs, 28 -> 14 -> 7, 7*7*64 = 3136)
     "lenet_large": dict(log_n=15, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
                         layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2), ("act",),
                                 ("avgpool",), ("fc", 512, 16), ("act",), ("fc", 10)],
-                        sigma=[0.05, 0.05, 0.05, 0.05]),
+                        sigma=[0.05, 0.05, 0.05, 0.05], act_gains=[4.0 ** 2, 4.0 ** 3, 4.0 ** 3]),
     # config 4 with its second conv CHW-tiled (several channels per ciphertext; the paper's
     # layout comparison, Fig. tilings)
     "lenet_large_chw": dict(log_n=15, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
                             layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2, "chw"),
                                     ("act",), ("avgpool",), ("fc", 512, 16), ("act",), ("fc", 10)],
-                            sigma=[0.05, 0.05, 0.05, 0.05]),
+                            sigma=[0.05, 0.05, 0.05, 0.05], act_gains=[4.0 ** 2, 4.0 ** 3, 4.0 ** 3]),
     # config 5: SqueezeNet-CIFAR-shaped (A33: conv1 + 4 fire modules + 1x1 conv + global avg pool;
     # 1 + 4*2 + 1 = 10 conv layers, 9 activations), N = 2^16, 24 limbs
     "squeezenet": dict(log_n=16, q_bits=[60] + [40] * 23, p_bits=60, scale=2.0 ** 40, input=(3, 32, 32),
                        layers=[("conv", 64, 3, 1, 1), ("act",), ("avgpool",), ("fire", 16, 32, 32),
                                ("fire", 16, 32, 32), ("avgpool",), ("fire", 32, 64, 64), ("fire", 32, 64, 64),
                                ("conv", 10, 1, 1, 0), ("gap",)],
-                       sigma=[0.05] * 14),
+                       sigma=[0.05] * 14, act_gains=[4.0 ** 2] + [4.0 ** e for e in range(4, 12)]),
 }
 
 

@@ -11,14 +11,33 @@ pytestmark = pytest.mark.gpu
 H = pytest.importorskip("paper_1810_00845_b200.hisa")
 
 
-def _run_pair(net, W, img, oracle_layers=None, rot_policy="exact"):
+# Accuracy bound (A36 + A41): decrypted outputs within REL_BOUND x max |float64| of the
+# float64 network, on top of the north star's 1e-3 absolute.  The CKKS error floor at Delta = 2^40
+# is ~1e-7 per slot (fresh encryption), and the compile-time gains keep every
+# activation's output peaking in (4, 16], so the measured relative error is 1e-7 .. 1e-6; the
+# bound leaves 100x headroom and fails on an all-zero or sign-flipped output (relative error >= 1).
+REL_BOUND = 1e-4
+
+
+def _rel(got, ref):
+    return float(np.abs(np.asarray(got) - ref).max() / np.abs(ref).max())
+
+
+def _run_pair(net, W, img, oracle_layers=None, rot_policy="exact", sample_layers=True):
     """GPU driver vs the oracle's lowering on identical seeded inputs; returns the decrypted
-    GPU output, the oracle's (None if the oracle stops early) and the float64 reference."""
+    GPU output, the oracle's (None if the oracle stops early) and the float64 reference.
+    After every layer <= oracle_layers the GPU ciphertexts must equal the oracle's word for
+    word; after every HW-layout layer two decrypted channels
+    must match the float64 network's intermediate tensor within REL_BOUND.
+    (decrypt_output undoes the layer's (gain, offset): a linear layer feeding an activation holds
+    the folded x' = r x + beta, A25/A41.)"""
     from oracle import plain
     from oracle.nets import OracleNet
     from paper_1810_00845_b200.driver import EncryptedNet
 
-    ref = plain.forward(net, img, W, SN.ACT_COEFFS)
+    ref_trace = []
+    ref = plain.forward(net, img, W, SN.ACT_COEFFS, trace=ref_trace)
+    ref_at = dict(ref_trace)
     on = OracleNet(net, W, SN.ACT_COEFFS, seed=0, rot_policy=rot_policy)
     ocs, olay = on.encrypt_image(img)
     otrace = []
@@ -34,32 +53,50 @@ def _run_pair(net, W, img, oracle_layers=None, rot_policy="exact"):
     for h, oc in zip(cts, ocs):
         assert (g.ct_export(h) == oc.data).all(), "input encryption parity"
     ocheck = dict(otrace)
+    checked = []
 
     def check(li, hs, ly):
-        if li not in ocheck:
-            return
-        octs = ocheck[li]
-        assert len(hs) == len(octs)
-        for c, (h, oc) in enumerate(zip(hs, octs)):
-            lv, _np, sc = g.ct_info(h)
-            assert lv == oc.level and sc == oc.scale, f"layer {li} ch {c}: level/scale"
-            d = g.ct_export(h)
-            if not (d == oc.data).all():
-                raise AssertionError(f"layer {li} {net['layers'][li]} channel {c}: "
-                                     f"{int((d != oc.data).sum())} words differ")
-    out, lay_out = en.forward(cts, lay, trace=check)
-    got = en.decrypt_output(out, lay_out)
+        if li in ocheck:
+            octs = ocheck[li]
+            assert len(hs) == len(octs)
+            for c, (h, oc) in enumerate(zip(hs, octs)):
+                lv, _np, sc = g.ct_info(h)
+                assert lv == oc.level and sc == oc.scale, f"layer {li} ch {c}: level/scale"
+                d = g.ct_export(h)
+                if not (d == oc.data).all():
+                    raise AssertionError(f"layer {li} {net['layers'][li]} channel {c}: "
+                                         f"{int((d != oc.data).sum())} words differ")
+            checked.append(("bit-exact", li))
+        if sample_layers and ly.kind == "hw":
+            from dataclasses import replace
+            n = min(2, len(hs))
+            got_l = en.decrypt_output(hs[:n], replace(ly, C=n), affine=en.layer_affine[li])
+            rel = _rel(got_l, ref_at[li][:n])
+            assert rel <= REL_BOUND, f"layer {li} {net['layers'][li]}: relative error {rel:.3g}"
+            checked.append(("decrypted", li))
+    try:
+        out, lay_out = en.forward(cts, lay, trace=check)
+        got = en.decrypt_output(out, lay_out)
+    finally:
+        g.close()          # a failed check must not leave the 96 GiB arena to the next test
     ogot = on.decrypt_output(ocs_out, olay_out) if oracle_layers is None else None
-    g.close()
+    if oracle_layers is not None:
+        assert ("bit-exact", oracle_layers) in checked
     return got, ogot, ref
+
+
+def _accurate(got, ref):
+    """North star (1e-3 absolute) AND relative to the output's magnitude (REL_BOUND)."""
+    assert got.shape == ref.shape
+    assert np.abs(got - ref).max() <= 1e-3, np.abs(got - ref).max()
+    assert _rel(got, ref) <= REL_BOUND, _rel(got, ref)
 
 
 @pytest.mark.parametrize("name", ["tiny", "lenet_small"])
 def test_driver_bit_exact_and_accurate(name):
     got, ogot, ref = _run_pair(SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0))
-    assert got.shape == ref.shape
-    assert np.abs(got - ref).max() <= 1e-3, np.abs(got - ref).max()
-    assert np.abs(got - ogot).max() < 1e-9
+    _accurate(got, ref)
+    assert _rel(got, ogot) < 1e-9          # same ciphertexts; the two decoders agree to ~1e-16
 
 
 @pytest.mark.parametrize("which", ["every_branch", "replicas", "squeezenet_kinds", "chw"])
@@ -73,31 +110,32 @@ def test_driver_small_nets_bit_exact(which):
               "squeezenet_kinds": (MINI_SQ, _mini_sq_weights()), "chw": (MINI_CHW, _mini_chw_weights())}[which]
     img = SN._image(5, net["input"])
     got, ogot, ref = _run_pair(net, W, img)
-    assert np.abs(got - ref).max() <= 1e-3
-    assert np.abs(got - ogot).max() < 1e-9
+    _accurate(got, ref)
+    assert _rel(got, ogot) < 1e-9          # same ciphertexts; the two decoders agree to ~1e-16
 
 
 @pytest.mark.slow
 def test_driver_lenet_large_sampled():
     """Config 4 (N = 2^15, 14 limbs, FC1 with R = 16 replicas): bit-exact against the oracle
     through conv1 + act + avgpool (the oracle cannot run the 51,200 scalar MACs of conv2 in
-    test time), and the full decrypted output within 1e-3 of the float64 network."""
+    test time), decrypted intermediate layers and the full output within REL_BOUND of float64."""
     name = "lenet_large"
     got, _o, ref = _run_pair(SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0), oracle_layers=2)
     assert got.shape == ref.shape == (10,)
-    assert np.abs(got - ref).max() <= 1e-3, np.abs(got - ref).max()
+    _accurate(got, ref)
 
 
 @pytest.mark.slow
 def test_driver_squeezenet_sampled():
-    """Config 5 (N = 2^16, 24 limbs, all 23 levels): conv1 + activation bit-exact against the
-    oracle at full size (sampled parity), the whole network decrypted within 1e-3 of
-    the float64 network (absolute, the north-star bound; the synthetic N(0, 0.05) weights shrink
-    the logits to ~1e-7, so the relative error is reported by bench.py, not asserted here)."""
+    """Config 5 (N = 2^16, 24 limbs, all 23 levels, compile-time gains A41): bit-exact against
+    the oracle at full size through conv1 + act + avgpool + the first fire module (SURVEY 8d:
+    conv1 + fire2), decrypted intermediate layers and the logits within REL_BOUND of float64
+    (max |logit| ~ 3e-7: the relative bound, not the 1e-3 absolute one, is what can fail)."""
     name = "squeezenet"
-    got, _o, ref = _run_pair(SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0), oracle_layers=1)
+    got, _o, ref = _run_pair(SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0), oracle_layers=3)
     assert got.shape == ref.shape == (10,)
-    assert np.abs(got - ref).max() <= 1e-3, np.abs(got - ref).max()
+    _accurate(got, ref)
+    assert np.array_equal(np.sign(got), np.sign(ref))
 
 
 @pytest.mark.parametrize("name", ["tiny", "lenet_small"])
@@ -115,8 +153,8 @@ def test_driver_pow2_rotation_keys(name):
     assert len(p2["rotations"]) < len(ex["rotations"])
     assert all(((k & (k - 1)) == 0) or (((s - k) & (s - k - 1)) == 0) for k in p2["rotations"])
     got, ogot, ref = _run_pair(net, W, SN.net_image(name, 2), rot_policy="pow2")
-    assert np.abs(got - ref).max() <= 1e-3
-    assert np.abs(got - ogot).max() < 1e-9
+    _accurate(got, ref)
+    assert _rel(got, ogot) < 1e-9          # same ciphertexts; the two decoders agree to ~1e-16
 
 
 @pytest.mark.slow
@@ -126,7 +164,7 @@ def test_driver_lenet_large_chw():
     with the oracle (the CHW lowering itself is bit-exact on MINI_CHW above)."""
     name = "lenet_large_chw"
     got, _o, ref = _run_pair(SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0), oracle_layers=2)
-    assert np.abs(got - ref).max() <= 1e-3, np.abs(got - ref).max()
+    _accurate(got, ref)
 
 
 def test_driver_lenet_small_fc_r1():
@@ -136,5 +174,5 @@ def test_driver_lenet_small_fc_r1():
     net = copy.deepcopy(SN.NETS["lenet_small"])
     net["layers"][2] = ("fc", 100)
     got, ogot, ref = _run_pair(net, SN.net_weights("lenet_small"), SN.net_image("lenet_small", 4))
-    assert np.abs(got - ref).max() <= 1e-3
-    assert np.abs(got - ogot).max() < 1e-9
+    _accurate(got, ref)
+    assert _rel(got, ogot) < 1e-9          # same ciphertexts; the two decoders agree to ~1e-16

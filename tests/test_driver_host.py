@@ -36,10 +36,11 @@ def _mini_rep_weights():
 
 
 # SqueezeNet-shaped (config 5 layer kinds): padded 3x3 conv, pools, two fire modules (squeeze,
-# mask, fused 1x1 || 3x3 SAME expand), final 1x1 conv, global average pool
+# mask, fused 1x1 || 3x3 SAME expand), final 1x1 conv, global average pool; compile-time gains
 MINI_SQ = dict(log_n=11, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(3, 8, 8),
                layers=[("conv", 4, 3, 1, 1), ("act",), ("avgpool",), ("fire", 2, 2, 2), ("avgpool",),
-                       ("fire", 2, 3, 1), ("conv", 3, 1, 1, 0), ("gap",)], sigma=[0.5] * 8)
+                       ("fire", 2, 3, 1), ("conv", 3, 1, 1, 0), ("gap",)], sigma=[0.5] * 8,
+               act_gains=[4.0, 16.0, 64.0, 4.0 ** 4, 4.0 ** 4])     # A41 gains on every fire path
 
 
 def _mini_sq_weights():
@@ -114,24 +115,67 @@ def test_plan_lenet_small_levels():
 
 
 def test_fold_identity():
-    """A25: a2 x^2 + a1 x + a0 == (r x + beta)^2 + gamma (the folded form, one level)."""
+    """A25 (+ A41 gain G): G (a2 x^2 + a1 x + a0) == (r x + beta)^2 + gamma (one level)."""
     from paper_1810_00845_b200.driver import act_fold
     x = np.linspace(-3, 3, 101)
     for coeffs in (SN.ACT_COEFFS, (0.1, -0.7, 2.0), (1.0, 0.0, 0.5)):
-        r, beta, gamma = act_fold(coeffs)
-        a0, a1, a2 = coeffs
-        assert np.allclose((r * x + beta) ** 2 + gamma, a0 + a1 * x + a2 * x * x, atol=1e-12)
+        for G in (1.0, 4.0, 4.0 ** 7):
+            r, beta, gamma = act_fold(coeffs, G)
+            a0, a1, a2 = coeffs
+            assert np.allclose((r * x + beta) ** 2 + gamma, G * (a0 + a1 * x + a2 * x * x), rtol=1e-12, atol=1e-12 * G)
 
 
 def test_compile_weights_pool_and_act_factors():
     from paper_1810_00845_b200.driver import compile_weights
     w = _mini_weights()
-    folded, gamma = compile_weights(MINI, w, SN.ACT_COEFFS)
+    folded, gammas, gains = compile_weights(MINI, w, SN.ACT_COEFFS)
     r = math.sqrt(SN.ACT_COEFFS[2])
     assert np.allclose(folded[0][0], w[0] * r) and folded[0][1] == pytest.approx(0.5)   # act after
     assert np.allclose(folded[1][0], w[1] * 0.25 * r)                                    # pool before
     assert np.allclose(folded[3][0], w[3]) and folded[3][1] == 0.0                       # last layer
-    assert gamma == pytest.approx(-0.25)
+    assert gammas == [pytest.approx(-0.25)] * 3
+    assert [g for g, _o in gains] == [r, 1.0, 4.0, r, 1.0, r, 1.0, 1.0]      # the pool holds 4 x its mean
+
+
+def test_compile_weights_gains():
+    """A41: with activation gains G_n every encrypted tensor holds G x its value: the linear layer
+    before activation n is scaled by sqrt(a2 G_n) / G_(n-1), its bias is sqrt(a2 G_n) a1 / (2 a2),
+    gamma_n = G_n gamma; other linear layers keep the gain (the output is decoded / G_last)."""
+    import copy
+    from paper_1810_00845_b200.driver import compile_weights
+    net = copy.deepcopy(MINI)
+    net["act_gains"] = [16.0, 4.0 ** 5, 4.0]
+    w = _mini_weights()
+    folded, gammas, gains = compile_weights(net, w, SN.ACT_COEFFS)
+    a0, a1, a2 = SN.ACT_COEFFS
+    assert np.array_equal(folded[0][0], w[0] * math.sqrt(a2 * 16))
+    assert np.array_equal(folded[1][0], w[1] * 0.25 * math.sqrt(a2 * 4 ** 5) / 16)
+    assert np.array_equal(folded[2][0], w[2] * math.sqrt(a2 * 4) / 4 ** 5)
+    assert np.array_equal(folded[3][0], w[3])
+    assert folded[1][1] == math.sqrt(a2 * 4 ** 5) * a1 / (2 * a2)
+    assert gammas == [16 * -0.25, 4 ** 5 * -0.25, 4 * -0.25]
+    r1, r2, r3 = (math.sqrt(a2 * G) for G in (16, 4 ** 5, 4))
+    assert gains == [(r1, r1), (16.0, 0.0), (64.0, 0.0), (r2, r2), (4.0 ** 5, 0.0), (r3, r3), (4.0, 0.0),
+                     (4.0, 0.0)]           # (gain, offset) of each layer's output; beta = r here
+    with pytest.raises(ValueError):
+        net["act_gains"] = [2.0, 4.0, 4.0]          # not a power of 4
+        compile_weights(net, w, SN.ACT_COEFFS)
+
+
+def test_act_gains_follow_calibration_rule():
+    """The stored act_gains (synth/nets.py) are what tools/calibrate_gains.py's rule gives
+    (floor(log4(16 / max|act|)) on the float64 network, calibration image seed 1007), and every
+    gained activation output peaks in (4, 16] (bounds |x'^2| = G/4 . (...) well inside the
+    modulus, A41)."""
+    from tools import calibrate_gains as CG
+    for name in ("lenet_small", "lenet_large", "lenet_large_chw", "squeezenet"):
+        net = SN.NETS[name]
+        img = SN._image(CG.CALIB_SEED, net["input"])
+        base = "lenet_large" if name == "lenet_large_chw" else name
+        W = SN.net_weights(base)
+        assert CG.gains_for(net, W, img) == net["act_gains"], name
+        for g, m in zip(net["act_gains"], CG.act_maxima(net, W, img, SN.ACT_COEFFS)):
+            assert 4.0 < g * m <= 16.0 or g == 1.0
 
 
 def test_oracle_net_tiny_matches_float64():
@@ -388,3 +432,40 @@ def test_plain_reference_ops_match_torch():
     y = F.avg_pool2d(y, 2).reshape(-1)
     want = F.linear(y, torch.from_numpy(W[1])).numpy()
     assert np.allclose(plain.forward(net, img, W, SN.ACT_COEFFS), want, atol=1e-12)
+
+
+@pytest.mark.slow
+def test_oracle_squeezenet_shape_relative_error_n4096():
+    """Config 5's network (A33 shapes, its N(0, 0.05) weights, its act_gains) on the oracle at
+    N = 2^12 (24 x 40-bit limbs; the 32 x 32 planes fit 2048 slots): decrypted logits within
+    1e-4 RELATIVE to the float64 network (max |ref| ~ 3e-7, so an absolute bound alone would
+    pass an all-zero output).  Measured: 1.4e-7 with the gains, 0.16 without them (same N, same
+    image) -- the CKKS error floor is what the gains (A41) keep the signal above."""
+    import copy
+    from oracle import plain
+    from oracle.nets import OracleNet
+    net = copy.deepcopy(SN.NETS["squeezenet"])
+    net["log_n"] = 12
+    W, img = SN.net_weights("squeezenet"), SN.net_image("squeezenet", 0)
+    ref = plain.forward(net, img, W, SN.ACT_COEFFS)
+    on = OracleNet(net, W, SN.ACT_COEFFS)
+    cts, lay = on.encrypt_image(img)
+    out, ol = on.forward(cts, lay)
+    got = on.decrypt_output(out, ol)
+    rel = np.abs(got - ref).max() / np.abs(ref).max()
+    assert rel <= 1e-4, rel
+    assert np.abs(got - ref).max() <= 1e-3
+
+
+def test_golden_plain_outputs_are_the_float64_network():
+    """tests/golden/plain_outputs.json (bench.py's accuracy reference) = oracle/plain.py on the
+    stated weights and images (spot check: first and last image of two nets)."""
+    import json
+    from oracle import plain
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "plain_outputs.json")))
+    assert gold["images"] == 20
+    for name in ("tiny", "lenet_small"):
+        W = SN.net_weights(name)
+        for s in (0, 19):
+            ref = plain.forward(SN.NETS[name], SN.net_image(name, s), W, SN.ACT_COEFFS).ravel()
+            assert np.array_equal(np.asarray(gold["outputs"][name][s]), ref)

@@ -120,6 +120,39 @@ def test_gpu_encode_exact_ties():
     g.close()
 
 
+def test_gpu_encode_near_ties_match_exact_real_rounding():
+    """A7 near ties on the GPU encoder (double-double FFT + host binary128 recomputation inside
+    its tie window): sparse slot vectors at N = 2^8 tuned through z_0 so that chosen
+    coefficients lie 2^-14 .. 2^-34 above / below half-integers of both signs; every coefficient
+    equals round-half-away of the exact real v_t (Decimal, tests/bigint_defs.py) and the oracle's."""
+    from decimal import Decimal, localcontext
+    from tests import bigint_defs as D
+    g, o = _pair(8, [60], 60, [])
+    N, s = g.N, g.slots
+    rng = np.random.default_rng(17)
+    pi = D.dec_pi()
+    q0 = o.q[0]
+    for case, (t, K, delta) in enumerate([(1, 1000, 2.0 ** -14), (3, -2000, -2.0 ** -20), (9, 777777, 2.0 ** -30),
+                                          (2, -31, 2.0 ** -34), (77, 123456, -2.0 ** -26)]):
+        z = np.zeros(s)
+        nz = rng.choice(np.arange(1, s), 6, replace=False)
+        z[nz] = rng.uniform(-1, 1, 6)
+        scale = 2.0 ** 20
+        with localcontext() as ctx:
+            ctx.prec = 90
+            rest = D.encode_values_exact(np.r_[0.0, z[1:]], scale, N)[t]
+            coef = Decimal(float(scale)) / N * 2 * D.dec_cos(pi * t / N)
+            target = Decimal(K) + (Decimal("0.5") if K >= 0 else Decimal("-0.5")) + Decimal(delta)
+            z[0] = float((target - rest) / coef)
+        want = [D.round_half_away(x) for x in D.encode_values_exact(z, scale, N)]
+        pt = g.encode(z, scale)
+        coeffs = o.intt(g.pt_export(pt)[0:1].copy(), 0)[0]
+        got = [int(c) if c <= q0 // 2 else int(c) - q0 for c in coeffs]
+        assert got == want, case
+        assert (g.pt_export(pt) == o.encode(z, scale).data).all(), case
+    g.close()
+
+
 _ENGINE_SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, %r)
