@@ -347,9 +347,11 @@ def measure_inference(name, device, images=20, rot_policy="exact"):
             "kernel_share": {n: round(v[0] / total, 4) for n, v in top}}
 
 
-def measure_inference_sharded(name, local, dist, reps=2):
-    """Encrypted inference over all ranks: every linear layer's input channels sharded,
-    one reduce-scatter per linear layer, final all-gather; latency = max over ranks (CUDA events)."""
+def measure_inference_sharded(name, local, dist, reps=2, partition="ic"):
+    """Encrypted inference over all ranks, latency = max over ranks (CUDA events).
+    partition "ic": every conv's input channels sharded, one int64 reduce-scatter per conv;
+    "oc" (the north star's split, the baseline): each conv's inputs all-gathered, output channels
+    partitioned.  FC layers: inputs all-gathered, neurons / R-groups partitioned; final all-gather."""
     import torch
     from synth import nets as SN
     from paper_1810_00845_b200 import hisa as H
@@ -360,7 +362,7 @@ def measure_inference_sharded(name, local, dist, reps=2):
     ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=local, arena_bytes=arena)
     plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli)
     ctx.keygen(plan["rotations"], True)
-    en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS, group=dist.group.WORLD)
+    en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS, group=dist.group.WORLD, partition=partition)
     stream = torch.cuda.current_stream(local)
     lat = []
     for r in range(reps + 1):                    # first pass encodes the weight plaintexts
@@ -382,9 +384,11 @@ def measure_inference_sharded(name, local, dist, reps=2):
     ctx.close()
     ctx = None
     torch.cuda.empty_cache()
-    return {"config": name, "latency_s": min(lat), "unit": "s", "n_gpus": dist.get_world_size(), "reps": reps,
-            "sharding": "input channels of every linear layer; NCCL reduce-scatter of int64 partial sums per "
-                        "layer; final all-gather (SURVEY 8e)"}
+    return {"config": name, "partition": partition, "latency_s": min(lat), "unit": "s",
+            "n_gpus": dist.get_world_size(), "reps": reps,
+            "sharding": ("convs: input channels sharded, NCCL reduce-scatter of int64 partial sums" if partition == "ic"
+                         else "convs: inputs all-gathered, output channels partitioned (north-star baseline)") +
+                        "; FCs: inputs all-gathered, neurons / R-groups partitioned; final all-gather (SURVEY 8e)"}
 
 
 def _allreduce_max(t):
@@ -502,6 +506,9 @@ def main():
         import datetime
         # bounded collectives: a failing sharded-inference run must not hang the whole bench
         backend = os.environ.get("HISA_BENCH_BACKEND", "nccl")   # gloo: one-GPU emulation (tests only)
+        # communicator setup (rings / trees / NVLS) logged to stderr for the scaling runs
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group(backend, device_id=torch.device(f"cuda:{local}") if backend == "nccl" else None,
                                 timeout=datetime.timedelta(seconds=300))
     B, L, log_n = a.batch, a.limbs, a.log_n
@@ -684,10 +691,11 @@ def main():
     if world > 1 and not a.no_inference:
         sharded = []
         for nm in [n for n in a.nets.split(",") if n]:
-            try:
-                sharded.append(measure_inference_sharded(nm, local, dist))
-            except Exception as exc:   # the rotation line must survive a failing network run
-                sharded.append({"config": nm, "error": f"{type(exc).__name__}: {exc}"[:300]})
+            for part in ("ic", "oc"):
+                try:
+                    sharded.append(measure_inference_sharded(nm, local, dist, partition=part))
+                except Exception as exc:   # the rotation line must survive a failing network run
+                    sharded.append({"config": nm, "partition": part, "error": f"{type(exc).__name__}: {exc}"[:300]})
     if rank == 0:
         if sharded is not None:
             line["inference"] = sharded

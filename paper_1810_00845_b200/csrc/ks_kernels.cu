@@ -205,6 +205,41 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     const double q = qd.x, qinv = qd.y;
     const double tq52 = __dadd_rn(2.0 * q, 4503599627370496.0);   // 2q + 2^52
     double* tws5 = reinterpret_cast<double*>(sm + 4 * K5_TILE);
+    // Prefetch stages (cp.async, each thread copies exactly the words it later reads, so no
+    // barrier is needed -- only its own cp.async.wait_group): stT1 = the next step's pass-1 rows
+    // (elements t + 64 e), stK = the current step's key words (b and a, elements 4t .. 4t + 3).
+    // Round 1's K4 waited on both loads in every step (ncu: long-scoreboard 2.5 warps / issue).
+    double* stT1 = tws5 + 256;                                         // [2][256]
+    uint64_t* stK = reinterpret_cast<uint64_t*>(stT1 + 512);         // [2 digits][b, a][256]
+    const int n_nd = l1 - 1;                                  // fp rows: ri < l1
+    auto digit = [&](int idx) { return idx < ri ? idx : idx + 1; };
+    auto issue_t1 = [&](int idx) {      // rows of the step starting at non-diagonal index idx
+        const int nd = idx + 1 < n_nd ? 2 : 1;
+        for (int n = 0; n < nd; n++) {
+            const uint64_t* src = tile_src(digit(idx + n)) + t;
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const unsigned sa_ = (unsigned)__cvta_generic_to_shared(stT1 + n * 256 + t + 64 * e);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa_), "l"(src + 64 * e) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto issue_keys = [&](int ja, int jb, int nd) {
+        for (int n = 0; n < nd; n++) {
+            const uint64_t* kb = key_r + (n == 0 ? ja : jb) * kstride_j + 4 * t;
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+#pragma unroll
+                for (int c = 0; c < 2; c++) {
+                    const unsigned sa_ = (unsigned)__cvta_generic_to_shared(stK + (2 * n + h) * 256 + 4 * t + 2 * c);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa_),
+                                 "l"(kb + h * kstride_p + 2 * c) : "memory");
+                }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    if (n_nd > 0) issue_t1(0);
     {
         const double* twg = tb.fwd_d + ((long long)mi << log_n);
         const int s0 = log_n - LOG_M;
@@ -254,14 +289,17 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
         A2[h][e] += (uint64_t)dh * kh;
     };
     // ND digits (1 or 2) through the four phases, then MAC from registers
-    auto run = [&](auto nd_c, int ja, int jb) {
+    auto run = [&](auto nd_c, int ja, int jb, int next_idx) {
         constexpr int ND = decltype(nd_c)::value;
         double r[ND][4];
-        const uint64_t* src[2] = {tile_src(ja), tile_src(jb)};
+        issue_keys(ja, jb, ND);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");      // this step's rows (not its keys)
 #pragma unroll
         for (int n = 0; n < ND; n++)
 #pragma unroll
-            for (int e = 0; e < 4; e++) r[n][e] = __longlong_as_double((long long)__ldcs(src[n] + t + 64 * e));
+            for (int e = 0; e < 4; e++) r[n][e] = stT1[n * 256 + t + 64 * e];
+        const bool more = next_idx < n_nd;
+        if (more) issue_t1(next_idx);
 #pragma unroll
         for (int ph = 0; ph < 4; ph++) {
             const int u0 = 2 * ph;
@@ -310,14 +348,14 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
                 __syncthreads();
             }
         }
-        // phase 3 left elements 4t + e in registers
+        // phase 3 left elements 4t + e in registers; the keys wait in stK
+        if (more) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 #pragma unroll
         for (int n = 0; n < ND; n++) {
-            const uint64_t* kb = key_r + (n == 0 ? ja : jb) * kstride_j + 4 * t;
-            const ulonglong2 b0 = __ldg(reinterpret_cast<const ulonglong2*>(kb));
-            const ulonglong2 b1 = __ldg(reinterpret_cast<const ulonglong2*>(kb) + 1);
-            const ulonglong2 a0 = __ldg(reinterpret_cast<const ulonglong2*>(kb + kstride_p));
-            const ulonglong2 a1 = __ldg(reinterpret_cast<const ulonglong2*>(kb + kstride_p) + 1);
+            const ulonglong2* kb = reinterpret_cast<const ulonglong2*>(stK + (2 * n) * 256 + 4 * t);
+            const ulonglong2* ka = reinterpret_cast<const ulonglong2*>(stK + (2 * n + 1) * 256 + 4 * t);
+            const ulonglong2 b0 = kb[0], b1 = kb[1], a0 = ka[0], a1 = ka[1];
             const uint64_t kbv[4] = {b0.x, b0.y, b1.x, b1.y}, kav[4] = {a0.x, a0.y, a1.x, a1.y};
 #pragma unroll
             for (int e = 0; e < 4; e++) {
@@ -327,11 +365,9 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
             }
         }
     };
-    const int n_nd = l1 - 1;                                  // fp rows: ri < l1
-    auto digit = [&](int idx) { return idx < ri ? idx : idx + 1; };
     int idx = 0;
-    for (; idx + 1 < n_nd; idx += 2) run(std::integral_constant<int, 2>(), digit(idx), digit(idx + 1));
-    if (idx < n_nd) run(std::integral_constant<int, 1>(), digit(idx), digit(idx));
+    for (; idx + 1 < n_nd; idx += 2) run(std::integral_constant<int, 2>(), digit(idx), digit(idx + 1), idx + 2);
+    if (idx < n_nd) run(std::integral_constant<int, 1>(), digit(idx), digit(idx), idx + 1);
     {   // the diagonal digit: d_ri, already in the NTT domain (canonical < q), elements 4t + e
         const uint64_t* src = tile_src(ri) + 4 * t;
         const ulonglong2 d0 = __ldg(reinterpret_cast<const ulonglong2*>(src));
@@ -366,7 +402,8 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
 template <int MINB>
 static cudaError_t ks_ip5_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
     const int rows = 1 << (tb.log_n - 8);
-    const size_t smem = (4 * (size_t)K5_TILE + 256) * sizeof(uint64_t);   // 4 exchange tiles + twiddles
+    // 4 exchange tiles + twiddles + row prefetch [2][256] + key stage [2][2][256]: 24 KB
+    const size_t smem = (4 * (size_t)K5_TILE + 256 + 512 + 1024) * sizeof(uint64_t);
     dim3 grid(rows * nz, job.l1 + 1, 1);
     k_ks_ip5<MINB><<<grid, 64, smem, st>>>(job, tb);
     return cudaGetLastError();

@@ -271,12 +271,21 @@ class EncryptedNet:
     `group` (torch.distributed process group, optional) shards every linear layer's input
     channels across ranks; None = single GPU."""
 
-    def __init__(self, backend, net: dict, weights, act_coeffs, group=None, rot_policy: str = "exact"):
+    def __init__(self, backend, net: dict, weights, act_coeffs, group=None, rot_policy: str = "exact",
+                 partition: str = "ic"):
         """rot_policy: "exact" = one key per distinct rotation amount, chosen by the compiler
         (CHET); "pow2" = HEAAN's default power-of-two keys (left and right),
-        every other amount composed from them (the baseline of the paper's Fig. rotopt)."""
+        every other amount composed from them (the baseline of the paper's Fig. rotopt).
+        partition (multi-GPU convs): "ic" = input channels sharded, partial sums for
+        all outputs reduce-scattered (each hoisted rotation computed once); "oc" = the north
+        star's output-channel partition: the layer's inputs all-gathered, every rank rotates all
+        of them and accumulates its own output channels (the measured baseline).  FC layers
+        always follow 8e's plan: inputs all-gathered, output neurons / R-groups partitioned."""
         if rot_policy not in ("exact", "pow2"):
             raise ValueError(rot_policy)
+        if partition not in ("ic", "oc"):
+            raise ValueError(partition)
+        self.partition = partition
         self.rot_policy = rot_policy
         self.b = backend
         self.net = net
@@ -524,6 +533,12 @@ class EncryptedNet:
             masked = True
         else:
             masked = False
+        oc_part = self.world > 1 and self.partition == "oc"
+        if oc_part:                               # north-star baseline: every rank holds all inputs
+            gathered = self._gather(cts, lay.C)
+            if masked:
+                self._free_all(cts)
+            cts, own_in, masked = gathered, range(lay.C), True
         amounts = [(lay.origin + (i - p) * lay.hS + (j - p) * lay.wS) % self.slots
                    for i in range(k) for j in range(k)]
         nz = [a for a in amounts if a]
@@ -540,7 +555,11 @@ class EncryptedNet:
                     temps.append(h)
             wcols.append(w[:, ci].reshape(oc_n, k * k))
         wmat = np.concatenate(wcols, axis=1) if wcols else np.zeros((oc_n, 0))
-        outs = self._accumulate(rotated, wmat, oc_n)
+        if oc_part:
+            own_out = self.owned(oc_n)
+            outs = self._accumulate_local(rotated, wmat[own_out.start:own_out.stop])
+        else:
+            outs = self._accumulate(rotated, wmat, oc_n)
         self._free_all(temps)
         if masked:
             self._free_all(cts)
@@ -550,6 +569,20 @@ class EncryptedNet:
         nl = Layout("hw", oc_n, (lay.H + 2 * p - k) // st + 1, (lay.W + 2 * p - k) // st + 1,
                     lay.hS * st, lay.wS * st, 0, False)
         return res, nl
+
+    def _gather(self, cts, n: int):
+        """All n channels of a sharded layer on every rank (NCCL all-gather); fresh
+        handles (the caller frees them).  Single GPU: copies."""
+        if self.world == 1:
+            return [self.b.copy(h) for h in cts]
+        from . import parallel
+        return parallel.gather_outputs(self, cts, n)
+
+    def _accumulate_local(self, rotated, wmat):
+        """sum_t W[o, t] rotated[t] for the rows of wmat, on this rank alone (no exchange)."""
+        if wmat.shape[0] == 0 or not rotated:
+            return []
+        return self.b.conv_accumulate(rotated, np.ascontiguousarray(wmat).ravel())
 
     def _accumulate(self, rotated, wmat, n_out):
         """sum_t W[o, t] rotated[t] for o < n_out (pre-rescale).  Single GPU: one fused kernel.
@@ -636,45 +669,52 @@ class EncryptedNet:
             res, first = nxt, False
         return res
 
-    def _mulplain_sums(self, cts, n_in, n_rows, key, li, vals_fn):
-        """acc_j = sum_c mulPlain(cts[c], P_{j,c}) for j < n_rows over this rank's channels of
-        the n_in inputs (None where the rank owns none); P built by vals_fn(j, global c).
-        Multi-GPU: reduce-scattered, so the result is this rank's owned rows."""
-        own_in = self.owned(n_in)
-        lv = self._level(cts[0]) if cts else None
-        if cts:   # one fused mulPlain-accumulate launch over all rows (hisa_mul_plain_accumulate)
-            keys = [((key, li, jo, ci), lv) for jo in range(n_rows) for ci in own_in]
-            missing = [(k, jo, ci) for k, (jo, ci) in zip(keys, [(jo, ci) for jo in range(n_rows) for ci in own_in])
-                       if k not in self._pts]
-            if missing:   # the layer's weight plaintexts, encoded once per model in one batch
-                hs = self.b.encode_batch(np.stack([vals_fn(jo, ci) for _k, jo, ci in missing]),
-                                         float(self.q[lv]), lv)
-                for (k, _jo, _ci), h in zip(missing, hs):
-                    self._pts[k] = h
-            pts = [self._pts[k] for k in keys]
-            sums = self.b.mul_plain_accumulate(list(cts), pts, n_rows)
-        else:
-            sums = [None] * n_rows
-        if self.world > 1:
-            from . import parallel
-            return parallel.reduce_scatter_cts(self, sums, n_rows)
-        return sums
+    def _mulplain_sums(self, cts, rows, key, li, vals_fn):
+        """acc_j = sum_c mulPlain(cts[c], P_{j,c}) for j in `rows` over ALL input channels c
+        (cts = every input, gathered on every rank under a process group); P built by
+        vals_fn(j, c).  One fused mulPlain-accumulate launch (hisa_mul_plain_accumulate)."""
+        if not cts or len(rows) == 0:
+            return []
+        lv = self._level(cts[0])
+        n_in = len(cts)
+        keys = [((key, li, jo, ci), lv) for jo in rows for ci in range(n_in)]
+        missing = [(k, jo, ci) for k, (jo, ci) in zip(keys, [(jo, ci) for jo in rows for ci in range(n_in)])
+                   if k not in self._pts]
+        if missing:   # the layer's weight plaintexts, encoded once per model in one batch
+            hs = self.b.encode_batch(np.stack([vals_fn(jo, ci) for _k, jo, ci in missing]), float(self.q[lv]), lv)
+            for (k, _jo, _ci), h in zip(missing, hs):
+                self._pts[k] = h
+        pts = [self._pts[k] for k in keys]
+        return self.b.mul_plain_accumulate(list(cts), pts, len(rows))
+
+    def _fc_inputs(self, cts, n: int):
+        """SURVEY 8e FC plan: the FC's inputs all-gathered to every rank (returns (all inputs,
+        temporaries to free)); single GPU: the inputs themselves."""
+        if self.world == 1:
+            return list(cts), []
+        allc = self._gather(cts, n)
+        return allc, allc
 
     def fc_replicated(self, cts, lay, layer, w, beta, li):
         """FC with R replicas per ciphertext ("replicas ... added in log number of
         rotations", A27): mask, replicate R times at block stride Bk (log2 R rotations), one
         mulPlain per (group of R neurons, input channel), rescale, rotate-and-sum inside each
-        block; neuron g R + r ends in slot r Bk of ciphertext g."""
+        block; neuron g R + r ends in slot r Bk of ciphertext g.  Multi-GPU (8e): inputs
+        all-gathered, the R-groups partitioned."""
         n_out, R = layer[1], layer[2]
-        if not lay.clean:
-            cts, lay = self.mask(cts, lay, li)
-            masked = True
+        masked = []
+        if not lay.clean:                          # each rank masks its own channels, then gathers
+            masked, lay = self.mask(cts, lay, li)
+            cts = masked
+        cts, temp_in = self._fc_inputs(cts, lay.C)
+        if temp_in:
+            self._free_all(masked)
         else:
-            masked = False
+            temp_in = masked
         Bk = 1 << math.ceil(math.log2(lay.span()))
         if R * Bk > self.slots or R & (R - 1):
             raise ValueError(f"replicas R={R} x block {Bk} exceed {self.slots} slots")
-        reps, temp = list(cts), masked
+        reps, temp = list(cts), bool(temp_in)
         for t in range(int(math.log2(R))):           # copies at r * Bk (right rotations, P:759)
             rs = [r[0] for r in self._rot_many(reps, [self.slots - (Bk << t)])]
             nxt = [self.b.add(x, r) for x, r in zip(reps, rs)]
@@ -691,7 +731,7 @@ class EncryptedNet:
                 if j < n_out:
                     v[r * Bk + idx] = w[j, c * hw:(c + 1) * hw]
             return v
-        sums = self._mulplain_sums(reps, lay.C, n_groups, "fcrep", li, vals)
+        sums = self._mulplain_sums(reps, self.owned(n_groups), "fcrep", li, vals)
         if temp:
             self._free_all(reps)
         res = self.b.rescale_batch(sums)
@@ -702,9 +742,11 @@ class EncryptedNet:
     def fc_from_rep(self, cts, lay, layer, w, beta, li):
         """FC whose input holds R values per ciphertext at slots r * Bk: one mulPlain per
         (output, input ciphertext) with the weights at those slots, rescale, rotate-and-sum
-        across the R blocks (log2 R rotations) into slot 0."""
+        across the R blocks (log2 R rotations) into slot 0.  Multi-GPU: inputs all-gathered,
+        outputs partitioned (8e)."""
         n_out = layer[1]
         R, Bk = lay.H, lay.hS
+        cts, temp_in = self._fc_inputs(cts, lay.C)
 
         def vals(k, g):
             v = np.zeros(self.slots)
@@ -713,7 +755,8 @@ class EncryptedNet:
                 if j < lay.count:
                     v[r * Bk] = w[k, j]
             return v
-        sums = self._mulplain_sums(cts, lay.C, n_out, "fcfromrep", li, vals)
+        sums = self._mulplain_sums(cts, self.owned(n_out), "fcfromrep", li, vals)
+        self._free_all(temp_in)
         res = self.b.rescale_batch(sums)
         self._free_all(sums)
         res = self._rotate_sum(res, [Bk << t for t in range(int(math.log2(R)))])
@@ -721,15 +764,18 @@ class EncryptedNet:
 
     def fc(self, cts, lay, layer, w, beta, li):
         """Matmul (A27): R = 1 (below), replicas (fc_replicated), or an input in
-        replica layout (fc_from_rep)."""
+        replica layout (fc_from_rep).  Multi-GPU: the inputs are all-gathered and
+        the output neurons partitioned across ranks -- no partial-sum exchange."""
         if lay.kind == "rep":
             return self.fc_from_rep(cts, lay, layer, w, beta, li)
         if lay.kind == "hw" and len(layer) > 2 and layer[2] > 1:
             return self.fc_replicated(cts, lay, layer, w, beta, li)
         n_out = layer[1]
+        own_out = self.owned(n_out)
+        allc, temp_in = self._fc_inputs(cts, lay.C)
         if lay.kind == "slot0":          # next FC reads slot 0: scalar MACs, fused
-            own = self.owned(lay.C)
-            outs = self._accumulate(list(cts), w[:, own.start:own.stop], n_out)
+            outs = self._accumulate_local(allc, w[own_out.start:own_out.stop, :])
+            self._free_all(temp_in)
             res = self.b.rescale_batch(outs)
             self._free_all(outs)
             return self._bias(res, beta), Layout("slot0", n_out)
@@ -741,7 +787,8 @@ class EncryptedNet:
             v = np.zeros(self.slots)
             v[idx] = w[jo, ci * hw:(ci + 1) * hw]
             return v
-        sums = self._mulplain_sums(cts, lay.C, n_out, "fc", li, vals)
+        sums = self._mulplain_sums(allc, own_out, "fc", li, vals)
+        self._free_all(temp_in)
         res = self.b.rescale_batch(sums)
         self._free_all(sums)
         res = self._rotate_sum(res, [1 << t for t in range(steps)])   # slot 0 <- dot product

@@ -1,9 +1,10 @@
 """Multi-GPU exchange of the encrypted CNN driver.
 
-One process per GPU (torch.distributed, NCCL over NVLink / NVSwitch).  Every linear layer's
-input channels are partitioned across ranks (EncryptedNet.owned): rank r hoists the rotations
-of ITS input channels only, and accumulates partial sums for ALL outputs.  The only exchange is
-one reduce-scatter per linear layer of those partials as int64 (SUM):
+One process per GPU (torch.distributed, NCCL over NVLink / NVSwitch).  Between layers every
+rank holds its own block of channels (EncryptedNet.owned).  Convolutions (partition "ic", the
+default): every conv's input channels are partitioned across ranks: rank r hoists the rotations
+of ITS input channels only, and accumulates partial sums for ALL outputs; the exchange is one
+reduce-scatter per conv of those partials as int64 (SUM):
 
   * exact -- each partial word is a fully reduced residue < q_i < 2^60 and world <= 8, so every
     sum is < 2^63; hisa_ct_adopt_sum reduces it back into [0, q_i) on the device;
@@ -11,6 +12,12 @@ one reduce-scatter per linear layer of those partials as int64 (SUM):
     shard of the next layer -- so no all-gather is needed between layers;
   * ModDown / rescale run only after the complete sum, so the outputs at 1 / 2 / 4 / 8 ranks
     are bit-identical to the single-GPU result (modular addition is order independent).
+
+Partition "oc" (the north star's output-channel split, kept as the measured baseline) and every
+FC layer (SURVEY 8e's FC plan): the layer's input channels are all-gathered (gather_outputs) and
+each rank computes its own output channels / neurons / R-groups from all of them -- no partial
+sums cross ranks, so the outputs are bit-identical by construction; the cost is that every rank
+repeats the inputs' rotations.
 
 The partial buffers are torch int64 tensors (PyTorch owns device memory); libhisa writes the
 partial sums into them directly (hisa_conv_accumulate_dev) or they are copied from ciphertext
@@ -26,6 +33,16 @@ class _DevArray:
 
     def __init__(self, ptr: int, n: int):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False), "version": 3}
+
+
+def _words(ptr: int, n: int, dev):
+    """n int64 words at `ptr` as a tensor on `dev` (zero-copy): a libhisa device view, or -- for a
+    host-memory backend (the CPU test double of tests/test_parallel_cpu.py) -- host memory."""
+    import torch
+    if dev.type == "cuda":
+        return torch.as_tensor(_DevArray(ptr, n), device=dev)
+    import ctypes
+    return torch.from_numpy(np.ctypeslib.as_array((ctypes.c_int64 * n).from_address(ptr)))
 
 
 def _host_staged(t, group) -> bool:
@@ -90,7 +107,7 @@ def layer_meta(en, handles, device):
 def _device(en):
     import torch
     from .driver import Symbolic
-    if isinstance(en.b, Symbolic):
+    if isinstance(en.b, Symbolic) or getattr(en.b, "host_memory", False):
         return torch.device("cpu")
     return torch.device("cuda", torch.cuda.current_device())
 
@@ -122,36 +139,6 @@ def reduce_scatter_partials(en, rotated, wmat: np.ndarray, n_out: int):
     return [en.b.ct_adopt_sum(blk[i].data_ptr(), lv, 2, sc_in * ps) for i in range(len(own))]
 
 
-def reduce_scatter_cts(en, sums, n_out: int):
-    """Ciphertext partial sums (mulPlain accumulations of the HW-input FC), one per output or
-    None where this rank owns no input channel -> reduce-scatter -> owned outputs."""
-    import torch
-    from .driver import Symbolic
-    dev = _device(en)
-    have = [h for h in sums if h is not None]
-    lv, sc = layer_meta(en, have, dev)
-    per = _per(en, n_out)
-    own = en.owned(n_out)
-    if isinstance(en.b, Symbolic):
-        for h in have:
-            en.b.free(h)
-        buf = torch.zeros((en.world * per, 1), dtype=torch.int64)
-        exchange(buf, per, en.group)
-        return [en.b.fresh(lv, sc) for _ in own]
-    N = 2 * en.slots
-    words = 2 * (lv + 1) * N
-    buf = torch.zeros((en.world * per, words), dtype=torch.int64, device=dev)
-    for j, h in enumerate(sums):
-        if h is None:
-            continue
-        ptr, w = en.b.ct_device_view(h)
-        assert w == words
-        buf[j].copy_(torch.as_tensor(_DevArray(ptr, w), device=dev))
-        en.b.free(h)
-    blk = exchange(buf, per, en.group)
-    return [en.b.ct_adopt_sum(blk[i].data_ptr(), lv, 2, sc) for i in range(len(own))]
-
-
 def gather_outputs(en, cts, n_out: int):
     """All-gather the final layer's owned outputs so every rank (rank 0 decrypts) holds all
     n_out ciphertexts (all-gather at the end)."""
@@ -171,7 +158,7 @@ def gather_outputs(en, cts, n_out: int):
     buf = torch.zeros((per, words), dtype=torch.int64, device=dev)
     for i, h in enumerate(cts):
         ptr, w = en.b.ct_device_view(h)
-        buf[i].copy_(torch.as_tensor(_DevArray(ptr, w), device=dev))
+        buf[i].copy_(_words(ptr, w, dev))
     allb = torch.empty((en.world * per, words), dtype=torch.int64, device=dev)
     _all_gather(allb, buf, en.group)
     return [en.b.ct_adopt_device(allb[j].data_ptr(), lv, 2, sc) for j in range(n_out)]

@@ -283,7 +283,7 @@ def test_plan_matches_oracle_rotation_selection():
     assert pl["levels_used"] == 8
 
 
-# ------------------------------------------------------------------------------ gloo, world 2
+# ------------------------------------------------------------------------------ gloo, world 2 / 4 / 8
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -308,29 +308,34 @@ def _worker(rank, world, port, q):
         parts = torch.from_numpy(rng.integers(0, qm, size=(world * per, 5), dtype=np.int64))
         res["parts"] = parts.numpy().copy()
         res["block"] = parallel.exchange(parts, per, None).numpy()
-        # (2) the sharded driver on the symbolic backend (metadata + real collectives)
+        # (2) the sharded driver on the symbolic backend (metadata + real collectives), both
+        # conv partitions
         net = SN.NETS["lenet_small"]
         from oracle.ckks import Oracle
         mod = Oracle(net["log_n"], net["q_bits"], net["p_bits"]).moduli
-        sym = Symbolic(net["log_n"], mod)
-        en = EncryptedNet(sym, net, SN.net_weights("lenet_small"), SN.ACT_COEFFS, group=dist.group.WORLD)
-        lay = input_layout(net)
-        cts = en.shard_input([sym.fresh(len(mod) - 2, net["scale"]) for _ in range(lay.C)])
-        out, ol = en.forward_gathered(cts, lay)
-        res["n_out"] = len(out)
-        res["final_level"] = sym.cts[out[0]][0]
-        res["counts"] = sym.counts
-        res["rotations"] = sorted(sym.rotations)
+        for part in ("ic", "oc"):
+            sym = Symbolic(net["log_n"], mod)
+            en = EncryptedNet(sym, net, SN.net_weights("lenet_small"), SN.ACT_COEFFS, group=dist.group.WORLD,
+                              partition=part)
+            lay = input_layout(net)
+            cts = en.shard_input([sym.fresh(len(mod) - 2, net["scale"]) for _ in range(lay.C)])
+            out, ol = en.forward_gathered(cts, lay)
+            res[part] = dict(n_out=len(out), final_level=sym.cts[out[0]][0], counts=sym.counts,
+                             rotations=sorted(sym.rotations))
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
 
 
-def test_multirank_gloo_world2():
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_multirank_gloo(world):
+    """Exchange numerics and the sharded plan at world 2 / 4 / 8 (lenet_small: 5 conv channels ->
+    uneven shards, idle ranks at world 8).  "ic": the (ic, tap) rotations and scalar MACs are
+    partitioned (they sum to the single-GPU counts); "oc": every rank repeats the conv's
+    rotations and owns its output channels.  FC layers (8e plan): mulPlains partitioned."""
     import torch.multiprocessing as mp
     from oracle.ckks import Oracle
     from paper_1810_00845_b200.driver import EncryptedNet
-    world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -342,26 +347,23 @@ def test_multirank_gloo_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     # exchange: rank r's block = rows [3r, 3r+3) summed over ranks (< 2^63, exact)
-    total = got[0]["parts"] + got[1]["parts"]
+    total = sum(got[r]["parts"] for r in range(world))
     for r in range(world):
         assert (got[r]["block"] == total[3 * r:3 * r + 3]).all()
-        assert ((got[r]["block"] % ((1 << 60) - 93)) >= 0).all()
-    # sharded symbolic run: same final level, all 10 outputs gathered on every rank, the
-    # (ic, tap) work partitioned (scalar MACs sum to the single-GPU count), keys needed only
-    # where the rank holds channels
     net = SN.NETS["lenet_small"]
     single = EncryptedNet.plan(net, SN.net_weights("lenet_small"), SN.ACT_COEFFS,
                                Oracle(net["log_n"], net["q_bits"], net["p_bits"]).moduli)
-    for r in range(world):
-        assert got[r]["n_out"] == 10
-        assert got[r]["final_level"] == single["final_level"]
-        assert set(got[r]["rotations"]) <= set(single["rotations"])
-    macs = sum(got[r]["counts"].get("scalar_mac_ct", 0) for r in range(world))
-    assert macs == single["counts"]["scalar_mac_ct"]
-    hoisted = sum(got[r]["counts"].get("rot_hoisted", 0) for r in range(world))
-    assert hoisted == single["counts"]["rot_hoisted"]
-    mulp = sum(got[r]["counts"].get("mul_plain", 0) for r in range(world))
-    assert mulp == single["counts"]["mul_plain"]
+    for part in ("ic", "oc"):
+        for r in range(world):
+            g = got[r][part]
+            assert g["n_out"] == 10 and g["final_level"] == single["final_level"]
+            assert set(g["rotations"]) <= set(single["rotations"])
+        total = {k: sum(got[r][part]["counts"].get(k, 0) for r in range(world))
+                 for k in ("scalar_mac_ct", "rot_hoisted", "mul_plain")}
+        assert total["scalar_mac_ct"] == single["counts"]["scalar_mac_ct"]
+        assert total["mul_plain"] == single["counts"]["mul_plain"]
+        want_h = single["counts"]["rot_hoisted"] * (world if part == "oc" else 1)
+        assert total["rot_hoisted"] == want_h
 
 
 def test_oracle_pow2_policy_matches_float64_and_planner():
