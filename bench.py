@@ -158,9 +158,9 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------ work model
 def kernel_units(name: str, log_n: int, l1: int, B: int) -> float:
-    """Algorithmic 64-bit modular multiplies per step for one kernel class:
-    an NTT pass over one limb = (N/2) * log2(M) butterflies (one Shoup modmul each); the key
-    inner product adds 2 multiply-accumulates per (digit, output prime, word)."""
+    """Algorithmic butterflies per step for one kernel class: an NTT pass over one
+    limb = (N/2) * log2(M) butterflies.  The key multiply-accumulates of the inner product run on
+    another pipe (IMAD) and are counted separately (kernel_macs)."""
     N = 1 << log_n
     m1 = log_n // 2
     m2 = log_n - m1
@@ -169,13 +169,21 @@ def kernel_units(name: str, log_n: int, l1: int, B: int) -> float:
         "ntt_inv_rows": l1 * hb * m2,
         "ntt_inv_cols": l1 * hb * m1,
         "ks_modup_cols": l1 * l1 * hb * m1,                       # (j, r != q_j) pairs, first log M1 stages
-        "ks_ip_rows": l1 * l1 * hb * m2 + 2 * l1 * (l1 + 1) * N,  # last log M2 stages + key MACs
+        "ks_ip_rows": l1 * l1 * hb * m2,                          # last log M2 stages
         "ks_intt_p_rows": 2 * hb * m2,
         "ks_intt_p_cols": 2 * hb * m1,
         "ks_moddown_cols": 2 * l1 * hb * m1,
         "ks_moddown_rows": 2 * l1 * hb * m2,
     }
     return float(per_ct.get(name, 0)) * B
+
+
+def kernel_macs(name: str, log_n: int, l1: int, B: int) -> float:
+    """Key multiply-accumulates per step: the inner product of K4 multiplies every digit j
+    (l1 of them) into the b and a key limbs of every output prime (l1 + 1) -> 2 l1 (l1+1) N."""
+    if name != "ks_ip_rows":
+        return 0.0
+    return float(2 * l1 * (l1 + 1) * (1 << log_n)) * B
 
 
 def rotation_alg_bytes(log_n: int, l1: int, B: int) -> float:
@@ -285,7 +293,7 @@ def measure_inference(name, device, images=20, rot_policy="exact"):
     ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=device, arena_bytes=64 << 30)
     t0 = time.perf_counter()
     plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli, rot_policy=rot_policy)
-    ctx.keygen(plan["rotations"], True)
+    EncryptedNet.keygen(ctx, plan)
     ctx.sync()
     t_keys = time.perf_counter() - t0
     en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS, rot_policy=rot_policy)
@@ -361,7 +369,7 @@ def measure_inference_sharded(name, local, dist, reps=2, partition="ic"):
     arena = int(float(os.environ.get("HISA_BENCH_ARENA_GB", "64")) * (1 << 30))
     ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, device=local, arena_bytes=arena)
     plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli)
-    ctx.keygen(plan["rotations"], True)
+    EncryptedNet.keygen(ctx, plan)
     en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS, group=dist.group.WORLD, partition=partition)
     stream = torch.cuda.current_stream(local)
     lat = []
@@ -571,8 +579,17 @@ def main():
     alg_bytes_step = rotation_alg_bytes(log_n, L, B)
     hbm_gbs = alg_bytes_step * a.steps / (ms / 1e3) / 1e9
     total_ms = sum(v[0] for v in prof.values()) or 1.0
+    peak_mac = ctx.microbench_mac(2000)
+    macs = kernel_macs(dom_name, log_n, L, B) * a.steps
+    mac_rate = macs / (dom_ms / 1e3) if dom_ms > 0 else 0.0
     roofline = {"bound": "alu", "kernel": dom_name, "achieved": achieved / 1e9, "peak": peak_bfly / 1e9,
-                "unit": "Gmodmul/s", "frac": achieved / peak_bfly if peak_bfly else None, "traffic": traffic,
+                "unit": "Gbutterfly/s", "frac": achieved / peak_bfly if peak_bfly else None, "traffic": traffic,
+                "counts": "butterflies only (FP64 pipe); the key MACs of the same kernel are in 'macs' against "
+                          "their own (IMAD-pipe) measured peak",
+                "macs": {"achieved": mac_rate / 1e9, "peak": peak_mac / 1e9, "unit": "GMAC/s",
+                         "frac": mac_rate / peak_mac if peak_mac and macs else None,
+                         "peak_source": "measured: hisa_microbench_mac (K4's split 64x64 MAC, 4 IMAD.WIDE.U32, "
+                                        "register-resident, all SMs)"},
                 "peak_source": "measured: hisa_microbench_butterfly_f64 (register-resident exact FP64 butterflies, "
                                "all SMs; the faster engine)", "peak_int_engine": peak_int / 1e9,
                 "peak_derived": {"fp64_engine": sm_count * 64 * sm_ghz / 9.5,
@@ -584,7 +601,7 @@ def main():
                                  "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak,
                                  "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
     kernels = {n: {"ms": v[0], "launches": v[1], "share": v[0] / total_ms,
-                   "gmodmul_s": kernel_units(n, log_n, L, B) * a.steps / (v[0] / 1e3) / 1e9 if v[0] else None}
+                   "gbutterfly_s": kernel_units(n, log_n, L, B) * a.steps / (v[0] / 1e3) / 1e9 if v[0] else None}
                for n, v in sorted(prof.items(), key=lambda kv: -kv[1][0])}
 
     # end-to-end through the C-ABI with pinned host buffers: every step copies its B input

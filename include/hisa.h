@@ -115,10 +115,17 @@ int hisa_mem_stats(const hisa_ctx* ctx, size_t* in_use, size_t* peak);
 /* ---- keys (outside the HISA) ---------------------------- */
 /* Generates (once) the secret key, public key and, if relin != 0, the relinearisation key, plus
  * one key-switching key per distinct left-rotation amount (k mod N/2, k != 0), as the compiler's
- * rotation-key selection would request.  May be called again to add rotation keys. */
-int hisa_keygen(hisa_ctx* ctx, const int64_t* rot_left_amounts, size_t n, int relin);
+ * rotation-key selection would request.  May be called again to add rotation keys.
+ * max_level (-1 = top, else 0 <= max_level < L): the rotation keys of this call are stored
+ * truncated to the highest level they serve (digits j <= max_level, moduli q_0..q_max_level and
+ * p: kL = max_level + 1 primes, [kL][2][kL+1][N] words -- the same words as the full key's
+ * blocks); a rotation at a level above its key's fails with HISA_E_NO_KEY.  Asking again for an
+ * existing amount at a higher max_level regenerates it; at a lower one keeps it.  The
+ * relinearisation key is always full.  HISA_E_PARAMS for max_level out of range. */
+int hisa_keygen(hisa_ctx* ctx, const int64_t* rot_left_amounts, size_t n, int relin, int max_level);
 /* which = -1 public key [2][L][N]; -2 secret key NTT [(L+1)][N]; 0 relin key; k>0 rotation key k
- * ([L][2][L+1][N], canonical NTT order); words must equal the object size. */
+ * ([kL][2][kL+1][N], kL = its max_level + 1, canonical NTT order); words must equal the object
+ * size. */
 int hisa_key_export(hisa_ctx* ctx, int64_t which, uint64_t* host, size_t words);
 
 /* ---- Encryption profile ------------------------------------------------------ */
@@ -260,6 +267,9 @@ int hisa_launch_count(hisa_ctx* ctx, uint64_t* n);
 int hisa_microbench_butterfly(hisa_ctx* ctx, int iters, double* bfly_per_s);
 /* the same with the exact FP64-pipe butterfly used for moduli < 2^50 (ntt_f64.cuh) */
 int hisa_microbench_butterfly_f64(hisa_ctx* ctx, int iters, double* bfly_per_s);
+/* the key multiply-accumulate of the key-switch inner product (K4: 64 x 64 -> three split 64-bit
+   sums, 4 IMAD.WIDE.U32 per MAC) on all SMs, in MACs per second: the denominator for the key MACs */
+int hisa_microbench_mac(hisa_ctx* ctx, int iters, double* mac_per_s);
 
 const char* hisa_last_error(void);
 

@@ -206,8 +206,11 @@ struct hisa_ctx {
     int64_t* d_s_int = nullptr;
     uint64_t* d_sk = nullptr;         // [(L+1)][N]
     uint64_t* d_pk = nullptr;         // [2][L][N]
-    uint64_t* d_rlk = nullptr;        // [L][2][L+1][N]
-    std::map<uint64_t, uint64_t*> rot_keys;
+    // key-switching keys, each truncated to the highest level it serves (SURVEY 7 hard part 3):
+    // kL = q primes covered (max level + 1), layout [kL digits][b, a][q_0..q_{kL-1}, p][N]
+    struct KeyRec { uint64_t* p = nullptr; int kL = 0; };
+    uint64_t* d_rlk = nullptr;        // [L][2][L+1][N] (relinearisation: always full)
+    std::map<uint64_t, KeyRec> rot_keys;
     uint64_t enc_counter = 0;
     // encode/decode long-double tables (built on first use): cis(2 pi k / N), k < N/2, and
     // cis(pi t / N), t < N
@@ -243,7 +246,10 @@ struct hisa_ctx {
     }
 };
 
-static size_t key_words(const hisa_ctx* c) { return (size_t)c->L * 2 * (c->L + 1) * c->N; }
+static size_t key_words(const hisa_ctx* c, int kL = -1) {
+    if (kL < 0) kL = c->L;
+    return (size_t)kL * 2 * (kL + 1) * c->N;
+}
 
 static void* dalloc(hisa_ctx* c, size_t bytes) {
     if (c->has_arena) return c->arena.alloc(bytes);
@@ -644,9 +650,11 @@ static int gen_ksk(hisa_ctx* c, uint64_t keyid, const uint64_t* sp, uint64_t** o
     return HISA_OK;
 }
 
-extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin) {
+extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin, int max_level) {
     CHECK_CTX(c);
     if (n && !rot) return fail(HISA_E_PARAMS, "null rotation list");
+    if (max_level < -1 || max_level >= c->L) return fail(HISA_E_PARAMS, "max_level %d outside [-1, %d]", max_level, c->L - 1);
+    const int kL = max_level < 0 ? c->L : max_level + 1;
     const int L = c->L, M = L + 1;
     const uint64_t N = c->N, slots = N / 2;
     uint8_t mm[MAXL];
@@ -687,7 +695,13 @@ extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin)
     for (size_t i = 0; i < n; i++) {
         int64_t k = rot[i] % (int64_t)slots;
         if (k < 0) k += (int64_t)slots;
-        if (k == 0 || c->rot_keys.count((uint64_t)k)) continue;
+        if (k == 0) continue;
+        auto have = c->rot_keys.find((uint64_t)k);
+        if (have != c->rot_keys.end()) {
+            if (have->second.kL >= kL) continue;
+            dfree(c, have->second.p);      // regenerate at the higher level (same words on the shared blocks)
+            c->rot_keys.erase(have);
+        }
         const uint64_t g = h_pow(5, (uint64_t)k, 2 * N);
         int64_t* sg = dalloc_t<int64_t>(c, N);
         uint64_t* sp = dalloc_t<uint64_t>(c, (size_t)M * N);
@@ -698,15 +712,29 @@ extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin)
         RET(ntt_fwd(c, pp, 1, M, mm));
         uint64_t* key = nullptr;
         RET(gen_ksk(c, (uint64_t)k, sp, &key));
+        if (kL < L) {   // truncate: digits j < kL, moduli q_0..q_{kL-1} and p (the same words)
+            uint64_t* tr = dalloc_t<uint64_t>(c, key_words(c, kL));
+            if (!tr) return fail(HISA_E_OOM, "key allocation (%zu MiB)", key_words(c, kL) * 8 >> 20);
+            for (int j = 0; j < kL; j++)
+                for (int h = 0; h < 2; h++) {
+                    const uint64_t* src = key + ((size_t)j * 2 + h) * M * N;
+                    uint64_t* dst = tr + ((size_t)j * 2 + h) * (kL + 1) * N;
+                    CK(cudaMemcpyAsync(dst, src, (size_t)kL * N * 8, cudaMemcpyDeviceToDevice, c->stream));
+                    CK(cudaMemcpyAsync(dst + (size_t)kL * N, src + (size_t)L * N, N * 8, cudaMemcpyDeviceToDevice,
+                                       c->stream));
+                }
+            dfree(c, key);
+            key = tr;
+        }
         // store key' = psi_g^-1(key) (see "Rotation" below); psi_g^-1 = psi_{5^(N/2 - k)}
-        uint64_t* kp = dalloc_t<uint64_t>(c, key_words(c));
-        if (!kp) return fail(HISA_E_OOM, "key allocation (%zu MiB)", key_words(c) * 8 >> 20);
+        uint64_t* kp = dalloc_t<uint64_t>(c, key_words(c, kL));
+        if (!kp) return fail(HISA_E_OOM, "key allocation (%zu MiB)", key_words(c, kL) * 8 >> 20);
         const uint64_t ginv = h_pow(5, slots - (uint64_t)k, 2 * N);
         const uint64_t* kin[1] = {key};
         uint64_t* kout[1] = {kp};
-        KL("automorphism", launch_automorphism(kin, kout, 1, 2 * L * M, c->log_n, &ginv, c->stream));
+        KL("automorphism", launch_automorphism(kin, kout, 1, 2 * kL * (kL + 1), c->log_n, &ginv, c->stream));
         dfree(c, key);
-        c->rot_keys[(uint64_t)k] = kp;
+        c->rot_keys[(uint64_t)k] = hisa_ctx::KeyRec{kp, kL};
         dfree(c, sg);
         dfree(c, sp);
     }
@@ -721,7 +749,12 @@ extern "C" int hisa_key_export(hisa_ctx* c, int64_t which, uint64_t* host, size_
     if (which == -1) { src = c->d_pk; w = (size_t)2 * c->L * c->N; }
     else if (which == -2) { src = c->d_sk; w = (size_t)(c->L + 1) * c->N; }
     else if (which == 0) { src = c->d_rlk; w = key_words(c); }
-    else if (c->rot_keys.count((uint64_t)which)) { src = c->rot_keys[(uint64_t)which]; w = key_words(c); }
+    int kL = c->L;
+    if (which > 0 && c->rot_keys.count((uint64_t)which)) {
+        src = c->rot_keys[(uint64_t)which].p;
+        kL = c->rot_keys[(uint64_t)which].kL;
+        w = key_words(c, kL);
+    }
     if (!src) return fail(HISA_E_NO_KEY, "no such key %lld", (long long)which);
     if (words != w) return fail(HISA_E_PARAMS, "key has %zu words", w);
     uint64_t* canon = nullptr;
@@ -731,7 +764,7 @@ extern "C" int hisa_key_export(hisa_ctx* c, int64_t which, uint64_t* host, size_
         const uint64_t g = h_pow(5, (uint64_t)which, 2 * c->N);
         const uint64_t* kin[1] = {src};
         uint64_t* kout[1] = {canon};
-        KL("automorphism", launch_automorphism(kin, kout, 1, 2 * c->L * (c->L + 1), c->log_n, &g, c->stream));
+        KL("automorphism", launch_automorphism(kin, kout, 1, 2 * kL * (kL + 1), c->log_n, &g, c->stream));
         src = canon;
     }
     CK(cudaMemcpyAsync(host, src, w * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1259,7 +1292,7 @@ static int ks_chunk(const hisa_ctx* c, int level) {
 
 // key switch of nz digits under ONE key: ModUp pass 1 -> fused pass 2 + key inner product (K4,
 // D never stored in NTT form) -> ModDown
-static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const KsBatch& kb) {
+static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, int kL, const KsBatch& kb) {
     const int l1 = level + 1, l2 = level + 2, L = c->L;
     const long long N = (long long)c->N;
     // scratch per ciphertext: dtil l1, T1 l1*l2, acc 2*l2, ptmp 2, md 2*l1
@@ -1282,7 +1315,7 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, const 
         for (int z = 0; z < nz; z++) { kj.t1[z] = t1[z]; kj.d[z] = kb.d[z]; kj.acc[z] = acc[z]; }
         kj.key = key;
         kj.l1 = l1;
-        kj.L = L;
+        kj.L = kL;      // key stride; the special prime's key limb is kL (mod_map gives the table's L)
         kj.nz = nz;
         for (int ri = 0; ri < l2; ri++) kj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
         Tables tb = c->tables();
@@ -1309,7 +1342,7 @@ extern "C" int hisa_relinearize(hisa_ctx* c, hisa_ct h) {
     kb.add[0] = o->ptr;
     kb.add_polys = 2;
     kb.add_a = (long long)l1 * N;
-    RET(keyswitch(c, 1, o->level, c->d_rlk, kb));
+    RET(keyswitch(c, 1, o->level, c->d_rlk, c->L, kb));
     dfree(c, o->ptr);
     o->ptr = out;
     o->npolys = 2;
@@ -1376,7 +1409,7 @@ extern "C" int hisa_mul_batch(hisa_ctx* c, const hisa_ct* a, const hisa_ct* b, s
         }
         kb.add_polys = 2;
         kb.add_a = (long long)l1 * N;
-        RET(keyswitch(c, nz, level, c->d_rlk, kb));
+        RET(keyswitch(c, nz, level, c->d_rlk, c->L, kb));
         dfree(c, t3);
         for (int z = 0; z < nz; z++)
             outs[i0 + z] = new_handle(c, OBJ_CT, res[z], level, 2, oa[i0 + z]->scale * ob[i0 + z]->scale);
@@ -1399,13 +1432,22 @@ static int normalize_rot(const hisa_ctx* c, int64_t k, uint64_t* out) {
     return HISA_OK;
 }
 static uint64_t galois(const hisa_ctx* c, uint64_t k) { return h_pow(5, k, 2 * c->N); }
+// a rotation key for amount k that serves `level` (keys are truncated to their max level)
+static int rot_key_check(hisa_ctx* c, uint64_t k, int level) {
+    auto it = c->rot_keys.find(k);
+    if (it == c->rot_keys.end()) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)k);
+    if (level >= it->second.kL)
+        return fail(HISA_E_NO_KEY, "rotation key for %llu generated up to level %d, ciphertext at level %d",
+                    (unsigned long long)k, it->second.kL - 1, level);
+    return HISA_OK;
+}
 
 // rotation of nz ciphertexts (same level, same amount, own key switch each): batched K4 path
 static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_t** outs, bool add_input = false) {
     const int level = in[0]->level, l1 = level + 1;
     const long long N = (long long)c->N;
-    auto it = c->rot_keys.find(k);
-    if (it == c->rot_keys.end()) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)k);
+    RET(rot_key_check(c, k, level));
+    const hisa_ctx::KeyRec& key = c->rot_keys[k];
     uint64_t* pre = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N * nz);
     if (!pre) return fail(HISA_E_OOM, "rotation scratch");
     const uint64_t* pres[MAXB];
@@ -1423,7 +1465,7 @@ static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_
     }
     kb.add_polys = 1;
     kb.add_a = 0;
-    RET(keyswitch(c, nz, level, it->second, kb));
+    RET(keyswitch(c, nz, level, key.p, key.kL, kb));
     if (add_input) {   // rotate-and-sum step: out = in + rot(in), the add fused into the permutation
         const uint64_t* adds[MAXB];
         for (int z = 0; z < nz; z++) adds[z] = in[z]->ptr;
@@ -1489,7 +1531,10 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
                     hj.diag[cg] = d1[g0 + cg];
                     for (int r = 0; r < R; r++) hj.acc[cg][r] = acc_of(g0 + cg, r);
                 }
-                for (int r = 0; r < R; r++) hj.key[r] = c->rot_keys[ks[r0 + r]];
+                for (int r = 0; r < R; r++) {
+                    hj.key[r] = c->rot_keys[ks[r0 + r]].p;
+                    hj.kL[r] = c->rot_keys[ks[r0 + r]].kL;
+                }
                 hj.l1 = l1;
                 hj.L = L;
                 for (int ri = 0; ri < l2; ri++) hj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
@@ -1546,8 +1591,7 @@ extern "C" int hisa_rot_left_hoisted_batch(hisa_ctx* c, const hisa_ct* in, size_
     std::vector<size_t> nz_idx;
     for (size_t r = 0; r < n; r++) {
         normalize_rot(c, k[r], &kk[r]);
-        if (kk[r] && !c->rot_keys.count(kk[r]))
-            return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk[r]);
+        if (kk[r]) RET(rot_key_check(c, kk[r], objs[0]->level));
         if (kk[r]) { nz_idx.push_back(r); amounts.push_back(kk[r]); }
     }
     for (size_t i = 0; i < nct; i++)
@@ -1573,7 +1617,7 @@ static int rot_common(hisa_ctx* c, hisa_ct h, int64_t k, hisa_ct* out) {
         if (!out) return HISA_OK;
         return hisa_copy(c, h, out);
     }
-    if (!c->rot_keys.count(kk)) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk);
+    RET(rot_key_check(c, kk, o->level));
     uint64_t* res[1];
     Obj* ins[1] = {o};
     RET(rotate_batch(c, ins, 1, kk, res));
@@ -1605,7 +1649,7 @@ extern "C" int hisa_rot_left_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int
         for (size_t i = 0; i < n; i++) RET(hisa_copy(c, in[i], &outs[i]));
         return HISA_OK;
     }
-    if (!c->rot_keys.count(kk)) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk);
+    RET(rot_key_check(c, kk, objs[0]->level));
     const size_t chunk = (size_t)ks_chunk(c, objs[0]->level);
     for (size_t i0 = 0; i0 < n; i0 += chunk) {
         const int nz = (int)std::min(chunk, n - i0);
@@ -1634,7 +1678,7 @@ extern "C" int hisa_rot_add_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int6
         for (size_t i = 0; i < n; i++) RET(hisa_add(c, in[i], in[i], &outs[i]));
         return HISA_OK;
     }
-    if (!c->rot_keys.count(kk)) return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk);
+    RET(rot_key_check(c, kk, objs[0]->level));
     const size_t chunk = (size_t)ks_chunk(c, objs[0]->level);
     for (size_t i0 = 0; i0 < n; i0 += chunk) {
         const int nz = (int)std::min(chunk, n - i0);
@@ -1701,8 +1745,7 @@ extern "C" int hisa_rot_left_hoisted(hisa_ctx* c, hisa_ct h, const int64_t* k, s
     std::vector<uint64_t> kk(n);
     for (size_t i = 0; i < n; i++) {
         normalize_rot(c, k[i], &kk[i]);
-        if (kk[i] && !c->rot_keys.count(kk[i]))
-            return fail(HISA_E_NO_KEY, "no rotation key for %llu", (unsigned long long)kk[i]);
+        if (kk[i]) RET(rot_key_check(c, kk[i], o->level));
     }
     // non-zero amounts share one ModUp (hoisted path); a single one uses the fused K4 path
     // (no D materialisation)
@@ -2390,6 +2433,63 @@ extern "C" int hisa_microbench_butterfly_f64(hisa_ctx* c, int iters, double* bfl
     c->ev_pool.push_back(b);
     dfree(c, out);
     *bfly_per_s = (double)blocks * threads * iters * 64.0 / (t * 1e-3);
+    return HISA_OK;
+}
+
+// the key multiply-accumulate of K4 (k_ks_ip5): a 52-bit D times a 50-bit key word, split into
+// 32 x 25-bit halves and accumulated in three 64-bit sums (4 IMAD.WIDE.U32 per MAC); two keys (b, a)
+// per D as in K4 -- the integer-pipe ceiling of the key inner products
+__global__ void __launch_bounds__(256) k_mb_mac(uint64_t* out, uint64_t k0, uint64_t k1, int iters) {
+    uint64_t D[8], A0[16], A1[16], A2[16];
+#pragma unroll
+    for (int e = 0; e < 8; e++) D[e] = ((uint64_t)(threadIdx.x * 8 + e + blockIdx.x) << 20) | 12345u;
+#pragma unroll
+    for (int e = 0; e < 16; e++) { A0[e] = 0; A1[e] = 0; A2[e] = 0; }
+    for (int it = 0; it < iters; it++) {
+        const uint32_t kl0 = (uint32_t)k0 & 0x1FFFFFFu, kh0 = (uint32_t)(k0 >> 25);
+        const uint32_t kl1 = (uint32_t)k1 & 0x1FFFFFFu, kh1 = (uint32_t)(k1 >> 25);
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            const uint32_t dl = (uint32_t)D[e], dh = (uint32_t)(D[e] >> 32);
+            A0[2 * e] += (uint64_t)dl * kl0;
+            A1[2 * e] += (uint64_t)dl * kh0;
+            A1[2 * e] += (uint64_t)(dh << 7) * kl0;
+            A2[2 * e] += (uint64_t)dh * kh0;
+            A0[2 * e + 1] += (uint64_t)dl * kl1;
+            A1[2 * e + 1] += (uint64_t)dl * kh1;
+            A1[2 * e + 1] += (uint64_t)(dh << 7) * kl1;
+            A2[2 * e + 1] += (uint64_t)dh * kh1;
+        }
+        k0 += 0x9E3779B97Full;
+        k1 += 0x7F4A7C15ull;
+    }
+    uint64_t x = 0;
+#pragma unroll
+    for (int e = 0; e < 16; e++) x ^= A0[e] + (A1[e] << 25) + (A2[e] << 57);
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x;
+}
+
+extern "C" int hisa_microbench_mac(hisa_ctx* c, int iters, double* mac_per_s) {
+    CHECK_CTX(c);
+    if (!mac_per_s || iters <= 0) return fail(HISA_E_PARAMS, "bad arguments");
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * 8, threads = 256;
+    uint64_t* out = dalloc_t<uint64_t>(c, (size_t)blocks * threads);
+    if (!out) return fail(HISA_E_OOM, "microbench");
+    cudaEvent_t a = take_event(c), b = take_event(c);
+    k_mb_mac<<<blocks, threads, 0, c->stream>>>(out, 0x2F0F0F0F0F0ull, 0x1234567890ull, 4);   // warm-up
+    CK(cudaEventRecord(a, c->stream));
+    k_mb_mac<<<blocks, threads, 0, c->stream>>>(out, 0x2F0F0F0F0F0ull, 0x1234567890ull, iters);
+    CK(cudaEventRecord(b, c->stream));
+    CK(cudaEventSynchronize(b));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, a, b));
+    c->ev_pool.push_back(a);
+    c->ev_pool.push_back(b);
+    dfree(c, out);
+    *mac_per_s = (double)blocks * threads * iters * 16.0 / (t * 1e-3);
     return HISA_OK;
 }
 

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
     const int t = threadIdx.x;
     const long long kstride_j = 2ll * (job.L + 1) << log_n;
     const long long kstride_p = (long long)(job.L + 1) << log_n;
-    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
+    const uint64_t* key_r = job.key + ((long long)(ri < l1 ? ri : job.L) << log_n) + off0;
     if (fp) {
         const double* twg = tb.fwd_d + ((long long)mi << log_n);
         const int s0 = log_n - LOG_M;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     const int t = threadIdx.x;
     const long long kstride_j = 2ll * (job.L + 1) << log_n;
     const long long kstride_p = (long long)(job.L + 1) << log_n;
-    const uint64_t* key_r = job.key + ((long long)mi << log_n) + off0;
+    const uint64_t* key_r = job.key + ((long long)(ri < l1 ? ri : job.L) << log_n) + off0;
     uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + off0;
     uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + off0;
     auto tile_src = [&](int j) -> const uint64_t* {
@@ -460,9 +460,6 @@ __global__ void __launch_bounds__(256) k_ks_ip_hoisted_multi(KsHoistMultiJob job
     for (int c = 0; c < CG; c++)
 #pragma unroll
         for (int k = 0; k < R; k++) { acc[c][k][0] = U128{0, 0}; acc[c][k][1] = U128{0, 0}; }
-    const long long kstride_j = 2ll * (job.L + 1) * N;
-    const long long kstride_p = (long long)(job.L + 1) * N;
-    const long long koff = (long long)mi * N + x;
     for (int j = 0; j < l1; j++) {
         uint64_t d[CG];
 #pragma unroll
@@ -473,7 +470,9 @@ __global__ void __launch_bounds__(256) k_ks_ip_hoisted_multi(KsHoistMultiJob job
         }
 #pragma unroll
         for (int k = 0; k < R; k++) {
-            const uint64_t* kb = job.key[k] + j * kstride_j + koff;
+            const int kL = job.kL[k];
+            const long long kstride_p = (long long)(kL + 1) * N;
+            const uint64_t* kb = job.key[k] + j * 2 * kstride_p + (long long)(ri < l1 ? ri : kL) * N + x;
             const uint64_t b = __ldcs(kb), a = __ldcs(kb + kstride_p);
 #pragma unroll
             for (int c = 0; c < CG; c++) {

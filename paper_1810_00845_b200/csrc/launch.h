@@ -60,8 +60,9 @@ constexpr int MAXCG = 4;
 struct KsHoistMultiJob {
     const uint64_t* D[MAXCG];       // per ciphertext [j][ri][N] (diagonal blocks unused)
     const uint64_t* diag[MAXCG];    // per ciphertext digit source [(l+1)][N]
-    const uint64_t* key[MAXR];      // R pre-permuted keys
+    const uint64_t* key[MAXR];      // R pre-permuted keys [kL][2][kL+1][N]
     uint64_t* acc[MAXCG][MAXR];     // out [2][l+2][N]
+    int kL[MAXR];                   // q primes each key covers (truncated keys, kL >= l+1)
     int l1, L, cg;
     uint8_t mod_map[MAXL];
 };
@@ -76,9 +77,9 @@ struct KsJob {
     const uint64_t* t1[MAXB];     // pass-1 output [j][ri][N] (ri over l+2 output primes)
     const uint64_t* d[MAXB];      // the digit source in NTT form [(l+1)][N] (D_{j,q_j} = d_j)
     uint64_t* acc[MAXB];          // out [2][l+2][N], fully reduced
-    const uint64_t* key;          // [L][2][L+1][N]
+    const uint64_t* key;          // [L][2][L+1][N] (L = the key's q primes; truncated keys L < ctx L)
     int l1;                       // active limbs l+1
-    int L;                        // total q primes (key stride)
+    int L;                        // q primes of the key: stride, and the special prime's key limb
     int nz;                       // ciphertexts in the batch (grid.x = tiles * nz)
     uint8_t mod_map[MAXL];        // ri -> modulus index
 };

@@ -162,6 +162,7 @@ class Symbolic:
         self.cts = {}
         self.next = 1
         self.rotations = set()
+        self.rot_level = {}       # amount -> highest level it is used at (key truncation)
         self.counts = {}
 
     def _new(self, level, scale):
@@ -169,6 +170,10 @@ class Symbolic:
         self.next += 1
         self.cts[h] = (level, scale)
         return h
+
+    def _rot(self, kk, lv):
+        self.rotations.add(kk)          # (lv = -1: an empty batch on a rank without channels)
+        self.rot_level[kk] = max(lv, self.rot_level.get(kk, -1))
 
     def _count(self, op, n=1):
         self.counts[op] = self.counts.get(op, 0) + n
@@ -189,7 +194,7 @@ class Symbolic:
         for k in ks:
             kk = k % self.slots
             if kk:
-                self.rotations.add(kk)
+                self._rot(kk, lv)
                 self._count("rot_hoisted")
             out.append(self._new(lv, sc))
         return out
@@ -200,7 +205,7 @@ class Symbolic:
     def rot_left_batch(self, hs, k):
         kk = k % self.slots
         if kk:
-            self.rotations.add(kk)
+            self._rot(kk, max((self.cts[h][0] for h in hs), default=-1))
             self._count("rot", len(hs))
         return [self._new(*self.cts[h]) for h in hs]
 
@@ -241,7 +246,7 @@ class Symbolic:
     def rot_add_batch(self, hs, k):
         kk = k % self.slots
         if kk:
-            self.rotations.add(kk)
+            self._rot(kk, max((self.cts[h][0] for h in hs), default=-1))
             self._count("rot", len(hs))
         self._count("add", len(hs))
         return [self._new(*self.cts[h]) for h in hs]
@@ -312,8 +317,20 @@ class EncryptedNet:
         cts = [sym.fresh(top, net["scale"]) for _ in range(lay.C)]
         outs, out_lay = en.forward(cts, lay)
         final = sym.cts[outs[0]][0]
-        return {"rotations": sorted(sym.rotations), "final_level": final, "levels_used": top - final,
-                "counts": dict(sym.counts), "out_layout": out_lay}
+        return {"rotations": sorted(sym.rotations), "rotation_levels": dict(sorted(sym.rot_level.items())),
+                "final_level": final, "levels_used": top - final, "counts": dict(sym.counts), "out_layout": out_lay}
+
+    @staticmethod
+    def keygen(backend, plan, relin: bool = True):
+        """Keys for a plan: the relinearisation key and one rotation key per amount, each rotation
+        key truncated to the highest level the network rotates by it (hisa_keygen max_level;
+        SURVEY 7 hard part 3 -- 600 MiB per full key at N = 2^16, L = 24)."""
+        by_level = {}
+        for k, lv in plan["rotation_levels"].items():
+            by_level.setdefault(lv, []).append(k)
+        backend.keygen([], relin)
+        for lv, ks in sorted(by_level.items()):
+            backend.keygen(ks, False, lv)
 
     # ---- sharding (SURVEY 8e) ---------------------------------------------------------------
     def owned(self, n: int) -> range:

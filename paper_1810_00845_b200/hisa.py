@@ -56,7 +56,7 @@ _SIGS = {
     "hisa_moduli": [_vp, _u64p, _csz],
     "hisa_ring_degree": [_vp, _u64p, ctypes.POINTER(_ci)],
     "hisa_mem_stats": [_vp, ctypes.POINTER(_csz), ctypes.POINTER(_csz)],
-    "hisa_keygen": [_vp, _i64p, _csz, _ci],
+    "hisa_keygen": [_vp, _i64p, _csz, _ci, _ci],
     "hisa_key_export": [_vp, _ci64, _u64p, _csz],
     "hisa_encrypt": [_vp, _cu64, _u64p],
     "hisa_decrypt": [_vp, _cu64, _u64p],
@@ -110,6 +110,7 @@ _SIGS = {
     "hisa_launch_count": [_vp, _u64p],
     "hisa_microbench_butterfly": [_vp, _ci, _dp],
     "hisa_microbench_butterfly_f64": [_vp, _ci, _dp],
+    "hisa_microbench_mac": [_vp, _ci, _dp],
     "hisa_last_error": [],
 }
 
@@ -199,9 +200,9 @@ def hisa_mem_stats(ctx) -> tuple[int, int]:
     return a.value, b.value
 
 
-def hisa_keygen(ctx, rot_left_amounts=(), relin: bool = True):
+def hisa_keygen(ctx, rot_left_amounts=(), relin: bool = True, max_level: int = -1):
     r = np.ascontiguousarray(list(rot_left_amounts), dtype=np.int64)
-    _chk(load().hisa_keygen(ctx, _ptr(r, _i64p) if r.size else None, r.size, int(relin)))
+    _chk(load().hisa_keygen(ctx, _ptr(r, _i64p) if r.size else None, r.size, int(relin), int(max_level)))
 
 
 def hisa_key_export(ctx, which: int, words: int) -> np.ndarray:
@@ -504,6 +505,12 @@ def hisa_microbench_butterfly(ctx, iters: int = 2000) -> float:
 def hisa_microbench_butterfly_f64(ctx, iters: int = 2000) -> float:
     out = _cd()
     _chk(load().hisa_microbench_butterfly_f64(ctx, iters, ctypes.byref(out)))
+    return out.value
+
+
+def hisa_microbench_mac(ctx, iters: int = 2000) -> float:
+    out = _cd()
+    _chk(load().hisa_microbench_mac(ctx, iters, ctypes.byref(out)))
     return out.value
 
 

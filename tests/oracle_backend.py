@@ -42,8 +42,14 @@ class OracleBackend:
         return c.level, c.npolys, c.scale
 
     # ---- keys / client
-    def keygen(self, rots, relin=True):
+    def keygen(self, rots, relin=True, max_level=-1):
+        # the oracle keeps full keys; a truncated key holds the same words on the levels it serves
+        if getattr(self, "_keyed", False) and not relin:
+            for k in rots:
+                self.o.add_rot_key(k)
+            return
         self.o.keygen(rot_amounts=list(rots), relin=relin)
+        self._keyed = True
 
     def encode(self, v, scale, level=-1):
         return self._put(self.o.encode(np.asarray(v, dtype=np.float64), scale, None if level < 0 else level))

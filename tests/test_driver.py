@@ -47,7 +47,7 @@ def _run_pair(net, W, img, oracle_layers=None, rot_policy="exact", sample_layers
     assert g.moduli == on.o.moduli
     plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli, rot_policy=rot_policy)
     assert plan["rotations"] == on.amounts          # the compiler's key selection
-    g.keygen(plan["rotations"], True)
+    EncryptedNet.keygen(g, plan)
     en = EncryptedNet(g, net, W, SN.ACT_COEFFS, rot_policy=rot_policy)
     cts, lay = en.encrypt_image(img)
     for h, oc in zip(cts, ocs):

@@ -195,3 +195,41 @@ def test_conv_engines_bit_identical(tmp_path):
             term = o.mul_scalar(cts[t], float(W[oc, t]), 2.0 ** 30)
             acc = term if acc is None else o.add(acc, term)
         assert (res["1"][oc] == acc.data).all(), oc
+
+
+def test_truncated_rotation_keys():
+    """hisa_keygen(max_level): a rotation key stored for levels <= m holds exactly the words of
+    the full key's digits j <= m on q_0..q_m and p (checked against the oracle's full key);
+    rotations at levels <= m are bit-exact with the oracle's (full-key) rotation, the rotation at
+    level m + 1 fails with NO_KEY, and a later request at a higher level regenerates the key."""
+    qb = [60, 40, 40, 40, 40]
+    L = len(qb)
+    g, o = _pair(11, qb, 60, [], seed=5)
+    N = g.N
+    m = 2
+    g.keygen([7, 300], False, m)
+    o.keygen(rot_amounts=[7, 300])
+    kL = m + 1
+    for k in (7, 300):
+        got = g.key_export(k, kL * 2 * (kL + 1) * N).reshape(kL, 2, kL + 1, N)
+        full = o.rot_keys[k]
+        assert (got[:, :, :kL] == full[:kL, :, :kL]).all()
+        assert (got[:, :, kL] == full[:kL, :, L]).all()          # the special prime's limb
+    for lv in (0, 1, 2):
+        a = g.ct_random(40 + lv, lv)
+        oa = o.bench_ct(40 + lv, lv)
+        assert (g.ct_export(g.rot_left(a, 7)) == o.rot_left(oa, 7).data).all()
+        hs = g.rot_left_hoisted(a, [7, 300])                   # K7 with truncated keys
+        assert (g.ct_export(hs[1]) == o.rot_left(oa, 300).data).all()
+    hi = g.ct_random(50, 3)
+    with pytest.raises(H.HisaError) as ei:
+        g.rot_left(hi, 7)
+    assert ei.value.code == "NO_KEY"
+    with pytest.raises(H.HisaError) as ei:
+        g.keygen([9], False, L)
+    assert ei.value.code == "PARAMS"
+    g.keygen([7], False, 3)                                     # regenerated at level 3
+    assert (g.ct_export(g.rot_left(hi, 7)) == o.rot_left(o.bench_ct(50, 3), 7).data).all()
+    g.keygen([7], False, 1)                                     # lower request keeps level 3
+    assert g.key_export(7, 4 * 2 * 5 * N).size == 4 * 2 * 5 * N
+    g.close()

@@ -34,7 +34,7 @@ def _rank(rank, world, port, name, q):
         net, W, img = SN.NETS[name], SN.net_weights(name), SN.net_image(name, 1)
         g = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=5, device=0, arena_bytes=12 << 30)
         plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli)
-        g.keygen(plan["rotations"], True)
+        EncryptedNet.keygen(g, plan)
         en = EncryptedNet(g, net, W, SN.ACT_COEFFS, group=dist.group.WORLD)
         cts, lay = en.encrypt_image(img)
         mine = en.shard_input(cts)
@@ -67,7 +67,7 @@ def test_sharded_network_bit_identical(name):
     net, W, img = SN.NETS[name], SN.net_weights(name), SN.net_image(name, 1)
     g = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=5, arena_bytes=12 << 30)
     plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, g.moduli)
-    g.keygen(plan["rotations"], True)
+    EncryptedNet.keygen(g, plan)
     en = EncryptedNet(g, net, W, SN.ACT_COEFFS)
     cts, lay = en.encrypt_image(img)
     out, _ = en.forward(cts, lay)

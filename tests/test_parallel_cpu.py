@@ -43,7 +43,7 @@ def _run(net, W, img, group=None, partition="ic"):
     from paper_1810_00845_b200.driver import EncryptedNet
     b = OracleBackend(net["log_n"], net["q_bits"], net["p_bits"], seed=3)
     plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, b.moduli)
-    b.keygen(plan["rotations"], True)
+    EncryptedNet.keygen(b, plan)
     en = EncryptedNet(b, net, W, SN.ACT_COEFFS, group=group, partition=partition)
     cts, lay = en.encrypt_image(img)
     if group is not None:

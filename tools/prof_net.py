@@ -16,7 +16,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "lenet_small"
 net, W, img = SN.NETS[name], SN.net_weights(name), SN.net_image(name, 0)
 ctx = H.Context(net["log_n"], net["q_bits"], net["p_bits"], seed=0, arena_bytes=64 << 30)
 plan = EncryptedNet.plan(net, W, SN.ACT_COEFFS, ctx.moduli)
-ctx.keygen(plan["rotations"], True)
+EncryptedNet.keygen(ctx, plan)
 en = EncryptedNet(ctx, net, W, SN.ACT_COEFFS)
 cts, lay = en.encrypt_image(img)
 out, _ = en.forward(cts, lay)       # warm-up (weight plaintexts encoded once)
