@@ -183,6 +183,10 @@ struct hisa_ctx {
     uint64_t seed = 0;
     int device = 0;
     cudaStream_t stream = 0;
+    // side stream for work that runs beside the main stream's (K4's integer-engine rows next to
+    // its FP64 rows); fork/join through events, created on first use
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     bool poisoned = false;
     Arena arena;
     bool has_arena = false;
@@ -529,6 +533,9 @@ extern "C" int hisa_ctx_destroy(hisa_ctx* c) {
         for (auto& kv : c->pool_sizes) cudaFree(kv.first);
     }
     for (void* q : c->table_allocs) cudaFree(q);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     cudaGetLastError();
     delete c;
     return HISA_OK;
@@ -1317,9 +1324,18 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, int kL
         kj.l1 = l1;
         kj.L = kL;      // key stride; the special prime's key limb is kL (mod_map gives the table's L)
         kj.nz = nz;
-        for (int ri = 0; ri < l2; ri++) kj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+        for (int ri = 0; ri < l2; ri++) {
+            kj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
+            if ((double)c->mod[kj.mod_map[ri]] < c->f64_max_q) kj.fp_rows |= 1ull << ri;
+        }
         Tables tb = c->tables();
-        KL("ks_ip_rows", launch_ks_ip(kj, tb, nz, c->stream));
+        if (!c->side) {
+            CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+        }
+        const SideStream side{c->side, c->ev_fork, c->ev_join};
+        KL("ks_ip_rows", launch_ks_ip(kj, tb, nz, c->stream, &side));
     }
     RET(ks_moddown(c, nz, level, acc, ptmp, md, kb));
     dfree(c, scratch);

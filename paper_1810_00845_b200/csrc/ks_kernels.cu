@@ -8,6 +8,7 @@
 // D never touches HBM in its NTT form; the key is streamed once per ciphertext.
 #include <cuda_runtime.h>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include "ntt_f64.cuh"
 #include "launch.h"
@@ -29,7 +30,7 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
     const int nz = job.nz;
     const int z = blockIdx.x % nz;
     // the special prime's CTAs (integer engine, slower) first, so they do not form the tail
-    const int ri = blockIdx.y == 0 ? job.l1 : (int)blockIdx.y - 1;
+    const int ri = job.ri_list[blockIdx.y];
     const int l1 = job.l1;
     const int nri = l1 + 1;
     const int log_n = tb.log_n;
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     double* tws = reinterpret_cast<double*>(sm + 2 * G::STRIDE);
     const int nz = job.nz;
     const int z = blockIdx.x % nz;
-    const int ri = blockIdx.y == 0 ? job.l1 : (int)blockIdx.y - 1;   // special prime first
+    const int ri = job.ri_list[blockIdx.y];
     const int l1 = job.l1;
     const int nri = l1 + 1;
     const int log_n = tb.log_n;
@@ -399,12 +400,242 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     o1[1] = make_ulonglong2(fold(1, 2), fold(1, 3));
 }
 
+
+// ------------------------------------------------------------------------------------------
+// K4 v6 (FP64 output primes, M = 256 rows: N = 2^15, 2^16).  ncu of k_ks_ip5 (profiles/
+// r2_ncu_k4_v1.txt) showed the shared-memory data pipe, not the FP64 pipe, as the bound: 72 % LSU
+// wavefronts against 35 % FP64, ~34 wavefronts per 32 element-digits (three radix-4 exchanges,
+// row and key staging, 65 M bank-conflict wavefronts) and ~108 instructions per element-digit
+// (the split 64-bit MACs alone ~30).  This kernel:
+//  * runs each 256-point row as two radix-16 register phases with ONE exchange, 16 threads per
+//    row (thread g holds elements 16a + g in phase 1, 16t + b in phase 2);
+//  * accumulates the key inner product on the FP64 pipe: acc += mulred(D, K) with D the centred
+//    phase-2 output (|D| <= 1.6 q) and K the key word (< q, exact u2d): |mulred| <= 1.1 q
+//    (ntt_f64.cuh bound, |a w| <= 1.6 q^2), so six products fit between re-centrings (|acc| <
+//    7.1 q < 2^53 for q < 2^50): every step is exact integer arithmetic, the result (one final
+//    canonical reduction) is the same residue as the integer MAC's -- two doubles per output
+//    word instead of three 64-bit words, no 64-bit multiplies;
+//  * puts CG ciphertexts x RB rows (G = CG RB groups of 16 threads) in one CTA: the key rows are
+//    staged once per row and shared by the CG ciphertexts;
+//  * stages each step's rows and keys with cp.async one step ahead (double buffer); the key rows
+//    are stored with the 16-byte chunks of every 128-byte line XOR-swizzled by the line index, so
+//    the phase-2 pattern (thread t reads words 16t .. 16t+15 as 16-byte pairs) is conflict-free;
+//    the exchange reuses the step's row buffer with the same swizzle; outputs leave through it
+//    as coalesced 8-byte stores.
+// Digit order: the l non-diagonal digits (pass-1 rows, two phases), then the diagonal digit d_ri
+// (already in the NTT domain, canonical, staged swizzled, no NTT).
+// ------------------------------------------------------------------------------------------
+template <int CG, int RB>
+struct Ip6 {
+    static constexpr int G = CG * RB;            // 16-thread groups per CTA
+    static constexpr int NT = 16 * G;
+    static constexpr int STAGE_T1 = G * 256;     // words: one row per group
+    static constexpr int STAGE_K = RB * 2 * 256; // b and a key rows per row
+    static constexpr int STAGE = STAGE_T1 + STAGE_K;
+    static constexpr size_t smem_bytes() { return (size_t)(256 * RB + 2 * STAGE) * 8; }
+};
+
+// word b of line t of a 256-word row in the pair-swizzled layout (lines of 16 words = 128 B)
+__device__ __forceinline__ int swz(int t, int b) { return t * 16 + ((((b >> 1) ^ t) & 7) << 1) + (b & 1); }
+
+template <int CG, int RB, int MINB>
+__global__ void __launch_bounds__(16 * CG * RB, MINB) k_ks_ip6(KsJob job, Tables tb) {
+    using P = Ip6<CG, RB>;
+    extern __shared__ uint64_t sm[];
+    double* tw_all = reinterpret_cast<double*>(sm);              // [RB][256] row twiddles (2^u + m)
+    uint64_t* stage0 = sm + 256 * RB;
+    const int l1 = job.l1, nri = l1 + 1, log_n = tb.log_n;
+    const int ri = job.ri_list[blockIdx.y];
+    const int nzb = job.nz / CG;                                 // ciphertext blocks
+    const int zb = blockIdx.x % nzb;
+    const int row_base = (blockIdx.x / nzb) * RB;
+    const int tid = threadIdx.x;
+    const int grp = tid >> 4, g = tid & 15;
+    const int cz = grp % CG, rr = grp / CG;
+    const int z = zb * CG + cz;
+    const int row = row_base + rr;
+    const int mi = job.mod_map[ri];
+    const double2 qd = tb.modd[mi];
+    const double q = qd.x, qinv = qd.y;
+    const long long kstride_p = (long long)(job.L + 1) << log_n;
+    const long long kstride_j = 2 * kstride_p;
+    const uint64_t* key_ri = job.key + ((long long)(ri < l1 ? ri : job.L) << log_n);
+    const int n_nd = l1 - 1;                                      // non-diagonal digits (ri < l1)
+    const int nsteps = n_nd + 1;
+    const double* tw = tw_all + rr * 256;
+
+    // cp.async copies of step `st` into stage buffer `buf`
+    auto issue = [&](int st, int buf) {
+        uint64_t* base = stage0 + buf * P::STAGE;
+        const bool diag = st == n_nd;
+        const int j = diag ? ri : (st < ri ? st : st + 1);
+        // rows: group k's row (256 words = 128 chunks of 16 B); plain for pass-1 rows, swizzled for
+        // the diagonal digit (read in the phase-2 pattern)
+        for (int c = tid; c < P::G * 128; c += P::NT) {
+            const int k = c >> 7, ch = c & 127;
+            const int zz = zb * CG + k % CG, rw = row_base + k / CG;
+            const uint64_t* src = diag ? job.d[zz] + ((long long)j << log_n) + (rw << 8)
+                                       : job.t1[zz] + (((long long)j * nri + ri) << log_n) + (rw << 8);
+            const int line = ch >> 3, cc = ch & 7;
+            const int dst = k * 256 + (diag ? line * 16 + ((cc ^ (line & 7)) << 1) : ch * 2);
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(base + dst);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + ch * 2) : "memory");
+        }
+        // keys: per row, b and a (swizzled)
+        uint64_t* kbase = base + P::STAGE_T1;
+        for (int c = tid; c < RB * 256; c += P::NT) {
+            const int rk = c >> 8, h = (c >> 7) & 1, ch = c & 127;
+            const uint64_t* src = key_ri + (long long)j * kstride_j + h * kstride_p + ((row_base + rk) << 8) + ch * 2;
+            const int line = ch >> 3, cc = ch & 7;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(kbase + (rk * 2 + h) * 256 + line * 16 +
+                                                                   ((cc ^ (line & 7)) << 1));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
+    issue(0, 0);
+    {   // each row's twiddles: stage u (0..7 of the last 8 stages), group m -> tw[2^u + m]
+        const double* twg = tb.fwd_d + ((long long)mi << log_n);
+        const int s0 = log_n - 8;
+        // phase 2 (u >= 4): thread g's k-th twiddle of stage u, m = g 2^(u-4) + k, is stored at
+        // 2^u + 16 k + g, so the 16 threads of a row read 16 consecutive words (conflict-free)
+        for (int i = tid; i < 256 * RB; i += P::NT) {
+            const int rk = i >> 8, idx = i & 255;
+            if (idx == 0) continue;
+            const int u = 31 - __clz(idx), m = idx - (1 << u);
+            const int pos = u < 4 ? idx : (1 << u) + ((m & ((1 << (u - 4)) - 1)) << 4) + (m >> (u - 4));
+            tw_all[rk * 256 + pos] = twg[(1 << (s0 + u)) + ((row_base + rk) << u) + m];
+        }
+    }
+
+    double accb[16], acca[16];
+#pragma unroll
+    for (int b = 0; b < 16; b++) { accb[b] = 0.0; acca[b] = 0.0; }
+
+    for (int st = 0; st < nsteps; st++) {
+        const int buf = st & 1;
+        if (st + 1 < nsteps) {
+            issue(st + 1, buf ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        uint64_t* base = stage0 + buf * P::STAGE;
+        double* rowbuf = reinterpret_cast<double*>(base + grp * 256);
+        const uint64_t* kb = base + P::STAGE_T1 + rr * 512;
+        double r[16];
+        if (st < n_nd) {
+            // phase 1: elements 16a + g, stages u = 0..3 on a (twiddles uniform per row)
+#pragma unroll
+            for (int a = 0; a < 16; a++) r[a] = rowbuf[16 * a + g];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int dist = 8 >> u;
+#pragma unroll
+                for (int a = 0; a < 16; a++) {
+                    if (a & dist) continue;
+                    const double W = tw[(1 << u) + (a >> (4 - u))];
+                    const double X = full_stage(u, 8) ? redd(r[a], q, qinv) : r[a];
+                    const double T = mulred(r[a + dist], W, q, qinv);
+                    r[a] = __dadd_rn(X, T);
+                    r[a + dist] = __dsub_rn(X, T);
+                }
+            }
+            __syncwarp();
+            // exchange in place (pair-swizzled): write (a, g), read line t = g
+#pragma unroll
+            for (int a = 0; a < 16; a++) rowbuf[swz(a, g)] = r[a];
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const double2 v = *reinterpret_cast<const double2*>(rowbuf + swz(g, 2 * c));
+                r[2 * c] = v.x;
+                r[2 * c + 1] = v.y;
+            }
+            // phase 2: elements 16t + b (t = g), stages u = 4..7 on b
+#pragma unroll
+            for (int u = 4; u < 8; u++) {
+                const int dist = 8 >> (u - 4);
+#pragma unroll
+                for (int b = 0; b < 16; b++) {
+                    if (b & dist) continue;
+                    const double W = tw[(1 << u) + ((b >> (8 - u)) << 4) + g];
+                    const double X = full_stage(u, 8) ? redd(r[b], q, qinv) : r[b];
+                    const double T = mulred(r[b + dist], W, q, qinv);
+                    r[b] = __dadd_rn(X, T);
+                    r[b + dist] = __dsub_rn(X, T);
+                }
+            }
+        } else {
+            // the diagonal digit d_ri: canonical NTT-domain words, staged swizzled
+            const uint64_t* dv = reinterpret_cast<const uint64_t*>(rowbuf);
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(dv + swz(g, 2 * c));
+                r[2 * c] = u2d(v.x);
+                r[2 * c + 1] = u2d(v.y);
+            }
+        }
+        // key inner product on the FP64 pipe (exact; see the header)
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const ulonglong2 vb = *reinterpret_cast<const ulonglong2*>(kb + swz(g, 2 * c));
+            const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(kb + 256 + swz(g, 2 * c));
+            accb[2 * c] = __dadd_rn(accb[2 * c], mulred(r[2 * c], u2d(vb.x), q, qinv));
+            accb[2 * c + 1] = __dadd_rn(accb[2 * c + 1], mulred(r[2 * c + 1], u2d(vb.y), q, qinv));
+            acca[2 * c] = __dadd_rn(acca[2 * c], mulred(r[2 * c], u2d(va.x), q, qinv));
+            acca[2 * c + 1] = __dadd_rn(acca[2 * c + 1], mulred(r[2 * c + 1], u2d(va.y), q, qinv));
+        }
+        if (st % 6 == 5) {
+#pragma unroll
+            for (int b = 0; b < 16; b++) { accb[b] = redd(accb[b], q, qinv); acca[b] = redd(acca[b], q, qinv); }
+        }
+        __syncthreads();   // this buffer is refilled by the next step's issue
+    }
+    // outputs: canonical residues, transposed through the group's row buffer (free now) for
+    // coalesced 8-byte stores
+    uint64_t* obuf = stage0 + grp * 256;
+    uint64_t* out0 = job.acc[z] + ((long long)ri << log_n) + (row << 8);
+    uint64_t* out1 = job.acc[z] + ((long long)(nri + ri) << log_n) + (row << 8);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const double* acc = h ? acca : accb;
+            *reinterpret_cast<ulonglong2*>(obuf + swz(g, 2 * c)) =
+                make_ulonglong2(d_canon(acc[2 * c], q, qinv), d_canon(acc[2 * c + 1], q, qinv));
+        }
+        __syncwarp();
+        uint64_t* o = h ? out1 : out0;
+#pragma unroll
+        for (int k = 0; k < 16; k++) o[16 * k + g] = obuf[swz(k, g)];
+        __syncwarp();
+    }
+}
+
+template <int CG, int RB, int MINB>
+static cudaError_t ks_ip6_t(const KsJob& job, const Tables& tb, int nfp, cudaStream_t st) {
+    using P = Ip6<CG, RB>;
+    const int rows = 1 << (tb.log_n - 8);
+    const size_t smem = P::smem_bytes();
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ks_ip6<CG, RB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    dim3 grid((rows / RB) * (job.nz / CG), nfp, 1);
+    k_ks_ip6<CG, RB, MINB><<<grid, P::NT, smem, st>>>(job, tb);
+    return cudaGetLastError();
+}
+
 template <int MINB>
-static cudaError_t ks_ip5_t(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+static cudaError_t ks_ip5_t(const KsJob& job, const Tables& tb, int nz, int nrows, cudaStream_t st) {
     const int rows = 1 << (tb.log_n - 8);
     // 4 exchange tiles + twiddles + row prefetch [2][256] + key stage [2][2][256]: 24 KB
     const size_t smem = (4 * (size_t)K5_TILE + 256 + 512 + 1024) * sizeof(uint64_t);
-    dim3 grid(rows * nz, job.l1 + 1, 1);
+    dim3 grid(rows * nz, nrows, 1);
     k_ks_ip5<MINB><<<grid, 64, smem, st>>>(job, tb);
     return cudaGetLastError();
 }
@@ -419,24 +650,74 @@ static cudaError_t ks_ip2_t(const KsJob& job, const Tables& tb, int nz, cudaStre
     return cudaGetLastError();
 }
 
-template <int LOG_M>
-static cudaError_t ks_ip_m(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
-    // measured best on B200 (profiles/r1_ks_variants.txt, profiles/r2_*): M = 256 rows -> the
-    // register-direct two-digit kernel k_ks_ip5 (>= 10 CTAs / SM); other row lengths -> k_ks_ip2
-    // (one row per 64-thread CTA, radix-4 phases, two digits interleaved through the FP64 engine
-    // with the row's twiddles staged in shared memory, >= 12 CTAs / SM)
-    if constexpr (LOG_M == 8) return ks_ip5_t<K5_MINB>(job, tb, nz, st);
-    return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
+#ifndef K4_V6
+#define K4_V6 1      // 0: round-1 k_ks_ip5 on every row (side builds for A/B timing only)
+#endif
+#ifndef K6_MINB
+#define K6_MINB 4      // 128 registers, no spills (5: spills)
+#endif
+
+// M = 256: the FP64 output primes run k_ks_ip6 (CG ciphertexts x RB rows per CTA: 8 x 1, 4 x 1,
+// 2 x 2 or 1 x 4 by the largest of 8, 4, 2, 1 dividing nz), the integer-engine primes (60-bit: the special prime, q_0 of
+// configs 1, 3-5) the integer path of k_ks_ip5, each as its own launch over its rows
+static cudaError_t ks_ip_256(KsJob job, const Tables& tb, int nz, cudaStream_t st, const SideStream* side) {
+    const int l2 = job.l1 + 1;
+    int nfp = 0, nint = 0;
+    uint8_t fp[MAXL], in[MAXL];
+    for (int ri = 0; ri < l2; ri++) {
+        if (K4_V6 && ((job.fp_rows >> ri) & 1)) fp[nfp++] = (uint8_t)ri;
+        else in[nint++] = (uint8_t)ri;
+    }
+    cudaError_t e;
+    // the integer rows (one or two of ~25: a few percent of the work at 2.3x the cost per row)
+    // run on the side stream beside the FP64 rows instead of as a serial tail
+    const bool fork = side && nint && nfp;
+    if (nint) {
+        KsJob ji = job;
+        memcpy(ji.ri_list, in, nint);
+        cudaStream_t si = st;
+        if (fork) {
+            if ((e = cudaEventRecord(side->fork, st)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(side->s, side->fork, 0)) != cudaSuccess) return e;
+            si = side->s;
+        }
+        if ((e = ks_ip5_t<K5_MINB>(ji, tb, nz, nint, si)) != cudaSuccess) return e;
+        if (fork && (e = cudaEventRecord(side->join, side->s)) != cudaSuccess) return e;
+    }
+    if (nfp) {
+        memcpy(job.ri_list, fp, nfp);
+        if (nz % 8 == 0) e = ks_ip6_t<8, 1, K6_MINB>(job, tb, nfp, st);
+        else if (nz % 4 == 0) e = ks_ip6_t<4, 1, K6_MINB>(job, tb, nfp, st);
+        else if (nz % 2 == 0) e = ks_ip6_t<2, 2, K6_MINB>(job, tb, nfp, st);
+        else e = ks_ip6_t<1, 4, K6_MINB>(job, tb, nfp, st);
+        if (e != cudaSuccess) return e;
+    }
+    if (fork) return cudaStreamWaitEvent(st, side->join, 0);
+    return cudaSuccess;
 }
 
-cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st) {
+template <int LOG_M>
+static cudaError_t ks_ip_m(KsJob job, const Tables& tb, int nz, cudaStream_t st, const SideStream* side) {
+    // M = 256 rows -> ks_ip_256; other row lengths -> k_ks_ip2 (one row per 64-thread CTA,
+    // radix-4 phases, two digits interleaved through the FP64 engine with the row's twiddles
+    // staged in shared memory, >= 12 CTAs / SM; the special prime's CTAs first)
+    if constexpr (LOG_M == 8) {
+        return ks_ip_256(job, tb, nz, st, side);
+    } else {
+        job.ri_list[0] = (uint8_t)job.l1;
+        for (int ri = 0; ri < job.l1; ri++) job.ri_list[ri + 1] = (uint8_t)ri;
+        return ks_ip2_t<LOG_M, 2, 12>(job, tb, nz, st);
+    }
+}
+
+cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st, const SideStream* side) {
     const int lm = tb.log_n - split_m1(tb.log_n);
     switch (lm) {
-        case 4: return ks_ip_m<4>(job, tb, nz, st);
-        case 5: return ks_ip_m<5>(job, tb, nz, st);
-        case 6: return ks_ip_m<6>(job, tb, nz, st);
-        case 7: return ks_ip_m<7>(job, tb, nz, st);
-        case 8: return ks_ip_m<8>(job, tb, nz, st);
+        case 4: return ks_ip_m<4>(job, tb, nz, st, side);
+        case 5: return ks_ip_m<5>(job, tb, nz, st, side);
+        case 6: return ks_ip_m<6>(job, tb, nz, st, side);
+        case 7: return ks_ip_m<7>(job, tb, nz, st, side);
+        case 8: return ks_ip_m<8>(job, tb, nz, st, side);
     }
     return cudaErrorInvalidValue;
 }

@@ -82,8 +82,15 @@ struct KsJob {
     int L;                        // q primes of the key: stride, and the special prime's key limb
     int nz;                       // ciphertexts in the batch (grid.x = tiles * nz)
     uint8_t mod_map[MAXL];        // ri -> modulus index
+    uint8_t ri_list[MAXL];        // grid.y -> output prime ri (filled by launch_ks_ip)
+    uint64_t fp_rows;             // bit ri: output prime ri runs the FP64 engine (q < 2^50)
 };
-cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st);
+// a second stream with fork / join events: independent launches of one step run side by side
+struct SideStream {
+    cudaStream_t s;
+    cudaEvent_t fork, join;
+};
+cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_t st, const SideStream* side = nullptr);
 
 // K8 on the tensor cores (conv_tc_kernels.cu): byte-split u8 x u8 -> s32 tcgen05 MMAs
 struct ConvTcJob {

@@ -423,3 +423,32 @@ def test_encode_batch_bit_exact(pair):
     hs = g.encode_batch(vs, float(o.q[lv]), lv)
     for h, v in zip(hs, vs):
         assert (g.pt_export(h) == o.encode(v, float(o.q[lv]), lv).data).all()
+
+
+@pytest.mark.parametrize("nz", [1, 2, 4, 5, 6, 8])
+def test_k4_batch_shapes_and_long_digit_chains(nz):
+    """K4 at M = 256 (N = 2^15) in every CTA shape (ciphertexts x rows per CTA: 8x1, 4x1, 2x2,
+    1x4, picked by the batch size) with 13 digits (the FP64 accumulators are re-centred every 6
+    products): a batched rotation of nz ciphertexts, one of them all (q - 1) residues (the
+    largest lifted digits and MAC operands), equal to the oracle word for word."""
+    log_n, qb = 15, [60] + [50] * 12
+    g = H.Context(log_n, qb, 60, seed=7, arena_bytes=8 << 30)
+    o = Oracle(log_n, qb, 60, seed=7)
+    L = len(qb)
+    g.keygen([5], False)
+    o.keygen(rot_amounts=[5], relin=False)
+    hs, ocs = [], []
+    for b in range(nz):
+        if b == nz - 1:
+            data = np.stack([np.stack([np.full(o.N, q - 1, dtype=np.uint64) for q in o.q[:L]])] * 2)
+            hs.append(g.ct_import(data, L - 1, 2, 2.0 ** 40))
+            ocs.append(Ct(data.copy(), L - 1, 2.0 ** 40))
+        else:
+            hs.append(g.ct_random(300 + b, L - 1))
+            ocs.append(o.bench_ct(300 + b, L - 1))
+    outs = g.rot_left_batch(hs, 5)
+    for b, (h, oc) in enumerate(zip(outs, ocs)):
+        want = o.rot_left(oc, 5).data
+        got = g.ct_export(h)
+        assert (got == want).all(), f"ct {b}: {int((got != want).sum())} words differ"
+    g.close()
