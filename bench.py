@@ -195,25 +195,31 @@ def rotation_alg_bytes(log_n: int, l1: int, B: int) -> float:
 K7_KEYS_PER_LAUNCH = 4   # hisa.cu rotate_hoisted_multi (RK)
 
 
-def hoisted_ip_alg_bytes(log_n: int, l1: int, R: int) -> float:
-    """K7 inner products of one hoisted call with R amounts, one ciphertext: per launch (<= 4 keys)
-    D is read once (l1 (l1+1) limbs), each key (2 l1 (l1+1) limbs) streamed once, each
-    accumulator (2 (l1+1) limbs) written once."""
+def hoisted_step_bytes(log_n: int, l1: int, nct: int, R: int) -> float:
+    """Compulsory HBM bytes of one hoisted step: the R keys once
+    (2 l1 (l1+1) limbs each), the nct input ciphertexts (2 l1 limbs) and the nct R outputs."""
     limb = 8 * (1 << log_n)
-    launches = -(-R // K7_KEYS_PER_LAUNCH)
-    return (launches * l1 * (l1 + 1) + R * (2 * l1 * (l1 + 1) + 2 * (l1 + 1))) * limb
+    return (R * 2 * l1 * (l1 + 1) + nct * 2 * l1 + nct * R * 2 * l1) * limb
 
 
-def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream):
-    """Hoisted rotations (the conv pattern): each ciphertext rotated by R amounts
-    sharing one ModUp.  Returns the sub-object of the JSON line."""
+def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream, batched=True):
+    """Hoisted rotations (the conv pattern): every ciphertext rotated by R amounts sharing
+    one ModUp.  batched: one hisa_rot_left_hoisted_batch over all ciphertexts (K7 streams each
+    key once per group of 4 ciphertexts; K7 of the next key group overlaps the ModDown of the
+    current one on a second stream); else one hisa_rot_left_hoisted per ciphertext.  roofline_step
+    = compulsory bytes (keys once + inputs + outputs) / step time against measured HBM."""
     import torch
     R = len(amounts)
 
     def step():
-        for h in cts:
-            for o in ctx.rot_left_hoisted(h, amounts):
-                ctx.free(o)
+        if batched:
+            for row in ctx.rot_left_hoisted_batch(cts, amounts):
+                for o in row:
+                    ctx.free(o)
+        else:
+            for h in cts:
+                for o in ctx.rot_left_hoisted(h, amounts):
+                    ctx.free(o)
     for _ in range(warmup):
         step()
     ctx.sync()
@@ -230,13 +236,26 @@ def measure_hoisted(ctx, cts, amounts, steps, warmup, log_n, L, stream):
     ip_ms, ip_n = prof.get("ks_ip_hoisted", (0.0, 0))
     total = sum(v[0] for v in prof.values()) or 1.0
     per_launch = ip_ms / max(ip_n, 1)
-    calls = len(cts) * steps
-    alg_call = hoisted_ip_alg_bytes(log_n, L, R)
-    alg = alg_call * calls / max(ip_n, 1)           # algorithmic bytes per launch
+    nct = len(cts)
+    # K7's algorithmic bytes: per launch (<= 4 ciphertexts x <= 4 keys) D of each ciphertext once,
+    # each key once, each accumulator written once
+    limb = 8 * (1 << log_n)
+    cg = min(4, nct) if batched else 1
+    k7_bytes_step = (-(-R // K7_KEYS_PER_LAUNCH)) * nct * L * (L + 1) * limb + \
+        (-(-nct // cg)) * R * 2 * L * (L + 1) * limb + nct * R * 2 * (L + 1) * limb
+    alg = k7_bytes_step * steps / max(ip_n, 1)
     hbm_peak = _hbm_peak()
-    rot = len(cts) * R * steps
-    return {"value": rot / (ms / 1e3), "unit": "rot/s", "amounts_per_modup": R, "ciphertexts": len(cts),
+    step_bytes = hoisted_step_bytes(log_n, L, nct, R)
+    step_gbs = step_bytes * steps / (ms / 1e3) / 1e9
+    rot = nct * R * steps
+    return {"value": rot / (ms / 1e3), "unit": "rot/s", "amounts_per_modup": R, "ciphertexts": nct,
+            "call": "hisa_rot_left_hoisted_batch" if batched else "hisa_rot_left_hoisted per ciphertext",
             "ms_per_step": ms / steps,
+            "roofline_step": {"bound": "hbm", "achieved": step_gbs, "peak": hbm_peak, "unit": "GB/s",
+                              "frac": step_gbs / hbm_peak, "compulsory_bytes_per_step": step_bytes,
+                              "model": "keys once + inputs + outputs (SURVEY 8d); ModUp / ModDown are FP64-bound "
+                                       "and overlap the key stream only partly",
+                              "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             "roofline": {"bound": "hbm", "kernel": "ks_ip_hoisted", "achieved": alg / (per_launch / 1e3) / 1e9,
                          "peak": hbm_peak, "unit": "GB/s", "frac": alg / (per_launch / 1e3) / 1e9 / hbm_peak,
                          "alg_bytes_per_launch": alg, "launch_ms_avg": per_launch, "share_of_step": ip_ms / total,
@@ -478,7 +497,19 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(a, k):
+    """The oracle (never tuned) rotating one top-level ciphertext on all host cores, and the same
+    on one thread (nproc, the CPU model and a single-thread number)."""
     from oracle.ckks import Oracle
     cores = os.cpu_count() or 1
     o = Oracle(a.log_n, [50] * a.limbs, 60, seed=a.seed, nthreads=cores)
@@ -487,9 +518,15 @@ def cpu_baseline(a, k):
     t0 = time.perf_counter()
     o.rot_left(ct, k)
     dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    o1 = Oracle(a.log_n, [50] * a.limbs, 60, seed=a.seed, nthreads=1)
+    o1.rot_keys, o1.s_int, o1.s_ntt, o1.pk = o.rot_keys, o.s_int, o.s_ntt, o.pk
+    t0 = time.perf_counter()
+    o1.rot_left(ct, k)
+    dt1 = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "single_thread": {"value": 1.0 / dt1, "unit": UNIT, "cores": 1},
             "sample": f"1 top-level rotation of 1 ciphertext (N=2^{a.log_n}, L={a.limbs}), "
-                      f"keygen excluded, {dt:.1f} s"}
+                      f"keygen excluded, {dt:.1f} s on {cores} threads, {dt1:.1f} s on 1"}
 
 
 # ------------------------------------------------------------------------------ GPU arm
@@ -681,12 +718,20 @@ def main():
         import synth as _s
         rng = _s.rng(a.seed, 11, log_n, L)
         amounts = sorted({int(x) for x in rng.integers(1, N // 2, size=a.hoist_r)})
-        ctx.keygen(amounts, False)
-        hoisted = measure_hoisted(ctx, cts[:2], amounts, max(2, a.steps // 2), a.warmup, log_n, L, stream)
+        amounts24 = sorted({int(x) for x in rng.integers(1, N // 2, size=24)})
+        ctx.keygen(sorted(set(amounts) | set(amounts24)), False)
+        hsteps = max(2, a.steps // 2)
+        # the conv pattern: all B ciphertexts x R amounts through the batched call (headline),
+        # plus one ciphertext by the 3x3 (8) and 5x5 (24) tap counts
+        hoisted = measure_hoisted(ctx, cts, amounts, hsteps, a.warmup, log_n, L, stream, batched=True)
+        hoisted["single_ct"] = [measure_hoisted(ctx, cts[:1], am, hsteps, a.warmup, log_n, L, stream, batched=False)
+                                for am in (amounts, amounts24)]
+        for v in hoisted["single_ct"]:
+            v.pop("kernels", None)
         if dist:
             t = torch.tensor([hoisted["ms_per_step"]], device=f"cuda:{local}", dtype=torch.float64)
             _allreduce_max(t)
-            hoisted["value"] = world * len(cts[:2]) * len(amounts) / (float(t.item()) / 1e3)
+            hoisted["value"] = world * len(cts) * len(amounts) / (float(t.item()) / 1e3)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -58,9 +58,18 @@ __device__ __forceinline__ void mma_u8(uint32_t d_tmem, uint64_t a, uint64_t b, 
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// set by a wait that exceeded its wall-clock budget; read (and cleared) by the host after the
+// launch's synchronisation -> HISA_E_CUDA (a __trap would poison the whole CUDA context, PyTorch's
+// included, and clock64 keeps counting while a CTA is time-sliced out)
+__device__ int g_ctc_timeout;
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
-    const long long t0 = clock64();
+    const uint64_t t0 = globaltimer_ns();
     while (!done) {
         asm volatile(
             "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
@@ -68,7 +77,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
             : "=r"(done)
             : "r"(bar), "r"(phase)
             : "memory");
-        if (!done && clock64() - t0 > (1ll << 32)) __trap();   // ~2 s: never hang the device, fail loudly
+        if (!done && globaltimer_ns() - t0 > 10000000000ull) {   // 10 s: flag it, never hang the device
+            atomicExch(&g_ctc_timeout, 1);
+            return;
+        }
     }
 }
 __device__ __forceinline__ uint32_t pick_byte(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t i) {
@@ -263,6 +275,16 @@ cudaError_t launch_conv_tc_wimg(const double* W, double ps, int T, int OC, int n
     const long long total = (long long)l1 * n_oct * n_chunks * CTC_BIMG;
     k_conv_tc_wimg<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(W, ps, T, OC, n_oct, n_chunks, mods, Pl, img, total);
     return cudaGetLastError();
+}
+
+bool conv_tc_timed_out() {
+    int v = 0;
+    cudaMemcpyFromSymbol(&v, g_ctc_timeout, sizeof v);
+    if (v) {
+        const int z = 0;
+        cudaMemcpyToSymbol(g_ctc_timeout, &z, sizeof z);
+    }
+    return v != 0;
 }
 
 size_t conv_tc_smem_bytes(int T) { return 2 * (8 * CTC_PLANE + CTC_MAXG * CTC_BIMG) + (size_t)T * sizeof(void*); }

@@ -187,6 +187,7 @@ struct hisa_ctx {
     // its FP64 rows); fork/join through events, created on first use
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_k7[2] = {nullptr, nullptr}, ev_md[2] = {nullptr, nullptr};   // hoisted pipeline
     bool poisoned = false;
     Arena arena;
     bool has_arena = false;
@@ -245,6 +246,9 @@ struct hisa_ctx {
         t.modd = d_modd;
         t.ninv_d = d_ninv_d;
         t.f64_max_q = f64_max_q;
+        t.fp_mods = 0;
+        for (size_t i = 0; i < mod.size() && i < 64; i++)
+            if ((double)mod[i] < f64_max_q) t.fp_mods |= 1ull << i;
         t.log_n = log_n;
         return t;
     }
@@ -277,6 +281,17 @@ static void dfree(hisa_ctx* c, void* p) {
 template <class T>
 static T* dalloc_t(hisa_ctx* c, size_t n) { return (T*)dalloc(c, n * sizeof(T)); }
 
+// frees its allocations when the scope ends (scratch), or on an early error return only (outputs:
+// keep() hands them to the caller) -- no arena leak on a failing call
+struct DGuard {
+    hisa_ctx* c;
+    std::vector<void*> p;
+    explicit DGuard(hisa_ctx* c_) : c(c_) {}
+    template <class T> T* add(T* x) { if (x) p.push_back((void*)x); return x; }
+    void keep() { p.clear(); }
+    ~DGuard() { for (void* x : p) dfree(c, x); }
+};
+
 #define CK(call)                                                                          \
     do {                                                                                  \
         cudaError_t e_ = (call);                                                          \
@@ -307,18 +322,20 @@ struct ProfScope {
     hisa_ctx* c;
     hisa_ctx::ProfRec r;
     bool on;
-    ProfScope(hisa_ctx* c_, const char* name) : c(c_), on(c_->prof_on) {
+    cudaStream_t st;
+    ProfScope(hisa_ctx* c_, const char* name, cudaStream_t s = nullptr)
+        : c(c_), on(c_->prof_on), st(s ? s : c_->stream) {
         c->launches++;
         if (on) {
             r.name = name;
             r.a = take_event(c);
             r.b = take_event(c);
-            cudaEventRecord(r.a, c->stream);
+            cudaEventRecord(r.a, st);
         }
     }
     ~ProfScope() {
         if (on) {
-            cudaEventRecord(r.b, c->stream);
+            cudaEventRecord(r.b, st);
             c->prof.push_back(r);
         }
     }
@@ -328,6 +345,12 @@ struct ProfScope {
     do {                               \
         ProfScope ps_(c, name);        \
         CK(call);                      \
+    } while (0)
+// the same for a launch on another stream (timed there)
+#define KLS(name, stream, call)          \
+    do {                                 \
+        ProfScope ps_(c, name, stream);  \
+        CK(call);                        \
     } while (0)
 
 // ---- handle table ----
@@ -534,8 +557,8 @@ extern "C" int hisa_ctx_destroy(hisa_ctx* c) {
     }
     for (void* q : c->table_allocs) cudaFree(q);
     if (c->side) cudaStreamDestroy(c->side);
-    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    for (cudaEvent_t e : {c->ev_fork, c->ev_join, c->ev_k7[0], c->ev_k7[1], c->ev_md[0], c->ev_md[1]})
+        if (e) cudaEventDestroy(e);
     cudaGetLastError();
     delete c;
     return HISA_OK;
@@ -1297,6 +1320,14 @@ static int ks_chunk(const hisa_ctx* c, int level) {
     return (int)n;
 }
 
+static int ensure_side(hisa_ctx* c) {
+    if (c->side) return HISA_OK;
+    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&c->ev_fork, &c->ev_join, &c->ev_k7[0], &c->ev_k7[1], &c->ev_md[0], &c->ev_md[1]})
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    return HISA_OK;
+}
+
 // key switch of nz digits under ONE key: ModUp pass 1 -> fused pass 2 + key inner product (K4,
 // D never stored in NTT form) -> ModDown
 static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, int kL, const KsBatch& kb) {
@@ -1304,7 +1335,8 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, int kL
     const long long N = (long long)c->N;
     // scratch per ciphertext: dtil l1, T1 l1*l2, acc 2*l2, ptmp 2, md 2*l1
     const size_t per = (size_t)N * ((size_t)l1 + (size_t)l1 * l2 + 2 * l2 + 2 + 2 * l1);
-    uint64_t* scratch = dalloc_t<uint64_t>(c, per * nz);
+    DGuard guard(c);
+    uint64_t* scratch = guard.add(dalloc_t<uint64_t>(c, per * nz));
     if (!scratch) return fail(HISA_E_OOM, "key-switch scratch (%zu MiB)", per * nz * 8 >> 20);
     uint64_t *dtil[MAXB], *t1[MAXB], *acc[MAXB], *ptmp[MAXB], *md[MAXB];
     for (int z = 0; z < nz; z++) {
@@ -1329,17 +1361,12 @@ static int keyswitch(hisa_ctx* c, int nz, int level, const uint64_t* key, int kL
             if ((double)c->mod[kj.mod_map[ri]] < c->f64_max_q) kj.fp_rows |= 1ull << ri;
         }
         Tables tb = c->tables();
-        if (!c->side) {
-            CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-            CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-        }
+        RET(ensure_side(c));
         const SideStream side{c->side, c->ev_fork, c->ev_join};
         KL("ks_ip_rows", launch_ks_ip(kj, tb, nz, c->stream, &side));
     }
     RET(ks_moddown(c, nz, level, acc, ptmp, md, kb));
-    dfree(c, scratch);
-    return HISA_OK;
+    return HISA_OK;   // guard frees the scratch
 }
 
 extern "C" int hisa_relinearize(hisa_ctx* c, hisa_ct h) {
@@ -1464,14 +1491,15 @@ static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_
     const long long N = (long long)c->N;
     RET(rot_key_check(c, k, level));
     const hisa_ctx::KeyRec& key = c->rot_keys[k];
-    uint64_t* pre = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N * nz);
+    DGuard scratch(c), outputs(c);
+    uint64_t* pre = scratch.add(dalloc_t<uint64_t>(c, (size_t)2 * l1 * N * nz));
     if (!pre) return fail(HISA_E_OOM, "rotation scratch");
     const uint64_t* pres[MAXB];
     uint64_t gs[MAXB];
     KsBatch kb;
     memset(&kb, 0, sizeof kb);
     for (int z = 0; z < nz; z++) {
-        outs[z] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        outs[z] = outputs.add(dalloc_t<uint64_t>(c, (size_t)2 * l1 * N));
         if (!outs[z]) return fail(HISA_E_OOM, "rotation output");
         kb.d[z] = in[z]->ptr + l1 * N;
         kb.out[z] = pre + (size_t)2 * l1 * N * z;
@@ -1490,13 +1518,16 @@ static int rotate_batch(hisa_ctx* c, Obj* const* in, int nz, uint64_t k, uint64_
     } else {
         KL("automorphism", launch_automorphism(pres, outs, nz, 2 * l1, c->log_n, gs, c->stream));
     }
-    dfree(c, pre);
+    outputs.keep();
     return HISA_OK;
 }
 
 // hoisted rotations of nct ciphertexts (one level) by the same n non-zero amounts: batched ModUp
 // (nz ciphertexts per launch), K7 over groups of <= 4 ciphertexts x <= 4 keys (each key word
 // streamed once per group), batched ModDown and permutation.  outs[i * n + r] = rot(in_i, ks[r]).
+// Pipeline: K7 (HBM-bound: the key stream) of key group g + 1 runs on the side stream while the
+// ModDown + permutation (FP64-bound) of group g runs on the main stream, through two accumulator
+// buffers -- the step costs about max(key stream, ModDown) per group instead of their sum.
 static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint64_t* ks, int n, uint64_t** outs) {
     const int level = os[0]->level, l1 = level + 1, l2 = level + 2, L = c->L;
     const long long N = (long long)c->N;
@@ -1504,14 +1535,21 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
     const size_t per_out = (size_t)N * (2 * l2 + 2 + 2 * l1 + 2 * l1);           // acc, ptmp, md, pre
     constexpr int RK = 4;                                                         // keys per K7 launch
     const size_t budget = (size_t)6 << 30;
-    int ct_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)MAXB, budget / ((per_ct + RK * per_out) * 8)));
+    int ct_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)MAXB, budget / ((per_ct + 2 * RK * per_out) * 8)));
     ct_chunk = std::min(ct_chunk, nct);
+    DGuard outputs(c), sguard(c);
     for (int i = 0; i < nct * n; i++) {
-        outs[i] = dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        outs[i] = outputs.add(dalloc_t<uint64_t>(c, (size_t)2 * l1 * N));
         if (!outs[i]) return fail(HISA_E_OOM, "rotation output");
     }
-    uint64_t* scratch = dalloc_t<uint64_t>(c, per_ct * ct_chunk + per_out * (size_t)ct_chunk * RK);
+    uint64_t* scratch = sguard.add(dalloc_t<uint64_t>(c, per_ct * ct_chunk + 2 * per_out * (size_t)ct_chunk * RK));
     if (!scratch) return fail(HISA_E_OOM, "hoisted rotation scratch");
+    RET(ensure_side(c));
+#ifndef HOIST_PIPE
+#define HOIST_PIPE 1   // 0: K7 on the main stream (side builds for A/B timing only)
+#endif
+    cudaStream_t k7s = HOIST_PIPE ? c->side : c->stream;
+    const int ngroups = (n + RK - 1) / RK;
     for (int c0 = 0; c0 < nct; c0 += ct_chunk) {
         const int nc = std::min(ct_chunk, nct - c0);
         uint64_t *dtil[MAXB], *D[MAXB];
@@ -1533,11 +1571,14 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
             Tables tb = c->tables();
             KL("ks_modup_rows", launch_fwd_pass2(j, tb, l1 * l2, nc, false, c->stream));
         }
-        uint64_t* outbase = scratch + per_ct * ct_chunk;
-        for (int r0 = 0; r0 < n; r0 += RK) {
-            const int R = std::min(RK, n - r0);
-            // per-output scratch: output (z, r) at index z * R + r
-            auto acc_of = [&](int z, int r) { return outbase + per_out * (size_t)(z * R + r); };
+        // side stream: starts after the ModUp; main stream: after the last ModDown, the scratch
+        // (D, accumulators) of this chunk may be reused by the next
+        CK(cudaEventRecord(c->ev_fork, c->stream));
+        CK(cudaStreamWaitEvent(k7s, c->ev_fork, 0));
+        auto outbase = [&](int buf) { return scratch + per_ct * ct_chunk + (size_t)buf * per_out * ct_chunk * RK; };
+        auto k7 = [&](int gi) -> int {   // K7 of key group gi into buffer gi % 2, on the side stream
+            const int r0 = gi * RK, R = std::min(RK, n - r0), buf = gi & 1;
+            if (gi >= 2) CK(cudaStreamWaitEvent(k7s, c->ev_md[buf], 0));   // ModDown of gi - 2 read it
             for (int g0 = 0; g0 < nc; g0 += MAXCG) {
                 KsHoistMultiJob hj;
                 memset(&hj, 0, sizeof hj);
@@ -1545,7 +1586,7 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
                 for (int cg = 0; cg < hj.cg; cg++) {
                     hj.D[cg] = D[g0 + cg];
                     hj.diag[cg] = d1[g0 + cg];
-                    for (int r = 0; r < R; r++) hj.acc[cg][r] = acc_of(g0 + cg, r);
+                    for (int r = 0; r < R; r++) hj.acc[cg][r] = outbase(buf) + per_out * (size_t)((g0 + cg) * R + r);
                 }
                 for (int r = 0; r < R; r++) {
                     hj.key[r] = c->rot_keys[ks[r0 + r]].p;
@@ -1554,8 +1595,16 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
                 hj.l1 = l1;
                 hj.L = L;
                 for (int ri = 0; ri < l2; ri++) hj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
-                KL("ks_ip_hoisted", launch_ks_ip_hoisted_multi(hj, R, c->d_mods, c->log_n, c->stream));
+                KLS("ks_ip_hoisted", k7s, launch_ks_ip_hoisted_multi(hj, R, c->d_mods, c->log_n, k7s));
             }
+            CK(cudaEventRecord(c->ev_k7[buf], k7s));
+            return HISA_OK;
+        };
+        RET(k7(0));
+        for (int gi = 0; gi < ngroups; gi++) {
+            if (gi + 1 < ngroups) RET(k7(gi + 1));
+            const int r0 = gi * RK, R = std::min(RK, n - r0), buf = gi & 1;
+            CK(cudaStreamWaitEvent(c->stream, c->ev_k7[buf], 0));
             const int nout = nc * R;
             for (int o0 = 0; o0 < nout; o0 += MAXB) {
                 const int m = std::min(MAXB, nout - o0);
@@ -1566,7 +1615,7 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
                 memset(&kb, 0, sizeof kb);
                 for (int q = 0; q < m; q++) {
                     const int o = o0 + q, z = o / R, r = o % R;
-                    uint64_t* sp = acc_of(z, r);
+                    uint64_t* sp = outbase(buf) + per_out * (size_t)(z * R + r);
                     acc[q] = sp; sp += (size_t)2 * l2 * N;
                     ptmp[q] = sp; sp += (size_t)2 * N;
                     md[q] = sp; sp += (size_t)2 * l1 * N;
@@ -1585,9 +1634,10 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
                 }
                 KL("automorphism", launch_automorphism(pres, dsts, m, 2 * l1, c->log_n, gs, c->stream));
             }
+            CK(cudaEventRecord(c->ev_md[buf], c->stream));
         }
     }
-    dfree(c, scratch);
+    outputs.keep();
     return HISA_OK;
 }
 
@@ -2056,15 +2106,16 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
     const bool use_tc = conv_tc_enabled() && N % 128 == 0 && T <= 4096;
     if (!use_tc && (size_t)T * sizeof(void*) + (size_t)CONV_OT * CONV_TT * 8 > 200 * 1024)
         return fail(HISA_E_PARAMS, "conv accumulation: T = %zu inputs too many", T);
+    DGuard outputs(c), scratch(c);
     std::vector<uint64_t*> optr(OC);
     for (size_t o = 0; o < OC; o++) {
-        optr[o] = dev_out ? dev_out + (size_t)o * 2 * l1 * N : dalloc_t<uint64_t>(c, (size_t)2 * l1 * N);
+        optr[o] = dev_out ? dev_out + (size_t)o * 2 * l1 * N : outputs.add(dalloc_t<uint64_t>(c, (size_t)2 * l1 * N));
         if (!optr[o]) return fail(HISA_E_OOM, "conv outputs");
     }
     std::vector<const uint64_t*> iptr(T);
     for (size_t t = 0; t < T; t++) iptr[t] = objs[t]->ptr;
-    const uint64_t** dip = (const uint64_t**)dalloc(c, T * sizeof(void*));
-    uint64_t** dop = (uint64_t**)dalloc(c, OC * sizeof(void*));
+    const uint64_t** dip = scratch.add((const uint64_t**)dalloc(c, T * sizeof(void*)));
+    uint64_t** dop = scratch.add((uint64_t**)dalloc(c, OC * sizeof(void*)));
     if (!dip || !dop) return fail(HISA_E_OOM, "conv scratch");
     CK(cudaMemcpyAsync(dip, iptr.data(), T * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(dop, optr.data(), OC * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
@@ -2083,9 +2134,9 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
             tj.limb_map[i] = (uint8_t)i;
         }
         const size_t img_bytes = (size_t)l1 * n_oct * n_chunks * 8 * 512;
-        uint8_t* dimg = (uint8_t*)dalloc(c, img_bytes);
-        double* dW = dalloc_t<double>(c, OC * T);
-        uint8_t* dP = (uint8_t*)dalloc(c, MAXL);
+        uint8_t* dimg = scratch.add((uint8_t*)dalloc(c, img_bytes));
+        double* dW = scratch.add(dalloc_t<double>(c, OC * T));
+        uint8_t* dP = scratch.add((uint8_t*)dalloc(c, MAXL));
         if (!dimg || !dW || !dP) return fail(HISA_E_OOM, "conv weight image");
         CK(cudaMemcpyAsync(dW, W, OC * T * sizeof(double), cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(dP, tj.P, MAXL, cudaMemcpyHostToDevice, c->stream));
@@ -2095,11 +2146,11 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
             CK(launch_conv_tc(dip, dop, dimg, tj, l1, c->d_mods, c->stream));
         }
         CK(cudaStreamSynchronize(c->stream));   // host staging vectors must outlive the copies
-        dfree(c, dimg);
-        dfree(c, (void*)dW);
-        dfree(c, (void*)dP);
-        dfree(c, (void*)dip);
-        dfree(c, (void*)dop);
+        if (conv_tc_timed_out()) {
+            c->poisoned = true;
+            return fail(HISA_E_CUDA, "conv accumulation: tensor-core mbarrier wait timed out");
+        }
+        outputs.keep();   // scratch (image, weights, pointer arrays) freed by its guard
         if (outs)
             for (size_t o = 0; o < OC; o++) outs[o] = new_handle(c, OBJ_CT, optr[o], level, 2, objs[0]->scale * ps);
         return HISA_OK;
@@ -2113,7 +2164,7 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
                 wres[((size_t)i * OC + o) * T + t] = (uint64_t)(((__int128)X % (__int128)q + q) % q);
             }
         }
-    uint64_t* dw = dalloc_t<uint64_t>(c, wres.size());
+    uint64_t* dw = scratch.add(dalloc_t<uint64_t>(c, wres.size()));
     if (!dw) return fail(HISA_E_OOM, "conv scratch");
     CK(cudaMemcpyAsync(dw, wres.data(), wres.size() * 8, cudaMemcpyHostToDevice, c->stream));
     uint64_t qmax = 0;
@@ -2145,9 +2196,7 @@ static int conv_acc_common(hisa_ctx* c, const hisa_ct* in, size_t T, const doubl
         CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(c->stream));   // host staging vectors must outlive the copies
-    dfree(c, dw);
-    dfree(c, (void*)dip);
-    dfree(c, (void*)dop);
+    outputs.keep();
     if (outs)
         for (size_t o = 0; o < OC; o++) outs[o] = new_handle(c, OBJ_CT, optr[o], level, 2, objs[0]->scale * ps);
     return HISA_OK;

@@ -54,6 +54,7 @@ struct Tables {
     const double2* modd;        // [mod] (q, fl(1/q))
     const double* ninv_d;       // [mod] N^-1 mod q as double
     double f64_max_q;           // moduli below this run the FP64 engine (0 disables it)
+    uint64_t fp_mods;           // bit mi: modulus mi runs the FP64 engine (host-computed, no I2F)
     int log_n;
 };
 

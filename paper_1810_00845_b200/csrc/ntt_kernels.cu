@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols(PassJob job, Tables tb) 
 // four radix-2 stages u0 .. u0 + 3 of a 256-point pass on 16 register operands (stride 8 >> uu);
 // twiddle index 2^(s0+u) + (high << u) + (ohigh << uu) + k as in fwd_engine.  FP64 stages re-centre
 // X at u % 3 == 0 only (outputs feed a pass that starts with a full stage, or a full reduction).
-template <typename V, bool FP>
+template <typename V, bool FP, bool SMEM_TW = false>
 __device__ __forceinline__ void col_phase16(V (&r)[16], int u0, int ohigh, const void* twp, double q, double qinv,
                                             uint64_t qi, int s0 = 0, uint32_t high = 0) {
 #pragma unroll
@@ -145,7 +145,8 @@ __device__ __forceinline__ void col_phase16(V (&r)[16], int u0, int ohigh, const
         for (int k = 0; k < 8; k++) {
             if (k >= (1 << uu)) break;
             if constexpr (FP) {
-                const double W = __ldg(reinterpret_cast<const double*>(twp) + tbase + k);
+                const double W = SMEM_TW ? reinterpret_cast<const double*>(twp)[tbase + k]
+                                         : __ldg(reinterpret_cast<const double*>(twp) + tbase + k);
 #pragma unroll
                 for (int e0 = 0; e0 < 8; e0++) {
                     if (e0 >= dist) break;
@@ -236,6 +237,133 @@ __global__ void __launch_bounds__(256, MINB) k_fwd_cols_r16(PassJob job, Tables 
     uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b;
     if (use_f64(md.q, tb)) fwd_cols_r16_body<true, LOADMODE>(job, tb, src, dst, mi, md, a, col0, M2);
     else fwd_cols_r16_body<false, LOADMODE>(job, tb, src, dst, mi, md, a, col0, M2);
+}
+
+// ------------------------------------------------------------------------------------------
+// ModUp pass 1 at M1 = 256 (N = 2^16), looped over output primes: one CTA per (16-column block,
+// digit a, chunk of output primes, ciphertext) loads its 16 x 256 coefficients of digit a ONCE,
+// lifts them once (centred w.r.t. q_a: an integer of magnitude < q_a / 2, held exactly as a
+// double when q_a < 2^50), then runs the first-pass NTT for every output prime b of its chunk
+// (b != a) from registers -- instead of one CTA per (a, b) limb that reloads and re-lifts the
+// same digit l + 1 times.  ncu (profiles/r2_ncu_modup_v1.txt): the per-limb kernel spent as many
+// issue slots on loads, 64-bit addressing, the lift's compare/select and per-CTA setup as on its
+// FP64 butterflies.  Wide source digits (q_a >= 2^50: the 60-bit q_0 of configs 1, 3-5) lift
+// per output prime with the integer lift (exact mod q_b), as before.
+// ------------------------------------------------------------------------------------------
+#ifndef MODUP_MINB
+#define MODUP_MINB 3
+#endif
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_modup_cols16(PassJob job, Tables tb, int bchunk, int nbc) {
+    using G = Geo<8, 4>;
+    constexpr int M2 = 256;
+    extern __shared__ uint64_t sm[];
+    const int a = blockIdx.y / nbc, bc = blockIdx.y % nbc;
+    const int z = blockIdx.z;
+    const int col0 = blockIdx.x * 16;
+    const int g = threadIdx.x & 15, t = threadIdx.x >> 4;
+    const uint64_t* src = job.src[z] + a * job.src_a + col0 + g + (long long)t * M2;
+    const uint64_t Qs = tb.mods[job.smod_map[a]].q;
+    const bool fast_lift = (tb.fp_mods >> job.smod_map[a]) & 1;
+    // raw residues (wide source) or the centred lift as exact doubles (fast path), 16 per thread
+    uint64_t v[16];
+#pragma unroll
+    for (int e = 0; e < 16; e++) v[e] = __ldg(src + (long long)16 * e * M2);
+    if (fast_lift) {
+        const uint64_t half = Qs >> 1;
+#pragma unroll
+        for (int e = 0; e < 16; e++) {
+            // signed s = v - Qs [v > Qs/2], |s| < 2^49, exact as a double via the 1.5 2^52 bias
+            const long long s = (long long)v[e] - (v[e] > half ? (long long)Qs : 0ll);
+            v[e] = (uint64_t)__double_as_longlong(
+                __dsub_rn(__longlong_as_double(s + 0x4338000000000000ll), 6755399441055744.0));
+        }
+    }
+    const int b_end = min(job.nb, (bc + 1) * bchunk);
+    // FP64 output primes first (the lifted digit stays in registers); each prime's 255 pass-1
+    // twiddles are staged into shared memory by cp.async one prime ahead (triple buffer: the
+    // buffer being filled is never one a lagging thread still reads)
+    double* tws = reinterpret_cast<double*>(sm + 16 * G::STRIDE);   // [3][256] after the tile
+    auto next_fp = [&](int b) {
+        for (; b < b_end; b++)
+            if (!(job.skip_diag && b == a) && ((tb.fp_mods >> job.mod_map[b]) & 1)) return b;
+        return b_end;
+    };
+    auto issue_tw = [&](int b, int buf) {
+        const double* twg = tb.fwd_d + ((long long)job.mod_map[b] << tb.log_n);
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(tws + buf * 256 + threadIdx.x);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(twg + threadIdx.x) : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    int bcur = next_fp(bc * bchunk);
+    if (bcur < b_end) issue_tw(bcur, 0);
+    for (int i = 0; bcur < b_end; i++) {
+        const int bnext = next_fp(bcur + 1);
+        if (bnext < b_end) {
+            issue_tw(bnext, (i + 1) % 3);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        const int b = bcur;
+        const int mi = job.mod_map[b];
+        uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + col0 + g;
+        double r[16];
+        if (fast_lift) {
+#pragma unroll
+            for (int e = 0; e < 16; e++) r[e] = __longlong_as_double((long long)v[e]);
+        } else {
+            const Mod md = tb.mods[mi];
+#pragma unroll
+            for (int e = 0; e < 16; e++) r[e] = u2d(lift_centered(v[e], Qs, md));
+        }
+        const double2 qd = tb.modd[mi];
+        const double* twp = tws + (i % 3) * 256;
+        double* tile = reinterpret_cast<double*>(sm);
+        __syncthreads();   // this prime's twiddles landed; the previous prime's exchange reads are done
+        col_phase16<double, true, true>(r, 0, 0, twp, qd.x, qd.y, 0);
+#pragma unroll
+        for (int e = 0; e < 16; e++) tile[G::addr(g, t + 16 * e)] = r[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 16; e++) r[e] = tile[G::addr(g, 16 * t + e)];
+        col_phase16<double, true, true>(r, 4, t, twp, qd.x, qd.y, 0);
+#pragma unroll
+        for (int e = 0; e < 16; e++) dst[(long long)(16 * t + e) * M2] = (uint64_t)__double_as_longlong(r[e]);
+        bcur = bnext;
+    }
+    // ... then the integer-engine ones (60-bit: the special prime), reloading the digit (L1 / L2)
+    for (int b = bc * bchunk; b < b_end; b++) {
+        if (job.skip_diag && b == a) continue;
+        const int mi = job.mod_map[b];
+        if ((tb.fp_mods >> mi) & 1) continue;
+        const Mod md = tb.mods[mi];
+        uint64_t* dst = job.dst[z] + a * job.dst_a + b * job.dst_b + col0 + g;
+        uint64_t r[16];
+        if (Qs < md.q) {   // a narrower source (every q_j into the 60-bit p): the centred lift is s or s + q
+            const uint64_t half = Qs >> 1, dq = md.q - Qs;
+#pragma unroll
+            for (int e = 0; e < 16; e++) {
+                const uint64_t w = __ldg(src + (long long)16 * e * M2);
+                r[e] = w > half ? w + dq : w;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; e++) r[e] = lift_centered(__ldg(src + (long long)16 * e * M2), Qs, md);
+        }
+        const void* twp = tb.fwd + ((long long)mi << tb.log_n);
+        col_phase16<uint64_t, false>(r, 0, 0, twp, 0.0, 0.0, md.q);
+        uint64_t* tile = sm;
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 16; e++) tile[G::addr(g, t + 16 * e)] = r[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 16; e++) r[e] = tile[G::addr(g, 16 * t + e)];
+        col_phase16<uint64_t, false>(r, 4, t, twp, 0.0, 0.0, md.q);
+#pragma unroll
+        for (int e = 0; e < 16; e++) dst[(long long)(16 * t + e) * M2] = r[e];
+    }
 }
 
 // forward pass 2 for M2 = 256, radix-16, register-direct load: thread (g = tid / 16, t = tid % 16)
@@ -614,6 +742,17 @@ static cudaError_t fwd_cols_v(const PassJob& job, const Tables& tb, int nlimbs, 
     constexpr int FULL = 256 / Geo<LOG_M, LOG_R>::T;
     const bool full = threads == 256;
     if constexpr (LOG_M == 8 && LOG_R == 4) {
+        if (full && lift && job.nb > 1 && tb.log_n == 16) {
+            // ModUp (and any multi-target lift): one CTA per (column block, source limb, chunk of
+            // output primes); chunks sized for >= ~4 CTAs per SM-slot wave
+            const int na = nlimbs / job.nb;
+            int bchunk = job.nb;
+            while (bchunk > 4 && (long long)gx * na * ((job.nb + bchunk - 1) / bchunk) * nz < 4 * 148 * 4) bchunk = (bchunk + 1) / 2;
+            const int nbc = (job.nb + bchunk - 1) / bchunk;
+            dim3 g2(gx, na * nbc, nz);
+            k_modup_cols16<MODUP_MINB><<<g2, 256, smem + 3 * 256 * sizeof(double), st>>>(job, tb, bchunk, nbc);
+            return cudaGetLastError();
+        }
         if (full) {   // register-direct radix-16 form
             if (lift) k_fwd_cols_r16<LOAD_LIFT, 4><<<grid, 256, smem, st>>>(job, tb);   // MINB 3: slower
             else k_fwd_cols_r16<LOAD_PLAIN, 4><<<grid, 256, smem, st>>>(job, tb);
