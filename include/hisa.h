@@ -147,8 +147,13 @@ int hisa_encode(hisa_ctx* ctx, const double* v, size_t n, double scale, int leve
  * weight / mask plaintexts (once per model). */
 int hisa_encode_batch(hisa_ctx* ctx, const double* v, size_t n_per, size_t count, double scale, int level,
                       hisa_pt* outs);
-/* slot values from limb 0 (A13): needs |value| * scale < q_0 / 2; out[0..n) */
+/* slot values from limb 0 (A13): needs |value| * scale < q_0 / 2; out[0..n), the real
+ * parts (A2).  On the GPU: INTT of limb 0, centred lift, twist, N-point double-precision FFT,
+ * gather (decode is approximate by definition: error ~ log2(N) 2^-53 max|m_t| / scale).
+ * Synchronising; HISA_E_CAPACITY for n > N/2. */
 int hisa_decode(hisa_ctx* ctx, hisa_pt pt, double* out, size_t n);
+/* count plaintexts at once: out[count][n] row-major, each row as hisa_decode (batched launches) */
+int hisa_decode_batch(hisa_ctx* ctx, const hisa_pt* pts, size_t count, double* out, size_t n);
 /* rotate left/right by k slots: out[i] = in[(i + k) mod N/2] (A15); k = 0 copies */
 int hisa_rot_left(hisa_ctx* ctx, hisa_ct ct, int64_t k, hisa_ct* out);
 int hisa_rot_right(hisa_ctx* ctx, hisa_ct ct, int64_t k, hisa_ct* out);

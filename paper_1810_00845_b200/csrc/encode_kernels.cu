@@ -133,4 +133,70 @@ cudaError_t launch_encode_fft(const double* z_dev, size_t n_per, size_t count, c
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// GPU decode (NEXT-4; A2, A13): from the limb-0 coefficients m_t (after the INTT),
+// centred mod q_0, the slot values are z_j = (1/Delta) sum_t m_t zeta^(5^j t), zeta = e^{i pi / N}
+// = (1/Delta) B[(5^j - 1) / 2] with B[k] = sum_t (m_t e^{i pi t / N}) e^{+2 pi i k t / N}: a twist,
+// one N-point complex FFT (double precision: decode is approximate by definition, the error is
+// ~log2(N) 2^-53 max|m_t| / Delta) and a gather of the real parts.
+// ------------------------------------------------------------------------------------------
+struct cdbl { double re, im; };
+
+__global__ void k_dec_twist(const uint64_t* const* m, uint64_t q0, const cdd* twist, cdbl* A, int log_n) {
+    const long long N = 1ll << log_n;
+    const uint64_t* mp = m[blockIdx.y];
+    cdbl* a = reinterpret_cast<cdbl*>(A) + (long long)blockIdx.y * N;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
+        const uint64_t v = mp[t];
+        const double x = v > (q0 >> 1) ? -(double)(q0 - v) : (double)v;
+        const cdd w = twist[t];
+        a[__brev((unsigned)t) >> (32 - log_n)] = cdbl{x * w.re.hi, x * w.im.hi};
+    }
+}
+
+// radix-2 DIT stage of length 2^s with w_k = root[k N / len] = e^{+2 pi i k / len}
+__global__ void k_dec_fft_stage(cdbl* A, const cdd* root, int log_n, int s) {
+    const long long N = 1ll << log_n;
+    const long long half = 1ll << (s - 1);
+    const long long step = N >> s;
+    cdbl* a = A + (long long)blockIdx.y * N;
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < N / 2; b += (long long)gridDim.x * blockDim.x) {
+        const long long grp = b / half, k = b - grp * half;
+        const long long i0 = grp * 2 * half + k, i1 = i0 + half;
+        const cdd r = root[k * step];
+        const double wr = r.re.hi, wi = r.im.hi;
+        const cdbl u = a[i0], x = a[i1];
+        const cdbl v{__fma_rn(x.re, wr, -x.im * wi), __fma_rn(x.re, wi, x.im * wr)};
+        a[i0] = cdbl{u.re + v.re, u.im + v.im};
+        a[i1] = cdbl{u.re - v.re, u.im - v.im};
+    }
+}
+
+// out[p][j] = Re B[(5^j - 1) / 2] / scale[p], j < n (pos_brv[2 j] = brv((5^j - 1) / 2))
+__global__ void k_dec_gather(const cdbl* A, const uint32_t* pos_brv, const double* inv_scale, double* out, size_t n,
+                             int log_n) {
+    const long long N = 1ll << log_n;
+    const cdbl* a = A + (long long)blockIdx.y * N;
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < n; j += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t k = __brev(pos_brv[2 * j]) >> (32 - log_n);
+        out[blockIdx.y * n + j] = a[k].re * inv_scale[blockIdx.y];
+    }
+}
+
+cudaError_t launch_decode_fft(const uint64_t* const* m_dev, size_t count, uint64_t q0, const uint32_t* pos_brv,
+                              const cdd* root, const cdd* twist, const double* inv_scale, int log_n, void* A,
+                              double* out, size_t n, cudaStream_t st) {
+    const long long N = 1ll << log_n;
+    cdbl* a = reinterpret_cast<cdbl*>(A);
+    dim3 gt((unsigned)((N + 255) / 256), (unsigned)count);
+    k_dec_twist<<<gt, 256, 0, st>>>(m_dev, q0, twist, a, log_n);
+    dim3 gf((unsigned)((N / 2 + 255) / 256), (unsigned)count);
+    for (int s = 1; s <= log_n; s++) k_dec_fft_stage<<<gf, 256, 0, st>>>(a, root, log_n, s);
+    if (n) {
+        dim3 gg((unsigned)((n + 255) / 256), (unsigned)count);
+        k_dec_gather<<<gg, 256, 0, st>>>(a, pos_brv, inv_scale, out, n, log_n);
+    }
+    return cudaGetLastError();
+}
+
 }  // namespace hisa

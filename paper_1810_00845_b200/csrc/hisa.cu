@@ -217,9 +217,6 @@ struct hisa_ctx {
     uint64_t* d_rlk = nullptr;        // [L][2][L+1][N] (relinearisation: always full)
     std::map<uint64_t, KeyRec> rot_keys;
     uint64_t enc_counter = 0;
-    // encode/decode long-double tables (built on first use): cis(2 pi k / N), k < N/2, and
-    // cis(pi t / N), t < N
-    std::vector<std::complex<long double>> enc_root, enc_twist;
     std::vector<__float128> enc_cosq;   // binary128 cos(pi e / N), e < 2N (near-tie recomputation, A7)
     uint32_t* d_enc_pos = nullptr;      // GPU encode: bit-reversed positions of the 2 x N/2 slot images
     cdd* d_enc_root = nullptr;          // e^{2 pi i k / N}, k < N/2, double-double from binary128
@@ -877,44 +874,6 @@ extern "C" int hisa_copy(hisa_ctx* c, hisa_ct h, hisa_ct* out) {
 // ============================================================================================
 // encode / decode (A7, A13): host boundary, long-double FFT, binary128 near-tie recomputation
 // ============================================================================================
-typedef std::complex<long double> cld;
-static void enc_tables(hisa_ctx* c) {
-    if (!c->enc_root.empty()) return;
-    const uint64_t N = c->N;
-    const long double pi = acosl(-1.0L);
-    c->enc_root.resize(N / 2);
-    for (uint64_t k = 0; k < N / 2; k++) {
-        const long double ang = 2.0L * pi * (long double)k / (long double)N;
-        c->enc_root[k] = cld(cosl(ang), sinl(ang));
-    }
-    c->enc_twist.resize(N);
-    for (uint64_t t = 0; t < N; t++) {
-        const long double ang = pi * (long double)t / (long double)N;
-        c->enc_twist[t] = cld(cosl(ang), sinl(ang));
-    }
-}
-// radix-2 DIT FFT in long double: a[t] <- sum_m a[m] e^{sign 2 pi i m t / n}, n = a.size() = N
-static void fft_ld(const hisa_ctx* c, std::vector<cld>& a, int sign) {
-    const size_t n = a.size();
-    int bits = 0;
-    while ((1ull << bits) < n) bits++;
-    for (size_t i = 0; i < n; i++) {
-        size_t j = h_brv((uint32_t)i, bits);
-        if (i < j) std::swap(a[i], a[j]);
-    }
-    for (size_t len = 2; len <= n; len <<= 1) {
-        const size_t half = len / 2, step = n / len;
-        for (size_t i = 0; i < n; i += len)
-            for (size_t k = 0; k < half; k++) {
-                const cld r = c->enc_root[k * step];
-                const cld w = sign < 0 ? std::conj(r) : r;
-                cld u = a[i + k], v = a[i + k + half] * w;
-                a[i + k] = u + v;
-                a[i + k + half] = u - v;
-            }
-    }
-}
-
 // one coefficient exactly (the A7 near-tie path): binary128 direct sum of v_t with a correctly
 // rounded binary128 cos table.  Its error is below E = (n + 2) 2^-112 (scale/N) sum_j |2 z_j|
 // (< 2^-36 even at |v| = 2^62, N = 2^16), so the result is round-half-away of the exact real
@@ -1091,37 +1050,54 @@ extern "C" int hisa_encode_batch(hisa_ctx* c, const double* v, size_t n_per, siz
     return HISA_OK;
 }
 
-extern "C" int hisa_decode(hisa_ctx* c, hisa_pt h, double* out, size_t n) {
+// GPU decode (NEXT-4; A2, A13): INTT of limb 0, then twist + N-point FFT + gather of
+// the slots' real parts on the device (encode_kernels.cu); out[i][j], j < n, for count plaintexts
+extern "C" int hisa_decode_batch(hisa_ctx* c, const hisa_pt* pts, size_t count, double* out, size_t n) {
     CHECK_CTX(c);
-    GET_PT(p, h);
     if (n > c->N / 2) return fail(HISA_E_CAPACITY, "n > N/2");
-    if (n && !out) return fail(HISA_E_PARAMS, "null out");
+    if (count && (!pts || (n && !out))) return fail(HISA_E_PARAMS, "null argument");
+    if (count == 0) return HISA_OK;
     const uint64_t N = c->N;
-    uint64_t* tmp = dalloc_t<uint64_t>(c, N);
-    if (!tmp) return fail(HISA_E_OOM, "decode");
-    uint8_t mm[1] = {0};
-    const uint64_t* s[1] = {p->ptr};
-    uint64_t* d[1] = {tmp};
-    RET(ntt_inv(c, s, d, 1, 1, mm));
-    std::vector<uint64_t> a(N);
-    CK(cudaMemcpyAsync(a.data(), tmp, N * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    dfree(c, tmp);
-    const uint64_t q0 = c->mod[0];
-    // G[m] = sum_t (m_t zeta^t) e^{+2 pi i m t / N};  value at zeta^(2m+1)
-    std::vector<cld> A(N);
-    enc_tables(c);
-    for (uint64_t t = 0; t < N; t++) {
-        const long double mt = a[t] > (q0 >> 1) ? -(long double)(q0 - a[t]) : (long double)a[t];
-        A[t] = mt * c->enc_twist[t];
+    std::vector<Obj*> ps(count);
+    for (size_t i = 0; i < count; i++) {
+        ps[i] = get_obj(c, pts[i], OBJ_PT);
+        if (!ps[i]) return fail(HISA_E_INVALID_HANDLE, "invalid plaintext handle at %zu", i);
     }
-    fft_ld(c, A, +1);
-    uint64_t k = 1;
-    for (size_t j = 0; j < n; j++) {
-        out[j] = (double)(A[(k - 1) / 2].real() / (long double)p->scale);
-        k = k * 5 % (2 * N);
+    RET(enc_gpu_tables(c));
+    const size_t chunk = std::min<size_t>(count, MAXB);
+    DGuard scratch(c);
+    uint64_t* tmp = scratch.add(dalloc_t<uint64_t>(c, N * chunk));
+    void* A = scratch.add(dalloc(c, N * chunk * 16));
+    double* dout = scratch.add(dalloc_t<double>(c, std::max<size_t>(1, n * chunk)));
+    double* dinv = scratch.add(dalloc_t<double>(c, chunk));
+    const uint64_t** dm = scratch.add((const uint64_t**)dalloc(c, chunk * sizeof(void*)));
+    if (!tmp || !A || !dout || !dinv || !dm) return fail(HISA_E_OOM, "decode");
+    std::vector<double> inv(chunk);
+    std::vector<const uint64_t*> mp(chunk);
+    for (size_t i0 = 0; i0 < count; i0 += chunk) {
+        const size_t m = std::min(chunk, count - i0);
+        uint8_t mm[1] = {0};
+        const uint64_t* s_[MAXB];
+        uint64_t* d_[MAXB];
+        for (size_t i = 0; i < m; i++) {
+            s_[i] = ps[i0 + i]->ptr;
+            d_[i] = tmp + i * N;
+            mp[i] = d_[i];
+            inv[i] = 1.0 / ps[i0 + i]->scale;
+        }
+        RET(ntt_inv(c, s_, d_, (int)m, 1, mm));
+        CK(cudaMemcpyAsync(dm, mp.data(), m * sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(dinv, inv.data(), m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        KL("decode", launch_decode_fft(dm, m, c->mod[0], c->d_enc_pos, c->d_enc_root, c->d_enc_twist, dinv, c->log_n,
+                                       A, dout, n, c->stream));
+        if (n) CK(cudaMemcpyAsync(out + i0 * n, dout, m * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));   // the host staging vectors are reused
     }
     return HISA_OK;
+}
+
+extern "C" int hisa_decode(hisa_ctx* c, hisa_pt h, double* out, size_t n) {
+    return hisa_decode_batch(c, &h, 1, out, n);
 }
 
 // ============================================================================================
@@ -1595,7 +1571,7 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
                 hj.l1 = l1;
                 hj.L = L;
                 for (int ri = 0; ri < l2; ri++) hj.mod_map[ri] = (uint8_t)(ri < l1 ? ri : L);
-                KLS("ks_ip_hoisted", k7s, launch_ks_ip_hoisted_multi(hj, R, c->d_mods, c->log_n, k7s));
+                KLS("ks_ip_hoisted", k7s, launch_ks_ip_hoisted_multi(hj, R, c->tables(), k7s));
             }
             CK(cudaEventRecord(c->ev_k7[buf], k7s));
             return HISA_OK;

@@ -723,13 +723,74 @@ cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_
 }
 
 // ------------------------------------------------------------------------------------------
-// K7 batched over ciphertexts: CG ciphertexts x R keys per thread-word (one word per thread),
-// 2 CG R 128-bit accumulators; the key words are loaded once for the CG ciphertexts.
+// K7: hoisted inner products, CG ciphertexts x R keys per thread-word (one word per thread).
+// FP64 output primes (q < 2^50): the multiply-accumulates run on the FP64 pipe as in K4 v6 --
+// acc += mulred(D, K), D (< q, the materialised ModUp output) and K (< q) converted exactly
+// (u2d): |mulred| <= q/2 + 1.5 2^-52 q^2 < 0.88 q, so eight products fit between re-centrings
+// (|acc| < 7.6 q < 2^53).  Two doubles per accumulator instead of a 128-bit pair: CG = 4, R = 4
+// needs 64 accumulator registers (the 128-bit form needed 255 registers, one CTA per SM, and left
+// the key stream latency-bound at ~0.4 of HBM), and the FP64 pipe's MAC rate is ~2x the integer
+// pipe's (measured: hisa_microbench_mac vs _butterfly_f64).  Integer-engine output primes (60-bit)
+// keep the 128-bit integer accumulation.
 // ------------------------------------------------------------------------------------------
+template <int CG, int R>
+__global__ void __launch_bounds__(128) k_ks_ip_hoisted_f64(KsHoistMultiJob job, Tables tb) {
+    const int ri = job.ri_list[blockIdx.y];
+    const int l1 = job.l1, l2 = l1 + 1;
+    const long long N = 1ll << tb.log_n;
+    const long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (x >= N) return;
+    const int mi = job.mod_map[ri];
+    const double2 qd = tb.modd[mi];
+    const double q = qd.x, qinv = qd.y;
+    double acc[CG][R][2];
+#pragma unroll
+    for (int c = 0; c < CG; c++)
+#pragma unroll
+        for (int k = 0; k < R; k++) { acc[c][k][0] = 0.0; acc[c][k][1] = 0.0; }
+    for (int j = 0; j < l1; j++) {
+        double d[CG];
+#pragma unroll
+        for (int c = 0; c < CG; c++) {
+            const uint64_t* src = (j == ri) ? job.diag[c] + (long long)j * N + x
+                                            : job.D[c] + ((long long)j * l2 + ri) * N + x;
+            d[c] = u2d(__ldcs(src));
+        }
+#pragma unroll
+        for (int k = 0; k < R; k++) {
+            const int kL = job.kL[k];
+            const long long kstride_p = (long long)(kL + 1) * N;
+            const uint64_t* kb = job.key[k] + j * 2 * kstride_p + (long long)(ri < l1 ? ri : kL) * N + x;
+            const double Kb = u2d(__ldcs(kb)), Ka = u2d(__ldcs(kb + kstride_p));
+#pragma unroll
+            for (int c = 0; c < CG; c++) {
+                acc[c][k][0] = __dadd_rn(acc[c][k][0], mulred(d[c], Kb, q, qinv));
+                acc[c][k][1] = __dadd_rn(acc[c][k][1], mulred(d[c], Ka, q, qinv));
+            }
+        }
+        if ((j & 7) == 7) {
+#pragma unroll
+            for (int c = 0; c < CG; c++)
+#pragma unroll
+                for (int k = 0; k < R; k++) {
+                    acc[c][k][0] = redd(acc[c][k][0], q, qinv);
+                    acc[c][k][1] = redd(acc[c][k][1], q, qinv);
+                }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < CG; c++)
+#pragma unroll
+        for (int k = 0; k < R; k++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+                __stcs(&job.acc[c][k][((long long)h * l2 + ri) * N + x], d_canon(acc[c][k][h], q, qinv));
+}
+
 template <int CG, int R>
 __global__ void __launch_bounds__(256) k_ks_ip_hoisted_multi(KsHoistMultiJob job, const Mod* __restrict__ mods,
                                                              int log_n) {
-    const int ri = blockIdx.y;
+    const int ri = job.ri_list[blockIdx.y];
     const int l1 = job.l1, l2 = l1 + 1;
     const long long N = 1ll << log_n;
     const long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -771,14 +832,35 @@ __global__ void __launch_bounds__(256) k_ks_ip_hoisted_multi(KsHoistMultiJob job
                 job.acc[c][k][((long long)h * l2 + ri) * N + x] = barrett128(acc[c][k][h].lo, acc[c][k][h].hi, md);
 }
 
-cudaError_t launch_ks_ip_hoisted_multi(const KsHoistMultiJob& job, int R, const Mod* mods, int log_n, cudaStream_t st) {
-    const long long N = 1ll << log_n;
-    dim3 grid((unsigned)((N + 255) / 256), job.l1 + 1, 1);
-#define C(CGV, RV) if (job.cg == CGV && R == RV) { k_ks_ip_hoisted_multi<CGV, RV><<<grid, 256, 0, st>>>(job, mods, log_n); return cudaGetLastError(); }
-    C(4, 1) C(4, 2) C(4, 3) C(4, 4) C(2, 1) C(2, 2) C(2, 3) C(2, 4) C(3, 1) C(3, 2) C(3, 3) C(3, 4)
-    C(1, 1) C(1, 2) C(1, 3) C(1, 4)
+cudaError_t launch_ks_ip_hoisted_multi(const KsHoistMultiJob& job_in, int R, const Tables& tb, cudaStream_t st) {
+    const long long N = 1ll << tb.log_n;
+    KsHoistMultiJob job = job_in;
+    const int l2 = job.l1 + 1;
+    uint8_t fp[MAXL], in[MAXL];
+    int nfp = 0, nint = 0;
+    for (int ri = 0; ri < l2; ri++) {
+        if ((tb.fp_mods >> job.mod_map[ri]) & 1) fp[nfp++] = (uint8_t)ri;
+        else in[nint++] = (uint8_t)ri;
+    }
+    if (nint) {
+        memcpy(job.ri_list, in, nint);
+        dim3 grid((unsigned)((N + 255) / 256), nint, 1);
+#define C(CGV, RV) if (job.cg == CGV && R == RV) { k_ks_ip_hoisted_multi<CGV, RV><<<grid, 256, 0, st>>>(job, tb.mods, tb.log_n); } else
+        C(4, 1) C(4, 2) C(4, 3) C(4, 4) C(2, 1) C(2, 2) C(2, 3) C(2, 4) C(3, 1) C(3, 2) C(3, 3) C(3, 4)
+        C(1, 1) C(1, 2) C(1, 3) C(1, 4) return cudaErrorInvalidValue;
 #undef C
-    return cudaErrorInvalidValue;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (nfp) {
+        memcpy(job.ri_list, fp, nfp);
+        dim3 grid((unsigned)((N + 127) / 128), nfp, 1);
+#define C(CGV, RV) if (job.cg == CGV && R == RV) { k_ks_ip_hoisted_f64<CGV, RV><<<grid, 128, 0, st>>>(job, tb); } else
+        C(4, 1) C(4, 2) C(4, 3) C(4, 4) C(2, 1) C(2, 2) C(2, 3) C(2, 4) C(3, 1) C(3, 2) C(3, 3) C(3, 4)
+        C(1, 1) C(1, 2) C(1, 3) C(1, 4) return cudaErrorInvalidValue;
+#undef C
+    }
+    return cudaGetLastError();
 }
 
 }  // namespace hisa

@@ -65,8 +65,9 @@ struct KsHoistMultiJob {
     int kL[MAXR];                   // q primes each key covers (truncated keys, kL >= l+1)
     int l1, L, cg;
     uint8_t mod_map[MAXL];
+    uint8_t ri_list[MAXL];          // grid.y -> output prime (filled by the launcher)
 };
-cudaError_t launch_ks_ip_hoisted_multi(const KsHoistMultiJob& job, int R, const Mod* mods, int log_n, cudaStream_t st);
+cudaError_t launch_ks_ip_hoisted_multi(const KsHoistMultiJob& job, int R, const Tables& tb, cudaStream_t st);
 
 // int64 sum of <= 8 fully reduced residue arrays (the NCCL reduce-scatter output, a15) -> residues
 cudaError_t launch_reduce_sum(const int64_t* in, uint64_t* out, int npolys, int l1, int log_n, const Mod* mods,
@@ -114,6 +115,11 @@ cudaError_t launch_encode_fft(const double* z_dev, size_t n_per, size_t count, c
                               const cdd* root, const cdd* twist, double scale_over_n, double window, int log_n,
                               cdd* A, int64_t* m, uint32_t* flags, unsigned int* nflag, unsigned int max_flags,
                               int* overflow, cudaStream_t st);
+// GPU decode (NEXT-4): twist, N-point double FFT, gather of the slots' real parts; A holds
+// count x N complex doubles (scratch)
+cudaError_t launch_decode_fft(const uint64_t* const* m_dev, size_t count, uint64_t q0, const uint32_t* pos_brv,
+                              const cdd* root, const cdd* twist, const double* inv_scale, int log_n, void* A,
+                              double* out, size_t n, cudaStream_t st);
 
 // samplers (ChaCha20, A11) -- rng_kernels.cu
 cudaError_t launch_sample_uniform(uint64_t* out, uint64_t seed, uint32_t tag, const uint64_t* index_per_limb_host,

@@ -413,6 +413,31 @@ __device__ __forceinline__ void fwd_rows_r16_body(const PassJob& job, const Tabl
             *reinterpret_cast<ulonglong2*>(dst + i) =
                 make_ulonglong2(canon(G::addr(i >> 8, i & 255)), canon(G::addr(i >> 8, (i & 255) + 1)));
         }
+    } else if (FP) {
+        // combine on the FP64 pipe: (acc - v) c mod q with c = p^-1 (or q_l^-1) centred, exact
+        // (acc < q, |v| <= 2.41 q after the lazy last stage: |acc - v| < 3.41 q, |c| <= q/2 ->
+        // |mulred| <= 1.14 q; + addend < q), then one canonical reduction
+        const uint64_t* aux = job.aux[z] + a * job.aux_a + b * job.aux_b + off0;
+        const ulonglong2 cm = tb.comb[mi];
+        const double q = qd.x, qinv = qd.y;
+        double cd = u2d(cm.x);
+        cd = cd > 0.5 * q ? __dsub_rn(cd, q) : cd;
+        const bool has_add = job.add[z] != nullptr && a < job.aux_limit;
+        const uint64_t* add = has_add ? job.add[z] + a * job.add_a + b * job.add_b + off0 : nullptr;
+        const double* dtile = reinterpret_cast<const double*>(tile);
+#pragma unroll 4
+        for (int k = 0; k < 8; k++) {
+            const int i = 2 * (threadIdx.x + k * 256);
+            const ulonglong2 ax = *reinterpret_cast<const ulonglong2*>(aux + i);
+            double r0 = mulred(__dsub_rn(u2d(ax.x), dtile[G::addr(i >> 8, i & 255)]), cd, q, qinv);
+            double r1 = mulred(__dsub_rn(u2d(ax.y), dtile[G::addr(i >> 8, (i & 255) + 1)]), cd, q, qinv);
+            if (has_add) {
+                const ulonglong2 ad = *reinterpret_cast<const ulonglong2*>(add + i);
+                r0 = __dadd_rn(r0, u2d(ad.x));
+                r1 = __dadd_rn(r1, u2d(ad.y));
+            }
+            *reinterpret_cast<ulonglong2*>(dst + i) = make_ulonglong2(d_canon(r0, q, qinv), d_canon(r1, q, qinv));
+        }
     } else {
         const uint64_t* aux = job.aux[z] + a * job.aux_a + b * job.aux_b + off0;
         const ulonglong2 cm = tb.comb[mi];

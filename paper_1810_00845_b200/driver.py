@@ -355,11 +355,13 @@ class EncryptedNet:
         """Decrypt + decode, undoing the tensor's compile-time (gain, offset) (A41; default: the
         network output's; an intermediate layer li passes self.layer_affine[li])."""
         g, off = self.layer_affine[-1] if affine is None else affine
-        vals = []
-        for ct in cts:
-            pt = self.b.decrypt(ct)
-            v = self.b.decode(pt, self.slots)
-            vals.append((v - off) / g if off else v / g)
+        pts = [self.b.decrypt(ct) for ct in cts]
+        if hasattr(self.b, "decode_batch"):      # GPU decode of all outputs at once (NEXT-4)
+            raw = list(self.b.decode_batch(pts, self.slots))
+        else:
+            raw = [self.b.decode(pt, self.slots) for pt in pts]
+        vals = [(v - off) / g if off else v / g for v in raw]
+        for pt in pts:
             self.b.free(pt)
         if lay.kind == "slot0":
             return np.array([v[0] for v in vals])

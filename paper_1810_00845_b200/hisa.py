@@ -65,6 +65,7 @@ _SIGS = {
     "hisa_encode": [_vp, _dp, _csz, _cd, _ci, _u64p],
     "hisa_encode_batch": [_vp, _dp, _csz, _csz, _cd, _ci, _u64p],
     "hisa_decode": [_vp, _cu64, _dp, _csz],
+    "hisa_decode_batch": [_vp, _u64p, _csz, _dp, _csz],
     "hisa_rot_left": [_vp, _cu64, _ci64, _u64p],
     "hisa_rot_right": [_vp, _cu64, _ci64, _u64p],
     "hisa_add": [_vp, _cu64, _cu64, _u64p],
@@ -259,6 +260,13 @@ def hisa_encode_batch(ctx, vs, scale: float, level: int = -1) -> list[int]:
 def hisa_decode(ctx, pt: int, n: int) -> np.ndarray:
     out = np.zeros(n, dtype=np.float64)
     _chk(load().hisa_decode(ctx, pt, _ptr(out, _dp), n))
+    return out
+
+
+def hisa_decode_batch(ctx, pts, n: int) -> np.ndarray:
+    ins = _u64(list(pts))
+    out = np.zeros((ins.size, n), dtype=np.float64)
+    _chk(load().hisa_decode_batch(ctx, _ptr(ins, _u64p), ins.size, _ptr(out, _dp), n))
     return out
 
 

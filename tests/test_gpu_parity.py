@@ -452,3 +452,25 @@ def test_k4_batch_shapes_and_long_digit_chains(nz):
         got = g.ct_export(h)
         assert (got == want).all(), f"ct {b}: {int((got != want).sum())} words differ"
     g.close()
+
+
+def test_gpu_decode_batch(pair):
+    """NEXT-4: decode on the GPU (INTT of limb 0, centred lift, twist, double FFT, gather).  A batch
+    of plaintexts (fresh encodings at two scales and a decrypted product) decodes within 1e-12 of the
+    oracle's long-double decode (decode is approximate by definition), equal to
+    one-at-a-time decoding, and an empty batch / n = 0 are no-ops."""
+    g, o = pair.g, pair.o
+    rng = np.random.default_rng(99)
+    n = o.slots
+    zs = [rng.uniform(-1, 1, n), rng.uniform(0, 1, n // 3), np.linspace(-2, 2, n)]
+    hs, ods = [], []
+    for z, sc in zip(zs, (2.0 ** 40, 2.0 ** 30, 2.0 ** 40)):
+        hs.append(g.encode(z, sc))
+        ods.append(o.encode(z, sc))
+    got = g.decode_batch(hs, n)
+    for i, (h, od) in enumerate(zip(hs, ods)):
+        ref = o.decode(od, n)
+        assert np.abs(got[i] - ref).max() < 1e-12 * max(1.0, np.abs(ref).max()), f"pt {i}"
+        assert (got[i] == g.decode(h, n)).all()
+    assert g.decode_batch([], n).shape == (0, n)
+    assert g.decode_batch(hs[:1], 0).shape == (1, 0)
