@@ -48,8 +48,8 @@ def parse():
     ap.add_argument("--images", type=int, default=20, help="images averaged per inference config (P:843-844)")
     ap.add_argument("--oracle-nets", default="tiny,lenet_small",
                     help="configs whose oracle inference latency is timed on the host cores (cpu_baseline)")
-    ap.add_argument("--tiling", default="lenet_large",
-                    help="config whose HW-tiled vs CHW-tiled (config + '_chw') latencies are compared ('' = skip)")
+    ap.add_argument("--tiling", default="lenet_small,lenet_large",
+                    help="configs whose four layout strategies (Fig. tilings) are timed ('' = skip)")
     ap.add_argument("--replica-sweep", default="",
                     help="config whose first FC is timed with R = 1, 2, 4, 8 replicas (NEXT-3), e.g. lenet_small")
     ap.add_argument("--policy-net", default="lenet_small",
@@ -770,15 +770,29 @@ def main():
                                                 "hardware": "2x Xeon E5-2667v3, 16 threads, non-RNS HEAAN"}
                 if not a.no_cpu_baseline and inf["config"] in a.oracle_nets.split(","):
                     inf["cpu_baseline"] = oracle_inference(inf["config"])
-            # NEXT-1: HW tiling vs CHW tiling of the second conv (the paper's layout
-            # comparison, Fig. tilings)
+            # NEXT-1: the paper's four layout strategies (Fig. tilings) on
+            # configs 3 and 4, each a lowering of the same network (variants: 3 images each)
             if a.tiling:
-                hw = next((i for i in line["inference"] if i["config"] == a.tiling), None) or \
-                    measure_inference(a.tiling, local, images=a.images)
-                chw = measure_inference(a.tiling + "_chw", local, images=a.images)
-                line["tiling"] = {"config": a.tiling, "hw_s": hw["latency_s"], "chw_s": chw["latency_s"],
-                                  "speedup_chw_over_hw": hw["latency_s"] / chw["latency_s"],
-                                  "chw_first_pass_incl_weight_encoding_s": chw["first_pass_incl_weight_encoding_s"]}
+                from synth import nets as SN
+                alias = SN.NETS.setdefault("_weights_alias", {})
+                line["tiling"] = {"figure": "Fig. tilings, P:883-900 (paper: CPU HEAAN latencies in s, context only)",
+                                  "nets": {}}
+                for base in [b for b in a.tiling.split(",") if b]:
+                    hw = next((i for i in line["inference"] if i["config"] == base), None) or \
+                        measure_inference(base, local, images=a.images)
+                    variants = {"CHW-fc HW-before": base + "_chwfc", "CHW": base + "_chw_all"}
+                    res = {"HW": {"config": base, "latency_s": hw["latency_s"], "rel_err": hw["rel_err"]}}
+                    for strat, nm in variants.items():
+                        if nm not in SN.NETS:
+                            nm = base + "_chwfc"     # no stride-1 conv to CHW-tile: CHW = CHW-fc
+                        alias[nm] = base
+                        r = measure_inference(nm, local, images=3)
+                        res[strat] = {"config": nm, "latency_s": r["latency_s"], "rel_err": r["rel_err"],
+                                      "levels_used": r["levels_used"], "rotation_keys": r["rotation_keys"]}
+                    res["HW-conv CHW-rest"] = dict(res["CHW-fc HW-before"],
+                                                   note="same lowering as CHW-fc HW-before in this build: "
+                                                        "activations and pools act per channel either way")
+                    line["tiling"]["nets"][base] = res
             # NEXT-3: replicas trade mulPlain for rotations
             if a.replica_sweep:
                 line["replica_sweep"] = {"config": a.replica_sweep, "latency_s": {

@@ -237,6 +237,14 @@ class OracleNet:
                 amts.update(lay.wS * 2 ** t for t in range(int(math.log2(lay.W))))
                 amts.update(lay.hS * 2 ** t for t in range(int(math.log2(lay.H))))
                 lay = Layout("slot0", lay.C, 1, 1)
+            elif kind == "fc" and lay.kind == "hw" and len(layer) > 3 and layer[3] == "chw":
+                span = (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+                cs = 2 ** math.ceil(math.log2(span))
+                G = min(max(1, s // cs), 2 ** math.ceil(math.log2(max(1, lay.C))))
+                for g in range(min(G, lay.C)):
+                    amts.add((s - (g * cs - lay.origin) % s) % s)
+                amts.update(2 ** t for t in range(int(math.log2(G * cs))))
+                lay = Layout("slot0", layer[1], 1, 1)
             elif kind == "fc" and lay.kind == "hw" and len(layer) > 2 and layer[2] > 1:
                 R = layer[2]
                 span = lay.origin + (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
@@ -435,10 +443,58 @@ class OracleNet:
             outs.append(acc)
         return outs, Layout("rep", groups, 1, 1, R=R, Bk=bk, count=n_out)
 
+    def fc_chw(self, cts, lay, layer, w, beta):
+        """CHW-tiled matmul (NEXT-1): mask, move channel c to block c mod G of
+        packed ciphertext c div G (blocks of cs slots, cs = span rounded up to a power of two),
+        then per neuron: sum over packed ciphertexts of mulPlain with the neuron's weights on every
+        block, rescale, rotate-and-sum by 1, 2, 4, ... < G cs into slot 0."""
+        o = self.o
+        n_out = layer[1]
+        if not lay.clean:
+            cts, lay = self._mask(cts, lay)
+        s = o.slots
+        span = (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+        cs = 2 ** math.ceil(math.log2(span))
+        G = min(max(1, s // cs), 2 ** math.ceil(math.log2(max(1, lay.C))))
+        C = lay.C
+        packed = []
+        for kk in range(-(-C // G)):
+            acc = None
+            for g in range(G):
+                c = kk * G + g
+                if c >= C:
+                    break
+                r = self._rot(cts[c], (s - (g * cs - lay.origin) % s) % s)
+                acc = r if acc is None else o.add(acc, r)
+            packed.append(acc)
+        rel = [y * lay.hS + x * lay.wS for y in range(lay.H) for x in range(lay.W)]
+        hw = lay.H * lay.W
+        outs = []
+        for jo in range(n_out):
+            acc = None
+            for kk, x in enumerate(packed):
+                v = np.zeros(s)
+                for g in range(G):
+                    c = kk * G + g
+                    if c < C:
+                        for i, r_ in enumerate(rel):
+                            v[g * cs + r_] = w[jo, c * hw + i]
+                term = o.mul_plain(x, o.encode(v, float(o.q[x.level]), x.level))
+                acc = term if acc is None else o.add(acc, term)
+            acc = o.rescale(acc)
+            for t in range(int(math.log2(G * cs))):
+                acc = o.add(acc, self._rot(acc, 2 ** t))
+            if beta:
+                acc = o.add_scalar(acc, beta)
+            outs.append(acc)
+        return outs, Layout("slot0", n_out, 1, 1)
+
     def fc(self, cts, lay, layer, w, beta):
         o = self.o
         n_out = layer[1]
         outs = []
+        if lay.kind == "hw" and len(layer) > 3 and layer[3] == "chw":
+            return self.fc_chw(cts, lay, layer, w, beta)
         if lay.kind == "hw" and len(layer) > 2 and layer[2] > 1:
             return self.fc_replicas(cts, lay, layer, w, beta)
         if lay.kind == "rep":

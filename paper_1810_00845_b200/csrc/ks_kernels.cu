@@ -464,28 +464,42 @@ __global__ void __launch_bounds__(16 * CG * RB, MINB) k_ks_ip6(KsJob job, Tables
     const int nsteps = n_nd + 1;
     const double* tw = tw_all + rr * 256;
 
+    // per-CTA source bases (hoisted out of the digit loop; the per-step offset is one add):
+    // group k's pass-1 rows T1[zz][j][ri][row] and diagonal row d[zz][ri][row]
+    const uint64_t* t1b[P::G];
+    const uint64_t* db[P::G];
+#pragma unroll
+    for (int k = 0; k < P::G; k++) {
+        const int zz = zb * CG + k % CG, rw = row_base + k / CG;
+        t1b[k] = job.t1[zz] + ((long long)ri << log_n) + (rw << 8);
+        db[k] = job.d[zz] + ((long long)ri << log_n) + (rw << 8);
+    }
+    const uint64_t* kb0 = key_ri + ((long long)row_base << 8);
+    const long long t1_step = (long long)nri << log_n;
     // cp.async copies of step `st` into stage buffer `buf`
     auto issue = [&](int st, int buf) {
         uint64_t* base = stage0 + buf * P::STAGE;
         const bool diag = st == n_nd;
         const int j = diag ? ri : (st < ri ? st : st + 1);
+        const long long joff = (long long)j * t1_step;
         // rows: group k's row (256 words = 128 chunks of 16 B); plain for pass-1 rows, swizzled for
         // the diagonal digit (read in the phase-2 pattern)
-        for (int c = tid; c < P::G * 128; c += P::NT) {
-            const int k = c >> 7, ch = c & 127;
-            const int zz = zb * CG + k % CG, rw = row_base + k / CG;
-            const uint64_t* src = diag ? job.d[zz] + ((long long)j << log_n) + (rw << 8)
-                                       : job.t1[zz] + (((long long)j * nri + ri) << log_n) + (rw << 8);
-            const int line = ch >> 3, cc = ch & 7;
-            const int dst = k * 256 + (diag ? line * 16 + ((cc ^ (line & 7)) << 1) : ch * 2);
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(base + dst);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src + ch * 2) : "memory");
+#pragma unroll
+        for (int k = 0; k < P::G; k++) {
+            for (int ch = tid; ch < 128; ch += P::NT) {
+                const uint64_t* src = (diag ? db[k] : t1b[k] + joff) + ch * 2;
+                const int line = ch >> 3, cc = ch & 7;
+                const int dst = k * 256 + (diag ? line * 16 + ((cc ^ (line & 7)) << 1) : ch * 2);
+                const unsigned sa = (unsigned)__cvta_generic_to_shared(base + dst);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src) : "memory");
+            }
         }
         // keys: per row, b and a (swizzled)
         uint64_t* kbase = base + P::STAGE_T1;
+        const uint64_t* kj = kb0 + (long long)j * kstride_j;
         for (int c = tid; c < RB * 256; c += P::NT) {
             const int rk = c >> 8, h = (c >> 7) & 1, ch = c & 127;
-            const uint64_t* src = key_ri + (long long)j * kstride_j + h * kstride_p + ((row_base + rk) << 8) + ch * 2;
+            const uint64_t* src = kj + h * kstride_p + (rk << 8) + ch * 2;
             const int line = ch >> 3, cc = ch & 7;
             const unsigned sa = (unsigned)__cvta_generic_to_shared(kbase + (rk * 2 + h) * 256 + line * 16 +
                                                                    ((cc ^ (line & 7)) << 1));

@@ -459,6 +459,76 @@ class EncryptedNet:
         cs = 1 << math.ceil(math.log2(span + 2 * pad_off))
         return cs, max(1, slots // cs), pad_off
 
+    def _pack(self, cts, lay, cs, G, pad_off):
+        """CHW packing (NEXT-1, P:679): clean channel c -> packed ciphertext c // G, block c % G,
+        its data origin moved to block offset g cs + pad_off (one right rotation per channel
+        outside block 0, batched per block; adds in between)."""
+        C = lay.C
+        npk = -(-C // G)
+        packed = [None] * npk
+        for g in range(G):
+            chans = [c for c in range(g, C, G)]
+            if not chans:
+                continue
+            shift = (g * cs + pad_off - lay.origin) % self.slots
+            amt = (self.slots - shift) % self.slots
+            if amt:
+                rs = [r[0] for r in self._rot_many([cts[c] for c in chans], [amt])]
+            else:
+                rs = [self.b.copy(cts[c]) for c in chans]
+            for c, r in zip(chans, rs):
+                kk = c // G
+                if packed[kk] is None:
+                    packed[kk] = r
+                else:
+                    nxt = self.b.add(packed[kk], r)
+                    self._free_all([packed[kk], r])
+                    packed[kk] = nxt
+        return packed
+
+    @staticmethod
+    def fc_chw_geometry(lay, slots):
+        """CHW FC packing (NEXT-1): block stride cs = the plane's span rounded up to a power of
+        two, G = channels per ciphertext (a power of two, <= slots / cs, no more than needed)."""
+        span = (lay.H - 1) * lay.hS + (lay.W - 1) * lay.wS + 1
+        cs = 1 << math.ceil(math.log2(span))
+        G = min(max(1, slots // cs), 1 << math.ceil(math.log2(max(1, lay.C))))
+        return cs, G
+
+    def fc_chw(self, cts, lay, layer, w, beta, li):
+        """CHW-tiled matmul (NEXT-1: the paper's "CHW-fc" layouts, P:722-725 with P:728): the
+        (masked, clean) channels packed G per ciphertext at block stride cs, one mulPlain per
+        (neuron, packed ciphertext) -- C / G instead of C -- with the weights laid on each block,
+        one rescale, then log2(G cs) rotate-and-sum steps into slot 0 (the dot product over all
+        blocks).  R = 1 form; the output is one ciphertext per neuron (slot-0 layout)."""
+        if self.world > 1:
+            raise NotImplementedError("CHW FC is single-GPU in this build")
+        n_out = layer[1]
+        masked = False
+        if not lay.clean:
+            cts, lay = self.mask(cts, lay, li)
+            masked = True
+        cs, G = self.fc_chw_geometry(lay, self.slots)
+        packed = self._pack(cts, lay, cs, G, 0)
+        if masked:
+            self._free_all(cts)
+        rel = lay.slots_of_valid() - lay.origin
+        hw = lay.H * lay.W
+
+        def vals(jo, kk):
+            v = np.zeros(self.slots)
+            for g in range(G):
+                c = kk * G + g
+                if c < lay.C:
+                    v[g * cs + rel] = w[jo, c * hw:(c + 1) * hw]
+            return v
+        sums = self._mulplain_sums(packed, range(n_out), "fcchw", li, vals)
+        self._free_all(packed)
+        res = self.b.rescale_batch(sums)
+        self._free_all(sums)
+        res = self._rotate_sum(res, [1 << t for t in range(int(math.log2(G * cs)))])
+        return self._bias(res, beta), Layout("slot0", n_out)
+
     def conv_chw(self, cts, lay, layer, w, beta, li):
         """CHW-tiled conv2d (NEXT-1), stride 1: G channels packed per ciphertext at
         block stride CS; the K^2 - 1 tap rotations are hoisted per PACKED ciphertext (G channels
@@ -479,26 +549,7 @@ class EncryptedNet:
         C = lay.C
         cs, G, pad_off = self.chw_geometry(lay, k, p, self.slots)
         npk = -(-C // G)
-        # pack: channel c -> packed ciphertext c // G, block c % G (right rotation by its offset)
-        packed = [None] * npk
-        for g in range(G):
-            chans = [c for c in range(g, C, G)]
-            if not chans:
-                continue
-            shift = (g * cs + pad_off - lay.origin) % self.slots
-            amt = (self.slots - shift) % self.slots
-            if amt:
-                rs = [r[0] for r in self._rot_many([cts[c] for c in chans], [amt])]
-            else:
-                rs = [self.b.copy(cts[c]) for c in chans]
-            for c, r in zip(chans, rs):
-                kk = c // G
-                if packed[kk] is None:
-                    packed[kk] = r
-                else:
-                    nxt = self.b.add(packed[kk], r)
-                    self._free_all([packed[kk], r])
-                    packed[kk] = nxt
+        packed = self._pack(cts, lay, cs, G, pad_off)
         if masked:
             self._free_all(cts)
         taps = [(i, j) for i in range(k) for j in range(k)]
@@ -787,6 +838,8 @@ class EncryptedNet:
         the output neurons partitioned across ranks -- no partial-sum exchange."""
         if lay.kind == "rep":
             return self.fc_from_rep(cts, lay, layer, w, beta, li)
+        if lay.kind == "hw" and len(layer) > 3 and layer[3] == "chw":
+            return self.fc_chw(cts, lay, layer, w, beta, li)
         if lay.kind == "hw" and len(layer) > 2 and layer[2] > 1:
             return self.fc_replicated(cts, lay, layer, w, beta, li)
         n_out = layer[1]

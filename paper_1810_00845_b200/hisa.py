@@ -541,11 +541,15 @@ class Context:
         self.slots = self.N // 2
         self.moduli = hisa_moduli(self.ctx, self.L + 1)
         self.q, self.p = self.moduli[:-1], self.moduli[-1]
-        if arena_bytes is None:
-            free, _total = torch.cuda.mem_get_info(device)
-            arena_bytes = int(free * 0.6)
-        self._arena = torch.empty(arena_bytes, dtype=torch.uint8, device=f"cuda:{device}")
-        hisa_attach_arena(self.ctx, self._arena.data_ptr(), arena_bytes)
+        self._arena = None
+        # HISA_NO_ARENA=1 (sanitizer runs, tools/sanitize.sh): every buffer its own
+        # cudaMallocAsync allocation, so compute-sanitizer memcheck sees each buffer's bounds
+        if not os.environ.get("HISA_NO_ARENA"):
+            if arena_bytes is None:
+                free, _total = torch.cuda.mem_get_info(device)
+                arena_bytes = int(free * 0.6)
+            self._arena = torch.empty(arena_bytes, dtype=torch.uint8, device=f"cuda:{device}")
+            hisa_attach_arena(self.ctx, self._arena.data_ptr(), arena_bytes)
         hisa_set_stream(self.ctx, torch.cuda.current_stream(device).cuda_stream)
 
     def close(self):

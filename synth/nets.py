@@ -12,8 +12,9 @@ Layer tuples (PyTorch semantics for the float64 definition):
     ("act",)                       a0 + a1 x + a2 x^2 with ACT_COEFFS (A25)
     ("square",)                    x^2 (config 1)
     ("avgpool",)                   2x2, stride 2
-    ("fc", out[, R])               W @ flatten(x) (flatten order c, y, x); R = replicas per
-                                   ciphertext in the encrypted lowering (A27), not semantics
+    ("fc", out[, R[, "chw"]])      W @ flatten(x) (flatten order c, y, x); R = replicas per
+                                   ciphertext in the encrypted lowering (A27), "chw" the CHW-tiled
+                                   FC lowering (NEXT-1, R = 1); not semantics
     ("fire", sq, e1, e3)           SqueezeNet fire module (config 5): s = act(conv1x1(x));
                                    out = concat(act(conv1x1(s)) [e1 ch], act(conv3x3 SAME(s)) [e3 ch])
     ("gap",)                       global average pool (config 5)
@@ -51,6 +52,22 @@ NETS = {
                             layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2, "chw"),
                                     ("act",), ("avgpool",), ("fc", 512, 16), ("act",), ("fc", 10)],
                             sigma=[0.05, 0.05, 0.05, 0.05], act_gains=[4.0 ** 2, 4.0 ** 3, 4.0 ** 3]),
+    # NEXT-1 layout strategies (Fig. tilings) on configs 3 / 4 -- lowering choices only,
+    # the same weights (seeds) and float64 network as the base config:
+    #   "CHW-fc HW-before": HW convs, CHW-tiled FC1 (also this build's "HW-conv CHW-rest": the
+    #   activations and pools act per channel in both, see DESIGN.md NEXT-1)
+    #   "CHW": every stride-1 conv and FC1 CHW-tiled
+    "lenet_small_chwfc": dict(log_n=14, q_bits=[60] + [40] * 6, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
+                              layers=[("conv", 5, 5, 2, 1), ("act",), ("fc", 100, 1, "chw"), ("act",), ("fc", 10)],
+                              sigma=[0.1, 0.1, 0.1], act_gains=[4.0 ** 3, 4.0 ** 2]),
+    "lenet_large_chwfc": dict(log_n=15, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
+                              layers=[("conv", 32, 5, 1, 2), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2), ("act",),
+                                      ("avgpool",), ("fc", 512, 1, "chw"), ("act",), ("fc", 10)],
+                              sigma=[0.05, 0.05, 0.05, 0.05], act_gains=[4.0 ** 2, 4.0 ** 3, 4.0 ** 3]),
+    "lenet_large_chw_all": dict(log_n=15, q_bits=[60] + [40] * 13, p_bits=60, scale=2.0 ** 40, input=(1, 28, 28),
+                                layers=[("conv", 32, 5, 1, 2, "chw"), ("act",), ("avgpool",), ("conv", 64, 5, 1, 2, "chw"),
+                                        ("act",), ("avgpool",), ("fc", 512, 1, "chw"), ("act",), ("fc", 10)],
+                                sigma=[0.05, 0.05, 0.05, 0.05], act_gains=[4.0 ** 2, 4.0 ** 3, 4.0 ** 3]),
     # config 5: SqueezeNet-CIFAR-shaped (A33: conv1 + 4 fire modules + 1x1 conv + global avg pool;
     # 1 + 4*2 + 1 = 10 conv layers, 9 activations), N = 2^16, 24 limbs
     "squeezenet": dict(log_n=16, q_bits=[60] + [40] * 23, p_bits=60, scale=2.0 ** 40, input=(3, 32, 32),

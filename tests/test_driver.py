@@ -99,15 +99,16 @@ def test_driver_bit_exact_and_accurate(name):
     assert _rel(got, ogot) < 1e-9          # same ciphertexts; the two decoders agree to ~1e-16
 
 
-@pytest.mark.parametrize("which", ["every_branch", "replicas", "squeezenet_kinds", "chw"])
+@pytest.mark.parametrize("which", ["every_branch", "replicas", "squeezenet_kinds", "chw", "chw_fc"])
 def test_driver_small_nets_bit_exact(which):
     """Every lowering branch (mask + SAME conv after a pool, both FC forms; replica FC and FC
-    from the replica layout; fire modules and global average pool) bit-exact against the
-    oracle at N = 2^11."""
-    from tests.test_driver_host import (MINI, MINI_CHW, MINI_REP, MINI_SQ, _mini_chw_weights, _mini_rep_weights,
-                                        _mini_sq_weights, _mini_weights)
+    from the replica layout; fire modules and global average pool; CHW conv; CHW FC) bit-exact
+    against the oracle at N = 2^11."""
+    from tests.test_driver_host import (MINI, MINI_CHW, MINI_CHWFC, MINI_REP, MINI_SQ, _mini_chw_weights,
+                                        _mini_chwfc_weights, _mini_rep_weights, _mini_sq_weights, _mini_weights)
     net, W = {"every_branch": (MINI, _mini_weights()), "replicas": (MINI_REP, _mini_rep_weights()),
-              "squeezenet_kinds": (MINI_SQ, _mini_sq_weights()), "chw": (MINI_CHW, _mini_chw_weights())}[which]
+              "squeezenet_kinds": (MINI_SQ, _mini_sq_weights()), "chw": (MINI_CHW, _mini_chw_weights()),
+              "chw_fc": (MINI_CHWFC, _mini_chwfc_weights())}[which]
     img = SN._image(5, net["input"])
     got, ogot, ref = _run_pair(net, W, img)
     _accurate(got, ref)

@@ -67,6 +67,18 @@ def _mini_chw_weights():
     return [SN._weights(51 + i, s, 0.3) for i, s in enumerate(shapes)]
 
 
+# CHW-tiled FC (NEXT-1, the paper's "CHW-fc" layouts): pooled 4x4 planes (span 67 -> block 128),
+# 3 channels -> one packed ciphertext (G = 4), 3 neurons from one mulPlain each, then slot-0 FC
+MINI_CHWFC = dict(log_n=11, q_bits=[60] + [40] * 7, p_bits=60, scale=2.0 ** 40, input=(2, 8, 8),
+                  layers=[("conv", 3, 3, 1, 1), ("act",), ("avgpool",), ("fc", 3, 1, "chw"), ("act",),
+                          ("fc", 2)], sigma=[0.3, 0.3, 0.3])
+
+
+def _mini_chwfc_weights():
+    shapes = [(3, 2, 3, 3), (3, 3 * 4 * 4), (2, 3)]
+    return [SN._weights(61 + i, s, 0.3) for i, s in enumerate(shapes)]
+
+
 def _mini_weights():
     shapes = [(2, 2, 3, 3), (2, 2, 3, 3), (3, 2 * 4 * 4), (2, 3)]
     return [SN._weights(77 + i, s, 0.3) for i, s in enumerate(shapes)]
@@ -408,6 +420,27 @@ def test_oracle_chw_conv_matches_float64_and_planner():
     pl = EncryptedNet.plan(MINI_CHW, W, SN.ACT_COEFFS, on.o.moduli)
     assert pl["rotations"] == on.amounts
     assert pl["levels_used"] == 6
+
+
+def test_oracle_chw_fc_matches_float64_and_planner():
+    """NEXT-1 pin: the oracle's CHW-tiled FC (mask, pack G channels per ciphertext, one mulPlain
+    per (neuron, packed ciphertext), rotate-and-sum over G blocks) decrypts within 1e-3 of the
+    float64 network, and the product planner selects the same keys and levels."""
+    from oracle import plain
+    from oracle.nets import OracleNet
+    from paper_1810_00845_b200.driver import EncryptedNet
+    W = _mini_chwfc_weights()
+    img = SN._image(13, MINI_CHWFC["input"])
+    on = OracleNet(MINI_CHWFC, W, SN.ACT_COEFFS)
+    cts, lay = on.encrypt_image(img)
+    out, ol = on.forward(cts, lay)
+    got = on.decrypt_output(out, ol)
+    ref = plain.forward(MINI_CHWFC, img, W, SN.ACT_COEFFS)
+    assert got.shape == ref.shape == (2,)
+    assert np.abs(got - ref).max() <= 1e-3, (got, ref)
+    pl = EncryptedNet.plan(MINI_CHWFC, W, SN.ACT_COEFFS, on.o.moduli)
+    assert pl["rotations"] == on.amounts
+    assert pl["levels_used"] == 6          # conv, act, mask, FC, act, FC
 
 
 def test_plain_reference_ops_match_torch():

@@ -34,6 +34,7 @@ for row in ctx.rot_left_hoisted_batch(cts, amts):
 ctx.sync()
 st = torch.cuda.current_stream()
 ctx.profile(True)
+torch.cuda.profiler.start()   # ncu --profile-from-start off captures the timed iterations only
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(st)
 for _ in range(a.iters):
@@ -42,6 +43,7 @@ for _ in range(a.iters):
             ctx.free(h)
 e1.record(st)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 ms = e0.elapsed_time(e1) / a.iters
 prof = ctx.profile_read()
 print(json.dumps({"lib": a.lib or "default", "batch": a.batch, "R": len(amts), "ms_per_step": ms,
