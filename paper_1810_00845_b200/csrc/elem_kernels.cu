@@ -3,24 +3,27 @@
 // 16-byte vector loads/stores, one pair of words per thread, grid = (pairs, ciphertexts).
 #include <cuda_runtime.h>
 #include "launch.h"
+#include "ntt_f64.cuh"
 
 namespace hisa {
 
 template <int OP>
 __global__ void __launch_bounds__(256) k_elem(ElemJob job, const Mod* __restrict__ mods) {
-    const int z = blockIdx.y;
+    const int z = blockIdx.z;
     const long long n2 = 1ll << (job.log_n - 1);               // word pairs per limb
     const long long per_poly = (long long)job.nl * n2;
     const int np_out = (OP == EL_TENSOR || OP == EL_SQUARE_TENSOR) ? 3
                      : (OP == EL_DECRYPT2 || OP == EL_DECRYPT3) ? 1 : job.npolys;
-    const long long total = (OP == EL_TENSOR || OP == EL_SQUARE_TENSOR || OP == EL_DECRYPT2 || OP == EL_DECRYPT3)
-                                ? per_poly : (long long)np_out * per_poly;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int p = (int)(idx / per_poly);
-        const long long rem = idx - p * per_poly;
-        const int i = (int)(rem / n2);
-        const long long w = (rem - (long long)i * n2) * 2;         // word offset in limb
+    (void)per_poly;
+    (void)np_out;
+    // grid (pairs of a limb, poly x limb, ciphertext): no 64-bit index divisions (the round-1
+    // grid-stride form spent most of its issue slots on them: mulPlain at ~0.39 of HBM)
+    {
+        const long long pair = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+        if (pair >= n2) return;
+        const int p = (int)blockIdx.y / job.nl;
+        const int i = (int)blockIdx.y - p * job.nl;
+        const long long w = pair * 2;                               // word offset in limb
         const Mod md = mods[i];
         const uint64_t q = md.q;
         const long long limb_off = (long long)i << job.log_n;
@@ -112,13 +115,10 @@ static int sm_count() {
 }
 
 cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, cudaStream_t st) {
-    const long long pairs = ((long long)job.nl << (job.log_n - 1)) *
-                            ((op == EL_TENSOR || op == EL_SQUARE_TENSOR || op == EL_DECRYPT2 || op == EL_DECRYPT3)
-                                 ? 1 : job.npolys);
-    long long blocks = (pairs + 255) / 256;
-    const long long cap = (long long)sm_count() * 8;
-    if (blocks > cap) blocks = cap;
-    dim3 grid((unsigned)blocks, nz);
+    const int np = (op == EL_TENSOR || op == EL_SQUARE_TENSOR || op == EL_DECRYPT2 || op == EL_DECRYPT3) ? 1
+                                                                                                      : job.npolys;
+    const long long n2 = 1ll << (job.log_n - 1);
+    dim3 grid((unsigned)((n2 + 255) / 256), (unsigned)(np * job.nl), (unsigned)nz);
     switch (op) {
 #define C(OPV) case OPV: k_elem<OPV><<<grid, 256, 0, st>>>(job, mods); break;
         C(EL_ADD) C(EL_SUB) C(EL_NEG) C(EL_ADD_PLAIN) C(EL_SUB_PLAIN) C(EL_MUL_PLAIN) C(EL_ADD_SCALAR)
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) k_mulplain_acc(const uint64_t* const* __r
     extern __shared__ uint64_t msm[];
     const uint64_t** ins = reinterpret_cast<const uint64_t**>(msm);   // [C]
     const long long N = 1ll << job.log_n;
-    const int limb = blockIdx.y;
+    const int limb = job.limb_map[blockIdx.y];
     const Mod md = mods[limb];
     const long long loff = (long long)limb * N;
     const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
@@ -296,13 +296,90 @@ __global__ void __launch_bounds__(256) k_mulplain_acc(const uint64_t* const* __r
     }
 }
 
-cudaError_t launch_mulplain_acc(const uint64_t* const* in_ptrs, const uint64_t* const* pt_ptrs,
-                                uint64_t* const* out_ptrs, const MpaJob& job, const Mod* mods, cudaStream_t st) {
+// FP64 limbs (q < 2^50): out_j = sum_c x_c p_jc accumulated as exact mulred products (both < q:
+// |mulred| < 0.88 q) in doubles, re-centred every 8 terms (|acc| < 7.6 q < 2^53) -- two registers
+// per accumulator instead of a 128-bit pair, so OT = 8 neurons per pass (each input word re-read
+// J / 8 times), and the FP64 pipe's MAC rate instead of the integer pipe's
+template <int OT>
+__global__ void __launch_bounds__(256) k_mulplain_acc_f64(const uint64_t* const* __restrict__ in_ptrs,
+                                                          const uint64_t* const* __restrict__ pt_ptrs,
+                                                          uint64_t* const* __restrict__ out_ptrs, MpaJob job,
+                                                          Tables tb) {
+    extern __shared__ uint64_t msm[];
+    const uint64_t** ins = reinterpret_cast<const uint64_t**>(msm);   // [C]
     const long long N = 1ll << job.log_n;
-    dim3 grid((unsigned)((N / 2 + 255) / 256), job.l1, 1);
-    const size_t smem = (size_t)job.C * sizeof(void*);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_mulplain_acc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_mulplain_acc<<<grid, 256, smem, st>>>(in_ptrs, pt_ptrs, out_ptrs, job, mods);
+    const int limb = job.limb_map[blockIdx.y];
+    const double2 qd = tb.modd[limb];
+    const double q = qd.x, qinv = qd.y;
+    const long long loff = (long long)limb * N;
+    const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
+    for (int c = threadIdx.x; c < job.C; c += blockDim.x) ins[c] = in_ptrs[c] + loff;
+    __syncthreads();
+    if (x >= N) return;
+    const long long pstride = (long long)job.l1 * N;
+    for (int j0 = 0; j0 < job.J; j0 += OT) {
+        double acc[OT][2][2];
+#pragma unroll
+        for (int k = 0; k < OT; k++)
+#pragma unroll
+            for (int p = 0; p < 2; p++) { acc[k][p][0] = 0.0; acc[k][p][1] = 0.0; }
+        for (int c = 0; c < job.C; c++) {
+            const ulonglong2 a0 = __ldg(reinterpret_cast<const ulonglong2*>(ins[c] + x));
+            const ulonglong2 a1 = __ldg(reinterpret_cast<const ulonglong2*>(ins[c] + pstride + x));
+            const double a00 = u2d(a0.x), a01 = u2d(a0.y), a10 = u2d(a1.x), a11 = u2d(a1.y);
+#pragma unroll
+            for (int k = 0; k < OT; k++) {
+                if (j0 + k >= job.J) break;
+                const ulonglong2 pv =
+                    __ldcs(reinterpret_cast<const ulonglong2*>(pt_ptrs[(long long)(j0 + k) * job.C + c] + loff + x));
+                const double p0 = u2d(pv.x), p1 = u2d(pv.y);
+                acc[k][0][0] = __dadd_rn(acc[k][0][0], mulred(a00, p0, q, qinv));
+                acc[k][0][1] = __dadd_rn(acc[k][0][1], mulred(a01, p1, q, qinv));
+                acc[k][1][0] = __dadd_rn(acc[k][1][0], mulred(a10, p0, q, qinv));
+                acc[k][1][1] = __dadd_rn(acc[k][1][1], mulred(a11, p1, q, qinv));
+            }
+            if ((c & 7) == 7) {
+#pragma unroll
+                for (int k = 0; k < OT; k++)
+#pragma unroll
+                    for (int p = 0; p < 2; p++) {
+                        acc[k][p][0] = redd(acc[k][p][0], q, qinv);
+                        acc[k][p][1] = redd(acc[k][p][1], q, qinv);
+                    }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < OT; k++) {
+            if (j0 + k >= job.J) break;
+#pragma unroll
+            for (int p = 0; p < 2; p++)
+                *reinterpret_cast<ulonglong2*>(out_ptrs[j0 + k] + p * pstride + loff + x) =
+                    make_ulonglong2(d_canon(acc[k][p][0], q, qinv), d_canon(acc[k][p][1], q, qinv));
+        }
+    }
+}
+
+cudaError_t launch_mulplain_acc(const uint64_t* const* in_ptrs, const uint64_t* const* pt_ptrs,
+                                uint64_t* const* out_ptrs, const MpaJob& job_in, const Tables& tb, cudaStream_t st) {
+    const long long N = 1ll << job_in.log_n;
+    const size_t smem = (size_t)job_in.C * sizeof(void*);
+    MpaJob jf = job_in, ji = job_in;
+    int nf = 0, ni = 0;
+    for (int i = 0; i < job_in.l1; i++) {
+        if ((tb.fp_mods >> i) & 1) jf.limb_map[nf++] = (uint8_t)i;
+        else ji.limb_map[ni++] = (uint8_t)i;
+    }
+    if (ni) {
+        dim3 grid((unsigned)((N / 2 + 255) / 256), ni, 1);
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_mulplain_acc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_mulplain_acc<<<grid, 256, smem, st>>>(in_ptrs, pt_ptrs, out_ptrs, ji, tb.mods);
+    }
+    if (nf) {
+        dim3 grid((unsigned)((N / 2 + 255) / 256), nf, 1);
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_mulplain_acc_f64<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_mulplain_acc_f64<8><<<grid, 256, smem, st>>>(in_ptrs, pt_ptrs, out_ptrs, jf, tb);
+    }
     return cudaGetLastError();
 }
 

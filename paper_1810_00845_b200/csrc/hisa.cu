@@ -1772,7 +1772,7 @@ extern "C" int hisa_mul_plain_accumulate(hisa_ctx* c, const hisa_ct* in, size_t 
     const double terms = std::ldexp(1.0, 127) / ((double)qmax * (double)qmax);
     MpaJob mj{(int)C, (int)J, l1, c->log_n, (int)std::min(1024.0, std::floor(terms) - 1)};
     KL("mulplain_acc", launch_mulplain_acc((const uint64_t* const*)dev, (const uint64_t* const*)(dev + C),
-                                           (uint64_t* const*)(dev + C + C * J), mj, c->d_mods, c->stream));
+                                           (uint64_t* const*)(dev + C + C * J), mj, c->tables(), c->stream));
     CK(cudaStreamSynchronize(c->stream));   // the host pointer staging must outlive the copy
     dfree(c, dev);
     for (size_t j = 0; j < J; j++) outs[j] = new_handle(c, OBJ_CT, op[j], level, 2, ci[0]->scale * pi[0]->scale);

@@ -49,9 +49,10 @@ cudaError_t launch_automorphism_add(const uint64_t* const* in, uint64_t* const* 
 struct MpaJob {
     int C, J, l1, log_n;
     int red_every;
+    uint8_t limb_map[MAXL];   // grid.y -> limb (filled by the launcher: FP64 limbs, integer limbs)
 };
 cudaError_t launch_mulplain_acc(const uint64_t* const* in_ptrs, const uint64_t* const* pt_ptrs,
-                                uint64_t* const* out_ptrs, const MpaJob& job, const Mod* mods, cudaStream_t st);
+                                uint64_t* const* out_ptrs, const MpaJob& job, const Tables& tb, cudaStream_t st);
 
 constexpr int MAXR = 8;
 

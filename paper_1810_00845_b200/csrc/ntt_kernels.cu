@@ -385,6 +385,18 @@ __device__ __forceinline__ void fwd_rows_r16_body(const PassJob& job, const Tabl
         if constexpr (FP) r[e] = __longlong_as_double((long long)w);   // lazy pass-1 doubles
         else r[e] = w;
     }
+    if (STOREMODE == STORE_COMBINE) {
+        // the combine's operands (acc, addend) pulled into L2 now, consumed after both phases
+        // (ncu, profiles/r2_ncu_mdrows_v1.txt: 58 % of stall samples waited on these loads)
+        const uint64_t* aux = job.aux[z] + a * job.aux_a + b * job.aux_b + off0;
+        const bool has_add = job.add[z] != nullptr && a < job.aux_limit;
+        const uint64_t* add = has_add ? job.add[z] + a * job.add_a + b * job.add_b + off0 : nullptr;
+        {   // one 128-byte line per thread per array: 256 x 128 B = the 16-row tile
+            const int i = 16 * threadIdx.x;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(aux + i));
+            if (has_add) asm volatile("prefetch.global.L2 [%0];" ::"l"(add + i));
+        }
+    }
     const double2 qd = FP ? tb.modd[mi] : make_double2(0, 0);
     const void* twp = FP ? (const void*)(tb.fwd_d + ((long long)mi << tb.log_n))
                          : (const void*)(tb.fwd + ((long long)mi << tb.log_n));
