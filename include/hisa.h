@@ -167,6 +167,9 @@ int hisa_sub_scalar(hisa_ctx* ctx, hisa_ct a, double x, hisa_ct* out);
 /* = mul_norelin + relinearize */
 int hisa_mul(hisa_ctx* ctx, hisa_ct a, hisa_ct b, hisa_ct* out);
 int hisa_mul_plain(hisa_ctx* ctx, hisa_ct a, hisa_pt p, hisa_ct* out);
+/* n independent mulPlains at one level in batched launches: outs[i] = a[i] (x) p[i] (fresh handles;
+ * HISA_E_LEVEL_MISMATCH unless every pair shares one level) */
+int hisa_mul_plain_batch(hisa_ctx* ctx, const hisa_ct* a, const hisa_pt* p, size_t n, hisa_ct* outs);
 /* X = llround(x * pt_scale); pt_scale == 0 means (double) q_top of the ciphertext (A8) */
 int hisa_mul_scalar(hisa_ctx* ctx, hisa_ct a, double x, double pt_scale, hisa_ct* out);
 

@@ -52,7 +52,13 @@ __global__ void __launch_bounds__(256) k_elem(ElemJob job, const Mod* __restrict
         } else if (OP == EL_MUL_PLAIN) {
             const ulonglong2 x = *A;
             const ulonglong2 y = *reinterpret_cast<const ulonglong2*>(job.b[z] + limb_off + w);
-            *O = make_ulonglong2(mul_mod(x.x, y.x, md), mul_mod(x.y, y.y, md));
+            if ((job.fp_mods >> i) & 1) {   // exact FP64 product (q < 2^50): fewer issue slots than Barrett
+                const double2 qd = job.modd[i];
+                *O = make_ulonglong2(d_canon(mulred(u2d(x.x), u2d(y.x), qd.x, qd.y), qd.x, qd.y),
+                                     d_canon(mulred(u2d(x.y), u2d(y.y), qd.x, qd.y), qd.x, qd.y));
+            } else {
+                *O = make_ulonglong2(mul_mod(x.x, y.x, md), mul_mod(x.y, y.y, md));
+            }
         } else if (OP == EL_ADD_SCALAR) {
             ulonglong2 x = *A;
             if (p == 0) { x.x = add_mod(x.x, job.scal[i], q); x.y = add_mod(x.y, job.scal[i], q); }
@@ -71,6 +77,21 @@ __global__ void __launch_bounds__(256) k_elem(ElemJob job, const Mod* __restrict
             } else { b0 = a0; b1 = a1; }
             uint64_t* o = job.out[z] + limb_off + w;
             ulonglong2 r0, r1, r2;
+            if ((job.fp_mods >> i) & 1) {   // exact FP64 products (q < 2^50)
+                const double2 qd = job.modd[i];
+                const double q_ = qd.x, qi_ = qd.y;
+                const double x0 = u2d(a0.x), y0 = u2d(a0.y), x1 = u2d(a1.x), y1 = u2d(a1.y);
+                const double u0 = u2d(b0.x), v0 = u2d(b0.y), u1 = u2d(b1.x), v1 = u2d(b1.y);
+                r0 = make_ulonglong2(d_canon(mulred(x0, u0, q_, qi_), q_, qi_), d_canon(mulred(y0, v0, q_, qi_), q_, qi_));
+                // a0 b1 + a1 b0: two exact products (each |.| < 0.88 q), one canonical reduction
+                r1 = make_ulonglong2(d_canon(__dadd_rn(mulred(x0, u1, q_, qi_), mulred(x1, u0, q_, qi_)), q_, qi_),
+                                     d_canon(__dadd_rn(mulred(y0, v1, q_, qi_), mulred(y1, v0, q_, qi_)), q_, qi_));
+                r2 = make_ulonglong2(d_canon(mulred(x1, u1, q_, qi_), q_, qi_), d_canon(mulred(y1, v1, q_, qi_), q_, qi_));
+                *reinterpret_cast<ulonglong2*>(o) = r0;
+                *reinterpret_cast<ulonglong2*>(o + job.out_poly) = r1;
+                *reinterpret_cast<ulonglong2*>(o + 2 * job.out_poly) = r2;
+                return;
+            }
             r0.x = mul_mod(a0.x, b0.x, md); r0.y = mul_mod(a0.y, b0.y, md);
             // a0 b1 + a1 b0 with one reduction: sum of two 120-bit products fits 128 bits
             {

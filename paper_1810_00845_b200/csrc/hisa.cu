@@ -625,6 +625,36 @@ __global__ void k_key_assemble(uint64_t* b, const uint64_t* a, const uint64_t* s
         b[idx] = v;
     }
 }
+// Internal key-switching-key format (K4 v6 / K7 inner products on the FP64 pipe):
+// limbs of FP64-engine moduli (q < 2^50) hold the centred residue K - q [K > q/2] as an exact
+// double (|K| <= q/2 halves the MAC bound), the others the canonical residue.  dir = +1:
+// canonical -> internal (keygen), -1: internal -> canonical (hisa_key_export).
+__global__ void k_key_format(uint64_t* key, int kL, int L, int log_n, const Mod* mods, uint64_t fp_mods, int dir) {
+    const long long N = 1ll << log_n;
+    const long long total = (long long)kL * 2 * (kL + 1) * N;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)((idx >> log_n) % (kL + 1));
+        const int mi = r < kL ? r : L;
+        if (!((fp_mods >> mi) & 1)) continue;
+        const uint64_t q = mods[mi].q;
+        if (dir > 0) {
+            const uint64_t u = key[idx];
+            const double d = u > (q >> 1) ? -(double)(q - u) : (double)u;
+            key[idx] = (uint64_t)__double_as_longlong(d);
+        } else {
+            const double d = __longlong_as_double((long long)key[idx]);
+            key[idx] = d < 0.0 ? q - (uint64_t)(-d) : (uint64_t)d;
+        }
+    }
+}
+static int key_format(hisa_ctx* c, uint64_t* key, int kL, int dir) {
+    const Tables tb = c->tables();
+    k_key_format<<<1184, 256, 0, c->stream>>>(key, kL, c->L, c->log_n, c->d_mods, tb.fp_mods, dir);
+    CK(cudaGetLastError());
+    return HISA_OK;
+}
+
 // c0 = v pk_b + e0 + m ; c1 = v pk_a + e1 (all NTT, limbs 0..l)
 __global__ void k_enc_assemble(uint64_t* ct, const uint64_t* v, const uint64_t* e0, const uint64_t* e1,
                                const uint64_t* m, const uint64_t* pk, int l1, int L, int log_n, const Mod* mods) {
@@ -717,6 +747,7 @@ extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin,
         ej.npolys = 1; ej.nl = M; ej.log_n = c->log_n;
         KL("elementwise", launch_elem(EL_MUL_PLAIN, ej, c->d_mods, 1, c->stream));
         RET(gen_ksk(c, 0, sp, &c->d_rlk));
+        RET(key_format(c, c->d_rlk, L, +1));
         dfree(c, sp);
     }
     for (size_t i = 0; i < n; i++) {
@@ -761,6 +792,7 @@ extern "C" int hisa_keygen(hisa_ctx* c, const int64_t* rot, size_t n, int relin,
         uint64_t* kout[1] = {kp};
         KL("automorphism", launch_automorphism(kin, kout, 1, 2 * kL * (kL + 1), c->log_n, &ginv, c->stream));
         dfree(c, key);
+        RET(key_format(c, kp, kL, +1));
         c->rot_keys[(uint64_t)k] = hisa_ctx::KeyRec{kp, kL};
         dfree(c, sg);
         dfree(c, sp);
@@ -785,13 +817,18 @@ extern "C" int hisa_key_export(hisa_ctx* c, int64_t which, uint64_t* host, size_
     if (!src) return fail(HISA_E_NO_KEY, "no such key %lld", (long long)which);
     if (words != w) return fail(HISA_E_PARAMS, "key has %zu words", w);
     uint64_t* canon = nullptr;
-    if (which > 0) {   // rotation keys are stored pre-permuted: export the canonical key (A37)
+    if (which >= 0) {   // key-switching keys: canonical words (internal FP64 format undone) ...
         canon = dalloc_t<uint64_t>(c, w);
         if (!canon) return fail(HISA_E_OOM, "key export");
-        const uint64_t g = h_pow(5, (uint64_t)which, 2 * c->N);
-        const uint64_t* kin[1] = {src};
-        uint64_t* kout[1] = {canon};
-        KL("automorphism", launch_automorphism(kin, kout, 1, 2 * kL * (kL + 1), c->log_n, &g, c->stream));
+        if (which > 0) {   // ... and rotation keys un-permuted (stored pre-permuted, A37)
+            const uint64_t g = h_pow(5, (uint64_t)which, 2 * c->N);
+            const uint64_t* kin[1] = {src};
+            uint64_t* kout[1] = {canon};
+            KL("automorphism", launch_automorphism(kin, kout, 1, 2 * kL * (kL + 1), c->log_n, &g, c->stream));
+        } else {
+            CK(cudaMemcpyAsync(canon, src, w * 8, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        RET(key_format(c, canon, kL, -1));
         src = canon;
     }
     CK(cudaMemcpyAsync(host, src, w * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -1110,6 +1147,8 @@ static ElemJob ejob(const hisa_ctx* c, int npolys, int level) {
     j.nl = level + 1;
     j.log_n = c->log_n;
     j.a_poly = j.b_poly = j.out_poly = (long long)(level + 1) * c->N;
+    j.fp_mods = c->tables().fp_mods & ((level + 1 >= 64) ? ~0ull : ((1ull << (level + 1)) - 1));
+    j.modd = c->d_modd;
     return j;
 }
 static bool scale_eq(double a, double b) { return fabs(a / b - 1.0) <= 0x1p-30; }
@@ -1150,6 +1189,42 @@ static int plain_op(hisa_ctx* c, hisa_ct ha, hisa_pt hp, hisa_ct* out, ElemOp op
 extern "C" int hisa_add_plain(hisa_ctx* c, hisa_ct a, hisa_pt p, hisa_ct* out) { return plain_op(c, a, p, out, EL_ADD_PLAIN); }
 extern "C" int hisa_sub_plain(hisa_ctx* c, hisa_ct a, hisa_pt p, hisa_ct* out) { return plain_op(c, a, p, out, EL_SUB_PLAIN); }
 extern "C" int hisa_mul_plain(hisa_ctx* c, hisa_ct a, hisa_pt p, hisa_ct* out) { return plain_op(c, a, p, out, EL_MUL_PLAIN); }
+
+// n independent mulPlains (same level) in one launch per MAXB pairs: outs[i] = a[i] (x) p[i]
+extern "C" int hisa_mul_plain_batch(hisa_ctx* c, const hisa_ct* a, const hisa_pt* p, size_t n, hisa_ct* outs) {
+    CHECK_CTX(c);
+    if ((!a || !p || !outs) && n) return fail(HISA_E_PARAMS, "null argument");
+    if (n == 0) return HISA_OK;
+    std::vector<Obj*> oa(n), op(n);
+    for (size_t i = 0; i < n; i++) {
+        oa[i] = get_obj(c, a[i], OBJ_CT);
+        op[i] = get_obj(c, p[i], OBJ_PT);
+        if (!oa[i] || !op[i]) return fail(HISA_E_INVALID_HANDLE, "invalid handle at %zu", i);
+        if (oa[i]->npolys != 2) return fail(HISA_E_NOT_RELINEARIZED, "3-poly ciphertext at %zu", i);
+        if (oa[i]->level != op[i]->level || oa[i]->level != oa[0]->level)
+            return fail(HISA_E_LEVEL_MISMATCH, "levels differ at %zu", i);
+    }
+    const int level = oa[0]->level;
+    DGuard outputs(c);
+    std::vector<uint64_t*> res(n);
+    for (size_t i = 0; i < n; i++) {
+        res[i] = outputs.add(dalloc_t<uint64_t>(c, obj_words(c, oa[i])));
+        if (!res[i]) return fail(HISA_E_OOM, "mul_plain batch");
+    }
+    for (size_t i0 = 0; i0 < n; i0 += MAXB) {
+        const int nz = (int)std::min<size_t>(MAXB, n - i0);
+        ElemJob j = ejob(c, 2, level);
+        for (int z = 0; z < nz; z++) {
+            j.a[z] = oa[i0 + z]->ptr;
+            j.b[z] = op[i0 + z]->ptr;
+            j.out[z] = res[i0 + z];
+        }
+        KL("elementwise", launch_elem(EL_MUL_PLAIN, j, c->d_mods, nz, c->stream));
+    }
+    outputs.keep();
+    for (size_t i = 0; i < n; i++) outs[i] = new_handle(c, OBJ_CT, res[i], level, 2, oa[i]->scale * op[i]->scale);
+    return HISA_OK;
+}
 
 // A20: X = llround(x * s), |X| < 2^62, residues X mod q_i
 static int scalar_residues(hisa_ctx* c, double x, double s, int l1, ElemJob& j) {

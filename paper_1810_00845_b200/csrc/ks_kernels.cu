@@ -15,6 +15,16 @@
 
 namespace hisa {
 
+// a key word of an FP64-engine limb: stored as the centred residue's exact double (internal key
+// format, hisa.cu k_key_format), |K| <= q/2
+__device__ __forceinline__ double kd(uint64_t raw) { return __longlong_as_double((long long)raw); }
+// the same word as a uint64 representative in [0, q) for the integer MACs of k_ks_ip2
+__device__ __forceinline__ uint64_t ku(uint64_t raw, double q) {
+    const double d = kd(raw);
+    return d2u(d < 0.0 ? __dadd_rn(d, q) : d);
+}
+
+
 // K4 for one row per CTA with two digits in flight (variant 30, FP64 output primes): the
 // non-diagonal digits j != ri are processed in pairs -- both D tiles copied, both transformed by
 // one interleaved engine call (fwd_engine_f64_rowtw2, twiddles staged once in shared memory),
@@ -76,8 +86,9 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
             const int i = threadIdx.x + k * NTHR;
             uint64_t D = buf[G::addr(0, i)];
             if (conv) D = d_rep4(__longlong_as_double((long long)D), tq52);   // in [0, 4q]
-            mac128(acc0[k], D, __ldg(kb + i));
-            mac128(acc1[k], D, __ldg(ka + i));
+            const uint64_t Kb = __ldg(kb + i), Ka = __ldg(ka + i);
+            mac128(acc0[k], D, fp ? ku(Kb, qd.x) : Kb);   // FP64 limbs: internal key format
+            mac128(acc1[k], D, fp ? ku(Ka, qd.x) : Ka);
         }
     };
     // digits j != ri, in pairs
@@ -125,17 +136,13 @@ __global__ void __launch_bounds__((1 << LOG_M) / (1 << LOG_R), MINB) k_ks_ip2(Ks
     }
 }
 
-// K4 register-direct (variant 80): the FP64 rows of k_ks_ip2 without the staging round trips.
-// M = 256 as four radix-4 phases over 64 threads: phase 0's operands (elements t + 64e) are
-// loaded from the pass-1 output straight into registers (a warp reads 256 contiguous bytes per
-// load), phases exchange through the swizzled shared tiles, and phase 3 leaves thread t holding
-// elements 4t + e, which are multiplied into the accumulators from registers with the key words
-// read as two 16-byte vectors.  Two digits in flight as in k_ks_ip2; the special prime's row
-// (integer engine) runs the k_ks_ip2 path.
+// K4 for the integer-engine output primes at M = 256 (60-bit: the special prime, the 60-bit q_0 of
+// configs 1, 3-5): one row per 64-thread CTA, the row's pass-1 words staged by cp.async, the last
+// 8 CT stages with the integer (Shoup) engine, 128-bit lazy key MACs, one Barrett per output word.
+// (The FP64 output primes run k_ks_ip6 below.)
 #ifndef K5_MINB
-#define K5_MINB 9     // k_ks_ip5 min CTAs / SM (64 threads): 9 -> <= 112 registers
+#define K5_MINB 9     // k_ks_ip5 min CTAs / SM (64 threads)
 #endif
-constexpr int K5_TILE = 320;   // >= pad_1(255) + 1 = 316, pad_2(255) + 1 = 319 (words)
 
 template <int MINB>
 __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
@@ -143,8 +150,6 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     using G = Geo<LOG_M, LOG_R>;
     extern __shared__ uint64_t sm[];
     uint64_t* sa = sm;
-    uint64_t* sb = sm + G::STRIDE;
-    double* tws = reinterpret_cast<double*>(sm + 2 * G::STRIDE);
     const int nz = job.nz;
     const int z = blockIdx.x % nz;
     const int ri = job.ri_list[blockIdx.y];
@@ -155,7 +160,6 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     const long long off0 = (long long)row0 << LOG_M;
     const int mi = job.mod_map[ri];
     const Mod md = tb.mods[mi];
-    const bool fp = (double)md.q < tb.f64_max_q;
     const int t = threadIdx.x;
     const long long kstride_j = 2ll * (job.L + 1) << log_n;
     const long long kstride_p = (long long)(job.L + 1) << log_n;
@@ -169,237 +173,37 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
     U128 acc0[4], acc1[4];
 #pragma unroll
     for (int k = 0; k < 4; k++) { acc0[k] = U128{0, 0}; acc1[k] = U128{0, 0}; }
-    if (!fp) {   // integer-engine row: staged engine, elements t + 64k
-        for (int j = 0; j < l1 + 1; j++) {
-            if (j == l1 && ri >= l1) break;
-            const int jj = j == l1 ? ri : j;
-            if (j < l1 && j == ri) continue;
-            const uint64_t* src = tile_src(jj);
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int i = t + k * 64;
-                const unsigned s_ = (unsigned)__cvta_generic_to_shared(&sa[G::addr(0, i)]);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_), "l"(src + i) : "memory");
-            }
-            asm volatile("cp.async.wait_all;\n" ::: "memory");
-            __syncthreads();
-            if (j < l1)
-                fwd_engine<LOG_M, LOG_R>(sa, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M, (uint32_t)row0, 0, t);
-            const uint64_t* kb = key_r + jj * kstride_j;
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int i = t + k * 64;
-                const uint64_t D = sa[G::addr(0, i)];
-                mac128(acc0[k], D, __ldg(kb + i));
-                mac128(acc1[k], D, __ldg(kb + kstride_p + i));
-            }
-            __syncthreads();
-        }
+    for (int j = 0; j < l1 + 1; j++) {   // the non-diagonal digits, then the diagonal one (if ri < l1)
+        if (j == l1 && ri >= l1) break;
+        const int jj = j == l1 ? ri : j;
+        if (j < l1 && j == ri) continue;
+        const uint64_t* src = tile_src(jj);
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            out0[t + k * 64] = barrett128(acc0[k].lo, acc0[k].hi, md);
-            out1[t + k * 64] = barrett128(acc1[k].lo, acc1[k].hi, md);
+            const int i = t + k * 64;
+            const unsigned s_ = (unsigned)__cvta_generic_to_shared(&sa[G::addr(0, i)]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s_), "l"(src + i) : "memory");
         }
-        return;
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncthreads();
+        if (j < l1)
+            fwd_engine<LOG_M, LOG_R>(sa, md.q, tb.fwd + ((long long)mi << log_n), log_n - LOG_M, (uint32_t)row0, 0, t);
+        const uint64_t* kb = key_r + jj * kstride_j;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int i = t + k * 64;
+            const uint64_t D = sa[G::addr(0, i)];
+            mac128(acc0[k], D, __ldg(kb + i));
+            mac128(acc1[k], D, __ldg(kb + kstride_p + i));
+        }
+        __syncthreads();
     }
-    const double2 qd = tb.modd[mi];
-    const double q = qd.x, qinv = qd.y;
-    const double tq52 = __dadd_rn(2.0 * q, 4503599627370496.0);   // 2q + 2^52
-    double* tws5 = reinterpret_cast<double*>(sm + 4 * K5_TILE);
-    // Prefetch stages (cp.async, each thread copies exactly the words it later reads, so no
-    // barrier is needed -- only its own cp.async.wait_group): stT1 = the next step's pass-1 rows
-    // (elements t + 64 e), stK = the current step's key words (b and a, elements 4t .. 4t + 3).
-    // Round 1's K4 waited on both loads in every step (ncu: long-scoreboard 2.5 warps / issue).
-    double* stT1 = tws5 + 256;                                         // [2][256]
-    uint64_t* stK = reinterpret_cast<uint64_t*>(stT1 + 512);         // [2 digits][b, a][256]
-    const int n_nd = l1 - 1;                                  // fp rows: ri < l1
-    auto digit = [&](int idx) { return idx < ri ? idx : idx + 1; };
-    auto issue_t1 = [&](int idx) {      // rows of the step starting at non-diagonal index idx
-        const int nd = idx + 1 < n_nd ? 2 : 1;
-        for (int n = 0; n < nd; n++) {
-            const uint64_t* src = tile_src(digit(idx + n)) + t;
 #pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const unsigned sa_ = (unsigned)__cvta_generic_to_shared(stT1 + n * 256 + t + 64 * e);
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa_), "l"(src + 64 * e) : "memory");
-            }
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    auto issue_keys = [&](int ja, int jb, int nd) {
-        for (int n = 0; n < nd; n++) {
-            const uint64_t* kb = key_r + (n == 0 ? ja : jb) * kstride_j + 4 * t;
-#pragma unroll
-            for (int h = 0; h < 2; h++)
-#pragma unroll
-                for (int c = 0; c < 2; c++) {
-                    const unsigned sa_ = (unsigned)__cvta_generic_to_shared(stK + (2 * n + h) * 256 + 4 * t + 2 * c);
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa_),
-                                 "l"(kb + h * kstride_p + 2 * c) : "memory");
-                }
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    if (n_nd > 0) issue_t1(0);
-    {
-        const double* twg = tb.fwd_d + ((long long)mi << log_n);
-        const int s0 = log_n - LOG_M;
-        for (int idx = t + 1; idx < G::M; idx += 64) {
-            const int u = 31 - __clz(idx), m = idx - (1 << u);
-            tws5[idx] = twg[(1 << (s0 + u)) + (row0 << u) + m];
-        }
+    for (int k = 0; k < 4; k++) {
+        out0[t + k * 64] = barrett128(acc0[k].lo, acc0[k].hi, md);
+        out1[t + k * 64] = barrett128(acc1[k].lo, acc1[k].hi, md);
     }
-    // Exchange tiles.  Phase ph's thread t holds elements mid = base_ph(t) | (e << lo_ph), e < 4
-    // (lo_ph = 6 - 2 ph).  Exchange x (after phase x) is written with phase x's pattern and read
-    // with phase x + 1's, through its own padded layout pad_x(m) = m + P_x (m >> S_x), chosen by
-    // exhaustive search (profiles/r2_k4_layouts.txt) so that BOTH patterns are conflict-free for
-    // 64-bit accesses (16 distinct 8-byte bank slots per half-warp; the XOR swizzle of round 1 had
-    // 48 extra wavefronts per digit-row, ncu: 58.5 M per launch) -- and, because a padding is
-    // additive in the bits above S_x, pad_x(base | e << lo) = pad_x(base) + e * step, so every
-    // access is one base register plus an immediate offset.  Exchanges 0 and 2 share buffer A,
-    // exchange 1 uses B (a thread's in-place read-then-write of one exchange can then never
-    // clobber another thread's unread word of a different layout).
-    auto pad = [](int x, int m) { return x == 1 ? m + 4 * (m >> 4) : x == 2 ? m + (m >> 2) : m; };
-    int wr[3], rd[3];
-#pragma unroll
-    for (int ph = 0; ph < 4; ph++) {
-        const int lo = 6 - 2 * ph;
-        const int base = ((t >> lo) << (lo + 2)) | (t & ((1 << lo) - 1));
-        if (ph < 3) wr[ph] = pad(ph, base);
-        if (ph > 0) rd[ph - 1] = pad(ph - 1, base);
-    }
-    // K5_STEP(x, lo): pad_x(e << lo) / e
-    auto step = [](int x, int lo) { return x == 1 ? (lo >= 4 ? 5 << (lo - 2) : 1 << lo)
-                                        : x == 2 ? (lo >= 2 ? 5 << (lo - 2) : 1 << lo) : 1 << lo; };
-    __syncthreads();
-    // Split 64-bit MACs (products < 2^102): D < 2^52 (d_rep4) = Dh 2^32 + Dl, key word K < q < 2^50
-    // = Kh 2^25 + Kl; D K = Dl Kl + (Dl Kh + (Dh << 7) Kl) 2^25 + Dh Kh 2^57.  Three 64-bit
-    // accumulators per output word, each term one IMAD.WIDE.U32 (32 x 32 + 64); bounds for at most
-    // 24 digits: A0 < 24 2^57, A1 < 24 (2^57 + 2^52), A2 < 24 2^45 -- no overflow.
-    uint64_t A0[2][4], A1[2][4], A2[2][4];
-#pragma unroll
-    for (int h = 0; h < 2; h++)
-#pragma unroll
-        for (int e = 0; e < 4; e++) { A0[h][e] = 0; A1[h][e] = 0; A2[h][e] = 0; }
-    auto mac_split = [&](int h, int e, uint64_t D, uint64_t K) {
-        const uint32_t dl = (uint32_t)D, dh = (uint32_t)(D >> 32);
-        const uint32_t kl = (uint32_t)K & 0x1FFFFFFu, kh = (uint32_t)(K >> 25);
-        A0[h][e] += (uint64_t)dl * kl;
-        A1[h][e] += (uint64_t)dl * kh;
-        A1[h][e] += (uint64_t)(dh << 7) * kl;
-        A2[h][e] += (uint64_t)dh * kh;
-    };
-    // ND digits (1 or 2) through the four phases, then MAC from registers
-    auto run = [&](auto nd_c, int ja, int jb, int next_idx) {
-        constexpr int ND = decltype(nd_c)::value;
-        double r[ND][4];
-        issue_keys(ja, jb, ND);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");      // this step's rows (not its keys)
-#pragma unroll
-        for (int n = 0; n < ND; n++)
-#pragma unroll
-            for (int e = 0; e < 4; e++) r[n][e] = stT1[n * 256 + t + 64 * e];
-        const bool more = next_idx < n_nd;
-        if (more) issue_t1(next_idx);
-#pragma unroll
-        for (int ph = 0; ph < 4; ph++) {
-            const int u0 = 2 * ph;
-            const int lo_bit = 6 - u0;
-            const int ohigh = t >> lo_bit;
-            if (ph > 0) {
-                const int x = ph - 1;
-#pragma unroll
-                for (int n = 0; n < ND; n++) {
-                    const double* b = reinterpret_cast<const double*>(sm + (2 * n + (x & 1)) * K5_TILE) + rd[x];
-#pragma unroll
-                    for (int e = 0; e < 4; e++) r[n][e] = b[e * step(x, lo_bit)];
-                }
-            }
-#pragma unroll
-            for (int uu = 0; uu < 2; uu++) {
-                const int u = u0 + uu;
-                const int dist = 2 >> uu;
-                const int tbase = (1 << u) + (ohigh << uu);
-#pragma unroll
-                for (int k = 0; k < 2; k++) {
-                    if (k >= (1 << uu)) break;
-                    const double W = tws5[tbase + k];
-#pragma unroll
-                    for (int e0 = 0; e0 < 2; e0++) {
-                        if (e0 >= dist) break;
-                        const int e = k * 2 * dist + e0;
-#pragma unroll
-                        for (int n = 0; n < ND; n++) {
-                            const double X = full_stage(u, LOG_M) ? redd(r[n][e], q, qinv) : r[n][e];
-                            const double T = mulred(r[n][e + dist], W, q, qinv);
-                            r[n][e] = __dadd_rn(X, T);
-                            r[n][e + dist] = __dsub_rn(X, T);
-                        }
-                    }
-                }
-            }
-            if (ph < 3) {
-                if (ph == 0) __syncthreads();   // the previous round's phase-3 reads of A are done
-#pragma unroll
-                for (int n = 0; n < ND; n++) {
-                    double* b = reinterpret_cast<double*>(sm + (2 * n + (ph & 1)) * K5_TILE) + wr[ph];
-#pragma unroll
-                    for (int e = 0; e < 4; e++) b[e * step(ph, lo_bit)] = r[n][e];
-                }
-                __syncthreads();
-            }
-        }
-        // phase 3 left elements 4t + e in registers; the keys wait in stK
-        if (more) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-        else asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-#pragma unroll
-        for (int n = 0; n < ND; n++) {
-            const ulonglong2* kb = reinterpret_cast<const ulonglong2*>(stK + (2 * n) * 256 + 4 * t);
-            const ulonglong2* ka = reinterpret_cast<const ulonglong2*>(stK + (2 * n + 1) * 256 + 4 * t);
-            const ulonglong2 b0 = kb[0], b1 = kb[1], a0 = ka[0], a1 = ka[1];
-            const uint64_t kbv[4] = {b0.x, b0.y, b1.x, b1.y}, kav[4] = {a0.x, a0.y, a1.x, a1.y};
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const uint64_t D = d_rep4(r[n][e], tq52);
-                mac_split(0, e, D, kbv[e]);
-                mac_split(1, e, D, kav[e]);
-            }
-        }
-    };
-    int idx = 0;
-    for (; idx + 1 < n_nd; idx += 2) run(std::integral_constant<int, 2>(), digit(idx), digit(idx + 1), idx + 2);
-    if (idx < n_nd) run(std::integral_constant<int, 1>(), digit(idx), digit(idx), idx + 1);
-    {   // the diagonal digit: d_ri, already in the NTT domain (canonical < q), elements 4t + e
-        const uint64_t* src = tile_src(ri) + 4 * t;
-        const ulonglong2 d0 = __ldg(reinterpret_cast<const ulonglong2*>(src));
-        const ulonglong2 d1 = __ldg(reinterpret_cast<const ulonglong2*>(src) + 1);
-        const uint64_t dv[4] = {d0.x, d0.y, d1.x, d1.y};
-        const uint64_t* kb = key_r + ri * kstride_j + 4 * t;
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-            mac_split(0, e, dv[e], __ldg(kb + e));
-            mac_split(1, e, dv[e], __ldg(kb + kstride_p + e));
-        }
-    }
-    // recombine A0 + A1 2^25 + A2 2^57 (< 2^107) as 128 bits, one Barrett reduction per word
-    auto fold = [&](int h, int e) {
-        uint64_t lo = A0[h][e], hi = 0;
-        const uint64_t t1 = A1[h][e] << 25;
-        lo += t1;
-        hi += (A1[h][e] >> 39) + (lo < t1);
-        const uint64_t t2 = A2[h][e] << 57;
-        lo += t2;
-        hi += (A2[h][e] >> 7) + (lo < t2);
-        return barrett128(lo, hi, md);
-    };
-    ulonglong2* o0 = reinterpret_cast<ulonglong2*>(out0 + 4 * t);
-    ulonglong2* o1 = reinterpret_cast<ulonglong2*>(out1 + 4 * t);
-    o0[0] = make_ulonglong2(fold(0, 0), fold(0, 1));
-    o0[1] = make_ulonglong2(fold(0, 2), fold(0, 3));
-    o1[0] = make_ulonglong2(fold(1, 0), fold(1, 1));
-    o1[1] = make_ulonglong2(fold(1, 2), fold(1, 3));
 }
-
 
 // ------------------------------------------------------------------------------------------
 // K4 v6 (FP64 output primes, M = 256 rows: N = 2^15, 2^16).  ncu of k_ks_ip5 (profiles/
@@ -410,11 +214,12 @@ __global__ void __launch_bounds__(64, MINB) k_ks_ip5(KsJob job, Tables tb) {
 //  * runs each 256-point row as two radix-16 register phases with ONE exchange, 16 threads per
 //    row (thread g holds elements 16a + g in phase 1, 16t + b in phase 2);
 //  * accumulates the key inner product on the FP64 pipe: acc += mulred(D, K) with D the centred
-//    phase-2 output (|D| <= 1.6 q) and K the key word (< q, exact u2d): |mulred| <= 1.1 q
-//    (ntt_f64.cuh bound, |a w| <= 1.6 q^2), so six products fit between re-centrings (|acc| <
-//    7.1 q < 2^53 for q < 2^50): every step is exact integer arithmetic, the result (one final
-//    canonical reduction) is the same residue as the integer MAC's -- two doubles per output
-//    word instead of three 64-bit words, no 64-bit multiplies;
+//    phase-2 output (|D| <= 1.7 q, k4_full schedule) and K the key word, stored as its centred
+//    residue's exact double (|K| <= q/2, internal key format): |mulred| <= q/2 + 1.5 2^-52 |D K|
+//    <= 0.82 q, so eight products fit between re-centrings (|acc| < 7.1 q < 2^53): every step is
+//    exact integer arithmetic, the result (one final canonical reduction) is the same residue as
+//    the integer MAC's -- two doubles per output word instead of three 64-bit words, no 64-bit
+//    multiplies;
 //  * puts CG ciphertexts x RB rows (G = CG RB groups of 16 threads) in one CTA: the key rows are
 //    staged once per row and shared by the CG ciphertexts;
 //  * stages each step's rows and keys with cp.async one step ahead (double buffer); the key rows
@@ -434,6 +239,11 @@ struct Ip6 {
     static constexpr int STAGE = STAGE_T1 + STAGE_K;
     static constexpr size_t smem_bytes() { return (size_t)(256 * RB + 2 * STAGE) * 8; }
 };
+
+// K4 v6's row-pass schedule: X re-centred at stages 0, 4, 7 only (the round-1 engines: 0, 3, 6, 7).
+// From a column-pass input |v| <= 2.41 q the magnitudes stay <= 4.23 q (< 2^52.1) and the output
+// is <= 1.68 q, the MAC's operand bound (tests/test_f64_arith.py::test_k4_row_schedule).
+__host__ __device__ constexpr bool k4_full(int u) { return u == 0 || u == 4 || u == 7; }
 
 // word b of line t of a 256-word row in the pair-swizzled layout (lines of 16 words = 128 B)
 __device__ __forceinline__ int swz(int t, int b) { return t * 16 + ((((b >> 1) ^ t) & 7) << 1) + (b & 1); }
@@ -551,7 +361,7 @@ __global__ void __launch_bounds__(16 * CG * RB, MINB) k_ks_ip6(KsJob job, Tables
                 for (int a = 0; a < 16; a++) {
                     if (a & dist) continue;
                     const double W = tw[(1 << u) + (a >> (4 - u))];
-                    const double X = full_stage(u, 8) ? redd(r[a], q, qinv) : r[a];
+                    const double X = k4_full(u) ? redd(r[a], q, qinv) : r[a];
                     const double T = mulred(r[a + dist], W, q, qinv);
                     r[a] = __dadd_rn(X, T);
                     r[a + dist] = __dsub_rn(X, T);
@@ -576,7 +386,7 @@ __global__ void __launch_bounds__(16 * CG * RB, MINB) k_ks_ip6(KsJob job, Tables
                 for (int b = 0; b < 16; b++) {
                     if (b & dist) continue;
                     const double W = tw[(1 << u) + ((b >> (8 - u)) << 4) + g];
-                    const double X = full_stage(u, 8) ? redd(r[b], q, qinv) : r[b];
+                    const double X = k4_full(u) ? redd(r[b], q, qinv) : r[b];
                     const double T = mulred(r[b + dist], W, q, qinv);
                     r[b] = __dadd_rn(X, T);
                     r[b + dist] = __dsub_rn(X, T);
@@ -597,12 +407,12 @@ __global__ void __launch_bounds__(16 * CG * RB, MINB) k_ks_ip6(KsJob job, Tables
         for (int c = 0; c < 8; c++) {
             const ulonglong2 vb = *reinterpret_cast<const ulonglong2*>(kb + swz(g, 2 * c));
             const ulonglong2 va = *reinterpret_cast<const ulonglong2*>(kb + 256 + swz(g, 2 * c));
-            accb[2 * c] = __dadd_rn(accb[2 * c], mulred(r[2 * c], u2d(vb.x), q, qinv));
-            accb[2 * c + 1] = __dadd_rn(accb[2 * c + 1], mulred(r[2 * c + 1], u2d(vb.y), q, qinv));
-            acca[2 * c] = __dadd_rn(acca[2 * c], mulred(r[2 * c], u2d(va.x), q, qinv));
-            acca[2 * c + 1] = __dadd_rn(acca[2 * c + 1], mulred(r[2 * c + 1], u2d(va.y), q, qinv));
+            accb[2 * c] = __dadd_rn(accb[2 * c], mulred(r[2 * c], kd(vb.x), q, qinv));
+            accb[2 * c + 1] = __dadd_rn(accb[2 * c + 1], mulred(r[2 * c + 1], kd(vb.y), q, qinv));
+            acca[2 * c] = __dadd_rn(acca[2 * c], mulred(r[2 * c], kd(va.x), q, qinv));
+            acca[2 * c + 1] = __dadd_rn(acca[2 * c + 1], mulred(r[2 * c + 1], kd(va.y), q, qinv));
         }
-        if (st % 6 == 5) {
+        if ((st & 7) == 7) {
 #pragma unroll
             for (int b = 0; b < 16; b++) { accb[b] = redd(accb[b], q, qinv); acca[b] = redd(acca[b], q, qinv); }
         }
@@ -647,8 +457,7 @@ static cudaError_t ks_ip6_t(const KsJob& job, const Tables& tb, int nfp, cudaStr
 template <int MINB>
 static cudaError_t ks_ip5_t(const KsJob& job, const Tables& tb, int nz, int nrows, cudaStream_t st) {
     const int rows = 1 << (tb.log_n - 8);
-    // 4 exchange tiles + twiddles + row prefetch [2][256] + key stage [2][2][256]: 24 KB
-    const size_t smem = (4 * (size_t)K5_TILE + 256 + 512 + 1024) * sizeof(uint64_t);
+    const size_t smem = (size_t)Geo<8, 2>::STRIDE * sizeof(uint64_t);   // the row tile
     dim3 grid(rows * nz, nrows, 1);
     k_ks_ip5<MINB><<<grid, 64, smem, st>>>(job, tb);
     return cudaGetLastError();
@@ -664,9 +473,6 @@ static cudaError_t ks_ip2_t(const KsJob& job, const Tables& tb, int nz, cudaStre
     return cudaGetLastError();
 }
 
-#ifndef K4_V6
-#define K4_V6 1      // 0: round-1 k_ks_ip5 on every row (side builds for A/B timing only)
-#endif
 #ifndef K6_MINB
 #define K6_MINB 4      // 128 registers, no spills (5: spills)
 #endif
@@ -679,7 +485,7 @@ static cudaError_t ks_ip_256(KsJob job, const Tables& tb, int nz, cudaStream_t s
     int nfp = 0, nint = 0;
     uint8_t fp[MAXL], in[MAXL];
     for (int ri = 0; ri < l2; ri++) {
-        if (K4_V6 && ((job.fp_rows >> ri) & 1)) fp[nfp++] = (uint8_t)ri;
+        if ((job.fp_rows >> ri) & 1) fp[nfp++] = (uint8_t)ri;
         else in[nint++] = (uint8_t)ri;
     }
     cudaError_t e;
@@ -739,9 +545,9 @@ cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_
 // ------------------------------------------------------------------------------------------
 // K7: hoisted inner products, CG ciphertexts x R keys per thread-word (one word per thread).
 // FP64 output primes (q < 2^50): the multiply-accumulates run on the FP64 pipe as in K4 v6 --
-// acc += mulred(D, K), D (< q, the materialised ModUp output) and K (< q) converted exactly
-// (u2d): |mulred| <= q/2 + 1.5 2^-52 q^2 < 0.88 q, so eight products fit between re-centrings
-// (|acc| < 7.6 q < 2^53).  Two doubles per accumulator instead of a 128-bit pair: CG = 4, R = 4
+// acc += mulred(D, K), D (< q, the materialised ModUp output, exact u2d) and K (the internal key
+// format's centred double, |K| <= q/2): |mulred| <= q/2 + 1.5 2^-52 q^2 / 2 < 0.69 q, so eight
+// products fit between re-centrings (|acc| < 6.1 q < 2^53).  Two doubles per accumulator instead of a 128-bit pair: CG = 4, R = 4
 // needs 64 accumulator registers (the 128-bit form needed 255 registers, one CTA per SM, and left
 // the key stream latency-bound at ~0.4 of HBM), and the FP64 pipe's MAC rate is ~2x the integer
 // pipe's (measured: hisa_microbench_mac vs _butterfly_f64).  Integer-engine output primes (60-bit)
@@ -749,6 +555,11 @@ cudaError_t launch_ks_ip(const KsJob& job, const Tables& tb, int nz, cudaStream_
 // ------------------------------------------------------------------------------------------
 template <int CG, int R>
 __global__ void __launch_bounds__(128) k_ks_ip_hoisted_f64(KsHoistMultiJob job, Tables tb) {
+    // each thread's CG D words and 2R key words of digit j + 1 are copied into its own slots of a
+    // double-buffered shared stage (cp.async) while digit j is multiplied: ncu of the direct-load
+    // form (profiles/r2_ncu_k7_v2.txt) had 61 % of its stall samples on those loads
+    constexpr int W = CG + 2 * R;
+    extern __shared__ uint64_t k7sm[];                          // [2][W][128]
     const int ri = job.ri_list[blockIdx.y];
     const int l1 = job.l1, l2 = l1 + 1;
     const long long N = 1ll << tb.log_n;
@@ -757,25 +568,48 @@ __global__ void __launch_bounds__(128) k_ks_ip_hoisted_f64(KsHoistMultiJob job, 
     const int mi = job.mod_map[ri];
     const double2 qd = tb.modd[mi];
     const double q = qd.x, qinv = qd.y;
-    double acc[CG][R][2];
-#pragma unroll
-    for (int c = 0; c < CG; c++)
-#pragma unroll
-        for (int k = 0; k < R; k++) { acc[c][k][0] = 0.0; acc[c][k][1] = 0.0; }
-    for (int j = 0; j < l1; j++) {
-        double d[CG];
+    const int tid = threadIdx.x;
+    auto issue = [&](int j, int buf) {
+        uint64_t* st = k7sm + buf * W * 128 + tid;
 #pragma unroll
         for (int c = 0; c < CG; c++) {
             const uint64_t* src = (j == ri) ? job.diag[c] + (long long)j * N + x
                                             : job.D[c] + ((long long)j * l2 + ri) * N + x;
-            d[c] = u2d(__ldcs(src));
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(st + c * 128);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src) : "memory");
         }
 #pragma unroll
         for (int k = 0; k < R; k++) {
             const int kL = job.kL[k];
             const long long kstride_p = (long long)(kL + 1) * N;
             const uint64_t* kb = job.key[k] + j * 2 * kstride_p + (long long)(ri < l1 ? ri : kL) * N + x;
-            const double Kb = u2d(__ldcs(kb)), Ka = u2d(__ldcs(kb + kstride_p));
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(st + (CG + 2 * k) * 128);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(kb) : "memory");
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa + 1024u), "l"(kb + kstride_p)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    double acc[CG][R][2];
+#pragma unroll
+    for (int c = 0; c < CG; c++)
+#pragma unroll
+        for (int k = 0; k < R; k++) { acc[c][k][0] = 0.0; acc[c][k][1] = 0.0; }
+    issue(0, 0);
+    for (int j = 0; j < l1; j++) {
+        if (j + 1 < l1) {
+            issue(j + 1, (j + 1) & 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        const uint64_t* st = k7sm + (j & 1) * W * 128 + tid;
+        double d[CG];
+#pragma unroll
+        for (int c = 0; c < CG; c++) d[c] = u2d(st[c * 128]);
+#pragma unroll
+        for (int k = 0; k < R; k++) {
+            const double Kb = kd(st[(CG + 2 * k) * 128]), Ka = kd(st[(CG + 2 * k + 1) * 128]);   // internal format
 #pragma unroll
             for (int c = 0; c < CG; c++) {
                 acc[c][k][0] = __dadd_rn(acc[c][k][0], mulred(d[c], Kb, q, qinv));
@@ -869,7 +703,8 @@ cudaError_t launch_ks_ip_hoisted_multi(const KsHoistMultiJob& job_in, int R, con
     if (nfp) {
         memcpy(job.ri_list, fp, nfp);
         dim3 grid((unsigned)((N + 127) / 128), nfp, 1);
-#define C(CGV, RV) if (job.cg == CGV && R == RV) { k_ks_ip_hoisted_f64<CGV, RV><<<grid, 128, 0, st>>>(job, tb); } else
+#define C(CGV, RV) if (job.cg == CGV && R == RV) { \
+            k_ks_ip_hoisted_f64<CGV, RV><<<grid, 128, (size_t)2 * (CGV + 2 * RV) * 128 * 8, st>>>(job, tb); } else
         C(4, 1) C(4, 2) C(4, 3) C(4, 4) C(2, 1) C(2, 2) C(2, 3) C(2, 4) C(3, 1) C(3, 2) C(3, 3) C(3, 4)
         C(1, 1) C(1, 2) C(1, 3) C(1, 4) return cudaErrorInvalidValue;
 #undef C

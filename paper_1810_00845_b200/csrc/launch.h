@@ -31,6 +31,8 @@ struct ElemJob {
     long long a_poly, b_poly, out_poly;  // poly strides (words)
     uint64_t scal[MAXL];    // per-limb scalar residues (add/mul scalar)
     uint64_t scalp[MAXL];   // Shoup companions
+    uint64_t fp_mods;       // bit i: limb i's products on the FP64 pipe (exact mulred); 0 = integer
+    const double2* modd;    // (q, 1/q) per limb (needed when fp_mods != 0)
 };
 cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, cudaStream_t st);
 

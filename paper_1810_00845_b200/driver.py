@@ -444,7 +444,11 @@ class EncryptedNet:
             v = np.zeros(self.slots)
             v[idx] = 1.0
             return v
-        ms = [self.b.mul_plain(ct, self._plaintext(("mask", li), vals, self._level(ct))) for ct in cts]
+        pts = [self._plaintext(("mask", li), vals, self._level(ct)) for ct in cts]
+        if hasattr(self.b, "mul_plain_batch"):   # one launch for the layer's channels
+            ms = self.b.mul_plain_batch(list(cts), pts)
+        else:
+            ms = [self.b.mul_plain(ct, pt) for ct, pt in zip(cts, pts)]
         out = self.b.rescale_batch(ms)
         self._free_all(ms)
         return out, replace(lay, clean=True)

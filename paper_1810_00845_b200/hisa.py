@@ -92,6 +92,7 @@ _SIGS = {
     "hisa_rot_add_batch": [_vp, _u64p, _csz, _ci64, _u64p],
     "hisa_mul_batch": [_vp, _u64p, _u64p, _csz, _u64p],
     "hisa_rescale_batch": [_vp, _u64p, _csz, _u64p],
+    "hisa_mul_plain_batch": [_vp, _u64p, _u64p, _csz, _u64p],
     "hisa_mul_plain_accumulate": [_vp, _u64p, _csz, _u64p, _csz, _u64p],
     "hisa_ct_adopt_sum": [_vp, _vp, _ci, _ci, _cd, _u64p],
     "hisa_ntt": [_vp, _cu64, _ci],
@@ -395,6 +396,13 @@ def hisa_rot_add_batch(ctx, cts, k: int) -> list[int]:
     ins = _u64(list(cts))
     outs = np.zeros(ins.size, dtype=np.uint64)
     _chk(load().hisa_rot_add_batch(ctx, _ptr(ins, _u64p), ins.size, k, _ptr(outs, _u64p)))
+    return [int(x) for x in outs]
+
+
+def hisa_mul_plain_batch(ctx, cts, pts) -> list[int]:
+    a, p = _u64(list(cts)), _u64(list(pts))
+    outs = np.zeros(a.size, dtype=np.uint64)
+    _chk(load().hisa_mul_plain_batch(ctx, _ptr(a, _u64p), _ptr(p, _u64p), a.size, _ptr(outs, _u64p)))
     return [int(x) for x in outs]
 
 

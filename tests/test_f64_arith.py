@@ -167,3 +167,47 @@ def test_lazy_schedule_accepts_wide_lift():
         assert t == int(t) and (int(t) - int(a) * w) % q == 0
         assert abs(t) <= q / 2 + 0.75 * 2 ** -52 * abs(a) * q + 1
         assert abs(redd(a, qf, qinv)) <= 0.5 * q + 1
+
+
+@pytest.mark.parametrize("q", _primes_near_2_50())
+def test_k4_row_schedule(q):
+    """K4 v6 (ks_kernels.cu k4_full): the 8-stage row pass re-centres X at stages 0, 4, 7 only.  From
+    a column-pass output (|v| <= 2.41 q, also driven by the greedy twiddle adversary) every value is
+    an exact integer congruent to the textbook butterfly's, magnitudes stay <= 4.3 q (< 2^52.1), the
+    output is <= 1.7 q, and the MAC that consumes it (a key word |K| <= q/2, the internal key
+    format) stays <= 0.82 q, so eight of them sum below 7.1 q < 2^53."""
+    rng = random.Random(q * 11)
+    qf, qinv = float(q), 1.0 / float(q)
+    M = 256
+    half = (q - 1) // 2
+    cands = [half, -half, half - 1, -(half - 1), 1, -1]
+    full = {0, 4, 7}
+    for trial in range(4):
+        adversary = trial % 2 == 1
+        # a column-pass output: the lazy column schedule from canonical inputs (<= 2.41 q)
+        x = [float(rng.randrange(-int(2.41 * q), int(2.41 * q))) for _ in range(M)]
+        xi = [int(v) % q for v in x]
+        top_all = 0.0
+        for u in range(8):
+            dist = M >> (u + 1)
+            for blk in range(0, M, 2 * dist):
+                w = rng.choice(cands) if not adversary else None
+                for e in range(blk, blk + dist):
+                    X = redd(x[e], qf, qinv) if u in full else x[e]
+                    if adversary:
+                        w = max((abs(mulred(x[e + dist], float(c), qf, qinv)), c) for c in cands[:2])[1]
+                    t = mulred(x[e + dist], float(w), qf, qinv)
+                    assert t == int(t) and abs(t) < 2 ** 53
+                    ti = (xi[e + dist] * w) % q
+                    assert (int(t) - ti) % q == 0
+                    x[e], x[e + dist] = X + t, X - t
+                    xi[e], xi[e + dist] = (xi[e] + ti) % q, (xi[e] - ti) % q
+            top = max(abs(v) for v in x)
+            top_all = max(top_all, top)
+            assert top < 2 ** 52.1 and top <= 4.3 * q, (u, top / q)
+        assert all((int(v) - vi) % q == 0 for v, vi in zip(x, xi))
+        assert max(abs(v) for v in x) <= 1.7 * q
+        for d in x[:64]:
+            for k in (half, -half, 0, 1):
+                m = mulred(d, float(k), qf, qinv)
+                assert (int(m) - int(d) * k) % q == 0 and abs(m) <= 0.82 * q

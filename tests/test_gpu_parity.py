@@ -474,3 +474,19 @@ def test_gpu_decode_batch(pair):
         assert (got[i] == g.decode(h, n)).all()
     assert g.decode_batch([], n).shape == (0, n)
     assert g.decode_batch(hs[:1], 0).shape == (1, 0)
+
+
+def test_mul_plain_batch(pair):
+    """hisa_mul_plain_batch: n mulPlains in one launch equal the per-pair oracle products; mixed
+    levels are refused; an empty batch is a no-op."""
+    g, o = pair.g, pair.o
+    hs, ocs = zip(*[pair.ct(500 + i) for i in range(3)])
+    ps, ops = zip(*[pair.pt(600 + i) for i in range(3)])
+    for h, oc, op in zip(g.mul_plain_batch(list(hs), list(ps)), ocs, ops):
+        pair.same(h, o.mul_plain(oc, op))
+    assert g.mul_plain_batch([], []) == []
+    if o.L > 1:
+        lo = g.mod_switch(hs[0], 1)
+        with pytest.raises(H.HisaError) as ei:
+            g.mul_plain_batch([lo, hs[1]], [ps[0], ps[1]])
+        assert ei.value.code == "LEVEL_MISMATCH"

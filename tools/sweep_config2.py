@@ -84,7 +84,7 @@ def main():
                     elif op == "intt":
                         ctx.ntt_batch(cts, True)
                     elif op == "mulplain":
-                        outs = [ctx.mul_plain(c, p) for c, p in zip(cts, pts_)]
+                        outs = ctx.mul_plain_batch(cts, pts_)
                     elif op == "mul_relin":
                         outs = ctx.mul_batch(cts, cts)
                     elif op == "rotate":
