@@ -21,22 +21,17 @@
 // Bit-exact integer arithmetic: the same residues as the FP64 / 128-bit CUDA-core kernel.
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include "launch.h"
 #include "modarith.cuh"
-
-#ifndef CTC_TMEM_COLS
-#define CTC_TMEM_COLS 256
-#define CTC_MAXG_TILES 1
-#endif
 
 namespace hisa {
 
 constexpr int CTC_ROWS = 128, CTC_K = 32, CTC_OT = 16, CTC_THREADS = 256;
 constexpr int CTC_PLANE = CTC_ROWS * CTC_K;   // bytes per A plane (4 KiB)
-constexpr int CTC_BIMG = 8 * 512;             // bytes per weight image slot (P <= 8)
-constexpr int CTC_TMEM = CTC_TMEM_COLS;       // TMEM columns per CTA
-constexpr int CTC_MAXG = CTC_MAXG_TILES;      // output tiles per pass (TMEM: G (2P - 1) 16 <= CTC_TMEM;
-                                              // 512 columns / 3 tiles measured slower: one CTA per SM)
+constexpr int CTC_BIMG = 8 * 512;             // bytes per weight image slot in global memory (P <= 8)
+constexpr int CTC_TMEM = 256;                 // TMEM columns per CTA: (2P - 1) 16 <= 240; two CTAs per SM
+constexpr int CTC_BREG = 6;                   // prefetched weight-image uint4 per thread (KC P <= 48)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -83,26 +78,42 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
         }
     }
 }
-__device__ __forceinline__ uint32_t pick_byte(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t i) {
-    // byte i (0..3) of each of a, b, c, d -> one word (a in the low byte)
-    const uint32_t sel = i | ((i + 4) << 4);
-    const uint32_t lo = __byte_perm(a, b, sel), hi = __byte_perm(c, d, sel);
-    return __byte_perm(lo, hi, 0x5410);
+// 4 x 4 byte transpose: words a, b, c, d (inputs k .. k + 3 of one row) -> p[i] = byte i of
+// (a, b, c, d), a in the low byte: 8 PRMT for four planes
+__device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t* p) {
+    const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+    const uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+    p[0] = __byte_perm(t0, t2, 0x5410);
+    p[1] = __byte_perm(t0, t2, 0x7632);
+    p[2] = __byte_perm(t1, t3, 0x5410);
+    p[3] = __byte_perm(t1, t3, 0x7632);
+}
+__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c) {
+    uint64_t d;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
 }
 
+// Schedule (round 2): the byte split of the inputs is the expensive CUDA-core part (ncu of the
+// round-1 kernel, profiles/r1_ncu_conv_tc.txt: issue-bound, tensor pipe 6 % busy, because every
+// 16-output tile re-loaded and re-split all T inputs).  Now a CTA splits a super-chunk of KC
+// K-chunks (32 KC inputs) of its 128 words ONCE into shared memory (A planes [kc][i], 4 KiB each)
+// and then walks the output tiles: per tile only the pre-split weight image (prefetched into
+// registers during the previous tile's epilogue) is stored, one thread issues the tile's KC P MMAs
+// and a single commit, and the epilogue folds the 2P - 1 diagonal sums four at a time with
+// IMAD.WIDE (C_4k + 2^8 C_4k+1 + 2^16 C_4k+2 + 2^24 C_4k+3 < 2^56) into two 128-bit halves and one
+// Barrett step (two for P = 8).  T > 32 KC: further super-chunks add onto the stored outputs.
+// KC = what fits the dynamic shared memory given by the launcher (two CTAs per SM when the whole T
+// fits in half an SM's shared memory, else one).
 __global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* __restrict__ in_ptrs,
                                                  uint64_t* const* __restrict__ out_ptrs,
                                                  const uint8_t* __restrict__ wimg, ConvTcJob job,
-                                                 const Mod* __restrict__ mods) {
-    extern __shared__ __align__(1024) uint8_t ctc_sm[];
-    // two buffers: buffer b = [P planes of A, 128 rows x 32 bytes][B: 16 P rows x 32 bytes]
-    constexpr int BUF = 8 * CTC_PLANE + CTC_MAXG * CTC_BIMG;
-    // the T input pointers (offset to this tile) staged once, after the two operand buffers
-    const uint64_t** sptr = reinterpret_cast<const uint64_t**>(ctc_sm + 2 * BUF);
+                                                 const Mod* __restrict__ mods, int smem_ab) {
+    extern __shared__ __align__(128) uint8_t ctc_sm[];
     __shared__ __align__(8) uint64_t mbar[1];
     __shared__ uint32_t tmem_slot;
-    // two warpgroups: warpgroup wg splits the K-chunks 2 step + wg into its own operand buffer;
-    // thread r = tid % 128 owns row r (TMEM lane r: warp w reads lanes 32 (w % 4) ..)
+    // thread r = tid % 128 owns row r (TMEM lane r: warp w reads lanes 32 (w % 4) ..); the two
+    // warpgroups split alternate K-chunks in phase 1 and the two output halves in the epilogue
     const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, r = tid & 127;
     const long long N = 1ll << job.log_n;
     const int limb = job.limb_map[blockIdx.y];
@@ -110,7 +121,10 @@ __global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* 
     const Mod md = mods[limb];
     const long long off = (long long)blockIdx.z * job.poly_stride + (long long)limb * N + (long long)blockIdx.x * CTC_ROWS;
     const uint32_t bar0 = smem_u32(&mbar[0]);
-    for (int t = tid; t < job.T; t += CTC_THREADS) sptr[t] = in_ptrs[t] + off;
+    const int bimg = 512 * P;                                  // bytes of one chunk's weight image
+    const int KC = min(min(job.n_chunks, smem_ab / (P * CTC_PLANE + bimg)), CTC_BREG * CTC_THREADS / (32 * P));
+    uint8_t* sA = ctc_sm;                                      // [KC][P][4096]
+    uint8_t* sB = ctc_sm + KC * P * CTC_PLANE;                 // [KC][512 P]
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)), "n"(CTC_TMEM));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -127,115 +141,153 @@ __global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* 
     const int ndiag = 2 * P - 1;
     const uint32_t idesc = umma_idesc_u8(CTC_ROWS, 16 * P);
     uint32_t ph0 = 0;
-    bool pend = false;
     // this thread's row in the canonical layout: group r / 8 at 256 B, row r % 8 at 16 B
     const int arow_off = (r >> 3) * 256 + (r & 7) * 16;
-    uint8_t* sA = ctc_sm + wg * BUF;
-    uint8_t* sB = sA + 8 * CTC_PLANE;
-    const int n_steps = (job.n_chunks + 1) / 2;
-    // G output tiles per pass share every input split (TMEM holds G x (2P - 1) x 16 columns)
-    const int G = min(CTC_MAXG, CTC_TMEM / (16 * ndiag));
-    for (int oct0 = 0; oct0 < job.n_oct; oct0 += G) {
-        const int ng = min(G, job.n_oct - oct0);
-        if (wg == 0) {   // zero the pass's diagonal blocks (warpgroup 0 covers all 128 lanes)
-            for (int s = 0; s < ng * ndiag; s++) {
-                asm volatile(
-                    "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
-                    "%1, %1, %1, %1};\n" ::"r"(lane_base + 16 * s),
-                    "r"(0u));
+    for (int c0 = 0; c0 < job.n_chunks; c0 += KC) {
+        const int nk = min(KC, job.n_chunks - c0);
+        // weight image of (limb, tile, chunks c0 .. c0 + nk): nk * 32 P uint4, CTC_BREG per thread
+        const int nb4 = nk * 32 * P;
+        uint4 breg[CTC_BREG];
+        auto fetch_b = [&](int oct) {
+            const uint8_t* base = wimg + (((size_t)limb * job.n_oct + oct) * job.n_chunks + c0) * CTC_BIMG;
+#pragma unroll
+            for (int k = 0; k < CTC_BREG; k++) {
+                const int u = tid + k * CTC_THREADS;
+                if (u < nb4) {
+                    const int kc = u / (32 * P), w = u - kc * 32 * P;
+                    breg[k] = __ldg(reinterpret_cast<const uint4*>(base + (size_t)kc * CTC_BIMG) + w);
+                }
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        }
-        for (int step = 0; step < n_steps; step++) {
-            const int ch = 2 * step + wg;
-            const bool active = ch < job.n_chunks;
-            // this warpgroup's chunk: loads in flight before waiting for the previous step's MMAs
+        };
+        fetch_b(0);
+        // phase 1: split this super-chunk's inputs once
+        for (int kc = wg; kc < nk; kc += 2) {
             uint32_t lo[CTC_K], hi[CTC_K];
 #pragma unroll
             for (int k = 0; k < CTC_K; k++) {
-                const int t = ch * CTC_K + k;
-                const uint64_t v = (active && t < job.T) ? __ldg(sptr[t] + r) : 0ull;
+                const int t = (c0 + kc) * CTC_K + k;
+                const uint64_t v = t < job.T ? __ldg(in_ptrs[t] + off + r) : 0ull;
                 lo[k] = (uint32_t)v;
                 hi[k] = (uint32_t)(v >> 32);
             }
-            if (pend) { mbar_wait(bar0, ph0); ph0 ^= 1; pend = false; }
-            if (active) {
-                for (int i = 0; i < P; i++) {
-                    const uint32_t* src = i < 4 ? lo : hi;
-                    const uint32_t bi = (uint32_t)(i & 3);
-                    uint32_t w[8];
+            uint8_t* a_ = sA + kc * P * CTC_PLANE + arow_off;
 #pragma unroll
-                    for (int u = 0; u < 8; u++)
-                        w[u] = pick_byte(src[4 * u], src[4 * u + 1], src[4 * u + 2], src[4 * u + 3], bi);
-                    *reinterpret_cast<uint4*>(sA + i * CTC_PLANE + arow_off) = make_uint4(w[0], w[1], w[2], w[3]);
-                    *reinterpret_cast<uint4*>(sA + i * CTC_PLANE + arow_off + 128) = make_uint4(w[4], w[5], w[6], w[7]);
+            for (int half = 0; half < 2; half++) {   // k 0..15 at +0, k 16..31 at +128
+                uint32_t w[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    uint32_t p[4];
+                    const int k = 16 * half + 4 * u;
+                    transpose4(lo[k], lo[k + 1], lo[k + 2], lo[k + 3], p);
+#pragma unroll
+                    for (int i = 0; i < 4; i++) w[i][u] = p[i];
                 }
-                // weights: the pre-split images of (limb, output tile, chunk) for the pass's tiles
-                for (int g = 0; g < ng; g++) {
-                    const uint4* wsrc = reinterpret_cast<const uint4*>(
-                        wimg + (((size_t)limb * job.n_oct + oct0 + g) * job.n_chunks + ch) * CTC_BIMG);
-                    for (int u = r; u < 32 * P; u += 128) reinterpret_cast<uint4*>(sB + g * CTC_BIMG)[u] = __ldg(wsrc + u);
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                    if (i < P)
+                        *reinterpret_cast<uint4*>(a_ + i * CTC_PLANE + 128 * half) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
+                if (P > 4) {
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        uint32_t p[4];
+                        const int k = 16 * half + 4 * u;
+                        transpose4(hi[k], hi[k + 1], hi[k + 2], hi[k + 3], p);
+#pragma unroll
+                        for (int i = 0; i < 4; i++) w[i][u] = p[i];
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; i++)
+                        if (4 + i < P)
+                            *reinterpret_cast<uint4*>(a_ + (4 + i) * CTC_PLANE + 128 * half) =
+                                make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
                 }
+            }
+        }
+        for (int oct = 0; oct < job.n_oct; oct++) {
+            if (wg == 0) {   // zero the tile's diagonal blocks (warpgroup 0 covers all 128 lanes)
+                for (int s = 0; s < ndiag; s++) {
+                    asm volatile(
+                        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+                        "%1, %1, %1, %1};\n" ::"r"(lane_base + 16 * s),
+                        "r"(0u));
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            }
+            // this tile's weight image (prefetched) -> shared memory, packed at 512 P per chunk
+#pragma unroll
+            for (int k = 0; k < CTC_BREG; k++) {
+                const int u = tid + k * CTC_THREADS;
+                if (u < nb4) reinterpret_cast<uint4*>(sB)[u] = breg[k];
             }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncthreads();
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             if (tid == 0) {
-                for (int h = 0; h < 2 && 2 * step + h < job.n_chunks; h++) {
-                    uint8_t* a_ = ctc_sm + h * BUF;
-                    for (int g = 0; g < ng; g++) {
-                        const uint64_t bdesc = umma_desc(smem_u32(a_ + 8 * CTC_PLANE + g * CTC_BIMG), 128, 256);
-                        for (int i = 0; i < P; i++)
-                            mma_u8(tmem + 16 * (g * ndiag + i), umma_desc(smem_u32(a_ + i * CTC_PLANE), 128, 256),
-                                   bdesc, idesc, 1u);
-                    }
+                for (int kc = 0; kc < nk; kc++) {
+                    const uint64_t bdesc = umma_desc(smem_u32(sB + kc * bimg), 128, 256);
+                    for (int i = 0; i < P; i++)
+                        mma_u8(tmem + 16 * i, umma_desc(smem_u32(sA + (kc * P + i) * CTC_PLANE), 128, 256), bdesc,
+                               idesc, 1u);
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
                              ::"r"(bar0) : "memory");
             }
-            pend = true;
-        }
-        if (pend) { mbar_wait(bar0, ph0); ph0 ^= 1; pend = false; }
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        // epilogue: row tid, outputs (oct0 + g) * 16 + o, in halves of 8
-        for (int gh = wg; gh < 2 * ng; gh += 2) {   // warpgroup wg: halves og = wg
-            const int g = gh >> 1, og = gh & 1;
-            const int oct = oct0 + g;
-            U128 accl[8], acch[8];
+            if (oct + 1 < job.n_oct) fetch_b(oct + 1);   // in flight across the MMAs and the epilogue
+            mbar_wait(bar0, ph0);
+            ph0 ^= 1;
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            // epilogue: row r, outputs oct * 16 + 8 wg + o, in quads
 #pragma unroll
-            for (int o = 0; o < 8; o++) { accl[o] = U128{0, 0}; acch[o] = U128{0, 0}; }
-            for (int s = 0; s < ndiag; s++) {
-                uint32_t r[8];
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
-                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                               "=r"(r[7])
-                             : "r"(lane_base + 16 * (g * ndiag + s) + 8 * og));
-                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                const int sh = 8 * (s & 7);
+            for (int qd = 0; qd < 2; qd++) {
+                uint64_t al[4], ah[4], bl[4], bh[4];   // accl = (al, ah): s < 8; acch = (bl, bh): s >= 8
 #pragma unroll
-                for (int o = 0; o < 8; o++) {
-                    const uint64_t cv = (uint64_t)r[o];
-                    const uint64_t l = sh ? cv << sh : cv, h = sh ? cv >> (64 - sh) : 0;
-                    U128& a = s < 8 ? accl[o] : acch[o];
-                    a.lo += l;
-                    a.hi += h + (a.lo < l);
+                for (int o = 0; o < 4; o++) { al[o] = ah[o] = bl[o] = bh[o] = 0; }
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    if (4 * k >= ndiag) break;
+                    uint32_t c[4][4];
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        if (4 * k + e < ndiag) {
+                            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                                         : "=r"(c[e][0]), "=r"(c[e][1]), "=r"(c[e][2]), "=r"(c[e][3])
+                                         : "r"(lane_base + 16 * (4 * k + e) + 8 * wg + 4 * qd));
+                        } else {
+                            c[e][0] = c[e][1] = c[e][2] = c[e][3] = 0;
+                        }
+                    }
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                    for (int o = 0; o < 4; o++) {
+                        uint64_t g = (uint64_t)c[0][o];
+                        g = mad_wide(c[1][o], 1u << 8, g);
+                        g = mad_wide(c[2][o], 1u << 16, g);
+                        g = mad_wide(c[3][o], 1u << 24, g);     // < 2^56
+                        if (k == 0) al[o] = g;
+                        else if (k == 1) { const uint64_t l = g << 32; al[o] += l; ah[o] = (g >> 32) + (al[o] < l); }
+                        else if (k == 2) bl[o] = g;
+                        else { const uint64_t l = g << 32; bl[o] += l; bh[o] = (g >> 32) + (bl[o] < l); }
+                    }
+                }
+#pragma unroll
+                for (int o = 0; o < 4; o++) {
+                    const int oo = oct * CTC_OT + wg * 8 + qd * 4 + o;
+                    if (oo >= job.OC) continue;
+                    // value = accl + acch 2^64 (< 2^128 for P <= 7: one Barrett step; P = 8: the high
+                    // half is reduced first)
+                    const uint64_t rh = P > 7 ? barrett128(bl[o], bh[o], md) : bl[o];
+                    uint64_t v = barrett128(al[o], ah[o] + rh, md);
+                    uint64_t* dst = out_ptrs[oo] + off + r;
+                    if (c0) v = csub(v + *dst, md.q);
+                    *dst = v;
                 }
             }
-#pragma unroll
-            for (int o = 0; o < 8; o++) {
-                const int oo = oct * CTC_OT + og * 8 + o;
-                if (oo >= job.OC) continue;
-                // value = accl + acch 2^64: reduce the high half first (accl.hi < 2^32, r < 2^60)
-                const uint64_t rh = barrett128(acch[o].lo, acch[o].hi, md);
-                out_ptrs[oo][off + r] = barrett128(accl[o].lo, accl[o].hi + rh, md);
-            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncthreads();
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     }
-    __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(CTC_TMEM));
 }
 
@@ -287,16 +339,32 @@ bool conv_tc_timed_out() {
     return v != 0;
 }
 
-size_t conv_tc_smem_bytes(int T) { return 2 * (8 * CTC_PLANE + CTC_MAXG * CTC_BIMG) + (size_t)T * sizeof(void*); }
+// dynamic shared memory (A planes + weight images; the kernel derives KC from it): half an SM's
+// shared memory (two CTAs per SM) when every limb's whole T fits in it, else one CTA per SM with
+// KC P <= 48.  HISA_CONV_TC_SMEM (bytes) overrides it (tools/prof_conv_tc.py, the multi-super-chunk
+// parity case).
+size_t conv_tc_smem_bytes(int T) {
+    static long forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("HISA_CONV_TC_SMEM");
+        forced = e ? atol(e) : 0;
+    }
+    if (forced > 0) return (size_t)forced;
+    const size_t unit = CTC_PLANE + 512, half = 115200;
+    const size_t n_chunks = ((size_t)T + CTC_K - 1) / CTC_K;
+    if (n_chunks * 5 * unit <= half) return half;
+    return 48 * unit;
+}
 
 cudaError_t launch_conv_tc(const uint64_t* const* in_ptrs, uint64_t* const* out_ptrs, const uint8_t* wimg,
                            const ConvTcJob& job, int nlimbs, const Mod* mods, cudaStream_t st) {
     const long long N = 1ll << job.log_n;
     if (N % CTC_ROWS) return cudaErrorInvalidValue;
     const size_t smem = conv_tc_smem_bytes(job.T);
+    if (smem < 8 * (CTC_PLANE + 512)) return cudaErrorInvalidValue;   // KC >= 1 for P = 8
     cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((unsigned)(N / CTC_ROWS), (unsigned)nlimbs, 2);
-    k_conv_tc<<<grid, CTC_THREADS, smem, st>>>(in_ptrs, out_ptrs, wimg, job, mods);
+    k_conv_tc<<<grid, CTC_THREADS, smem, st>>>(in_ptrs, out_ptrs, wimg, job, mods, (int)smem);
     return cudaGetLastError();
 }
 

@@ -277,7 +277,7 @@ class EncryptedNet:
     channels across ranks; None = single GPU."""
 
     def __init__(self, backend, net: dict, weights, act_coeffs, group=None, rot_policy: str = "exact",
-                 partition: str = "ic"):
+                 partition: str = "ic", exchange_at_world1: bool = False):
         """rot_policy: "exact" = one key per distinct rotation amount, chosen by the compiler
         (CHET); "pow2" = HEAAN's default power-of-two keys (left and right),
         every other amount composed from them (the baseline of the paper's Fig. rotopt).
@@ -305,6 +305,10 @@ class EncryptedNet:
             self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         else:
             self.rank, self.world = 0, 1
+        # the exchange code path (reduce-scatter / all-gather, adoption of the int64 sums) runs
+        # when there is more than one rank -- or, on request, on a one-rank group: the only way
+        # to drive the NCCL data plane on a single-GPU box (tests/test_nccl_world1.py)
+        self.sharded = self.world > 1 or (group is not None and exchange_at_world1)
 
     # ---- planning (symbolic execution) ------------------------------------------------------
     @staticmethod
@@ -607,7 +611,7 @@ class EncryptedNet:
             masked = True
         else:
             masked = False
-        oc_part = self.world > 1 and self.partition == "oc"
+        oc_part = self.sharded and self.partition == "oc"
         if oc_part:                               # north-star baseline: every rank holds all inputs
             gathered = self._gather(cts, lay.C)
             if masked:
@@ -647,7 +651,7 @@ class EncryptedNet:
     def _gather(self, cts, n: int):
         """All n channels of a sharded layer on every rank (NCCL all-gather); fresh
         handles (the caller frees them).  Single GPU: copies."""
-        if self.world == 1:
+        if not self.sharded:
             return [self.b.copy(h) for h in cts]
         from . import parallel
         return parallel.gather_outputs(self, cts, n)
@@ -662,7 +666,7 @@ class EncryptedNet:
         """sum_t W[o, t] rotated[t] for o < n_out (pre-rescale).  Single GPU: one fused kernel.
         Multi-GPU: partial sums over this rank's inputs for ALL outputs, NCCL reduce-scatter,
         mod-q fix-up; returns the outputs this rank owns (owned(n_out))."""
-        if self.world == 1:
+        if not self.sharded:
             return self.b.conv_accumulate(rotated, wmat.ravel())
         from . import parallel
         return parallel.reduce_scatter_partials(self, rotated, wmat, n_out)
@@ -764,7 +768,7 @@ class EncryptedNet:
     def _fc_inputs(self, cts, n: int):
         """SURVEY 8e FC plan: the FC's inputs all-gathered to every rank (returns (all inputs,
         temporaries to free)); single GPU: the inputs themselves."""
-        if self.world == 1:
+        if not self.sharded:
             return list(cts), []
         allc = self._gather(cts, n)
         return allc, allc
@@ -916,7 +920,7 @@ class EncryptedNet:
         """forward() followed, under a process group, by the final all-gather: every rank ends
         with all output ciphertexts (rank 0 decrypts)."""
         out, lay = self.forward(cts, lay)
-        if self.world > 1:
+        if self.sharded:
             from . import parallel
             allc = parallel.gather_outputs(self, out, lay.C)
             self._free_all(out)

@@ -177,12 +177,16 @@ def test_conv_engines_bit_identical(tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {}
-    for tc in ("1", "0"):
+    # "small": the tensor-core kernel with shared memory for ONE K-chunk per super-chunk, so the
+    # second (ragged) chunk goes through the add-onto-stored-outputs path on every limb
+    for tc, extra in (("1", {}), ("0", {}), ("small", {"HISA_CONV_TC": "1", "HISA_CONV_TC_SMEM": str(8 * 4608)})):
         out = tmp_path / f"conv_{tc}.npy"
         env = dict(os.environ, HISA_CONV_TC=tc)
+        env.update(extra)
         subprocess.run([sys.executable, "-c", _ENGINE_SCRIPT % root, str(out)], env=env, check=True, timeout=600)
         res[tc] = np.load(out)
     assert res["1"].shape == res["0"].shape and (res["1"] == res["0"]).all()
+    assert (res["small"] == res["1"]).all()
     o = Oracle(16, [60, 50, 40], 60, seed=4)
     rng = np.random.default_rng(2)
     T, OC = 45, 19
