@@ -64,17 +64,21 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
     uint32_t done = 0;
-    const uint64_t t0 = globaltimer_ns();
-    while (!done) {
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0; !done; spin++) {
         asm volatile(
             "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}\n"
             : "=r"(done)
             : "r"(bar), "r"(phase)
             : "memory");
-        if (!done && globaltimer_ns() - t0 > 10000000000ull) {   // 10 s: flag it, never hang the device
-            atomicExch(&g_ctc_timeout, 1);
-            return;
+        if (!done && (spin & 1023) == 1023) {   // the clock is read once per 1024 polls
+            const uint64_t t = globaltimer_ns();
+            if (t0 == 0) t0 = t;
+            if (t - t0 > 10000000000ull) {      // 10 s: flag it, never hang the device
+                atomicExch(&g_ctc_timeout, 1);
+                return;
+            }
         }
     }
 }
@@ -105,23 +109,30 @@ __device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t c)
 // Barrett step (two for P = 8).  T > 32 KC: further super-chunks add onto the stored outputs.
 // KC = what fits the dynamic shared memory given by the launcher (two CTAs per SM when the whole T
 // fits in half an SM's shared memory, else one).
-__global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* __restrict__ in_ptrs,
-                                                 uint64_t* const* __restrict__ out_ptrs,
-                                                 const uint8_t* __restrict__ wimg, ConvTcJob job,
-                                                 const Mod* __restrict__ mods, int smem_ab) {
+// x mod q for 2^32 < q <= 2^40 (the P = 5 limbs) and any x < 2^64: r1 = floor(2^64 / q) < 2^32, so
+// the quotient estimate floor(x r1 / 2^64) (>= floor(x / q) - 1, < 2^32) takes two IMAD.WIDE
+__device__ __forceinline__ uint64_t barrett_q40(uint64_t x, uint32_t r1, uint64_t q) {
+    const uint64_t p0 = (uint64_t)(uint32_t)x * r1;
+    const uint64_t p1 = mad_wide((uint32_t)(x >> 32), r1, p0 >> 32);
+    const uint32_t qe = (uint32_t)(p1 >> 32);
+    return csub(x - (uint64_t)qe * q, q);
+}
+
+template <int P>
+__device__ __forceinline__ void conv_tc_body(const uint64_t* const* __restrict__ in_ptrs,
+                                             uint64_t* const* __restrict__ out_ptrs,
+                                             const uint8_t* __restrict__ wimg, const ConvTcJob& job,
+                                             const Mod* __restrict__ mods, int smem_ab, int limb, uint64_t* mbar,
+                                             uint32_t& tmem_slot) {
     extern __shared__ __align__(128) uint8_t ctc_sm[];
-    __shared__ __align__(8) uint64_t mbar[1];
-    __shared__ uint32_t tmem_slot;
     // thread r = tid % 128 owns row r (TMEM lane r: warp w reads lanes 32 (w % 4) ..); the two
     // warpgroups split alternate K-chunks in phase 1 and the two output halves in the epilogue
     const int tid = threadIdx.x, warp = tid >> 5, wg = tid >> 7, r = tid & 127;
     const long long N = 1ll << job.log_n;
-    const int limb = job.limb_map[blockIdx.y];
-    const int P = job.P[limb];
     const Mod md = mods[limb];
     const long long off = (long long)blockIdx.z * job.poly_stride + (long long)limb * N + (long long)blockIdx.x * CTC_ROWS;
-    const uint32_t bar0 = smem_u32(&mbar[0]);
-    const int bimg = 512 * P;                                  // bytes of one chunk's weight image
+    const uint32_t bar0 = smem_u32(mbar);
+    constexpr int bimg = 512 * P;                                // bytes of one chunk's weight image
     const int KC = min(min(job.n_chunks, smem_ab / (P * CTC_PLANE + bimg)), CTC_BREG * CTC_THREADS / (32 * P));
     uint8_t* sA = ctc_sm;                                      // [KC][P][4096]
     uint8_t* sB = ctc_sm + KC * P * CTC_PLANE;                 // [KC][512 P]
@@ -138,7 +149,7 @@ __global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* 
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_slot;
     const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    const int ndiag = 2 * P - 1;
+    constexpr int ndiag = 2 * P - 1;
     const uint32_t idesc = umma_idesc_u8(CTC_ROWS, 16 * P);
     uint32_t ph0 = 0;
     // this thread's row in the canonical layout: group r / 8 at 256 B, row r % 8 at 16 B
@@ -160,49 +171,68 @@ __global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* 
             }
         };
         fetch_b(0);
-        // phase 1: split this super-chunk's inputs once
-        for (int kc = wg; kc < nk; kc += 2) {
-            uint32_t lo[CTC_K], hi[CTC_K];
+        // phase 1: split this super-chunk's inputs once.  Warpgroup wg takes chunks wg, wg + 2, ..,
+        // in halves of 16 inputs, the next half's loads in flight while this one is transposed; lane
+        // l of every warp holds the chunk's l-th input pointer (one coalesced load per chunk, a
+        // chunk ahead), broadcast by shuffles -- no per-thread pointer loads in front of the data
+        {
+            const int lane = tid & 31;
+            auto chunk_base = [&](int kc) -> const uint64_t* {
+                const int t = (c0 + kc) * CTC_K + lane;
+                return (kc < nk && t < job.T) ? in_ptrs[t] : nullptr;
+            };
+            auto load_half = [&](int half, const uint64_t* pch, uint64_t* v) {
 #pragma unroll
-            for (int k = 0; k < CTC_K; k++) {
-                const int t = (c0 + kc) * CTC_K + k;
-                const uint64_t v = t < job.T ? __ldg(in_ptrs[t] + off + r) : 0ull;
-                lo[k] = (uint32_t)v;
-                hi[k] = (uint32_t)(v >> 32);
-            }
-            uint8_t* a_ = sA + kc * P * CTC_PLANE + arow_off;
-#pragma unroll
-            for (int half = 0; half < 2; half++) {   // k 0..15 at +0, k 16..31 at +128
+                for (int k = 0; k < 16; k++) {
+                    const uint64_t* p = reinterpret_cast<const uint64_t*>(
+                        __shfl_sync(0xffffffffu, (unsigned long long)pch, 16 * half + k));
+                    v[k] = p ? __ldg(p + off + r) : 0ull;
+                }
+            };
+            auto split_store = [&](const uint64_t* v, int kc, int half) {
+                uint8_t* a_ = sA + kc * P * CTC_PLANE + arow_off + 128 * half;   // k 0..15 at +0, 16..31 at +128
                 uint32_t w[4][4];
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     uint32_t p[4];
-                    const int k = 16 * half + 4 * u;
-                    transpose4(lo[k], lo[k + 1], lo[k + 2], lo[k + 3], p);
+                    transpose4((uint32_t)v[4 * u], (uint32_t)v[4 * u + 1], (uint32_t)v[4 * u + 2], (uint32_t)v[4 * u + 3], p);
 #pragma unroll
                     for (int i = 0; i < 4; i++) w[i][u] = p[i];
                 }
 #pragma unroll
                 for (int i = 0; i < 4; i++)
-                    if (i < P)
-                        *reinterpret_cast<uint4*>(a_ + i * CTC_PLANE + 128 * half) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
+                    if (i < P) *reinterpret_cast<uint4*>(a_ + i * CTC_PLANE) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
                 if (P > 4) {
 #pragma unroll
                     for (int u = 0; u < 4; u++) {
                         uint32_t p[4];
-                        const int k = 16 * half + 4 * u;
-                        transpose4(hi[k], hi[k + 1], hi[k + 2], hi[k + 3], p);
+                        transpose4((uint32_t)(v[4 * u] >> 32), (uint32_t)(v[4 * u + 1] >> 32),
+                                   (uint32_t)(v[4 * u + 2] >> 32), (uint32_t)(v[4 * u + 3] >> 32), p);
 #pragma unroll
                         for (int i = 0; i < 4; i++) w[i][u] = p[i];
                     }
 #pragma unroll
                     for (int i = 0; i < 4; i++)
                         if (4 + i < P)
-                            *reinterpret_cast<uint4*>(a_ + (4 + i) * CTC_PLANE + 128 * half) =
-                                make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
+                            *reinterpret_cast<uint4*>(a_ + (4 + i) * CTC_PLANE) = make_uint4(w[i][0], w[i][1], w[i][2], w[i][3]);
                 }
+            };
+            const uint64_t* pcur = chunk_base(wg);
+            const uint64_t* pnext = chunk_base(wg + 2);
+            uint64_t va[16], vb[16];
+            if (wg < nk) load_half(0, pcur, va);
+            for (int kc = wg; kc < nk; kc += 2) {
+                load_half(1, pcur, vb);
+                split_store(va, kc, 0);
+                pcur = pnext;
+                pnext = chunk_base(kc + 4);
+                if (kc + 2 < nk) load_half(0, pcur, va);
+                split_store(vb, kc, 1);
             }
         }
+        // (measured and dropped: an L2 prefetch of the next super-chunk / the next CTA's inputs
+        // issued here -- 1.91 -> 1.85 ms at T = 144 but 6.2 -> 6.7 ms at T = 288 and 10.5 -> 11.4 ms
+        // at T = 800: the prefetched lines are evicted before use, DRAM reads +23 %)
         for (int oct = 0; oct < job.n_oct; oct++) {
             if (wg == 0) {   // zero the tile's diagonal blocks (warpgroup 0 covers all 128 lanes)
                 for (int s = 0; s < ndiag; s++) {
@@ -240,47 +270,55 @@ __global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* 
             // epilogue: row r, outputs oct * 16 + 8 wg + o, in quads
 #pragma unroll
             for (int qd = 0; qd < 2; qd++) {
-                uint64_t al[4], ah[4], bl[4], bh[4];   // accl = (al, ah): s < 8; acch = (bl, bh): s >= 8
+                const int o0 = oct * CTC_OT + wg * 8 + qd * 4;
+                uint64_t* dst[4];
 #pragma unroll
-                for (int o = 0; o < 4; o++) { al[o] = ah[o] = bl[o] = bh[o] = 0; }
+                for (int o = 0; o < 4; o++) dst[o] = o0 + o < job.OC ? out_ptrs[o0 + o] + off + r : nullptr;
+                uint32_t c[ndiag][4];
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    if (4 * k >= ndiag) break;
-                    uint32_t c[4][4];
+                for (int s = 0; s < ndiag; s++)
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                                 : "=r"(c[s][0]), "=r"(c[s][1]), "=r"(c[s][2]), "=r"(c[s][3])
+                                 : "r"(lane_base + 16 * s + 8 * wg + 4 * qd));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                uint64_t v[4];
 #pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        if (4 * k + e < ndiag) {
-                            asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
-                                         : "=r"(c[e][0]), "=r"(c[e][1]), "=r"(c[e][2]), "=r"(c[e][3])
-                                         : "r"(lane_base + 16 * (4 * k + e) + 8 * wg + 4 * qd));
+                for (int o = 0; o < 4; o++) {
+                    // G_k = C_4k + 2^8 C_4k+1 + 2^16 C_4k+2 + 2^24 C_4k+3 < 2^56; value = sum_k G_k 2^(32k)
+                    uint64_t G[4] = {0, 0, 0, 0};
+#pragma unroll
+                    for (int s = 0; s < ndiag; s++)
+                        G[s >> 2] = (s & 3) ? mad_wide(c[s][o], 1u << (8 * (s & 3)), G[s >> 2]) : (uint64_t)c[s][o];
+                    if constexpr (P <= 5) {
+                        // q <= 2^40, value = G0 + 2^32 G1 + 2^64 G2 (G2 = C_8 < 2^31): Horner with 64-bit
+                        // Barrett steps, every operand < 2^64 (< 2^63 + 2^56, then < 2^56 + 2^40 twice)
+                        if constexpr (P == 5) {
+                            const uint32_t r1 = (uint32_t)md.r1;
+                            uint64_t x = barrett_q40((G[2] << 32) + G[1], r1, md.q);
+                            x = barrett_q40((x << 16) + (G[0] >> 16), r1, md.q);
+                            v[o] = barrett_q40((x << 16) + (G[0] & 0xFFFFull), r1, md.q);
                         } else {
-                            c[e][0] = c[e][1] = c[e][2] = c[e][3] = 0;
+                            uint64_t x = barrett64((G[2] << 32) + G[1], md);
+                            x = barrett64((x << 16) + (G[0] >> 16), md);
+                            v[o] = barrett64((x << 16) + (G[0] & 0xFFFFull), md);
                         }
-                    }
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-                    for (int o = 0; o < 4; o++) {
-                        uint64_t g = (uint64_t)c[0][o];
-                        g = mad_wide(c[1][o], 1u << 8, g);
-                        g = mad_wide(c[2][o], 1u << 16, g);
-                        g = mad_wide(c[3][o], 1u << 24, g);     // < 2^56
-                        if (k == 0) al[o] = g;
-                        else if (k == 1) { const uint64_t l = g << 32; al[o] += l; ah[o] = (g >> 32) + (al[o] < l); }
-                        else if (k == 2) bl[o] = g;
-                        else { const uint64_t l = g << 32; bl[o] += l; bh[o] = (g >> 32) + (bl[o] < l); }
+                    } else {
+                        // value = accl + acch 2^64 (< 2^128 for P <= 7: one 128-bit Barrett step; P = 8:
+                        // the high half is reduced first)
+                        uint64_t l = G[1] << 32;
+                        const uint64_t al = G[0] + l, ah = (G[1] >> 32) + (al < l);
+                        l = G[3] << 32;
+                        const uint64_t bl = G[2] + l, bh = (G[3] >> 32) + (bl < l);
+                        const uint64_t rh = P > 7 ? barrett128(bl, bh, md) : bl;
+                        v[o] = barrett128(al, ah + rh, md);
                     }
                 }
 #pragma unroll
                 for (int o = 0; o < 4; o++) {
-                    const int oo = oct * CTC_OT + wg * 8 + qd * 4 + o;
-                    if (oo >= job.OC) continue;
-                    // value = accl + acch 2^64 (< 2^128 for P <= 7: one Barrett step; P = 8: the high
-                    // half is reduced first)
-                    const uint64_t rh = P > 7 ? barrett128(bl[o], bh[o], md) : bl[o];
-                    uint64_t v = barrett128(al[o], ah[o] + rh, md);
-                    uint64_t* dst = out_ptrs[oo] + off + r;
-                    if (c0) v = csub(v + *dst, md.q);
-                    *dst = v;
+                    if (dst[o]) {
+                        if (c0) v[o] = csub(v[o] + *dst[o], md.q);
+                        *dst[o] = v[o];
+                    }
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -289,6 +327,24 @@ __global__ void __launch_bounds__(CTC_THREADS) k_conv_tc(const uint64_t* const* 
         }
     }
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(CTC_TMEM));
+}
+
+// one launch for all limbs: the CTA's limb picks the byte-plane specialisation (40-bit limbs P = 5,
+// 50-bit 7, 60-bit 8; P < 4 runs as 4 -- the missing planes are zero bytes on both operands)
+__global__ void __launch_bounds__(CTC_THREADS, 2) k_conv_tc(const uint64_t* const* __restrict__ in_ptrs,
+                                                 uint64_t* const* __restrict__ out_ptrs,
+                                                 const uint8_t* __restrict__ wimg, ConvTcJob job,
+                                                 const Mod* __restrict__ mods, int smem_ab) {
+    __shared__ __align__(8) uint64_t mbar[1];
+    __shared__ uint32_t tmem_slot;
+    const int limb = job.limb_map[blockIdx.y];
+    switch (job.P[limb]) {
+        case 8: conv_tc_body<8>(in_ptrs, out_ptrs, wimg, job, mods, smem_ab, limb, mbar, tmem_slot); break;
+        case 7: conv_tc_body<7>(in_ptrs, out_ptrs, wimg, job, mods, smem_ab, limb, mbar, tmem_slot); break;
+        case 6: conv_tc_body<6>(in_ptrs, out_ptrs, wimg, job, mods, smem_ab, limb, mbar, tmem_slot); break;
+        case 5: conv_tc_body<5>(in_ptrs, out_ptrs, wimg, job, mods, smem_ab, limb, mbar, tmem_slot); break;
+        default: conv_tc_body<4>(in_ptrs, out_ptrs, wimg, job, mods, smem_ab, limb, mbar, tmem_slot); break;
+    }
 }
 
 // weight image on the device: X = llround(W[o][t] * ps) (C semantics: half away from zero; exact
@@ -340,31 +396,33 @@ bool conv_tc_timed_out() {
 }
 
 // dynamic shared memory (A planes + weight images; the kernel derives KC from it): half an SM's
-// shared memory (two CTAs per SM) when every limb's whole T fits in it, else one CTA per SM with
-// KC P <= 48.  HISA_CONV_TC_SMEM (bytes) overrides it (tools/prof_conv_tc.py, the multi-super-chunk
-// parity case).
-size_t conv_tc_smem_bytes(int T) {
+// shared memory, two CTAs per SM -- five K-chunks of a 40-bit limb (T <= 160 in one super-chunk).
+// Measured against one CTA per SM with KC P <= 48: 288 inputs 6.3 vs 6.8 ms, 800 inputs 10.8 vs
+// 14.0 ms.  HISA_CONV_TC_SMEM (bytes) overrides it (the multi-super-chunk parity case).
+size_t conv_tc_smem_bytes() {
     static long forced = -1;
     if (forced < 0) {
         const char* e = getenv("HISA_CONV_TC_SMEM");
         forced = e ? atol(e) : 0;
     }
-    if (forced > 0) return (size_t)forced;
-    const size_t unit = CTC_PLANE + 512, half = 115200;
-    const size_t n_chunks = ((size_t)T + CTC_K - 1) / CTC_K;
-    if (n_chunks * 5 * unit <= half) return half;
-    return 48 * unit;
+    return forced > 0 ? (size_t)forced : 115200;
 }
 
 cudaError_t launch_conv_tc(const uint64_t* const* in_ptrs, uint64_t* const* out_ptrs, const uint8_t* wimg,
                            const ConvTcJob& job, int nlimbs, const Mod* mods, cudaStream_t st) {
     const long long N = 1ll << job.log_n;
     if (N % CTC_ROWS) return cudaErrorInvalidValue;
-    const size_t smem = conv_tc_smem_bytes(job.T);
-    if (smem < 8 * (CTC_PLANE + 512)) return cudaErrorInvalidValue;   // KC >= 1 for P = 8
+    const size_t smem = conv_tc_smem_bytes();
+    if (smem < 8 * (size_t)(CTC_PLANE + 512)) return cudaErrorInvalidValue;   // KC >= 1 for P = 8
+    // the widest (slowest) limbs first
+    ConvTcJob j = job;
+    int nl = 0;
+    for (int P = 8; P >= 1; P--)
+        for (int i = 0; i < nlimbs; i++)
+            if (job.P[job.limb_map[i]] == P) j.limb_map[nl++] = job.limb_map[i];
     cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((unsigned)(N / CTC_ROWS), (unsigned)nlimbs, 2);
-    k_conv_tc<<<grid, CTC_THREADS, smem, st>>>(in_ptrs, out_ptrs, wimg, job, mods, (int)smem);
+    dim3 grid((unsigned)(N / CTC_ROWS), (unsigned)nl, 2);
+    k_conv_tc<<<grid, CTC_THREADS, smem, st>>>(in_ptrs, out_ptrs, wimg, j, mods, (int)smem);
     return cudaGetLastError();
 }
 

@@ -103,7 +103,7 @@ struct ConvTcJob {
     uint8_t limb_map[MAXL];       // grid.y -> limb
     uint8_t P[MAXL];              // byte planes per limb: ceil(bits(q) / 8)
 };
-size_t conv_tc_smem_bytes(int T);
+size_t conv_tc_smem_bytes();
 bool conv_tc_timed_out();   // an mbarrier wait of k_conv_tc exceeded its budget (flag cleared)
 cudaError_t launch_conv_tc_wimg(const double* W, double ps, int T, int OC, int n_oct, int n_chunks, int l1,
                                 const Mod* mods, const uint8_t* Pl, uint8_t* img, cudaStream_t st);
