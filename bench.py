@@ -720,6 +720,9 @@ def main():
         e2e = {"value": world * B * n_e2e / dt, "unit": UNIT, "h2d_bytes_per_step": B * words * 8,
                "d2h_bytes_per_step": B * words * 8, "steps": n_e2e,
                "pipeline": "3 streams: H2D(i+1) || key switch(i) || D2H(i-1), pinned host buffers",
+               "api": "torch pinned-memory copies + hisa_ct_adopt_device -> hisa_rot_left_batch -> "
+                      "hisa_ct_device_view (zero-copy hand-over); NOT the C-ABI's host-buffer calls "
+                      "hisa_ct_import / hisa_ct_export, which are synchronous and would serialise the copies",
                "result_check": e2e_ok}
 
     hoisted = None

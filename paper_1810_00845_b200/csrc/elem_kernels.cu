@@ -124,6 +124,88 @@ __global__ void __launch_bounds__(256) k_elem(ElemJob job, const Mod* __restrict
     }
 }
 
+// The HBM-bound binary ops with TWO word pairs per thread (pairs x and x + 256 of a 512-pair block),
+// all loads issued before the arithmetic: twice the bytes in flight per thread.  One pair per thread
+// left mulPlain at ~0.5 of measured HBM at N = 2^16 (profiles/r2_config2_sweep.txt): 2048 threads x
+// 32 B per SM in flight against ~3 us of loaded latency.  Same arithmetic as k_elem, bit for bit.
+template <int OP>
+__global__ void __launch_bounds__(256) k_elem2(ElemJob job, const Mod* __restrict__ mods) {
+    constexpr int U = 2;
+    const int z = blockIdx.z;
+    const int p = (int)blockIdx.y / job.nl;
+    const int i = (int)blockIdx.y - p * job.nl;
+    const long long w0 = (blockIdx.x * (256ll * U) + threadIdx.x) * 2;   // pair u at word w0 + 512 u
+    const Mod md = mods[i];
+    const uint64_t q = md.q;
+    const long long limb_off = (long long)i << job.log_n;
+    auto ld = [](const uint64_t* a) { return *reinterpret_cast<const ulonglong2*>(a); };
+    auto st = [](uint64_t* a, ulonglong2 v) { *reinterpret_cast<ulonglong2*>(a) = v; };
+    if (OP == EL_ADD || OP == EL_SUB || OP == EL_MUL_PLAIN) {
+        const uint64_t* A = job.a[z] + p * job.a_poly + limb_off + w0;
+        const uint64_t* B = job.b[z] + (OP == EL_MUL_PLAIN ? 0 : p * job.b_poly) + limb_off + w0;
+        uint64_t* O = job.out[z] + p * job.out_poly + limb_off + w0;
+        ulonglong2 x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) { x[u] = ld(A + 512 * u); y[u] = ld(B + 512 * u); }
+        const bool fp = OP == EL_MUL_PLAIN && ((job.fp_mods >> i) & 1);
+        double2 qd = make_double2(0.0, 0.0);
+        if (fp) qd = job.modd[i];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            ulonglong2 r;
+            if (OP == EL_ADD) { r.x = add_mod(x[u].x, y[u].x, q); r.y = add_mod(x[u].y, y[u].y, q); }
+            else if (OP == EL_SUB) { r.x = sub_mod(x[u].x, y[u].x, q); r.y = sub_mod(x[u].y, y[u].y, q); }
+            else if (fp) {
+                r = make_ulonglong2(d_canon(mulred(u2d(x[u].x), u2d(y[u].x), qd.x, qd.y), qd.x, qd.y),
+                                    d_canon(mulred(u2d(x[u].y), u2d(y[u].y), qd.x, qd.y), qd.x, qd.y));
+            } else {
+                r = make_ulonglong2(mul_mod(x[u].x, y[u].x, md), mul_mod(x[u].y, y[u].y, md));
+            }
+            st(O + 512 * u, r);
+        }
+    } else {   // EL_TENSOR / EL_SQUARE_TENSOR
+        const uint64_t* A = job.a[z] + limb_off + w0;
+        const uint64_t* B = job.b[z] + limb_off + w0;
+        uint64_t* o = job.out[z] + limb_off + w0;
+        ulonglong2 a0[U], a1[U], b0[U], b1[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            a0[u] = ld(A + 512 * u);
+            a1[u] = ld(A + job.a_poly + 512 * u);
+            if (OP == EL_TENSOR) { b0[u] = ld(B + 512 * u); b1[u] = ld(B + job.b_poly + 512 * u); }
+            else { b0[u] = a0[u]; b1[u] = a1[u]; }
+        }
+        const bool fp = (job.fp_mods >> i) & 1;
+        double2 qd = make_double2(0.0, 0.0);
+        if (fp) qd = job.modd[i];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            ulonglong2 r0, r1, r2;
+            if (fp) {
+                const double q_ = qd.x, qi_ = qd.y;
+                const double x0 = u2d(a0[u].x), y0 = u2d(a0[u].y), x1 = u2d(a1[u].x), y1 = u2d(a1[u].y);
+                const double u0 = u2d(b0[u].x), v0 = u2d(b0[u].y), u1 = u2d(b1[u].x), v1 = u2d(b1[u].y);
+                r0 = make_ulonglong2(d_canon(mulred(x0, u0, q_, qi_), q_, qi_), d_canon(mulred(y0, v0, q_, qi_), q_, qi_));
+                r1 = make_ulonglong2(d_canon(__dadd_rn(mulred(x0, u1, q_, qi_), mulred(x1, u0, q_, qi_)), q_, qi_),
+                                     d_canon(__dadd_rn(mulred(y0, v1, q_, qi_), mulred(y1, v0, q_, qi_)), q_, qi_));
+                r2 = make_ulonglong2(d_canon(mulred(x1, u1, q_, qi_), q_, qi_), d_canon(mulred(y1, v1, q_, qi_), q_, qi_));
+            } else {
+                r0.x = mul_mod(a0[u].x, b0[u].x, md); r0.y = mul_mod(a0[u].y, b0[u].y, md);
+                U128 s{0, 0};
+                mac128(s, a0[u].x, b1[u].x); mac128(s, a1[u].x, b0[u].x);
+                r1.x = barrett128(s.lo, s.hi, md);
+                U128 t{0, 0};
+                mac128(t, a0[u].y, b1[u].y); mac128(t, a1[u].y, b0[u].y);
+                r1.y = barrett128(t.lo, t.hi, md);
+                r2.x = mul_mod(a1[u].x, b1[u].x, md); r2.y = mul_mod(a1[u].y, b1[u].y, md);
+            }
+            st(o + 512 * u, r0);
+            st(o + job.out_poly + 512 * u, r1);
+            st(o + 2 * job.out_poly + 512 * u, r2);
+        }
+    }
+}
+
 static int sm_count() {
     static int n = 0;
     if (!n) {
@@ -140,6 +222,15 @@ cudaError_t launch_elem(ElemOp op, const ElemJob& job, const Mod* mods, int nz, 
                                                                                                       : job.npolys;
     const long long n2 = 1ll << (job.log_n - 1);
     dim3 grid((unsigned)((n2 + 255) / 256), (unsigned)(np * job.nl), (unsigned)nz);
+    if (n2 % 512 == 0) {   // two pairs per thread for the HBM-bound binary ops
+        dim3 g2((unsigned)(n2 / 512), grid.y, grid.z);
+        switch (op) {
+#define C2(OPV) case OPV: k_elem2<OPV><<<g2, 256, 0, st>>>(job, mods); return cudaGetLastError();
+            C2(EL_ADD) C2(EL_SUB) C2(EL_MUL_PLAIN) C2(EL_TENSOR) C2(EL_SQUARE_TENSOR)
+#undef C2
+            default: break;
+        }
+    }
     switch (op) {
 #define C(OPV) case OPV: k_elem<OPV><<<grid, 256, 0, st>>>(job, mods); break;
         C(EL_ADD) C(EL_SUB) C(EL_NEG) C(EL_ADD_PLAIN) C(EL_SUB_PLAIN) C(EL_MUL_PLAIN) C(EL_ADD_SCALAR)
