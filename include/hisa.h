@@ -223,7 +223,9 @@ int hisa_mul_plain_accumulate(hisa_ctx* ctx, const hisa_ct* in, size_t C, const 
  * the mulScalar + add accumulation of Alg. 1 for OC outputs; all inputs one level,
  * one scale; no rescale (caller divScalars once per output).  Engine: the tcgen05 int8
  * tensor cores (byte-split modular GEMM, T <= 4096, N a multiple of 128) unless the environment
- * sets HISA_CONV_TC=0 (CUDA-core kernel); both give the same words.  Errors: HISA_E_PARAMS
+ * sets HISA_CONV_TC=0 (CUDA-core kernel); both give the same words.  HISA_CONV_TC_SMEM=<bytes>
+ * overrides the tensor-core kernel's shared-memory budget (inputs resident per pass; test knob,
+ * same words for any value >= 36864).  Errors: HISA_E_PARAMS
  * (non-finite or |W pt_scale| >= 2^62 weight, T or OC 0, T too large for the CUDA-core kernel),
  * HISA_E_LEVEL_MISMATCH / HISA_E_SCALE_MISMATCH / HISA_E_NOT_RELINEARIZED (inputs), HISA_E_OOM. */
 int hisa_conv_accumulate(hisa_ctx* ctx, const hisa_ct* in, size_t T, const double* W, size_t OC, double pt_scale,

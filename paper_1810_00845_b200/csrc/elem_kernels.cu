@@ -417,33 +417,59 @@ __global__ void __launch_bounds__(256) k_mulplain_acc_f64(const uint64_t* const*
                                                           const uint64_t* const* __restrict__ pt_ptrs,
                                                           uint64_t* const* __restrict__ out_ptrs, MpaJob job,
                                                           Tables tb) {
-    extern __shared__ uint64_t msm[];
-    const uint64_t** ins = reinterpret_cast<const uint64_t**>(msm);   // [C]
+    // every thread's 2 ciphertext word pairs and OT plaintext word pairs of input c + 1 are copied
+    // into its own slots of a double-buffered shared stage (cp.async, 16 B each) while input c is
+    // multiplied -- the direct-load form ran at 0.33 of HBM (profiles/r2_ncu_elem.txt: issue 14 %,
+    // 16 warps per SM at 128 registers, every iteration waiting on its own loads)
+    constexpr int W = 2 + OT;
+    extern __shared__ __align__(16) uint64_t msm[];
+    ulonglong2* stage = reinterpret_cast<ulonglong2*>(msm);                          // [2][W][256]
+    const uint64_t** ins = reinterpret_cast<const uint64_t**>(msm + 2 * W * 256 * 2);   // [C]
     const long long N = 1ll << job.log_n;
     const int limb = job.limb_map[blockIdx.y];
     const double2 qd = tb.modd[limb];
     const double q = qd.x, qinv = qd.y;
     const long long loff = (long long)limb * N;
-    const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + threadIdx.x);
-    for (int c = threadIdx.x; c < job.C; c += blockDim.x) ins[c] = in_ptrs[c] + loff;
+    const int tid = threadIdx.x;
+    const long long x = 2ll * (blockIdx.x * (long long)blockDim.x + tid);
+    for (int c = tid; c < job.C; c += blockDim.x) ins[c] = in_ptrs[c] + loff;
     __syncthreads();
     if (x >= N) return;
     const long long pstride = (long long)job.l1 * N;
+    auto cp16 = [](const void* dst, const void* src) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src) : "memory");
+    };
     for (int j0 = 0; j0 < job.J; j0 += OT) {
+        auto issue = [&](int c, int buf) {
+            ulonglong2* st = stage + buf * W * 256 + tid;
+            cp16(st, ins[c] + x);
+            cp16(st + 256, ins[c] + pstride + x);
+#pragma unroll
+            for (int k = 0; k < OT; k++)
+                if (j0 + k < job.J) cp16(st + (2 + k) * 256, pt_ptrs[(long long)(j0 + k) * job.C + c] + loff + x);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        };
         double acc[OT][2][2];
 #pragma unroll
         for (int k = 0; k < OT; k++)
 #pragma unroll
             for (int p = 0; p < 2; p++) { acc[k][p][0] = 0.0; acc[k][p][1] = 0.0; }
+        issue(0, 0);
         for (int c = 0; c < job.C; c++) {
-            const ulonglong2 a0 = __ldg(reinterpret_cast<const ulonglong2*>(ins[c] + x));
-            const ulonglong2 a1 = __ldg(reinterpret_cast<const ulonglong2*>(ins[c] + pstride + x));
+            if (c + 1 < job.C) {
+                issue(c + 1, (c + 1) & 1);
+                asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+            }
+            const ulonglong2* st = stage + (c & 1) * W * 256 + tid;
+            const ulonglong2 a0 = st[0], a1 = st[256];
             const double a00 = u2d(a0.x), a01 = u2d(a0.y), a10 = u2d(a1.x), a11 = u2d(a1.y);
 #pragma unroll
             for (int k = 0; k < OT; k++) {
                 if (j0 + k >= job.J) break;
-                const ulonglong2 pv =
-                    __ldcs(reinterpret_cast<const ulonglong2*>(pt_ptrs[(long long)(j0 + k) * job.C + c] + loff + x));
+                const ulonglong2 pv = st[(2 + k) * 256];
                 const double p0 = u2d(pv.x), p1 = u2d(pv.y);
                 acc[k][0][0] = __dadd_rn(acc[k][0][0], mulred(a00, p0, q, qinv));
                 acc[k][0][1] = __dadd_rn(acc[k][0][1], mulred(a01, p1, q, qinv));
@@ -488,9 +514,9 @@ cudaError_t launch_mulplain_acc(const uint64_t* const* in_ptrs, const uint64_t* 
     }
     if (nf) {
         dim3 grid((unsigned)((N / 2 + 255) / 256), nf, 1);
-        if (smem > 48 * 1024)
-            cudaFuncSetAttribute(k_mulplain_acc_f64<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_mulplain_acc_f64<8><<<grid, 256, smem, st>>>(in_ptrs, pt_ptrs, out_ptrs, jf, tb);
+        const size_t smem_f = smem + (size_t)2 * (2 + 8) * 256 * 16;   // + the cp.async stage
+        cudaFuncSetAttribute(k_mulplain_acc_f64<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f);
+        k_mulplain_acc_f64<8><<<grid, 256, smem_f, st>>>(in_ptrs, pt_ptrs, out_ptrs, jf, tb);
     }
     return cudaGetLastError();
 }
