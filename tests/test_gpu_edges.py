@@ -237,3 +237,26 @@ def test_truncated_rotation_keys():
     g.keygen([7], False, 1)                                     # lower request keeps level 3
     assert g.key_export(7, 4 * 2 * 5 * N).size == 4 * 2 * 5 * N
     g.close()
+
+
+def test_conv_tc_squeezenet_shape_sampled():
+    """K8 at the shape the bench's config-5 leg spends its conv time in (N = 2^16, a 60-bit q_0 +
+    15 x 40-bit limbs, T = 144 inputs = 16 channels x 9 taps, OC = 64: one super-chunk of five
+    K-chunks per CTA, two CTAs per SM, four output tiles) -- three sampled output channels against
+    the oracle's mulScalar + add chain, all words."""
+    qb = [60] + [40] * 15
+    g = H.Context(16, qb, 60, seed=6, arena_bytes=24 << 30)
+    o = Oracle(16, qb, 60, seed=6)
+    T, OC = 144, 64
+    lvl = len(qb) - 1
+    hs = [g.ct_random(t, lvl) for t in range(T)]
+    W = np.random.default_rng(12).normal(0, 0.05, (OC, T))
+    outs = g.conv_accumulate(hs, W.ravel())
+    cts = [o.bench_ct(t, lvl) for t in range(T)]
+    for oc in (0, 37, 63):
+        acc = None
+        for t in range(T):
+            term = o.mul_scalar(cts[t], float(W[oc, t]))
+            acc = term if acc is None else o.add(acc, term)
+        assert (g.ct_export(outs[oc]) == acc.data).all(), oc
+    g.close()
