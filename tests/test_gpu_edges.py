@@ -260,3 +260,25 @@ def test_conv_tc_squeezenet_shape_sampled():
             acc = term if acc is None else o.add(acc, term)
         assert (g.ct_export(outs[oc]) == acc.data).all(), oc
     g.close()
+
+
+def test_conv_tc_all_plane_counts():
+    """Every byte-plane specialisation of the tensor-core K8: 45-bit (P = 6), 30-bit (P = 4) and
+    24 / 22-bit limbs (P = 3, run as 4 with a zero plane) beside the 60 / 50 / 40-bit ones of the
+    other conv tests (P = 8 / 7 / 5); ragged chunk and output tile, negative weights."""
+    qb = [45, 30, 24, 22]
+    g = H.Context(12, qb, 60, seed=8, arena_bytes=2 << 30)
+    o = Oracle(12, qb, 60, seed=8)
+    T, OC = 40, 5
+    lvl = len(qb) - 1
+    hs = [g.ct_random(t, lvl) for t in range(T)]
+    W = np.random.default_rng(13).normal(0, 0.4, (OC, T))
+    outs = g.conv_accumulate(hs, W.ravel(), 2.0 ** 20)
+    cts = [o.bench_ct(t, lvl) for t in range(T)]
+    for oc in range(OC):
+        acc = None
+        for t in range(T):
+            term = o.mul_scalar(cts[t], float(W[oc, t]), 2.0 ** 20)
+            acc = term if acc is None else o.add(acc, term)
+        assert (g.ct_export(outs[oc]) == acc.data).all(), oc
+    g.close()
