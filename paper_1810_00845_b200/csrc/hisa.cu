@@ -1368,7 +1368,23 @@ static int ks_chunk(const hisa_ctx* c, int level) {
     size_t n = budget / per;
     if (n < 1) n = 1;
     if (n > (size_t)MAXB) n = MAXB;
+    // K4 shares every staged key row among 8 / 4 / 2 ciphertexts of a batch by the largest of those
+    // dividing it: a chunk of 10 (what 4 GiB gives at N = 2^16, L = 24) would run the 2-ciphertext
+    // form -- 3.0k instead of 3.2k rotations/s in the config-2 sweep at B >= 16
+    if (n >= 8) n -= n % 8;
+    else if (n >= 4) n = 4;
+    else if (n >= 2) n = 2;
     return (int)n;
+}
+// n items in chunks of at most `maxc`: as many chunks as that needs, of equal size rounded up to
+// the sharing quantum q (8 ciphertexts per staged key row in K4, 4 in K7) -- 16 items under a cap of
+// 12 run as 8 + 8, not 12 + 4
+static int balanced_chunk(size_t n, size_t maxc, size_t q) {
+    if (n <= maxc || maxc < q) return (int)std::min(n, maxc);
+    const size_t nch = (n + maxc - 1) / maxc;
+    size_t per = (n + nch - 1) / nch;
+    per = (per + q - 1) / q * q;
+    return (int)std::min(per, maxc);
 }
 
 static int ensure_side(hisa_ctx* c) {
@@ -1477,7 +1493,7 @@ extern "C" int hisa_mul_batch(hisa_ctx* c, const hisa_ct* a, const hisa_ct* b, s
     if (n == 0) return HISA_OK;
     const int level = oa[0]->level, l1 = level + 1;
     const long long N = (long long)c->N;
-    const size_t chunk = (size_t)ks_chunk(c, level);
+    const size_t chunk = (size_t)balanced_chunk(n, (size_t)ks_chunk(c, level), 8);
     for (size_t i0 = 0; i0 < n; i0 += chunk) {
         const int nz = (int)std::min(chunk, n - i0);
         uint64_t* t3 = dalloc_t<uint64_t>(c, (size_t)3 * l1 * N * nz);
@@ -1585,15 +1601,24 @@ static int rotate_hoisted_multi(hisa_ctx* c, Obj* const* os, int nct, const uint
     const size_t per_ct = (size_t)N * ((size_t)l1 + (size_t)l1 * l2);           // dtil, D
     const size_t per_out = (size_t)N * (2 * l2 + 2 + 2 * l1 + 2 * l1);           // acc, ptmp, md, pre
     constexpr int RK = 4;                                                         // keys per K7 launch
-    const size_t budget = (size_t)6 << 30;
+    // 8 GiB of scratch: 8 ciphertexts per chunk at N = 2^16, L = 24 (ModUp batched over 8, K7 in two
+    // groups of 4); a smaller arena falls back to smaller chunks below
+    const size_t budget = (size_t)8 << 30;
     int ct_chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)MAXB, budget / ((per_ct + 2 * RK * per_out) * 8)));
-    ct_chunk = std::min(ct_chunk, nct);
+    if (ct_chunk >= 4) ct_chunk -= ct_chunk % 4;   // K7 streams each key once per group of 4 ciphertexts
+    ct_chunk = balanced_chunk((size_t)nct, (size_t)ct_chunk, 4);
     DGuard outputs(c), sguard(c);
     for (int i = 0; i < nct * n; i++) {
         outs[i] = outputs.add(dalloc_t<uint64_t>(c, (size_t)2 * l1 * N));
         if (!outs[i]) return fail(HISA_E_OOM, "rotation output");
     }
-    uint64_t* scratch = sguard.add(dalloc_t<uint64_t>(c, per_ct * ct_chunk + 2 * per_out * (size_t)ct_chunk * RK));
+    uint64_t* scratch = nullptr;
+    for (;;) {
+        scratch = dalloc_t<uint64_t>(c, per_ct * ct_chunk + 2 * per_out * (size_t)ct_chunk * RK);
+        if (scratch || ct_chunk == 1) break;
+        ct_chunk = std::max(1, ct_chunk / 2);
+    }
+    sguard.add(scratch);
     if (!scratch) return fail(HISA_E_OOM, "hoisted rotation scratch");
     RET(ensure_side(c));
 #ifndef HOIST_PIPE
@@ -1767,7 +1792,7 @@ extern "C" int hisa_rot_left_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int
         return HISA_OK;
     }
     RET(rot_key_check(c, kk, objs[0]->level));
-    const size_t chunk = (size_t)ks_chunk(c, objs[0]->level);
+    const size_t chunk = (size_t)balanced_chunk(n, (size_t)ks_chunk(c, objs[0]->level), 8);
     for (size_t i0 = 0; i0 < n; i0 += chunk) {
         const int nz = (int)std::min(chunk, n - i0);
         uint64_t* res[MAXB];
@@ -1796,7 +1821,7 @@ extern "C" int hisa_rot_add_batch(hisa_ctx* c, const hisa_ct* in, size_t n, int6
         return HISA_OK;
     }
     RET(rot_key_check(c, kk, objs[0]->level));
-    const size_t chunk = (size_t)ks_chunk(c, objs[0]->level);
+    const size_t chunk = (size_t)balanced_chunk(n, (size_t)ks_chunk(c, objs[0]->level), 8);
     for (size_t i0 = 0; i0 < n; i0 += chunk) {
         const int nz = (int)std::min(chunk, n - i0);
         uint64_t* res[MAXB];

@@ -506,11 +506,21 @@ static cudaError_t ks_ip_256(KsJob job, const Tables& tb, int nz, cudaStream_t s
     }
     if (nfp) {
         memcpy(job.ri_list, fp, nfp);
-        if (nz % 8 == 0) e = ks_ip6_t<8, 1, K6_MINB>(job, tb, nfp, st);
-        else if (nz % 4 == 0) e = ks_ip6_t<4, 1, K6_MINB>(job, tb, nfp, st);
-        else if (nz % 2 == 0) e = ks_ip6_t<2, 2, K6_MINB>(job, tb, nfp, st);
-        else e = ks_ip6_t<1, 4, K6_MINB>(job, tb, nfp, st);
-        if (e != cudaSuccess) return e;
+        // the batch in groups of 8 k / 4 / 2 / 1 ciphertexts, each group in the form that shares a
+        // staged key row among all its ciphertexts (10 = 8 + 2, 5 = 4 + 1, 100 = 96 + 4)
+        for (int z0 = 0; z0 < nz;) {
+            const int rem = nz - z0;
+            const int m = rem >= 8 ? rem - rem % 8 : rem >= 4 ? 4 : rem >= 2 ? 2 : 1;
+            KsJob sub = job;
+            for (int z = 0; z < m; z++) { sub.t1[z] = job.t1[z0 + z]; sub.d[z] = job.d[z0 + z]; sub.acc[z] = job.acc[z0 + z]; }
+            sub.nz = m;
+            if (m % 8 == 0) e = ks_ip6_t<8, 1, K6_MINB>(sub, tb, nfp, st);
+            else if (m == 4) e = ks_ip6_t<4, 1, K6_MINB>(sub, tb, nfp, st);
+            else if (m == 2) e = ks_ip6_t<2, 2, K6_MINB>(sub, tb, nfp, st);
+            else e = ks_ip6_t<1, 4, K6_MINB>(sub, tb, nfp, st);
+            if (e != cudaSuccess) return e;
+            z0 += m;
+        }
     }
     if (fork) return cudaStreamWaitEvent(st, side->join, 0);
     return cudaSuccess;

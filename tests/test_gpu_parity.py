@@ -425,10 +425,11 @@ def test_encode_batch_bit_exact(pair):
         assert (g.pt_export(h) == o.encode(v, float(o.q[lv]), lv).data).all()
 
 
-@pytest.mark.parametrize("nz", [1, 2, 4, 5, 6, 8])
+@pytest.mark.parametrize("nz", [1, 2, 4, 5, 7, 8, 11])
 def test_k4_batch_shapes_and_long_digit_chains(nz):
     """K4 at M = 256 (N = 2^15) in every CTA shape (ciphertexts x rows per CTA: 8x1, 4x1, 2x2,
-    1x4, picked by the batch size) with 13 digits (the FP64 accumulators are re-centred every 6
+    1x4; a batch is split into groups of 8k / 4 / 2 / 1: 5 = 4 + 1, 7 = 4 + 2 + 1, 11 = 8 + 2 + 1)
+    with 13 digits (the FP64 accumulators are re-centred every 6
     products): a batched rotation of nz ciphertexts, one of them all (q - 1) residues (the
     largest lifted digits and MAC operands), equal to the oracle word for word."""
     log_n, qb = 15, [60] + [50] * 12
